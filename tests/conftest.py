@@ -1,0 +1,19 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA B200 (runs via gpurun / round-end GPU tier)")
+    config.addinivalue_line("markers", "slow: long-running (large configs)")
+
+
+@pytest.fixture(scope="session")
+def c1_inputs():
+    from synth import make_inputs
+    return make_inputs("c1")
