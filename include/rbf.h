@@ -1,0 +1,247 @@
+/*
+ * rbf.h -- C-ABI of the B200-native Gaussian-RBF implicit-surface hot path.
+ *
+ * Method: Cuomo, Galletti, Giunta, Starace, "Surface reconstruction from
+ * scattered point via RBF interpolation on GPU" (arXiv 1305.5179).
+ * Citations "P:<lines>" are lines of that paper's text with the
+ * section / equation / algorithm they fall in.
+ *
+ * What the library computes (all on the GPU; there is no CPU fallback):
+ *
+ *   centres   x_1..x_n in R^3 (fp32; for the paper's problem n = 3N: the
+ *             surface points X and their +/-delta normal offsets
+ *             §2.1.1; building that set is the caller's job)
+ *   operator  A_ij = a * exp(-||x_i - x_j||^2 / (2 sigma^2))   if ||x_i-x_j|| <= c
+ *             A_ij = 0                                          otherwise
+ *             a = 1/(sqrt(2 pi) sigma) by default (Eq.6; Table I
+ *             P:299); c = cutoff_sigmas * sigma (the "finite bandwidth" of
+ *             P:361-369; reading R5: inclusive, c = 6 sigma)
+ *   matvec    f = A w                                   (Eq.4)
+ *   solve     A w = b by restarted right-preconditioned GMRES with a
+ *             restricted additive Schwarz (RAS) preconditioner
+ *                                                       (§3.1)
+ *   evaluate  F(xi_k) = sum_j A(xi_k, x_j) w_j on a regular grid
+ *                                                       (Eq.5, P:264-271;
+ *                                                        §2.1.3)
+ *
+ * Conventions (apply to every entry point):
+ *  - Device pointers are caller-owned device memory (cudaMalloc / torch),
+ *    host pointers are plain host memory; each argument says which.
+ *  - Every call is stream-ordered on the context's stream; calls only
+ *    synchronise where they must return host values (documented per call).
+ *  - Vectors are indexed in the CALLER's order of the centres passed to
+ *    rbf_build_cells (internal cell order is hidden) unless stated otherwise.
+ *  - Errors: functions return rbf_status; on error nothing is written to the
+ *    output buffers' contents that the caller may rely on, and
+ *    rbf_last_error() returns a human-readable message (thread-local).
+ *    Non-convergence of GMRES is NOT an error (see rbf_solve_report).
+ *  - Handles (rbf_ctx, rbf_cells, rbf_precond) are library-owned and freed by
+ *    their *_free / rbf_destroy call.  One rbf_ctx per host thread.
+ */
+#ifndef RBF_B200_H
+#define RBF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RBF_ABI_VERSION 1
+
+typedef enum {
+  RBF_OK = 0,
+  RBF_EINVAL = 1,   /* invalid argument (sizes, sigma <= 0, non-finite input, ...) */
+  RBF_ENOMEM = 2,   /* device allocation failed */
+  RBF_ECUDA = 3,    /* CUDA runtime error (message in rbf_last_error) */
+  RBF_ENCCL = 4,    /* reserved for the multi-GPU layer */
+  RBF_EUNSUPPORTED = 5
+} rbf_status;
+
+typedef enum { RBF_F32 = 0, RBF_F64 = 1 } rbf_precision;
+
+/* Gaussian kernel of Eq.6 with truncation radius
+ * cutoff_sigmas*sigma.  amplitude <= 0 selects Eq.6's
+ * a = 1/(sqrt(2 pi) sigma). */
+typedef struct {
+  double sigma;          /* > 0 */
+  double cutoff_sigmas;  /* > 0; the configs use 6 */
+  double amplitude;      /* <= 0 => 1/(sqrt(2 pi) sigma) */
+} rbf_kernel;
+
+/* Cell binning of the centres ("truncation area", Alg.2).
+ * Cell edge h; frame lo (fp32) and inv_h = float32(1/h):
+ *   lo_a  = float32(double(min_a x) - h/2),  dim_a = floor(f32(f32(max_a x - lo_a) * inv_h)) + 1
+ *   cell_a(x) = clamp(floor(f32(f32(x_a - lo_a) * inv_h)), 0, dim_a - 1)
+ *   key = cx + dimx*(cy + dimy*cz);   cells sorted stably by key.
+ * (bit-exact with oracle/cells.py.) */
+typedef struct {
+  double cell_edge;      /* <= 0 => cutoff / 3.999 (4 cells
+                            per cutoff with a rounding margin) */
+  int tile_cap;          /* targets per warp tile, 32 or 64; <= 0 => 64 */
+  int tile_span;         /* max cells a tile spans along x; <= 0 => 2 */
+} rbf_cell_cfg;
+
+/* RAS preconditioner (§3.1; reading R8). */
+typedef struct {
+  int kind;              /* 0 none, 1 block-Jacobi (overlap 0), 2 RAS */
+  int core_target;       /* centres per core (whole cells); <= 0 => 512 */
+  double overlap_sigmas; /* extended set = centres within overlap*sigma of the core */
+  int max_ext;           /* reject blocks larger than this; <= 0 => 4096 */
+} rbf_precond_cfg;
+
+/* Restarted right-preconditioned FGMRES(m).
+ * Phase 1 iterates with the fp32 operator tier down to phase1_rtol of the
+ * TRUE relative residual; phase 2 continues with the fp64 operator tier and
+ * fp64 vectors until ||b - A w||_2 / ||b||_2 <= rtol (fp64 operator). */
+typedef struct {
+  int restart;           /* m; <= 0 => 30 */
+  double rtol;           /* final true relative residual; <= 0 => 1e-6 */
+  double phase1_rtol;    /* <= 0 => 1e-4 */
+  int max_iters;         /* total inner iterations; <= 0 => 500 */
+  int polish_fp64;       /* 1 => phase 2 in fp64 (needed for rtol < ~1e-5) */
+} rbf_gmres_cfg;
+
+typedef struct {
+  int iters_phase1, iters_phase2, restarts, converged, breakdown;
+  double rel_residual_true;   /* ||b - A w|| / ||b|| with the fp64 operator */
+  double rel_residual_est;    /* GMRES (Arnoldi) estimate at exit */
+  double t_setup, t_phase1, t_phase2;  /* seconds (host clock around device work) */
+  int64_t nblocks;            /* RAS blocks */
+  int64_t precond_bytes;      /* device bytes held by the preconditioner */
+  int64_t matvecs_f32, matvecs_f64;
+} rbf_solve_report;
+
+/* Regular evaluation grid: n[a] >= 2 inclusive nodes per axis from lo[a] to
+ * hi[a]; node (i,j,k) = lo + (i,j,k)*(hi-lo)/(n-1) (computed in fp64 then
+ * rounded to fp32); flat index i + n0*(j + n1*k) (x fastest). */
+typedef struct {
+  double lo[3], hi[3];
+  int n[3];
+} rbf_grid;
+
+typedef struct rbf_ctx rbf_ctx;
+typedef struct rbf_cells rbf_cells;
+typedef struct rbf_precond rbf_precond;
+
+/* Description of a built cell list (host struct, filled by rbf_cells_info). */
+typedef struct {
+  int64_t n;             /* centres */
+  int dim[3];
+  float lo[3];
+  float inv_h;
+  double cell_edge;
+  int reach;             /* stencil reach in cells (>= ceil(cutoff/h)) */
+  int64_t ncell;         /* dim0*dim1*dim2 */
+  int64_t ntiles;        /* matvec target tiles */
+  int64_t nonempty_cells;
+} rbf_cells_desc;
+
+/* ---- context ------------------------------------------------------------ */
+
+/* Create a context on CUDA device `device` that issues all work on
+ * `cuda_stream` (a cudaStream_t; NULL = the legacy default stream).
+ * nccl_unique_id must be NULL and world 1 in this ABI version (multi-GPU
+ * runs shard independent problems per rank).
+ * Errors: RBF_EINVAL (bad device / world != 1), RBF_ECUDA. */
+rbf_status rbf_create(rbf_ctx** ctx, int device, void* cuda_stream,
+                      const void* nccl_unique_id, int rank, int world);
+void rbf_destroy(rbf_ctx* ctx);
+const char* rbf_status_str(rbf_status s);
+const char* rbf_last_error(void);
+int rbf_abi_version(void);
+
+/* ---- a0: extended interpolation set (§2.1.1-2.1.2) ------------
+ * x, nrm: DEVICE fp64, N x 3 (surface points and unit normals).
+ * centres: DEVICE fp32, 3N x 3 = [x; x + delta n; x - delta n], each sum formed
+ * in fp64 (one multiply, one add) and rounded once to fp32.
+ * b: DEVICE fp32, 3N = [0 x N; +label x N; -label x N] (P:186-193 uses
+ * label 1; the benchmark configs use label = delta, reading R2).
+ * b may be NULL.  Errors: RBF_EINVAL for N < 1 or NULL x/nrm/centres. */
+rbf_status rbf_extend_points(rbf_ctx* ctx, const double* x, const double* nrm, int64_t N,
+                             double delta, double label, float* centres, float* b);
+
+/* ---- a1/a2: cell build + tile plan (Alg.2 "truncation area") -------------
+ * xyz: DEVICE, n x 3 fp32 row-major (x0,y0,z0,x1,...), caller-owned, read only
+ * during the call.  n >= 1.  Non-finite coordinates => RBF_EINVAL.
+ * Synchronises once (reads back the bounding box to size the grid of cells).
+ * *out receives a library-owned handle (free with rbf_cells_free). */
+rbf_status rbf_build_cells(rbf_ctx* ctx, const float* xyz, int64_t n,
+                           const rbf_kernel* kern, const rbf_cell_cfg* cfg,
+                           rbf_cells** out);
+void rbf_cells_free(rbf_cells* cells);
+rbf_status rbf_cells_info(const rbf_cells* cells, rbf_cells_desc* out /* host */);
+/* Library-owned DEVICE arrays, valid until rbf_cells_free:
+ *   perm[n]           sorted position -> caller index (stable by key)
+ *   sorted[4n]        float4 records (x, y, z, 0) in sorted order
+ *   keys[n]           uint32 cell key per sorted position
+ *   cell_start[ncell+1]  cell k holds sorted positions [cell_start[k], cell_start[k+1])
+ *                        (= searchsorted left of k; cell_end = cell_start + 1) */
+rbf_status rbf_cells_view(const rbf_cells* cells, const int32_t** perm,
+                          const float** sorted, const uint32_t** keys,
+                          const int32_t** cell_start);
+
+/* ---- a3: matrix-free matvec f = A w (Eq.4/Eq.6) ---------------------------
+ * w, f: DEVICE, n entries, caller order; fp32 (RBF_F32) or fp64 (RBF_F64).
+ * RBF_F32: fp32 coordinates differences in tile-local scaled frame,
+ * ex2.approx, fp32 accumulation.
+ * RBF_F64: fp64 distances (same rounding order as the oracle), fp64 exp,
+ * fp64 weights and accumulation.  w and f must not alias. */
+rbf_status rbf_matvec(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern,
+                      rbf_precision prec, const void* w, void* f);
+
+/* Pair accounting of the fp32 matvec traversal (host outputs; synchronises):
+ * useful = ordered (target, source) pairs with r^2 <= c^2 (self included),
+ * visited = pairs the kernel evaluated (after culling). */
+rbf_status rbf_matvec_pairs(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern,
+                            int64_t* useful, int64_t* visited);
+
+/* ---- a4/a5: RAS preconditioner (§3.1) -------------------------------------
+ * Builds blocks (cores = runs of whole non-empty cells in Morton order of
+ * ~core_target centres; extended set = centres within overlap of a core
+ * centre), assembles each A_ext in fp32, factors it by LU with partial
+ * pivoting (the truncated block may be indefinite) and keeps the restricted
+ * inverse W_i = (A_ext^-1)[core, :] (fp32).  Synchronises. */
+rbf_status rbf_precond_create(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern,
+                              const rbf_precond_cfg* cfg, rbf_precond** out);
+void rbf_precond_free(rbf_precond* p);
+/* z = M r, M = sum_i R~_i^T A_i^-1 R_i (restricted: only core rows written).
+ * r, z: DEVICE fp32, n entries, caller order. */
+rbf_status rbf_precond_apply(rbf_ctx* ctx, const rbf_precond* p, const float* r, float* z);
+/* Block structure (host outputs, synchronises): nblocks, and if the arrays are
+ * non-NULL: core_ptr[nblocks+1], ext_ptr[nblocks+1] (host, caller-allocated)
+ * and core_idx[core_ptr[nb]], ext_idx[ext_ptr[nb]] (host) holding SORTED
+ * positions; each block's ext list is [non-core members ascending] + [core]. */
+rbf_status rbf_precond_blocks(const rbf_precond* p, int64_t* nblocks, int64_t* bytes,
+                              int64_t* core_ptr, int64_t* ext_ptr,
+                              int32_t* core_idx, int32_t* ext_idx);
+
+/* ---- a6/a7: GMRES solve A w = b ------------------------------------------
+ * b: DEVICE fp32 (n), w: DEVICE fp64 (n) output, both caller order; rep: HOST.
+ * precond may be NULL (then pcfg builds one internally, freed on return).
+ * Synchronises (returns the report).  Non-convergence: RBF_OK, converged=0. */
+rbf_status rbf_gmres_solve(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern,
+                           const rbf_precond* precond, const rbf_precond_cfg* pcfg,
+                           const rbf_gmres_cfg* gcfg, const float* b, double* w,
+                           rbf_solve_report* rep);
+
+/* ---- a8: grid evaluation F(xi) = sum_j A(xi, x_j) w_j (Eq.5) --------------
+ * w: DEVICE fp64 (n, caller order); field: DEVICE fp32, n0*n1*n2, x fastest.
+ * Nodes with no centre within the cutoff get exactly 0.0f. */
+rbf_status rbf_eval_grid(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern,
+                         const double* w, const rbf_grid* grid, float* field);
+
+/* ---- Alg.1 steps 2-3 end to end from HOST buffers -------------------------
+ * xyz (n x 3 fp32), b (n fp32), w_out (n fp64), field_out (grid nodes fp32),
+ * rep: all HOST.  Copies in, builds cells, preconditioner, solves, evaluates
+ * the grid, copies out.  Synchronises. */
+rbf_status rbf_reconstruct_host(rbf_ctx* ctx, const float* xyz, const float* b, int64_t n,
+                                const rbf_kernel* kern, const rbf_cell_cfg* ccfg,
+                                const rbf_precond_cfg* pcfg, const rbf_gmres_cfg* gcfg,
+                                const rbf_grid* grid, double* w_out, float* field_out,
+                                rbf_solve_report* rep);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RBF_B200_H */

@@ -1,0 +1,11 @@
+"""B200-native Gaussian-RBF implicit-surface hot path (arXiv 1305.5179).
+
+The product path is librbf.so (C-ABI, include/rbf.h: hand-written sm_100a
+CUDA) and the thin ctypes binding in `rbf`.  This package never imports the
+CPU oracle (oracle/, test infrastructure only) and has no CPU fallback.
+"""
+from .rbf import (Context, Cells, Kernel, Precond, RbfError, SolveReport, eval_grid, extend_points,
+                  gmres_solve, load_library, matvec, matvec_pairs, reconstruct_host)
+
+__all__ = ["Context", "Cells", "Kernel", "Precond", "RbfError", "SolveReport", "eval_grid",
+           "extend_points", "gmres_solve", "load_library", "matvec", "matvec_pairs", "reconstruct_host"]

@@ -1,0 +1,208 @@
+// C-ABI entry points (include/rbf.h): validation, handle management and
+// dispatch to the device code.  Every step of the path runs in this
+// library's kernels; there is no host compute fallback.
+#include <cmath>
+#include <cstring>
+#include <new>
+
+#include "internal.h"
+
+namespace rbf {
+namespace {
+thread_local std::string g_last_error;
+}
+void set_error(const std::string& msg) { g_last_error = msg; }
+const char* last_error_cstr() { return g_last_error.c_str(); }
+}  // namespace rbf
+
+using namespace rbf;
+
+namespace {
+
+rbf_status check_kernel(const rbf_kernel* k) {
+  if (!k) { set_error("kernel is NULL"); return RBF_EINVAL; }
+  if (!(k->sigma > 0) || !std::isfinite(k->sigma)) { set_error("sigma must be > 0"); return RBF_EINVAL; }
+  if (!(k->cutoff_sigmas > 0) || !std::isfinite(k->cutoff_sigmas)) {
+    set_error("cutoff_sigmas must be > 0");
+    return RBF_EINVAL;
+  }
+  if (!std::isfinite(k->amplitude)) { set_error("amplitude must be finite"); return RBF_EINVAL; }
+  return RBF_OK;
+}
+
+rbf_status check_cells(const rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* k) {
+  if (!ctx) { set_error("ctx is NULL"); return RBF_EINVAL; }
+  if (!c) { set_error("cells is NULL"); return RBF_EINVAL; }
+  RBF_TRY(check_kernel(k));
+  // the stencil was sized for the cutoff given at build time
+  double cut = k->cutoff_sigmas * k->sigma;
+  if (cut > c->cutoff * (1 + 1e-12)) {
+    set_error("kernel cutoff exceeds the cutoff the cells were built for");
+    return RBF_EINVAL;
+  }
+  return RBF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rbf_status_str(rbf_status s) {
+  switch (s) {
+    case RBF_OK: return "RBF_OK";
+    case RBF_EINVAL: return "RBF_EINVAL";
+    case RBF_ENOMEM: return "RBF_ENOMEM";
+    case RBF_ECUDA: return "RBF_ECUDA";
+    case RBF_ENCCL: return "RBF_ENCCL";
+    case RBF_EUNSUPPORTED: return "RBF_EUNSUPPORTED";
+  }
+  return "RBF_UNKNOWN";
+}
+
+const char* rbf_last_error(void) { return last_error_cstr(); }
+
+int rbf_abi_version(void) { return RBF_ABI_VERSION; }
+
+rbf_status rbf_create(rbf_ctx** out, int device, void* cuda_stream, const void* nccl_unique_id, int rank,
+                      int world) {
+  if (!out) { set_error("out is NULL"); return RBF_EINVAL; }
+  *out = nullptr;
+  if (nccl_unique_id != nullptr || world != 1 || rank != 0) {
+    set_error("this ABI version runs one problem per GPU: nccl_unique_id must be NULL, world 1, rank 0");
+    return RBF_EINVAL;
+  }
+  int ndev = 0;
+  RBF_CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) { set_error("bad device ordinal"); return RBF_EINVAL; }
+  RBF_CUDA_TRY(cudaSetDevice(device));
+  rbf_ctx* c = new (std::nothrow) rbf_ctx();
+  if (!c) { set_error("host allocation failed"); return RBF_ENOMEM; }
+  c->device = device;
+  c->stream = static_cast<cudaStream_t>(cuda_stream);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) c->sm_count = prop.multiProcessorCount;
+  if (prop.major != 10) {
+    delete c;
+    set_error("librbf is built for sm_100a (B200); device has compute capability " +
+              std::to_string(prop.major) + "." + std::to_string(prop.minor));
+    return RBF_EUNSUPPORTED;
+  }
+  *out = c;
+  return RBF_OK;
+}
+
+void rbf_destroy(rbf_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = ctx->stream;
+  delete ctx;  // DevBufs free stream-ordered
+  cudaStreamSynchronize(s);
+}
+
+rbf_status rbf_build_cells(rbf_ctx* ctx, const float* xyz, int64_t n, const rbf_kernel* kern,
+                           const rbf_cell_cfg* cfg, rbf_cells** out) {
+  if (!ctx || !out) { set_error("ctx/out is NULL"); return RBF_EINVAL; }
+  *out = nullptr;
+  RBF_TRY(check_kernel(kern));
+  if (n < 1 || n > (int64_t)INT32_MAX / 2) { set_error("n out of range"); return RBF_EINVAL; }
+  if (!xyz) { set_error("xyz is NULL"); return RBF_EINVAL; }
+  if (cfg && cfg->cell_edge < 0) { set_error("cell_edge must be >= 0"); return RBF_EINVAL; }
+  RBF_CUDA_TRY(cudaSetDevice(ctx->device));
+  rbf_cells* c = new (std::nothrow) rbf_cells();
+  if (!c) { set_error("host allocation failed"); return RBF_ENOMEM; }
+  rbf_status st = build_cells(ctx, xyz, n, kern, cfg, c);
+  if (st != RBF_OK) { delete c; return st; }
+  *out = c;
+  return RBF_OK;
+}
+
+void rbf_cells_free(rbf_cells* c) { delete c; }
+
+rbf_status rbf_cells_info(const rbf_cells* c, rbf_cells_desc* d) {
+  if (!c || !d) { set_error("NULL argument"); return RBF_EINVAL; }
+  d->n = c->n;
+  for (int a = 0; a < 3; ++a) { d->dim[a] = c->dim[a]; d->lo[a] = c->lo[a]; }
+  d->inv_h = c->inv_h;
+  d->cell_edge = c->h;
+  d->reach = c->reach;
+  d->ncell = c->ncell;
+  d->ntiles = c->ntiles;
+  d->nonempty_cells = c->nonempty;
+  return RBF_OK;
+}
+
+rbf_status rbf_cells_view(const rbf_cells* c, const int32_t** perm, const float** sorted, const uint32_t** keys,
+                          const int32_t** cell_start) {
+  if (!c) { set_error("cells is NULL"); return RBF_EINVAL; }
+  if (perm) *perm = c->perm.as<int32_t>();
+  if (sorted) *sorted = c->sorted.as<float>();
+  if (keys) *keys = c->keys.as<uint32_t>();
+  if (cell_start) *cell_start = c->cell_start.as<int32_t>();
+  return RBF_OK;
+}
+
+rbf_status rbf_matvec(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, rbf_precision prec, const void* w,
+                      void* f) {
+  RBF_TRY(check_cells(ctx, c, kern));
+  if (!w || !f) { set_error("w/f is NULL"); return RBF_EINVAL; }
+  if (w == f) { set_error("w and f must not alias"); return RBF_EINVAL; }
+  RBF_CUDA_TRY(cudaSetDevice(ctx->device));
+  KernelParams kp = kernel_params(kern);
+  const int64_t n = c->n;
+  if (prec == RBF_F32) {
+    RBF_TRY(ctx->vec_a.ensure(sizeof(float) * n, ctx->stream));
+    RBF_TRY(gather_f32_to_sorted(ctx, static_cast<const float*>(w), c->perm.as<int32_t>(), ctx->vec_a.as<float>(), n));
+    return matvec_sorted_f32(ctx, c, kp, ctx->vec_a.as<float>(), static_cast<float*>(f), c->perm.as<int32_t>(),
+                             nullptr);
+  } else if (prec == RBF_F64) {
+    RBF_TRY(ctx->vec_a.ensure(sizeof(double) * n, ctx->stream));
+    RBF_TRY(gather_f64_to_sorted(ctx, static_cast<const double*>(w), c->perm.as<int32_t>(), ctx->vec_a.as<double>(),
+                                 n));
+    return matvec_sorted_f64(ctx, c, kp, ctx->vec_a.as<double>(), static_cast<double*>(f), c->perm.as<int32_t>());
+  }
+  set_error("bad precision");
+  return RBF_EINVAL;
+}
+
+rbf_status rbf_matvec_pairs(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, int64_t* useful,
+                            int64_t* visited) {
+  RBF_TRY(check_cells(ctx, c, kern));
+  RBF_CUDA_TRY(cudaSetDevice(ctx->device));
+  KernelParams kp = kernel_params(kern);
+  const int64_t n = c->n;
+  cudaStream_t s = ctx->stream;
+  RBF_TRY(ctx->vec_a.ensure(sizeof(float) * n, s));
+  RBF_TRY(ctx->vec_b.ensure(sizeof(float) * n, s));
+  RBF_TRY(ctx->stats.ensure(64, s));
+  RBF_CUDA_TRY(cudaMemsetAsync(ctx->vec_a.p, 0, sizeof(float) * n, s));
+  RBF_CUDA_TRY(cudaMemsetAsync(ctx->stats.p, 0, 16, s));
+  RBF_TRY(matvec_sorted_f32(ctx, c, kp, ctx->vec_a.as<float>(), ctx->vec_b.as<float>(), nullptr,
+                            ctx->stats.as<unsigned long long>()));
+  unsigned long long h[2];
+  RBF_CUDA_TRY(cudaMemcpyAsync(h, ctx->stats.p, 16, cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  if (useful) *useful = (int64_t)h[0];
+  if (visited) *visited = (int64_t)h[1];
+  return RBF_OK;
+}
+
+rbf_status rbf_eval_grid(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, const double* w,
+                         const rbf_grid* g, float* field) {
+  RBF_TRY(check_cells(ctx, c, kern));
+  if (!w || !g || !field) { set_error("NULL argument"); return RBF_EINVAL; }
+  for (int a = 0; a < 3; ++a) {
+    if (g->n[a] < 2) { set_error("grid needs n >= 2 nodes per axis"); return RBF_EINVAL; }
+    if (!std::isfinite(g->lo[a]) || !std::isfinite(g->hi[a]) || !(g->hi[a] > g->lo[a])) {
+      set_error("grid box must satisfy lo < hi (finite)");
+      return RBF_EINVAL;
+    }
+  }
+  if ((double)g->n[0] * g->n[1] * g->n[2] > 4e9) { set_error("grid too large"); return RBF_EINVAL; }
+  RBF_CUDA_TRY(cudaSetDevice(ctx->device));
+  KernelParams kp = kernel_params(kern);
+  RBF_TRY(ctx->vec_a.ensure(sizeof(double) * c->n, ctx->stream));
+  RBF_TRY(gather_f64_to_sorted(ctx, w, c->perm.as<int32_t>(), ctx->vec_a.as<double>(), c->n));
+  return eval_grid_sorted(ctx, c, kp, ctx->vec_a.as<double>(), g, field);
+}
+
+}  // extern "C"

@@ -1,0 +1,160 @@
+// Internal declarations shared by the library's translation units.
+// Nothing here is part of the C-ABI (see include/rbf.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/rbf.h"
+
+namespace rbf {
+
+void set_error(const std::string& msg);
+
+#define RBF_CUDA_TRY(expr)                                                     \
+  do {                                                                         \
+    cudaError_t _e = (expr);                                                   \
+    if (_e != cudaSuccess) {                                                   \
+      ::rbf::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));    \
+      return RBF_ECUDA;                                                        \
+    }                                                                          \
+  } while (0)
+
+#define RBF_TRY(expr)                                                          \
+  do {                                                                         \
+    rbf_status _s = (expr);                                                    \
+    if (_s != RBF_OK) return _s;                                               \
+  } while (0)
+
+#define RBF_CHECK_LAUNCH() RBF_CUDA_TRY(cudaGetLastError())
+
+constexpr int kWarp = 32;
+
+// Stream-ordered device buffer (cudaMallocAsync on the context stream).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), s(o.s) { o.p = nullptr; o.bytes = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; bytes = o.bytes; s = o.s; o.p = nullptr; o.bytes = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    bytes = 0;
+  }
+  rbf_status alloc(size_t nbytes, cudaStream_t stream) {
+    release();
+    s = stream;
+    if (nbytes == 0) nbytes = 16;
+    cudaError_t e = cudaMallocAsync(&p, nbytes, stream);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      set_error(std::string("cudaMallocAsync(") + std::to_string(nbytes) + "): " + cudaGetErrorString(e));
+      cudaGetLastError();
+      return RBF_ENOMEM;
+    }
+    bytes = nbytes;
+    return RBF_OK;
+  }
+  // grow-only
+  rbf_status ensure(size_t nbytes, cudaStream_t stream) {
+    if (p && bytes >= nbytes) return RBF_OK;
+    return alloc(nbytes, stream);
+  }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+}  // namespace rbf
+
+struct rbf_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sm_count = 148;
+  rbf::DevBuf scratch;       // generic scratch (radix sort, scans)
+  rbf::DevBuf counter;       // work counters (int32 x 64)
+  rbf::DevBuf stats;         // pair counters (u64 x 4)
+  rbf::DevBuf pinned_dummy;
+  // vector workspaces for matvec (sorted order)
+  rbf::DevBuf vec_a, vec_b, src4;
+};
+
+// Tile of targets for the summation kernels: sorted positions [start, start+count).
+struct rbf_cells {
+  int64_t n = 0;
+  int dim[3] = {0, 0, 0};
+  float lo[3] = {0, 0, 0};
+  float inv_h = 0.f;
+  double h = 0.0;
+  double cutoff = 0.0;       // cutoff radius used to size the stencil at build time
+  int reach = 0;
+  int64_t ncell = 0;
+  int64_t ntiles = 0;
+  int64_t nonempty = 0;
+  int tile_cap = 64;
+  int tile_span = 2;
+  rbf::DevBuf perm;          // int32[n]
+  rbf::DevBuf sorted;        // float4[n]
+  rbf::DevBuf keys;          // uint32[n]
+  rbf::DevBuf cell_start;    // int32[ncell+1]
+  rbf::DevBuf tiles;         // int2[ntiles] (start, count)
+  rbf::DevBuf tile_box;      // float4[2*ntiles] (lo.xyz, ctr.x) (hi.xyz, unused)
+  cudaStream_t stream = nullptr;
+};
+
+namespace rbf {
+
+// Geometry constants handed to the summation kernels.
+struct CellGrid {
+  float lo[3];
+  float inv_h;
+  float h;
+  int dim[3];
+};
+
+// cells.cu
+rbf_status build_cells(rbf_ctx* ctx, const float* xyz, int64_t n, const rbf_kernel* k,
+                       const rbf_cell_cfg* cfg, rbf_cells* c);
+rbf_status exclusive_scan_u32(rbf_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t n,
+                              uint32_t* total_dev /* may be null */);
+
+// summation.cu
+struct KernelParams {
+  double sigma, cutoff, amp;
+};
+KernelParams kernel_params(const rbf_kernel* k);
+// w_sorted: fp32 sorted-order weights (matvec fp32) -> f_sorted fp32
+rbf_status matvec_sorted_f32(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
+                             const float* w_sorted, float* f_sorted, const int32_t* out_perm,
+                             unsigned long long* pair_stats);
+rbf_status matvec_sorted_f64(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
+                             const double* w_sorted, double* f_sorted, const int32_t* out_perm);
+rbf_status eval_grid_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
+                            const double* w_sorted, const rbf_grid* g, float* field);
+
+// small vector kernels (vec.cu)
+rbf_status gather_f32_to_sorted(rbf_ctx* ctx, const float* src, const int32_t* perm, float* dst, int64_t n);
+rbf_status gather_f64_to_sorted(rbf_ctx* ctx, const double* src, const int32_t* perm, double* dst, int64_t n);
+rbf_status gather_f64_to_sorted_f32(rbf_ctx* ctx, const double* src, const int32_t* perm, float* dst, int64_t n);
+rbf_status scatter_f32_from_sorted(rbf_ctx* ctx, const float* src, const int32_t* perm, float* dst, int64_t n);
+rbf_status scatter_f64_from_sorted(rbf_ctx* ctx, const double* src, const int32_t* perm, double* dst, int64_t n);
+
+inline int grid_for(int64_t n, int threads, int max_blocks = 148 * 16) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > max_blocks) b = max_blocks;
+  return (int)b;
+}
+
+}  // namespace rbf
+
+namespace rbf {
+const char* last_error_cstr();
+}

@@ -1,0 +1,581 @@
+// a3 / a7 / a8 of SURVEY.md §8(a): the truncated Gaussian kernel summation
+//
+//     f_i = a * sum_{j : |x_i - x_j|^2 <= c^2} w_j exp(-|x_i - x_j|^2 / (2 sigma^2))
+//
+// (Eq.6 P:363-366 entries; Eq.4 P:257-262 matvec; Eq.5 P:264-271 evaluation
+// on a grid; truncation P:361-369).  Alg.3 stages centres in
+// shared memory and loops over ALL of them; here the loop runs only over the
+// cells within the cutoff of a target tile (matrix-free, never assembled).
+//
+// Execution model (sm_100a):
+//  * one warp owns one target tile (<= 64 targets, 2 per lane) and pulls
+//    tiles from a global work counter (dynamic balance over 148 SMs);
+//  * the sources of the cell rows within the cutoff of the tile's bounding
+//    box are streamed 32 at a time with coalesced float4 loads (x,y,z,w),
+//    culled against the box (ballot + compaction), and staged in a
+//    warp-private shared-memory ring as SoA; every 64 staged sources the warp
+//    runs the dense inner loop;
+//  * fp32 tier inner loop: coordinates are shifted to the tile centre and
+//    scaled by sqrt(k), k = log2(e)/(2 sigma^2), so one packed FADD2 per
+//    coordinate, FMUL2 + 2 FFMA2 give the scaled r^2 of two pairs; the
+//    cutoff is an integer compare+select on the bits of r^2 (ALU pipe),
+//    MUFU.EX2 evaluates 2^-r'^2, and a packed FFMA2 accumulates.  No
+//    tensor cores: the K=3 distance form is not a dense contraction.
+//  * fp64 tier: same traversal; |x_i-x_j|^2 in fp64 with the oracle's
+//    rounding order ((dx^2 + dy^2) + dz^2), fp64 exp, fp64 weights.
+#include <cmath>
+#include <algorithm>
+
+#include "internal.h"
+
+namespace rbf {
+namespace {
+
+constexpr int kSumWarps = 4;            // warps per CTA
+constexpr int kFlush = 64;              // sources per inner-loop batch
+constexpr int kBuf = kFlush + 32 + 4;   // staging ring capacity (SoA, floats)
+constexpr int kBufPad = 104;            // multiple of 4 >= kBuf
+
+// --------------------------------------------------------------- packed ops
+__device__ __forceinline__ unsigned long long pk(float2 a) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
+}
+__device__ __forceinline__ float2 upk(unsigned long long r) {
+  float2 a;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+  return a;
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk(a)), "l"(pk(b)));
+  return upk(d);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk(a)), "l"(pk(b)));
+  return upk(d);
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk(a)), "l"(pk(b)), "l"(pk(c)));
+  return upk(d);
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// r2 if r2 <= C2 else +inf, compared on the bit pattern (r2 >= 0): ISETP+SEL.
+__device__ __forceinline__ float cutmask(float r2, int c2bits) {
+  int b = __float_as_int(r2);
+  return __int_as_float(b <= c2bits ? b : 0x7f800000);
+}
+
+struct SumGeom {
+  CellGrid g;
+  float cc;     // culling radius (cutoff inflated by rounding margins)
+  float cc2;
+  float s;      // sqrt(k), k = log2(e) / (2 sigma^2)
+  int c2bits;   // bits of float32(k c^2)
+  float amp;    // a
+  // fp64 tier
+  double c2d;        // (cutoff_sigmas * sigma)^2 exactly as the oracle forms it
+  double two_s2;     // 2 sigma^2
+  double ampd;
+};
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+__device__ __forceinline__ int cellof(float x, float lo, float inv_h, int dim) {
+  float t = floorf((x - lo) * inv_h);
+  t = fminf(fmaxf(t, -1.f), (float)dim);
+  return clampi((int)t, 0, dim - 1);
+}
+
+// Row-streaming traversal shared by all tiers.  For every cell row within the
+// (inflated) cutoff of the box [blo, bhi], the contiguous source range is
+// streamed through `stage(j, valid)` (32 lanes at a time; returns whether the
+// lane keeps its source and writes it to the ring at the position it is
+// given) and `flush(count)` is called on full batches.
+template <class Load, class Flush>
+__device__ __forceinline__ void traverse(const SumGeom& G, const int32_t* __restrict__ cell_start,
+                                         float3 blo, float3 bhi, int lane, Load&& load, Flush&& flush,
+                                         int& nbuf) {
+  const CellGrid& g = G.g;
+  const float cc = G.cc, cc2 = G.cc2, h = g.h;
+  const int z0 = cellof(blo.z - cc, g.lo[2], g.inv_h, g.dim[2]);
+  const int z1 = cellof(bhi.z + cc, g.lo[2], g.inv_h, g.dim[2]);
+  const int y0 = cellof(blo.y - cc, g.lo[1], g.inv_h, g.dim[1]);
+  const int y1 = cellof(bhi.y + cc, g.lo[1], g.inv_h, g.dim[1]);
+  const unsigned lt = (1u << lane) - 1u;
+  for (int cz = z0; cz <= z1; ++cz) {
+    const float czlo = g.lo[2] + (float)cz * h;
+    const float gz = fmaxf(0.f, fmaxf(czlo - bhi.z, blo.z - (czlo + h)));
+    for (int cy = y0; cy <= y1; ++cy) {
+      const float cylo = g.lo[1] + (float)cy * h;
+      const float gy = fmaxf(0.f, fmaxf(cylo - bhi.y, blo.y - (cylo + h)));
+      const float rem = cc2 - gy * gy - gz * gz;
+      if (rem < 0.f) continue;
+      const float rx = sqrtf(rem);
+      const int x0 = cellof(blo.x - rx, g.lo[0], g.inv_h, g.dim[0]);
+      const int x1 = cellof(bhi.x + rx, g.lo[0], g.inv_h, g.dim[0]);
+      const int64_t rowbase = ((int64_t)cz * g.dim[1] + cy) * g.dim[0];
+      const int sb = __ldg(cell_start + rowbase + x0);
+      const int se = __ldg(cell_start + rowbase + x1 + 1);
+      for (int j0 = sb; j0 < se; j0 += 32) {
+        const int j = j0 + lane;
+        bool keep = load(j, j < se);  // loads + culls into registers
+        unsigned bal = __ballot_sync(0xffffffffu, keep);
+        int pos = nbuf + __popc(bal & lt);
+        load.store(keep, pos);
+        nbuf += __popc(bal);
+        if (nbuf >= kFlush) {
+          __syncwarp();
+          flush(kFlush);
+          __syncwarp();
+          load.shift(nbuf - kFlush, lane);
+          __syncwarp();
+          nbuf -= kFlush;
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------- fp32 tier ---
+struct Ring32 {
+  float* bx; float* by; float* bz; float* bw;
+};
+
+struct Stage32 {
+  Ring32 r;
+  const float4* __restrict__ src;
+  float3 blo, bhi, ctr;
+  float cc2, s;
+  float4 p;
+  __device__ __forceinline__ bool operator()(int j, bool valid) {
+    p = valid ? __ldg(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float gx = fmaxf(0.f, fmaxf(blo.x - p.x, p.x - bhi.x));
+    float gy = fmaxf(0.f, fmaxf(blo.y - p.y, p.y - bhi.y));
+    float gz = fmaxf(0.f, fmaxf(blo.z - p.z, p.z - bhi.z));
+    return valid && (gx * gx + gy * gy + gz * gz <= cc2);
+  }
+  __device__ __forceinline__ void store(bool keep, int pos) {
+    if (keep) {
+      r.bx[pos] = (p.x - ctr.x) * s;
+      r.by[pos] = (p.y - ctr.y) * s;
+      r.bz[pos] = (p.z - ctr.z) * s;
+      r.bw[pos] = p.w;
+    }
+  }
+  __device__ __forceinline__ void shift(int rest, int lane) {
+    if (lane < rest) {
+      float a = r.bx[kFlush + lane], b = r.by[kFlush + lane], c = r.bz[kFlush + lane], d = r.bw[kFlush + lane];
+      r.bx[lane] = a; r.by[lane] = b; r.bz[lane] = c; r.bw[lane] = d;
+    }
+  }
+};
+
+template <int T>
+struct Flush32 {
+  Ring32 r;
+  float2* acc;            // [T]
+  const float* xt; const float* yt; const float* zt;   // [T] scaled local target coords
+  int c2bits;
+  __device__ __forceinline__ void operator()(int cnt) {
+#pragma unroll 2
+    for (int j = 0; j < cnt; j += 4) {
+      const float4 X = *reinterpret_cast<const float4*>(r.bx + j);
+      const float4 Y = *reinterpret_cast<const float4*>(r.by + j);
+      const float4 Z = *reinterpret_cast<const float4*>(r.bz + j);
+      const float4 W = *reinterpret_cast<const float4*>(r.bw + j);
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const float2 tx = make_float2(xt[t], xt[t]);
+        const float2 ty = make_float2(yt[t], yt[t]);
+        const float2 tz = make_float2(zt[t], zt[t]);
+        float2 dxa = sub2(make_float2(X.x, X.y), tx), dxb = sub2(make_float2(X.z, X.w), tx);
+        float2 dya = sub2(make_float2(Y.x, Y.y), ty), dyb = sub2(make_float2(Y.z, Y.w), ty);
+        float2 dza = sub2(make_float2(Z.x, Z.y), tz), dzb = sub2(make_float2(Z.z, Z.w), tz);
+        float2 ra = mul2(dxa, dxa), rb = mul2(dxb, dxb);
+        ra = fma2(dya, dya, ra); rb = fma2(dyb, dyb, rb);
+        ra = fma2(dza, dza, ra); rb = fma2(dzb, dzb, rb);
+        float2 ea = make_float2(ex2(-cutmask(ra.x, c2bits)), ex2(-cutmask(ra.y, c2bits)));
+        float2 eb = make_float2(ex2(-cutmask(rb.x, c2bits)), ex2(-cutmask(rb.y, c2bits)));
+        acc[t] = fma2(ea, make_float2(W.x, W.y), acc[t]);
+        acc[t] = fma2(eb, make_float2(W.z, W.w), acc[t]);
+      }
+    }
+  }
+};
+
+// pair statistics variant (slow; used only by rbf_matvec_pairs)
+template <int T>
+struct FlushStats {
+  Ring32 r;
+  const float* xt; const float* yt; const float* zt;
+  const bool* tvalid;
+  int c2bits;
+  unsigned long long* useful; unsigned long long* visited;
+  __device__ __forceinline__ void operator()(int cnt) {
+    for (int j = 0; j < cnt; ++j) {
+      if (r.bx[j] > 1e17f) continue;  // padding
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        if (!tvalid[t]) continue;
+        float dx = r.bx[j] - xt[t], dy = r.by[j] - yt[t], dz = r.bz[j] - zt[t];
+        float r2 = dx * dx + dy * dy + dz * dz;
+        *visited += 1;
+        if (__float_as_int(r2) <= c2bits) *useful += 1;
+      }
+    }
+  }
+};
+
+__device__ __forceinline__ void pad_ring(Ring32 r, int nbuf, int lane, int& cnt) {
+  cnt = (nbuf + 3) & ~3;
+  if (lane < cnt - nbuf) {
+    const int q = nbuf + lane;
+    r.bx[q] = 1e18f; r.by[q] = 1e18f; r.bz[q] = 1e18f; r.bw[q] = 0.f;
+  }
+  __syncwarp();
+}
+
+// Targets: mode 0 = tile of sorted centres, mode 1 = 4x4x4 block of grid nodes.
+struct GridDesc {
+  double lo[3], step[3];
+  int n[3];
+  int nb[3];   // blocks per axis
+};
+
+__device__ __forceinline__ float node_coord(const GridDesc& gd, int a, int i) {
+  return (float)(gd.lo[a] + (double)i * gd.step[a]);
+}
+
+template <int MODE, bool STATS>
+__global__ void __launch_bounds__(kSumWarps * 32)
+sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* __restrict__ src,
+               const int2* __restrict__ tiles, const float4* __restrict__ tbox, int64_t ntiles,
+               GridDesc gd, float* __restrict__ out, const int32_t* __restrict__ out_perm,
+               int* __restrict__ work, unsigned long long* __restrict__ stats) {
+  __shared__ __align__(16) float ring[kSumWarps][4][kBufPad];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  Ring32 R{ring[wib][0], ring[wib][1], ring[wib][2], ring[wib][3]};
+  unsigned long long useful = 0, visited = 0;
+  for (;;) {
+    int64_t tile;
+    {
+      int t0 = 0;
+      if (lane == 0) t0 = atomicAdd(work, 1);
+      tile = __shfl_sync(0xffffffffu, t0, 0);
+    }
+    if (tile >= ntiles) break;
+    float3 blo, bhi;
+    float xr[2], yr[2], zr[2];   // raw target coordinates
+    bool tv[2];
+    int tcount;
+    int64_t tidx[2];
+    if (MODE == 0) {
+      const int2 tl = tiles[tile];
+      const float4 a = tbox[2 * tile], b = tbox[2 * tile + 1];
+      blo = make_float3(a.x, a.y, a.z);
+      bhi = make_float3(b.x, b.y, b.z);
+      tcount = tl.y;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        int q = lane + 32 * t;
+        tv[t] = q < tl.y;
+        tidx[t] = tl.x + (tv[t] ? q : 0);
+        float4 p = src[tidx[t]];
+        xr[t] = p.x; yr[t] = p.y; zr[t] = p.z;
+      }
+    } else {
+      const int bx = (int)(tile % gd.nb[0]);
+      const int by = (int)((tile / gd.nb[0]) % gd.nb[1]);
+      const int bz = (int)(tile / ((int64_t)gd.nb[0] * gd.nb[1]));
+      const int i0 = 4 * bx, j0 = 4 * by, k0 = 4 * bz;
+      const int i1 = min(i0 + 3, gd.n[0] - 1), j1 = min(j0 + 3, gd.n[1] - 1), k1 = min(k0 + 3, gd.n[2] - 1);
+      blo = make_float3(node_coord(gd, 0, i0), node_coord(gd, 1, j0), node_coord(gd, 2, k0));
+      bhi = make_float3(node_coord(gd, 0, i1), node_coord(gd, 1, j1), node_coord(gd, 2, k1));
+      tcount = (k1 - k0 + 1) > 2 ? 64 : 32;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        int i = i0 + (lane & 3), j = j0 + ((lane >> 2) & 3), k = k0 + (lane >> 4) + 2 * t;
+        tv[t] = (i <= i1) && (j <= j1) && (k <= k1);
+        i = min(i, i1); j = min(j, j1); k = min(k, k1);
+        tidx[t] = (int64_t)i + (int64_t)gd.n[0] * ((int64_t)j + (int64_t)gd.n[1] * k);
+        xr[t] = node_coord(gd, 0, i); yr[t] = node_coord(gd, 1, j); zr[t] = node_coord(gd, 2, k);
+      }
+    }
+    const float3 ctr = make_float3(0.5f * (blo.x + bhi.x), 0.5f * (blo.y + bhi.y), 0.5f * (blo.z + bhi.z));
+    float xt[2], yt[2], zt[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      xt[t] = (xr[t] - ctr.x) * G.s; yt[t] = (yr[t] - ctr.y) * G.s; zt[t] = (zr[t] - ctr.z) * G.s;
+    }
+    float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    Stage32 st{R, src, blo, bhi, ctr, G.cc2, G.s, make_float4(0, 0, 0, 0)};
+    int nbuf = 0;
+    const bool two = tcount > 32;
+    if (STATS) {
+      FlushStats<2> fs{R, xt, yt, zt, tv, G.c2bits, &useful, &visited};
+      traverse(G, cell_start, blo, bhi, lane, st, fs, nbuf);
+      int cnt;
+      pad_ring(R, nbuf, lane, cnt);
+      fs(cnt);
+      __syncwarp();
+    } else if (two) {
+      Flush32<2> fl{R, acc, xt, yt, zt, G.c2bits};
+      traverse(G, cell_start, blo, bhi, lane, st, fl, nbuf);
+      int cnt;
+      pad_ring(R, nbuf, lane, cnt);
+      fl(cnt);
+      __syncwarp();
+    } else {
+      Flush32<1> fl{R, acc, xt, yt, zt, G.c2bits};
+      traverse(G, cell_start, blo, bhi, lane, st, fl, nbuf);
+      int cnt;
+      pad_ring(R, nbuf, lane, cnt);
+      fl(cnt);
+      __syncwarp();
+    }
+    if (!STATS) {
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        if (!tv[t]) continue;
+        float v = G.amp * (acc[t].x + acc[t].y);
+        int64_t o = tidx[t];
+        if (MODE == 0 && out_perm) o = out_perm[o];
+        out[o] = v;
+      }
+    }
+  }
+  if (STATS) {
+    for (int o = 16; o > 0; o >>= 1) {
+      useful += __shfl_xor_sync(0xffffffffu, useful, o);
+      visited += __shfl_xor_sync(0xffffffffu, visited, o);
+    }
+    if (lane == 0) { atomicAdd(stats, useful); atomicAdd(stats + 1, visited); }
+  }
+}
+
+// ------------------------------------------------------------- fp64 tier ---
+struct Ring64 {
+  float* bx; float* by; float* bz; double* bw;
+};
+
+struct Stage64 {
+  Ring64 r;
+  const float4* __restrict__ src;
+  const double* __restrict__ w;
+  float3 blo, bhi;
+  float cc2;
+  float4 p;
+  double wj;
+  __device__ __forceinline__ bool operator()(int j, bool valid) {
+    p = valid ? __ldg(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    wj = valid ? __ldg(w + j) : 0.0;
+    float gx = fmaxf(0.f, fmaxf(blo.x - p.x, p.x - bhi.x));
+    float gy = fmaxf(0.f, fmaxf(blo.y - p.y, p.y - bhi.y));
+    float gz = fmaxf(0.f, fmaxf(blo.z - p.z, p.z - bhi.z));
+    return valid && (gx * gx + gy * gy + gz * gz <= cc2);
+  }
+  __device__ __forceinline__ void store(bool keep, int pos) {
+    if (keep) { r.bx[pos] = p.x; r.by[pos] = p.y; r.bz[pos] = p.z; r.bw[pos] = wj; }
+  }
+  __device__ __forceinline__ void shift(int rest, int lane) {
+    if (lane < rest) {
+      float a = r.bx[kFlush + lane], b = r.by[kFlush + lane], c = r.bz[kFlush + lane];
+      double d = r.bw[kFlush + lane];
+      r.bx[lane] = a; r.by[lane] = b; r.bz[lane] = c; r.bw[lane] = d;
+    }
+  }
+};
+
+struct Flush64 {
+  Ring64 r;
+  double* acc;                       // [2]
+  const double* xt; const double* yt; const double* zt;
+  double c2, two_s2, amp;
+  __device__ __forceinline__ void operator()(int cnt) {
+    for (int j = 0; j < cnt; ++j) {
+      const double sx = (double)r.bx[j], sy = (double)r.by[j], sz = (double)r.bz[j], wj = r.bw[j];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        double dx = __dsub_rn(sx, xt[t]), dy = __dsub_rn(sy, yt[t]), dz = __dsub_rn(sz, zt[t]);
+        double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+        if (d2 <= c2) {
+          double v = __dmul_rn(amp, exp(-d2 / two_s2));
+          acc[t] = __fma_rn(v, wj, acc[t]);
+        }
+      }
+    }
+  }
+};
+
+__global__ void __launch_bounds__(kSumWarps * 32)
+sum_f64_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* __restrict__ src,
+               const double* __restrict__ w, const int2* __restrict__ tiles,
+               const float4* __restrict__ tbox, int64_t ntiles, double* __restrict__ out,
+               const int32_t* __restrict__ out_perm, int* __restrict__ work) {
+  __shared__ __align__(16) float ringf[kSumWarps][3][kBufPad];
+  __shared__ __align__(16) double ringd[kSumWarps][kBufPad];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  Ring64 R{ringf[wib][0], ringf[wib][1], ringf[wib][2], ringd[wib]};
+  for (;;) {
+    int64_t tile;
+    {
+      int t0 = 0;
+      if (lane == 0) t0 = atomicAdd(work, 1);
+      tile = __shfl_sync(0xffffffffu, t0, 0);
+    }
+    if (tile >= ntiles) break;
+    const int2 tl = tiles[tile];
+    const float4 a = tbox[2 * tile], b = tbox[2 * tile + 1];
+    const float3 blo = make_float3(a.x, a.y, a.z), bhi = make_float3(b.x, b.y, b.z);
+    double xt[2], yt[2], zt[2], acc[2] = {0.0, 0.0};
+    bool tv[2];
+    int64_t tidx[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      int q = lane + 32 * t;
+      tv[t] = q < tl.y;
+      tidx[t] = tl.x + (tv[t] ? q : 0);
+      float4 p = src[tidx[t]];
+      xt[t] = p.x; yt[t] = p.y; zt[t] = p.z;
+    }
+    Stage64 st{R, src, w, blo, bhi, G.cc2, make_float4(0, 0, 0, 0), 0.0};
+    Flush64 fl{R, acc, xt, yt, zt, G.c2d, G.two_s2, G.ampd};
+    int nbuf = 0;
+    traverse(G, cell_start, blo, bhi, lane, st, fl, nbuf);
+    __syncwarp();
+    fl(nbuf);
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      if (!tv[t]) continue;
+      int64_t o = out_perm ? out_perm[tidx[t]] : tidx[t];
+      out[o] = acc[t];
+    }
+  }
+}
+
+// pack (x, y, z, w) records in sorted order for the fp32 tier
+__global__ void pack_src_f32(const float4* __restrict__ sorted, const float* __restrict__ w, int64_t n,
+                             float4* __restrict__ src) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 p = sorted[i];
+    p.w = w[i];
+    src[i] = p;
+  }
+}
+__global__ void pack_src_f64w(const float4* __restrict__ sorted, const double* __restrict__ w, int64_t n,
+                              float4* __restrict__ src) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 p = sorted[i];
+    p.w = (float)w[i];
+    src[i] = p;
+  }
+}
+
+SumGeom make_geom(const rbf_cells* c, const KernelParams& kp) {
+  SumGeom G;
+  for (int a = 0; a < 3; ++a) { G.g.lo[a] = c->lo[a]; G.g.dim[a] = c->dim[a]; }
+  G.g.inv_h = c->inv_h;
+  G.g.h = (float)c->h;
+  double maxabs = 0;
+  for (int a = 0; a < 3; ++a)
+    maxabs = std::max(maxabs, std::max(std::fabs((double)c->lo[a]), std::fabs(c->lo[a] + c->dim[a] * c->h)));
+  double cc = kp.cutoff * (1.0 + 1e-5) + 4e-7 * maxabs + 1e-30;
+  G.cc = (float)cc;
+  G.cc2 = (float)(cc * cc);
+  const double k = 1.4426950408889634 / (2.0 * kp.sigma * kp.sigma);
+  G.s = (float)std::sqrt(k);
+  float c2s = (float)(k * kp.cutoff * kp.cutoff);
+  int bits;
+  memcpy(&bits, &c2s, 4);
+  G.c2bits = bits;
+  G.amp = (float)kp.amp;
+  G.c2d = kp.cutoff * kp.cutoff;
+  G.two_s2 = 2.0 * kp.sigma * kp.sigma;
+  G.ampd = kp.amp;
+  return G;
+}
+
+int sum_blocks(rbf_ctx* ctx) { return ctx->sm_count * 8; }
+
+}  // namespace
+
+KernelParams kernel_params(const rbf_kernel* k) {
+  KernelParams p;
+  p.sigma = k->sigma;
+  p.cutoff = k->cutoff_sigmas * k->sigma;
+  p.amp = k->amplitude > 0 ? k->amplitude : 1.0 / (std::sqrt(2.0 * M_PI) * k->sigma);
+  return p;
+}
+
+rbf_status matvec_sorted_f32(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
+                             const float* w_sorted, float* f_out, const int32_t* out_perm,
+                             unsigned long long* pair_stats) {
+  cudaStream_t s = ctx->stream;
+  const int64_t n = c->n;
+  RBF_TRY(ctx->src4.ensure(sizeof(float4) * n, s));
+  RBF_TRY(ctx->counter.ensure(256, s));
+  pack_src_f32<<<grid_for(n, 256), 256, 0, s>>>(c->sorted.as<float4>(), w_sorted, n, ctx->src4.as<float4>());
+  RBF_CHECK_LAUNCH();
+  RBF_CUDA_TRY(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
+  SumGeom G = make_geom(c, kp);
+  GridDesc gd{};
+  if (pair_stats) {
+    sum_f32_kernel<0, true><<<sum_blocks(ctx), kSumWarps * 32, 0, s>>>(
+        G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), c->tiles.as<int2>(), c->tile_box.as<float4>(),
+        c->ntiles, gd, f_out, out_perm, ctx->counter.as<int>(), pair_stats);
+  } else {
+    sum_f32_kernel<0, false><<<sum_blocks(ctx), kSumWarps * 32, 0, s>>>(
+        G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), c->tiles.as<int2>(), c->tile_box.as<float4>(),
+        c->ntiles, gd, f_out, out_perm, ctx->counter.as<int>(), nullptr);
+  }
+  RBF_CHECK_LAUNCH();
+  return RBF_OK;
+}
+
+rbf_status matvec_sorted_f64(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
+                             const double* w_sorted, double* f_out, const int32_t* out_perm) {
+  cudaStream_t s = ctx->stream;
+  RBF_TRY(ctx->counter.ensure(256, s));
+  RBF_CUDA_TRY(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
+  SumGeom G = make_geom(c, kp);
+  sum_f64_kernel<<<sum_blocks(ctx), kSumWarps * 32, 0, s>>>(
+      G, c->cell_start.as<int32_t>(), c->sorted.as<float4>(), w_sorted, c->tiles.as<int2>(),
+      c->tile_box.as<float4>(), c->ntiles, f_out, out_perm, ctx->counter.as<int>());
+  RBF_CHECK_LAUNCH();
+  return RBF_OK;
+}
+
+rbf_status eval_grid_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
+                            const double* w_sorted, const rbf_grid* g, float* field) {
+  cudaStream_t s = ctx->stream;
+  const int64_t n = c->n;
+  RBF_TRY(ctx->src4.ensure(sizeof(float4) * n, s));
+  RBF_TRY(ctx->counter.ensure(256, s));
+  pack_src_f64w<<<grid_for(n, 256), 256, 0, s>>>(c->sorted.as<float4>(), w_sorted, n, ctx->src4.as<float4>());
+  RBF_CHECK_LAUNCH();
+  RBF_CUDA_TRY(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
+  SumGeom G = make_geom(c, kp);
+  GridDesc gd;
+  for (int a = 0; a < 3; ++a) {
+    gd.lo[a] = g->lo[a];
+    gd.step[a] = (g->hi[a] - g->lo[a]) / (double)(g->n[a] - 1);
+    gd.n[a] = g->n[a];
+    gd.nb[a] = (g->n[a] + 3) / 4;
+  }
+  int64_t nblk = (int64_t)gd.nb[0] * gd.nb[1] * gd.nb[2];
+  sum_f32_kernel<1, false><<<sum_blocks(ctx), kSumWarps * 32, 0, s>>>(
+      G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), nullptr, nullptr, nblk, gd, field, nullptr,
+      ctx->counter.as<int>(), nullptr);
+  RBF_CHECK_LAUNCH();
+  return RBF_OK;
+}
+
+}  // namespace rbf

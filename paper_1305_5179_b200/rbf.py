@@ -1,0 +1,375 @@
+"""Thin Python binding of the C-ABI in include/rbf.h (argument marshalling only).
+
+Every step of the path runs in librbf.so's CUDA kernels; torch supplies device
+memory, the current stream and process groups.  There is no CPU fallback: if
+the library is missing or the device is not a B200 the calls raise.
+
+Names follow include/rbf.h (and the paper's notation: sigma, centres, w for the
+coefficients c_j of Eq.3, the grid xi of Eq.5).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librbf.so")
+
+RBF_OK, RBF_EINVAL, RBF_ENOMEM, RBF_ECUDA, RBF_ENCCL, RBF_EUNSUPPORTED = range(6)
+RBF_F32, RBF_F64 = 0, 1
+
+
+class RbfError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_STATUS = {0: "RBF_OK", 1: "RBF_EINVAL", 2: "RBF_ENOMEM", 3: "RBF_ECUDA", 4: "RBF_ENCCL",
+           5: "RBF_EUNSUPPORTED"}
+
+
+# ----------------------------------------------------------------- structs --
+class _Kernel(C.Structure):
+    _fields_ = [("sigma", C.c_double), ("cutoff_sigmas", C.c_double), ("amplitude", C.c_double)]
+
+
+class _CellCfg(C.Structure):
+    _fields_ = [("cell_edge", C.c_double), ("tile_cap", C.c_int), ("tile_span", C.c_int)]
+
+
+class _PrecondCfg(C.Structure):
+    _fields_ = [("kind", C.c_int), ("core_target", C.c_int), ("overlap_sigmas", C.c_double),
+                ("max_ext", C.c_int)]
+
+
+class _GmresCfg(C.Structure):
+    _fields_ = [("restart", C.c_int), ("rtol", C.c_double), ("phase1_rtol", C.c_double),
+                ("max_iters", C.c_int), ("polish_fp64", C.c_int)]
+
+
+class SolveReport(C.Structure):
+    _fields_ = [("iters_phase1", C.c_int), ("iters_phase2", C.c_int), ("restarts", C.c_int),
+                ("converged", C.c_int), ("breakdown", C.c_int),
+                ("rel_residual_true", C.c_double), ("rel_residual_est", C.c_double),
+                ("t_setup", C.c_double), ("t_phase1", C.c_double), ("t_phase2", C.c_double),
+                ("nblocks", C.c_int64), ("precond_bytes", C.c_int64),
+                ("matvecs_f32", C.c_int64), ("matvecs_f64", C.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class _Grid(C.Structure):
+    _fields_ = [("lo", C.c_double * 3), ("hi", C.c_double * 3), ("n", C.c_int * 3)]
+
+
+class _CellsDesc(C.Structure):
+    _fields_ = [("n", C.c_int64), ("dim", C.c_int * 3), ("lo", C.c_float * 3), ("inv_h", C.c_float),
+                ("cell_edge", C.c_double), ("reach", C.c_int), ("ncell", C.c_int64),
+                ("ntiles", C.c_int64), ("nonempty_cells", C.c_int64)]
+
+
+_P = C.c_void_p
+EXPORTS = {
+    # name: (restype, argtypes)
+    "rbf_create": (C.c_int, [C.POINTER(_P), C.c_int, _P, _P, C.c_int, C.c_int]),
+    "rbf_destroy": (None, [_P]),
+    "rbf_status_str": (C.c_char_p, [C.c_int]),
+    "rbf_last_error": (C.c_char_p, []),
+    "rbf_abi_version": (C.c_int, []),
+    "rbf_extend_points": (C.c_int, [_P, _P, _P, C.c_int64, C.c_double, C.c_double, _P, _P]),
+    "rbf_build_cells": (C.c_int, [_P, _P, C.c_int64, C.POINTER(_Kernel), C.POINTER(_CellCfg),
+                                  C.POINTER(_P)]),
+    "rbf_cells_free": (None, [_P]),
+    "rbf_cells_info": (C.c_int, [_P, C.POINTER(_CellsDesc)]),
+    "rbf_cells_view": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)]),
+    "rbf_matvec": (C.c_int, [_P, _P, C.POINTER(_Kernel), C.c_int, _P, _P]),
+    "rbf_matvec_pairs": (C.c_int, [_P, _P, C.POINTER(_Kernel), C.POINTER(C.c_int64),
+                                   C.POINTER(C.c_int64)]),
+    "rbf_precond_create": (C.c_int, [_P, _P, C.POINTER(_Kernel), C.POINTER(_PrecondCfg),
+                                     C.POINTER(_P)]),
+    "rbf_precond_free": (None, [_P]),
+    "rbf_precond_apply": (C.c_int, [_P, _P, _P, _P]),
+    "rbf_precond_blocks": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), _P, _P, _P, _P]),
+    "rbf_gmres_solve": (C.c_int, [_P, _P, C.POINTER(_Kernel), _P, C.POINTER(_PrecondCfg),
+                                  C.POINTER(_GmresCfg), _P, _P, C.POINTER(SolveReport)]),
+    "rbf_eval_grid": (C.c_int, [_P, _P, C.POINTER(_Kernel), _P, C.POINTER(_Grid), _P]),
+    "rbf_reconstruct_host": (C.c_int, [_P, _P, _P, C.c_int64, C.POINTER(_Kernel), C.POINTER(_CellCfg),
+                                       C.POINTER(_PrecondCfg), C.POINTER(_GmresCfg), C.POINTER(_Grid),
+                                       _P, _P, C.POINTER(SolveReport)]),
+}
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load librbf.so; raises (never falls back) when it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"librbf.so not found at {path}: run __graft_entry__.build() "
+                           "(python -m paper_1305_5179_b200.build); there is no CPU fallback")
+    lib = C.CDLL(path)
+    for name, (res, args) in EXPORTS.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(status: int):
+    if status != RBF_OK:
+        msg = _lib.rbf_last_error()
+        raise RbfError(status, msg.decode() if msg else "")
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _need(t: torch.Tensor, dtype, n: int | None = None, name: str = "tensor"):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if n is not None and t.numel() != n:
+        raise ValueError(f"{name} must have {n} elements, got {t.numel()}")
+
+
+class _DevArray:
+    """Exposes a library-owned device pointer through __cuda_array_interface__."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), True), "version": 2, "strides": None}
+
+
+def _wrap_copy(ptr, shape, typestr, dtype, device):
+    if ptr is None or int(ptr) == 0:
+        return torch.empty(shape, dtype=dtype, device=device)
+    return torch.as_tensor(_DevArray(ptr, shape, typestr), device=device).clone()
+
+
+# -------------------------------------------------------------- public API --
+@dataclass(frozen=True)
+class Kernel:
+    """Gaussian RBF of Eq.6: a exp(-r^2/(2 sigma^2)), 0 beyond cutoff_sigmas*sigma."""
+    sigma: float
+    cutoff_sigmas: float = 6.0
+    amplitude: float = 0.0   # <= 0 => 1/(sqrt(2 pi) sigma)
+
+    def _c(self):
+        return _Kernel(self.sigma, self.cutoff_sigmas, self.amplitude)
+
+
+class Context:
+    """rbf_create on `device`, issuing work on torch's current stream of that device."""
+
+    def __init__(self, device: int = 0, stream: torch.cuda.Stream | None = None):
+        lib = load_library()
+        self.device = device
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        h = C.c_void_p()
+        _check(lib.rbf_create(C.byref(h), device, C.c_void_p(self.stream.cuda_stream), None, 0, 1))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.rbf_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def extend_points(ctx: Context, x: torch.Tensor, normals: torch.Tensor, delta: float, label: float | None = None):
+    """Extended set of §2.1.1 and labels of §2.1.2:
+    centres [X; X + delta n; X - delta n] (fp32, 3N x 3) and b = [0; +label; -label]
+    (label defaults to delta, reading R2)."""
+    _need(x, torch.float64, name="x")
+    _need(normals, torch.float64, x.numel(), "normals")
+    N = x.shape[0]
+    centres = torch.empty((3 * N, 3), dtype=torch.float32, device=x.device)
+    b = torch.empty(3 * N, dtype=torch.float32, device=x.device)
+    _check(_lib.rbf_extend_points(ctx._h, _ptr(x), _ptr(normals), N, float(delta),
+                                  float(delta if label is None else label), _ptr(centres), _ptr(b)))
+    return centres, b
+
+
+class Cells:
+    """rbf_build_cells: cell list + tile plan over the centres (Alg.2 'truncation area')."""
+
+    def __init__(self, ctx: Context, xyz: torch.Tensor, kernel: Kernel, cell_edge: float = 0.0,
+                 tile_cap: int = 64, tile_span: int = 2):
+        _need(xyz, torch.float32, name="xyz")
+        if xyz.dim() != 2 or xyz.shape[1] != 3:
+            raise ValueError("xyz must be (n, 3)")
+        self.ctx, self.kernel = ctx, kernel
+        self.n = xyz.shape[0]
+        h = C.c_void_p()
+        cfg = _CellCfg(cell_edge, tile_cap, tile_span)
+        _check(_lib.rbf_build_cells(ctx._h, _ptr(xyz), self.n, C.byref(kernel._c()), C.byref(cfg),
+                                    C.byref(h)))
+        self._h = h
+
+    def info(self) -> dict:
+        d = _CellsDesc()
+        _check(_lib.rbf_cells_info(self._h, C.byref(d)))
+        return dict(n=d.n, dim=tuple(d.dim), lo=tuple(d.lo), inv_h=d.inv_h, cell_edge=d.cell_edge,
+                    reach=d.reach, ncell=d.ncell, ntiles=d.ntiles, nonempty_cells=d.nonempty_cells)
+
+    def view(self) -> dict:
+        """Copies of the library's cell arrays (perm, sorted float4, keys, cell_start)."""
+        perm, srt, keys, cs = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _check(_lib.rbf_cells_view(self._h, C.byref(perm), C.byref(srt), C.byref(keys), C.byref(cs)))
+        info = self.info()
+        dev = torch.device("cuda", self.ctx.device)
+        torch.cuda.current_stream(dev).synchronize()
+        n = self.n
+        return dict(perm=_wrap_copy(perm.value, (n,), "<i4", torch.int32, dev),
+                    sorted=_wrap_copy(srt.value, (n, 4), "<f4", torch.float32, dev),
+                    keys=_wrap_copy(keys.value, (n,), "<u4", torch.int32, dev),
+                    cell_start=_wrap_copy(cs.value, (info["ncell"] + 1,), "<i4", torch.int32, dev),
+                    **info)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.rbf_cells_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def matvec(ctx: Context, cells: Cells, kernel: Kernel, w: torch.Tensor, out: torch.Tensor | None = None):
+    """f = A w (Eq.4 with Eq.6 entries); fp32 tier for float32 w, fp64 tier for float64 w."""
+    prec = {torch.float32: RBF_F32, torch.float64: RBF_F64}.get(w.dtype)
+    if prec is None:
+        raise TypeError("w must be float32 or float64")
+    _need(w, w.dtype, cells.n, "w")
+    f = torch.empty_like(w) if out is None else out
+    _need(f, w.dtype, cells.n, "out")
+    _check(_lib.rbf_matvec(ctx._h, cells._h, C.byref(kernel._c()), prec, _ptr(w), _ptr(f)))
+    return f
+
+
+def matvec_pairs(ctx: Context, cells: Cells, kernel: Kernel):
+    """(useful, visited) pair counts of the fp32 matvec traversal."""
+    u, v = C.c_int64(), C.c_int64()
+    _check(_lib.rbf_matvec_pairs(ctx._h, cells._h, C.byref(kernel._c()), C.byref(u), C.byref(v)))
+    return u.value, v.value
+
+
+def _grid_c(lo, hi, n):
+    n = (n, n, n) if isinstance(n, int) else tuple(n)
+    return _Grid((C.c_double * 3)(*lo), (C.c_double * 3)(*hi), (C.c_int * 3)(*n)), n
+
+
+def eval_grid(ctx: Context, cells: Cells, kernel: Kernel, w: torch.Tensor, lo, hi, n,
+              out: torch.Tensor | None = None):
+    """F(xi) on the inclusive grid lo..hi with n nodes per axis (Eq.5); returns (nz, ny, nx) fp32."""
+    _need(w, torch.float64, cells.n, "w")
+    g, n3 = _grid_c(lo, hi, n)
+    field = torch.empty((n3[2], n3[1], n3[0]), dtype=torch.float32, device=w.device) if out is None else out
+    _need(field, torch.float32, n3[0] * n3[1] * n3[2], "field")
+    _check(_lib.rbf_eval_grid(ctx._h, cells._h, C.byref(kernel._c()), _ptr(w), C.byref(g), _ptr(field)))
+    return field
+
+
+class Precond:
+    """rbf_precond_create: RAS (§3.1) / block-Jacobi preconditioner."""
+
+    def __init__(self, ctx: Context, cells: Cells, kernel: Kernel, kind: int = 2, core_target: int = 512,
+                 overlap_sigmas: float = 1.0, max_ext: int = 0):
+        self.ctx, self.cells = ctx, cells
+        h = C.c_void_p()
+        cfg = _PrecondCfg(kind, core_target, overlap_sigmas, max_ext)
+        _check(_lib.rbf_precond_create(ctx._h, cells._h, C.byref(kernel._c()), C.byref(cfg), C.byref(h)))
+        self._h = h
+
+    def apply(self, r: torch.Tensor, out: torch.Tensor | None = None):
+        _need(r, torch.float32, self.cells.n, "r")
+        z = torch.empty_like(r) if out is None else out
+        _check(_lib.rbf_precond_apply(self.ctx._h, self._h, _ptr(r), _ptr(z)))
+        return z
+
+    def blocks(self):
+        """(core lists, ext lists) in SORTED positions, plus device bytes."""
+        import numpy as np
+        nb, nbytes = C.c_int64(), C.c_int64()
+        _check(_lib.rbf_precond_blocks(self._h, C.byref(nb), C.byref(nbytes), None, None, None, None))
+        cp = np.zeros(nb.value + 1, dtype=np.int64)
+        ep = np.zeros(nb.value + 1, dtype=np.int64)
+        _check(_lib.rbf_precond_blocks(self._h, C.byref(nb), C.byref(nbytes), cp.ctypes.data_as(C.c_void_p),
+                                       ep.ctypes.data_as(C.c_void_p), None, None))
+        ci = np.zeros(int(cp[-1]), dtype=np.int32)
+        ei = np.zeros(int(ep[-1]), dtype=np.int32)
+        _check(_lib.rbf_precond_blocks(self._h, C.byref(nb), C.byref(nbytes), cp.ctypes.data_as(C.c_void_p),
+                                       ep.ctypes.data_as(C.c_void_p), ci.ctypes.data_as(C.c_void_p),
+                                       ei.ctypes.data_as(C.c_void_p)))
+        cores = [ci[cp[i]:cp[i + 1]] for i in range(nb.value)]
+        exts = [ei[ep[i]:ep[i + 1]] for i in range(nb.value)]
+        return cores, exts, nbytes.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.rbf_precond_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def gmres_solve(ctx: Context, cells: Cells, kernel: Kernel, b: torch.Tensor, precond: Precond | None = None,
+                kind: int = 2, core_target: int = 512, overlap_sigmas: float = 1.0, restart: int = 30,
+                rtol: float = 1e-6, phase1_rtol: float = 1e-4, max_iters: int = 500, polish_fp64: int = 1,
+                out: torch.Tensor | None = None):
+    """Solve A w = b (Eq.4) with RAS-preconditioned FGMRES; returns (w fp64, report dict)."""
+    _need(b, torch.float32, cells.n, "b")
+    w = torch.empty(cells.n, dtype=torch.float64, device=b.device) if out is None else out
+    _need(w, torch.float64, cells.n, "w")
+    pc = _PrecondCfg(kind, core_target, overlap_sigmas, 0)
+    gc = _GmresCfg(restart, rtol, phase1_rtol, max_iters, polish_fp64)
+    rep = SolveReport()
+    _check(_lib.rbf_gmres_solve(ctx._h, cells._h, C.byref(kernel._c()), None if precond is None else precond._h,
+                                C.byref(pc), C.byref(gc), _ptr(b), _ptr(w), C.byref(rep)))
+    return w, rep.as_dict()
+
+
+def reconstruct_host(ctx: Context, xyz, b, kernel: Kernel, lo, hi, n, *, cell_edge: float = 0.0,
+                     kind: int = 2, core_target: int = 512, overlap_sigmas: float = 1.0, restart: int = 30,
+                     rtol: float = 1e-6, phase1_rtol: float = 1e-4, max_iters: int = 500,
+                     w_out=None, field_out=None):
+    """Alg.1 steps 2-3 from HOST buffers (numpy or CPU tensors; pinned is fastest)."""
+    import numpy as np
+    xyz = torch.as_tensor(xyz, dtype=torch.float32).contiguous()
+    b = torch.as_tensor(b, dtype=torch.float32).contiguous()
+    nn = xyz.shape[0]
+    g, n3 = _grid_c(lo, hi, n)
+    w = torch.empty(nn, dtype=torch.float64) if w_out is None else w_out
+    field = torch.empty((n3[2], n3[1], n3[0]), dtype=torch.float32) if field_out is None else field_out
+    rep = SolveReport()
+    _check(_lib.rbf_reconstruct_host(ctx._h, _ptr(xyz), _ptr(b), nn, C.byref(kernel._c()),
+                                     C.byref(_CellCfg(cell_edge, 64, 2)),
+                                     C.byref(_PrecondCfg(kind, core_target, overlap_sigmas, 0)),
+                                     C.byref(_GmresCfg(restart, rtol, phase1_rtol, max_iters, 1)),
+                                     C.byref(g), _ptr(w), _ptr(field), C.byref(rep)))
+    del np
+    return w, field, rep.as_dict()

@@ -1,0 +1,80 @@
+"""Host-side checks of the C-ABI boundary (no GPU needed).
+
+* librbf.so builds for sm_100a and exports every function include/rbf.h declares;
+* the product package never imports the oracle and has no CPU fallback path.
+"""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "rbf.h")
+PKG = os.path.join(ROOT, "paper_1305_5179_b200")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\*?(rbf_\w+)\s*\(", src, flags=re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib_path():
+    from paper_1305_5179_b200.build import build
+    return build()
+
+
+def test_header_declares_the_section_8b_calls():
+    names = declared_functions()
+    for must in ["rbf_create", "rbf_destroy", "rbf_build_cells", "rbf_cells_view", "rbf_matvec",
+                 "rbf_gmres_solve", "rbf_eval_grid", "rbf_precond_create", "rbf_precond_apply",
+                 "rbf_extend_points", "rbf_reconstruct_host", "rbf_status_str"]:
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(lib_path):
+    out = subprocess.run(["nm", "-D", "--defined-only", lib_path], capture_output=True, text=True,
+                         check=True).stdout
+    exported = set(re.findall(r"\sT\s+(rbf_\w+)$", out, flags=re.M))
+    missing = [f for f in declared_functions() if f not in exported]
+    assert not missing, missing
+
+
+def test_library_is_sm100a(lib_path):
+    out = subprocess.run(["cuobjdump", "--list-elf", lib_path], capture_output=True, text=True,
+                         check=True).stdout
+    assert "sm_100a" in out
+
+
+def test_library_loads_and_binds_without_gpu(lib_path):
+    import ctypes
+    from paper_1305_5179_b200 import rbf
+    lib = rbf.load_library(lib_path)
+    assert lib.rbf_abi_version() == 1
+    assert lib.rbf_status_str(1) == b"RBF_EINVAL"
+    for name in rbf.EXPORTS:
+        assert hasattr(lib, name)
+    # the binding covers every declared function
+    assert set(declared_functions()) <= set(rbf.EXPORTS)
+    # without a GPU, creating a context fails loudly (no CPU fallback)
+    h = ctypes.c_void_p()
+    st = lib.rbf_create(ctypes.byref(h), 0, None, None, 0, 1)
+    assert st != 0
+
+
+def test_product_path_never_touches_the_oracle():
+    for dirpath, _, files in os.walk(PKG):
+        for f in files:
+            if f.endswith((".py", ".cu", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(from|import)\s+oracle", src, flags=re.M), f
+                assert not re.search(r"import_module\(|__import__\(|sys\.path", src), f
+
+
+def test_oracle_never_imports_the_product_path():
+    for f in os.listdir(os.path.join(ROOT, "oracle")):
+        if f.endswith(".py"):
+            src = open(os.path.join(ROOT, "oracle", f)).read()
+            assert not re.search(r"^\s*(from|import)\s+paper_1305_5179_b200", src, flags=re.M), f

@@ -1,0 +1,257 @@
+"""GPU parity of the hot path (a0-a3, a8 of SURVEY.md §8(a)) against the CPU oracle.
+
+Every comparison feeds the SAME seeded synthetic inputs (synth/) to both sides:
+the CUDA path through the C-ABI (paper_1305_5179_b200 -> librbf.so) and the
+oracle (oracle/).  Integer work (cells, keys, permutation) is compared bit for
+bit; floating point against tolerances derived in DESIGN.md "Tolerances":
+
+  fp32 tier matvec   rel-L2 <= 1e-4 (BASELINE north_star) and per row
+                     |f_gpu - f_ref| <= 5e-5 * g_i,  g_i = a sum_j |A_ij w_j|
+  fp64 tier matvec   per row <= 1e-12 * g_i
+  grid               |F_gpu - F_ref|_inf <= 1e-3 max|b| (reading R3) and per node
+                     <= 5e-5 * g(xi); exact zeros where no centre is in range
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import cells as OC
+from oracle import extend as OE
+from oracle import grid as OG
+from oracle import kernel as OK
+from oracle import solve as OS
+from synth import make_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def R():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device (no CPU fallback)"
+    import paper_1305_5179_b200 as R
+    R.load_library()
+    return R
+
+
+@pytest.fixture(scope="module")
+def ctx(R):
+    return R.Context(0)
+
+
+def dev(a, dtype):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype, device="cuda")
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def gpu_extend(R, ctx, d):
+    c, b = R.extend_points(ctx, dev(d["x"], torch.float64), dev(d["normals"], torch.float64), d["delta"])
+    return c, b
+
+
+def abs_rowsum(X, w, sigma, rows=None, targets=None):
+    return OK.matvec(X, np.abs(w), sigma, rows=rows, targets=targets)
+
+
+CASES = {
+    "c1": dict(name="c1"),
+    "torus9k": dict(name="c2", n=3000, seed=3),
+    "c2": dict(name="c2"),
+}
+
+
+@pytest.fixture(scope="module", params=list(CASES))
+def case(request, R, ctx):
+    spec = CASES[request.param]
+    d = make_inputs(spec["name"], seed=spec.get("seed", 0), n=spec.get("n"))
+    X = OE.extend(d["x"], d["normals"], d["delta"])
+    cg, bg = gpu_extend(R, ctx, d)
+    return dict(key=request.param, d=d, X=X, cg=cg, bg=bg, sigma=d["sigma"])
+
+
+# ------------------------------------------------------------------ a0 -------
+def test_extend_bit_exact(case):
+    d = case["d"]
+    assert np.array_equal(host(case["cg"]).view(np.uint32), case["X"].view(np.uint32))
+    b_ref = OE.labels(len(d["x"]), d["delta"]).astype(np.float32)
+    assert np.array_equal(host(case["bg"]), b_ref)
+
+
+# ------------------------------------------------------------------ a1 -------
+def _compare_cells(R, ctx, X, sigma, h):
+    kern = R.Kernel(sigma)
+    cells = R.Cells(ctx, dev(X, torch.float32), kern, cell_edge=h)
+    v = cells.view()
+    ref = OC.build(X, 6 * sigma, cell_edge=h)
+    assert tuple(v["dim"]) == tuple(int(x) for x in ref["dim"])
+    assert np.array_equal(np.array(v["lo"], dtype=np.float32), ref["lo"])
+    assert np.float32(v["inv_h"]) == ref["inv_h"]
+    assert np.array_equal(host(v["perm"]), ref["perm"])
+    assert np.array_equal(host(v["keys"]).view(np.uint32).astype(np.int64), ref["keys"])
+    assert np.array_equal(host(v["sorted"])[:, :3].view(np.uint32), ref["sorted"].view(np.uint32))
+    cs = host(v["cell_start"])
+    assert np.array_equal(cs[:-1], ref["cell_start"]) and np.array_equal(cs[1:], ref["cell_end"])
+    return cells, v
+
+
+def test_cells_bit_exact(R, ctx, case):
+    sigma = case["sigma"]
+    _compare_cells(R, ctx, case["X"], sigma, 6 * sigma / 3.999)
+    _compare_cells(R, ctx, case["X"], sigma, 6 * sigma / 4)      # exactly cutoff/4 (oracle default)
+
+
+def test_cells_edge_cases(R, ctx):
+    rng = np.random.default_rng(7)
+    h = 0.125                                   # exact binary fraction: points on faces
+    lattice = (np.stack(np.meshgrid(*[np.arange(9)] * 3, indexing="ij"), -1).reshape(-1, 3) * h
+               ).astype(np.float32)
+    dup = np.repeat(lattice[:5], 3, axis=0)     # duplicates
+    mx = np.full((2, 3), lattice.max(), np.float32)   # points at the bbox max
+    X = np.concatenate([lattice, dup, mx, rng.uniform(0, 1, (4097, 3)).astype(np.float32)])
+    rng.shuffle(X)
+    _compare_cells(R, ctx, X, 0.5 / 6, h)
+    _compare_cells(R, ctx, X[:1], 0.5 / 6, h)   # n = 1
+    _compare_cells(R, ctx, X[:4097], 0.5 / 6, h)  # ragged radix tile
+
+
+def test_cells_reject_bad_input(R, ctx):
+    X = np.zeros((10, 3), np.float32)
+    X[3, 1] = np.nan
+    with pytest.raises(R.RbfError):
+        R.Cells(ctx, dev(X, torch.float32), R.Kernel(0.1))
+    with pytest.raises(R.RbfError):
+        R.Cells(ctx, dev(np.zeros((4, 3)), torch.float32), R.Kernel(-1.0))
+
+
+# ------------------------------------------------------------------ a3 -------
+def _rows(case, n):
+    if case["key"] == "c2":
+        return np.sort(np.random.default_rng(11).choice(n, 3000, replace=False))
+    return None
+
+
+def test_matvec_f32_parity(R, ctx, case):
+    X, sigma = case["X"], case["sigma"]
+    n = len(X)
+    kern = R.Kernel(sigma)
+    cells = R.Cells(ctx, case["cg"], kern)
+    w = np.random.default_rng(5).normal(size=n)
+    f = host(R.matvec(ctx, cells, kern, dev(w, torch.float32)))
+    rows = _rows(case, n)
+    w32 = w.astype(np.float32).astype(np.float64)          # the fp32 tier's input
+    ref = OK.matvec(X, w32, sigma, rows=rows)
+    g = abs_rowsum(X, w32, sigma, rows=rows)
+    fg = f if rows is None else f[rows]
+    rel = np.linalg.norm(fg - ref) / np.linalg.norm(ref)
+    assert rel <= 1e-4, rel
+    assert (np.abs(fg - ref) <= 5e-5 * g + 1e-30).all(), np.max(np.abs(fg - ref) / g)
+
+
+def test_matvec_f64_parity(R, ctx, case):
+    X, sigma = case["X"], case["sigma"]
+    n = len(X)
+    kern = R.Kernel(sigma)
+    cells = R.Cells(ctx, case["cg"], kern)
+    w = np.random.default_rng(6).normal(size=n)
+    f = host(R.matvec(ctx, cells, kern, dev(w, torch.float64)))
+    rows = _rows(case, n)
+    ref = OK.matvec(X, w, sigma, rows=rows)
+    g = abs_rowsum(X, w, sigma, rows=rows)
+    fg = f if rows is None else f[rows]
+    assert (np.abs(fg - ref) <= 1e-12 * g + 1e-300).all(), np.max(np.abs(fg - ref) / g)
+
+
+def test_matvec_pairs(R, ctx, case):
+    if case["key"] == "c2":
+        pytest.skip("full pair count is O(n^2) on the oracle; covered by c1/torus9k")
+    X, sigma = case["X"], case["sigma"]
+    kern = R.Kernel(sigma)
+    cells = R.Cells(ctx, case["cg"], kern)
+    useful, visited = R.matvec_pairs(ctx, cells, kern)
+    ref = OK.pair_count(X, sigma)
+    assert abs(useful - ref) <= 1e-6 * ref + 2     # fp32 vs fp64 predicate at r = cutoff
+    assert visited >= useful
+    assert useful / visited > 0.3
+
+
+def test_matvec_degenerate(R, ctx):
+    sigma = 0.1
+    kern = R.Kernel(sigma)
+    a = OK.amplitude(sigma)
+    # one centre: f = a w
+    cells = R.Cells(ctx, dev(np.array([[0.3, -0.2, 0.7]]), torch.float32), kern)
+    f = host(R.matvec(ctx, cells, kern, dev([2.5], torch.float64)))
+    assert f[0] == pytest.approx(a * 2.5, rel=1e-15)
+    # two centres farther apart than the cutoff: no coupling
+    X = np.array([[0, 0, 0], [0.61, 0, 0]], np.float32)
+    cells = R.Cells(ctx, dev(X, torch.float32), kern)
+    f = host(R.matvec(ctx, cells, kern, dev([1.0, -3.0], torch.float32)))
+    np.testing.assert_allclose(f, [a, -3 * a], rtol=1e-6)
+    # linearity and the zero vector
+    rng = np.random.default_rng(1)
+    X = rng.uniform(-1, 1, (3000, 3)).astype(np.float32)
+    cells = R.Cells(ctx, dev(X, torch.float32), kern)
+    u, v = rng.normal(size=3000), rng.normal(size=3000)
+    fu = host(R.matvec(ctx, cells, kern, dev(u, torch.float64)))
+    fv = host(R.matvec(ctx, cells, kern, dev(v, torch.float64)))
+    fuv = host(R.matvec(ctx, cells, kern, dev(2 * u - v, torch.float64)))
+    np.testing.assert_allclose(fuv, 2 * fu - fv, atol=1e-12 * np.abs(fuv).max())
+    assert not host(R.matvec(ctx, cells, kern, dev(np.zeros(3000), torch.float32))).any()
+
+
+# ------------------------------------------------------------------ a8 -------
+def test_grid_parity_c1(R, ctx):
+    d = make_inputs("c1")
+    X = OE.extend(d["x"], d["normals"], d["delta"])
+    b = OE.labels(len(d["x"]), d["delta"])
+    sigma = d["sigma"]
+    w = OS.lu_solve(X, b, sigma)                        # oracle weights, shared input
+    kern = R.Kernel(sigma)
+    cells = R.Cells(ctx, dev(X, torch.float32), kern)
+    lo, hi, n = d["grid_lo"], d["grid_hi"], d["grid_n"]
+    F = host(R.eval_grid(ctx, cells, kern, dev(w, torch.float64), lo, hi, n)).ravel()
+    ref = OG.evaluate(X, w, sigma, lo, hi, n)
+    g = OG.evaluate(X, np.abs(w), sigma, lo, hi, n)
+    assert np.abs(F - ref).max() <= 1e-3 * np.abs(b).max()
+    assert (np.abs(F - ref) <= 5e-5 * g + 1e-30).all(), np.max(np.abs(F - ref) / np.maximum(g, 1e-300))
+    # exact zeros where no centre lies within the cutoff (boundary band excluded)
+    dmin = OG._min_dist(OG.nodes(lo, hi, n), X.astype(np.float64))
+    far, near = dmin > 6 * sigma * (1 + 1e-5), dmin < 6 * sigma * (1 - 1e-5)
+    assert (F[far] == 0).all() and (F[near] != 0).all()
+    assert far.sum() > 1000
+
+
+def test_grid_parity_sampled_c2(R, ctx):
+    d = make_inputs("c2")
+    X = OE.extend(d["x"], d["normals"], d["delta"])
+    sigma = d["sigma"]
+    w = np.random.default_rng(9).normal(size=len(X)) * 1e-3
+    kern = R.Kernel(sigma)
+    cells = R.Cells(ctx, dev(X, torch.float32), kern)
+    lo, hi, n = d["grid_lo"], d["grid_hi"], d["grid_n"]
+    F = host(R.eval_grid(ctx, cells, kern, dev(w, torch.float64), lo, hi, n)).ravel()
+    M = int(np.prod(n))
+    flat = np.sort(np.random.default_rng(4).choice(M, 4000, replace=False))
+    ref = OG.evaluate(X, w, sigma, lo, hi, n, flat=flat)
+    g = OG.evaluate(X, np.abs(w), sigma, lo, hi, n, flat=flat)
+    assert (np.abs(F[flat] - ref) <= 5e-5 * g + 1e-30).all()
+    assert ((F[flat] == 0) == (g == 0)).mean() > 0.999
+
+
+def test_grid_ragged_and_anisotropic(R, ctx):
+    rng = np.random.default_rng(2)
+    X = rng.uniform(-0.5, 0.5, (2000, 3)).astype(np.float32)
+    sigma = 0.05
+    w = rng.normal(size=2000)
+    kern = R.Kernel(sigma)
+    cells = R.Cells(ctx, dev(X, torch.float32), kern)
+    lo, hi, n = (-0.6, -0.55, -0.7), (0.6, 0.5, 0.65), (13, 7, 10)   # not multiples of the 4^3 block
+    F = host(R.eval_grid(ctx, cells, kern, dev(w, torch.float64), lo, hi, n)).ravel()
+    ref = OG.evaluate(X, w, sigma, lo, hi, n)
+    g = OG.evaluate(X, np.abs(w), sigma, lo, hi, n)
+    assert (np.abs(F - ref) <= 5e-5 * g + 1e-30).all()
+    with pytest.raises(R.RbfError):
+        R.eval_grid(ctx, cells, kern, dev(w, torch.float64), lo, hi, (1, 5, 5))
