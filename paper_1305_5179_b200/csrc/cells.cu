@@ -86,7 +86,8 @@ constexpr int kRsIpt = 16;
 constexpr int kRsWarps = kRsThreads / 32;
 constexpr int kRsTile = kRsThreads * kRsIpt;  // 4096
 
-__global__ void radix_hist(const uint32_t* __restrict__ keys, int64_t n, int shift,
+template <class K>
+__global__ void radix_hist(const K* __restrict__ keys, int64_t n, int shift,
                            uint32_t* __restrict__ counts, int ntiles) {
   __shared__ uint32_t h[256];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
@@ -95,14 +96,15 @@ __global__ void radix_hist(const uint32_t* __restrict__ keys, int64_t n, int shi
 #pragma unroll 4
   for (int r = 0; r < kRsIpt; ++r) {
     int64_t i = base + r * kRsThreads + threadIdx.x;
-    if (i < n) atomicAdd(&h[(keys[i] >> shift) & 255u], 1u);
+    if (i < n) atomicAdd(&h[(unsigned)(keys[i] >> shift) & 255u], 1u);
   }
   __syncthreads();
   for (int d = threadIdx.x; d < 256; d += blockDim.x) counts[(int64_t)d * ntiles + blockIdx.x] = h[d];
 }
 
-__global__ void radix_scatter(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
-                              uint32_t* __restrict__ kout, int32_t* __restrict__ vout, int64_t n,
+template <class K>
+__global__ void radix_scatter(const K* __restrict__ kin, const int32_t* __restrict__ vin,
+                              K* __restrict__ kout, int32_t* __restrict__ vout, int64_t n,
                               int shift, const uint32_t* __restrict__ offsets, int ntiles) {
   __shared__ uint32_t wh[kRsWarps][257];
   const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -110,20 +112,20 @@ __global__ void radix_scatter(const uint32_t* __restrict__ kin, const int32_t* _
   __syncthreads();
   const int64_t wbase = (int64_t)blockIdx.x * kRsTile + (int64_t)w * (32 * kRsIpt);
   const unsigned lt = (1u << lane) - 1u;
-  uint32_t k[kRsIpt];
+  K k[kRsIpt];
   int32_t v[kRsIpt];
 #pragma unroll
   for (int r = 0; r < kRsIpt; ++r) {
     int64_t i = wbase + r * 32 + lane;
     bool valid = i < n;
-    k[r] = valid ? kin[i] : 0u;
+    k[r] = valid ? kin[i] : (K)0;
     v[r] = valid ? vin[i] : 0;
   }
 #pragma unroll
   for (int r = 0; r < kRsIpt; ++r) {
     int64_t i = wbase + r * 32 + lane;
     bool valid = i < n;
-    unsigned d = valid ? ((k[r] >> shift) & 255u) : 256u;
+    unsigned d = valid ? ((unsigned)(k[r] >> shift) & 255u) : 256u;
     unsigned peers = __match_any_sync(0xffffffffu, d);
     if (valid && (peers & lt) == 0u) wh[w][d] += __popc(peers);
     __syncwarp();
@@ -142,7 +144,7 @@ __global__ void radix_scatter(const uint32_t* __restrict__ kin, const int32_t* _
   for (int r = 0; r < kRsIpt; ++r) {
     int64_t i = wbase + r * 32 + lane;
     bool valid = i < n;
-    unsigned d = valid ? ((k[r] >> shift) & 255u) : 256u;
+    unsigned d = valid ? ((unsigned)(k[r] >> shift) & 255u) : 256u;
     unsigned peers = __match_any_sync(0xffffffffu, d);
     if (valid) {
       uint32_t rank = wh[w][d] + __popc(peers & lt);
@@ -346,6 +348,41 @@ rbf_status exclusive_scan_u32(rbf_ctx* ctx, const uint32_t* in, uint32_t* out, i
   return RBF_OK;
 }
 
+template <class K>
+rbf_status radix_sort_pairs(rbf_ctx* ctx, K* keys, int32_t* vals, K* keys_out, int32_t* vals_out, int64_t n,
+                            int bits) {
+  cudaStream_t s = ctx->stream;
+  if (n <= 0) return RBF_OK;
+  const int passes = std::max(1, (bits + 7) / 8);
+  const int64_t nt = (n + kRsTile - 1) / kRsTile;
+  DevBuf counts, offs;
+  RBF_TRY(counts.alloc(sizeof(uint32_t) * 256 * nt, s));
+  RBF_TRY(offs.alloc(sizeof(uint32_t) * 256 * nt, s));
+  K* kin = keys;
+  int32_t* vin = vals;
+  K* kout = keys_out;
+  int32_t* vout = vals_out;
+  for (int p = 0; p < passes; ++p) {
+    const int shift = 8 * p;
+    radix_hist<K><<<(unsigned)nt, kRsThreads, 0, s>>>(kin, n, shift, counts.as<uint32_t>(), (int)nt);
+    RBF_CHECK_LAUNCH();
+    RBF_TRY(exclusive_scan_u32(ctx, counts.as<uint32_t>(), offs.as<uint32_t>(), 256 * nt, nullptr));
+    radix_scatter<K><<<(unsigned)nt, kRsThreads, 0, s>>>(kin, vin, kout, vout, n, shift, offs.as<uint32_t>(),
+                                                          (int)nt);
+    RBF_CHECK_LAUNCH();
+    std::swap(kin, kout);
+    std::swap(vin, vout);
+  }
+  if (kin != keys_out) {
+    RBF_CUDA_TRY(cudaMemcpyAsync(keys_out, kin, sizeof(K) * n, cudaMemcpyDeviceToDevice, s));
+    RBF_CUDA_TRY(cudaMemcpyAsync(vals_out, vin, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+  }
+  return RBF_OK;
+}
+template rbf_status radix_sort_pairs<uint32_t>(rbf_ctx*, uint32_t*, int32_t*, uint32_t*, int32_t*, int64_t, int);
+template rbf_status radix_sort_pairs<unsigned long long>(rbf_ctx*, unsigned long long*, int32_t*,
+                                                         unsigned long long*, int32_t*, int64_t, int);
+
 rbf_status build_cells(rbf_ctx* ctx, const float* xyz, int64_t n, const rbf_kernel* k,
                        const rbf_cell_cfg* cfg, rbf_cells* c) {
   cudaStream_t s = ctx->stream;
@@ -417,31 +454,8 @@ rbf_status build_cells(rbf_ctx* ctx, const float* xyz, int64_t n, const rbf_kern
   RBF_CHECK_LAUNCH();
   int bits = 1;
   while (bits < 32 && ((uint64_t)1 << bits) < (uint64_t)ncell) ++bits;
-  int passes = (bits + 7) / 8;
-  const int64_t ntile_rs = (n + kRsTile - 1) / kRsTile;
-  DevBuf counts, offs;
-  RBF_TRY(counts.alloc(sizeof(uint32_t) * 256 * ntile_rs, s));
-  RBF_TRY(offs.alloc(sizeof(uint32_t) * 256 * ntile_rs, s));
-  uint32_t* kin = k2.as<uint32_t>();
-  int32_t* vin = v2.as<int32_t>();
-  uint32_t* kout = c->keys.as<uint32_t>();
-  int32_t* vout = c->perm.as<int32_t>();
-  for (int p = 0; p < passes; ++p) {
-    int shift = 8 * p;
-    radix_hist<<<(unsigned)ntile_rs, kRsThreads, 0, s>>>(kin, n, shift, counts.as<uint32_t>(), (int)ntile_rs);
-    RBF_CHECK_LAUNCH();
-    RBF_TRY(exclusive_scan_u32(ctx, counts.as<uint32_t>(), offs.as<uint32_t>(), 256 * ntile_rs, nullptr));
-    radix_scatter<<<(unsigned)ntile_rs, kRsThreads, 0, s>>>(kin, vin, kout, vout, n, shift,
-                                                            offs.as<uint32_t>(), (int)ntile_rs);
-    RBF_CHECK_LAUNCH();
-    std::swap(kin, kout);
-    std::swap(vin, vout);
-  }
-  // the latest output is in kin/vin; land it in c->keys / c->perm
-  if (kin != c->keys.as<uint32_t>()) {
-    RBF_CUDA_TRY(cudaMemcpyAsync(c->keys.p, kin, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
-    RBF_CUDA_TRY(cudaMemcpyAsync(c->perm.p, vin, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
-  }
+  RBF_TRY(radix_sort_pairs(ctx, k2.as<uint32_t>(), v2.as<int32_t>(), c->keys.as<uint32_t>(),
+                           c->perm.as<int32_t>(), n, bits));
 
   // cell offsets
   RBF_TRY(c->cell_start.alloc(sizeof(int32_t) * (ncell + 1), s));

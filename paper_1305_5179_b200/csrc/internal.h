@@ -122,6 +122,11 @@ struct CellGrid {
 // cells.cu
 rbf_status build_cells(rbf_ctx* ctx, const float* xyz, int64_t n, const rbf_kernel* k,
                        const rbf_cell_cfg* cfg, rbf_cells* c);
+// Stable LSD radix sort of (key, value) pairs on the low `bits` bits of the keys.
+// keys/vals are clobbered; the result lands in keys_out/vals_out.
+template <class K>
+rbf_status radix_sort_pairs(rbf_ctx* ctx, K* keys, int32_t* vals, K* keys_out, int32_t* vals_out, int64_t n,
+                            int bits);
 rbf_status exclusive_scan_u32(rbf_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t n,
                               uint32_t* total_dev /* may be null */);
 

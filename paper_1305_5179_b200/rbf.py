@@ -149,7 +149,7 @@ class _DevArray:
 
     def __init__(self, ptr: int, shape, typestr: str):
         self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
-                                         "data": (int(ptr), True), "version": 2, "strides": None}
+                                         "data": (int(ptr), False), "version": 2, "strides": None}
 
 
 def _wrap_copy(ptr, shape, typestr, dtype, device):

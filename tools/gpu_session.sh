@@ -1,0 +1,3 @@
+set -x
+python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -1
+timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -40 > gpurun_out/pytest_gpu.log; tail -40 gpurun_out/pytest_gpu.log
