@@ -1,0 +1,334 @@
+"""Benchmark: one step = the whole hot path of the method on config c4 (BASELINE
+configs[3]: blobby surface, N = 1M surface points -> 3M centres, sigma 0.01,
+cutoff 6 sigma, GMRES(50) + RAS(512, 1 sigma), 256^3 grid).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+Step (all on the GPU, inputs resident in HBM when the timed region starts):
+  a0 extend X -> X_ext, labels b      rbf_extend_points
+  a1/a2 cell build + tile plan        rbf_build_cells
+  a4 RAS setup (blocks, fp64 LU, W)   inside rbf_gmres_solve
+  a5-a7 FGMRES fp32 tier -> fp64 tier  rbf_gmres_solve (true residual <= 1e-6)
+  a8 grid evaluation                  rbf_eval_grid
+value = useful kernel-pair evaluations of the step (matvecs x useful pairs per
+matvec + grid pairs) / step seconds, summed over ranks (weak scaling: every rank
+solves its own seeded instance -- see DESIGN.md "Multi-GPU").
+e2e = the same metric through rbf_reconstruct_host with HOST buffers (H2D of
+centres + b and D2H of weights + field inside the timed region).
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "RBF kernel-pair evals/s and fit+eval seconds at N=1M, 1/2/4/8 B200"
+MUFU_PER_CLK_PER_SM = 16          # MUFU.EX2 lanes per SM per clock (B200_PROFILING / SURVEY §6.4)
+SMS = 148
+SM_MAX_MHZ = 1965.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-rows", type=int, default=0)
+    ap.add_argument("--fit-iters", type=int, default=50)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (the recipe's clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for k, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(k)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def make_problem(cfg_name: str, seed: int):
+    from synth import make_inputs
+    t = time.time()
+    d = make_inputs(cfg_name, seed=seed)
+    d["gen_s"] = time.time() - t
+    return d
+
+
+# ------------------------------------------------------------------ ours ----
+def run_ours(args, rank, world, local):
+    import torch
+    import paper_1305_5179_b200 as R
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    d = make_problem(args.config, args.seed + rank)
+    cfg = d["cfg"]
+    ctx = R.Context(local)
+    kern = R.Kernel(d["sigma"], d["cutoff_sigmas"])
+    x = torch.as_tensor(d["x"], device=dev)
+    nrm = torch.as_tensor(d["normals"], device=dev)
+    lo, hi, gn = d["grid_lo"], d["grid_hi"], d["grid_n"]
+    # fit budget: the paper's Table II protocol, a fixed 50 GMRES iterations;
+    # the 1e-6 gate is unattainable at c4's sigma/spacing (DESIGN.md finding F1)
+    solve_kw = dict(restart=cfg.restart, rtol=1e-6, phase1_rtol=1e-4, core_target=cfg.core_target,
+                    overlap_sigmas=cfg.overlap_sigmas, max_iters=args.fit_iters)
+
+    def step():
+        centres, b = R.extend_points(ctx, x, nrm, d["delta"])
+        cells = R.Cells(ctx, centres, kern)
+        w, rep = R.gmres_solve(ctx, cells, kern, b, **solve_kw)
+        field = R.eval_grid(ctx, cells, kern, w, lo, hi, gn)
+        return cells, w, field, rep
+
+    # pair accounting (outside the timed region): useful pairs per matvec and per grid pass
+    centres, b = R.extend_points(ctx, x, nrm, d["delta"])
+    cells = R.Cells(ctx, centres, kern)
+    useful_mv, visited_mv = R.matvec_pairs(ctx, cells, kern)
+    useful_grid = R.eval_grid_pairs(ctx, cells, kern, lo, hi, gn)
+    info = cells.info()
+    del cells
+
+    for _ in range(args.warmup):
+        _, _, _, rep = step()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    ctx.profile(True)
+    ctx.profile_query()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = []
+    e0.record(s)
+    for _ in range(args.steps):
+        _, w, field, rep = step()
+        reps.append(rep)
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop()
+    prof = ctx.profile_query()
+    ctx.profile(False)
+    mv32 = sum(r["matvecs_f32"] for r in reps)
+    mv64 = sum(r["matvecs_f64"] for r in reps)
+    pairs_rank = useful_mv * (mv32 + mv64) + useful_grid * args.steps
+    if world > 1:
+        t = torch.tensor([ms, pairs_rank], dtype=torch.float64, device=dev)
+        tmax = t.clone()
+        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
+        tsum = t.clone()
+        torch.distributed.all_reduce(tsum, op=torch.distributed.ReduceOp.SUM)
+        ms_max, pairs_all = float(tmax[0]), float(tsum[1])
+    else:
+        ms_max, pairs_all = ms, float(pairs_rank)
+    value = pairs_all / (ms_max * 1e-3)
+
+    # e2e through the C-ABI with HOST buffers (rank-local problem)
+    e2e = None
+    if not args.no_e2e:
+        centres, b = R.extend_points(ctx, x, nrm, d["delta"])
+        xyz_h = centres.cpu().pin_memory()
+        b_h = b.cpu().pin_memory()
+        n = xyz_h.shape[0]
+        w_h = torch.empty(n, dtype=torch.float64).pin_memory()
+        f_h = torch.empty((gn[2], gn[1], gn[0]), dtype=torch.float32).pin_memory()
+        rkw = dict(restart=cfg.restart, rtol=1e-6, phase1_rtol=1e-4, core_target=cfg.core_target,
+                   overlap_sigmas=cfg.overlap_sigmas, max_iters=args.fit_iters)
+        R.reconstruct_host(ctx, xyz_h, b_h, kern, lo, hi, gn, w_out=w_h, field_out=f_h, **rkw)   # warm
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        mv_e2e = 0
+        for _ in range(args.steps):
+            _, _, rep_e = R.reconstruct_host(ctx, xyz_h, b_h, kern, lo, hi, gn, w_out=w_h, field_out=f_h, **rkw)
+            mv_e2e += rep_e["matvecs_f32"] + rep_e["matvecs_f64"]
+        torch.cuda.synchronize()
+        te = (time.perf_counter() - t0) * 1e3
+        pe = useful_mv * mv_e2e + useful_grid * args.steps
+        if world > 1:
+            t = torch.tensor([te, pe], dtype=torch.float64, device=dev)
+            tm = t.clone()
+            torch.distributed.all_reduce(tm, op=torch.distributed.ReduceOp.MAX)
+            ts = t.clone()
+            torch.distributed.all_reduce(ts, op=torch.distributed.ReduceOp.SUM)
+            te, pe = float(tm[0]), float(ts[1])
+        e2e = {"value": pe / (te * 1e-3), "unit": "pairs/s", "ms_per_step": te / args.steps,
+               "h2d_bytes_per_step": int(xyz_h.numel() * 4 + b_h.numel() * 4),
+               "d2h_bytes_per_step": int(w_h.numel() * 8 + f_h.numel() * 4)}
+
+    # roofline of the dominant kernel (fp32 summation), live CUDA-event timing
+    t_mv, n_mv = prof["matvec_f32"]
+    avg_mv_ms = t_mv / max(n_mv, 1)
+    achieved = useful_mv / (avg_mv_ms * 1e-3) / 1e12
+    peak_max = SMS * MUFU_PER_CLK_PER_SM * SM_MAX_MHZ * 1e6 / 1e12
+    roofline = {"bound": "alu", "kernel": "sum_f32_kernel (MUFU.EX2)", "achieved": achieved, "peak": peak_max,
+                "unit": "Tpairs/s", "frac": achieved / peak_max,
+                "peak_basis": "148 SMs x 16 MUFU.EX2/clk x 1965 MHz (max clock); 1 ex2 per useful pair",
+                "frac_at_measured_clock": (achieved / (SMS * MUFU_PER_CLK_PER_SM * clk["sm_mhz"] * 1e6 / 1e12)
+                                           if clk.get("sm_mhz") else None),
+                "avg_launch_ms": avg_mv_ms, "launches": n_mv, "useful_pairs_per_launch": useful_mv,
+                "visited_pairs_per_launch": visited_mv, "traffic": None}
+    stage_ms = {k: round(v[0] / args.steps, 3) for k, v in prof.items()}
+
+    cpu = None
+    if rank == 0 and world == 1:
+        cpu = cpu_baseline(d, args)
+    last = reps[-1]
+    out = {
+        "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "fit_eval_s": ms_max / args.steps / 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64",
+        "data": "synthetic (seeded blobby surface, SURVEY §8(c) reading 14)",
+        "config": {"workload": f"{args.config}: {cfg.kind} K={cfg.kw.get('K')} N={cfg.n} surface points "
+                               f"({3 * cfg.n} centres), sigma={cfg.sigma}, cutoff 6 sigma, GMRES({cfg.restart}) "
+                               f"+ RAS({cfg.core_target}, {cfg.overlap_sigmas} sigma), {args.fit_iters} iterations "
+                               f"(Table II protocol) or true residual 1e-6, "
+                               f"grid {gn[0]}^3",
+                   "centres_per_gpu": 3 * cfg.n, "global_centres": 3 * cfg.n * world,
+                   "parallelism": f"replicas x{world} (independent seeded instances)",
+                   "l2": "working set >> 126 MB L2 (W 30+ GB, Krylov basis 2.4 GB); no explicit flush"},
+        "e2e": e2e, "gpu_launches": None, "clocks": clk, "roofline": roofline, "cpu_baseline": cpu,
+        "detail": {"useful_pairs_per_matvec": useful_mv, "visited_pairs_per_matvec": visited_mv,
+                   "useful_pairs_grid": useful_grid, "matvecs_f32_per_step": mv32 / args.steps,
+                   "matvecs_f64_per_step": mv64 / args.steps, "stage_ms_per_step": stage_ms,
+                   "iters_phase1": last["iters_phase1"], "iters_phase2": last["iters_phase2"],
+                   "rel_residual_true": last["rel_residual_true"], "converged": last["converged"],
+                   "ras_blocks": last["nblocks"], "precond_bytes": last["precond_bytes"], "cells": info,
+                   "gen_s": round(d["gen_s"], 1)},
+    }
+    out["gpu_launches"] = estimate_launches(prof, reps, args.steps)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def estimate_launches(prof, reps, steps):
+    """Our kernel launches in the timed region: profiled stages + per-iteration Krylov kernels."""
+    n = sum(v[1] for k, v in prof.items() if k in ("matvec_f32", "matvec_f64", "grid", "precond_apply"))
+    its = sum(r["iters_phase1"] + r["iters_phase2"] for r in reps)
+    restarts = sum(r["restarts"] for r in reps)
+    # per iteration: 3 multi-dot+reduce pairs (6) + 2 axpy + scale + pack = 10; per restart ~6; build ~30
+    return int(n + 10 * its + 6 * restarts + 40 * steps)
+
+
+# ------------------------------------------------------------- cpu oracle ---
+def cpu_baseline(d, args, rows: int | None = None):
+    """The oracle (oracle/kernel.py brute-force fp64 matvec, as it stands) on a bounded
+    row sample of the same workload, on all host cores."""
+    from oracle import extend as OE
+    from oracle import kernel as OK
+    X = OE.extend(d["x"], d["normals"], d["delta"])
+    n = X.shape[0]
+    rows = rows or args.cpu_sample_rows or 200
+    sel = np.sort(np.random.default_rng(1).choice(n, rows, replace=False))
+    w = np.random.default_rng(2).normal(size=n)
+    procs = os.cpu_count() or 1
+    t = time.perf_counter()
+    OK.matvec_parallel(X, w, d["sigma"], rows=sel, procs=procs)
+    dt = time.perf_counter() - t
+    useful = OK.pair_count(X, d["sigma"], rows=sel[: min(rows, 50)]) * rows / min(rows, 50)
+    return {"value": useful / dt, "unit": "pairs/s", "cores": procs, "kind": "oracle",
+            "dense_pairs_per_s": rows * n / dt,
+            "sample": f"brute-force fp64 matvec rows ({rows} of {n} sampled targets x all {n} centres) of the "
+                      f"same config; useful pairs estimated from 50 rows", "seconds": dt}
+
+
+def run_reference(args, rank, world, local):
+    if rank != 0:
+        return
+    d = make_problem(args.config, args.seed)
+    rows = max(50, args.cpu_sample_rows or 200)
+    for _ in range(max(args.warmup, 0) and 1):
+        cpu_baseline(d, args, rows=50)
+    times, vals = [], []
+    for _ in range(args.steps):
+        cb = cpu_baseline(d, args, rows=rows)
+        times.append(cb["seconds"])
+        vals.append(cb["value"])
+    cfg = d["cfg"]
+    v = float(np.median(vals))
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "pairs/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(times)) * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": {"workload": f"{args.config}: N={cfg.n} ({3 * cfg.n} centres) "
+                                                      f"sampled-row brute-force matvec"},
+           "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": os.cpu_count(), "kind": "oracle",
+                            "sample": f"{rows} sampled target rows x all centres per step"},
+           "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world, local)
+    else:
+        run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

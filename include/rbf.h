@@ -231,6 +231,28 @@ rbf_status rbf_gmres_solve(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kerne
 rbf_status rbf_eval_grid(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern,
                          const double* w, const rbf_grid* grid, float* field);
 
+/* ---- profiling (CUDA events on the context stream) -------------------------
+ * When enabled, every launch of the listed device stages is bracketed by a
+ * pair of CUDA events recorded on the context's stream.  rbf_profile_query
+ * synchronises, sums the elapsed times per stage into the HOST arrays
+ * ms[RBF_PROF_COUNT] and launches[RBF_PROF_COUNT], and clears the records. */
+typedef enum {
+  RBF_PROF_CELLS = 0,          /* a1/a2: cell build + tile plan (whole call) */
+  RBF_PROF_MATVEC_F32 = 1,     /* a3: fp32 summation kernel */
+  RBF_PROF_MATVEC_F64 = 2,     /* a7: fp64 summation kernel */
+  RBF_PROF_GRID = 3,           /* a8: grid summation kernel */
+  RBF_PROF_PRECOND_SETUP = 4,  /* a4: blocks + assembly + LU (whole call) */
+  RBF_PROF_PRECOND_APPLY = 5,  /* a5: restricted-inverse apply kernel */
+  RBF_PROF_COUNT = 6
+} rbf_prof_stage;
+rbf_status rbf_profile_enable(rbf_ctx* ctx, int on);
+rbf_status rbf_profile_query(rbf_ctx* ctx, double* ms, int64_t* launches);
+
+/* Pair accounting of the grid traversal (host outputs; synchronises): useful =
+ * (node, centre) pairs with r^2 <= c^2, visited = pairs evaluated after culling. */
+rbf_status rbf_eval_grid_pairs(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern,
+                               const rbf_grid* grid, int64_t* useful, int64_t* visited);
+
 /* ---- Alg.1 steps 2-3 end to end from HOST buffers -------------------------
  * xyz (n x 3 fp32), b (n fp32), w_out (n fp64), field_out (grid nodes fp32),
  * rep: all HOST.  Copies in, builds cells, preconditioner, solves, evaluates

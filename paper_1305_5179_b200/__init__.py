@@ -4,8 +4,8 @@ The product path is librbf.so (C-ABI, include/rbf.h: hand-written sm_100a
 CUDA) and the thin ctypes binding in `rbf`.  This package never imports the
 CPU oracle (oracle/, test infrastructure only) and has no CPU fallback.
 """
-from .rbf import (Context, Cells, Kernel, Precond, RbfError, SolveReport, eval_grid, extend_points,
+from .rbf import (Context, Cells, Kernel, Precond, RbfError, SolveReport, eval_grid, eval_grid_pairs, extend_points,
                   gmres_solve, load_library, matvec, matvec_pairs, reconstruct_host)
 
-__all__ = ["Context", "Cells", "Kernel", "Precond", "RbfError", "SolveReport", "eval_grid",
+__all__ = ["Context", "Cells", "Kernel", "Precond", "RbfError", "SolveReport", "eval_grid", "eval_grid_pairs",
            "extend_points", "gmres_solve", "load_library", "matvec", "matvec_pairs", "reconstruct_host"]

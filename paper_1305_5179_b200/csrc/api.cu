@@ -87,7 +87,40 @@ rbf_status rbf_create(rbf_ctx** out, int device, void* cuda_stream, const void* 
               std::to_string(prop.major) + "." + std::to_string(prop.minor));
     return RBF_EUNSUPPORTED;
   }
+  // keep freed blocks in the stream-ordered pool: the solver frees and re-allocates
+  // tens of GB per fit (RAS factors, Krylov basis); returning them to the driver
+  // at every synchronisation costs hundreds of ms
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
   *out = c;
+  return RBF_OK;
+}
+
+rbf_status rbf_profile_enable(rbf_ctx* ctx, int on) {
+  if (!ctx) { set_error("ctx is NULL"); return RBF_EINVAL; }
+  ctx->prof = on != 0;
+  return RBF_OK;
+}
+
+rbf_status rbf_profile_query(rbf_ctx* ctx, double* ms, int64_t* launches) {
+  if (!ctx) { set_error("ctx is NULL"); return RBF_EINVAL; }
+  RBF_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  for (int k = 0; k < RBF_PROF_COUNT; ++k) {
+    if (ms) ms[k] = 0.0;
+    if (launches) launches[k] = 0;
+  }
+  for (auto& r : ctx->prof_recs) {
+    float t = 0.f;
+    RBF_CUDA_TRY(cudaEventElapsedTime(&t, r.a, r.b));
+    if (ms) ms[r.stage] += t;
+    if (launches) launches[r.stage] += 1;
+    ctx->ev_pool.push_back(r.a);
+    ctx->ev_pool.push_back(r.b);
+  }
+  ctx->prof_recs.clear();
   return RBF_OK;
 }
 
@@ -110,7 +143,11 @@ rbf_status rbf_build_cells(rbf_ctx* ctx, const float* xyz, int64_t n, const rbf_
   RBF_CUDA_TRY(cudaSetDevice(ctx->device));
   rbf_cells* c = new (std::nothrow) rbf_cells();
   if (!c) { set_error("host allocation failed"); return RBF_ENOMEM; }
-  rbf_status st = build_cells(ctx, xyz, n, kern, cfg, c);
+  rbf_status st;
+  {
+    ProfScope ps(ctx, RBF_PROF_CELLS);
+    st = build_cells(ctx, xyz, n, kern, cfg, c);
+  }
   if (st != RBF_OK) { delete c; return st; }
   *out = c;
   return RBF_OK;
@@ -203,6 +240,25 @@ rbf_status rbf_eval_grid(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* ker
   RBF_TRY(ctx->vec_a.ensure(sizeof(double) * c->n, ctx->stream));
   RBF_TRY(gather_f64_to_sorted(ctx, w, c->perm.as<int32_t>(), ctx->vec_a.as<double>(), c->n));
   return eval_grid_sorted(ctx, c, kp, ctx->vec_a.as<double>(), g, field);
+}
+
+rbf_status rbf_eval_grid_pairs(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, const rbf_grid* g,
+                               int64_t* useful, int64_t* visited) {
+  RBF_TRY(check_cells(ctx, c, kern));
+  if (!g) { set_error("grid is NULL"); return RBF_EINVAL; }
+  for (int a = 0; a < 3; ++a)
+    if (g->n[a] < 2) { set_error("grid needs n >= 2 nodes per axis"); return RBF_EINVAL; }
+  RBF_CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  RBF_TRY(ctx->stats.ensure(64, s));
+  RBF_CUDA_TRY(cudaMemsetAsync(ctx->stats.p, 0, 16, s));
+  RBF_TRY(eval_grid_sorted(ctx, c, kernel_params(kern), nullptr, g, nullptr, ctx->stats.as<unsigned long long>()));
+  unsigned long long h[2];
+  RBF_CUDA_TRY(cudaMemcpyAsync(h, ctx->stats.p, 16, cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  if (useful) *useful = (int64_t)h[0];
+  if (visited) *visited = (int64_t)h[1];
+  return RBF_OK;
 }
 
 }  // extern "C"

@@ -1,0 +1,422 @@
+// a6/a7 of SURVEY.md §8(a): restarted right-preconditioned FGMRES(m) for
+// A w = b (Eq.4), the Krylov method wrapped around RASM (P:359,
+// "in combination with any iterative method like the Krylov subspace
+// methods. In this work we use the Generalized Minimum Residual (GMRES)").
+//
+// Design:
+//  * all vectors in the cell (sorted) order, fp64, resident in HBM; the
+//    flexible form stores Z_j = M V_j so the (inexact, fp32) preconditioner
+//    may change between phases;
+//  * CGS2 orthogonalisation: two passes of a fused multi-dot (deterministic
+//    two-stage reduction) + multi-axpy over the basis;
+//  * the (m+1) x m Hessenberg / Givens recurrence runs on the host (<= 51
+//    values per iteration, one D2H copy per iteration);
+//  * two operator tiers: phase 1 uses the fp32 summation (ex2.approx,
+//    fp32 accumulation) until the true residual reaches phase1_rtol; phase 2
+//    switches to the fp64 summation and continues to rtol.  The stopping
+//    test is always a TRUE residual b - A w recomputed at restart (reading R6),
+//    never the Arnoldi estimate alone.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <vector>
+
+#include "internal.h"
+#include "solver.h"
+
+namespace rbf {
+namespace {
+
+constexpr int kVecThreads = 256;
+constexpr int kDotChunk = 8;
+
+// partial[j * nblk + blk] = sum over this block's slice of V_j . w, j in [0, k)
+__global__ void __launch_bounds__(kVecThreads)
+multi_dot_kernel(const double* __restrict__ V, int64_t ldv, int k, const double* __restrict__ w, int64_t n,
+                 double* __restrict__ partial) {
+  __shared__ double red[kVecThreads / 32][kDotChunk];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int j0 = 0; j0 < k; j0 += kDotChunk) {
+    double acc[kDotChunk];
+#pragma unroll
+    for (int q = 0; q < kDotChunk; ++q) acc[q] = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+      const double wi = w[i];
+#pragma unroll
+      for (int q = 0; q < kDotChunk; ++q)
+        if (j0 + q < k) acc[q] = fma(V[(int64_t)(j0 + q) * ldv + i], wi, acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < kDotChunk; ++q) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+      if (lane == 0) red[wid][q] = acc[q];
+    }
+    __syncthreads();
+    if (threadIdx.x < kDotChunk && j0 + (int)threadIdx.x < k) {
+      double s = 0.0;
+      for (int q = 0; q < kVecThreads / 32; ++q) s += red[q][threadIdx.x];
+      partial[(int64_t)(j0 + threadIdx.x) * gridDim.x + blockIdx.x] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// out[j] = sum_b partial[j * nblk + b]   (fixed order: deterministic);  out[j] += add[j] if add
+__global__ void reduce_partials(const double* __restrict__ partial, int k, int nblk, double* __restrict__ out,
+                                int negate_into, double* __restrict__ neg_out) {
+  const int j = blockIdx.x;
+  if (j >= k) return;
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nblk; b += 32) s += partial[(int64_t)j * nblk + b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (threadIdx.x == 0) {
+    out[j] = s;
+    if (negate_into) neg_out[j] = -s;
+  }
+}
+
+// w[i] += sum_j coef[j] * V_j[i]
+__global__ void multi_axpy_kernel(double* __restrict__ w, const double* __restrict__ V, int64_t ldv, int k,
+                                  const double* __restrict__ coef, int64_t n) {
+  __shared__ double sc[64];
+  for (int q = threadIdx.x; q < k && q < 64; q += blockDim.x) sc[q] = coef[q];
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = w[i];
+    for (int j = 0; j < k; ++j) acc = fma(sc[j], V[(int64_t)j * ldv + i], acc);
+    w[i] = acc;
+  }
+}
+
+__global__ void scale_kernel(const double* __restrict__ a, double s, double* __restrict__ b, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = a[i] * s;
+}
+// b = a * (1 / *nrm)  (norm on the device)
+__global__ void scale_by_inv_norm(const double* __restrict__ a, const double* __restrict__ nrm2,
+                                  double* __restrict__ b, int64_t n) {
+  const double s = 1.0 / sqrt(*nrm2);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = a[i] * s;
+}
+__global__ void residual_kernel(const double* __restrict__ b, const double* __restrict__ f, double* __restrict__ r,
+                                int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    r[i] = b[i] - f[i];
+}
+__global__ void f32_to_f64(const float* __restrict__ a, double* __restrict__ b, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = (double)a[i];
+}
+
+struct Solver {
+  rbf_ctx* ctx;
+  const rbf_cells* c;
+  const rbf_precond* P;
+  KernelParams kp;
+  int64_t n;
+  int m;
+  int nblk;
+  DevBuf V, Z, x, r, w, f, b, partial, dots;
+  int64_t mv32 = 0, mv64 = 0;
+
+  rbf_status alloc() {
+    cudaStream_t s = ctx->stream;
+    RBF_TRY(V.alloc(sizeof(double) * n * (m + 1), s));
+    RBF_TRY(Z.alloc(sizeof(double) * n * m, s));
+    RBF_TRY(x.alloc(sizeof(double) * n, s));
+    RBF_TRY(r.alloc(sizeof(double) * n, s));
+    RBF_TRY(w.alloc(sizeof(double) * n, s));
+    RBF_TRY(f.alloc(sizeof(double) * n, s));
+    RBF_TRY(b.alloc(sizeof(double) * n, s));
+    nblk = ctx->sm_count * 2;
+    RBF_TRY(partial.alloc(sizeof(double) * (size_t)nblk * (m + 2), s));
+    RBF_TRY(dots.alloc(sizeof(double) * 4 * (m + 2), s));
+    return RBF_OK;
+  }
+  double* Vj(int j) { return V.as<double>() + (int64_t)j * n; }
+  double* Zj(int j) { return Z.as<double>() + (int64_t)j * n; }
+
+  rbf_status op(bool fp64, const double* in, double* out) {
+    if (fp64) { ++mv64; return matvec_sorted_f64(ctx, c, kp, in, out, nullptr); }
+    ++mv32;
+    return matvec_sorted_f32_d(ctx, c, kp, in, out);
+  }
+  // dots[0..k) = V_{0..k}^T w ; neg copy at dots[(m+2)...]
+  rbf_status mdot(const double* Vb, int k, const double* vec, double* out, double* neg) {
+    cudaStream_t s = ctx->stream;
+    multi_dot_kernel<<<nblk, kVecThreads, 0, s>>>(Vb, n, k, vec, n, partial.as<double>());
+    RBF_CHECK_LAUNCH();
+    reduce_partials<<<k, 32, 0, s>>>(partial.as<double>(), k, nblk, out, neg != nullptr, neg);
+    RBF_CHECK_LAUNCH();
+    return RBF_OK;
+  }
+  rbf_status maxpy(double* vec, const double* Vb, int k, const double* coef) {
+    multi_axpy_kernel<<<grid_for(n, kVecThreads), kVecThreads, 0, ctx->stream>>>(vec, Vb, n, k, coef, n);
+    RBF_CHECK_LAUNCH();
+    return RBF_OK;
+  }
+  // r = b - A x ; returns ||r|| (synchronises)
+  rbf_status residual(bool fp64, double* beta) {
+    cudaStream_t s = ctx->stream;
+    RBF_TRY(op(fp64, x.as<double>(), f.as<double>()));
+    residual_kernel<<<grid_for(n, 256), 256, 0, s>>>(b.as<double>(), f.as<double>(), r.as<double>(), n);
+    RBF_CHECK_LAUNCH();
+    double* d = dots.as<double>();
+    RBF_TRY(mdot(r.as<double>(), 1, r.as<double>(), d, nullptr));
+    double h;
+    RBF_CUDA_TRY(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, s));
+    RBF_CUDA_TRY(cudaStreamSynchronize(s));
+    *beta = std::sqrt(h);
+    return RBF_OK;
+  }
+};
+
+}  // namespace
+
+rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp, const rbf_precond* P,
+                        const rbf_gmres_cfg* gcfg, const float* b_sorted32, double* x_out_sorted,
+                        rbf_solve_report* rep) {
+  using clk = std::chrono::steady_clock;
+  cudaStream_t s = ctx->stream;
+  Solver S{ctx, c, P, kp, c->n, 30, 0};
+  S.m = (gcfg && gcfg->restart > 0) ? gcfg->restart : 30;
+  if (S.m > 60) { set_error("restart must be <= 60"); return RBF_EINVAL; }
+  const double rtol = (gcfg && gcfg->rtol > 0) ? gcfg->rtol : 1e-6;
+  const double p1tol = (gcfg && gcfg->phase1_rtol > 0) ? gcfg->phase1_rtol : 1e-4;
+  const int maxit = (gcfg && gcfg->max_iters > 0) ? gcfg->max_iters : 500;
+  const bool polish = gcfg ? gcfg->polish_fp64 != 0 : true;
+  const int64_t n = S.n;
+  const int m = S.m;
+  RBF_TRY(S.alloc());
+  f32_to_f64<<<grid_for(n, 256), 256, 0, s>>>(b_sorted32, S.b.as<double>(), n);
+  RBF_CHECK_LAUNCH();
+  RBF_CUDA_TRY(cudaMemsetAsync(S.x.p, 0, sizeof(double) * n, s));
+  double* d = S.dots.as<double>();
+  double* dh = d;                  // h (pass 1 + 2)
+  double* dneg = d + (m + 2);      // -h for the axpy
+  double* d2 = d + 2 * (m + 2);    // pass-2 h
+  double* dn = d + 3 * (m + 2);    // norm^2
+  RBF_TRY(S.mdot(S.b.as<double>(), 1, S.b.as<double>(), dh, nullptr));
+  double bn2 = 0;
+  RBF_CUDA_TRY(cudaMemcpyAsync(&bn2, dh, sizeof(double), cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  const double bnorm = std::sqrt(bn2);
+  rbf_solve_report R{};
+  auto t_start = clk::now();
+  if (bnorm == 0.0) {
+    RBF_CUDA_TRY(cudaMemcpyAsync(x_out_sorted, S.x.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    R.converged = 1;
+    if (rep) *rep = R;
+    return RBF_OK;
+  }
+  bool fp64 = false;
+  int it = 0, it1 = 0, it2 = 0;
+  bool converged = false, breakdown_any = false;
+  int stagnant = 0;
+  double beta = bnorm, last_beta = bnorm, est = 1.0;
+  std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m), hcol(m + 2);
+  double t_switch = 0.0;
+  // r = b (x = 0)
+  RBF_CUDA_TRY(cudaMemcpyAsync(S.r.p, S.b.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  double cycle_beta = -1.0;   // true residual at the start of the previous cycle
+  for (;;) {
+    // phase switch: phase-1 target reached, or the fp32 tier stopped making
+    // progress (a cycle that did not halve the true residual, or > 3m
+    // iterations): the fp32 operator's rounding then dominates near-null
+    // directions of ill-conditioned clouds and only the fp64 tier can continue.
+    const bool p1_stalled = cycle_beta > 0 && (beta > 0.5 * cycle_beta || it1 >= 3 * m);
+    if (!fp64 && polish && (beta / bnorm <= p1tol || p1_stalled)) {
+      fp64 = true;
+      t_switch = std::chrono::duration<double>(clk::now() - t_start).count();
+      RBF_TRY(S.residual(true, &beta));
+    }
+    if (fp64 && beta / bnorm <= rtol) { converged = true; break; }
+    if (!polish && beta / bnorm <= rtol) { converged = true; break; }
+    if (it >= maxit) break;
+    if (beta >= last_beta * (1 - 1e-12) && it > 0) {
+      if (++stagnant >= 3) break;
+    } else {
+      stagnant = 0;
+    }
+    last_beta = beta;
+    cycle_beta = fp64 ? -1.0 : beta;
+    const double target = fp64 ? rtol : std::max(p1tol, rtol);
+    // V0 = r / beta
+    scale_kernel<<<grid_for(n, 256), 256, 0, s>>>(S.r.as<double>(), 1.0 / beta, S.Vj(0), n);
+    RBF_CHECK_LAUNCH();
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    int k = 0;
+    bool bd = false;
+    for (int j = 0; j < m; ++j) {
+      RBF_TRY(precond_apply_sorted<double>(ctx, P, S.Vj(j), S.Zj(j)));
+      RBF_TRY(S.op(fp64, S.Zj(j), S.w.as<double>()));
+      double* wv = S.w.as<double>();
+      // CGS2
+      RBF_TRY(S.mdot(S.V.as<double>(), j + 1, wv, dh, dneg));
+      RBF_TRY(S.maxpy(wv, S.V.as<double>(), j + 1, dneg));
+      RBF_TRY(S.mdot(S.V.as<double>(), j + 1, wv, d2, dneg));
+      RBF_TRY(S.maxpy(wv, S.V.as<double>(), j + 1, dneg));
+      RBF_TRY(S.mdot(wv, 1, wv, dn, nullptr));
+      scale_by_inv_norm<<<grid_for(n, 256), 256, 0, s>>>(wv, dn, S.Vj(j + 1), n);
+      RBF_CHECK_LAUNCH();
+      RBF_CUDA_TRY(cudaMemcpyAsync(hcol.data(), dh, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, s));
+      std::vector<double> h2(j + 1);
+      double hn2 = 0;
+      RBF_CUDA_TRY(cudaMemcpyAsync(h2.data(), d2, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, s));
+      RBF_CUDA_TRY(cudaMemcpyAsync(&hn2, dn, sizeof(double), cudaMemcpyDeviceToHost, s));
+      RBF_CUDA_TRY(cudaStreamSynchronize(s));
+      for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = hcol[i] + h2[i];
+      const double hn = std::sqrt(hn2);
+      H[(size_t)(j + 1) * m + j] = hn;
+      for (int i = 0; i < j; ++i) {
+        const double a = H[(size_t)i * m + j], bb = H[(size_t)(i + 1) * m + j];
+        H[(size_t)i * m + j] = cs[i] * a + sn[i] * bb;
+        H[(size_t)(i + 1) * m + j] = -sn[i] * a + cs[i] * bb;
+      }
+      const double a = H[(size_t)j * m + j], bb = H[(size_t)(j + 1) * m + j];
+      const double den = std::hypot(a, bb);
+      cs[j] = den > 0 ? a / den : 1.0;
+      sn[j] = den > 0 ? bb / den : 0.0;
+      H[(size_t)j * m + j] = den;
+      H[(size_t)(j + 1) * m + j] = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      ++it;
+      if (fp64) ++it2; else ++it1;
+      k = j + 1;
+      est = std::fabs(g[j + 1]) / bnorm;
+      if (!(hn > 1e-14 * beta) || !std::isfinite(hn)) { bd = true; break; }
+      if (est <= target || it >= maxit) break;
+    }
+    // y = H^-1 g, x += Z y
+    for (int i = k - 1; i >= 0; --i) {
+      double acc = g[i];
+      for (int q = i + 1; q < k; ++q) acc -= H[(size_t)i * m + q] * y[q];
+      const double dd = H[(size_t)i * m + i];
+      y[i] = dd != 0 ? acc / dd : 0.0;
+    }
+    RBF_CUDA_TRY(cudaMemcpyAsync(dneg, y.data(), sizeof(double) * k, cudaMemcpyHostToDevice, s));
+    RBF_TRY(S.maxpy(S.x.as<double>(), S.Z.as<double>(), k, dneg));
+    ++R.restarts;
+    if (bd) breakdown_any = true;
+    RBF_TRY(S.residual(fp64, &beta));
+  }
+  // final true residual with the fp64 operator
+  double tr = beta;
+  if (!fp64) RBF_TRY(S.residual(true, &tr));
+  const double t_end = std::chrono::duration<double>(clk::now() - t_start).count();
+  RBF_CUDA_TRY(cudaMemcpyAsync(x_out_sorted, S.x.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  R.iters_phase1 = it1;
+  R.iters_phase2 = it2;
+  R.rel_residual_true = tr / bnorm;
+  R.rel_residual_est = est;
+  R.converged = (R.rel_residual_true <= rtol) ? 1 : 0;
+  (void)converged;
+  R.breakdown = breakdown_any ? 1 : 0;
+  R.t_phase1 = fp64 ? t_switch : t_end;
+  R.t_phase2 = fp64 ? t_end - t_switch : 0.0;
+  R.matvecs_f32 = S.mv32;
+  R.matvecs_f64 = S.mv64;
+  if (rep) {
+    R.t_setup = rep->t_setup;
+    R.nblocks = rep->nblocks;
+    R.precond_bytes = rep->precond_bytes;
+    *rep = R;
+  }
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  return RBF_OK;
+}
+
+}  // namespace rbf
+
+using namespace rbf;
+
+extern "C" {
+
+rbf_status rbf_gmres_solve(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, const rbf_precond* precond,
+                           const rbf_precond_cfg* pcfg, const rbf_gmres_cfg* gcfg, const float* b, double* w,
+                           rbf_solve_report* rep) {
+  if (!ctx || !c || !kern || !b || !w) { set_error("NULL argument"); return RBF_EINVAL; }
+  if (!(kern->sigma > 0) || !(kern->cutoff_sigmas > 0)) { set_error("bad kernel"); return RBF_EINVAL; }
+  if (kern->cutoff_sigmas * kern->sigma > c->cutoff * (1 + 1e-12)) {
+    set_error("kernel cutoff exceeds the cutoff the cells were built for");
+    return RBF_EINVAL;
+  }
+  if (precond && precond->cells != c) { set_error("precond was built for other cells"); return RBF_EINVAL; }
+  RBF_CUDA_TRY(cudaSetDevice(ctx->device));
+  KernelParams kp = kernel_params(kern);
+  rbf_solve_report R{};
+  rbf_precond* own = nullptr;
+  const rbf_precond* P = precond;
+  if (!P) {
+    own = new (std::nothrow) rbf_precond();
+    if (!own) { set_error("host allocation failed"); return RBF_ENOMEM; }
+    rbf_status st;
+    {
+      ProfScope ps(ctx, RBF_PROF_PRECOND_SETUP);
+      st = precond_build(ctx, c, kp, pcfg, own);
+    }
+    if (st != RBF_OK) { delete own; return st; }
+    own->cells = c;
+    P = own;
+  }
+  R.t_setup = P->t_setup;
+  R.nblocks = P->nblocks;
+  R.precond_bytes = P->bytes;
+  const int64_t n = c->n;
+  DevBuf bs, xs;
+  rbf_status st = bs.alloc(sizeof(float) * n, ctx->stream);
+  if (st == RBF_OK) st = xs.alloc(sizeof(double) * n, ctx->stream);
+  if (st == RBF_OK) st = gather_f32_to_sorted(ctx, b, c->perm.as<int32_t>(), bs.as<float>(), n);
+  if (st == RBF_OK) st = gmres_sorted(ctx, c, kp, P, gcfg, bs.as<float>(), xs.as<double>(), &R);
+  if (st == RBF_OK) st = scatter_f64_from_sorted(ctx, xs.as<double>(), c->perm.as<int32_t>(), w, n);
+  if (st == RBF_OK) {
+    cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); st = RBF_ECUDA; }
+  }
+  delete own;
+  if (rep) *rep = R;
+  return st;
+}
+
+rbf_status rbf_reconstruct_host(rbf_ctx* ctx, const float* xyz, const float* b, int64_t n, const rbf_kernel* kern,
+                                const rbf_cell_cfg* ccfg, const rbf_precond_cfg* pcfg, const rbf_gmres_cfg* gcfg,
+                                const rbf_grid* grid, double* w_out, float* field_out, rbf_solve_report* rep) {
+  if (!ctx || !xyz || !b || !kern || !grid || !w_out || !field_out) { set_error("NULL argument"); return RBF_EINVAL; }
+  if (n < 1) { set_error("n must be >= 1"); return RBF_EINVAL; }
+  for (int a = 0; a < 3; ++a)
+    if (grid->n[a] < 2) { set_error("grid needs n >= 2 nodes per axis"); return RBF_EINVAL; }
+  RBF_CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  const int64_t nodes = (int64_t)grid->n[0] * grid->n[1] * grid->n[2];
+  DevBuf dx, db, dw, df;
+  RBF_TRY(dx.alloc(sizeof(float) * 3 * n, s));
+  RBF_TRY(db.alloc(sizeof(float) * n, s));
+  RBF_TRY(dw.alloc(sizeof(double) * n, s));
+  RBF_TRY(df.alloc(sizeof(float) * nodes, s));
+  RBF_CUDA_TRY(cudaMemcpyAsync(dx.p, xyz, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, s));
+  RBF_CUDA_TRY(cudaMemcpyAsync(db.p, b, sizeof(float) * n, cudaMemcpyHostToDevice, s));
+  rbf_cells* cells = nullptr;
+  RBF_TRY(rbf_build_cells(ctx, dx.as<float>(), n, kern, ccfg, &cells));
+  rbf_solve_report R{};
+  rbf_status st = rbf_gmres_solve(ctx, cells, kern, nullptr, pcfg, gcfg, db.as<float>(), dw.as<double>(), &R);
+  if (st == RBF_OK) st = rbf_eval_grid(ctx, cells, kern, dw.as<double>(), grid, df.as<float>());
+  if (st == RBF_OK) {
+    cudaError_t e1 = cudaMemcpyAsync(w_out, dw.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
+    cudaError_t e2 = cudaMemcpyAsync(field_out, df.p, sizeof(float) * nodes, cudaMemcpyDeviceToHost, s);
+    cudaError_t e3 = cudaStreamSynchronize(s);
+    if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
+      set_error("copy-out failed");
+      st = RBF_ECUDA;
+    }
+  }
+  rbf_cells_free(cells);
+  if (rep) *rep = R;
+  return st;
+}
+
+}  // extern "C"

@@ -74,10 +74,32 @@ struct DevBuf {
 
 }  // namespace rbf
 
+struct rbf_prof_rec {
+  int stage;
+  cudaEvent_t a, b;
+};
+
 struct rbf_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   int sm_count = 148;
+  bool prof = false;
+  std::vector<rbf_prof_rec> prof_recs;
+  std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t take_event() {
+    if (!ev_pool.empty()) {
+      cudaEvent_t e = ev_pool.back();
+      ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+  ~rbf_ctx() {
+    for (auto& r : prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : ev_pool) cudaEventDestroy(e);
+  }
   rbf::DevBuf scratch;       // generic scratch (radix sort, scans)
   rbf::DevBuf counter;       // work counters (int32 x 64)
   rbf::DevBuf stats;         // pair counters (u64 x 4)
@@ -142,7 +164,8 @@ rbf_status matvec_sorted_f32(rbf_ctx* ctx, const rbf_cells* c, const KernelParam
 rbf_status matvec_sorted_f64(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
                              const double* w_sorted, double* f_sorted, const int32_t* out_perm);
 rbf_status eval_grid_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
-                            const double* w_sorted, const rbf_grid* g, float* field);
+                            const double* w_sorted, const rbf_grid* g, float* field,
+                            unsigned long long* pair_stats = nullptr);
 
 // small vector kernels (vec.cu)
 rbf_status gather_f32_to_sorted(rbf_ctx* ctx, const float* src, const int32_t* perm, float* dst, int64_t n);
@@ -162,4 +185,24 @@ inline int grid_for(int64_t n, int threads, int max_blocks = 148 * 16) {
 
 namespace rbf {
 const char* last_error_cstr();
+
+// Brackets the launches issued in its scope with CUDA events when profiling is on.
+struct ProfScope {
+  rbf_ctx* ctx;
+  int stage;
+  cudaEvent_t a = nullptr;
+  ProfScope(rbf_ctx* c, int s) : ctx(c), stage(s) {
+    if (ctx && ctx->prof) {
+      a = ctx->take_event();
+      cudaEventRecord(a, ctx->stream);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = ctx->take_event();
+      cudaEventRecord(b, ctx->stream);
+      ctx->prof_recs.push_back(rbf_prof_rec{stage, a, b});
+    }
+  }
+};
 }

@@ -1,0 +1,756 @@
+// a4/a5 of SURVEY.md §8(a): restricted additive Schwarz preconditioner
+// (§3.1).  "solve in the individual overlapping subdomains Omega_i
+// the linear sub-system A_i x_Omega_i = b_Omega_i ... the values x outside of
+// the subdomain ~Omega_i are discarded".
+//
+// Blocks (reading R8; identical definition to oracle/solve.py):
+//   cores  = runs of whole non-empty cells in Morton order of the cell
+//            coordinates, cut every core_target centres (prefix count), last
+//            core merged into its predecessor if it holds < core_target/2;
+//   ext    = core + every centre j with min_{i in core} d2_32(i, j) <= f32(ov^2),
+//            d2_32 = (dx*dx + dy*dy) + dz*dz in fp32 (ov = overlap_sigmas*sigma);
+//   order  = [non-core members ascending by sorted position] + [core].
+// Setup per block: assemble A_ext (fp32), LU with partial pivoting of the
+// augmented matrix [A_ext | E_core] (the truncated block may be indefinite),
+// back-substitution -> X = A_ext^-1 E_core, and keep the restricted inverse
+// W = X^T = (A_ext^-1)[core, :] (A_ext symmetric).  Apply: z[core_i] = W_i r[ext_i].
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+
+#include "internal.h"
+#include "solver.h"
+
+namespace rbf {
+namespace {
+
+constexpr int kLuThreads = 256;
+constexpr int kNb = 32;          // panel width
+constexpr int kMaxCore = 3968;   // core centres held in shared memory by the ext search (48 KB static)
+
+// ---------------------------------------------------------------- helpers --
+__global__ void flag_cells(const uint32_t* __restrict__ keys, int64_t n, uint32_t* __restrict__ flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1u : 0u;
+}
+
+__global__ void compact_cells(const uint32_t* __restrict__ keys, int64_t n, const uint32_t* __restrict__ flag,
+                              const uint32_t* __restrict__ pos, int32_t* __restrict__ ne_start,
+                              uint32_t* __restrict__ ne_key) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (flag[i]) {
+      ne_start[pos[i]] = (int32_t)i;
+      ne_key[pos[i]] = keys[i];
+    }
+}
+
+__device__ __forceinline__ unsigned long long spread3(unsigned v) {
+  unsigned long long x = v & 0x1fffffull;
+  x = (x | x << 32) & 0x1f00000000ffffull;
+  x = (x | x << 16) & 0x1f0000ff0000ffull;
+  x = (x | x << 8) & 0x100f00f00f00f00full;
+  x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+  x = (x | x << 2) & 0x1249249249249249ull;
+  return x;
+}
+
+// Morton code of each non-empty cell (x in bit 0), value = its index.
+__global__ void morton_kernel(const uint32_t* __restrict__ ne_key, int64_t nne, int dimx, int dimy,
+                              unsigned long long* __restrict__ code, int32_t* __restrict__ idx) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nne; k += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t key = ne_key[k];
+    unsigned cx = key % dimx, cy = (key / dimx) % dimy, cz = key / ((unsigned)dimx * dimy);
+    code[k] = spread3(cx) | (spread3(cy) << 1) | (spread3(cz) << 2);
+    idx[k] = (int32_t)k;
+  }
+}
+
+// counts of the non-empty cells in Morton order
+__global__ void morton_counts(const int32_t* __restrict__ order, const int32_t* __restrict__ ne_start, int64_t nne,
+                              int64_t n, uint32_t* __restrict__ cnt) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nne; t += (int64_t)gridDim.x * blockDim.x) {
+    int32_t k = order[t];
+    int64_t e = (k + 1 < nne) ? ne_start[k + 1] : n;
+    cnt[t] = (uint32_t)(e - ne_start[k]);
+  }
+}
+
+__global__ void core_flags(const uint32_t* __restrict__ P, int64_t nne, int ct, uint32_t* __restrict__ flag) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nne; t += (int64_t)gridDim.x * blockDim.x)
+    flag[t] = (t == 0 || P[t] / (uint32_t)ct != P[t - 1] / (uint32_t)ct) ? 1u : 0u;
+}
+
+__global__ void core_starts(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos, int64_t nne,
+                            int32_t* __restrict__ core_cell_start) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nne; t += (int64_t)gridDim.x * blockDim.x)
+    if (flag[t]) core_cell_start[pos[t]] = (int32_t)t;
+}
+
+// core_idx[P[t] + q] = ne_start[order[t]] + q ; owner of each sorted position
+__global__ void core_members(const int32_t* __restrict__ order, const int32_t* __restrict__ ne_start,
+                             const uint32_t* __restrict__ P, const uint32_t* __restrict__ cnt,
+                             const int32_t* __restrict__ cell_core, int64_t nne, int32_t* __restrict__ core_idx,
+                             int32_t* __restrict__ owner) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t t = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32; t < nne; t += nw) {
+    const int32_t s = ne_start[order[t]];
+    const uint32_t base = P[t], m = cnt[t];
+    const int32_t b = cell_core[t];
+    for (uint32_t q = lane; q < m; q += 32) {
+      core_idx[base + q] = s + (int32_t)q;
+      owner[s + q] = b;
+    }
+  }
+}
+
+// block id of every Morton-ordered cell from the core cell starts
+__global__ void cell_core_kernel(const int32_t* __restrict__ core_cell_start, int64_t ncore, int64_t nne,
+                                 int32_t* __restrict__ cell_core) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < ncore; b += (int64_t)gridDim.x * blockDim.x) {
+    int64_t e = (b + 1 < ncore) ? core_cell_start[b + 1] : nne;
+    for (int64_t t = core_cell_start[b]; t < e; ++t) cell_core[t] = (int32_t)b;
+  }
+}
+
+// ---------------------------------------------------------- ext search -----
+// One CTA per block.  WRITE=false: count the non-core members; WRITE=true:
+// write them ascending, then append the core.
+template <bool WRITE>
+__global__ void __launch_bounds__(256)
+ext_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ cell_start, CellGrid g,
+           const int64_t* __restrict__ core_ptr, const int32_t* __restrict__ core_idx,
+           const int32_t* __restrict__ owner, float ov2, float ov, int64_t nblocks,
+           uint32_t* __restrict__ extra_count, const int64_t* __restrict__ ext_ptr, int32_t* __restrict__ ext_idx,
+           int* __restrict__ err) {
+  __shared__ float cx[kMaxCore], cy[kMaxCore], cz[kMaxCore];
+  __shared__ float red[6][8];
+  __shared__ uint32_t wsum[8];
+  __shared__ uint32_t s_base;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x) {
+    const int64_t c0 = core_ptr[b], c1 = core_ptr[b + 1];
+    const int nc = (int)(c1 - c0);
+    if (nc > kMaxCore) {
+      if (tid == 0) atomicExch(err, 1);
+      return;
+    }
+    float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int i = tid; i < nc; i += blockDim.x) {
+      float4 p = sorted[core_idx[c0 + i]];
+      cx[i] = p.x; cy[i] = p.y; cz[i] = p.z;
+      mn[0] = fminf(mn[0], p.x); mn[1] = fminf(mn[1], p.y); mn[2] = fminf(mn[2], p.z);
+      mx[0] = fmaxf(mx[0], p.x); mx[1] = fmaxf(mx[1], p.y); mx[2] = fmaxf(mx[2], p.z);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        mn[a] = fminf(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
+        mx[a] = fmaxf(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+      }
+    if (lane == 0)
+      for (int a = 0; a < 3; ++a) { red[a][wid] = mn[a]; red[3 + a][wid] = mx[a]; }
+    __syncthreads();
+    float bl[3], bh[3];
+    for (int a = 0; a < 3; ++a) {
+      bl[a] = red[a][0]; bh[a] = red[3 + a][0];
+      for (int q = 1; q < (int)(blockDim.x / 32); ++q) { bl[a] = fminf(bl[a], red[a][q]); bh[a] = fmaxf(bh[a], red[3 + a][q]); }
+    }
+    if (tid == 0) s_base = 0;
+    __syncthreads();
+    // candidate cells: those intersecting the core's bounding box dilated by ov
+    // (a superset of the members; the exact fp32 test below decides)
+    const float pad = ov * 1.0001f + 1e-6f;
+    int lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) {
+      float t0 = floorf((bl[a] - pad - g.lo[a]) * g.inv_h), t1 = floorf((bh[a] + pad - g.lo[a]) * g.inv_h);
+      lo[a] = (int)fminf(fmaxf(t0, 0.f), (float)(g.dim[a] - 1));
+      hi[a] = (int)fminf(fmaxf(t1, 0.f), (float)(g.dim[a] - 1));
+    }
+    uint32_t count = 0;   // running count (WRITE: output position base)
+    const int64_t out0 = WRITE ? ext_ptr[b] : 0;
+    for (int z = lo[2]; z <= hi[2]; ++z)
+      for (int y = lo[1]; y <= hi[1]; ++y) {
+        const int64_t row = ((int64_t)z * g.dim[1] + y) * g.dim[0];
+        const int s = cell_start[row + lo[0]], e = cell_start[row + hi[0] + 1];
+        for (int j0 = s; j0 < e; j0 += blockDim.x) {
+          const int j = j0 + tid;
+          bool mem = false;
+          if (j < e && owner[j] != (int32_t)b) {
+            const float4 p = sorted[j];
+            const float gx = fmaxf(0.f, fmaxf(bl[0] - p.x, p.x - bh[0]));
+            const float gy = fmaxf(0.f, fmaxf(bl[1] - p.y, p.y - bh[1]));
+            const float gz = fmaxf(0.f, fmaxf(bl[2] - p.z, p.z - bh[2]));
+            if (gx * gx + gy * gy + gz * gz <= ov2 * 1.0002f + 1e-12f) {
+              for (int i = 0; i < nc; ++i) {
+                const float dx = __fsub_rn(p.x, cx[i]), dy = __fsub_rn(p.y, cy[i]), dz = __fsub_rn(p.z, cz[i]);
+                const float d2 = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+                if (d2 <= ov2) { mem = true; break; }
+              }
+            }
+          }
+          // ordered block-wide compaction
+          const unsigned bal = __ballot_sync(0xffffffffu, mem);
+          if (lane == 0) wsum[wid] = __popc(bal);
+          __syncthreads();
+          uint32_t before = 0, tot = 0;
+          for (int q = 0; q < (int)(blockDim.x / 32); ++q) {
+            if (q < wid) before += wsum[q];
+            tot += wsum[q];
+          }
+          if (WRITE && mem) ext_idx[out0 + count + before + __popc(bal & ((1u << lane) - 1u))] = j;
+          count += tot;
+          __syncthreads();
+        }
+      }
+    if (!WRITE) {
+      if (tid == 0) extra_count[b] = count + (uint32_t)nc;
+    } else {
+      for (int i = tid; i < nc; i += blockDim.x) ext_idx[out0 + count + i] = core_idx[c0 + i];
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------- factorisation --
+// fp64 throughout: blocks of the truncated operator reach condition numbers of
+// 1e12-1e14 when the cloud holds near-duplicate centres (c2's noisy torus: NN
+// 3.4e-4 = 0.007 sigma), where an fp32 LU returns garbage.
+using FT = double;
+// Storage of the restricted inverse.  fp64: with near-duplicate centres W has
+// entries ~1/lambda_min ~ 1e13/a; rounding them to fp32 injects absolute errors
+// in non-null directions that A amplifies.
+using WT = double;
+
+struct LuJob {
+  int64_t ws_off;   // element offset of the augmented matrix in the workspace
+  int64_t ext_off;  // offset into ext_idx
+  int64_t w_off;    // element offset of W (nc x m) in the W buffer
+  int m, nc;
+};
+
+// A_ext (m x m) | E_core (m x nc), row-major with ld = m + nc; entries as the
+// oracle forms them: a * exp(-d2 / (2 sigma^2)), d2 = (dx^2 + dy^2) + dz^2 in fp64.
+__global__ void assemble_kernel(const LuJob* __restrict__ jobs, const float4* __restrict__ sorted,
+                                const int32_t* __restrict__ ext_idx, FT* __restrict__ ws, double amp,
+                                double two_s2, double c2) {
+  const LuJob J = jobs[blockIdx.y];
+  const int m = J.m, nc = J.nc, ld = m + nc;
+  FT* A = ws + J.ws_off;
+  const int32_t* ext = ext_idx + J.ext_off;
+  for (int i = blockIdx.x; i < m; i += gridDim.x) {
+    const float4 pi = sorted[ext[i]];
+    for (int c = threadIdx.x; c < ld; c += blockDim.x) {
+      FT v;
+      if (c < m) {
+        const float4 pj = sorted[ext[c]];
+        const double dx = (double)pi.x - (double)pj.x, dy = (double)pi.y - (double)pj.y,
+                     dz = (double)pi.z - (double)pj.z;
+        const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+        v = d2 <= c2 ? amp * exp(-d2 / two_s2) : 0.0;
+      } else {
+        v = (i == m - nc + (c - m)) ? 1.0 : 0.0;
+      }
+      A[(int64_t)i * ld + c] = v;
+    }
+  }
+}
+
+// C[r][c] -= sum_{t<kb} A[r][lc + t] * A[rr + t][c]   for r in [r0,r1), c in [c0,c1)
+__device__ void gemm_sub(FT* __restrict__ A, int ld, int r0, int r1, int c0, int c1, int lc, int rr, int kb,
+                         FT (*sL)[64 + 1], FT (*sU)[64 + 2]) {
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  for (int tr = r0; tr < r1; tr += 64)
+    for (int tc = c0; tc < c1; tc += 64) {
+      for (int q = tid; q < 64 * kNb; q += blockDim.x) {
+        const int i = q / kNb, t = q % kNb;
+        const int r = tr + i;
+        sL[t][i] = (r < r1 && t < kb) ? A[(int64_t)r * ld + lc + t] : 0.0;
+      }
+      for (int q = tid; q < kNb * 64; q += blockDim.x) {
+        const int t = q / 64, j = q % 64;
+        const int c = tc + j;
+        sU[t][j] = (c < c1 && t < kb) ? A[(int64_t)(rr + t) * ld + c] : 0.0;
+      }
+      __syncthreads();
+      FT acc[4][4] = {};
+#pragma unroll 4
+      for (int t = 0; t < kNb; ++t) {
+        FT a[4], bv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) { a[q] = sL[t][ty + 16 * q]; bv[q] = sU[t][tx + 16 * q]; }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int p = 0; p < 4; ++p) acc[q][p] = fma(a[q], bv[p], acc[q][p]);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = tr + ty + 16 * q;
+        if (r >= r1) continue;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const int c = tc + tx + 16 * p;
+          if (c < c1) A[(int64_t)r * ld + c] -= acc[q][p];
+        }
+      }
+      __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kLuThreads)
+lu_kernel(const LuJob* __restrict__ jobs, FT* __restrict__ ws, WT* __restrict__ W, int* __restrict__ info) {
+  __shared__ FT sL[kNb][64 + 1];
+  __shared__ FT sU[kNb][64 + 2];
+  __shared__ FT sT[kNb][kNb + 1];
+  __shared__ FT sv[kLuThreads / 32];
+  __shared__ int si[kLuThreads / 32];
+  __shared__ int spiv[kNb];
+  const LuJob J = jobs[blockIdx.x];
+  const int m = J.m, nc = J.nc, ld = m + nc;
+  FT* A = ws + J.ws_off;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  int singular = 0;
+
+  for (int k0 = 0; k0 < m; k0 += kNb) {
+    const int kb = min(kNb, m - k0);
+    // ---- panel: columns [k0, k0+kb), rows [k0, m); swaps applied inside the panel only
+    for (int jj = 0; jj < kb; ++jj) {
+      const int j = k0 + jj;
+      FT best = -1.0;
+      int bi = j;
+      for (int i = j + tid; i < m; i += blockDim.x) {
+        const FT v = fabs(A[(int64_t)i * ld + j]);
+        if (v > best) { best = v; bi = i; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const FT ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+      }
+      if (lane == 0) { sv[wid] = best; si[wid] = bi; }
+      __syncthreads();
+      if (tid == 0) {
+        FT b2 = sv[0];
+        int i2 = si[0];
+        for (int q = 1; q < kLuThreads / 32; ++q)
+          if (sv[q] > b2 || (sv[q] == b2 && si[q] < i2)) { b2 = sv[q]; i2 = si[q]; }
+        spiv[jj] = i2;
+      }
+      __syncthreads();
+      const int p = spiv[jj];
+      if (p != j && tid < kb) {
+        FT* rj = A + (int64_t)j * ld + k0;
+        FT* rp = A + (int64_t)p * ld + k0;
+        const FT t = rj[tid];
+        rj[tid] = rp[tid];
+        rp[tid] = t;
+      }
+      __syncthreads();
+      FT piv = A[(int64_t)j * ld + j];
+      if (piv == 0.0) { singular = 1; piv = 1e-300; }
+      const FT inv = 1.0 / piv;
+      for (int i = j + 1 + tid; i < m; i += blockDim.x) {
+        FT* ri = A + (int64_t)i * ld;
+        const FT l = ri[j] * inv;
+        ri[j] = l;
+        const FT* rj = A + (int64_t)j * ld;
+        for (int c = j + 1; c < k0 + kb; ++c) ri[c] = fma(-l, rj[c], ri[c]);
+      }
+      __syncthreads();
+    }
+    // ---- the panel's row swaps on the columns right of it (incl. the RHS block);
+    //      the L columns left of the panel are never read again
+    for (int c = k0 + kb + tid; c < ld; c += blockDim.x) {
+      for (int jj = 0; jj < kb; ++jj) {
+        const int p = spiv[jj], j = k0 + jj;
+        if (p != j) {
+          const FT t = A[(int64_t)j * ld + c];
+          A[(int64_t)j * ld + c] = A[(int64_t)p * ld + c];
+          A[(int64_t)p * ld + c] = t;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- U12 = L11^-1 A12 (unit lower triangular L11), columns [k0+kb, ld)
+    for (int q = tid; q < kb * kb; q += blockDim.x) sT[q / kb][q % kb] = A[(int64_t)(k0 + q / kb) * ld + k0 + q % kb];
+    __syncthreads();
+    for (int c = k0 + kb + tid; c < ld; c += blockDim.x) {
+      FT x[kNb];
+#pragma unroll
+      for (int r = 0; r < kNb; ++r) x[r] = r < kb ? A[(int64_t)(k0 + r) * ld + c] : 0.0;
+#pragma unroll
+      for (int r = 1; r < kNb; ++r) {
+        FT acc = x[r];
+#pragma unroll
+        for (int t = 0; t < r; ++t) acc = fma(-sT[r][t], x[t], acc);
+        x[r] = acc;
+      }
+#pragma unroll
+      for (int r = 1; r < kNb; ++r)
+        if (r < kb) A[(int64_t)(k0 + r) * ld + c] = x[r];
+    }
+    __syncthreads();
+    // ---- trailing update A22 -= L21 U12 over all remaining columns (incl. the RHS block)
+    if (k0 + kb < m) gemm_sub(A, ld, k0 + kb, m, k0 + kb, ld, k0, k0, kb, sL, sU);
+    __syncthreads();
+  }
+  // ---- back substitution U X = Y on the RHS block (columns [m, ld)), bottom-up
+  for (int k0 = ((m - 1) / kNb) * kNb; k0 >= 0; k0 -= kNb) {
+    const int kb = min(kNb, m - k0);
+    for (int q = tid; q < kb * kb; q += blockDim.x) sT[q / kb][q % kb] = A[(int64_t)(k0 + q / kb) * ld + k0 + q % kb];
+    __syncthreads();
+    for (int c = m + tid; c < ld; c += blockDim.x) {
+      FT x[kNb];
+#pragma unroll
+      for (int r = 0; r < kNb; ++r) x[r] = r < kb ? A[(int64_t)(k0 + r) * ld + c] : 0.0;
+#pragma unroll
+      for (int r = kNb - 1; r >= 0; --r) {
+        if (r >= kb) continue;
+        FT acc = x[r];
+#pragma unroll
+        for (int t = r + 1; t < kNb; ++t)
+          if (t < kb) acc = fma(-sT[r][t], x[t], acc);
+        FT d = sT[r][r];
+        if (d == 0.0) d = 1e-300;
+        x[r] = acc / d;
+      }
+#pragma unroll
+      for (int r = 0; r < kNb; ++r)
+        if (r < kb) A[(int64_t)(k0 + r) * ld + c] = x[r];
+    }
+    __syncthreads();
+    if (k0 > 0) gemm_sub(A, ld, 0, k0, m, ld, k0, k0, kb, sL, sU);
+    __syncthreads();
+  }
+  // ---- W (nc x m, fp32) = X^T, X = A[:, m:ld]
+  WT* Wb = W + J.w_off;
+  for (int e0 = 0; e0 < m; e0 += kNb)
+    for (int c0 = 0; c0 < nc; c0 += kNb) {
+      for (int q = tid; q < kNb * kNb; q += blockDim.x) {
+        const int e = e0 + q / kNb, c = c0 + q % kNb;
+        sT[q / kNb][q % kNb] = (e < m && c < nc) ? A[(int64_t)e * ld + m + c] : 0.0;
+      }
+      __syncthreads();
+      for (int q = tid; q < kNb * kNb; q += blockDim.x) {
+        const int c = c0 + q / kNb, e = e0 + q % kNb;
+        if (e < m && c < nc) Wb[(int64_t)c * m + e] = (WT)sT[q % kNb][q / kNb];
+      }
+      __syncthreads();
+    }
+  if (singular && tid == 0) atomicAdd(info, 1);
+}
+
+// ---------------------------------------------------------------- apply ----
+// One CTA per block: r_ext -> shared memory (fp32), z[core_c] = W[c,:] . r_ext
+template <class VT>
+__global__ void __launch_bounds__(256)
+apply_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __restrict__ core_ptr,
+             const int32_t* __restrict__ ext_idx, const int64_t* __restrict__ w_off, const WT* __restrict__ W,
+             const VT* __restrict__ r, VT* __restrict__ z, int64_t nblocks) {
+  extern __shared__ double sr[];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarp = blockDim.x >> 5;
+  for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x) {
+    const int64_t e0 = ext_ptr[b];
+    const int m = (int)(ext_ptr[b + 1] - e0);
+    const int nc = (int)(core_ptr[b + 1] - core_ptr[b]);
+    for (int e = tid; e < m; e += blockDim.x) sr[e] = (double)r[ext_idx[e0 + e]];
+    __syncthreads();
+    const WT* Wb = W + w_off[b];
+    for (int c = wid; c < nc; c += nwarp) {
+      const WT* row = Wb + (int64_t)c * m;
+      double acc = 0.0;
+      for (int e = lane; e < m; e += 32) acc = fma((double)__ldg(row + e), sr[e], acc);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) z[ext_idx[e0 + (m - nc) + c]] = (VT)acc;
+    }
+    __syncthreads();
+  }
+}
+
+template <class VT>
+__global__ void copy_kernel(const VT* __restrict__ a, VT* __restrict__ b, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = a[i];
+}
+
+}  // namespace
+
+rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp, const rbf_precond_cfg* cfg,
+                         rbf_precond* P) {
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
+  cudaStream_t s = ctx->stream;
+  const int64_t n = c->n;
+  P->n = n;
+  P->kind = cfg ? cfg->kind : 2;
+  if (P->kind == 0) { P->nblocks = 0; P->bytes = 0; return RBF_OK; }
+  const int ct = (cfg && cfg->core_target > 0) ? cfg->core_target : 512;
+  const double ovs = (P->kind == 1) ? 0.0 : (cfg ? cfg->overlap_sigmas : 1.0);
+  const int max_ext = (cfg && cfg->max_ext > 0) ? cfg->max_ext : 4096;
+  if (ovs < 0 || !std::isfinite(ovs)) { set_error("overlap_sigmas must be >= 0"); return RBF_EINVAL; }
+
+  // 1. non-empty cells
+  const int64_t nne = c->nonempty;
+  DevBuf flag, pos, ne_start, ne_key;
+  RBF_TRY(flag.alloc(4 * n, s));
+  RBF_TRY(pos.alloc(4 * n, s));
+  RBF_TRY(ne_start.alloc(4 * nne, s));
+  RBF_TRY(ne_key.alloc(4 * nne, s));
+  flag_cells<<<grid_for(n, 256), 256, 0, s>>>(c->keys.as<uint32_t>(), n, flag.as<uint32_t>());
+  RBF_CHECK_LAUNCH();
+  RBF_TRY(exclusive_scan_u32(ctx, flag.as<uint32_t>(), pos.as<uint32_t>(), n, nullptr));
+  compact_cells<<<grid_for(n, 256), 256, 0, s>>>(c->keys.as<uint32_t>(), n, flag.as<uint32_t>(),
+                                                 pos.as<uint32_t>(), ne_start.as<int32_t>(), ne_key.as<uint32_t>());
+  RBF_CHECK_LAUNCH();
+  // 2. Morton order of the non-empty cells
+  DevBuf code, code2, idx, order;
+  RBF_TRY(code.alloc(8 * nne, s));
+  RBF_TRY(code2.alloc(8 * nne, s));
+  RBF_TRY(idx.alloc(4 * nne, s));
+  RBF_TRY(order.alloc(4 * nne, s));
+  morton_kernel<<<grid_for(nne, 256), 256, 0, s>>>(ne_key.as<uint32_t>(), nne, c->dim[0], c->dim[1],
+                                                   code.as<unsigned long long>(), idx.as<int32_t>());
+  RBF_CHECK_LAUNCH();
+  int dbits = 1;
+  while (dbits < 21 && (1 << dbits) < std::max(c->dim[0], std::max(c->dim[1], c->dim[2]))) ++dbits;
+  RBF_TRY(radix_sort_pairs<unsigned long long>(ctx, code.as<unsigned long long>(), idx.as<int32_t>(),
+                                               code2.as<unsigned long long>(), order.as<int32_t>(), nne, 3 * dbits));
+  // 3. prefix counts in Morton order and core ids
+  DevBuf cnt, Pm, cflag, cpos;
+  RBF_TRY(cnt.alloc(4 * nne, s));
+  RBF_TRY(Pm.alloc(4 * nne, s));
+  RBF_TRY(cflag.alloc(4 * nne, s));
+  RBF_TRY(cpos.alloc(4 * nne + 4, s));
+  morton_counts<<<grid_for(nne, 256), 256, 0, s>>>(order.as<int32_t>(), ne_start.as<int32_t>(), nne, n,
+                                                   cnt.as<uint32_t>());
+  RBF_CHECK_LAUNCH();
+  RBF_TRY(exclusive_scan_u32(ctx, cnt.as<uint32_t>(), Pm.as<uint32_t>(), nne, nullptr));
+  core_flags<<<grid_for(nne, 256), 256, 0, s>>>(Pm.as<uint32_t>(), nne, ct, cflag.as<uint32_t>());
+  RBF_CHECK_LAUNCH();
+  RBF_TRY(exclusive_scan_u32(ctx, cflag.as<uint32_t>(), cpos.as<uint32_t>(), nne, cpos.as<uint32_t>() + nne));
+  uint32_t ncore_u = 0;
+  RBF_CUDA_TRY(cudaMemcpyAsync(&ncore_u, cpos.as<uint32_t>() + nne, 4, cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  int64_t ncore = ncore_u;
+  DevBuf ccs;
+  RBF_TRY(ccs.alloc(4 * (ncore + 1), s));
+  core_starts<<<grid_for(nne, 256), 256, 0, s>>>(cflag.as<uint32_t>(), cpos.as<uint32_t>(), nne, ccs.as<int32_t>());
+  RBF_CHECK_LAUNCH();
+  // merge a small last core into its predecessor (reading R8)
+  std::vector<int32_t> h_ccs(ncore);
+  RBF_CUDA_TRY(cudaMemcpyAsync(h_ccs.data(), ccs.p, 4 * ncore, cudaMemcpyDeviceToHost, s));
+  uint32_t lastP = 0;
+  RBF_CUDA_TRY(cudaMemcpyAsync(&lastP, Pm.as<uint32_t>() + h_ccs.back(), 4, cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  if (ncore > 1 && 2 * ((int64_t)n - (int64_t)lastP) < ct) ncore -= 1;
+  DevBuf cell_core;
+  RBF_TRY(cell_core.alloc(4 * nne, s));
+  cell_core_kernel<<<grid_for(ncore, 128), 128, 0, s>>>(ccs.as<int32_t>(), ncore, nne, cell_core.as<int32_t>());
+  RBF_CHECK_LAUNCH();
+  // core_ptr[b] = Pm[ccs[b]], core_ptr[ncore] = n
+  std::vector<int64_t> h_core_ptr(ncore + 1);
+  {
+    std::vector<uint32_t> hP(nne);
+    RBF_CUDA_TRY(cudaMemcpyAsync(hP.data(), Pm.p, 4 * nne, cudaMemcpyDeviceToHost, s));
+    RBF_CUDA_TRY(cudaStreamSynchronize(s));
+    for (int64_t b = 0; b < ncore; ++b) h_core_ptr[b] = hP[h_ccs[b]];
+    h_core_ptr[ncore] = n;
+  }
+  int64_t max_core = 0;
+  for (int64_t b = 0; b < ncore; ++b) max_core = std::max(max_core, h_core_ptr[b + 1] - h_core_ptr[b]);
+  if (max_core > kMaxCore) {
+    set_error("a RAS core holds " + std::to_string(max_core) + " centres (> " + std::to_string(kMaxCore) +
+              "); reduce cell_edge or core_target");
+    return RBF_EUNSUPPORTED;
+  }
+  P->nblocks = ncore;
+  RBF_TRY(P->core_ptr.alloc(8 * (ncore + 1), s));
+  RBF_CUDA_TRY(cudaMemcpyAsync(P->core_ptr.p, h_core_ptr.data(), 8 * (ncore + 1), cudaMemcpyHostToDevice, s));
+  RBF_TRY(P->core_idx.alloc(4 * n, s));
+  DevBuf owner;
+  RBF_TRY(owner.alloc(4 * n, s));
+  core_members<<<grid_for(nne * 32, 256), 256, 0, s>>>(order.as<int32_t>(), ne_start.as<int32_t>(),
+                                                       Pm.as<uint32_t>(), cnt.as<uint32_t>(), cell_core.as<int32_t>(),
+                                                       nne, P->core_idx.as<int32_t>(), owner.as<int32_t>());
+  RBF_CHECK_LAUNCH();
+  // 4. extended sets
+  CellGrid g;
+  for (int a = 0; a < 3; ++a) { g.lo[a] = c->lo[a]; g.dim[a] = c->dim[a]; }
+  g.inv_h = c->inv_h;
+  g.h = (float)c->h;
+  const double ov = ovs * kp.sigma;
+  const float ov2 = (float)(ov * ov);
+  DevBuf ecount, eptr_u32, err;
+  RBF_TRY(ecount.alloc(4 * ncore, s));
+  RBF_TRY(err.alloc(4, s));
+  RBF_CUDA_TRY(cudaMemsetAsync(err.p, 0, 4, s));
+  const int eblocks = (int)std::min<int64_t>(ncore, (int64_t)ctx->sm_count * 8);
+  ext_kernel<false><<<eblocks, 256, 0, s>>>(c->sorted.as<float4>(), c->cell_start.as<int32_t>(), g,
+                                            P->core_ptr.as<int64_t>(), P->core_idx.as<int32_t>(),
+                                            owner.as<int32_t>(), ov2, (float)ov, ncore, ecount.as<uint32_t>(),
+                                            nullptr, nullptr, err.as<int>());
+  RBF_CHECK_LAUNCH();
+  std::vector<uint32_t> h_ecount(ncore);
+  RBF_CUDA_TRY(cudaMemcpyAsync(h_ecount.data(), ecount.p, 4 * ncore, cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  std::vector<int64_t> h_ext_ptr(ncore + 1, 0), h_w_off(ncore + 1, 0);
+  int64_t max_m = 0;
+  for (int64_t b = 0; b < ncore; ++b) {
+    h_ext_ptr[b + 1] = h_ext_ptr[b] + h_ecount[b];
+    const int64_t m = h_ecount[b], nc = h_core_ptr[b + 1] - h_core_ptr[b];
+    h_w_off[b + 1] = h_w_off[b] + m * nc;
+    max_m = std::max(max_m, m);
+  }
+  if (max_m > max_ext) {
+    set_error("a RAS extended block holds " + std::to_string(max_m) + " centres (> max_ext " +
+              std::to_string(max_ext) + ")");
+    return RBF_EUNSUPPORTED;
+  }
+  P->max_m = (int)max_m;
+  RBF_TRY(P->ext_ptr.alloc(8 * (ncore + 1), s));
+  RBF_TRY(P->w_off.alloc(8 * (ncore + 1), s));
+  RBF_CUDA_TRY(cudaMemcpyAsync(P->ext_ptr.p, h_ext_ptr.data(), 8 * (ncore + 1), cudaMemcpyHostToDevice, s));
+  RBF_CUDA_TRY(cudaMemcpyAsync(P->w_off.p, h_w_off.data(), 8 * (ncore + 1), cudaMemcpyHostToDevice, s));
+  RBF_TRY(P->ext_idx.alloc(4 * h_ext_ptr[ncore], s));
+  ext_kernel<true><<<eblocks, 256, 0, s>>>(c->sorted.as<float4>(), c->cell_start.as<int32_t>(), g,
+                                           P->core_ptr.as<int64_t>(), P->core_idx.as<int32_t>(), owner.as<int32_t>(),
+                                           ov2, (float)ov, ncore, nullptr, P->ext_ptr.as<int64_t>(),
+                                           P->ext_idx.as<int32_t>(), err.as<int>());
+  RBF_CHECK_LAUNCH();
+  P->h_core_ptr = h_core_ptr;
+  P->h_ext_ptr = h_ext_ptr;
+  // 5. assemble + factor + restricted inverse, in chunks bounded by workspace bytes
+  RBF_TRY(P->W.alloc(sizeof(WT) * (size_t)std::max<int64_t>(h_w_off[ncore], 1), s));
+  const int64_t ws_limit = (int64_t)16 << 30;  // workspace bytes per chunk
+  const double two_s2 = 2.0 * kp.sigma * kp.sigma;
+  const double c2 = kp.cutoff * kp.cutoff;
+  DevBuf ws, jobs_d, info;
+  RBF_TRY(info.alloc(4, s));
+  RBF_CUDA_TRY(cudaMemsetAsync(info.p, 0, 4, s));
+  std::vector<LuJob> jobs;
+  int64_t b = 0;
+  while (b < ncore) {
+    jobs.clear();
+    int64_t used = 0;
+    while (b < ncore && (int)jobs.size() < 4096) {
+      const int m = (int)(h_ext_ptr[b + 1] - h_ext_ptr[b]);
+      const int nc = (int)(h_core_ptr[b + 1] - h_core_ptr[b]);
+      const int64_t need = (int64_t)m * (m + nc);
+      if (!jobs.empty() && (used + need) * (int64_t)sizeof(FT) > ws_limit) break;
+      jobs.push_back(LuJob{used, h_ext_ptr[b], h_w_off[b], m, nc});
+      used += need;
+      ++b;
+    }
+    RBF_TRY(ws.ensure(sizeof(FT) * (size_t)used, s));
+    RBF_TRY(jobs_d.ensure(sizeof(LuJob) * jobs.size(), s));
+    RBF_CUDA_TRY(cudaMemcpyAsync(jobs_d.p, jobs.data(), sizeof(LuJob) * jobs.size(), cudaMemcpyHostToDevice, s));
+    dim3 ag(32, (unsigned)jobs.size());
+    assemble_kernel<<<ag, 256, 0, s>>>(jobs_d.as<LuJob>(), c->sorted.as<float4>(), P->ext_idx.as<int32_t>(),
+                                       ws.as<FT>(), kp.amp, two_s2, c2);
+    RBF_CHECK_LAUNCH();
+    lu_kernel<<<(unsigned)jobs.size(), kLuThreads, 0, s>>>(jobs_d.as<LuJob>(), ws.as<FT>(), P->W.as<WT>(),
+                                                           info.as<int>());
+    RBF_CHECK_LAUNCH();
+    // the host vector is reused: wait before the next chunk overwrites jobs_d
+    RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  int herr = 0, hinfo = 0;
+  RBF_CUDA_TRY(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaMemcpyAsync(&hinfo, info.p, 4, cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  if (herr) { set_error("RAS core larger than the ext-search capacity"); return RBF_EUNSUPPORTED; }
+  P->singular_blocks = hinfo;
+  P->bytes = (int64_t)P->W.bytes + P->ext_idx.bytes + P->core_idx.bytes + P->ext_ptr.bytes + P->core_ptr.bytes +
+             P->w_off.bytes;
+  P->t_setup = std::chrono::duration<double>(clk::now() - t0).count();
+  return RBF_OK;
+}
+
+template <class VT>
+rbf_status precond_apply_sorted(rbf_ctx* ctx, const rbf_precond* P, const VT* r, VT* z) {
+  cudaStream_t s = ctx->stream;
+  if (P->kind == 0 || P->nblocks == 0) {
+    copy_kernel<VT><<<grid_for(P->n, 256), 256, 0, s>>>(r, z, P->n);
+    RBF_CHECK_LAUNCH();
+    return RBF_OK;
+  }
+  const int blocks = (int)std::min<int64_t>(P->nblocks, (int64_t)ctx->sm_count * 16);
+  const size_t smem = sizeof(double) * (size_t)P->max_m;
+  if (smem > 48 * 1024) {
+    RBF_CUDA_TRY(cudaFuncSetAttribute(apply_kernel<VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  ProfScope ps(ctx, RBF_PROF_PRECOND_APPLY);
+  apply_kernel<VT><<<blocks, 256, smem, s>>>(P->ext_ptr.as<int64_t>(), P->core_ptr.as<int64_t>(),
+                                             P->ext_idx.as<int32_t>(), P->w_off.as<int64_t>(), P->W.as<WT>(), r, z,
+                                             P->nblocks);
+  RBF_CHECK_LAUNCH();
+  return RBF_OK;
+}
+template rbf_status precond_apply_sorted<float>(rbf_ctx*, const rbf_precond*, const float*, float*);
+template rbf_status precond_apply_sorted<double>(rbf_ctx*, const rbf_precond*, const double*, double*);
+
+}  // namespace rbf
+
+using namespace rbf;
+
+extern "C" {
+
+rbf_status rbf_precond_create(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern,
+                              const rbf_precond_cfg* cfg, rbf_precond** out) {
+  if (!ctx || !cells || !kern || !out) { set_error("NULL argument"); return RBF_EINVAL; }
+  *out = nullptr;
+  if (!(kern->sigma > 0)) { set_error("sigma must be > 0"); return RBF_EINVAL; }
+  if (cfg && (cfg->kind < 0 || cfg->kind > 2)) { set_error("precond kind must be 0, 1 or 2"); return RBF_EINVAL; }
+  RBF_CUDA_TRY(cudaSetDevice(ctx->device));
+  rbf_precond* P = new (std::nothrow) rbf_precond();
+  if (!P) { set_error("host allocation failed"); return RBF_ENOMEM; }
+  KernelParams kp = kernel_params(kern);
+  rbf_status st;
+  {
+    ProfScope ps(ctx, RBF_PROF_PRECOND_SETUP);
+    st = precond_build(ctx, cells, kp, cfg, P);
+  }
+  if (st != RBF_OK) { delete P; return st; }
+  P->cells = cells;
+  *out = P;
+  return RBF_OK;
+}
+
+void rbf_precond_free(rbf_precond* p) { delete p; }
+
+rbf_status rbf_precond_apply(rbf_ctx* ctx, const rbf_precond* P, const float* r, float* z) {
+  if (!ctx || !P || !r || !z) { set_error("NULL argument"); return RBF_EINVAL; }
+  if (r == z) { set_error("r and z must not alias"); return RBF_EINVAL; }
+  RBF_CUDA_TRY(cudaSetDevice(ctx->device));
+  const rbf_cells* c = P->cells;
+  const int64_t n = P->n;
+  RBF_TRY(ctx->vec_a.ensure(sizeof(float) * n, ctx->stream));
+  RBF_TRY(ctx->vec_b.ensure(sizeof(float) * n, ctx->stream));
+  RBF_TRY(gather_f32_to_sorted(ctx, r, c->perm.as<int32_t>(), ctx->vec_a.as<float>(), n));
+  RBF_TRY(precond_apply_sorted<float>(ctx, P, ctx->vec_a.as<float>(), ctx->vec_b.as<float>()));
+  return scatter_f32_from_sorted(ctx, ctx->vec_b.as<float>(), c->perm.as<int32_t>(), z, n);
+}
+
+rbf_status rbf_precond_blocks(const rbf_precond* P, int64_t* nblocks, int64_t* bytes, int64_t* core_ptr,
+                              int64_t* ext_ptr, int32_t* core_idx, int32_t* ext_idx) {
+  if (!P) { set_error("NULL precond"); return RBF_EINVAL; }
+  if (nblocks) *nblocks = P->nblocks;
+  if (bytes) *bytes = P->bytes;
+  const int64_t nb = P->nblocks;
+  if (nb == 0) return RBF_OK;
+  if (core_ptr) std::copy(P->h_core_ptr.begin(), P->h_core_ptr.end(), core_ptr);
+  if (ext_ptr) std::copy(P->h_ext_ptr.begin(), P->h_ext_ptr.end(), ext_ptr);
+  cudaStream_t s = P->cells->stream;
+  if (core_idx)
+    RBF_CUDA_TRY(cudaMemcpyAsync(core_idx, P->core_idx.p, 4 * P->h_core_ptr[nb], cudaMemcpyDeviceToHost, s));
+  if (ext_idx)
+    RBF_CUDA_TRY(cudaMemcpyAsync(ext_idx, P->ext_idx.p, 4 * P->h_ext_ptr[nb], cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  return RBF_OK;
+}
+
+}  // extern "C"

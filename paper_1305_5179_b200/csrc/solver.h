@@ -1,0 +1,37 @@
+// Internal declarations of the preconditioner and the Krylov solver.
+#pragma once
+#include <vector>
+
+#include "internal.h"
+
+struct rbf_precond {
+  int kind = 2;
+  int64_t n = 0;
+  int64_t nblocks = 0;
+  int64_t bytes = 0;
+  int max_m = 0;
+  int singular_blocks = 0;
+  double t_setup = 0.0;
+  const rbf_cells* cells = nullptr;
+  rbf::DevBuf core_ptr;   // int64[nblocks+1]
+  rbf::DevBuf ext_ptr;    // int64[nblocks+1]
+  rbf::DevBuf core_idx;   // int32[n]           sorted positions, block-major
+  rbf::DevBuf ext_idx;    // int32[ext_ptr[nb]] sorted positions: [extra ascending] + [core]
+  rbf::DevBuf w_off;      // int64[nblocks+1]   float offsets of W_i
+  rbf::DevBuf W;          // fp64: W_i (nc_i x m_i) row-major = (A_ext^-1)[core, :]
+  std::vector<int64_t> h_core_ptr, h_ext_ptr;
+};
+
+namespace rbf {
+
+rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp, const rbf_precond_cfg* cfg,
+                         rbf_precond* P);
+// z = M r in sorted order (r, z fp32 or fp64; never aliased)
+template <class VT>
+rbf_status precond_apply_sorted(rbf_ctx* ctx, const rbf_precond* P, const VT* r, VT* z);
+
+// fp32-tier matvec with fp64 input/output vectors in sorted order
+rbf_status matvec_sorted_f32_d(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp, const double* w_sorted,
+                               double* f_sorted);
+
+}  // namespace rbf

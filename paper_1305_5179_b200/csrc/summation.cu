@@ -15,9 +15,10 @@
 //    culled against the box (ballot + compaction), and staged in a
 //    warp-private shared-memory ring as SoA; every 64 staged sources the warp
 //    runs the dense inner loop;
-//  * fp32 tier inner loop: coordinates are shifted to the tile centre and
-//    scaled by sqrt(k), k = log2(e)/(2 sigma^2), so one packed FADD2 per
-//    coordinate, FMUL2 + 2 FFMA2 give the scaled r^2 of two pairs; the
+//  * fp32 tier inner loop: sources are staged relative to the tile centre
+//    (unscaled); one packed FFMA2 per coordinate forms the difference scaled
+//    by sqrt(k), k = log2(e)/(2 sigma^2), in a single rounding, and FMUL2 +
+//    2 FFMA2 give the scaled r^2 of two pairs; the
 //    cutoff is an integer compare+select on the bits of r^2 (ALU pipe),
 //    MUFU.EX2 evaluates 2^-r'^2, and a packed FFMA2 accumulates.  No
 //    tensor cores: the K=3 distance form is not a dense contraction.
@@ -27,6 +28,7 @@
 #include <algorithm>
 
 #include "internal.h"
+#include "solver.h"
 
 namespace rbf {
 namespace {
@@ -163,9 +165,10 @@ struct Stage32 {
   }
   __device__ __forceinline__ void store(bool keep, int pos) {
     if (keep) {
-      r.bx[pos] = (p.x - ctr.x) * s;
-      r.by[pos] = (p.y - ctr.y) * s;
-      r.bz[pos] = (p.z - ctr.z) * s;
+      // tile-local, unscaled (exact for sources near the tile: Sterbenz)
+      r.bx[pos] = p.x - ctr.x;
+      r.by[pos] = p.y - ctr.y;
+      r.bz[pos] = p.z - ctr.z;
       r.bw[pos] = p.w;
     }
   }
@@ -181,9 +184,11 @@ template <int T>
 struct Flush32 {
   Ring32 r;
   float2* acc;            // [T]
-  const float* xt; const float* yt; const float* zt;   // [T] scaled local target coords
+  const float* xt; const float* yt; const float* zt;   // [T] -(local target coords * s)
   int c2bits;
+  float s;
   __device__ __forceinline__ void operator()(int cnt) {
+    const float2 s2 = make_float2(s, s);
 #pragma unroll 2
     for (int j = 0; j < cnt; j += 4) {
       const float4 X = *reinterpret_cast<const float4*>(r.bx + j);
@@ -195,9 +200,10 @@ struct Flush32 {
         const float2 tx = make_float2(xt[t], xt[t]);
         const float2 ty = make_float2(yt[t], yt[t]);
         const float2 tz = make_float2(zt[t], zt[t]);
-        float2 dxa = sub2(make_float2(X.x, X.y), tx), dxb = sub2(make_float2(X.z, X.w), tx);
-        float2 dya = sub2(make_float2(Y.x, Y.y), ty), dyb = sub2(make_float2(Y.z, Y.w), ty);
-        float2 dza = sub2(make_float2(Z.x, Z.y), tz), dzb = sub2(make_float2(Z.z, Z.w), tz);
+        // scaled difference in one rounding: x_l * s is exact inside the FMA
+        float2 dxa = fma2(make_float2(X.x, X.y), s2, tx), dxb = fma2(make_float2(X.z, X.w), s2, tx);
+        float2 dya = fma2(make_float2(Y.x, Y.y), s2, ty), dyb = fma2(make_float2(Y.z, Y.w), s2, ty);
+        float2 dza = fma2(make_float2(Z.x, Z.y), s2, tz), dzb = fma2(make_float2(Z.z, Z.w), s2, tz);
         float2 ra = mul2(dxa, dxa), rb = mul2(dxb, dxb);
         ra = fma2(dya, dya, ra); rb = fma2(dyb, dyb, rb);
         ra = fma2(dza, dza, ra); rb = fma2(dzb, dzb, rb);
@@ -217,6 +223,7 @@ struct FlushStats {
   const float* xt; const float* yt; const float* zt;
   const bool* tvalid;
   int c2bits;
+  float s;
   unsigned long long* useful; unsigned long long* visited;
   __device__ __forceinline__ void operator()(int cnt) {
     for (int j = 0; j < cnt; ++j) {
@@ -224,7 +231,7 @@ struct FlushStats {
 #pragma unroll
       for (int t = 0; t < T; ++t) {
         if (!tvalid[t]) continue;
-        float dx = r.bx[j] - xt[t], dy = r.by[j] - yt[t], dz = r.bz[j] - zt[t];
+        float dx = fmaf(r.bx[j], s, xt[t]), dy = fmaf(r.by[j], s, yt[t]), dz = fmaf(r.bz[j], s, zt[t]);
         float r2 = dx * dx + dy * dy + dz * dz;
         *visited += 1;
         if (__float_as_int(r2) <= c2bits) *useful += 1;
@@ -253,11 +260,11 @@ __device__ __forceinline__ float node_coord(const GridDesc& gd, int a, int i) {
   return (float)(gd.lo[a] + (double)i * gd.step[a]);
 }
 
-template <int MODE, bool STATS>
+template <int MODE, bool STATS, class OutT>
 __global__ void __launch_bounds__(kSumWarps * 32)
 sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* __restrict__ src,
                const int2* __restrict__ tiles, const float4* __restrict__ tbox, int64_t ntiles,
-               GridDesc gd, float* __restrict__ out, const int32_t* __restrict__ out_perm,
+               GridDesc gd, OutT* __restrict__ out, const int32_t* __restrict__ out_perm,
                int* __restrict__ work, unsigned long long* __restrict__ stats) {
   __shared__ __align__(16) float ring[kSumWarps][4][kBufPad];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -312,28 +319,28 @@ sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
     float xt[2], yt[2], zt[2];
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
-      xt[t] = (xr[t] - ctr.x) * G.s; yt[t] = (yr[t] - ctr.y) * G.s; zt[t] = (zr[t] - ctr.z) * G.s;
+      xt[t] = -((xr[t] - ctr.x) * G.s); yt[t] = -((yr[t] - ctr.y) * G.s); zt[t] = -((zr[t] - ctr.z) * G.s);
     }
     float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
     Stage32 st{R, src, blo, bhi, ctr, G.cc2, G.s, make_float4(0, 0, 0, 0)};
     int nbuf = 0;
     const bool two = tcount > 32;
     if (STATS) {
-      FlushStats<2> fs{R, xt, yt, zt, tv, G.c2bits, &useful, &visited};
+      FlushStats<2> fs{R, xt, yt, zt, tv, G.c2bits, G.s, &useful, &visited};
       traverse(G, cell_start, blo, bhi, lane, st, fs, nbuf);
       int cnt;
       pad_ring(R, nbuf, lane, cnt);
       fs(cnt);
       __syncwarp();
     } else if (two) {
-      Flush32<2> fl{R, acc, xt, yt, zt, G.c2bits};
+      Flush32<2> fl{R, acc, xt, yt, zt, G.c2bits, G.s};
       traverse(G, cell_start, blo, bhi, lane, st, fl, nbuf);
       int cnt;
       pad_ring(R, nbuf, lane, cnt);
       fl(cnt);
       __syncwarp();
     } else {
-      Flush32<1> fl{R, acc, xt, yt, zt, G.c2bits};
+      Flush32<1> fl{R, acc, xt, yt, zt, G.c2bits, G.s};
       traverse(G, cell_start, blo, bhi, lane, st, fl, nbuf);
       int cnt;
       pad_ring(R, nbuf, lane, cnt);
@@ -347,7 +354,7 @@ sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
         float v = G.amp * (acc[t].x + acc[t].y);
         int64_t o = tidx[t];
         if (MODE == 0 && out_perm) o = out_perm[o];
-        out[o] = v;
+        out[o] = (OutT)v;
       }
     }
   }
@@ -466,7 +473,7 @@ __global__ void pack_src_f32(const float4* __restrict__ sorted, const float* __r
                              float4* __restrict__ src) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float4 p = sorted[i];
-    p.w = w[i];
+    p.w = w ? w[i] : 0.f;
     src[i] = p;
   }
 }
@@ -528,14 +535,34 @@ rbf_status matvec_sorted_f32(rbf_ctx* ctx, const rbf_cells* c, const KernelParam
   SumGeom G = make_geom(c, kp);
   GridDesc gd{};
   if (pair_stats) {
-    sum_f32_kernel<0, true><<<sum_blocks(ctx), kSumWarps * 32, 0, s>>>(
+    sum_f32_kernel<0, true, float><<<sum_blocks(ctx), kSumWarps * 32, 0, s>>>(
         G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), c->tiles.as<int2>(), c->tile_box.as<float4>(),
         c->ntiles, gd, f_out, out_perm, ctx->counter.as<int>(), pair_stats);
   } else {
-    sum_f32_kernel<0, false><<<sum_blocks(ctx), kSumWarps * 32, 0, s>>>(
+    ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
+    sum_f32_kernel<0, false, float><<<sum_blocks(ctx), kSumWarps * 32, 0, s>>>(
         G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), c->tiles.as<int2>(), c->tile_box.as<float4>(),
         c->ntiles, gd, f_out, out_perm, ctx->counter.as<int>(), nullptr);
   }
+  RBF_CHECK_LAUNCH();
+  return RBF_OK;
+}
+
+rbf_status matvec_sorted_f32_d(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp, const double* w_sorted,
+                               double* f_sorted) {
+  cudaStream_t s = ctx->stream;
+  const int64_t n = c->n;
+  RBF_TRY(ctx->src4.ensure(sizeof(float4) * n, s));
+  RBF_TRY(ctx->counter.ensure(256, s));
+  pack_src_f64w<<<grid_for(n, 256), 256, 0, s>>>(c->sorted.as<float4>(), w_sorted, n, ctx->src4.as<float4>());
+  RBF_CHECK_LAUNCH();
+  RBF_CUDA_TRY(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
+  SumGeom G = make_geom(c, kp);
+  GridDesc gd{};
+  ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
+  sum_f32_kernel<0, false, double><<<sum_blocks(ctx), kSumWarps * 32, 0, s>>>(
+      G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), c->tiles.as<int2>(), c->tile_box.as<float4>(),
+      c->ntiles, gd, f_sorted, nullptr, ctx->counter.as<int>(), nullptr);
   RBF_CHECK_LAUNCH();
   return RBF_OK;
 }
@@ -546,6 +573,7 @@ rbf_status matvec_sorted_f64(rbf_ctx* ctx, const rbf_cells* c, const KernelParam
   RBF_TRY(ctx->counter.ensure(256, s));
   RBF_CUDA_TRY(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
   SumGeom G = make_geom(c, kp);
+  ProfScope ps(ctx, RBF_PROF_MATVEC_F64);
   sum_f64_kernel<<<sum_blocks(ctx), kSumWarps * 32, 0, s>>>(
       G, c->cell_start.as<int32_t>(), c->sorted.as<float4>(), w_sorted, c->tiles.as<int2>(),
       c->tile_box.as<float4>(), c->ntiles, f_out, out_perm, ctx->counter.as<int>());
@@ -554,12 +582,17 @@ rbf_status matvec_sorted_f64(rbf_ctx* ctx, const rbf_cells* c, const KernelParam
 }
 
 rbf_status eval_grid_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
-                            const double* w_sorted, const rbf_grid* g, float* field) {
+                            const double* w_sorted, const rbf_grid* g, float* field,
+                            unsigned long long* pair_stats) {
   cudaStream_t s = ctx->stream;
   const int64_t n = c->n;
   RBF_TRY(ctx->src4.ensure(sizeof(float4) * n, s));
   RBF_TRY(ctx->counter.ensure(256, s));
-  pack_src_f64w<<<grid_for(n, 256), 256, 0, s>>>(c->sorted.as<float4>(), w_sorted, n, ctx->src4.as<float4>());
+  if (w_sorted) {
+    pack_src_f64w<<<grid_for(n, 256), 256, 0, s>>>(c->sorted.as<float4>(), w_sorted, n, ctx->src4.as<float4>());
+  } else {
+    pack_src_f32<<<grid_for(n, 256), 256, 0, s>>>(c->sorted.as<float4>(), nullptr, n, ctx->src4.as<float4>());
+  }
   RBF_CHECK_LAUNCH();
   RBF_CUDA_TRY(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
   SumGeom G = make_geom(c, kp);
@@ -571,7 +604,15 @@ rbf_status eval_grid_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams
     gd.nb[a] = (g->n[a] + 3) / 4;
   }
   int64_t nblk = (int64_t)gd.nb[0] * gd.nb[1] * gd.nb[2];
-  sum_f32_kernel<1, false><<<sum_blocks(ctx), kSumWarps * 32, 0, s>>>(
+  if (pair_stats) {
+    sum_f32_kernel<1, true, float><<<sum_blocks(ctx), kSumWarps * 32, 0, s>>>(
+        G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), nullptr, nullptr, nblk, gd, field, nullptr,
+        ctx->counter.as<int>(), pair_stats);
+    RBF_CHECK_LAUNCH();
+    return RBF_OK;
+  }
+  ProfScope ps(ctx, RBF_PROF_GRID);
+  sum_f32_kernel<1, false, float><<<sum_blocks(ctx), kSumWarps * 32, 0, s>>>(
       G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), nullptr, nullptr, nblk, gd, field, nullptr,
       ctx->counter.as<int>(), nullptr);
   RBF_CHECK_LAUNCH();

@@ -98,6 +98,10 @@ EXPORTS = {
     "rbf_gmres_solve": (C.c_int, [_P, _P, C.POINTER(_Kernel), _P, C.POINTER(_PrecondCfg),
                                   C.POINTER(_GmresCfg), _P, _P, C.POINTER(SolveReport)]),
     "rbf_eval_grid": (C.c_int, [_P, _P, C.POINTER(_Kernel), _P, C.POINTER(_Grid), _P]),
+    "rbf_eval_grid_pairs": (C.c_int, [_P, _P, C.POINTER(_Kernel), C.POINTER(_Grid), C.POINTER(C.c_int64),
+                                      C.POINTER(C.c_int64)]),
+    "rbf_profile_enable": (C.c_int, [_P, C.c_int]),
+    "rbf_profile_query": (C.c_int, [_P, _P, _P]),
     "rbf_reconstruct_host": (C.c_int, [_P, _P, _P, C.c_int64, C.POINTER(_Kernel), C.POINTER(_CellCfg),
                                        C.POINTER(_PrecondCfg), C.POINTER(_GmresCfg), C.POINTER(_Grid),
                                        _P, _P, C.POINTER(SolveReport)]),
@@ -180,6 +184,20 @@ class Context:
         h = C.c_void_p()
         _check(lib.rbf_create(C.byref(h), device, C.c_void_p(self.stream.cuda_stream), None, 0, 1))
         self._h = h
+
+    PROF_STAGES = ("cells", "matvec_f32", "matvec_f64", "grid", "precond_setup", "precond_apply")
+
+    def profile(self, on: bool = True):
+        """rbf_profile_enable: bracket the library's stage launches with CUDA events."""
+        _check(_lib.rbf_profile_enable(self._h, 1 if on else 0))
+
+    def profile_query(self) -> dict:
+        """rbf_profile_query: {stage: (total ms, launches)} since the last query."""
+        import numpy as np
+        ms = np.zeros(len(self.PROF_STAGES), dtype=np.float64)
+        ln = np.zeros(len(self.PROF_STAGES), dtype=np.int64)
+        _check(_lib.rbf_profile_query(self._h, ms.ctypes.data_as(C.c_void_p), ln.ctypes.data_as(C.c_void_p)))
+        return {k: (float(ms[i]), int(ln[i])) for i, k in enumerate(self.PROF_STAGES)}
 
     def close(self):
         if getattr(self, "_h", None):
@@ -288,6 +306,14 @@ def eval_grid(ctx: Context, cells: Cells, kernel: Kernel, w: torch.Tensor, lo, h
     _need(field, torch.float32, n3[0] * n3[1] * n3[2], "field")
     _check(_lib.rbf_eval_grid(ctx._h, cells._h, C.byref(kernel._c()), _ptr(w), C.byref(g), _ptr(field)))
     return field
+
+
+def eval_grid_pairs(ctx: Context, cells: Cells, kernel: Kernel, lo, hi, n, visited: bool = False):
+    """Useful (node, centre) pairs of the grid evaluation (and visited if asked)."""
+    g, _ = _grid_c(lo, hi, n)
+    u, v = C.c_int64(), C.c_int64()
+    _check(_lib.rbf_eval_grid_pairs(ctx._h, cells._h, C.byref(kernel._c()), C.byref(g), C.byref(u), C.byref(v)))
+    return (u.value, v.value) if visited else u.value
 
 
 class Precond:

@@ -1,0 +1,221 @@
+"""GPU parity of the solve (a4-a7 of SURVEY.md §8(a)) against the CPU oracle.
+
+* RAS block structure (integer work): bit-identical to oracle.solve.ras_blocks
+  on the same cells (reading R8);
+* RAS apply z = M r: fp32 factors vs the oracle's fp64 LU, on a well-conditioned
+  problem (relative error <= 1e-3: fp32 LU, block condition numbers <= ~1e3);
+* GMRES: the gate is the TRUE residual ||b - A w|| / ||b|| computed by the
+  ORACLE's fp64 brute-force matvec (reading R7): c1 to 1e-8 (BASELINE configs[0])
+  and c2 to 1e-6; weights agree with the dense LU up to the conditioning bound;
+* the grid of the GPU solution reconstructs the unit sphere (reading R11).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import cells as OC
+from oracle import extend as OE
+from oracle import grid as OG
+from oracle import kernel as OK
+from oracle import solve as OS
+from synth import make_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def R():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device (no CPU fallback)"
+    import paper_1305_5179_b200 as R
+    R.load_library()
+    return R
+
+
+@pytest.fixture(scope="module")
+def ctx(R):
+    return R.Context(0)
+
+
+def dev(a, dtype):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype, device="cuda")
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def problem(name, **kw):
+    """Inputs of config `name`; b is the fp32 right-hand side the C-ABI takes,
+    promoted to fp64 (the system both sides solve)."""
+    d = make_inputs(name, **kw)
+    X = OE.extend(d["x"], d["normals"], d["delta"])
+    b = OE.labels(len(d["x"]), d["delta"]).astype(np.float32).astype(np.float64)
+    return d, X, b
+
+
+@pytest.mark.parametrize("name,n,core,ov", [("c1", None, 512, 3.0), ("c2", 3000, 512, 1.3),
+                                           ("c2", 3000, 128, 1.0), ("c1", None, 300, 0.0)])
+def test_ras_blocks_bit_exact(R, ctx, name, n, core, ov):
+    d, X, _ = problem(name, n=n)
+    sigma = d["sigma"]
+    h = 6 * sigma / 3.999
+    kern = R.Kernel(sigma)
+    cells = R.Cells(ctx, dev(X, torch.float32), kern, cell_edge=h)
+    P = R.Precond(ctx, cells, kern, kind=2 if ov > 0 else 1, core_target=core, overlap_sigmas=ov)
+    cores, exts, nbytes = P.blocks()
+    ref = OS.ras_blocks(OC.build(X, 6 * sigma, cell_edge=h), sigma, core, ov)
+    assert len(cores) == len(ref)
+    for k, blk in enumerate(ref):
+        assert np.array_equal(cores[k], blk["core"]), k
+        assert np.array_equal(exts[k], blk["ext"]), k
+    assert nbytes > 0
+
+
+def test_ras_apply_parity(R, ctx):
+    rng = np.random.default_rng(3)
+    X = rng.uniform(-1, 1, (6000, 3)).astype(np.float32)
+    sigma = 0.04
+    kern = R.Kernel(sigma)
+    h = 6 * sigma / 3.999
+    cells = R.Cells(ctx, dev(X, torch.float32), kern, cell_edge=h)
+    P = R.Precond(ctx, cells, kern, core_target=256, overlap_sigmas=2.0)
+    r = rng.normal(size=6000).astype(np.float32)
+    z = host(P.apply(dev(r, torch.float32)))
+    oc = OC.build(X, 6 * sigma, cell_edge=h)
+    blocks = OS.ras_blocks(oc, sigma, 256, 2.0)
+    perm = oc["perm"]
+    zs = OS.ras_apply(blocks, oc["sorted"], r.astype(np.float64)[perm], sigma)
+    zref = np.empty_like(zs)
+    zref[perm] = zs
+    err = np.linalg.norm(z - zref) / np.linalg.norm(zref)
+    assert err <= 1e-3, err
+
+
+def test_precond_none_and_jacobi_are_valid(R, ctx):
+    d, X, b = problem("c1")
+    kern = R.Kernel(d["sigma"])
+    cells = R.Cells(ctx, dev(X, torch.float32), kern)
+    P0 = R.Precond(ctx, cells, kern, kind=0)
+    r = dev(np.random.default_rng(1).normal(size=len(X)), torch.float32)
+    assert torch.equal(P0.apply(r), r)                      # M = I
+    P1 = R.Precond(ctx, cells, kern, kind=1, core_target=512)
+    cores, exts, _ = P1.blocks()
+    assert all(np.array_equal(c, e) for c, e in zip(cores, exts))   # no overlap
+    with pytest.raises(R.RbfError):
+        R.Precond(ctx, cells, kern, kind=7)
+
+
+@pytest.fixture(scope="module")
+def c1_solution(R, ctx):
+    d, X, b = problem("c1")
+    sigma = d["sigma"]
+    kern = R.Kernel(sigma)
+    cells = R.Cells(ctx, dev(X, torch.float32), kern)
+    w, rep = R.gmres_solve(ctx, cells, kern, dev(b, torch.float32), restart=30, rtol=1e-8,
+                           core_target=512, overlap_sigmas=3.0)
+    return dict(d=d, X=X, b=b, w=host(w), rep=rep, cells=cells, kern=kern)
+
+
+def test_gmres_c1_true_residual_and_lu(c1_solution):
+    s = c1_solution
+    X, b, w, sigma = s["X"], s["b"], s["w"], s["d"]["sigma"]
+    rep = s["rep"]
+    assert rep["converged"] == 1, rep
+    res = np.linalg.norm(b - OK.matvec(X, w, sigma)) / np.linalg.norm(b)
+    assert res <= 1e-8 * 1.5, (res, rep)                      # oracle's own fp64 operator
+    assert abs(res - rep["rel_residual_true"]) <= 1e-9        # GPU fp64 tier agrees
+    w_lu = OS.lu_solve(X, b, sigma)
+    # kappa(A) ~ 2.2e7: weights agree to ~kappa * residual
+    assert np.linalg.norm(w - w_lu) / np.linalg.norm(w_lu) < 1e-2
+    assert rep["iters_phase1"] + rep["iters_phase2"] < 100
+
+
+def test_gmres_c1_sphere_zero_set(R, ctx, c1_solution):
+    s = c1_solution
+    d = s["d"]
+    sigma = d["sigma"]
+    F = host(R.eval_grid(ctx, s["cells"], s["kern"], dev(s["w"], torch.float64), d["grid_lo"], d["grid_hi"],
+                         d["grid_n"])).ravel()
+    Fr = OG.evaluate(s["X"], s["w"], sigma, d["grid_lo"], d["grid_hi"], d["grid_n"])
+    assert np.abs(F - Fr).max() <= 1e-3 * np.abs(s["b"]).max()
+    pts = OG.zero_crossings(F, d["grid_lo"], d["grid_hi"], d["grid_n"], d["x"], 2 * sigma)
+    assert len(pts) > 1000
+    assert np.abs(np.linalg.norm(pts, axis=1) - 1.0).max() <= 5e-3
+
+
+def test_gmres_torus_well_posed_to_1e6(R, ctx):
+    """c2's geometry (noisy torus) at sigma/spacing 0.78 (N=3000 surface points,
+    9000 centres, several RAS blocks), where the truncated operator is still
+    positive definite: the two-phase solve reaches the 1e-6 gate, certified by
+    the ORACLE's fp64 matvec on sampled rows (reading R13)."""
+    d, X, b = problem("c2", n=3000)
+    sigma = d["sigma"]
+    kern = R.Kernel(sigma)
+    cells = R.Cells(ctx, dev(X, torch.float32), kern)
+    w, rep = R.gmres_solve(ctx, cells, kern, dev(b, torch.float32), restart=50, rtol=1e-6,
+                           core_target=512, overlap_sigmas=1.3, max_iters=400)
+    w = host(w)
+    assert rep["converged"] == 1 and rep["rel_residual_true"] <= 1e-6, rep
+    assert rep["nblocks"] > 10
+    res = np.linalg.norm(b - OK.matvec(X, w, sigma)) / np.linalg.norm(b)
+    assert res <= 1.5e-6 and abs(res - rep["rel_residual_true"]) <= 1e-7, (res, rep)
+    # interpolation audit at the data sites: ||r||_inf <= ||r||_2 <= 1e-6 ||b||_2
+    r = b - OK.matvec(X, w, sigma)
+    assert np.abs(r).max() <= 1.5e-6 * np.linalg.norm(b)
+
+
+def test_gmres_c2_ill_posed_budget(R, ctx):
+    """Full c2 (sigma/spacing 1.9): the 6-sigma-truncated operator is indefinite
+    (oracle pin: tests/test_oracle_solve.py::test_truncated_operator_indefinite_at_high_ratio)
+    and the 1e-6 gate is unattainable (DESIGN.md finding F1).  The solver must
+    stop inside its budget, report converged=0, and report the TRUE residual,
+    which the oracle's sampled rows confirm."""
+    d, X, b = problem("c2")
+    sigma = d["sigma"]
+    kern = R.Kernel(sigma)
+    cells = R.Cells(ctx, dev(X, torch.float32), kern)
+    w, rep = R.gmres_solve(ctx, cells, kern, dev(b, torch.float32), restart=50, rtol=1e-6,
+                           core_target=512, overlap_sigmas=1.3, max_iters=100)
+    w = host(w)
+    assert rep["iters_phase1"] + rep["iters_phase2"] <= 100
+    assert rep["converged"] == 0 and 0 < rep["rel_residual_true"] <= 1.0, rep
+    rows = np.sort(np.random.default_rng(2).choice(len(X), 4000, replace=False))
+    r = b[rows] - OK.matvec(X, w, sigma, rows=rows)
+    est = np.sqrt(np.mean(r ** 2)) / np.sqrt(np.mean(b ** 2))   # sampled estimate of the 2-norm ratio
+    assert abs(est - rep["rel_residual_true"]) <= 0.05 * rep["rel_residual_true"] + 1e-9, (est, rep)
+
+
+def test_gmres_edge_cases(R, ctx):
+    sigma = 0.2
+    kern = R.Kernel(sigma)
+    # N = 1 closed form (SPEC S:393 idea): a w = b  =>  w = b sqrt(2 pi) sigma
+    cells = R.Cells(ctx, dev([[0.1, 0.2, 0.3]], torch.float32), kern)
+    w, rep = R.gmres_solve(ctx, cells, kern, dev([0.7], torch.float32), rtol=1e-10)
+    assert host(w)[0] == pytest.approx(float(np.float32(0.7)) * np.sqrt(2 * np.pi) * sigma, rel=1e-12)
+    # b = 0 => w = 0, converged
+    X = np.random.default_rng(0).uniform(-1, 1, (500, 3)).astype(np.float32)
+    cells = R.Cells(ctx, dev(X, torch.float32), kern)
+    w, rep = R.gmres_solve(ctx, cells, kern, dev(np.zeros(500), torch.float32))
+    assert rep["converged"] == 1 and not host(w).any()
+    # one RAS block holding everything = exact solve: one iteration per phase
+    b = np.random.default_rng(1).normal(size=500)
+    w, rep = R.gmres_solve(ctx, cells, kern, dev(b, torch.float32), core_target=100000, overlap_sigmas=1.0,
+                           rtol=1e-8)
+    assert rep["nblocks"] == 1 and rep["converged"] == 1
+    assert rep["iters_phase1"] + rep["iters_phase2"] <= 6
+    res = np.linalg.norm(b.astype(np.float32) - OK.matvec(X, host(w), sigma)) / np.linalg.norm(b)
+    assert res <= 1e-8 * 1.5
+
+
+def test_reconstruct_host_matches_device_path(R, ctx, c1_solution):
+    s = c1_solution
+    d = s["d"]
+    w, F, rep = R.reconstruct_host(ctx, s["X"], s["b"].astype(np.float32), s["kern"], d["grid_lo"], d["grid_hi"],
+                                   d["grid_n"], restart=30, rtol=1e-8, overlap_sigmas=3.0)
+    w = w.numpy()
+    assert rep["converged"] == 1
+    np.testing.assert_array_equal(w, s["w"])                  # deterministic: same kernels, same order
+    Fd = host(R.eval_grid(ctx, s["cells"], s["kern"], dev(s["w"], torch.float64), d["grid_lo"], d["grid_hi"],
+                          d["grid_n"]))
+    np.testing.assert_array_equal(F.numpy(), Fd)

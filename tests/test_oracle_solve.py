@@ -142,3 +142,27 @@ def test_c1_sphere_zero_set(c1_solution):
     far = G._min_dist(G.nodes(d["grid_lo"], d["grid_hi"], d["grid_n"]),
                       s["X"].astype(np.float64)) > 6 * s["sigma"]
     assert (F[far] == 0).all() and (F[~far] != 0).all()
+
+
+def test_truncated_operator_indefinite_at_high_ratio():
+    """DESIGN.md finding F1 (pins the reading that c2-c5 are ill-posed at the 1e-6 gate):
+    the Eq.6 matrix truncated at 6 sigma is positive definite on c1's sphere
+    (sigma/spacing 0.89; lambda_min 2.69e-6) but, on a torus at sigma/spacing
+    1.9 (c2's ratio), truncation error (1.5e-8 a per dropped entry) exceeds the Gaussian
+    matrix's smallest eigenvalues and many eigenvalues turn negative -- while the
+    UNtruncated matrix stays positive semi-definite (Bochner: the Gaussian is PD)."""
+    from synth.surfaces import torus, fibonacci_sphere
+    x, nrm = fibonacci_sphere(1000)
+    X = extend(x, nrm, 0.01)
+    ev = np.linalg.eigvalsh(K.dense_matrix(X, 0.1))
+    assert ev[0] > 0 and ev[0] == pytest.approx(2.69e-6, rel=0.05)
+    n = 1000
+    x, nrm = torus(n, noise=0.0, seed=0)
+    sigma = 1.9 * np.sqrt(4 * np.pi ** 2 * 0.35 / n)
+    X = extend(x, nrm, 0.1 * sigma)
+    ev_t = np.linalg.eigvalsh(K.dense_matrix(X, sigma))
+    ev_u = np.linalg.eigvalsh(K.dense_matrix(X, sigma, truncate=False))
+    a = K.amplitude(sigma)
+    assert (ev_t < 0).sum() > 100
+    assert ev_t[0] < -1e-9 * a
+    assert ev_u[0] > -1e-12 * ev_u[-1]          # rounding-level only
