@@ -112,6 +112,7 @@ def make_problem(cfg_name: str, seed: int):
 def run_ours(args, rank, world, local):
     import torch
     import paper_1305_5179_b200 as R
+    from paper_1305_5179_b200.dist import throughput
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -173,16 +174,7 @@ def run_ours(args, rank, world, local):
     mv32 = sum(r["matvecs_f32"] for r in reps)
     mv64 = sum(r["matvecs_f64"] for r in reps)
     pairs_rank = useful_mv * (mv32 + mv64) + useful_grid * args.steps
-    if world > 1:
-        t = torch.tensor([ms, pairs_rank], dtype=torch.float64, device=dev)
-        tmax = t.clone()
-        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
-        tsum = t.clone()
-        torch.distributed.all_reduce(tsum, op=torch.distributed.ReduceOp.SUM)
-        ms_max, pairs_all = float(tmax[0]), float(tsum[1])
-    else:
-        ms_max, pairs_all = ms, float(pairs_rank)
-    value = pairs_all / (ms_max * 1e-3)
+    ms_max, pairs_all, value = throughput(ms, pairs_rank, dev)
 
     # e2e through the C-ABI with HOST buffers (rank-local problem)
     e2e = None
@@ -207,14 +199,8 @@ def run_ours(args, rank, world, local):
         torch.cuda.synchronize()
         te = (time.perf_counter() - t0) * 1e3
         pe = useful_mv * mv_e2e + useful_grid * args.steps
-        if world > 1:
-            t = torch.tensor([te, pe], dtype=torch.float64, device=dev)
-            tm = t.clone()
-            torch.distributed.all_reduce(tm, op=torch.distributed.ReduceOp.MAX)
-            ts = t.clone()
-            torch.distributed.all_reduce(ts, op=torch.distributed.ReduceOp.SUM)
-            te, pe = float(tm[0]), float(ts[1])
-        e2e = {"value": pe / (te * 1e-3), "unit": "pairs/s", "ms_per_step": te / args.steps,
+        te, pe, ve = throughput(te, pe, dev)
+        e2e = {"value": ve, "unit": "pairs/s", "ms_per_step": te / args.steps,
                "h2d_bytes_per_step": int(xyz_h.numel() * 4 + b_h.numel() * 4),
                "d2h_bytes_per_step": int(w_h.numel() * 8 + f_h.numel() * 4)}
 

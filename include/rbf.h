@@ -80,6 +80,8 @@ typedef struct {
                             per cutoff with a rounding margin) */
   int tile_cap;          /* targets per warp tile, 32 or 64; <= 0 => 64 */
   int tile_span;         /* max cells a tile spans along x; <= 0 => 2 */
+  int tile_mode;         /* 0 => full cap-sized chunks of cell runs (default),
+                            1 => whole cells merged greedily */
 } rbf_cell_cfg;
 
 /* RAS preconditioner (§3.1; reading R8). */

@@ -240,19 +240,46 @@ __global__ void gather_sorted(const float* __restrict__ xyz, const int32_t* __re
 }
 
 // ------------------------------------------------------------ tiles ---------
-// Greedy per cell row (fixed y,z): consecutive non-empty cells along x are
-// merged into one tile while it holds <= cap targets and spans < span cells;
-// cells holding more than cap targets are cut into cap-sized chunks.  Tiles
-// never cross rows, so a tile's targets are a contiguous sorted range.
+// Per cell row (fixed y,z); tiles never cross rows, so a tile's targets are a
+// contiguous sorted range.
+//  mode 0 (runs, default): a run of adjacent non-empty cells along x is cut into
+//    chunks of exactly `cap` targets (a chunk may straddle a cell face); a chunk
+//    is closed early at a gap (empty cell) or when it would span `span` cells.
+//    Full chunks keep both target slots of every lane busy.
+//  mode 1 (cells): consecutive non-empty cells are merged while the tile holds
+//    <= cap targets and spans < span cells; big cells are cut into cap chunks.
 template <bool kEmit>
 __device__ int64_t plan_row(const int32_t* __restrict__ start, int dimx, int64_t rowbase, int cap,
-                            int span, int2* __restrict__ out) {
+                            int span, int mode, int2* __restrict__ out) {
   int64_t cnt = 0;
   int cur_s = 0, cur_n = 0, cur_x0 = 0;
   auto emit = [&](int s, int m) {
     if (kEmit) out[cnt] = make_int2(s, m);
     ++cnt;
   };
+  if (mode == 0) {
+    int last_x = -2;
+    for (int x = 0; x < dimx; ++x) {
+      const int s = start[rowbase + x];
+      const int m = start[rowbase + x + 1] - s;
+      if (m == 0) continue;
+      if (cur_n > 0 && (x != last_x + 1 || x - cur_x0 >= span)) {
+        emit(cur_s, cur_n);
+        cur_n = 0;
+      }
+      int off = 0;
+      while (off < m) {
+        if (cur_n == 0) { cur_s = s + off; cur_x0 = x; }
+        const int take = min(cap - cur_n, m - off);
+        cur_n += take;
+        off += take;
+        if (cur_n == cap) { emit(cur_s, cur_n); cur_n = 0; }
+      }
+      last_x = x;
+    }
+    if (cur_n > 0) emit(cur_s, cur_n);
+    return cnt;
+  }
   for (int x = 0; x < dimx; ++x) {
     int s = start[rowbase + x];
     int m = start[rowbase + x + 1] - s;
@@ -274,20 +301,20 @@ __device__ int64_t plan_row(const int32_t* __restrict__ start, int dimx, int64_t
   return cnt;
 }
 
-__global__ void plan_count(const int32_t* __restrict__ start, CellGrid g, int cap, int span,
+__global__ void plan_count(const int32_t* __restrict__ start, CellGrid g, int cap, int span, int mode,
                            uint32_t* __restrict__ row_counts) {
   int64_t rows = (int64_t)g.dim[1] * g.dim[2];
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
        r += (int64_t)gridDim.x * blockDim.x)
-    row_counts[r] = (uint32_t)plan_row<false>(start, g.dim[0], r * g.dim[0], cap, span, nullptr);
+    row_counts[r] = (uint32_t)plan_row<false>(start, g.dim[0], r * g.dim[0], cap, span, mode, nullptr);
 }
 
-__global__ void plan_emit(const int32_t* __restrict__ start, CellGrid g, int cap, int span,
+__global__ void plan_emit(const int32_t* __restrict__ start, CellGrid g, int cap, int span, int mode,
                           const uint32_t* __restrict__ row_off, int2* __restrict__ tiles) {
   int64_t rows = (int64_t)g.dim[1] * g.dim[2];
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
        r += (int64_t)gridDim.x * blockDim.x)
-    plan_row<true>(start, g.dim[0], r * g.dim[0], cap, span, tiles + row_off[r]);
+    plan_row<true>(start, g.dim[0], r * g.dim[0], cap, span, mode, tiles + row_off[r]);
 }
 
 // One warp per tile: axis-aligned bounding box of its targets.
@@ -390,6 +417,8 @@ rbf_status build_cells(rbf_ctx* ctx, const float* xyz, int64_t n, const rbf_kern
   double h = (cfg && cfg->cell_edge > 0) ? cfg->cell_edge : cutoff / 3.999;
   int cap = (cfg && cfg->tile_cap > 0) ? cfg->tile_cap : 64;
   int span = (cfg && cfg->tile_span > 0) ? cfg->tile_span : 2;
+  const int mode = cfg ? cfg->tile_mode : 0;
+  if (mode != 0 && mode != 1) { set_error("tile_mode must be 0 or 1"); return RBF_EINVAL; }
   if (cap != 32 && cap != 64) { set_error("tile_cap must be 32 or 64"); return RBF_EINVAL; }
   c->n = n;
   c->stream = s;
@@ -475,7 +504,8 @@ rbf_status build_cells(rbf_ctx* ctx, const float* xyz, int64_t n, const rbf_kern
   RBF_TRY(rc.alloc(sizeof(uint32_t) * rows, s));
   RBF_TRY(ro.alloc(sizeof(uint32_t) * rows, s));
   RBF_TRY(tot.alloc(sizeof(uint32_t) * 2, s));
-  plan_count<<<grid_for(rows, 128), 128, 0, s>>>(c->cell_start.as<int32_t>(), g, cap, span, rc.as<uint32_t>());
+  plan_count<<<grid_for(rows, 128), 128, 0, s>>>(c->cell_start.as<int32_t>(), g, cap, span, mode,
+                                                 rc.as<uint32_t>());
   RBF_CHECK_LAUNCH();
   RBF_TRY(exclusive_scan_u32(ctx, rc.as<uint32_t>(), ro.as<uint32_t>(), rows, tot.as<uint32_t>()));
   uint32_t ntiles = 0;
@@ -487,7 +517,7 @@ rbf_status build_cells(rbf_ctx* ctx, const float* xyz, int64_t n, const rbf_kern
   c->nonempty = (int64_t)nonempty;
   RBF_TRY(c->tiles.alloc(sizeof(int2) * (size_t)std::max<uint32_t>(ntiles, 1), s));
   RBF_TRY(c->tile_box.alloc(sizeof(float4) * 2 * (size_t)std::max<uint32_t>(ntiles, 1), s));
-  plan_emit<<<grid_for(rows, 128), 128, 0, s>>>(c->cell_start.as<int32_t>(), g, cap, span,
+  plan_emit<<<grid_for(rows, 128), 128, 0, s>>>(c->cell_start.as<int32_t>(), g, cap, span, mode,
                                                 ro.as<uint32_t>(), c->tiles.as<int2>());
   RBF_CHECK_LAUNCH();
   if (ntiles > 0) {

@@ -1,0 +1,513 @@
+// a4 of SURVEY.md §8(a): batched fp64 LU with partial pivoting of the RAS
+// extended blocks, fused with the solve for the restricted inverse
+// (§3.1: "solving smaller systems" on every subdomain Omega_i).
+//
+// For each block b the workspace holds the augmented matrix [A_ext | E_core]
+// (m x (m + nc), row-major).  Gaussian elimination with partial pivoting turns
+// it into [U | L^-1 P E_core]; blocked back-substitution then gives
+// X = A_ext^-1 E_core and W = X^T = (A_ext^-1)[core, :] (A_ext symmetric).
+//
+// The elimination is driven from the host in steps of kNb = 64 columns so that
+// every kernel has thousands of CTAs (all blocks of a chunk x all tiles):
+//   panel      one thread-block cluster per block: pivoted factorisation of the
+//              (m-k0) x 64 panel held in the cluster's shared memory (DSMEM
+//              pivot search and row exchange); then inv(L11) per block
+//   swap_trsm  (block, 64-column tile): the panel's row swaps on the columns
+//              right of it, then U12 = inv(L11) A12
+//   gemm       (block, 64x64 tile): A22 -= L21 U12 — register-blocked fp64
+//              (4x4 per thread, operands staged in shared memory, K = 64)
+// and the back-substitution in steps of 64 rows from the bottom:
+//   diag_solve (block, 64-column RHS tile): X_k = inv(U_kk) Y_k
+//   gemm       (block, tile): Y[0:k0] -= U[0:k0, k0:k0+64] X_k
+#include <algorithm>
+#include <cmath>
+
+#include <cooperative_groups.h>
+
+#include "internal.h"
+#include "solver.h"
+
+namespace rbf {
+namespace {
+
+constexpr int kNb = 64;
+constexpr int kThreads = 256;
+constexpr int kLd = kNb + 4;   // padded smem row (doubles)
+
+// ------------------------------------------------------------------ panel ---
+// Panel factorisation held on chip: a cluster of CL CTAs per block matrix, CTA
+// `rank` owns panel rows [rank*R, rank*R + R) (relative to k0) in its shared
+// memory.  Per column: local pivot candidates -> cluster barrier -> every CTA
+// reduces the CL candidates through DSMEM (same result everywhere) -> the
+// pivot row and the displaced row are exchanged through DSMEM -> local rank-1
+// update of the owned rows (fused with the next column's candidate search).
+// HBM sees one read and one write of the panel per elimination step.
+constexpr int kPs = kNb + 1;   // smem row stride (doubles) of the cluster panel
+
+__global__ void __launch_bounds__(kThreads)
+panel_cluster_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, int k0, int* __restrict__ piv,
+                     int R, int* __restrict__ info) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank(), CL = (int)cl.num_blocks();
+  const int job = blockIdx.x / CL;
+  extern __shared__ double Pn[];   // R x kPs
+  __shared__ double srow[kNb], tmp[kNb];
+  __shared__ double sv[kThreads / 32];
+  __shared__ int si[kThreads / 32];
+  __shared__ double cand_v;
+  __shared__ int cand_i, s_p;
+  const LuJob J = jobs[job];
+  const int m = J.m, ld = J.m + J.nc;
+  if (k0 >= m) return;                       // uniform over the cluster
+  const int kb = min(kNb, m - k0);
+  double* A = ws + J.ws_off;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int rows = m - k0;
+  const int rb = rank * R;                   // first owned row (relative)
+  const int nl = max(0, min(R, rows - rb));  // owned rows
+  for (int q = tid; q < nl * kb; q += kThreads) {
+    const int lr = q / kb, c = q % kb;
+    Pn[lr * kPs + c] = A[(int64_t)(k0 + rb + lr) * ld + k0 + c];
+  }
+  __syncthreads();
+  int singular = 0;
+  double best = -1.0;
+  int bi = 0x7fffffff;
+  for (int lr = tid; lr < nl; lr += kThreads) {
+    const double v = fabs(Pn[lr * kPs]);
+    if (v > best) { best = v; bi = rb + lr; }
+  }
+  for (int jj = 0; jj < kb; ++jj) {
+    // local candidate (largest |a|, lowest row on ties)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    if (lane == 0) { sv[wid] = best; si[wid] = bi; }
+    __syncthreads();
+    if (tid == 0) {
+      double b2 = sv[0];
+      int i2 = si[0];
+      for (int q = 1; q < kThreads / 32; ++q)
+        if (sv[q] > b2 || (sv[q] == b2 && si[q] < i2)) { b2 = sv[q]; i2 = si[q]; }
+      cand_v = b2;
+      cand_i = i2;
+    }
+    cl.sync();
+    // global pivot: reduce the CL candidates (DSMEM), identically in every CTA
+    if (wid == 0) {
+      double v = -1.0;
+      int i = 0x7fffffff;
+      if (lane < CL) {
+        v = *cl.map_shared_rank(&cand_v, lane);
+        i = *cl.map_shared_rank(&cand_i, lane);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, i, o);
+        if (ov > v || (ov == v && oi < i)) { v = ov; i = oi; }
+      }
+      if (lane == 0) s_p = i;
+    }
+    __syncthreads();
+    const int p = s_p;
+    const int own_p = p / R, own_j = jj / R;
+    if (tid < kb) {
+      srow[tid] = cl.map_shared_rank(Pn, own_p)[(p - own_p * R) * kPs + tid];
+      if (rank == own_p && p != jj) tmp[tid] = cl.map_shared_rank(Pn, own_j)[(jj - own_j * R) * kPs + tid];
+    }
+    cl.sync();                               // all reads of the old rows are done
+    if (tid < kb) {
+      if (rank == own_j) Pn[(jj - rb) * kPs + tid] = srow[tid];
+      if (rank == own_p && p != jj) Pn[(p - rb) * kPs + tid] = tmp[tid];
+    }
+    if (rank == 0 && tid == 0) piv[(int64_t)job * kNb + jj] = k0 + p;
+    __syncthreads();
+    double pv = srow[jj];
+    if (pv == 0.0) { singular = 1; pv = 1e-300; }
+    const double inv = 1.0 / pv;
+    best = -1.0;
+    bi = 0x7fffffff;
+    for (int lr = max(0, jj + 1 - rb) + tid; lr < nl; lr += kThreads) {
+      double* row = Pn + lr * kPs;
+      const double l = row[jj] * inv;
+      row[jj] = l;
+      if (jj + 1 < kb) {
+        const double v1 = fma(-l, srow[jj + 1], row[jj + 1]);
+        row[jj + 1] = v1;
+        if (fabs(v1) > best) { best = fabs(v1); bi = rb + lr; }
+        for (int c = jj + 2; c < kb; ++c) row[c] = fma(-l, srow[c], row[c]);
+      }
+    }
+    __syncthreads();
+  }
+  for (int q = tid; q < nl * kb; q += kThreads) {
+    const int lr = q / kb, c = q % kb;
+    A[(int64_t)(k0 + rb + lr) * ld + k0 + c] = Pn[lr * kPs + c];
+  }
+  if (singular && tid == 0) atomicAdd(info, 1);
+  cl.sync();                                 // keep DSMEM alive until all peers are done
+}
+
+// inv(L11) of every block after its panel (one CTA per block)
+__global__ void __launch_bounds__(kThreads)
+linv_kernel(const LuJob* __restrict__ jobs, const double* __restrict__ ws, int k0, double* __restrict__ linv) {
+  extern __shared__ double sm[];
+  double* sL = sm;                 // kNb x kLd : L11 (unit lower)
+  double* sI = sm + kNb * kLd;     // kNb x kLd : inv(L11)
+  const LuJob J = jobs[blockIdx.x];
+  const int m = J.m, ld = J.m + J.nc;
+  if (k0 >= m) return;
+  const int kb = min(kNb, m - k0);
+  const double* A = ws + J.ws_off;
+  const int tid = threadIdx.x;
+  for (int q = tid; q < kNb * kNb; q += kThreads) {
+    const int r = q / kNb, c = q % kNb;
+    sL[r * kLd + c] = (r < kb && c < kb) ? A[(int64_t)(k0 + r) * ld + k0 + c] : 0.0;
+  }
+  __syncthreads();
+  if (tid < kNb) {
+    const int t = tid;
+    for (int r = 0; r < kNb; ++r) {
+      double x;
+      if (r < t) x = 0.0;
+      else if (r == t) x = 1.0;
+      else {
+        double acc = 0.0;
+        for (int s = t; s < r; ++s) acc = fma(sL[r * kLd + s], sI[s * kLd + t], acc);
+        x = (r < kb) ? -acc : 0.0;
+      }
+      sI[r * kLd + t] = x;
+    }
+  }
+  __syncthreads();
+  double* Li = linv + (int64_t)blockIdx.x * kNb * kNb;
+  for (int q = tid; q < kNb * kNb; q += kThreads) Li[q] = sI[(q / kNb) * kLd + q % kNb];
+}
+
+// ------------------------------------------------------------- swap + trsm --
+__global__ void __launch_bounds__(kThreads)
+swap_trsm_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, int k0, const int* __restrict__ piv,
+                 const double* __restrict__ linv) {
+  extern __shared__ double sm[];
+  double* sI = sm;                 // inv(L11)
+  double* sT = sm + kNb * kLd;     // A12 tile
+  const LuJob J = jobs[blockIdx.x];
+  const int m = J.m, ld = J.m + J.nc;
+  if (k0 >= m) return;
+  const int kb = min(kNb, m - k0);
+  double* A = ws + J.ws_off;
+  const int tid = threadIdx.x;
+  const int* P = piv + (int64_t)blockIdx.x * kNb;
+  const double* Li = linv + (int64_t)blockIdx.x * kNb * kNb;
+  for (int q = tid; q < kNb * kNb; q += kThreads) sI[(q / kNb) * kLd + q % kNb] = Li[q];
+  const int tx = tid & 15, ty = tid >> 4;
+  for (int c0 = k0 + kb + kNb * blockIdx.y; c0 < ld; c0 += kNb * gridDim.y) {
+    const int cw = min(kNb, ld - c0);
+    // row swaps of the panel, in order, on this tile's columns
+    if (tid < cw) {
+      const int c = c0 + tid;
+      for (int jj = 0; jj < kb; ++jj) {
+        const int p = P[jj], j = k0 + jj;
+        if (p != j) {
+          const double t = A[(int64_t)j * ld + c];
+          A[(int64_t)j * ld + c] = A[(int64_t)p * ld + c];
+          A[(int64_t)p * ld + c] = t;
+        }
+      }
+    }
+    __syncthreads();
+    for (int q = tid; q < kNb * kNb; q += kThreads) {
+      const int r = q / kNb, c = q % kNb;
+      sT[r * kLd + c] = (r < kb && c < cw) ? A[(int64_t)(k0 + r) * ld + c0 + c] : 0.0;
+    }
+    __syncthreads();
+    // U12 = inv(L11) * A12 : thread owns rows 4ty.., cols 4tx..
+    double acc[4][4] = {};
+    for (int t = 0; t < kb; ++t) {
+      double a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { a[q] = sI[(4 * ty + q) * kLd + t]; b[q] = sT[t * kLd + 4 * tx + q]; }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int p = 0; p < 4; ++p) acc[q][p] = fma(a[q], b[p], acc[q][p]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = 4 * ty + q;
+      if (r >= kb) continue;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const int c = 4 * tx + p;
+        if (c < cw) A[(int64_t)(k0 + r) * ld + c0 + c] = acc[q][p];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------- gemm ---
+// mode 0 (elimination):       C = A[k0+kb:m, k0+kb:ld]
+// mode 1 (back-substitution): C = A[0:k0, m:ld]
+// C -= A[rows, k0:k0+kb] * A[k0:k0+kb, cols]
+__global__ void __launch_bounds__(kThreads)
+gemm_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, int k0, int mode) {
+  extern __shared__ double sm[];
+  double* sA = sm;                 // [t][i] : kNb x kLd  (A[r0+i][k0+t])
+  double* sB = sm + kNb * kLd;     // [t][j] : kNb x kLd  (A[k0+t][c0+j])
+  const LuJob J = jobs[blockIdx.x];
+  const int m = J.m, ld = J.m + J.nc;
+  if (k0 >= m) return;
+  const int kb = min(kNb, m - k0);
+  int r0, r1, cb0, cb1;
+  if (mode == 0) { r0 = k0 + kb; r1 = m; cb0 = k0 + kb; cb1 = ld; }
+  else { r0 = 0; r1 = k0; cb0 = m; cb1 = ld; }
+  if (r0 >= r1 || cb0 >= cb1) return;
+  const int ntc = (cb1 - cb0 + kNb - 1) / kNb;
+  const int ntr = (r1 - r0 + kNb - 1) / kNb;
+  double* A = ws + J.ws_off;
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  for (int tile = blockIdx.y; tile < ntr * ntc; tile += gridDim.y) {
+    const int tr = r0 + kNb * (tile / ntc);
+    const int tc = cb0 + kNb * (tile % ntc);
+    for (int q = tid; q < kNb * kNb; q += kThreads) {
+      const int i = q / kNb, t = q % kNb;     // consecutive threads: consecutive t (row-contiguous)
+      const int r = tr + i;
+      sA[t * kLd + i] = (r < r1 && t < kb) ? A[(int64_t)r * ld + k0 + t] : 0.0;
+    }
+    for (int q = tid; q < kNb * kNb; q += kThreads) {
+      const int t = q / kNb, j = q % kNb;
+      const int c = tc + j;
+      sB[t * kLd + j] = (c < cb1 && t < kb) ? A[(int64_t)(k0 + t) * ld + c] : 0.0;
+    }
+    __syncthreads();
+    double acc[4][4] = {};
+#pragma unroll 4
+    for (int t = 0; t < kNb; ++t) {
+      const double2 a01 = *reinterpret_cast<const double2*>(sA + t * kLd + 4 * ty);
+      const double2 a23 = *reinterpret_cast<const double2*>(sA + t * kLd + 4 * ty + 2);
+      const double2 b01 = *reinterpret_cast<const double2*>(sB + t * kLd + 4 * tx);
+      const double2 b23 = *reinterpret_cast<const double2*>(sB + t * kLd + 4 * tx + 2);
+      const double a[4] = {a01.x, a01.y, a23.x, a23.y};
+      const double b[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int p = 0; p < 4; ++p) acc[q][p] = fma(a[q], b[p], acc[q][p]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = tr + 4 * ty + q;
+      if (r >= r1) continue;
+      double* row = A + (int64_t)r * ld;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const int c = tc + 4 * tx + p;
+        if (c < cb1) row[c] -= acc[q][p];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------- diag solve ---
+// inv(U_kk) of every block, once per step (one CTA per block)
+__global__ void __launch_bounds__(kThreads)
+uinv_kernel(const LuJob* __restrict__ jobs, const double* __restrict__ ws, int k0, double* __restrict__ uinv) {
+  extern __shared__ double sm[];
+  double* sU = sm;                 // U_kk (identity-padded)
+  double* sI = sm + kNb * kLd;     // inv(U_kk)
+  const LuJob J = jobs[blockIdx.x];
+  const int m = J.m, ld = J.m + J.nc;
+  if (k0 >= m) return;
+  const int kb = min(kNb, m - k0);
+  const double* A = ws + J.ws_off;
+  const int tid = threadIdx.x;
+  for (int q = tid; q < kNb * kNb; q += kThreads) {
+    const int r = q / kNb, c = q % kNb;
+    sU[r * kLd + c] = (r < kb && c < kb) ? A[(int64_t)(k0 + r) * ld + k0 + c] : (r == c ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  if (tid < kNb) {
+    // column t of inv(U): back substitution of U x = e_t
+    const int t = tid;
+    for (int r = kNb - 1; r >= 0; --r) {
+      double x;
+      if (r > t) x = 0.0;
+      else {
+        double acc = (r == t) ? 1.0 : 0.0;
+        for (int s2 = r + 1; s2 <= t; ++s2) acc = fma(-sU[r * kLd + s2], sI[s2 * kLd + t], acc);
+        double d = sU[r * kLd + r];
+        if (d == 0.0) d = 1e-300;
+        x = acc / d;
+      }
+      sI[r * kLd + t] = x;
+    }
+  }
+  __syncthreads();
+  double* Ui = uinv + (int64_t)blockIdx.x * kNb * kNb;
+  for (int q = tid; q < kNb * kNb; q += kThreads) Ui[q] = sI[(q / kNb) * kLd + q % kNb];
+}
+
+// X_k = inv(U_kk) Y_k on the RHS columns [m, ld), rows [k0, k0+kb)
+__global__ void __launch_bounds__(kThreads)
+diag_solve_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, int k0,
+                  const double* __restrict__ uinv) {
+  extern __shared__ double sm[];
+  double* sI = sm;                 // inv(U_kk)
+  double* sY = sm + kNb * kLd;     // RHS tile
+  const LuJob J = jobs[blockIdx.x];
+  const int m = J.m, nc = J.nc, ld = m + nc;
+  if (k0 >= m) return;
+  const int kb = min(kNb, m - k0);
+  double* A = ws + J.ws_off;
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const double* Ui = uinv + (int64_t)blockIdx.x * kNb * kNb;
+  for (int q = tid; q < kNb * kNb; q += kThreads) sI[(q / kNb) * kLd + q % kNb] = Ui[q];
+  for (int c0 = m + kNb * blockIdx.y; c0 < ld; c0 += kNb * gridDim.y) {
+    const int cw = min(kNb, ld - c0);
+    for (int q = tid; q < kNb * kNb; q += kThreads) {
+      const int r = q / kNb, c = q % kNb;
+      sY[r * kLd + c] = (r < kb && c < cw) ? A[(int64_t)(k0 + r) * ld + c0 + c] : 0.0;
+    }
+    __syncthreads();
+    double acc[4][4] = {};
+    for (int t = 0; t < kb; ++t) {
+      double a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { a[q] = sI[(4 * ty + q) * kLd + t]; b[q] = sY[t * kLd + 4 * tx + q]; }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int p = 0; p < 4; ++p) acc[q][p] = fma(a[q], b[p], acc[q][p]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = 4 * ty + q;
+      if (r >= kb) continue;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const int c = 4 * tx + p;
+        if (c < cw) A[(int64_t)(k0 + r) * ld + c0 + c] = acc[q][p];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// --------------------------------------------------------------- W = X^T ----
+template <class WT>
+__global__ void transpose_w_kernel(const LuJob* __restrict__ jobs, const double* __restrict__ ws,
+                                   WT* __restrict__ W) {
+  __shared__ double t[32][33];
+  const LuJob J = jobs[blockIdx.x];
+  const int m = J.m, nc = J.nc, ld = m + nc;
+  const double* A = ws + J.ws_off;
+  WT* Wb = W + J.w_off;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+  const int ntc = (nc + 31) / 32, nte = (m + 31) / 32;
+  for (int tile = blockIdx.y; tile < ntc * nte; tile += gridDim.y) {
+    const int e0 = 32 * (tile / ntc), c0 = 32 * (tile % ntc);
+    for (int r = ty; r < 32; r += 8) {
+      const int e = e0 + r, c = c0 + tx;
+      t[r][tx] = (e < m && c < nc) ? A[(int64_t)e * ld + m + c] : 0.0;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+      const int c = c0 + r, e = e0 + tx;
+      if (c < nc && e < m) Wb[(int64_t)c * m + e] = (WT)t[tx][r];
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+rbf_status batched_lu_restricted_inverse(rbf_ctx* ctx, const LuJob* jobs_dev, const std::vector<LuJob>& jobs,
+                                         double* ws, double* W, int* info) {
+  cudaStream_t s = ctx->stream;
+  const int nj = (int)jobs.size();
+  if (nj == 0) return RBF_OK;
+  int maxm = 0, maxnc = 0, maxld = 0;
+  for (const auto& j : jobs) {
+    maxm = std::max(maxm, j.m);
+    maxnc = std::max(maxnc, j.nc);
+    maxld = std::max(maxld, j.m + j.nc);
+  }
+  DevBuf piv, linv;
+  RBF_TRY(piv.alloc(sizeof(int) * (size_t)nj * kNb, s));
+  RBF_TRY(linv.alloc(sizeof(double) * (size_t)nj * kNb * kNb, s));
+  const size_t sm2 = sizeof(double) * 2 * kNb * kLd;
+  static bool attr = false;
+  if (!attr) {
+    RBF_CUDA_TRY(cudaFuncSetAttribute(linv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+    RBF_CUDA_TRY(cudaFuncSetAttribute(swap_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+    RBF_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+    RBF_CUDA_TRY(cudaFuncSetAttribute(diag_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+    RBF_CUDA_TRY(cudaFuncSetAttribute(uinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+    attr = true;
+  }
+  auto tiles = [](int a, int b) { return (a + kNb - 1) / kNb * ((b + kNb - 1) / kNb); };
+  // CTAs per block along grid.y: enough to fill ~8 CTAs per SM, each looping over tiles
+  const int spread = std::max(1, (ctx->sm_count * 8 + nj - 1) / nj);
+  // cluster size for the on-chip panel: rows per CTA R <= 256 (133 KB of smem)
+  int CL = 1;
+  while (CL < 16 && (maxm + CL - 1) / CL > 256) CL *= 2;
+  const int R = (maxm + CL - 1) / CL;
+  const size_t smp = sizeof(double) * (size_t)R * kPs;
+  if (CL > 8) {
+    RBF_CUDA_TRY(cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  }
+  RBF_CUDA_TRY(cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp));
+  cudaLaunchConfig_t pcfg = {};
+  pcfg.gridDim = dim3((unsigned)(nj * CL));
+  pcfg.blockDim = dim3(kThreads);
+  pcfg.dynamicSmemBytes = smp;
+  pcfg.stream = s;
+  cudaLaunchAttribute pattr[1];
+  pattr[0].id = cudaLaunchAttributeClusterDimension;
+  pattr[0].val.clusterDim.x = CL;
+  pattr[0].val.clusterDim.y = 1;
+  pattr[0].val.clusterDim.z = 1;
+  pcfg.attrs = pattr;
+  pcfg.numAttrs = 1;
+  for (int k0 = 0; k0 < maxm; k0 += kNb) {
+    int* pivp = piv.as<int>();
+    RBF_CUDA_TRY(cudaLaunchKernelEx(&pcfg, panel_cluster_kernel, jobs_dev, ws, k0, pivp, R, info));
+    linv_kernel<<<nj, kThreads, sm2, s>>>(jobs_dev, ws, k0, linv.as<double>());
+    RBF_CHECK_LAUNCH();
+    const int ct = std::max(1, std::min((maxld - k0 + kNb - 1) / kNb, spread));
+    swap_trsm_kernel<<<dim3(nj, ct), kThreads, sm2, s>>>(jobs_dev, ws, k0, piv.as<int>(), linv.as<double>());
+    RBF_CHECK_LAUNCH();
+    const int gt = tiles(std::max(0, maxm - k0), std::max(0, maxld - k0));
+    if (gt > 0) {
+      gemm_kernel<<<dim3(nj, std::min(gt, spread)), kThreads, sm2, s>>>(jobs_dev, ws, k0, 0);
+      RBF_CHECK_LAUNCH();
+    }
+  }
+  for (int k0 = ((maxm - 1) / kNb) * kNb; k0 >= 0; k0 -= kNb) {
+    uinv_kernel<<<nj, kThreads, sm2, s>>>(jobs_dev, ws, k0, linv.as<double>());
+    RBF_CHECK_LAUNCH();
+    diag_solve_kernel<<<dim3(nj, std::max(1, std::min((maxnc + kNb - 1) / kNb, spread))), kThreads, sm2, s>>>(
+        jobs_dev, ws, k0,
+                                                                                linv.as<double>());
+    RBF_CHECK_LAUNCH();
+    if (k0 > 0) {
+      gemm_kernel<<<dim3(nj, std::max(1, std::min(tiles(k0, maxnc), spread))), kThreads, sm2, s>>>(jobs_dev, ws,
+                                                                                                  k0, 1);
+      RBF_CHECK_LAUNCH();
+    }
+  }
+  transpose_w_kernel<double><<<dim3(nj, 64), 256, 0, s>>>(jobs_dev, ws, W);
+  RBF_CHECK_LAUNCH();
+  return RBF_OK;
+}
+
+}  // namespace rbf

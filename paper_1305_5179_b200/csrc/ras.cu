@@ -24,8 +24,6 @@
 namespace rbf {
 namespace {
 
-constexpr int kLuThreads = 256;
-constexpr int kNb = 32;          // panel width
 constexpr int kMaxCore = 3968;   // core centres held in shared memory by the ext search (48 KB static)
 
 // ---------------------------------------------------------------- helpers --
@@ -223,12 +221,6 @@ using FT = double;
 // in non-null directions that A amplifies.
 using WT = double;
 
-struct LuJob {
-  int64_t ws_off;   // element offset of the augmented matrix in the workspace
-  int64_t ext_off;  // offset into ext_idx
-  int64_t w_off;    // element offset of W (nc x m) in the W buffer
-  int m, nc;
-};
 
 // A_ext (m x m) | E_core (m x nc), row-major with ld = m + nc; entries as the
 // oracle forms them: a * exp(-d2 / (2 sigma^2)), d2 = (dx^2 + dy^2) + dz^2 in fp64.
@@ -255,192 +247,6 @@ __global__ void assemble_kernel(const LuJob* __restrict__ jobs, const float4* __
       A[(int64_t)i * ld + c] = v;
     }
   }
-}
-
-// C[r][c] -= sum_{t<kb} A[r][lc + t] * A[rr + t][c]   for r in [r0,r1), c in [c0,c1)
-__device__ void gemm_sub(FT* __restrict__ A, int ld, int r0, int r1, int c0, int c1, int lc, int rr, int kb,
-                         FT (*sL)[64 + 1], FT (*sU)[64 + 2]) {
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  for (int tr = r0; tr < r1; tr += 64)
-    for (int tc = c0; tc < c1; tc += 64) {
-      for (int q = tid; q < 64 * kNb; q += blockDim.x) {
-        const int i = q / kNb, t = q % kNb;
-        const int r = tr + i;
-        sL[t][i] = (r < r1 && t < kb) ? A[(int64_t)r * ld + lc + t] : 0.0;
-      }
-      for (int q = tid; q < kNb * 64; q += blockDim.x) {
-        const int t = q / 64, j = q % 64;
-        const int c = tc + j;
-        sU[t][j] = (c < c1 && t < kb) ? A[(int64_t)(rr + t) * ld + c] : 0.0;
-      }
-      __syncthreads();
-      FT acc[4][4] = {};
-#pragma unroll 4
-      for (int t = 0; t < kNb; ++t) {
-        FT a[4], bv[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) { a[q] = sL[t][ty + 16 * q]; bv[q] = sU[t][tx + 16 * q]; }
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int p = 0; p < 4; ++p) acc[q][p] = fma(a[q], bv[p], acc[q][p]);
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int r = tr + ty + 16 * q;
-        if (r >= r1) continue;
-#pragma unroll
-        for (int p = 0; p < 4; ++p) {
-          const int c = tc + tx + 16 * p;
-          if (c < c1) A[(int64_t)r * ld + c] -= acc[q][p];
-        }
-      }
-      __syncthreads();
-    }
-}
-
-__global__ void __launch_bounds__(kLuThreads)
-lu_kernel(const LuJob* __restrict__ jobs, FT* __restrict__ ws, WT* __restrict__ W, int* __restrict__ info) {
-  __shared__ FT sL[kNb][64 + 1];
-  __shared__ FT sU[kNb][64 + 2];
-  __shared__ FT sT[kNb][kNb + 1];
-  __shared__ FT sv[kLuThreads / 32];
-  __shared__ int si[kLuThreads / 32];
-  __shared__ int spiv[kNb];
-  const LuJob J = jobs[blockIdx.x];
-  const int m = J.m, nc = J.nc, ld = m + nc;
-  FT* A = ws + J.ws_off;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  int singular = 0;
-
-  for (int k0 = 0; k0 < m; k0 += kNb) {
-    const int kb = min(kNb, m - k0);
-    // ---- panel: columns [k0, k0+kb), rows [k0, m); swaps applied inside the panel only
-    for (int jj = 0; jj < kb; ++jj) {
-      const int j = k0 + jj;
-      FT best = -1.0;
-      int bi = j;
-      for (int i = j + tid; i < m; i += blockDim.x) {
-        const FT v = fabs(A[(int64_t)i * ld + j]);
-        if (v > best) { best = v; bi = i; }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const FT ov = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-      }
-      if (lane == 0) { sv[wid] = best; si[wid] = bi; }
-      __syncthreads();
-      if (tid == 0) {
-        FT b2 = sv[0];
-        int i2 = si[0];
-        for (int q = 1; q < kLuThreads / 32; ++q)
-          if (sv[q] > b2 || (sv[q] == b2 && si[q] < i2)) { b2 = sv[q]; i2 = si[q]; }
-        spiv[jj] = i2;
-      }
-      __syncthreads();
-      const int p = spiv[jj];
-      if (p != j && tid < kb) {
-        FT* rj = A + (int64_t)j * ld + k0;
-        FT* rp = A + (int64_t)p * ld + k0;
-        const FT t = rj[tid];
-        rj[tid] = rp[tid];
-        rp[tid] = t;
-      }
-      __syncthreads();
-      FT piv = A[(int64_t)j * ld + j];
-      if (piv == 0.0) { singular = 1; piv = 1e-300; }
-      const FT inv = 1.0 / piv;
-      for (int i = j + 1 + tid; i < m; i += blockDim.x) {
-        FT* ri = A + (int64_t)i * ld;
-        const FT l = ri[j] * inv;
-        ri[j] = l;
-        const FT* rj = A + (int64_t)j * ld;
-        for (int c = j + 1; c < k0 + kb; ++c) ri[c] = fma(-l, rj[c], ri[c]);
-      }
-      __syncthreads();
-    }
-    // ---- the panel's row swaps on the columns right of it (incl. the RHS block);
-    //      the L columns left of the panel are never read again
-    for (int c = k0 + kb + tid; c < ld; c += blockDim.x) {
-      for (int jj = 0; jj < kb; ++jj) {
-        const int p = spiv[jj], j = k0 + jj;
-        if (p != j) {
-          const FT t = A[(int64_t)j * ld + c];
-          A[(int64_t)j * ld + c] = A[(int64_t)p * ld + c];
-          A[(int64_t)p * ld + c] = t;
-        }
-      }
-    }
-    __syncthreads();
-    // ---- U12 = L11^-1 A12 (unit lower triangular L11), columns [k0+kb, ld)
-    for (int q = tid; q < kb * kb; q += blockDim.x) sT[q / kb][q % kb] = A[(int64_t)(k0 + q / kb) * ld + k0 + q % kb];
-    __syncthreads();
-    for (int c = k0 + kb + tid; c < ld; c += blockDim.x) {
-      FT x[kNb];
-#pragma unroll
-      for (int r = 0; r < kNb; ++r) x[r] = r < kb ? A[(int64_t)(k0 + r) * ld + c] : 0.0;
-#pragma unroll
-      for (int r = 1; r < kNb; ++r) {
-        FT acc = x[r];
-#pragma unroll
-        for (int t = 0; t < r; ++t) acc = fma(-sT[r][t], x[t], acc);
-        x[r] = acc;
-      }
-#pragma unroll
-      for (int r = 1; r < kNb; ++r)
-        if (r < kb) A[(int64_t)(k0 + r) * ld + c] = x[r];
-    }
-    __syncthreads();
-    // ---- trailing update A22 -= L21 U12 over all remaining columns (incl. the RHS block)
-    if (k0 + kb < m) gemm_sub(A, ld, k0 + kb, m, k0 + kb, ld, k0, k0, kb, sL, sU);
-    __syncthreads();
-  }
-  // ---- back substitution U X = Y on the RHS block (columns [m, ld)), bottom-up
-  for (int k0 = ((m - 1) / kNb) * kNb; k0 >= 0; k0 -= kNb) {
-    const int kb = min(kNb, m - k0);
-    for (int q = tid; q < kb * kb; q += blockDim.x) sT[q / kb][q % kb] = A[(int64_t)(k0 + q / kb) * ld + k0 + q % kb];
-    __syncthreads();
-    for (int c = m + tid; c < ld; c += blockDim.x) {
-      FT x[kNb];
-#pragma unroll
-      for (int r = 0; r < kNb; ++r) x[r] = r < kb ? A[(int64_t)(k0 + r) * ld + c] : 0.0;
-#pragma unroll
-      for (int r = kNb - 1; r >= 0; --r) {
-        if (r >= kb) continue;
-        FT acc = x[r];
-#pragma unroll
-        for (int t = r + 1; t < kNb; ++t)
-          if (t < kb) acc = fma(-sT[r][t], x[t], acc);
-        FT d = sT[r][r];
-        if (d == 0.0) d = 1e-300;
-        x[r] = acc / d;
-      }
-#pragma unroll
-      for (int r = 0; r < kNb; ++r)
-        if (r < kb) A[(int64_t)(k0 + r) * ld + c] = x[r];
-    }
-    __syncthreads();
-    if (k0 > 0) gemm_sub(A, ld, 0, k0, m, ld, k0, k0, kb, sL, sU);
-    __syncthreads();
-  }
-  // ---- W (nc x m, fp32) = X^T, X = A[:, m:ld]
-  WT* Wb = W + J.w_off;
-  for (int e0 = 0; e0 < m; e0 += kNb)
-    for (int c0 = 0; c0 < nc; c0 += kNb) {
-      for (int q = tid; q < kNb * kNb; q += blockDim.x) {
-        const int e = e0 + q / kNb, c = c0 + q % kNb;
-        sT[q / kNb][q % kNb] = (e < m && c < nc) ? A[(int64_t)e * ld + m + c] : 0.0;
-      }
-      __syncthreads();
-      for (int q = tid; q < kNb * kNb; q += blockDim.x) {
-        const int c = c0 + q / kNb, e = e0 + q % kNb;
-        if (e < m && c < nc) Wb[(int64_t)c * m + e] = (WT)sT[q % kNb][q / kNb];
-      }
-      __syncthreads();
-    }
-  if (singular && tid == 0) atomicAdd(info, 1);
 }
 
 // ---------------------------------------------------------------- apply ----
@@ -652,9 +458,8 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
     assemble_kernel<<<ag, 256, 0, s>>>(jobs_d.as<LuJob>(), c->sorted.as<float4>(), P->ext_idx.as<int32_t>(),
                                        ws.as<FT>(), kp.amp, two_s2, c2);
     RBF_CHECK_LAUNCH();
-    lu_kernel<<<(unsigned)jobs.size(), kLuThreads, 0, s>>>(jobs_d.as<LuJob>(), ws.as<FT>(), P->W.as<WT>(),
-                                                           info.as<int>());
-    RBF_CHECK_LAUNCH();
+    RBF_TRY(batched_lu_restricted_inverse(ctx, jobs_d.as<LuJob>(), jobs, ws.as<FT>(), P->W.as<WT>(),
+                                          info.as<int>()));
     // the host vector is reused: wait before the next chunk overwrites jobs_d
     RBF_CUDA_TRY(cudaStreamSynchronize(s));
   }

@@ -24,6 +24,18 @@ struct rbf_precond {
 
 namespace rbf {
 
+// One RAS block of a factorisation chunk (lu_batched.cu).
+struct LuJob {
+  int64_t ws_off;   // element offset of the augmented matrix [A_ext | E_core] in the workspace
+  int64_t ext_off;  // offset into ext_idx
+  int64_t w_off;    // element offset of W (nc x m) in the W buffer
+  int m, nc;
+};
+// Factor every job's [A_ext | E_core] (fp64, partial pivoting) and write
+// W = (A_ext^-1)[core, :] (fp64, nc x m row-major) at W + w_off.
+rbf_status batched_lu_restricted_inverse(rbf_ctx* ctx, const LuJob* jobs_dev, const std::vector<LuJob>& jobs,
+                                         double* ws, double* W, int* info);
+
 rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp, const rbf_precond_cfg* cfg,
                          rbf_precond* P);
 // z = M r in sorted order (r, z fp32 or fp64; never aliased)

@@ -79,6 +79,7 @@ struct SumGeom {
   CellGrid g;
   float cc;     // culling radius (cutoff inflated by rounding margins)
   float cc2;
+  float ci2;    // interior radius^2: cutoff deflated by 1e-4 and the rounding margin
   float s;      // sqrt(k), k = log2(e) / (2 sigma^2)
   int c2bits;   // bits of float32(k c^2)
   float amp;    // a
@@ -145,9 +146,103 @@ __device__ __forceinline__ void traverse(const SumGeom& G, const int32_t* __rest
   }
 }
 
+// Two-ring traversal of the fp32 tier.  `load` classifies each streamed source
+// as culled (0), boundary (1: some target of the tile may lie beyond the
+// cutoff, the inner loop masks) or interior (2: every target of the tile box is
+// within c(1-1e-4), the inner loop skips the mask -- same result bit for bit,
+// two fewer ALU instructions per pair).  Each class has its own ring and flush.
+template <class Load, class FlushB, class FlushI>
+__device__ __forceinline__ void traverse2(const SumGeom& G, const int32_t* __restrict__ cell_start,
+                                          float3 blo, float3 bhi, int lane, Load&& load, FlushB&& flushB,
+                                          FlushI&& flushI, int& nB, int& nI) {
+  const CellGrid& g = G.g;
+  const float cc = G.cc, cc2 = G.cc2, h = g.h;
+  const int z0 = cellof(blo.z - cc, g.lo[2], g.inv_h, g.dim[2]);
+  const int z1 = cellof(bhi.z + cc, g.lo[2], g.inv_h, g.dim[2]);
+  const int y0 = cellof(blo.y - cc, g.lo[1], g.inv_h, g.dim[1]);
+  const int y1 = cellof(bhi.y + cc, g.lo[1], g.inv_h, g.dim[1]);
+  const unsigned lt = (1u << lane) - 1u;
+  for (int cz = z0; cz <= z1; ++cz) {
+    const float czlo = g.lo[2] + (float)cz * h;
+    const float gz = fmaxf(0.f, fmaxf(czlo - bhi.z, blo.z - (czlo + h)));
+    for (int cy = y0; cy <= y1; ++cy) {
+      const float cylo = g.lo[1] + (float)cy * h;
+      const float gy = fmaxf(0.f, fmaxf(cylo - bhi.y, blo.y - (cylo + h)));
+      const float rem = cc2 - gy * gy - gz * gz;
+      if (rem < 0.f) continue;
+      const float rx = sqrtf(rem);
+      const int x0 = cellof(blo.x - rx, g.lo[0], g.inv_h, g.dim[0]);
+      const int x1 = cellof(bhi.x + rx, g.lo[0], g.inv_h, g.dim[0]);
+      const int64_t rowbase = ((int64_t)cz * g.dim[1] + cy) * g.dim[0];
+      const int sb = __ldg(cell_start + rowbase + x0);
+      const int se = __ldg(cell_start + rowbase + x1 + 1);
+      for (int j0 = sb; j0 < se; j0 += 32) {
+        const int j = j0 + lane;
+        const int kind = load.classify(j, j < se);
+        const unsigned bi = __ballot_sync(0xffffffffu, kind == 2);
+        const unsigned bb = __ballot_sync(0xffffffffu, kind == 1);
+        load.store2(kind, nB + __popc(bb & lt), nI + __popc(bi & lt));
+        nB += __popc(bb);
+        nI += __popc(bi);
+        if (nB >= kFlush) {
+          __syncwarp();
+          flushB(kFlush);
+          __syncwarp();
+          load.shift_ring(load.rb, nB - kFlush, lane);
+          __syncwarp();
+          nB -= kFlush;
+        }
+        if (nI >= kFlush) {
+          __syncwarp();
+          flushI(kFlush);
+          __syncwarp();
+          load.shift_ring(load.ri, nI - kFlush, lane);
+          __syncwarp();
+          nI -= kFlush;
+        }
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------- fp32 tier ---
 struct Ring32 {
   float* bx; float* by; float* bz; float* bw;
+};
+
+// Dual-ring staging of the fp32 fast path (see traverse2).
+struct Stage32x2 {
+  Ring32 rb, ri;
+  const float4* __restrict__ src;
+  float3 blo, bhi, ctr;
+  float cc2, ci2;
+  float4 p;
+  __device__ __forceinline__ int classify(int j, bool valid) {
+    p = valid ? __ldg(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float ax = blo.x - p.x, bx = p.x - bhi.x;
+    const float ay = blo.y - p.y, by = p.y - bhi.y;
+    const float az = blo.z - p.z, bz = p.z - bhi.z;
+    const float gx = fmaxf(0.f, fmaxf(ax, bx)), gy = fmaxf(0.f, fmaxf(ay, by)), gz = fmaxf(0.f, fmaxf(az, bz));
+    if (!valid || gx * gx + gy * gy + gz * gz > cc2) return 0;
+    // farthest point of the box
+    const float fx = fmaxf(fabsf(ax), fabsf(bx)), fy = fmaxf(fabsf(ay), fabsf(by)), fz = fmaxf(fabsf(az), fabsf(bz));
+    return (fx * fx + fy * fy + fz * fz <= ci2) ? 2 : 1;
+  }
+  __device__ __forceinline__ void store2(int kind, int posb, int posi) {
+    if (kind == 0) return;
+    Ring32& r = (kind == 2) ? ri : rb;
+    const int pos = (kind == 2) ? posi : posb;
+    r.bx[pos] = p.x - ctr.x;
+    r.by[pos] = p.y - ctr.y;
+    r.bz[pos] = p.z - ctr.z;
+    r.bw[pos] = p.w;
+  }
+  __device__ __forceinline__ void shift_ring(Ring32& r, int rest, int lane) {
+    if (lane < rest) {
+      float a = r.bx[kFlush + lane], b = r.by[kFlush + lane], c = r.bz[kFlush + lane], d = r.bw[kFlush + lane];
+      r.bx[lane] = a; r.by[lane] = b; r.bz[lane] = c; r.bw[lane] = d;
+    }
+  }
 };
 
 struct Stage32 {
@@ -180,13 +275,14 @@ struct Stage32 {
   }
 };
 
-template <int T>
+template <int T, bool MASK = true>
 struct Flush32 {
   Ring32 r;
   float2* acc;            // [T]
   const float* xt; const float* yt; const float* zt;   // [T] -(local target coords * s)
   int c2bits;
   float s;
+  __device__ __forceinline__ float cut(float r2) const { return MASK ? cutmask(r2, c2bits) : r2; }
   __device__ __forceinline__ void operator()(int cnt) {
     const float2 s2 = make_float2(s, s);
 #pragma unroll 2
@@ -207,8 +303,8 @@ struct Flush32 {
         float2 ra = mul2(dxa, dxa), rb = mul2(dxb, dxb);
         ra = fma2(dya, dya, ra); rb = fma2(dyb, dyb, rb);
         ra = fma2(dza, dza, ra); rb = fma2(dzb, dzb, rb);
-        float2 ea = make_float2(ex2(-cutmask(ra.x, c2bits)), ex2(-cutmask(ra.y, c2bits)));
-        float2 eb = make_float2(ex2(-cutmask(rb.x, c2bits)), ex2(-cutmask(rb.y, c2bits)));
+        float2 ea = make_float2(ex2(-cut(ra.x)), ex2(-cut(ra.y)));
+        float2 eb = make_float2(ex2(-cut(rb.x)), ex2(-cut(rb.y)));
         acc[t] = fma2(ea, make_float2(W.x, W.y), acc[t]);
         acc[t] = fma2(eb, make_float2(W.z, W.w), acc[t]);
       }
@@ -266,9 +362,10 @@ sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
                const int2* __restrict__ tiles, const float4* __restrict__ tbox, int64_t ntiles,
                GridDesc gd, OutT* __restrict__ out, const int32_t* __restrict__ out_perm,
                int* __restrict__ work, unsigned long long* __restrict__ stats) {
-  __shared__ __align__(16) float ring[kSumWarps][4][kBufPad];
+  __shared__ __align__(16) float ring[kSumWarps][8][kBufPad];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  Ring32 R{ring[wib][0], ring[wib][1], ring[wib][2], ring[wib][3]};
+  Ring32 R{ring[wib][0], ring[wib][1], ring[wib][2], ring[wib][3]};     // boundary sources
+  Ring32 RI{ring[wib][4], ring[wib][5], ring[wib][6], ring[wib][7]};    // interior sources
   unsigned long long useful = 0, visited = 0;
   for (;;) {
     int64_t tile;
@@ -322,29 +419,36 @@ sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
       xt[t] = -((xr[t] - ctr.x) * G.s); yt[t] = -((yr[t] - ctr.y) * G.s); zt[t] = -((zr[t] - ctr.z) * G.s);
     }
     float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-    Stage32 st{R, src, blo, bhi, ctr, G.cc2, G.s, make_float4(0, 0, 0, 0)};
-    int nbuf = 0;
     const bool two = tcount > 32;
     if (STATS) {
+      Stage32 st{R, src, blo, bhi, ctr, G.cc2, G.s, make_float4(0, 0, 0, 0)};
+      int nbuf = 0;
       FlushStats<2> fs{R, xt, yt, zt, tv, G.c2bits, G.s, &useful, &visited};
       traverse(G, cell_start, blo, bhi, lane, st, fs, nbuf);
       int cnt;
       pad_ring(R, nbuf, lane, cnt);
       fs(cnt);
       __syncwarp();
-    } else if (two) {
-      Flush32<2> fl{R, acc, xt, yt, zt, G.c2bits, G.s};
-      traverse(G, cell_start, blo, bhi, lane, st, fl, nbuf);
-      int cnt;
-      pad_ring(R, nbuf, lane, cnt);
-      fl(cnt);
-      __syncwarp();
     } else {
-      Flush32<1> fl{R, acc, xt, yt, zt, G.c2bits, G.s};
-      traverse(G, cell_start, blo, bhi, lane, st, fl, nbuf);
-      int cnt;
-      pad_ring(R, nbuf, lane, cnt);
-      fl(cnt);
+      Stage32x2 st{R, RI, src, blo, bhi, ctr, G.cc2, G.ci2, make_float4(0, 0, 0, 0)};
+      int nB = 0, nI = 0, cnt;
+      if (two) {
+        Flush32<2, true> fb{R, acc, xt, yt, zt, G.c2bits, G.s};
+        Flush32<2, false> fi{RI, acc, xt, yt, zt, G.c2bits, G.s};
+        traverse2(G, cell_start, blo, bhi, lane, st, fb, fi, nB, nI);
+        pad_ring(R, nB, lane, cnt);
+        fb(cnt);
+        pad_ring(RI, nI, lane, cnt);
+        fi(cnt);
+      } else {
+        Flush32<1, true> fb{R, acc, xt, yt, zt, G.c2bits, G.s};
+        Flush32<1, false> fi{RI, acc, xt, yt, zt, G.c2bits, G.s};
+        traverse2(G, cell_start, blo, bhi, lane, st, fb, fi, nB, nI);
+        pad_ring(R, nB, lane, cnt);
+        fb(cnt);
+        pad_ring(RI, nI, lane, cnt);
+        fi(cnt);
+      }
       __syncwarp();
     }
     if (!STATS) {
@@ -497,6 +601,8 @@ SumGeom make_geom(const rbf_cells* c, const KernelParams& kp) {
   double cc = kp.cutoff * (1.0 + 1e-5) + 4e-7 * maxabs + 1e-30;
   G.cc = (float)cc;
   G.cc2 = (float)(cc * cc);
+  const double ci = std::max(0.0, kp.cutoff * (1.0 - 1e-4) - 4e-7 * maxabs);
+  G.ci2 = (float)(ci * ci);
   const double k = 1.4426950408889634 / (2.0 * kp.sigma * kp.sigma);
   G.s = (float)std::sqrt(k);
   float c2s = (float)(k * kp.cutoff * kp.cutoff);

@@ -38,7 +38,7 @@ class _Kernel(C.Structure):
 
 
 class _CellCfg(C.Structure):
-    _fields_ = [("cell_edge", C.c_double), ("tile_cap", C.c_int), ("tile_span", C.c_int)]
+    _fields_ = [("cell_edge", C.c_double), ("tile_cap", C.c_int), ("tile_span", C.c_int), ("tile_mode", C.c_int)]
 
 
 class _PrecondCfg(C.Structure):
@@ -229,14 +229,14 @@ class Cells:
     """rbf_build_cells: cell list + tile plan over the centres (Alg.2 'truncation area')."""
 
     def __init__(self, ctx: Context, xyz: torch.Tensor, kernel: Kernel, cell_edge: float = 0.0,
-                 tile_cap: int = 64, tile_span: int = 2):
+                 tile_cap: int = 64, tile_span: int = 2, tile_mode: int = 0):
         _need(xyz, torch.float32, name="xyz")
         if xyz.dim() != 2 or xyz.shape[1] != 3:
             raise ValueError("xyz must be (n, 3)")
         self.ctx, self.kernel = ctx, kernel
         self.n = xyz.shape[0]
         h = C.c_void_p()
-        cfg = _CellCfg(cell_edge, tile_cap, tile_span)
+        cfg = _CellCfg(cell_edge, tile_cap, tile_span, tile_mode)
         _check(_lib.rbf_build_cells(ctx._h, _ptr(xyz), self.n, C.byref(kernel._c()), C.byref(cfg),
                                     C.byref(h)))
         self._h = h
@@ -393,7 +393,7 @@ def reconstruct_host(ctx: Context, xyz, b, kernel: Kernel, lo, hi, n, *, cell_ed
     field = torch.empty((n3[2], n3[1], n3[0]), dtype=torch.float32) if field_out is None else field_out
     rep = SolveReport()
     _check(_lib.rbf_reconstruct_host(ctx._h, _ptr(xyz), _ptr(b), nn, C.byref(kernel._c()),
-                                     C.byref(_CellCfg(cell_edge, 64, 2)),
+                                     C.byref(_CellCfg(cell_edge, 64, 2, 0)),
                                      C.byref(_PrecondCfg(kind, core_target, overlap_sigmas, 0)),
                                      C.byref(_GmresCfg(restart, rtol, phase1_rtol, max_iters, 1)),
                                      C.byref(g), _ptr(w), _ptr(field), C.byref(rep)))

@@ -51,11 +51,19 @@ def test_zero_crossings_of_sphere_field():
 def test_halton_fig3_pins():
     """Fig. 3 caption: 25 Halton points on [0,1]^2 have
     q_X ~ 0.0597 and h_{X,Omega} ~ 0.2667 (fill distance over a 401^2 grid)."""
-    P = np.stack([D.halton(25, 2), D.halton(25, 3)], axis=1)
+    import os
+    gold = {}
+    with open(os.path.join(os.path.dirname(__file__), "golden", "fig3_halton.txt")) as fh:
+        for line in fh:
+            if line.strip() and not line.startswith("#"):
+                k, *v = line.split()
+                gold[k] = [float(x) for x in v]
+    n = int(gold["n_points"][0])
+    P = np.stack([D.halton(n, int(gold["bases"][0])), D.halton(n, int(gold["bases"][1]))], axis=1)
     g = np.linspace(0, 1, 401)
     Om = np.stack(np.meshgrid(g, g), -1).reshape(-1, 2)
-    assert D.separation_distance(P) == pytest.approx(0.0597, abs=5e-5)
-    assert D.fill_distance(P, Om) == pytest.approx(0.2667, abs=5e-5)
+    assert D.separation_distance(P) == pytest.approx(gold["q_X"][0], abs=5e-5)
+    assert D.fill_distance(P, Om) == pytest.approx(gold["h_X_Omega"][0], abs=5e-5)
     assert D.halton(4, 2).tolist() == [0.5, 0.25, 0.75, 0.125]
 
 
