@@ -82,6 +82,7 @@ struct rbf_prof_rec {
 struct rbf_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t aux_stream = nullptr;   // library-owned second stream (RAS factorisation overlap)
   int sm_count = 148;
   bool prof = false;
   std::vector<rbf_prof_rec> prof_recs;
@@ -99,6 +100,7 @@ struct rbf_ctx {
   ~rbf_ctx() {
     for (auto& r : prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : ev_pool) cudaEventDestroy(e);
+    if (aux_stream) cudaStreamDestroy(aux_stream);
   }
   rbf::DevBuf scratch;       // generic scratch (radix sort, scans)
   rbf::DevBuf counter;       // work counters (int32 x 64)

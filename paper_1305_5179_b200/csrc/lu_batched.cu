@@ -195,7 +195,9 @@ swap_trsm_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, int k0
                  const double* __restrict__ linv) {
   extern __shared__ double sm[];
   double* sI = sm;                 // inv(L11)
-  double* sT = sm + kNb * kLd;     // A12 tile
+  double* sT = sm + kNb * kLd;     // A12 tile; also the staging of the permuted rows (2 kNb x kNb)
+  __shared__ int s_rows[2 * kNb], s_src[2 * kNb];
+  __shared__ int s_n;
   const LuJob J = jobs[blockIdx.x];
   const int m = J.m, ld = J.m + J.nc;
   if (k0 >= m) return;
@@ -203,22 +205,36 @@ swap_trsm_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, int k0
   double* A = ws + J.ws_off;
   const int tid = threadIdx.x;
   const int* P = piv + (int64_t)blockIdx.x * kNb;
+  // the panel's sequence of row swaps as one permutation of the affected rows
+  if (tid == 0) {
+    int n = 0;
+    for (int jj = 0; jj < kb; ++jj) { s_rows[n] = k0 + jj; s_src[n] = k0 + jj; ++n; }
+    for (int jj = 0; jj < kb; ++jj) {
+      const int p = P[jj];
+      int ip = -1;
+      for (int q = 0; q < n; ++q)
+        if (s_rows[q] == p) { ip = q; break; }
+      if (ip < 0) { s_rows[n] = p; s_src[n] = p; ip = n; ++n; }
+      const int t = s_src[jj]; s_src[jj] = s_src[ip]; s_src[ip] = t;   // row k0+jj is slot jj
+    }
+    s_n = n;
+  }
   const double* Li = linv + (int64_t)blockIdx.x * kNb * kNb;
   for (int q = tid; q < kNb * kNb; q += kThreads) sI[(q / kNb) * kLd + q % kNb] = Li[q];
+  __syncthreads();
+  const int n = s_n;
   const int tx = tid & 15, ty = tid >> 4;
   for (int c0 = k0 + kb + kNb * blockIdx.y; c0 < ld; c0 += kNb * gridDim.y) {
     const int cw = min(kNb, ld - c0);
-    // row swaps of the panel, in order, on this tile's columns
-    if (tid < cw) {
-      const int c = c0 + tid;
-      for (int jj = 0; jj < kb; ++jj) {
-        const int p = P[jj], j = k0 + jj;
-        if (p != j) {
-          const double t = A[(int64_t)j * ld + c];
-          A[(int64_t)j * ld + c] = A[(int64_t)p * ld + c];
-          A[(int64_t)p * ld + c] = t;
-        }
-      }
+    // gather the permuted rows of this column tile, then scatter them (coalesced along columns)
+    for (int q = tid; q < n * kNb; q += kThreads) {
+      const int i = q / kNb, c = q % kNb;
+      if (c < cw) sT[i * kNb + c] = A[(int64_t)s_src[i] * ld + c0 + c];
+    }
+    __syncthreads();
+    for (int q = tid; q < n * kNb; q += kThreads) {
+      const int i = q / kNb, c = q % kNb;
+      if (c < cw && s_src[i] != s_rows[i]) A[(int64_t)s_rows[i] * ld + c0 + c] = sT[i * kNb + c];
     }
     __syncthreads();
     for (int q = tid; q < kNb * kNb; q += kThreads) {
@@ -258,7 +274,7 @@ swap_trsm_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, int k0
 __global__ void __launch_bounds__(kThreads)
 gemm_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, int k0, int mode) {
   extern __shared__ double sm[];
-  double* sA = sm;                 // [t][i] : kNb x kLd  (A[r0+i][k0+t])
+  double* sA = sm;                 // [i][t] : kNb x kLd  (A[r0+i][k0+t])
   double* sB = sm + kNb * kLd;     // [t][j] : kNb x kLd  (A[k0+t][c0+j])
   const LuJob J = jobs[blockIdx.x];
   const int m = J.m, ld = J.m + J.nc;
@@ -272,14 +288,29 @@ gemm_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, int k0, int
   const int ntr = (r1 - r0 + kNb - 1) / kNb;
   double* A = ws + J.ws_off;
   const int tid = threadIdx.x;
-  const int tx = tid & 15, ty = tid >> 4;
+  // fp64 tensor cores (DMMA 8x8x4): 8 warps, warp tile 16 x 32 = 2 x 4 mma tiles
+  const int lane = tid & 31, w = tid >> 5;
+  const int wm = w >> 1, wn = w & 1, g = lane >> 2, t4 = lane & 3;
   for (int tile = blockIdx.y; tile < ntr * ntc; tile += gridDim.y) {
     const int tr = r0 + kNb * (tile / ntc);
     const int tc = cb0 + kNb * (tile % ntc);
+    // C tile -> accumulators (fragment layout) first: its HBM latency overlaps the staging
+    double acc[2][4][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int r = tr + 16 * wm + 8 * mt + g;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int c = tc + 32 * wn + 8 * nt + 2 * t4 + i;
+          acc[mt][nt][i] = (r < r1 && c < cb1) ? A[(int64_t)r * ld + c] : 0.0;
+        }
+    }
     for (int q = tid; q < kNb * kNb; q += kThreads) {
-      const int i = q / kNb, t = q % kNb;     // consecutive threads: consecutive t (row-contiguous)
+      const int i = q / kNb, t = q % kNb;     // row-major: sA[i][t] = A[tr+i][k0+t]
       const int r = tr + i;
-      sA[t * kLd + i] = (r < r1 && t < kb) ? A[(int64_t)r * ld + k0 + t] : 0.0;
+      sA[i * kLd + t] = (r < r1 && t < kb) ? A[(int64_t)r * ld + k0 + t] : 0.0;
     }
     for (int q = tid; q < kNb * kNb; q += kThreads) {
       const int t = q / kNb, j = q % kNb;
@@ -287,30 +318,33 @@ gemm_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, int k0, int
       sB[t * kLd + j] = (c < cb1 && t < kb) ? A[(int64_t)(k0 + t) * ld + c] : 0.0;
     }
     __syncthreads();
-    double acc[4][4] = {};
 #pragma unroll 4
-    for (int t = 0; t < kNb; ++t) {
-      const double2 a01 = *reinterpret_cast<const double2*>(sA + t * kLd + 4 * ty);
-      const double2 a23 = *reinterpret_cast<const double2*>(sA + t * kLd + 4 * ty + 2);
-      const double2 b01 = *reinterpret_cast<const double2*>(sB + t * kLd + 4 * tx);
-      const double2 b23 = *reinterpret_cast<const double2*>(sB + t * kLd + 4 * tx + 2);
-      const double a[4] = {a01.x, a01.y, a23.x, a23.y};
-      const double b[4] = {b01.x, b01.y, b23.x, b23.y};
+    for (int kk = 0; kk < kNb / 4; ++kk) {
+      double af[2], bf[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int mt = 0; mt < 2; ++mt) af[mt] = -sA[(16 * wm + 8 * mt + g) * kLd + 4 * kk + t4];
 #pragma unroll
-        for (int p = 0; p < 4; ++p) acc[q][p] = fma(a[q], b[p], acc[q][p]);
+      for (int nt = 0; nt < 4; ++nt) bf[nt] = sB[(4 * kk + t4) * kLd + 32 * wn + 8 * nt + g];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[mt][nt][0]), "+d"(acc[mt][nt][1])
+                       : "d"(af[mt]), "d"(bf[nt]));
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int r = tr + 4 * ty + q;
+    for (int mt = 0; mt < 2; ++mt) {
+      const int r = tr + 16 * wm + 8 * mt + g;
       if (r >= r1) continue;
       double* row = A + (int64_t)r * ld;
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        const int c = tc + 4 * tx + p;
-        if (c < cb1) row[c] -= acc[q][p];
-      }
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int c = tc + 32 * wn + 8 * nt + 2 * t4 + i;
+          if (c < cb1) row[c] = acc[mt][nt][i];
+        }
     }
     __syncthreads();
   }
@@ -430,83 +464,153 @@ __global__ void transpose_w_kernel(const LuJob* __restrict__ jobs, const double*
 
 }  // namespace
 
+namespace {
+
+// One independent group of factorisation jobs issued on its own stream.
+struct LuGroup {
+  cudaStream_t s;
+  const LuJob* jobs_dev;
+  int nj, maxm, maxnc, maxld;
+  int* piv;
+  double* linv;
+  int spread, CL, R;
+  cudaLaunchConfig_t pcfg;
+  cudaLaunchAttribute pattr[1];
+};
+
+size_t sm2_bytes() { return sizeof(double) * 2 * kNb * kLd; }
+size_t smsw_bytes() { return sizeof(double) * (kNb * kLd + 2 * kNb * kNb); }   // inv(L11) + permutation staging
+
+int tiles_of(int a, int b) { return (a + kNb - 1) / kNb * ((b + kNb - 1) / kNb); }
+
+rbf_status lu_forward_step(LuGroup& G, int k0, double* ws, int* info) {
+  if (k0 >= G.maxm) return RBF_OK;
+  G.pcfg.attrs = G.pattr;
+  RBF_CUDA_TRY(cudaLaunchKernelEx(&G.pcfg, panel_cluster_kernel, G.jobs_dev, ws, k0, G.piv, G.R, info));
+  linv_kernel<<<G.nj, kThreads, sm2_bytes(), G.s>>>(G.jobs_dev, ws, k0, G.linv);
+  RBF_CHECK_LAUNCH();
+  const int ct = std::max(1, std::min((G.maxld - k0 + kNb - 1) / kNb, G.spread));
+  swap_trsm_kernel<<<dim3(G.nj, ct), kThreads, smsw_bytes(), G.s>>>(G.jobs_dev, ws, k0, G.piv, G.linv);
+  RBF_CHECK_LAUNCH();
+  const int gt = tiles_of(std::max(0, G.maxm - k0), std::max(0, G.maxld - k0));
+  if (gt > 0) {
+    gemm_kernel<<<dim3(G.nj, std::min(gt, G.spread)), kThreads, sm2_bytes(), G.s>>>(G.jobs_dev, ws, k0, 0);
+    RBF_CHECK_LAUNCH();
+  }
+  return RBF_OK;
+}
+
+rbf_status lu_backward_step(LuGroup& G, int k0, double* ws) {
+  if (k0 >= G.maxm) return RBF_OK;
+  uinv_kernel<<<G.nj, kThreads, sm2_bytes(), G.s>>>(G.jobs_dev, ws, k0, G.linv);
+  RBF_CHECK_LAUNCH();
+  diag_solve_kernel<<<dim3(G.nj, std::max(1, std::min((G.maxnc + kNb - 1) / kNb, G.spread))), kThreads,
+                      sm2_bytes(), G.s>>>(G.jobs_dev, ws, k0, G.linv);
+  RBF_CHECK_LAUNCH();
+  if (k0 > 0) {
+    gemm_kernel<<<dim3(G.nj, std::max(1, std::min(tiles_of(k0, G.maxnc), G.spread))), kThreads, sm2_bytes(),
+                  G.s>>>(G.jobs_dev, ws, k0, 1);
+    RBF_CHECK_LAUNCH();
+  }
+  return RBF_OK;
+}
+
+}  // namespace
+
 rbf_status batched_lu_restricted_inverse(rbf_ctx* ctx, const LuJob* jobs_dev, const std::vector<LuJob>& jobs,
                                          double* ws, double* W, int* info) {
   cudaStream_t s = ctx->stream;
   const int nj = (int)jobs.size();
   if (nj == 0) return RBF_OK;
-  int maxm = 0, maxnc = 0, maxld = 0;
-  for (const auto& j : jobs) {
-    maxm = std::max(maxm, j.m);
-    maxnc = std::max(maxnc, j.nc);
-    maxld = std::max(maxld, j.m + j.nc);
+  static bool attr = false;
+  if (!attr) {
+    RBF_CUDA_TRY(cudaFuncSetAttribute(linv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2_bytes()));
+    RBF_CUDA_TRY(cudaFuncSetAttribute(swap_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smsw_bytes()));
+    RBF_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2_bytes()));
+    RBF_CUDA_TRY(cudaFuncSetAttribute(diag_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sm2_bytes()));
+    RBF_CUDA_TRY(cudaFuncSetAttribute(uinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2_bytes()));
+    RBF_CUDA_TRY(cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr = true;
   }
   DevBuf piv, linv;
   RBF_TRY(piv.alloc(sizeof(int) * (size_t)nj * kNb, s));
   RBF_TRY(linv.alloc(sizeof(double) * (size_t)nj * kNb * kNb, s));
-  const size_t sm2 = sizeof(double) * 2 * kNb * kLd;
-  static bool attr = false;
-  if (!attr) {
-    RBF_CUDA_TRY(cudaFuncSetAttribute(linv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
-    RBF_CUDA_TRY(cudaFuncSetAttribute(swap_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
-    RBF_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
-    RBF_CUDA_TRY(cudaFuncSetAttribute(diag_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
-    RBF_CUDA_TRY(cudaFuncSetAttribute(uinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
-    attr = true;
+  // two groups on two streams: one group's latency-bound panels (1 CTA/SM, 133 KB of
+  // smem) co-run with the other's GEMMs (70 KB): the SM has room for both
+  const int ngroups = nj >= 64 ? 2 : 1;
+  if (ngroups == 2 && !ctx->aux_stream) {
+    RBF_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
   }
-  auto tiles = [](int a, int b) { return (a + kNb - 1) / kNb * ((b + kNb - 1) / kNb); };
-  // CTAs per block along grid.y: enough to fill ~8 CTAs per SM, each looping over tiles
-  const int spread = std::max(1, (ctx->sm_count * 8 + nj - 1) / nj);
-  // cluster size for the on-chip panel: rows per CTA R <= 256 (133 KB of smem)
-  int CL = 1;
-  while (CL < 16 && (maxm + CL - 1) / CL > 256) CL *= 2;
-  const int R = (maxm + CL - 1) / CL;
-  const size_t smp = sizeof(double) * (size_t)R * kPs;
-  if (CL > 8) {
-    RBF_CUDA_TRY(cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  }
-  RBF_CUDA_TRY(cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp));
-  cudaLaunchConfig_t pcfg = {};
-  pcfg.gridDim = dim3((unsigned)(nj * CL));
-  pcfg.blockDim = dim3(kThreads);
-  pcfg.dynamicSmemBytes = smp;
-  pcfg.stream = s;
-  cudaLaunchAttribute pattr[1];
-  pattr[0].id = cudaLaunchAttributeClusterDimension;
-  pattr[0].val.clusterDim.x = CL;
-  pattr[0].val.clusterDim.y = 1;
-  pattr[0].val.clusterDim.z = 1;
-  pcfg.attrs = pattr;
-  pcfg.numAttrs = 1;
-  for (int k0 = 0; k0 < maxm; k0 += kNb) {
-    int* pivp = piv.as<int>();
-    RBF_CUDA_TRY(cudaLaunchKernelEx(&pcfg, panel_cluster_kernel, jobs_dev, ws, k0, pivp, R, info));
-    linv_kernel<<<nj, kThreads, sm2, s>>>(jobs_dev, ws, k0, linv.as<double>());
-    RBF_CHECK_LAUNCH();
-    const int ct = std::max(1, std::min((maxld - k0 + kNb - 1) / kNb, spread));
-    swap_trsm_kernel<<<dim3(nj, ct), kThreads, sm2, s>>>(jobs_dev, ws, k0, piv.as<int>(), linv.as<double>());
-    RBF_CHECK_LAUNCH();
-    const int gt = tiles(std::max(0, maxm - k0), std::max(0, maxld - k0));
-    if (gt > 0) {
-      gemm_kernel<<<dim3(nj, std::min(gt, spread)), kThreads, sm2, s>>>(jobs_dev, ws, k0, 0);
-      RBF_CHECK_LAUNCH();
+  LuGroup Gs[2];
+  int lo = 0;
+  for (int gi = 0; gi < ngroups; ++gi) {
+    const int hi = (gi + 1 == ngroups) ? nj : nj / 2;
+    LuGroup& G = Gs[gi];
+    G.s = gi == 0 ? s : ctx->aux_stream;
+    G.jobs_dev = jobs_dev + lo;
+    G.nj = hi - lo;
+    G.maxm = G.maxnc = G.maxld = 0;
+    for (int j = lo; j < hi; ++j) {
+      G.maxm = std::max(G.maxm, jobs[j].m);
+      G.maxnc = std::max(G.maxnc, jobs[j].nc);
+      G.maxld = std::max(G.maxld, jobs[j].m + jobs[j].nc);
     }
+    G.piv = piv.as<int>() + (size_t)lo * kNb;
+    G.linv = linv.as<double>() + (size_t)lo * kNb * kNb;
+    // CTAs per block along grid.y: enough to fill ~8 CTAs per SM, each looping over tiles
+    G.spread = std::max(1, (ctx->sm_count * 8 / ngroups + G.nj - 1) / G.nj);
+    // cluster size for the on-chip panel: rows per CTA R <= 256 (133 KB of smem)
+    G.CL = 1;
+    while (G.CL < 16 && (G.maxm + G.CL - 1) / G.CL > 256) G.CL *= 2;
+    G.R = (G.maxm + G.CL - 1) / G.CL;
+    const size_t smp = sizeof(double) * (size_t)G.R * kPs;
+    RBF_CUDA_TRY(cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)std::max<size_t>(smp, 48 * 1024)));
+    G.pcfg = {};
+    G.pcfg.gridDim = dim3((unsigned)(G.nj * G.CL));
+    G.pcfg.blockDim = dim3(kThreads);
+    G.pcfg.dynamicSmemBytes = smp;
+    G.pcfg.stream = G.s;
+    G.pattr[0].id = cudaLaunchAttributeClusterDimension;
+    G.pattr[0].val.clusterDim.x = G.CL;
+    G.pattr[0].val.clusterDim.y = 1;
+    G.pattr[0].val.clusterDim.z = 1;
+    G.pcfg.attrs = G.pattr;
+    G.pcfg.numAttrs = 1;
+    lo = hi;
   }
-  for (int k0 = ((maxm - 1) / kNb) * kNb; k0 >= 0; k0 -= kNb) {
-    uinv_kernel<<<nj, kThreads, sm2, s>>>(jobs_dev, ws, k0, linv.as<double>());
-    RBF_CHECK_LAUNCH();
-    diag_solve_kernel<<<dim3(nj, std::max(1, std::min((maxnc + kNb - 1) / kNb, spread))), kThreads, sm2, s>>>(
-        jobs_dev, ws, k0,
-                                                                                linv.as<double>());
-    RBF_CHECK_LAUNCH();
-    if (k0 > 0) {
-      gemm_kernel<<<dim3(nj, std::max(1, std::min(tiles(k0, maxnc), spread))), kThreads, sm2, s>>>(jobs_dev, ws,
-                                                                                                  k0, 1);
-      RBF_CHECK_LAUNCH();
-    }
+  // the panel kernel's smem attribute is per function: use the larger group's need
+  {
+    size_t need = 0;
+    for (int gi = 0; gi < ngroups; ++gi) need = std::max(need, sizeof(double) * (size_t)Gs[gi].R * kPs);
+    RBF_CUDA_TRY(cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)std::max<size_t>(need, 48 * 1024)));
   }
-  transpose_w_kernel<double><<<dim3(nj, 64), 256, 0, s>>>(jobs_dev, ws, W);
-  RBF_CHECK_LAUNCH();
+  cudaEvent_t fork = nullptr, join = nullptr;
+  if (ngroups == 2) {
+    fork = ctx->take_event();
+    join = ctx->take_event();
+    RBF_CUDA_TRY(cudaEventRecord(fork, s));
+    RBF_CUDA_TRY(cudaStreamWaitEvent(Gs[1].s, fork, 0));
+  }
+  int maxm = 0;
+  for (int gi = 0; gi < ngroups; ++gi) maxm = std::max(maxm, Gs[gi].maxm);
+  for (int k0 = 0; k0 < maxm; k0 += kNb)
+    for (int gi = 0; gi < ngroups; ++gi) RBF_TRY(lu_forward_step(Gs[gi], k0, ws, info));
+  for (int k0 = ((maxm - 1) / kNb) * kNb; k0 >= 0; k0 -= kNb)
+    for (int gi = 0; gi < ngroups; ++gi) RBF_TRY(lu_backward_step(Gs[gi], k0, ws));
+  for (int gi = 0; gi < ngroups; ++gi) {
+    transpose_w_kernel<double><<<dim3(Gs[gi].nj, 64), 256, 0, Gs[gi].s>>>(Gs[gi].jobs_dev, ws, W);
+    RBF_CHECK_LAUNCH();
+  }
+  if (ngroups == 2) {
+    RBF_CUDA_TRY(cudaEventRecord(join, Gs[1].s));
+    RBF_CUDA_TRY(cudaStreamWaitEvent(s, join, 0));
+    ctx->ev_pool.push_back(fork);
+    ctx->ev_pool.push_back(join);
+  }
   return RBF_OK;
 }
 

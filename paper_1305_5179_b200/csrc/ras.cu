@@ -24,7 +24,7 @@
 namespace rbf {
 namespace {
 
-constexpr int kMaxCore = 3968;   // core centres held in shared memory by the ext search (48 KB static)
+constexpr int kMaxCore = 3200;   // core centres held in shared memory by the ext search
 
 // ---------------------------------------------------------------- helpers --
 __global__ void flag_cells(const uint32_t* __restrict__ keys, int64_t n, uint32_t* __restrict__ flag) {
@@ -112,19 +112,26 @@ __global__ void cell_core_kernel(const int32_t* __restrict__ core_cell_start, in
 }
 
 // ---------------------------------------------------------- ext search -----
-// One CTA per block.  WRITE=false: count the non-core members; WRITE=true:
-// write them ascending, then append the core.
-template <bool WRITE>
+// One CTA per block, one pass: the non-core members (centres within ov of a
+// core centre, exact fp32 test of reading R8) are written in ascending sorted
+// position to stage[b * cap ...]; their count + nc goes to ext_count[b].
+// Candidates are the centres of the cell rows crossing the core's bounding box
+// dilated by ov; each candidate tests only the core points of core cells whose
+// cell box lies within ov of it (cells are whole in a core, in Morton order).
+constexpr int kMaxCoreCells = 256;
+
 __global__ void __launch_bounds__(256)
 ext_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ cell_start, CellGrid g,
            const int64_t* __restrict__ core_ptr, const int32_t* __restrict__ core_idx,
-           const int32_t* __restrict__ owner, float ov2, float ov, int64_t nblocks,
-           uint32_t* __restrict__ extra_count, const int64_t* __restrict__ ext_ptr, int32_t* __restrict__ ext_idx,
+           const int32_t* __restrict__ owner, const uint32_t* __restrict__ keys, float ov2, float ov,
+           int64_t nblocks, int cap, uint32_t* __restrict__ ext_count, int32_t* __restrict__ stage,
            int* __restrict__ err) {
   __shared__ float cx[kMaxCore], cy[kMaxCore], cz[kMaxCore];
+  __shared__ float cbox[kMaxCoreCells][3];      // lower corner of each core cell
+  __shared__ int cbeg[kMaxCoreCells + 1];       // core-local start of each core cell
+  __shared__ int s_ncells;
   __shared__ float red[6][8];
   __shared__ uint32_t wsum[8];
-  __shared__ uint32_t s_base;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x) {
     const int64_t c0 = core_ptr[b], c1 = core_ptr[b + 1];
@@ -135,10 +142,32 @@ ext_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ cell_s
     }
     float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int i = tid; i < nc; i += blockDim.x) {
-      float4 p = sorted[core_idx[c0 + i]];
+      const int32_t si = core_idx[c0 + i];
+      const float4 p = sorted[si];
       cx[i] = p.x; cy[i] = p.y; cz[i] = p.z;
       mn[0] = fminf(mn[0], p.x); mn[1] = fminf(mn[1], p.y); mn[2] = fminf(mn[2], p.z);
       mx[0] = fmaxf(mx[0], p.x); mx[1] = fmaxf(mx[1], p.y); mx[2] = fmaxf(mx[2], p.z);
+    }
+    // core cells: boundaries where the cell key changes along the core list
+    if (tid == 0) {
+      int nce = 0;
+      uint32_t prev = 0xffffffffu;
+      for (int i = 0; i < nc; ++i) {
+        const uint32_t k = keys[core_idx[c0 + i]];
+        if (k != prev) {
+          if (nce < kMaxCoreCells) {
+            cbeg[nce] = i;
+            const unsigned kx = k % g.dim[0], ky = (k / g.dim[0]) % g.dim[1], kz = k / ((unsigned)g.dim[0] * g.dim[1]);
+            cbox[nce][0] = g.lo[0] + (float)kx * g.h;
+            cbox[nce][1] = g.lo[1] + (float)ky * g.h;
+            cbox[nce][2] = g.lo[2] + (float)kz * g.h;
+          }
+          ++nce;
+          prev = k;
+        }
+      }
+      s_ncells = nce;
+      if (nce <= kMaxCoreCells) cbeg[nce] = nc;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
@@ -155,10 +184,12 @@ ext_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ cell_s
       bl[a] = red[a][0]; bh[a] = red[3 + a][0];
       for (int q = 1; q < (int)(blockDim.x / 32); ++q) { bl[a] = fminf(bl[a], red[a][q]); bh[a] = fmaxf(bh[a], red[3 + a][q]); }
     }
-    if (tid == 0) s_base = 0;
-    __syncthreads();
-    // candidate cells: those intersecting the core's bounding box dilated by ov
-    // (a superset of the members; the exact fp32 test below decides)
+    const int ncells = s_ncells;
+    const bool pruned = ncells <= kMaxCoreCells;
+    // cell-box margin: a centre may sit ~1 ulp outside its cell's nominal box
+    const float cm = g.h * 1e-4f + 1e-6f;
+    const float ovp = ov * 1.0001f + cm;
+    const float ovp2 = ovp * ovp;
     const float pad = ov * 1.0001f + 1e-6f;
     int lo[3], hi[3];
     for (int a = 0; a < 3; ++a) {
@@ -166,8 +197,8 @@ ext_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ cell_s
       lo[a] = (int)fminf(fmaxf(t0, 0.f), (float)(g.dim[a] - 1));
       hi[a] = (int)fminf(fmaxf(t1, 0.f), (float)(g.dim[a] - 1));
     }
-    uint32_t count = 0;   // running count (WRITE: output position base)
-    const int64_t out0 = WRITE ? ext_ptr[b] : 0;
+    uint32_t count = 0;
+    int32_t* out = stage + b * (int64_t)cap;
     for (int z = lo[2]; z <= hi[2]; ++z)
       for (int y = lo[1]; y <= hi[1]; ++y) {
         const int64_t row = ((int64_t)z * g.dim[1] + y) * g.dim[0];
@@ -181,10 +212,24 @@ ext_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ cell_s
             const float gy = fmaxf(0.f, fmaxf(bl[1] - p.y, p.y - bh[1]));
             const float gz = fmaxf(0.f, fmaxf(bl[2] - p.z, p.z - bh[2]));
             if (gx * gx + gy * gy + gz * gz <= ov2 * 1.0002f + 1e-12f) {
-              for (int i = 0; i < nc; ++i) {
-                const float dx = __fsub_rn(p.x, cx[i]), dy = __fsub_rn(p.y, cy[i]), dz = __fsub_rn(p.z, cz[i]);
-                const float d2 = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
-                if (d2 <= ov2) { mem = true; break; }
+              if (pruned) {
+                for (int q = 0; q < ncells && !mem; ++q) {
+                  const float hx = fmaxf(0.f, fmaxf(cbox[q][0] - p.x, p.x - (cbox[q][0] + g.h)));
+                  const float hy = fmaxf(0.f, fmaxf(cbox[q][1] - p.y, p.y - (cbox[q][1] + g.h)));
+                  const float hz = fmaxf(0.f, fmaxf(cbox[q][2] - p.z, p.z - (cbox[q][2] + g.h)));
+                  if (hx * hx + hy * hy + hz * hz > ovp2) continue;
+                  for (int i = cbeg[q]; i < cbeg[q + 1]; ++i) {
+                    const float dx = __fsub_rn(p.x, cx[i]), dy = __fsub_rn(p.y, cy[i]), dz = __fsub_rn(p.z, cz[i]);
+                    const float d2 = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+                    if (d2 <= ov2) { mem = true; break; }
+                  }
+                }
+              } else {
+                for (int i = 0; i < nc; ++i) {
+                  const float dx = __fsub_rn(p.x, cx[i]), dy = __fsub_rn(p.y, cy[i]), dz = __fsub_rn(p.z, cz[i]);
+                  const float d2 = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+                  if (d2 <= ov2) { mem = true; break; }
+                }
               }
             }
           }
@@ -197,17 +242,31 @@ ext_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ cell_s
             if (q < wid) before += wsum[q];
             tot += wsum[q];
           }
-          if (WRITE && mem) ext_idx[out0 + count + before + __popc(bal & ((1u << lane) - 1u))] = j;
+          const uint32_t pos = count + before + __popc(bal & ((1u << lane) - 1u));
+          if (mem && pos + nc < (uint32_t)cap) out[pos] = j;
           count += tot;
           __syncthreads();
         }
       }
-    if (!WRITE) {
-      if (tid == 0) extra_count[b] = count + (uint32_t)nc;
-    } else {
-      for (int i = tid; i < nc; i += blockDim.x) ext_idx[out0 + count + i] = core_idx[c0 + i];
+    if (tid == 0) {
+      ext_count[b] = count + (uint32_t)nc;
+      if (count + nc > (uint32_t)cap) atomicExch(err, 2);
     }
     __syncthreads();
+  }
+}
+
+// ext_idx[ext_ptr[b] ...] = [staged members] + [core]
+__global__ void ext_assemble(const int64_t* __restrict__ core_ptr, const int32_t* __restrict__ core_idx,
+                             const int64_t* __restrict__ ext_ptr, const int32_t* __restrict__ stage, int cap,
+                             int64_t nblocks, int32_t* __restrict__ ext_idx) {
+  for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x) {
+    const int64_t e0 = ext_ptr[b], c0 = core_ptr[b];
+    const int nc = (int)(core_ptr[b + 1] - c0);
+    const int extra = (int)(ext_ptr[b + 1] - e0) - nc;
+    const int32_t* st = stage + b * (int64_t)cap;
+    for (int i = threadIdx.x; i < extra; i += blockDim.x) ext_idx[e0 + i] = st[i];
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) ext_idx[e0 + extra + i] = core_idx[c0 + i];
   }
 }
 
@@ -390,18 +449,21 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
   g.h = (float)c->h;
   const double ov = ovs * kp.sigma;
   const float ov2 = (float)(ov * ov);
-  DevBuf ecount, eptr_u32, err;
+  DevBuf ecount, stage, err;
   RBF_TRY(ecount.alloc(4 * ncore, s));
+  RBF_TRY(stage.alloc(sizeof(int32_t) * (size_t)ncore * max_ext, s));
   RBF_TRY(err.alloc(4, s));
   RBF_CUDA_TRY(cudaMemsetAsync(err.p, 0, 4, s));
   const int eblocks = (int)std::min<int64_t>(ncore, (int64_t)ctx->sm_count * 8);
-  ext_kernel<false><<<eblocks, 256, 0, s>>>(c->sorted.as<float4>(), c->cell_start.as<int32_t>(), g,
-                                            P->core_ptr.as<int64_t>(), P->core_idx.as<int32_t>(),
-                                            owner.as<int32_t>(), ov2, (float)ov, ncore, ecount.as<uint32_t>(),
-                                            nullptr, nullptr, err.as<int>());
+  ext_kernel<<<eblocks, 256, 0, s>>>(c->sorted.as<float4>(), c->cell_start.as<int32_t>(), g,
+                                     P->core_ptr.as<int64_t>(), P->core_idx.as<int32_t>(), owner.as<int32_t>(),
+                                     c->keys.as<uint32_t>(), ov2, (float)ov, ncore, max_ext,
+                                     ecount.as<uint32_t>(), stage.as<int32_t>(), err.as<int>());
   RBF_CHECK_LAUNCH();
   std::vector<uint32_t> h_ecount(ncore);
+  int herr0 = 0;
   RBF_CUDA_TRY(cudaMemcpyAsync(h_ecount.data(), ecount.p, 4 * ncore, cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaMemcpyAsync(&herr0, err.p, 4, cudaMemcpyDeviceToHost, s));
   RBF_CUDA_TRY(cudaStreamSynchronize(s));
   std::vector<int64_t> h_ext_ptr(ncore + 1, 0), h_w_off(ncore + 1, 0);
   int64_t max_m = 0;
@@ -411,7 +473,8 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
     h_w_off[b + 1] = h_w_off[b] + m * nc;
     max_m = std::max(max_m, m);
   }
-  if (max_m > max_ext) {
+  if (herr0 == 1) { set_error("RAS core larger than the ext-search capacity"); return RBF_EUNSUPPORTED; }
+  if (max_m > max_ext || herr0 == 2) {
     set_error("a RAS extended block holds " + std::to_string(max_m) + " centres (> max_ext " +
               std::to_string(max_ext) + ")");
     return RBF_EUNSUPPORTED;
@@ -422,10 +485,9 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
   RBF_CUDA_TRY(cudaMemcpyAsync(P->ext_ptr.p, h_ext_ptr.data(), 8 * (ncore + 1), cudaMemcpyHostToDevice, s));
   RBF_CUDA_TRY(cudaMemcpyAsync(P->w_off.p, h_w_off.data(), 8 * (ncore + 1), cudaMemcpyHostToDevice, s));
   RBF_TRY(P->ext_idx.alloc(4 * h_ext_ptr[ncore], s));
-  ext_kernel<true><<<eblocks, 256, 0, s>>>(c->sorted.as<float4>(), c->cell_start.as<int32_t>(), g,
-                                           P->core_ptr.as<int64_t>(), P->core_idx.as<int32_t>(), owner.as<int32_t>(),
-                                           ov2, (float)ov, ncore, nullptr, P->ext_ptr.as<int64_t>(),
-                                           P->ext_idx.as<int32_t>(), err.as<int>());
+  ext_assemble<<<eblocks, 256, 0, s>>>(P->core_ptr.as<int64_t>(), P->core_idx.as<int32_t>(),
+                                       P->ext_ptr.as<int64_t>(), stage.as<int32_t>(), max_ext, ncore,
+                                       P->ext_idx.as<int32_t>());
   RBF_CHECK_LAUNCH();
   P->h_core_ptr = h_core_ptr;
   P->h_ext_ptr = h_ext_ptr;
