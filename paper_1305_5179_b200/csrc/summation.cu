@@ -82,6 +82,7 @@ struct SumGeom {
   float ci2;    // interior radius^2: cutoff deflated by 1e-4 and the rounding margin
   float s;      // sqrt(k), k = log2(e) / (2 sigma^2)
   int c2bits;   // bits of float32(k c^2)
+  float c2s;    // float32(k c^2)
   float amp;    // a
   // fp64 tier
   double c2d;        // (cutoff_sigmas * sigma)^2 exactly as the oracle forms it
@@ -208,6 +209,7 @@ __device__ __forceinline__ void traverse2(const SumGeom& G, const int32_t* __res
 // ------------------------------------------------------------- fp32 tier ---
 struct Ring32 {
   float* bx; float* by; float* bz; float* bw;
+  float* bs = nullptr;   // |s'|^2 (expansion path only)
 };
 
 // Dual-ring staging of the fp32 fast path (see traverse2).
@@ -215,7 +217,7 @@ struct Stage32x2 {
   Ring32 rb, ri;
   const float4* __restrict__ src;
   float3 blo, bhi, ctr;
-  float cc2, ci2;
+  float cc2, ci2, s;
   float4 p;
   __device__ __forceinline__ int classify(int j, bool valid) {
     p = valid ? __ldg(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -232,15 +234,57 @@ struct Stage32x2 {
     if (kind == 0) return;
     Ring32& r = (kind == 2) ? ri : rb;
     const int pos = (kind == 2) ? posi : posb;
-    r.bx[pos] = p.x - ctr.x;
-    r.by[pos] = p.y - ctr.y;
-    r.bz[pos] = p.z - ctr.z;
+    // scaled tile-local coordinates s' = (x - ctr) sqrt(k) and |s'|^2
+    const float sx = (p.x - ctr.x) * s, sy = (p.y - ctr.y) * s, sz = (p.z - ctr.z) * s;
+    r.bx[pos] = sx;
+    r.by[pos] = sy;
+    r.bz[pos] = sz;
+    r.bs[pos] = fmaf(sz, sz, fmaf(sy, sy, sx * sx));
     r.bw[pos] = p.w;
   }
   __device__ __forceinline__ void shift_ring(Ring32& r, int rest, int lane) {
     if (lane < rest) {
       float a = r.bx[kFlush + lane], b = r.by[kFlush + lane], c = r.bz[kFlush + lane], d = r.bw[kFlush + lane];
-      r.bx[lane] = a; r.by[lane] = b; r.bz[lane] = c; r.bw[lane] = d;
+      float e = r.bs[kFlush + lane];
+      r.bx[lane] = a; r.by[lane] = b; r.bz[lane] = c; r.bw[lane] = d; r.bs[lane] = e;
+    }
+  }
+};
+
+// Inner loop of the fp32 tier by the expansion |s'-t'|^2 = |s'|^2 - 2 t'.s' + |t'|^2
+// in the tile-local scaled frame: rr = |s'|^2 - 2 t'.s' is 3 packed FFMA2 per two
+// pairs, 2^-|t'|^2 is a per-target factor applied once at the end, and the cutoff
+// |s'-t'|^2 <= k c^2 becomes rr <= k c^2 - |t'|^2 (per-target threshold).
+// |t'| <= ~2 (tile half-diagonal), so the rounding of the expansion costs
+// <= ~17u in the exponent where the term is not negligible.
+template <int T, bool MASK>
+struct Flush32e {
+  Ring32 r;
+  float2* acc;                                     // [T]
+  const float* mx; const float* my; const float* mz;   // [T] -2 t'
+  const float* thr;                                // [T] k c^2 - |t'|^2
+  __device__ __forceinline__ float cut(float v, float th) const { return (MASK && !(v <= th)) ? INFINITY : v; }
+  __device__ __forceinline__ void operator()(int cnt) {
+#pragma unroll 2
+    for (int j = 0; j < cnt; j += 4) {
+      const float4 X = *reinterpret_cast<const float4*>(r.bx + j);
+      const float4 Y = *reinterpret_cast<const float4*>(r.by + j);
+      const float4 Z = *reinterpret_cast<const float4*>(r.bz + j);
+      const float4 S = *reinterpret_cast<const float4*>(r.bs + j);
+      const float4 W = *reinterpret_cast<const float4*>(r.bw + j);
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const float2 ax = make_float2(mx[t], mx[t]), ay = make_float2(my[t], my[t]), az = make_float2(mz[t], mz[t]);
+        float2 ra = fma2(make_float2(Z.x, Z.y), az, make_float2(S.x, S.y));
+        float2 rb = fma2(make_float2(Z.z, Z.w), az, make_float2(S.z, S.w));
+        ra = fma2(make_float2(Y.x, Y.y), ay, ra); rb = fma2(make_float2(Y.z, Y.w), ay, rb);
+        ra = fma2(make_float2(X.x, X.y), ax, ra); rb = fma2(make_float2(X.z, X.w), ax, rb);
+        const float th = thr[t];
+        float2 ea = make_float2(ex2(-cut(ra.x, th)), ex2(-cut(ra.y, th)));
+        float2 eb = make_float2(ex2(-cut(rb.x, th)), ex2(-cut(rb.y, th)));
+        acc[t] = fma2(ea, make_float2(W.x, W.y), acc[t]);
+        acc[t] = fma2(eb, make_float2(W.z, W.w), acc[t]);
+      }
     }
   }
 };
@@ -336,11 +380,18 @@ struct FlushStats {
   }
 };
 
-__device__ __forceinline__ void pad_ring(Ring32 r, int nbuf, int lane, int& cnt) {
+// Pads the ring to a multiple of 4 with sources that contribute exactly 0:
+// far away (difference path) or with |s'|^2 = 1e30 (expansion path, 2^-1e30 = 0).
+__device__ __forceinline__ void pad_ring(Ring32 r, int nbuf, int lane, int& cnt, bool expansion = false) {
   cnt = (nbuf + 3) & ~3;
   if (lane < cnt - nbuf) {
     const int q = nbuf + lane;
-    r.bx[q] = 1e18f; r.by[q] = 1e18f; r.bz[q] = 1e18f; r.bw[q] = 0.f;
+    r.bw[q] = 0.f;
+    if (expansion) {
+      r.bx[q] = 0.f; r.by[q] = 0.f; r.bz[q] = 0.f; r.bs[q] = 1e30f;
+    } else {
+      r.bx[q] = 1e18f; r.by[q] = 1e18f; r.bz[q] = 1e18f;
+    }
   }
   __syncwarp();
 }
@@ -362,10 +413,10 @@ sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
                const int2* __restrict__ tiles, const float4* __restrict__ tbox, int64_t ntiles,
                GridDesc gd, OutT* __restrict__ out, const int32_t* __restrict__ out_perm,
                int* __restrict__ work, unsigned long long* __restrict__ stats) {
-  __shared__ __align__(16) float ring[kSumWarps][8][kBufPad];
+  __shared__ __align__(16) float ring[kSumWarps][10][kBufPad];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  Ring32 R{ring[wib][0], ring[wib][1], ring[wib][2], ring[wib][3]};     // boundary sources
-  Ring32 RI{ring[wib][4], ring[wib][5], ring[wib][6], ring[wib][7]};    // interior sources
+  Ring32 R{ring[wib][0], ring[wib][1], ring[wib][2], ring[wib][3], ring[wib][8]};    // boundary sources
+  Ring32 RI{ring[wib][4], ring[wib][5], ring[wib][6], ring[wib][7], ring[wib][9]};   // interior sources
   unsigned long long useful = 0, visited = 0;
   for (;;) {
     int64_t tile;
@@ -419,6 +470,7 @@ sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
       xt[t] = -((xr[t] - ctr.x) * G.s); yt[t] = -((yr[t] - ctr.y) * G.s); zt[t] = -((zr[t] - ctr.z) * G.s);
     }
     float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    float tf[2] = {1.f, 1.f};
     const bool two = tcount > 32;
     if (STATS) {
       Stage32 st{R, src, blo, bhi, ctr, G.cc2, G.s, make_float4(0, 0, 0, 0)};
@@ -430,23 +482,33 @@ sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
       fs(cnt);
       __syncwarp();
     } else {
-      Stage32x2 st{R, RI, src, blo, bhi, ctr, G.cc2, G.ci2, make_float4(0, 0, 0, 0)};
+      // expansion path: per-target -2 t', threshold k c^2 - |t'|^2, factor 2^-|t'|^2
+      float mx[2], my[2], mz[2], th[2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const float tx = (xr[t] - ctr.x) * G.s, ty = (yr[t] - ctr.y) * G.s, tz = (zr[t] - ctr.z) * G.s;
+        const float T2 = fmaf(tz, tz, fmaf(ty, ty, tx * tx));
+        mx[t] = -2.f * tx; my[t] = -2.f * ty; mz[t] = -2.f * tz;
+        th[t] = G.c2s - T2;
+        tf[t] = ex2(-T2);
+      }
+      Stage32x2 st{R, RI, src, blo, bhi, ctr, G.cc2, G.ci2, G.s, make_float4(0, 0, 0, 0)};
       int nB = 0, nI = 0, cnt;
       if (two) {
-        Flush32<2, true> fb{R, acc, xt, yt, zt, G.c2bits, G.s};
-        Flush32<2, false> fi{RI, acc, xt, yt, zt, G.c2bits, G.s};
+        Flush32e<2, true> fb{R, acc, mx, my, mz, th};
+        Flush32e<2, false> fi{RI, acc, mx, my, mz, th};
         traverse2(G, cell_start, blo, bhi, lane, st, fb, fi, nB, nI);
-        pad_ring(R, nB, lane, cnt);
+        pad_ring(R, nB, lane, cnt, true);
         fb(cnt);
-        pad_ring(RI, nI, lane, cnt);
+        pad_ring(RI, nI, lane, cnt, true);
         fi(cnt);
       } else {
-        Flush32<1, true> fb{R, acc, xt, yt, zt, G.c2bits, G.s};
-        Flush32<1, false> fi{RI, acc, xt, yt, zt, G.c2bits, G.s};
+        Flush32e<1, true> fb{R, acc, mx, my, mz, th};
+        Flush32e<1, false> fi{RI, acc, mx, my, mz, th};
         traverse2(G, cell_start, blo, bhi, lane, st, fb, fi, nB, nI);
-        pad_ring(R, nB, lane, cnt);
+        pad_ring(R, nB, lane, cnt, true);
         fb(cnt);
-        pad_ring(RI, nI, lane, cnt);
+        pad_ring(RI, nI, lane, cnt, true);
         fi(cnt);
       }
       __syncwarp();
@@ -455,7 +517,7 @@ sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         if (!tv[t]) continue;
-        float v = G.amp * (acc[t].x + acc[t].y);
+        float v = G.amp * ((acc[t].x + acc[t].y) * tf[t]);
         int64_t o = tidx[t];
         if (MODE == 0 && out_perm) o = out_perm[o];
         out[o] = (OutT)v;
@@ -609,6 +671,7 @@ SumGeom make_geom(const rbf_cells* c, const KernelParams& kp) {
   int bits;
   memcpy(&bits, &c2s, 4);
   G.c2bits = bits;
+  G.c2s = c2s;
   G.amp = (float)kp.amp;
   G.c2d = kp.cutoff * kp.cutoff;
   G.two_s2 = 2.0 * kp.sigma * kp.sigma;
@@ -616,7 +679,17 @@ SumGeom make_geom(const rbf_cells* c, const KernelParams& kp) {
   return G;
 }
 
-int sum_blocks(rbf_ctx* ctx) { return ctx->sm_count * 8; }
+// Persistent grid: as many CTAs as can be resident (the kernels pull tiles from a
+// work counter, so CTAs beyond one wave would only add tail imbalance).
+template <class K>
+int sum_blocks(rbf_ctx* ctx, K kernel) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kSumWarps * 32, 0) != cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    per_sm = 4;
+  }
+  return ctx->sm_count * per_sm;
+}
 
 }  // namespace
 
@@ -641,12 +714,12 @@ rbf_status matvec_sorted_f32(rbf_ctx* ctx, const rbf_cells* c, const KernelParam
   SumGeom G = make_geom(c, kp);
   GridDesc gd{};
   if (pair_stats) {
-    sum_f32_kernel<0, true, float><<<sum_blocks(ctx), kSumWarps * 32, 0, s>>>(
+    sum_f32_kernel<0, true, float><<<sum_blocks(ctx, sum_f32_kernel<0, true, float>), kSumWarps * 32, 0, s>>>(
         G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), c->tiles.as<int2>(), c->tile_box.as<float4>(),
         c->ntiles, gd, f_out, out_perm, ctx->counter.as<int>(), pair_stats);
   } else {
     ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
-    sum_f32_kernel<0, false, float><<<sum_blocks(ctx), kSumWarps * 32, 0, s>>>(
+    sum_f32_kernel<0, false, float><<<sum_blocks(ctx, sum_f32_kernel<0, false, float>), kSumWarps * 32, 0, s>>>(
         G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), c->tiles.as<int2>(), c->tile_box.as<float4>(),
         c->ntiles, gd, f_out, out_perm, ctx->counter.as<int>(), nullptr);
   }
@@ -666,7 +739,7 @@ rbf_status matvec_sorted_f32_d(rbf_ctx* ctx, const rbf_cells* c, const KernelPar
   SumGeom G = make_geom(c, kp);
   GridDesc gd{};
   ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
-  sum_f32_kernel<0, false, double><<<sum_blocks(ctx), kSumWarps * 32, 0, s>>>(
+  sum_f32_kernel<0, false, double><<<sum_blocks(ctx, sum_f32_kernel<0, false, double>), kSumWarps * 32, 0, s>>>(
       G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), c->tiles.as<int2>(), c->tile_box.as<float4>(),
       c->ntiles, gd, f_sorted, nullptr, ctx->counter.as<int>(), nullptr);
   RBF_CHECK_LAUNCH();
@@ -680,7 +753,7 @@ rbf_status matvec_sorted_f64(rbf_ctx* ctx, const rbf_cells* c, const KernelParam
   RBF_CUDA_TRY(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
   SumGeom G = make_geom(c, kp);
   ProfScope ps(ctx, RBF_PROF_MATVEC_F64);
-  sum_f64_kernel<<<sum_blocks(ctx), kSumWarps * 32, 0, s>>>(
+  sum_f64_kernel<<<sum_blocks(ctx, sum_f64_kernel), kSumWarps * 32, 0, s>>>(
       G, c->cell_start.as<int32_t>(), c->sorted.as<float4>(), w_sorted, c->tiles.as<int2>(),
       c->tile_box.as<float4>(), c->ntiles, f_out, out_perm, ctx->counter.as<int>());
   RBF_CHECK_LAUNCH();
@@ -711,14 +784,14 @@ rbf_status eval_grid_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams
   }
   int64_t nblk = (int64_t)gd.nb[0] * gd.nb[1] * gd.nb[2];
   if (pair_stats) {
-    sum_f32_kernel<1, true, float><<<sum_blocks(ctx), kSumWarps * 32, 0, s>>>(
+    sum_f32_kernel<1, true, float><<<sum_blocks(ctx, sum_f32_kernel<1, true, float>), kSumWarps * 32, 0, s>>>(
         G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), nullptr, nullptr, nblk, gd, field, nullptr,
         ctx->counter.as<int>(), pair_stats);
     RBF_CHECK_LAUNCH();
     return RBF_OK;
   }
   ProfScope ps(ctx, RBF_PROF_GRID);
-  sum_f32_kernel<1, false, float><<<sum_blocks(ctx), kSumWarps * 32, 0, s>>>(
+  sum_f32_kernel<1, false, float><<<sum_blocks(ctx, sum_f32_kernel<1, false, float>), kSumWarps * 32, 0, s>>>(
       G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), nullptr, nullptr, nblk, gd, field, nullptr,
       ctx->counter.as<int>(), nullptr);
   RBF_CHECK_LAUNCH();
