@@ -152,6 +152,9 @@ void rbf_destroy(rbf_ctx* ctx);
 const char* rbf_status_str(rbf_status s);
 const char* rbf_last_error(void);
 int rbf_abi_version(void);
+/* Number of CUDA kernels this library has launched in the process so far
+ * (all contexts); host-side counter, no synchronisation. */
+int64_t rbf_launch_count(void);
 
 /* ---- a0: extended interpolation set (§2.1.1-2.1.2) ------------
  * x, nrm: DEVICE fp64, N x 3 (surface points and unit normals).

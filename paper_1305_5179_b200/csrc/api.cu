@@ -3,6 +3,7 @@
 // library's kernels; there is no host compute fallback.
 #include <cmath>
 #include <cstring>
+#include <atomic>
 #include <new>
 
 #include "internal.h"
@@ -12,6 +13,10 @@ namespace {
 thread_local std::string g_last_error;
 }
 void set_error(const std::string& msg) { g_last_error = msg; }
+namespace {
+std::atomic<unsigned long long> g_launches{0};
+}
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 const char* last_error_cstr() { return g_last_error.c_str(); }
 }  // namespace rbf
 
@@ -62,6 +67,8 @@ const char* rbf_status_str(rbf_status s) {
 const char* rbf_last_error(void) { return last_error_cstr(); }
 
 int rbf_abi_version(void) { return RBF_ABI_VERSION; }
+
+int64_t rbf_launch_count(void) { return (int64_t)g_launches.load(std::memory_order_relaxed); }
 
 rbf_status rbf_create(rbf_ctx** out, int device, void* cuda_stream, const void* nccl_unique_id, int rank,
                       int world) {

@@ -27,7 +27,14 @@ void set_error(const std::string& msg);
     if (_s != RBF_OK) return _s;                                               \
   } while (0)
 
-#define RBF_CHECK_LAUNCH() RBF_CUDA_TRY(cudaGetLastError())
+// Every kernel launch of the library is followed by RBF_CHECK_LAUNCH(), which also
+// counts it (rbf_launch_count: the evidence of how many of our kernels ran).
+void count_launch();
+#define RBF_CHECK_LAUNCH()        \
+  do {                            \
+    ::rbf::count_launch();        \
+    RBF_CUDA_TRY(cudaGetLastError()); \
+  } while (0)
 
 constexpr int kWarp = 32;
 

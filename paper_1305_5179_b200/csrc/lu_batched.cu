@@ -487,6 +487,7 @@ rbf_status lu_forward_step(LuGroup& G, int k0, double* ws, int* info) {
   if (k0 >= G.maxm) return RBF_OK;
   G.pcfg.attrs = G.pattr;
   RBF_CUDA_TRY(cudaLaunchKernelEx(&G.pcfg, panel_cluster_kernel, G.jobs_dev, ws, k0, G.piv, G.R, info));
+  count_launch();
   linv_kernel<<<G.nj, kThreads, sm2_bytes(), G.s>>>(G.jobs_dev, ws, k0, G.linv);
   RBF_CHECK_LAUNCH();
   const int ct = std::max(1, std::min((G.maxld - k0 + kNb - 1) / kNb, G.spread));

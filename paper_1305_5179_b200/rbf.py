@@ -81,6 +81,7 @@ EXPORTS = {
     "rbf_status_str": (C.c_char_p, [C.c_int]),
     "rbf_last_error": (C.c_char_p, []),
     "rbf_abi_version": (C.c_int, []),
+    "rbf_launch_count": (C.c_int64, []),
     "rbf_extend_points": (C.c_int, [_P, _P, _P, C.c_int64, C.c_double, C.c_double, _P, _P]),
     "rbf_build_cells": (C.c_int, [_P, _P, C.c_int64, C.POINTER(_Kernel), C.POINTER(_CellCfg),
                                   C.POINTER(_P)]),
@@ -108,6 +109,11 @@ EXPORTS = {
 }
 
 _lib = None
+
+
+def launch_count() -> int:
+    """rbf_launch_count: kernels launched by librbf in this process so far."""
+    return int(load_library().rbf_launch_count())
 
 
 def load_library(path: str = LIB_PATH):
