@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define RBF_ABI_VERSION 1
+#define RBF_ABI_VERSION 2
 
 typedef enum {
   RBF_OK = 0,
@@ -84,12 +84,22 @@ typedef struct {
                             1 => whole cells merged greedily */
 } rbf_cell_cfg;
 
-/* RAS preconditioner (§3.1; reading R8). */
+/* RAS preconditioner (§3.1; readings R8, R9, R17).
+ * The local systems are A_i + shift*a*I (a = the kernel amplitude).  shift = 0
+ * gives the paper's exact local solves; shift > 0 (reading R17) keeps the local
+ * inverses bounded when sigma/spacing makes A_i numerically singular (the
+ * preconditioner stays an approximation of A^-1 either way; GMRES iterates
+ * with the unshifted A).  local_fp32 = 1 factors every block with m <= 224 on
+ * chip in fp32 (Gauss-Jordan, partial pivoting) and stores W in fp32; it is
+ * accurate only when shift*a dominates fp32 rounding of A_i (shift >= ~1e-4).
+ * Larger blocks, and local_fp32 = 0, use the fp64 batched LU and fp64 W. */
 typedef struct {
   int kind;              /* 0 none, 1 block-Jacobi (overlap 0), 2 RAS */
   int core_target;       /* centres per core (whole cells); <= 0 => 512 */
   double overlap_sigmas; /* extended set = centres within overlap*sigma of the core */
   int max_ext;           /* reject blocks larger than this; <= 0 => 4096 */
+  double shift;          /* >= 0; diagonal shift of the local matrices in units of a */
+  int local_fp32;        /* 0 => fp64 LU + fp64 W; 1 => fp32 on-chip inverse + fp32 W */
 } rbf_precond_cfg;
 
 /* Restarted right-preconditioned FGMRES(m).
@@ -204,9 +214,12 @@ rbf_status rbf_matvec_pairs(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kern
 /* ---- a4/a5: RAS preconditioner (§3.1) -------------------------------------
  * Builds blocks (cores = runs of whole non-empty cells in Morton order of
  * ~core_target centres; extended set = centres within overlap of a core
- * centre), assembles each A_ext in fp32, factors it by LU with partial
- * pivoting (the truncated block may be indefinite) and keeps the restricted
- * inverse W_i = (A_ext^-1)[core, :] (fp32).  Synchronises. */
+ * centre), assembles each local matrix B_i = A_ext + shift*a*I from the fp32
+ * centres (entries formed in fp64), inverts it with partial pivoting (the
+ * truncated block may be indefinite) and keeps the restricted inverse
+ * W_i = (B_i^-1)[core, :] (fp64, or fp32 with local_fp32; see rbf_precond_cfg).
+ * Synchronises.  Errors: RBF_EINVAL (kind outside 0..2, shift < 0 or
+ * non-finite, overlap < 0), RBF_EUNSUPPORTED (a block exceeds max_ext). */
 rbf_status rbf_precond_create(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern,
                               const rbf_precond_cfg* cfg, rbf_precond** out);
 void rbf_precond_free(rbf_precond* p);

@@ -19,7 +19,10 @@
       d2_32 = ((dx*dx + dy*dy) + dz*dz) in float32 from float32 coordinates;
       candidates are the cells within Chebyshev distance ceil(ov/h)+1 of a
       core cell;
-    - local ordering: [non-core members ascending by sorted index] + [core].
+    - local ordering: [non-core members ascending by sorted index] + [core];
+    - local matrix B_i = A_i + shift*a*I (reading R17: a diagonal shift keeps
+      the local inverses bounded when sigma/spacing makes A_i numerically
+      singular; the paper's exact local solve is shift = 0).
 * gmres: restarted GMRES(m) with right preconditioning (l.359 "in
   combination with any iterative method like the Krylov subspace methods";
   l.389-391 KSPSolve), modified Gram-Schmidt Arnoldi and Givens rotations as
@@ -32,7 +35,7 @@ import numpy as np
 import scipy.linalg as sla
 
 from .cells import morton3
-from .kernel import dense_matrix
+from .kernel import amplitude, dense_matrix
 
 
 def lu_solve(centres, b, sigma, cutoff_sigmas=6.0, amp=None):
@@ -101,17 +104,22 @@ def ras_blocks(cells, sigma: float, core_target: int = 512, overlap_sigmas: floa
     return blocks
 
 
-def ras_apply(blocks, sorted_centres, r, sigma, cutoff_sigmas=6.0, amp=None, factors=None):
-    """z = sum_i R~_i^T A_i^{-1} R_i r (restricted additive Schwarz), sorted order.
-    `factors` caches the scipy LU of each A_i (fp64)."""
+def ras_apply(blocks, sorted_centres, r, sigma, cutoff_sigmas=6.0, amp=None, factors=None,
+              shift: float = 0.0):
+    """z = sum_i R~_i^T B_i^{-1} R_i r (restricted additive Schwarz), sorted order,
+    B_i = A_i + shift * a * I (reading R17; shift = 0 is the paper's
+    exact local solve A_i^{-1}).  `factors` caches the scipy LU of each B_i (fp64)."""
     r = np.asarray(r, dtype=np.float64)
     z = np.zeros_like(r)
+    a = amplitude(sigma) if amp is None or amp <= 0 else float(amp)
     for k, blk in enumerate(blocks):
         ext = blk["ext"]
         if factors is not None and k in factors:
             f = factors[k]
         else:
-            f = sla.lu_factor(dense_matrix(sorted_centres[ext], sigma, cutoff_sigmas, amp))
+            B = dense_matrix(sorted_centres[ext], sigma, cutoff_sigmas, amp)
+            B[np.diag_indices_from(B)] += shift * a
+            f = sla.lu_factor(B)
             if factors is not None:
                 factors[k] = f
         y = sla.lu_solve(f, r[ext])

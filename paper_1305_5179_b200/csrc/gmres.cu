@@ -131,7 +131,7 @@ struct Solver {
     RBF_TRY(w.alloc(sizeof(double) * n, s));
     RBF_TRY(f.alloc(sizeof(double) * n, s));
     RBF_TRY(b.alloc(sizeof(double) * n, s));
-    nblk = ctx->sm_count * 2;
+    nblk = ctx->sm_count * 8;   // 64 warps per SM in flight for the HBM-bound multi-dot
     RBF_TRY(partial.alloc(sizeof(double) * (size_t)nblk * (m + 2), s));
     RBF_TRY(dots.alloc(sizeof(double) * 4 * (m + 2), s));
     return RBF_OK;

@@ -285,7 +285,7 @@ using WT = double;
 // oracle forms them: a * exp(-d2 / (2 sigma^2)), d2 = (dx^2 + dy^2) + dz^2 in fp64.
 __global__ void assemble_kernel(const LuJob* __restrict__ jobs, const float4* __restrict__ sorted,
                                 const int32_t* __restrict__ ext_idx, FT* __restrict__ ws, double amp,
-                                double two_s2, double c2) {
+                                double two_s2, double c2, double shift_abs) {
   const LuJob J = jobs[blockIdx.y];
   const int m = J.m, nc = J.nc, ld = m + nc;
   FT* A = ws + J.ws_off;
@@ -300,6 +300,7 @@ __global__ void assemble_kernel(const LuJob* __restrict__ jobs, const float4* __
                      dz = (double)pi.z - (double)pj.z;
         const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
         v = d2 <= c2 ? amp * exp(-d2 / two_s2) : 0.0;
+        if (c == i) v += shift_abs;
       } else {
         v = (i == m - nc + (c - m)) ? 1.0 : 0.0;
       }
@@ -308,12 +309,133 @@ __global__ void assemble_kernel(const LuJob* __restrict__ jobs, const float4* __
   }
 }
 
+// --------------------------------------------- on-chip fp32 inversion -----
+// local_fp32 path (reading R17): one CTA per block holds
+// B = A_ext + shift*a*I (m <= kGjMax, fp32, entries formed in fp64 exactly as
+// assemble_kernel forms them and rounded once) in shared memory and inverts it
+// in place by Gauss-Jordan elimination with partial pivoting (largest |b_ik|,
+// lowest row on ties).  Step k: pivot row swap; f_i = B[i][k]; B[k][:] /= B[k][k]
+// with B[k][k] := 1/pivot; B[i][:] -= f_i B[k][:] for i != k with B[i][k] := 0
+// first.  The row swaps turn into column swaps of the result, undone in
+// reverse order through the permutation pi (write-out reads column pi[e]).
+// Work per block: m^3 FMAs, m steps of 3 block barriers; HBM sees the W write
+// (4 nc m bytes) and the centre reads only.
+constexpr int kGjMax = 224;
+constexpr int kGjThreads = 512;
+
+__global__ void __launch_bounds__(kGjThreads)
+gj_inverse_f32_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __restrict__ core_ptr,
+                      const int32_t* __restrict__ ext_idx, const int64_t* __restrict__ w_off,
+                      const float4* __restrict__ sorted, double amp, double two_s2, double c2,
+                      double shift_abs, float* __restrict__ W, const int64_t* __restrict__ blist,
+                      int64_t nlist, int* __restrict__ info) {
+  extern __shared__ float B[];          // m x ld, ld = m + 1 (odd: conflict-free column reads)
+  __shared__ float col[kGjMax];
+  __shared__ int piv[kGjMax], pi[kGjMax];
+  __shared__ float4 pos[kGjMax];
+  __shared__ int s_p;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int64_t t = blockIdx.x; t < nlist; t += gridDim.x) {
+    const int64_t b = blist[t];
+    const int64_t e0 = ext_ptr[b];
+    const int m = (int)(ext_ptr[b + 1] - e0);
+    const int nc = (int)(core_ptr[b + 1] - core_ptr[b]);
+    const int ld = m + 1;
+    for (int i = tid; i < m; i += kGjThreads) pos[i] = sorted[ext_idx[e0 + i]];
+    __syncthreads();
+    for (int q = tid; q < m * m; q += kGjThreads) {
+      const int i = q / m, j = q - i * m;
+      const float4 pi4 = pos[i], pj4 = pos[j];
+      const double dx = (double)pi4.x - (double)pj4.x, dy = (double)pi4.y - (double)pj4.y,
+                   dz = (double)pi4.z - (double)pj4.z;
+      const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+      double v = d2 <= c2 ? amp * exp(-d2 / two_s2) : 0.0;
+      if (i == j) v += shift_abs;
+      B[i * ld + j] = (float)v;
+    }
+    __syncthreads();
+    int singular = 0;
+    for (int k = 0; k < m; ++k) {
+      if (wid == 0) {
+        float best = -1.0f;
+        int bi = k;
+        for (int i = k + lane; i < m; i += 32) {
+          const float v = fabsf(B[i * ld + k]);
+          if (v > best) { best = v; bi = i; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+        }
+        if (lane == 0) { s_p = bi; piv[k] = bi; }
+      }
+      __syncthreads();
+      const int p = s_p;
+      if (p != k)
+        for (int j = tid; j < m; j += kGjThreads) {
+          const float t = B[k * ld + j];
+          B[k * ld + j] = B[p * ld + j];
+          B[p * ld + j] = t;
+        }
+      __syncthreads();
+      const float pv = B[k * ld + k];
+      if (pv == 0.0f) singular = 1;
+      const float d = 1.0f / pv;
+      for (int i = tid; i < m; i += kGjThreads) col[i] = (i == k) ? 0.0f : B[i * ld + k];
+      // every warp keeps the scaled pivot row in registers (lane owns j = lane + 32 t)
+      float rk[kGjMax / 32];
+#pragma unroll
+      for (int t = 0; t < kGjMax / 32; ++t) {
+        const int j = lane + 32 * t;
+        rk[t] = (j < m) ? ((j == k) ? d : B[k * ld + j] * d) : 0.0f;
+      }
+      __syncthreads();
+      for (int i = wid; i < m; i += kGjThreads / 32) {
+        float* row = B + i * ld;
+        if (i == k) {
+#pragma unroll
+          for (int t = 0; t < kGjMax / 32; ++t) {
+            const int j = lane + 32 * t;
+            if (j < m) row[j] = rk[t];
+          }
+          continue;
+        }
+        const float f = col[i];
+#pragma unroll
+        for (int t = 0; t < kGjMax / 32; ++t) {
+          const int j = lane + 32 * t;
+          if (j < m) row[j] = fmaf(-f, rk[t], (j == k) ? 0.0f : row[j]);
+        }
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      for (int j = 0; j < m; ++j) pi[j] = j;
+      for (int k = m - 1; k >= 0; --k) {
+        const int t = pi[k];
+        pi[k] = pi[piv[k]];
+        pi[piv[k]] = t;
+      }
+      if (singular) atomicAdd(info, 1);
+    }
+    __syncthreads();
+    float* Wb = W + w_off[b];
+    for (int q = tid; q < nc * m; q += kGjThreads) {
+      const int c = q / m, e = q - c * m;
+      Wb[q] = B[(m - nc + c) * ld + pi[e]];
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- apply ----
-// One CTA per block: r_ext -> shared memory (fp32), z[core_c] = W[c,:] . r_ext
-template <class VT>
+// One CTA per block: r_ext -> shared memory (fp64), z[core_c] = W[c,:] . r_ext
+template <class VT, class WT2>
 __global__ void __launch_bounds__(256)
 apply_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __restrict__ core_ptr,
-             const int32_t* __restrict__ ext_idx, const int64_t* __restrict__ w_off, const WT* __restrict__ W,
+             const int32_t* __restrict__ ext_idx, const int64_t* __restrict__ w_off, const WT2* __restrict__ W,
              const VT* __restrict__ r, VT* __restrict__ z, int64_t nblocks) {
   extern __shared__ double sr[];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarp = blockDim.x >> 5;
@@ -323,9 +445,9 @@ apply_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __restrict__ co
     const int nc = (int)(core_ptr[b + 1] - core_ptr[b]);
     for (int e = tid; e < m; e += blockDim.x) sr[e] = (double)r[ext_idx[e0 + e]];
     __syncthreads();
-    const WT* Wb = W + w_off[b];
+    const WT2* Wb = W + w_off[b];
     for (int c = wid; c < nc; c += nwarp) {
-      const WT* row = Wb + (int64_t)c * m;
+      const WT2* row = Wb + (int64_t)c * m;
       double acc = 0.0;
       for (int e = lane; e < m; e += 32) acc = fma((double)__ldg(row + e), sr[e], acc);
 #pragma unroll
@@ -333,6 +455,16 @@ apply_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __restrict__ co
       if (lane == 0) z[ext_idx[e0 + (m - nc) + c]] = (VT)acc;
     }
     __syncthreads();
+  }
+}
+
+// fp64 restricted inverses of the blocks too large for the on-chip path,
+// rounded into the fp32 W (local_fp32): triples (src offset, dst offset, count)
+__global__ void round_w_kernel(const int64_t* __restrict__ trip, int64_t ntrip, const double* __restrict__ src,
+                               float* __restrict__ dst) {
+  for (int64_t t = blockIdx.x; t < ntrip; t += gridDim.x) {
+    const int64_t so = trip[3 * t], d0 = trip[3 * t + 1], cnt = trip[3 * t + 2];
+    for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) dst[d0 + i] = (float)src[so + i];
   }
 }
 
@@ -357,6 +489,11 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
   const double ovs = (P->kind == 1) ? 0.0 : (cfg ? cfg->overlap_sigmas : 1.0);
   const int max_ext = (cfg && cfg->max_ext > 0) ? cfg->max_ext : 4096;
   if (ovs < 0 || !std::isfinite(ovs)) { set_error("overlap_sigmas must be >= 0"); return RBF_EINVAL; }
+  const double shift = cfg ? cfg->shift : 0.0;
+  if (!(shift >= 0) || !std::isfinite(shift)) { set_error("shift must be finite and >= 0"); return RBF_EINVAL; }
+  P->shift = shift;
+  const double shift_abs = shift * kp.amp;
+  const bool want_fp32 = cfg && cfg->local_fp32;
 
   // 1. non-empty cells
   const int64_t nne = c->nonempty;
@@ -491,38 +628,94 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
   RBF_CHECK_LAUNCH();
   P->h_core_ptr = h_core_ptr;
   P->h_ext_ptr = h_ext_ptr;
-  // 5. assemble + factor + restricted inverse, in chunks bounded by workspace bytes
-  RBF_TRY(P->W.alloc(sizeof(WT) * (size_t)std::max<int64_t>(h_w_off[ncore], 1), s));
-  const int64_t ws_limit = (int64_t)16 << 30;  // workspace bytes per chunk
+  // 5. assemble + factor + restricted inverse
   const double two_s2 = 2.0 * kp.sigma * kp.sigma;
   const double c2 = kp.cutoff * kp.cutoff;
   DevBuf ws, jobs_d, info;
   RBF_TRY(info.alloc(4, s));
   RBF_CUDA_TRY(cudaMemsetAsync(info.p, 0, 4, s));
+  // local_fp32 (reading R17): blocks with m <= kGjMax are inverted on chip in
+  // fp32; larger ones go through the fp64 batched LU and are rounded into W.
+  P->w_fp32 = want_fp32;
+  std::vector<int64_t> small, big;
+  int64_t small_max_m = 0, big_w = 0;
+  for (int64_t b = 0; b < ncore; ++b) {
+    const int64_t m = h_ext_ptr[b + 1] - h_ext_ptr[b];
+    if (want_fp32 && m <= kGjMax) {
+      small.push_back(b);
+      small_max_m = std::max(small_max_m, m);
+    } else {
+      big.push_back(b);
+      big_w += h_w_off[b + 1] - h_w_off[b];
+    }
+  }
+  P->gj_blocks = (int64_t)small.size();
+  if (P->w_fp32) {
+    RBF_TRY(P->W.alloc(sizeof(float) * (size_t)std::max<int64_t>(h_w_off[ncore], 1), s));
+  } else {
+    RBF_TRY(P->W.alloc(sizeof(WT) * (size_t)std::max<int64_t>(h_w_off[ncore], 1), s));
+  }
+  DevBuf blist;
+  if (!small.empty()) {
+    RBF_TRY(blist.alloc(8 * small.size(), s));
+    RBF_CUDA_TRY(cudaMemcpyAsync(blist.p, small.data(), 8 * small.size(), cudaMemcpyHostToDevice, s));
+    const size_t smem = sizeof(float) * (size_t)small_max_m * (small_max_m + 1);
+    RBF_CUDA_TRY(cudaFuncSetAttribute(gj_inverse_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    RBF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gj_inverse_f32_kernel, kGjThreads, smem));
+    const int gblocks = (int)std::min<int64_t>((int64_t)small.size(), (int64_t)ctx->sm_count * std::max(per_sm, 1));
+    gj_inverse_f32_kernel<<<gblocks, kGjThreads, smem, s>>>(
+        P->ext_ptr.as<int64_t>(), P->core_ptr.as<int64_t>(), P->ext_idx.as<int32_t>(), P->w_off.as<int64_t>(),
+        c->sorted.as<float4>(), kp.amp, two_s2, c2, shift_abs, P->W.as<float>(), blist.as<int64_t>(),
+        (int64_t)small.size(), info.as<int>());
+    RBF_CHECK_LAUNCH();
+  }
+  const int64_t ws_limit = (int64_t)16 << 30;  // fp64 LU workspace bytes per chunk
+  DevBuf w64;                                  // fp64 W of the big blocks when W is fp32
+  std::vector<int64_t> trip;
+  if (P->w_fp32 && !big.empty()) RBF_TRY(w64.alloc(sizeof(double) * (size_t)big_w, s));
   std::vector<LuJob> jobs;
-  int64_t b = 0;
-  while (b < ncore) {
+  size_t bi = 0;
+  int64_t tmp_off = 0;
+  while (bi < big.size()) {
     jobs.clear();
     int64_t used = 0;
-    while (b < ncore && (int)jobs.size() < 4096) {
+    while (bi < big.size() && (int)jobs.size() < 4096) {
+      const int64_t b = big[bi];
       const int m = (int)(h_ext_ptr[b + 1] - h_ext_ptr[b]);
       const int nc = (int)(h_core_ptr[b + 1] - h_core_ptr[b]);
       const int64_t need = (int64_t)m * (m + nc);
       if (!jobs.empty() && (used + need) * (int64_t)sizeof(FT) > ws_limit) break;
-      jobs.push_back(LuJob{used, h_ext_ptr[b], h_w_off[b], m, nc});
+      int64_t wo = h_w_off[b];
+      if (P->w_fp32) {
+        trip.insert(trip.end(), {tmp_off, h_w_off[b], (int64_t)m * nc});
+        wo = tmp_off;
+        tmp_off += (int64_t)m * nc;
+      }
+      jobs.push_back(LuJob{used, h_ext_ptr[b], wo, m, nc});
       used += need;
-      ++b;
+      ++bi;
     }
     RBF_TRY(ws.ensure(sizeof(FT) * (size_t)used, s));
     RBF_TRY(jobs_d.ensure(sizeof(LuJob) * jobs.size(), s));
     RBF_CUDA_TRY(cudaMemcpyAsync(jobs_d.p, jobs.data(), sizeof(LuJob) * jobs.size(), cudaMemcpyHostToDevice, s));
     dim3 ag(32, (unsigned)jobs.size());
     assemble_kernel<<<ag, 256, 0, s>>>(jobs_d.as<LuJob>(), c->sorted.as<float4>(), P->ext_idx.as<int32_t>(),
-                                       ws.as<FT>(), kp.amp, two_s2, c2);
+                                       ws.as<FT>(), kp.amp, two_s2, c2, shift_abs);
     RBF_CHECK_LAUNCH();
-    RBF_TRY(batched_lu_restricted_inverse(ctx, jobs_d.as<LuJob>(), jobs, ws.as<FT>(), P->W.as<WT>(),
-                                          info.as<int>()));
+    RBF_TRY(batched_lu_restricted_inverse(ctx, jobs_d.as<LuJob>(), jobs, ws.as<FT>(),
+                                          P->w_fp32 ? w64.as<double>() : P->W.as<WT>(), info.as<int>()));
     // the host vector is reused: wait before the next chunk overwrites jobs_d
+    RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  if (!trip.empty()) {
+    DevBuf trip_d;
+    const int64_t nt = (int64_t)trip.size() / 3;
+    RBF_TRY(trip_d.alloc(8 * trip.size(), s));
+    RBF_CUDA_TRY(cudaMemcpyAsync(trip_d.p, trip.data(), 8 * trip.size(), cudaMemcpyHostToDevice, s));
+    round_w_kernel<<<(unsigned)std::min<int64_t>(nt, 4096), 256, 0, s>>>(trip_d.as<int64_t>(), nt,
+                                                                          w64.as<double>(), P->W.as<float>());
+    RBF_CHECK_LAUNCH();
     RBF_CUDA_TRY(cudaStreamSynchronize(s));
   }
   int herr = 0, hinfo = 0;
@@ -547,13 +740,24 @@ rbf_status precond_apply_sorted(rbf_ctx* ctx, const rbf_precond* P, const VT* r,
   }
   const int blocks = (int)std::min<int64_t>(P->nblocks, (int64_t)ctx->sm_count * 16);
   const size_t smem = sizeof(double) * (size_t)P->max_m;
+  if (P->w_fp32) {
+    if (smem > 48 * 1024)
+      RBF_CUDA_TRY(cudaFuncSetAttribute(apply_kernel<VT, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+    ProfScope ps(ctx, RBF_PROF_PRECOND_APPLY);
+    apply_kernel<VT, float><<<blocks, 256, smem, s>>>(P->ext_ptr.as<int64_t>(), P->core_ptr.as<int64_t>(),
+                                                      P->ext_idx.as<int32_t>(), P->w_off.as<int64_t>(),
+                                                      P->W.as<float>(), r, z, P->nblocks);
+    RBF_CHECK_LAUNCH();
+    return RBF_OK;
+  }
   if (smem > 48 * 1024) {
-    RBF_CUDA_TRY(cudaFuncSetAttribute(apply_kernel<VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RBF_CUDA_TRY(cudaFuncSetAttribute(apply_kernel<VT, WT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }
   ProfScope ps(ctx, RBF_PROF_PRECOND_APPLY);
-  apply_kernel<VT><<<blocks, 256, smem, s>>>(P->ext_ptr.as<int64_t>(), P->core_ptr.as<int64_t>(),
-                                             P->ext_idx.as<int32_t>(), P->w_off.as<int64_t>(), P->W.as<WT>(), r, z,
-                                             P->nblocks);
+  apply_kernel<VT, WT><<<blocks, 256, smem, s>>>(P->ext_ptr.as<int64_t>(), P->core_ptr.as<int64_t>(),
+                                                 P->ext_idx.as<int32_t>(), P->w_off.as<int64_t>(), P->W.as<WT>(), r,
+                                                 z, P->nblocks);
   RBF_CHECK_LAUNCH();
   return RBF_OK;
 }

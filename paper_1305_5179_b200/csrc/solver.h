@@ -11,6 +11,9 @@ struct rbf_precond {
   int64_t bytes = 0;
   int max_m = 0;
   int singular_blocks = 0;
+  double shift = 0.0;     // diagonal shift of the local matrices, units of the amplitude a
+  bool w_fp32 = false;    // W stored in fp32 (local_fp32)
+  int64_t gj_blocks = 0;  // blocks inverted on chip in fp32 (the rest by the fp64 batched LU)
   double t_setup = 0.0;
   const rbf_cells* cells = nullptr;
   rbf::DevBuf core_ptr;   // int64[nblocks+1]
@@ -18,7 +21,8 @@ struct rbf_precond {
   rbf::DevBuf core_idx;   // int32[n]           sorted positions, block-major
   rbf::DevBuf ext_idx;    // int32[ext_ptr[nb]] sorted positions: [extra ascending] + [core]
   rbf::DevBuf w_off;      // int64[nblocks+1]   float offsets of W_i
-  rbf::DevBuf W;          // fp64: W_i (nc_i x m_i) row-major = (A_ext^-1)[core, :]
+  rbf::DevBuf W;          // fp64 or fp32 (w_fp32): W_i (nc_i x m_i) row-major = (B_i^-1)[core, :],
+                          // B_i = A_ext + shift*a*I
   std::vector<int64_t> h_core_ptr, h_ext_ptr;
 };
 

@@ -408,7 +408,7 @@ __device__ __forceinline__ float node_coord(const GridDesc& gd, int a, int i) {
 }
 
 template <int MODE, bool STATS, class OutT>
-__global__ void __launch_bounds__(kSumWarps * 32)
+__global__ void __launch_bounds__(kSumWarps * 32, 8)
 sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* __restrict__ src,
                const int2* __restrict__ tiles, const float4* __restrict__ tbox, int64_t ntiles,
                GridDesc gd, OutT* __restrict__ out, const int32_t* __restrict__ out_perm,

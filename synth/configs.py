@@ -29,6 +29,9 @@ class Config:
     restart: int = 50
     core_target: int = 512
     overlap_sigmas: float = 1.0
+    precond_kind: int = 2     # 0 none, 1 block-Jacobi, 2 RAS (include/rbf.h)
+    shift: float = 0.0        # local diagonal shift in units of a (reading R17)
+    local_fp32: int = 0       # fp32 on-chip local inverses (reading R17)
     kw: dict = field(default_factory=dict)
 
 
@@ -40,13 +43,16 @@ CONFIGS = {
     "c2": Config("c2", "torus", 20000, 0.05, 0.005, 128, overlap_sigmas=1.3,
                  kw=dict(R=1.0, r=0.35, noise=1e-3)),
     # configs[2]: blobby K=16, N=200k, 10x density, sigma 0.02 (delta = 0.1 sigma, reading 4)
-    "c3": Config("c3", "blobby", 200000, 0.02, 0.002, 256,
-                 kw=dict(K=16, density_mod=True)),
-    # configs[3]: blobby K=64, N=1M, sigma 0.01, RAS ~512, 256^3  (the metric config)
-    "c4": Config("c4", "blobby", 1000000, 0.01, 0.001, 256, kw=dict(K=64)),
+    # c3-c5 sit at sigma/spacing ~3-4 where exact local solves stall GMRES (DESIGN.md
+    # finding F4): shifted block-Jacobi local solves, fp32 on chip (reading R17)
+    "c3": Config("c3", "blobby", 200000, 0.02, 0.002, 256, core_target=128, overlap_sigmas=0.0,
+                 precond_kind=1, shift=0.01, local_fp32=1, kw=dict(K=16, density_mod=True)),
+    # configs[3]: blobby K=64, N=1M, sigma 0.01, 256^3  (the metric config)
+    "c4": Config("c4", "blobby", 1000000, 0.01, 0.001, 256, core_target=128, overlap_sigmas=0.0,
+                 precond_kind=1, shift=0.01, local_fp32=1, kw=dict(K=64)),
     # configs[4]: blobby K=64 with 5 caps removed, N=10M, sigma 0.004, 512^3
-    "c5": Config("c5", "blobby", 10000000, 0.004, 0.0004, 512,
-                 kw=dict(K=64, holes=5)),
+    "c5": Config("c5", "blobby", 10000000, 0.004, 0.0004, 512, core_target=128, overlap_sigmas=0.0,
+                 precond_kind=1, shift=0.01, local_fp32=1, kw=dict(K=64, holes=5)),
 }
 
 

@@ -52,7 +52,7 @@ def test_library_loads_and_binds_without_gpu(lib_path):
     import ctypes
     from paper_1305_5179_b200 import rbf
     lib = rbf.load_library(lib_path)
-    assert lib.rbf_abi_version() == 1
+    assert lib.rbf_abi_version() == 2
     assert lib.rbf_status_str(1) == b"RBF_EINVAL"
     for name in rbf.EXPORTS:
         assert hasattr(lib, name)

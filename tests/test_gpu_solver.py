@@ -92,6 +92,103 @@ def test_ras_apply_parity(R, ctx):
     assert err <= 1e-3, err
 
 
+@pytest.mark.parametrize("kind,core,ov,mu", [(2, 256, 2.0, 0.05), (1, 128, 0.0, 0.01)])
+def test_shifted_apply_parity_fp64(R, ctx, kind, core, ov, mu):
+    """Reading R17, fp64 local factors: z = sum_i R~_i^T (A_i + mu a I)^{-1} R_i r
+    against the oracle's scipy LU of the same shifted blocks."""
+    rng = np.random.default_rng(11)
+    X = rng.uniform(-1, 1, (6000, 3)).astype(np.float32)
+    sigma = 0.04
+    kern = R.Kernel(sigma)
+    h = 6 * sigma / 3.999
+    cells = R.Cells(ctx, dev(X, torch.float32), kern, cell_edge=h)
+    P = R.Precond(ctx, cells, kern, kind=kind, core_target=core, overlap_sigmas=ov, shift=mu)
+    r = rng.normal(size=6000).astype(np.float32)
+    z = host(P.apply(dev(r, torch.float32)))
+    oc = OC.build(X, 6 * sigma, cell_edge=h)
+    blocks = OS.ras_blocks(oc, sigma, core, ov)
+    perm = oc["perm"]
+    zs = OS.ras_apply(blocks, oc["sorted"], r.astype(np.float64)[perm], sigma, shift=mu)
+    zref = np.empty_like(zs)
+    zref[perm] = zs
+    # fp64 factors; z is rounded to fp32 once
+    err = np.linalg.norm(z - zref) / np.linalg.norm(zref)
+    assert err <= 1e-6, err
+
+
+def _flat_cap(ratio=3.0, n_sphere=6000, zcut=0.55):
+    """+-delta triplets of a sphere cap at sigma/spacing = ratio (c4's regime):
+    the setting of DESIGN.md finding F4."""
+    from synth.surfaces import fibonacci_sphere
+    xs, nrm = fibonacci_sphere(n_sphere)
+    sel = xs[:, 2] > zcut
+    xs, nrm = xs[sel], nrm[sel]
+    sigma = ratio * np.sqrt(4 * np.pi / n_sphere)
+    delta = 0.1 * sigma
+    X = OE.extend(xs, nrm, delta)
+    b = OE.labels(len(xs), delta).astype(np.float32).astype(np.float64)
+    return X, b, sigma
+
+
+@pytest.mark.parametrize("core", [128, 256])
+def test_gj_fp32_apply_parity(R, ctx, core):
+    """Reading R17, on-chip fp32 Gauss-Jordan factors (local_fp32=1) against the
+    oracle's fp64 LU of the same shifted blocks.  Bound: the fp32 inverse of B
+    carries a relative error <= c kappa(B) m u32 (u32 = 2^-24); kappa(B) is
+    computed here from the oracle's blocks, c = 4."""
+    X, _, sigma = _flat_cap()
+    mu = 0.01
+    kern = R.Kernel(sigma)
+    cells = R.Cells(ctx, dev(X, torch.float32), kern)
+    P = R.Precond(ctx, cells, kern, kind=1, core_target=core, shift=mu, local_fp32=1)
+    cores, exts, nbytes = P.blocks()
+    oc = OC.build(X, 6 * sigma, cell_edge=6 * sigma / 3.999)
+    blocks = OS.ras_blocks(oc, sigma, core, 0.0)
+    # core 256 puts blocks on both sides of the on-chip limit (m <= 224 fp32
+    # Gauss-Jordan; larger ones fp64 LU rounded into the fp32 W)
+    if core == 256:
+        ms = [len(e) for e in exts]
+        assert min(ms) <= 224 < max(ms), (min(ms), max(ms))
+    assert len(cores) == len(blocks)
+    assert all(np.array_equal(c, b_["core"]) for c, b_ in zip(cores, blocks))
+    # W is fp32: bytes = 4 * sum m^2 (+ index arrays)
+    assert nbytes < 8 * sum(len(e) ** 2 for e in exts)
+    a = OK.amplitude(sigma)
+    kappa, mmax = 0.0, 0
+    for blk in blocks:
+        B = OK.dense_matrix(oc["sorted"][blk["ext"]], sigma) + mu * a * np.eye(len(blk["ext"]))
+        kappa = max(kappa, np.linalg.cond(B))
+        mmax = max(mmax, len(blk["ext"]))
+    rng = np.random.default_rng(12)
+    r = rng.normal(size=len(X)).astype(np.float32)
+    z = host(P.apply(dev(r, torch.float32)))
+    perm = oc["perm"]
+    zs = OS.ras_apply(blocks, oc["sorted"], r.astype(np.float64)[perm], sigma, shift=mu)
+    zref = np.empty_like(zs)
+    zref[perm] = zs
+    err = np.linalg.norm(z - zref) / np.linalg.norm(zref)
+    bound = 4 * kappa * mmax * 2.0 ** -24
+    assert err <= bound, (err, bound, kappa, mmax)
+
+
+def test_shifted_bj_solve_at_flat_ratio(R, ctx):
+    """Finding F4 on the GPU: at sigma/spacing 3 the exact-RAS solve stalls,
+    shifted block-Jacobi (fp32 on-chip factors) reaches < 1e-2 in 30 iterations;
+    both residuals are certified by the ORACLE's fp64 matvec."""
+    X, b, sigma = _flat_cap()
+    kern = R.Kernel(sigma)
+    cells = R.Cells(ctx, dev(X, torch.float32), kern)
+    bd = dev(b, torch.float32)
+    out = {}
+    for name, kw in (("exact-ras", dict(kind=2, core_target=128, overlap_sigmas=1.0)),
+                     ("shifted-bj", dict(kind=1, core_target=128, shift=0.01, local_fp32=1))):
+        w, rep = R.gmres_solve(ctx, cells, kern, bd, restart=30, rtol=1e-6, max_iters=30, **kw)
+        res = np.linalg.norm(b - OK.matvec(X, host(w), sigma)) / np.linalg.norm(b)
+        assert abs(res - rep["rel_residual_true"]) <= 1e-6 + 1e-6 * res, (res, rep)
+        out[name] = res
+    assert out["shifted-bj"] < 1e-2 and out["shifted-bj"] < 0.1 * out["exact-ras"], out
+
+
 def test_precond_none_and_jacobi_are_valid(R, ctx):
     d, X, b = problem("c1")
     kern = R.Kernel(d["sigma"])

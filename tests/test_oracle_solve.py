@@ -68,6 +68,66 @@ def test_ras_single_block_is_exact():
     assert info["iters"] == 1 and info["converged"]
 
 
+def test_ras_shift_single_block_solves_shifted_system():
+    """Reading R17: with one subdomain and shift mu the RAS apply is
+    (A + mu a I)^{-1} r with a = 1/(sqrt(2 pi) sigma).  Checked by multiplying
+    back with the brute-force row matvec (an independent code path) plus the
+    mu a r term; a dropped a, a wrong sign or an off-diagonal shift fails."""
+    X, _, sigma = _small_problem(4, n=200)
+    cells = C.build(X, 6 * sigma)
+    blocks = S.ras_blocks(cells, sigma, core_target=10_000, overlap_sigmas=0.0)
+    Ss = cells["sorted"].astype(np.float64)
+    r = np.random.default_rng(5).normal(size=200)
+    a = 1.0 / (np.sqrt(2 * np.pi) * sigma)
+    for mu in (0.0, 0.01, 0.3):
+        z = S.ras_apply(blocks, Ss, r, sigma, shift=mu)
+        back = K.matvec(Ss, z, sigma) + mu * a * z
+        np.testing.assert_allclose(back, r, rtol=0, atol=1e-9 * np.abs(r).max())
+
+
+def test_ras_shift_large_limit_and_monotone_norm():
+    """mu -> infinity: B^{-1} r -> r / (mu a) (Neumann series, error O(||A||/(mu a)));
+    ||z|| decreases with mu for the SPD single-site-dominated blocks used here."""
+    X, _, sigma = _small_problem(6, n=150, sigma=0.05)
+    cells = C.build(X, 6 * sigma)
+    blocks = S.ras_blocks(cells, sigma, core_target=40, overlap_sigmas=0.0)
+    Ss = cells["sorted"].astype(np.float64)
+    r = np.random.default_rng(7).normal(size=150)
+    a = 1.0 / (np.sqrt(2 * np.pi) * sigma)
+    mu = 1e6
+    z = S.ras_apply(blocks, Ss, r, sigma, shift=mu)
+    np.testing.assert_allclose(z * mu * a, r, rtol=1e-4)
+    norms = [np.linalg.norm(S.ras_apply(blocks, Ss, r, sigma, shift=m)) for m in (0.01, 0.1, 1.0, 10.0)]
+    assert all(x > y for x, y in zip(norms, norms[1:]))
+
+
+def test_shifted_block_jacobi_beats_exact_ras_at_flat_ratio():
+    """DESIGN.md finding F4 in miniature: at sigma/spacing ~3 with +-delta
+    triplets (delta = 0.1 sigma) the exact local solves make GMRES stall,
+    while shifted block-Jacobi local solves (mu = 0.01) make progress."""
+    from synth.surfaces import fibonacci_sphere
+    xs, nrm = fibonacci_sphere(1500)
+    sel = xs[:, 2] > 0.55                           # a cap: ~340 surface points
+    xs, nrm = xs[sel], nrm[sel]
+    spacing = np.sqrt(4 * np.pi / 1500)
+    sigma = 3.0 * spacing
+    delta = 0.1 * sigma
+    X = extend(xs, nrm, delta).astype(np.float32)
+    b = labels(len(xs), delta)
+    cells = C.build(X, 6 * sigma)
+    Ss = cells["sorted"].astype(np.float64)
+    bs = b[cells["perm"]]
+    A = K.dense_matrix(Ss, sigma)
+    res = {}
+    for name, ov, mu in (("exact-ras", 1.0, 0.0), ("shifted-bj", 0.0, 0.01)):
+        blocks = S.ras_blocks(cells, sigma, core_target=128, overlap_sigmas=ov)
+        facs = {}
+        _, info = S.gmres(lambda v: A @ v, bs, restart=30, rtol=1e-12, maxit=30,
+                          apply_M=lambda r: S.ras_apply(blocks, Ss, r, sigma, factors=facs, shift=mu))
+        res[name] = info["rel_residual"]
+    assert res["shifted-bj"] < 1e-2 and res["shifted-bj"] < 0.1 * res["exact-ras"], res
+
+
 def test_ras_blocks_partition_and_overlap(c1_inputs):
     d = c1_inputs
     X = extend(d["x"], d["normals"], d["delta"])

@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--f64", action="store_true")
+    ap.add_argument("--precond", action="store_true", help="time the config's preconditioner setup + apply")
     args = ap.parse_args()
     t0 = time.time()
     d = make_inputs(args.config, n=args.n)
@@ -68,6 +69,15 @@ def main():
         f64 = torch.empty_like(w64)
         t64 = timed(lambda: R.matvec(ctx, cells, kern, w64, out=f64), max(3, args.iters // 4), warm=1)
         out.update(matvec_f64_ms=t64, f64_useful_pairs_per_s=useful / (t64 * 1e-3))
+    if args.precond:
+        cfg = d["cfg"]
+        kw = dict(kind=cfg.precond_kind, core_target=cfg.core_target, overlap_sigmas=cfg.overlap_sigmas,
+                  shift=cfg.shift, local_fp32=cfg.local_fp32)
+        P = R.Precond(ctx, cells, kern, **kw)
+        tp = timed(lambda: R.Precond(ctx, cells, kern, **kw), 3, warm=1)
+        z = P.apply(w)
+        ta = timed(lambda: P.apply(w, out=z), args.iters)
+        out.update(precond_setup_ms=tp, precond_apply_ms=ta)
     lo, hi, gn = d["grid_lo"], d["grid_hi"], d["grid_n"]
     wd = w.double()
     field = R.eval_grid(ctx, cells, kern, wd, lo, hi, gn)
