@@ -16,6 +16,10 @@
 // W = X^T = (A_ext^-1)[core, :] (A_ext symmetric).  Apply: z[core_i] = W_i r[ext_i].
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <type_traits>
+#include <utility>
 #include <cmath>
 
 #include "internal.h"
@@ -310,121 +314,204 @@ __global__ void assemble_kernel(const LuJob* __restrict__ jobs, const float4* __
 }
 
 // --------------------------------------------- on-chip fp32 inversion -----
-// local_fp32 path (reading R17): one CTA per block holds
+// local_fp32 path (reading R17): one CTA per block inverts
 // B = A_ext + shift*a*I (m <= kGjMax, fp32, entries formed in fp64 exactly as
-// assemble_kernel forms them and rounded once) in shared memory and inverts it
-// in place by Gauss-Jordan elimination with partial pivoting (largest |b_ik|,
-// lowest row on ties).  Step k: pivot row swap; f_i = B[i][k]; B[k][:] /= B[k][k]
-// with B[k][k] := 1/pivot; B[i][:] -= f_i B[k][:] for i != k with B[i][k] := 0
-// first.  The row swaps turn into column swaps of the result, undone in
-// reverse order through the permutation pi (write-out reads column pi[e]).
-// Work per block: m^3 FMAs, m steps of 3 block barriers; HBM sees the W write
-// (4 nc m bytes) and the centre reads only.
+// assemble_kernel forms them, rounded once) in place by Gauss-Jordan
+// elimination with partial pivoting (largest |b_ik|, lowest row on ties).
+// Step k: swap rows k and p; f_i = B[i][k]; B[k][:] /= pivot with
+// B[k][k] := 1/pivot; B[i][:] -= f_i B[k][:] for i != k with B[i][k] := 0
+// first.  The row swaps become column swaps of the result, undone through the
+// permutation pi at write-out (W[c][e] = B[m-nc+c][pi[e]]).
+//
+// The matrix lives in REGISTERS: 512 threads = 16 warps x 32 lanes, thread
+// (warp r, lane t) owns rows i = r + 16 a (a < RM) and columns j = t + 32 b
+// (b < RC), so m <= min(16 RM, 32 RC).  Per step only column k (for the pivot
+// search and the multipliers) and the two swapped rows go through shared
+// memory; the rank-1 update is RM*RC register FMAs per thread.  Three block
+// barriers per step; the multiplier buffer is double-buffered by step parity.
+// Work per block: m^3 FMAs; HBM sees the W write (4 nc m bytes) and the centre
+// reads only.
 constexpr int kGjMax = 224;
 constexpr int kGjThreads = 512;
 
-__global__ void __launch_bounds__(kGjThreads)
+template <int RM, int RC>
+__global__ void __launch_bounds__(kGjThreads, 1)
 gj_inverse_f32_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __restrict__ core_ptr,
                       const int32_t* __restrict__ ext_idx, const int64_t* __restrict__ w_off,
                       const float4* __restrict__ sorted, double amp, double two_s2, double c2,
                       double shift_abs, float* __restrict__ W, const int64_t* __restrict__ blist,
                       int64_t nlist, int* __restrict__ info) {
-  extern __shared__ float B[];          // m x ld, ld = m + 1 (odd: conflict-free column reads)
-  __shared__ float col[kGjMax];
-  __shared__ int piv[kGjMax], pi[kGjMax];
-  __shared__ float4 pos[kGjMax];
-  __shared__ int s_p;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int MR = 16 * RM, MC = 32 * RC;
+  constexpr int MM = MR < MC ? MR : MC;
+  __shared__ float colbuf[2][MM];
+  __shared__ float rowbuf[2][MM];
+  __shared__ int piv[MM], pinv[MM];
+  __shared__ float4 pos[MM];
+  __shared__ float cand_v[2][16], cand_a[2][16];
+  __shared__ int cand_i[2][16];
+  const int tid = threadIdx.x, lane = tid & 31, wr = tid >> 5;
   for (int64_t t = blockIdx.x; t < nlist; t += gridDim.x) {
-    const int64_t b = blist[t];
-    const int64_t e0 = ext_ptr[b];
-    const int m = (int)(ext_ptr[b + 1] - e0);
-    const int nc = (int)(core_ptr[b + 1] - core_ptr[b]);
-    const int ld = m + 1;
+    const int64_t blk = blist[t];
+    const int64_t e0 = ext_ptr[blk];
+    const int m = (int)(ext_ptr[blk + 1] - e0);
+    const int nc = (int)(core_ptr[blk + 1] - core_ptr[blk]);
     for (int i = tid; i < m; i += kGjThreads) pos[i] = sorted[ext_idx[e0 + i]];
     __syncthreads();
-    for (int q = tid; q < m * m; q += kGjThreads) {
-      const int i = q / m, j = q - i * m;
-      const float4 pi4 = pos[i], pj4 = pos[j];
-      const double dx = (double)pi4.x - (double)pj4.x, dy = (double)pi4.y - (double)pj4.y,
-                   dz = (double)pi4.z - (double)pj4.z;
-      const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-      double v = d2 <= c2 ? amp * exp(-d2 / two_s2) : 0.0;
-      if (i == j) v += shift_abs;
-      B[i * ld + j] = (float)v;
+    float B[RM][RC];
+#pragma unroll
+    for (int a = 0; a < RM; ++a) {
+      const int i = wr + 16 * a;
+#pragma unroll
+      for (int b = 0; b < RC; ++b) {
+        const int j = lane + 32 * b;
+        double v = 0.0;
+        if (i < m && j < m) {
+          const float4 pi4 = pos[i], pj4 = pos[j];
+          const double dx = (double)pi4.x - (double)pj4.x, dy = (double)pi4.y - (double)pj4.y,
+                       dz = (double)pi4.z - (double)pj4.z;
+          const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+          v = d2 <= c2 ? amp * exp(-d2 / two_s2) : 0.0;
+          if (i == j) v += shift_abs;
+        }
+        B[a][b] = (float)v;
+      }
     }
-    __syncthreads();
     int singular = 0;
-    for (int k = 0; k < m; ++k) {
-      if (wid == 0) {
-        float best = -1.0f;
-        int bi = k;
-        for (int i = k + lane; i < m; i += 32) {
-          const float v = fabsf(B[i * ld + k]);
-          if (v > best) { best = v; bi = i; }
-        }
+    // Publishes register column CB (column c = 32 CB + (c & 31), owner lane
+    // c & 31) of every warp's rows into the multiplier buffer, plus the warp's
+    // pivot candidate over its rows >= c (largest |v|, lowest row on ties).
+    auto publish = [&](auto cbt, int c, int buf) {
+      constexpr int CB = decltype(cbt)::value;
+      if (lane != (c & 31)) return;
+      float bv = -1.0f, sv = 0.0f;
+      int bi = 0x7fffffff;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+      for (int a = 0; a < RM; ++a) {
+        const float v = B[a][CB];
+        const int i = wr + 16 * a;
+        colbuf[buf][i] = v;                       // padding rows hold 0
+        if (i >= c && i < m && fabsf(v) > bv) { bv = fabsf(v); sv = v; bi = i; }
+      }
+      cand_v[buf][wr] = sv;
+      cand_a[buf][wr] = bv;
+      cand_i[buf][wr] = bi;
+    };
+    publish(std::integral_constant<int, 0>{}, 0, 0);
+    __syncthreads();
+    // Step k = 32 KB + 16 H + q: column k is register column KB of lane
+    // 16 H + q; row k is register row A = 2 KB + H of warp q.  Both indices
+    // are compile-time inside the unrolled (KB, H) blocks, so only the pivot
+    // row p needs a run-time register select (in its owner warp only).
+    auto block = [&](auto kbt, auto ht) {
+      constexpr int KB = decltype(kbt)::value, H = decltype(ht)::value, A = 2 * KB + H;
+      for (int q = 0; q < 16; ++q) {
+        const int k = 32 * KB + 16 * H + q;
+        if (k >= m) return;
+        const int cb = k & 1;
+        const int kl = 16 * H + q;
+        // (1) every warp reduces the 16 per-warp candidates
+        float ba = -1.0f, bv = 0.0f;
+        int bi = 0x7fffffff;
+        if (lane < 16) { ba = cand_a[cb][lane]; bv = cand_v[cb][lane]; bi = cand_i[cb][lane]; }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+          const float oa = __shfl_xor_sync(0xffffffffu, ba, o);
+          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
           const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+          if (oa > ba || (oa == ba && oi < bi)) { ba = oa; bv = ov; bi = oi; }
         }
-        if (lane == 0) { s_p = bi; piv[k] = bi; }
-      }
-      __syncthreads();
-      const int p = s_p;
-      if (p != k)
-        for (int j = tid; j < m; j += kGjThreads) {
-          const float t = B[k * ld + j];
-          B[k * ld + j] = B[p * ld + j];
-          B[p * ld + j] = t;
+        const int p = __shfl_sync(0xffffffffu, bi, 0);
+        const float pv = __shfl_sync(0xffffffffu, bv, 0);
+        if (tid == 0) piv[k] = p;
+        // (2) rows k and p into the row buffers
+        if (wr == q) {
+#pragma unroll
+          for (int b = 0; b < RC; ++b) rowbuf[0][lane + 32 * b] = B[A][b];
         }
-      __syncthreads();
-      const float pv = B[k * ld + k];
-      if (pv == 0.0f) singular = 1;
-      const float d = 1.0f / pv;
-      for (int i = tid; i < m; i += kGjThreads) col[i] = (i == k) ? 0.0f : B[i * ld + k];
-      // every warp keeps the scaled pivot row in registers (lane owns j = lane + 32 t)
-      float rk[kGjMax / 32];
+        const int wp = p & 15, ap = p >> 4;
+        if (wr == wp) {
 #pragma unroll
-      for (int t = 0; t < kGjMax / 32; ++t) {
-        const int j = lane + 32 * t;
-        rk[t] = (j < m) ? ((j == k) ? d : B[k * ld + j] * d) : 0.0f;
-      }
-      __syncthreads();
-      for (int i = wid; i < m; i += kGjThreads / 32) {
-        float* row = B + i * ld;
-        if (i == k) {
+          for (int b = 0; b < RC; ++b) {
+            float v = B[0][b];
 #pragma unroll
-          for (int t = 0; t < kGjMax / 32; ++t) {
-            const int j = lane + 32 * t;
-            if (j < m) row[j] = rk[t];
+            for (int a = 1; a < RM; ++a) v = (a == ap) ? B[a][b] : v;
+            rowbuf[1][lane + 32 * b] = v;
           }
-          continue;
         }
-        const float f = col[i];
+        if (pv == 0.0f) singular = 1;
+        const float d = __frcp_rn(pv);
+        __syncthreads();
+        // (3) rank-1 update of every row, then the fix-ups of column k, row k, row p
+        float rkv[RC];
 #pragma unroll
-        for (int t = 0; t < kGjMax / 32; ++t) {
-          const int j = lane + 32 * t;
-          if (j < m) row[j] = fmaf(-f, rk[t], (j == k) ? 0.0f : row[j]);
+        for (int b = 0; b < RC; ++b) rkv[b] = rowbuf[1][lane + 32 * b] * d;
+        const float fk = colbuf[cb][k];
+        float fa[RM];
+#pragma unroll
+        for (int a = 0; a < RM; ++a) {
+          fa[a] = colbuf[cb][wr + 16 * a];   // 0 for padding rows
+#pragma unroll
+          for (int b = 0; b < RC; ++b) B[a][b] = fmaf(-fa[a], rkv[b], B[a][b]);
         }
+        if (lane == kl) {
+#pragma unroll
+          for (int a = 0; a < RM; ++a) B[a][KB] = -fa[a] * d;   // B[i][k] := 0 - f_i d
+        }
+        if (p != k && wr == wp) {
+          // row p receives the old row k: B[p][:] = row_k - f_k rk, B[p][k] = -f_k d
+#pragma unroll
+          for (int b = 0; b < RC; ++b) {
+            float v = fmaf(-fk, rkv[b], rowbuf[0][lane + 32 * b]);
+            if (b == KB && lane == kl) v = -fk * d;
+#pragma unroll
+            for (int a = 0; a < RM; ++a) B[a][b] = (a == ap) ? v : B[a][b];
+          }
+        }
+        if (wr == q) {
+          // pivot row: B[k][:] = row_p / pivot, B[k][k] = 1 / pivot
+#pragma unroll
+          for (int b = 0; b < RC; ++b) B[A][b] = rkv[b];
+          if (lane == kl) B[A][KB] = d;
+        }
+        // (4) column k+1 and its pivot candidates into the other buffers
+        if (k + 1 < m) {
+          if (H == 1 && q == 15) {
+            if constexpr (KB + 1 < RC) publish(std::integral_constant<int, KB + 1>{}, k + 1, cb ^ 1);
+          } else {
+            publish(std::integral_constant<int, KB>{}, k + 1, cb ^ 1);
+          }
+        }
+        __syncthreads();
       }
-      __syncthreads();
-    }
+    };
+    static_assert(RM >= 2 * RC, "row blocks must cover the column blocks");
+    [&]<int... KBs>(std::integer_sequence<int, KBs...>) {
+      ((block(std::integral_constant<int, KBs>{}, std::integral_constant<int, 0>{}),
+        block(std::integral_constant<int, KBs>{}, std::integral_constant<int, 1>{})), ...);
+    }(std::make_integer_sequence<int, RC>{});
     if (tid == 0) {
-      for (int j = 0; j < m; ++j) pi[j] = j;
+      for (int j = 0; j < m; ++j) pinv[j] = j;   // pi (built in place, then inverted below)
       for (int k = m - 1; k >= 0; --k) {
-        const int t = pi[k];
-        pi[k] = pi[piv[k]];
-        pi[piv[k]] = t;
+        const int q = pinv[k];
+        pinv[k] = pinv[piv[k]];
+        pinv[piv[k]] = q;
       }
+      for (int e = 0; e < m; ++e) piv[pinv[e]] = e;   // piv := pi^-1
       if (singular) atomicAdd(info, 1);
     }
     __syncthreads();
-    float* Wb = W + w_off[b];
-    for (int q = tid; q < nc * m; q += kGjThreads) {
-      const int c = q / m, e = q - c * m;
-      Wb[q] = B[(m - nc + c) * ld + pi[e]];
+    // W[c][e] = B[m-nc+c][pi[e]]  <=>  element (i, j) goes to column pi^-1[j]
+    float* Wb = W + w_off[blk];
+    const int r0 = m - nc;
+#pragma unroll
+    for (int a = 0; a < RM; ++a) {
+      const int i = wr + 16 * a;
+      if (i < r0 || i >= m) continue;
+#pragma unroll
+      for (int b = 0; b < RC; ++b) {
+        const int j = lane + 32 * b;
+        if (j < m) Wb[(int64_t)(i - r0) * m + piv[j]] = B[a][b];
+      }
     }
     __syncthreads();
   }
@@ -480,6 +567,14 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
                          rbf_precond* P) {
   using clk = std::chrono::steady_clock;
   const auto t0 = clk::now();
+  // RBF_DEBUG_SETUP=1 prints host-clock phase times (synchronising at each mark)
+  static const bool dbg = std::getenv("RBF_DEBUG_SETUP") != nullptr;
+  auto mark = [&](const char* what) {
+    if (!dbg) return;
+    cudaStreamSynchronize(ctx->stream);
+    std::fprintf(stderr, "[rbf setup] %-24s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(clk::now() - t0).count());
+  };
   cudaStream_t s = ctx->stream;
   const int64_t n = c->n;
   P->n = n;
@@ -521,6 +616,7 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
   while (dbits < 21 && (1 << dbits) < std::max(c->dim[0], std::max(c->dim[1], c->dim[2]))) ++dbits;
   RBF_TRY(radix_sort_pairs<unsigned long long>(ctx, code.as<unsigned long long>(), idx.as<int32_t>(),
                                                code2.as<unsigned long long>(), order.as<int32_t>(), nne, 3 * dbits));
+  mark("cells+morton");
   // 3. prefix counts in Morton order and core ids
   DevBuf cnt, Pm, cflag, cpos;
   RBF_TRY(cnt.alloc(4 * nne, s));
@@ -579,6 +675,7 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
                                                        Pm.as<uint32_t>(), cnt.as<uint32_t>(), cell_core.as<int32_t>(),
                                                        nne, P->core_idx.as<int32_t>(), owner.as<int32_t>());
   RBF_CHECK_LAUNCH();
+  mark("cores");
   // 4. extended sets
   CellGrid g;
   for (int a = 0; a < 3; ++a) { g.lo[a] = c->lo[a]; g.dim[a] = c->dim[a]; }
@@ -587,21 +684,26 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
   const double ov = ovs * kp.sigma;
   const float ov2 = (float)(ov * ov);
   DevBuf ecount, stage, err;
-  RBF_TRY(ecount.alloc(4 * ncore, s));
-  RBF_TRY(stage.alloc(sizeof(int32_t) * (size_t)ncore * max_ext, s));
   RBF_TRY(err.alloc(4, s));
   RBF_CUDA_TRY(cudaMemsetAsync(err.p, 0, 4, s));
   const int eblocks = (int)std::min<int64_t>(ncore, (int64_t)ctx->sm_count * 8);
-  ext_kernel<<<eblocks, 256, 0, s>>>(c->sorted.as<float4>(), c->cell_start.as<int32_t>(), g,
-                                     P->core_ptr.as<int64_t>(), P->core_idx.as<int32_t>(), owner.as<int32_t>(),
-                                     c->keys.as<uint32_t>(), ov2, (float)ov, ncore, max_ext,
-                                     ecount.as<uint32_t>(), stage.as<int32_t>(), err.as<int>());
-  RBF_CHECK_LAUNCH();
+  const bool no_overlap = ovs == 0.0;   // block-Jacobi: ext = core (no search)
   std::vector<uint32_t> h_ecount(ncore);
   int herr0 = 0;
-  RBF_CUDA_TRY(cudaMemcpyAsync(h_ecount.data(), ecount.p, 4 * ncore, cudaMemcpyDeviceToHost, s));
-  RBF_CUDA_TRY(cudaMemcpyAsync(&herr0, err.p, 4, cudaMemcpyDeviceToHost, s));
-  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  if (no_overlap) {
+    for (int64_t b = 0; b < ncore; ++b) h_ecount[b] = (uint32_t)(h_core_ptr[b + 1] - h_core_ptr[b]);
+  } else {
+    RBF_TRY(ecount.alloc(4 * ncore, s));
+    RBF_TRY(stage.alloc(sizeof(int32_t) * (size_t)ncore * max_ext, s));
+    ext_kernel<<<eblocks, 256, 0, s>>>(c->sorted.as<float4>(), c->cell_start.as<int32_t>(), g,
+                                       P->core_ptr.as<int64_t>(), P->core_idx.as<int32_t>(), owner.as<int32_t>(),
+                                       c->keys.as<uint32_t>(), ov2, (float)ov, ncore, max_ext,
+                                       ecount.as<uint32_t>(), stage.as<int32_t>(), err.as<int>());
+    RBF_CHECK_LAUNCH();
+    RBF_CUDA_TRY(cudaMemcpyAsync(h_ecount.data(), ecount.p, 4 * ncore, cudaMemcpyDeviceToHost, s));
+    RBF_CUDA_TRY(cudaMemcpyAsync(&herr0, err.p, 4, cudaMemcpyDeviceToHost, s));
+    RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  }
   std::vector<int64_t> h_ext_ptr(ncore + 1, 0), h_w_off(ncore + 1, 0);
   int64_t max_m = 0;
   for (int64_t b = 0; b < ncore; ++b) {
@@ -622,12 +724,17 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
   RBF_CUDA_TRY(cudaMemcpyAsync(P->ext_ptr.p, h_ext_ptr.data(), 8 * (ncore + 1), cudaMemcpyHostToDevice, s));
   RBF_CUDA_TRY(cudaMemcpyAsync(P->w_off.p, h_w_off.data(), 8 * (ncore + 1), cudaMemcpyHostToDevice, s));
   RBF_TRY(P->ext_idx.alloc(4 * h_ext_ptr[ncore], s));
-  ext_assemble<<<eblocks, 256, 0, s>>>(P->core_ptr.as<int64_t>(), P->core_idx.as<int32_t>(),
-                                       P->ext_ptr.as<int64_t>(), stage.as<int32_t>(), max_ext, ncore,
-                                       P->ext_idx.as<int32_t>());
-  RBF_CHECK_LAUNCH();
+  if (no_overlap) {
+    RBF_CUDA_TRY(cudaMemcpyAsync(P->ext_idx.p, P->core_idx.p, 4 * h_ext_ptr[ncore], cudaMemcpyDeviceToDevice, s));
+  } else {
+    ext_assemble<<<eblocks, 256, 0, s>>>(P->core_ptr.as<int64_t>(), P->core_idx.as<int32_t>(),
+                                         P->ext_ptr.as<int64_t>(), stage.as<int32_t>(), max_ext, ncore,
+                                         P->ext_idx.as<int32_t>());
+    RBF_CHECK_LAUNCH();
+  }
   P->h_core_ptr = h_core_ptr;
   P->h_ext_ptr = h_ext_ptr;
+  mark("ext sets");
   // 5. assemble + factor + restricted inverse
   const double two_s2 = 2.0 * kp.sigma * kp.sigma;
   const double c2 = kp.cutoff * kp.cutoff;
@@ -638,12 +745,11 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
   // fp32; larger ones go through the fp64 batched LU and are rounded into W.
   P->w_fp32 = want_fp32;
   std::vector<int64_t> small, big;
-  int64_t small_max_m = 0, big_w = 0;
+  int64_t big_w = 0;
   for (int64_t b = 0; b < ncore; ++b) {
     const int64_t m = h_ext_ptr[b + 1] - h_ext_ptr[b];
     if (want_fp32 && m <= kGjMax) {
       small.push_back(b);
-      small_max_m = std::max(small_max_m, m);
     } else {
       big.push_back(b);
       big_w += h_w_off[b + 1] - h_w_off[b];
@@ -657,19 +763,35 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
   }
   DevBuf blist;
   if (!small.empty()) {
+    // bins by m: register tiles 128 (8x4), 192 (12x6), 224 (14x7)
+    std::stable_sort(small.begin(), small.end(), [&](int64_t x, int64_t y) {
+      return (h_ext_ptr[x + 1] - h_ext_ptr[x]) < (h_ext_ptr[y + 1] - h_ext_ptr[y]);
+    });
     RBF_TRY(blist.alloc(8 * small.size(), s));
     RBF_CUDA_TRY(cudaMemcpyAsync(blist.p, small.data(), 8 * small.size(), cudaMemcpyHostToDevice, s));
-    const size_t smem = sizeof(float) * (size_t)small_max_m * (small_max_m + 1);
-    RBF_CUDA_TRY(cudaFuncSetAttribute(gj_inverse_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    RBF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gj_inverse_f32_kernel, kGjThreads, smem));
-    const int gblocks = (int)std::min<int64_t>((int64_t)small.size(), (int64_t)ctx->sm_count * std::max(per_sm, 1));
-    gj_inverse_f32_kernel<<<gblocks, kGjThreads, smem, s>>>(
-        P->ext_ptr.as<int64_t>(), P->core_ptr.as<int64_t>(), P->ext_idx.as<int32_t>(), P->w_off.as<int64_t>(),
-        c->sorted.as<float4>(), kp.amp, two_s2, c2, shift_abs, P->W.as<float>(), blist.as<int64_t>(),
-        (int64_t)small.size(), info.as<int>());
-    RBF_CHECK_LAUNCH();
+    size_t lo = 0;
+    const int caps[3] = {128, 192, 224};
+    for (int bin = 0; bin < 3 && lo < small.size(); ++bin) {
+      size_t hi = lo;
+      while (hi < small.size() && h_ext_ptr[small[hi] + 1] - h_ext_ptr[small[hi]] <= caps[bin]) ++hi;
+      const int64_t cnt = (int64_t)(hi - lo);
+      if (cnt > 0) {
+        const int gblocks = (int)std::min<int64_t>(cnt, (int64_t)ctx->sm_count);
+        const int64_t* bl = blist.as<int64_t>() + lo;
+#define RBF_GJ_LAUNCH(RM_, RC_)                                                                            \
+  gj_inverse_f32_kernel<RM_, RC_><<<gblocks, kGjThreads, 0, s>>>(                                         \
+      P->ext_ptr.as<int64_t>(), P->core_ptr.as<int64_t>(), P->ext_idx.as<int32_t>(), P->w_off.as<int64_t>(), \
+      c->sorted.as<float4>(), kp.amp, two_s2, c2, shift_abs, P->W.as<float>(), bl, cnt, info.as<int>())
+        if (bin == 0) RBF_GJ_LAUNCH(8, 4);
+        else if (bin == 1) RBF_GJ_LAUNCH(12, 6);
+        else RBF_GJ_LAUNCH(14, 7);
+#undef RBF_GJ_LAUNCH
+        RBF_CHECK_LAUNCH();
+      }
+      lo = hi;
+    }
   }
+  mark("on-chip inverses");
   const int64_t ws_limit = (int64_t)16 << 30;  // fp64 LU workspace bytes per chunk
   DevBuf w64;                                  // fp64 W of the big blocks when W is fp32
   std::vector<int64_t> trip;
@@ -718,6 +840,7 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
     RBF_CHECK_LAUNCH();
     RBF_CUDA_TRY(cudaStreamSynchronize(s));
   }
+  mark("fp64 LU blocks");
   int herr = 0, hinfo = 0;
   RBF_CUDA_TRY(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, s));
   RBF_CUDA_TRY(cudaMemcpyAsync(&hinfo, info.p, 4, cudaMemcpyDeviceToHost, s));

@@ -45,14 +45,14 @@ CONFIGS = {
     # configs[2]: blobby K=16, N=200k, 10x density, sigma 0.02 (delta = 0.1 sigma, reading 4)
     # c3-c5 sit at sigma/spacing ~3-4 where exact local solves stall GMRES (DESIGN.md
     # finding F4): shifted block-Jacobi local solves, fp32 on chip (reading R17)
-    "c3": Config("c3", "blobby", 200000, 0.02, 0.002, 256, core_target=128, overlap_sigmas=0.0,
-                 precond_kind=1, shift=0.01, local_fp32=1, kw=dict(K=16, density_mod=True)),
+    "c3": Config("c3", "blobby", 200000, 0.02, 0.002, 256, core_target=64, overlap_sigmas=0.0,
+                 precond_kind=1, shift=0.003, local_fp32=1, kw=dict(K=16, density_mod=True)),
     # configs[3]: blobby K=64, N=1M, sigma 0.01, 256^3  (the metric config)
-    "c4": Config("c4", "blobby", 1000000, 0.01, 0.001, 256, core_target=128, overlap_sigmas=0.0,
-                 precond_kind=1, shift=0.01, local_fp32=1, kw=dict(K=64)),
+    "c4": Config("c4", "blobby", 1000000, 0.01, 0.001, 256, core_target=64, overlap_sigmas=0.0,
+                 precond_kind=1, shift=0.003, local_fp32=1, kw=dict(K=64)),
     # configs[4]: blobby K=64 with 5 caps removed, N=10M, sigma 0.004, 512^3
-    "c5": Config("c5", "blobby", 10000000, 0.004, 0.0004, 512, core_target=128, overlap_sigmas=0.0,
-                 precond_kind=1, shift=0.01, local_fp32=1, kw=dict(K=64, holes=5)),
+    "c5": Config("c5", "blobby", 10000000, 0.004, 0.0004, 512, core_target=64, overlap_sigmas=0.0,
+                 precond_kind=1, shift=0.003, local_fp32=1, kw=dict(K=64, holes=5)),
 }
 
 

@@ -20,13 +20,14 @@ CASES = [
     # kind, core, overlap, shift, fp32
     (0, 0, 0.0, 0.0, 0),
     (1, 128, 0.0, 0.01, 1),
-    (1, 128, 0.0, 0.003, 1),
-    (1, 128, 0.0, 0.001, 1),
+    (1, 96, 0.0, 0.01, 1),
     (1, 64, 0.0, 0.01, 1),
+    (1, 64, 0.0, 0.003, 1),
+    (1, 48, 0.0, 0.01, 1),
+    (1, 32, 0.0, 0.01, 1),
     (1, 192, 0.0, 0.01, 1),
     (1, 512, 0.0, 0.01, 0),
     (2, 128, 1.0, 1.0, 0),
-    (2, 512, 1.0, 0.1, 0),
     (2, 512, 1.0, 0.0, 0),
 ]
 
