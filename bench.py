@@ -12,8 +12,9 @@ Step (all on the GPU, inputs resident in HBM when the timed region starts):
   a5-a7 FGMRES fp32 tier -> fp64 tier  rbf_gmres_solve (true residual <= 1e-6)
   a8 grid evaluation                  rbf_eval_grid
 value = useful kernel-pair evaluations of the step (matvecs x useful pairs per
-matvec + grid pairs) / step seconds, summed over ranks (weak scaling: every rank
-solves its own seeded instance -- see DESIGN.md "Multi-GPU").
+matvec + grid pairs) / step seconds (max over ranks), summed over ranks.  N > 1:
+one problem split by z slabs over the ranks (strong scaling, DESIGN.md §7;
+--parallel replicas runs an independent seeded problem per rank instead).
 e2e = the same metric through rbf_reconstruct_host with HOST buffers (H2D of
 centres + b and D2H of weights + field inside the timed region).
 Prints ONE JSON line on rank 0.
@@ -49,6 +50,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-rows", type=int, default=0)
     ap.add_argument("--fit-iters", type=int, default=50)
+    ap.add_argument("--parallel", default="slab", choices=["slab", "replicas"],
+                    help="N>1: one problem split by slabs over the ranks (strong scaling, SURVEY §8(e)) "
+                         "or one independent seeded problem per rank (weak scaling)")
     return ap.parse_args()
 
 
@@ -129,9 +133,10 @@ def run_ours(args, rank, world, local):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    d = make_problem(args.config, args.seed + rank)
+    slab = world > 1 and args.parallel == "slab"
+    d = make_problem(args.config, args.seed if slab else args.seed + rank)
     cfg = d["cfg"]
-    ctx = R.Context(local)
+    ctx = R.Context(local, distributed=slab)
     kern = R.Kernel(d["sigma"], d["cutoff_sigmas"])
     x = torch.as_tensor(d["x"], device=dev)
     nrm = torch.as_tensor(d["normals"], device=dev)
@@ -237,15 +242,17 @@ def run_ours(args, rank, world, local):
     out = {
         "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "fit_eval_s": ms_max / args.steps / 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64",
+        "higher_is_better": True, "scaling": "strong" if slab else "weak", "vs_baseline": None, "dtype": "f32+f64",
         "data": "synthetic (seeded blobby surface, SURVEY §8(c) reading 14)",
         "config": {"workload": f"{args.config}: {cfg.kind} K={cfg.kw.get('K')} N={cfg.n} surface points "
                                f"({3 * cfg.n} centres), sigma={cfg.sigma}, cutoff 6 sigma, GMRES({cfg.restart}) "
                                f"+ {precond_name(cfg)}, {args.fit_iters} iterations "
                                f"(Table II protocol) or true residual 1e-6, "
                                f"grid {gn[0]}^3",
-                   "centres_per_gpu": 3 * cfg.n, "global_centres": 3 * cfg.n * world,
-                   "parallelism": f"replicas x{world} (independent seeded instances)",
+                   "centres_per_gpu": 3 * cfg.n // world if slab else 3 * cfg.n,
+                   "global_centres": 3 * cfg.n if slab else 3 * cfg.n * world,
+                   "parallelism": (f"slab x{world} (z cell planes, halo send/recv + allreduce over NCCL)" if slab
+                                   else f"replicas x{world} (independent seeded instances)"),
                    "l2": "working set >> 126 MB L2 (W 30+ GB, Krylov basis 2.4 GB); no explicit flush"},
         "e2e": e2e, "gpu_launches": None, "clocks": clk, "roofline": roofline, "cpu_baseline": cpu,
         "detail": {"useful_pairs_per_matvec": useful_mv, "visited_pairs_per_matvec": visited_mv,

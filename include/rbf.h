@@ -153,11 +153,34 @@ typedef struct {
 
 /* Create a context on CUDA device `device` that issues all work on
  * `cuda_stream` (a cudaStream_t; NULL = the legacy default stream).
- * nccl_unique_id must be NULL and world 1 in this ABI version (multi-GPU
- * runs shard independent problems per rank).
- * Errors: RBF_EINVAL (bad device / world != 1), RBF_ECUDA. */
+ * world == 1: single GPU (nccl_unique_id ignored, rank must be 0).
+ * world > 1: one process (context) per GPU, `rank` in [0, world), and
+ * nccl_unique_id = the 128-byte id rank 0 obtained from rbf_nccl_unique_id(),
+ * broadcast to every rank by the caller (e.g. torch.distributed).  The context
+ * then partitions every call by slabs of cell planes (DESIGN.md
+ * "Multi-GPU"): inputs are REPLICATED (every rank passes the full centre set,
+ * right-hand side and weights), the work and the solver state are sharded, and
+ * outputs (weights, matvec results, grid field) are returned full on every rank.
+ * NCCL (libnccl.so.2) is loaded at run time, only when world > 1.
+ * Errors: RBF_EINVAL (bad device / rank / world, missing id), RBF_ECUDA,
+ * RBF_ENCCL (NCCL unavailable or communicator init failed). */
 rbf_status rbf_create(rbf_ctx** ctx, int device, void* cuda_stream,
                       const void* nccl_unique_id, int rank, int world);
+/* 128 bytes (HOST) of a fresh NCCL unique id, for rank 0 to share.  RBF_ENCCL if
+ * NCCL cannot be loaded. */
+rbf_status rbf_nccl_unique_id(void* out128);
+/* Slab partition plan (HOST only, no GPU; the same function the library runs at
+ * rbf_build_cells when world > 1).  Inputs: plane_start[dimz+1] = sorted
+ * position of the first centre of each z cell plane (non-decreasing, last =
+ * n), plane_weight[dimz] >= 0 (the library uses sum over the plane's cells of
+ * n_c^2, an estimate of its useful pairs), reach = planes a target's cutoff can
+ * span.  Outputs (HOST, caller-allocated): plane_lo[world+1] (rank r owns planes
+ * [plane_lo[r], plane_lo[r+1]), cut where the cumulative weight crosses r/world),
+ * own_lo/own_hi[world] (owned sorted range), win_lo/win_hi[world] (matvec source
+ * window = planes [plane_lo[r] - reach, plane_lo[r+1] + reach) clipped; empty
+ * for an empty slab).  Any output may be NULL.  Errors: RBF_EINVAL. */
+rbf_status rbf_slab_plan(const int64_t* plane_start, const double* plane_weight, int dimz, int reach, int world,
+                         int32_t* plane_lo, int64_t* own_lo, int64_t* own_hi, int64_t* win_lo, int64_t* win_hi);
 void rbf_destroy(rbf_ctx* ctx);
 const char* rbf_status_str(rbf_status s);
 const char* rbf_last_error(void);
@@ -186,6 +209,13 @@ rbf_status rbf_build_cells(rbf_ctx* ctx, const float* xyz, int64_t n,
                            rbf_cells** out);
 void rbf_cells_free(rbf_cells* cells);
 rbf_status rbf_cells_info(const rbf_cells* cells, rbf_cells_desc* out /* host */);
+/* This rank's slab (HOST out[8]): owned sorted range [out[0], out[1]), matvec
+ * source window [out[2], out[3]), target tiles [out[4], out[5]), z cell planes
+ * [out[6], out[7]).  Single GPU: everything.  (world > 1, or the test-only
+ * RBF_SLAB_EMULATE="r/W" environment variable, which gives single-GPU cells
+ * rank r's slab of a W-way partition for rbf_matvec / rbf_eval_grid /
+ * rbf_precond_create checks; the solver refuses such cells.) */
+rbf_status rbf_cells_slab(const rbf_cells* cells, int64_t* out);
 /* Library-owned DEVICE arrays, valid until rbf_cells_free:
  *   perm[n]           sorted position -> caller index (stable by key)
  *   sorted[4n]        float4 records (x, y, z, 0) in sorted order
@@ -207,7 +237,8 @@ rbf_status rbf_matvec(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* ke
 
 /* Pair accounting of the fp32 matvec traversal (host outputs; synchronises):
  * useful = ordered (target, source) pairs with r^2 <= c^2 (self included),
- * visited = pairs the kernel evaluated (after culling). */
+ * visited = pairs the kernel evaluated (after culling).  world > 1: the pairs
+ * of this rank's targets (sum over ranks = the whole product). */
 rbf_status rbf_matvec_pairs(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern,
                             int64_t* useful, int64_t* visited);
 
@@ -245,7 +276,9 @@ rbf_status rbf_gmres_solve(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kerne
 
 /* ---- a8: grid evaluation F(xi) = sum_j A(xi, x_j) w_j (Eq.5) --------------
  * w: DEVICE fp64 (n, caller order); field: DEVICE fp32, n0*n1*n2, x fastest.
- * Nodes with no centre within the cutoff get exactly 0.0f. */
+ * Nodes with no centre within the cutoff get exactly 0.0f.  world > 1: each
+ * rank evaluates the node layers of its slab and the field is summed over ranks
+ * (the other layers are 0 on each rank), so every rank returns the full field. */
 rbf_status rbf_eval_grid(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern,
                          const double* w, const rbf_grid* grid, float* field);
 

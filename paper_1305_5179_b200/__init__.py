@@ -5,7 +5,9 @@ CUDA) and the thin ctypes binding in `rbf`.  This package never imports the
 CPU oracle (oracle/, test infrastructure only) and has no CPU fallback.
 """
 from .rbf import (Context, Cells, Kernel, Precond, RbfError, SolveReport, eval_grid, eval_grid_pairs, extend_points,
-                  gmres_solve, launch_count, load_library, matvec, matvec_pairs, reconstruct_host)
+                  gmres_solve, launch_count, load_library, matvec, matvec_pairs, nccl_unique_id, reconstruct_host,
+                  slab_plan)
 
 __all__ = ["Context", "Cells", "Kernel", "Precond", "RbfError", "SolveReport", "eval_grid", "eval_grid_pairs",
-           "extend_points", "gmres_solve", "launch_count", "load_library", "matvec", "matvec_pairs", "reconstruct_host"]
+           "extend_points", "gmres_solve", "launch_count", "load_library", "matvec", "matvec_pairs", "nccl_unique_id",
+           "reconstruct_host", "slab_plan"]

@@ -1,12 +1,14 @@
 // C-ABI entry points (include/rbf.h): validation, handle management and
 // dispatch to the device code.  Every step of the path runs in this
 // library's kernels; there is no host compute fallback.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <atomic>
 #include <new>
 
 #include "internal.h"
+#include "solver.h"
 
 namespace rbf {
 namespace {
@@ -45,6 +47,7 @@ rbf_status check_cells(const rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel*
     set_error("kernel cutoff exceeds the cutoff the cells were built for");
     return RBF_EINVAL;
   }
+  if (c->world != ctx->world) { set_error("cells were partitioned for another world size"); return RBF_EINVAL; }
   return RBF_OK;
 }
 
@@ -74,8 +77,9 @@ rbf_status rbf_create(rbf_ctx** out, int device, void* cuda_stream, const void* 
                       int world) {
   if (!out) { set_error("out is NULL"); return RBF_EINVAL; }
   *out = nullptr;
-  if (nccl_unique_id != nullptr || world != 1 || rank != 0) {
-    set_error("this ABI version runs one problem per GPU: nccl_unique_id must be NULL, world 1, rank 0");
+  if (world < 1 || rank < 0 || rank >= world) { set_error("need 0 <= rank < world"); return RBF_EINVAL; }
+  if (world > 1 && nccl_unique_id == nullptr) {
+    set_error("world > 1 needs the NCCL unique id of rank 0 (rbf_nccl_unique_id)");
     return RBF_EINVAL;
   }
   int ndev = 0;
@@ -101,6 +105,10 @@ rbf_status rbf_create(rbf_ctx** out, int device, void* cuda_stream, const void* 
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  if (world > 1) {
+    rbf_status st = dist_init(c, nccl_unique_id, rank, world);
+    if (st != RBF_OK) { delete c; return st; }
   }
   *out = c;
   return RBF_OK;
@@ -135,6 +143,8 @@ void rbf_destroy(rbf_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStream_t s = ctx->stream;
+  cudaStreamSynchronize(s);
+  dist_destroy(ctx);
   delete ctx;  // DevBufs free stream-ordered
   cudaStreamSynchronize(s);
 }
@@ -175,6 +185,14 @@ rbf_status rbf_cells_info(const rbf_cells* c, rbf_cells_desc* d) {
   return RBF_OK;
 }
 
+rbf_status rbf_cells_slab(const rbf_cells* c, int64_t* out) {
+  if (!c || !out) { set_error("NULL argument"); return RBF_EINVAL; }
+  const SlabView& V = c->view;
+  const int64_t v[8] = {V.o0, V.o1, V.h0, V.h1, V.t0, V.t1, V.p0, V.p1};
+  std::copy(v, v + 8, out);
+  return RBF_OK;
+}
+
 rbf_status rbf_cells_view(const rbf_cells* c, const int32_t** perm, const float** sorted, const uint32_t** keys,
                           const int32_t** cell_start) {
   if (!c) { set_error("cells is NULL"); return RBF_EINVAL; }
@@ -193,6 +211,24 @@ rbf_status rbf_matvec(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, 
   RBF_CUDA_TRY(cudaSetDevice(ctx->device));
   KernelParams kp = kernel_params(kern);
   const int64_t n = c->n;
+  if (ctx->world > 1 || c->emulated) {
+    // slab partition: replicated in, this rank's rows, gathered out
+    if (prec != RBF_F32 && prec != RBF_F64) { set_error("bad precision"); return RBF_EINVAL; }
+    RBF_TRY(ctx->vec_a.ensure(sizeof(double) * n, ctx->stream));
+    RBF_TRY(ctx->vec_b.ensure(sizeof(double) * n, ctx->stream));
+    double* ws = ctx->vec_a.as<double>();
+    double* fs = ctx->vec_b.as<double>();
+    if (prec == RBF_F32) {
+      RBF_TRY(gather_f32_to_sorted_f64(ctx, static_cast<const float*>(w), c->perm.as<int32_t>(), ws, n));
+      RBF_TRY(matvec_sorted_f32_d(ctx, c, kp, ws + c->view.o0, fs + c->view.o0));
+    } else {
+      RBF_TRY(gather_f64_to_sorted(ctx, static_cast<const double*>(w), c->perm.as<int32_t>(), ws, n));
+      RBF_TRY(matvec_sorted_f64(ctx, c, kp, ws + c->view.o0, fs + c->view.o0, nullptr));
+    }
+    RBF_TRY(allgather_sorted(ctx, c, fs));
+    if (prec == RBF_F32) return scatter_f64_from_sorted_f32(ctx, fs, c->perm.as<int32_t>(), static_cast<float*>(f), n);
+    return scatter_f64_from_sorted(ctx, fs, c->perm.as<int32_t>(), static_cast<double*>(f), n);
+  }
   if (prec == RBF_F32) {
     RBF_TRY(ctx->vec_a.ensure(sizeof(float) * n, ctx->stream));
     RBF_TRY(gather_f32_to_sorted(ctx, static_cast<const float*>(w), c->perm.as<int32_t>(), ctx->vec_a.as<float>(), n));
@@ -246,7 +282,13 @@ rbf_status rbf_eval_grid(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* ker
   KernelParams kp = kernel_params(kern);
   RBF_TRY(ctx->vec_a.ensure(sizeof(double) * c->n, ctx->stream));
   RBF_TRY(gather_f64_to_sorted(ctx, w, c->perm.as<int32_t>(), ctx->vec_a.as<double>(), c->n));
-  return eval_grid_sorted(ctx, c, kp, ctx->vec_a.as<double>(), g, field);
+  if (ctx->world == 1 && !c->emulated) return eval_grid_sorted(ctx, c, kp, ctx->vec_a.as<double>(), g, field);
+  // slab partition: each rank evaluates the node layers of its slab, the
+  // others stay 0, and a sum over ranks completes the field on every rank
+  const int64_t nodes = (int64_t)g->n[0] * g->n[1] * g->n[2];
+  RBF_CUDA_TRY(cudaMemsetAsync(field, 0, sizeof(float) * nodes, ctx->stream));
+  RBF_TRY(eval_grid_sorted(ctx, c, kp, ctx->vec_a.as<double>(), g, field));
+  return allreduce_sum_f32(ctx, field, nodes);
 }
 
 rbf_status rbf_eval_grid_pairs(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, const rbf_grid* g,

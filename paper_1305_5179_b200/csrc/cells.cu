@@ -9,6 +9,8 @@
 // the CPU replica in oracle/cells.py.
 #include <cmath>
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -524,6 +526,31 @@ rbf_status build_cells(rbf_ctx* ctx, const float* xyz, int64_t n, const rbf_kern
     tile_box_kernel<<<grid_for((int64_t)ntiles * 32, 256), 256, 0, s>>>(
         c->sorted.as<float4>(), c->tiles.as<int2>(), ntiles, c->tile_box.as<float4>());
     RBF_CHECK_LAUNCH();
+  }
+  // this rank's share (dist.cu): everything on one GPU, a slab of z planes otherwise
+  c->world = ctx->world;
+  c->view = SlabView{0, n, 0, n, 0, (int64_t)ntiles, 0, c->dim[2]};
+  // RBF_SLAB_EMULATE="r/W" (single GPU, tests only): give these cells rank r's
+  // slab of a W-way partition so the slab kernels can be checked on one device
+  int erank = 0, eworld = 1;
+  if (ctx->world == 1) {
+    if (const char* e = std::getenv("RBF_SLAB_EMULATE")) {
+      if (std::sscanf(e, "%d/%d", &erank, &eworld) != 2 || eworld < 1 || erank < 0 || erank >= eworld) {
+        set_error("RBF_SLAB_EMULATE must be r/W with 0 <= r < W");
+        return RBF_EINVAL;
+      }
+    }
+  }
+  if (ctx->world > 1 || eworld > 1) {
+    std::vector<uint32_t> hro(rows);
+    RBF_CUDA_TRY(cudaMemcpyAsync(hro.data(), ro.p, sizeof(uint32_t) * rows, cudaMemcpyDeviceToHost, s));
+    RBF_CUDA_TRY(cudaStreamSynchronize(s));
+    if (ctx->world > 1) {
+      RBF_TRY(dist_plan_cells(ctx, c, hro, (int64_t)ntiles, ctx->rank, ctx->world));
+    } else {
+      RBF_TRY(dist_plan_cells(ctx, c, hro, (int64_t)ntiles, erank, eworld));
+      c->emulated = true;
+    }
   }
   return RBF_OK;
 }

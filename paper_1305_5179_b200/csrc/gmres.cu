@@ -106,6 +106,9 @@ __global__ void residual_kernel(const double* __restrict__ b, const double* __re
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     r[i] = b[i] - f[i];
 }
+__global__ void negate_kernel(const double* __restrict__ a, double* __restrict__ b, int k) {
+  for (int i = threadIdx.x; i < k; i += blockDim.x) b[i] = -a[i];
+}
 __global__ void f32_to_f64(const float* __restrict__ a, double* __restrict__ b, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     b[i] = (double)a[i];
@@ -149,8 +152,19 @@ struct Solver {
     cudaStream_t s = ctx->stream;
     multi_dot_kernel<<<nblk, kVecThreads, 0, s>>>(Vb, n, k, vec, n, partial.as<double>());
     RBF_CHECK_LAUNCH();
-    reduce_partials<<<k, 32, 0, s>>>(partial.as<double>(), k, nblk, out, neg != nullptr, neg);
+    if (ctx->world == 1) {
+      reduce_partials<<<k, 32, 0, s>>>(partial.as<double>(), k, nblk, out, neg != nullptr, neg);
+      RBF_CHECK_LAUNCH();
+      return RBF_OK;
+    }
+    // slab partition: local partial sums, then the sum over ranks (ncclAllReduce)
+    reduce_partials<<<k, 32, 0, s>>>(partial.as<double>(), k, nblk, out, 0, nullptr);
     RBF_CHECK_LAUNCH();
+    RBF_TRY(allreduce_sum(ctx, out, k));
+    if (neg) {
+      negate_kernel<<<1, 64, 0, s>>>(out, neg, k);
+      RBF_CHECK_LAUNCH();
+    }
     return RBF_OK;
   }
   rbf_status maxpy(double* vec, const double* Vb, int k, const double* coef) {
@@ -181,7 +195,7 @@ rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp
                         rbf_solve_report* rep) {
   using clk = std::chrono::steady_clock;
   cudaStream_t s = ctx->stream;
-  Solver S{ctx, c, P, kp, c->n, 30, 0};
+  Solver S{ctx, c, P, kp, c->n_loc(), 30, 0};   // this rank's owned slice (all of it on one GPU)
   S.m = (gcfg && gcfg->restart > 0) ? gcfg->restart : 30;
   if (S.m > 60) { set_error("restart must be <= 60"); return RBF_EINVAL; }
   const double rtol = (gcfg && gcfg->rtol > 0) ? gcfg->rtol : 1e-6;
@@ -347,6 +361,8 @@ rbf_status rbf_gmres_solve(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* k
     return RBF_EINVAL;
   }
   if (precond && precond->cells != c) { set_error("precond was built for other cells"); return RBF_EINVAL; }
+  if (c->world != ctx->world) { set_error("cells were partitioned for another world size"); return RBF_EINVAL; }
+  if (c->emulated) { set_error("RBF_SLAB_EMULATE cells support matvec / grid / precond blocks only"); return RBF_EUNSUPPORTED; }
   RBF_CUDA_TRY(cudaSetDevice(ctx->device));
   KernelParams kp = kernel_params(kern);
   rbf_solve_report R{};
@@ -368,11 +384,15 @@ rbf_status rbf_gmres_solve(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* k
   R.nblocks = P->nblocks;
   R.precond_bytes = P->bytes;
   const int64_t n = c->n;
+  const int64_t o0 = c->view.o0;
   DevBuf bs, xs;
   rbf_status st = bs.alloc(sizeof(float) * n, ctx->stream);
   if (st == RBF_OK) st = xs.alloc(sizeof(double) * n, ctx->stream);
   if (st == RBF_OK) st = gather_f32_to_sorted(ctx, b, c->perm.as<int32_t>(), bs.as<float>(), n);
-  if (st == RBF_OK) st = gmres_sorted(ctx, c, kp, P, gcfg, bs.as<float>(), xs.as<double>(), &R);
+  // the solve runs on this rank's slice [o0, o1) of the sorted order; the full
+  // solution is gathered from all ranks (replicated out)
+  if (st == RBF_OK) st = gmres_sorted(ctx, c, kp, P, gcfg, bs.as<float>() + o0, xs.as<double>() + o0, &R);
+  if (st == RBF_OK) st = allgather_sorted(ctx, c, xs.as<double>());
   if (st == RBF_OK) st = scatter_f64_from_sorted(ctx, xs.as<double>(), c->perm.as<int32_t>(), w, n);
   if (st == RBF_OK) {
     cudaError_t e = cudaStreamSynchronize(ctx->stream);

@@ -115,7 +115,29 @@ struct rbf_ctx {
   rbf::DevBuf pinned_dummy;
   // vector workspaces for matvec (sorted order)
   rbf::DevBuf vec_a, vec_b, src4;
+  // multi-GPU (dist.cu): NCCL communicator (ncclComm_t), rank, world, halo window
+  void* nccl_comm = nullptr;
+  int rank = 0, world = 1;
+  rbf::DevBuf win;
 };
+
+namespace rbf {
+// This rank's share of the global sorted order (dist.cu).  Single GPU: the
+// whole range.  Slab partition: owned targets [o0, o1) = cell planes [p0, p1)
+// along z, their tiles [t0, t1), and the matvec source window [h0, h1).
+struct SlabView {
+  int64_t o0 = 0, o1 = 0;
+  int64_t h0 = 0, h1 = 0;
+  int64_t t0 = 0, t1 = 0;
+  int p0 = 0, p1 = 0;
+};
+// Every rank's slab (identical on all ranks: computed from the replicated cells).
+struct SlabPlan {
+  int world = 1;
+  std::vector<int> plane_lo;                          // [world + 1]
+  std::vector<int64_t> own_lo, own_hi, win_lo, win_hi;  // [world]
+};
+}  // namespace rbf
 
 // Tile of targets for the summation kernels: sorted positions [start, start+count).
 struct rbf_cells {
@@ -138,6 +160,11 @@ struct rbf_cells {
   rbf::DevBuf tiles;         // int2[ntiles] (start, count)
   rbf::DevBuf tile_box;      // float4[2*ntiles] (lo.xyz, ctr.x) (hi.xyz, unused)
   cudaStream_t stream = nullptr;
+  rbf::SlabView view;        // this rank's share (whole range on one GPU)
+  rbf::SlabPlan plan;        // all ranks' slabs (world > 1)
+  int world = 1;             // ranks the cells were partitioned for
+  bool emulated = false;     // RBF_SLAB_EMULATE: one rank's slab on a single GPU (tests)
+  int64_t n_loc() const { return view.o1 - view.o0; }
 };
 
 namespace rbf {
@@ -176,10 +203,24 @@ rbf_status eval_grid_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams
                             const double* w_sorted, const rbf_grid* g, float* field,
                             unsigned long long* pair_stats = nullptr);
 
+// dist.cu (multi-GPU slab partition)
+rbf_status dist_init(rbf_ctx* ctx, const void* unique_id, int rank, int world);
+void dist_destroy(rbf_ctx* ctx);
+void slab_plan(const int64_t* plane_start, const double* weight, int dimz, int reach, int world, SlabPlan& P);
+rbf_status dist_plan_cells(rbf_ctx* ctx, rbf_cells* c, const std::vector<uint32_t>& row_tile_off, int64_t ntiles,
+                           int rank, int world);
+template <class T>
+rbf_status halo_exchange(rbf_ctx* ctx, const rbf_cells* c, const T* x_loc, T* win);
+rbf_status allreduce_sum(rbf_ctx* ctx, double* x, int64_t count);
+rbf_status allreduce_sum_f32(rbf_ctx* ctx, float* x, int64_t count);
+rbf_status allgather_sorted(rbf_ctx* ctx, const rbf_cells* c, double* full);
+
 // small vector kernels (vec.cu)
 rbf_status gather_f32_to_sorted(rbf_ctx* ctx, const float* src, const int32_t* perm, float* dst, int64_t n);
 rbf_status gather_f64_to_sorted(rbf_ctx* ctx, const double* src, const int32_t* perm, double* dst, int64_t n);
 rbf_status gather_f64_to_sorted_f32(rbf_ctx* ctx, const double* src, const int32_t* perm, float* dst, int64_t n);
+rbf_status gather_f32_to_sorted_f64(rbf_ctx* ctx, const float* src, const int32_t* perm, double* dst, int64_t n);
+rbf_status scatter_f64_from_sorted_f32(rbf_ctx* ctx, const double* src, const int32_t* perm, float* dst, int64_t n);
 rbf_status scatter_f32_from_sorted(rbf_ctx* ctx, const float* src, const int32_t* perm, float* dst, int64_t n);
 rbf_status scatter_f64_from_sorted(rbf_ctx* ctx, const double* src, const int32_t* perm, double* dst, int64_t n);
 

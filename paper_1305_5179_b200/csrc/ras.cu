@@ -576,7 +576,12 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
                  std::chrono::duration<double, std::milli>(clk::now() - t0).count());
   };
   cudaStream_t s = ctx->stream;
-  const int64_t n = c->n;
+  // blocks are built from this rank's slice [o0, o1) of the sorted order
+  // (everything on one GPU); block indices are relative to o0
+  const int64_t base = c->view.o0;
+  const int64_t n = c->n_loc();
+  const uint32_t* keys = c->keys.as<uint32_t>() + base;
+  const float4* sorted = c->sorted.as<float4>() + base;
   P->n = n;
   P->kind = cfg ? cfg->kind : 2;
   if (P->kind == 0) { P->nblocks = 0; P->bytes = 0; return RBF_OK; }
@@ -590,17 +595,30 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
   const double shift_abs = shift * kp.amp;
   const bool want_fp32 = cfg && cfg->local_fp32;
 
+  if (ctx->world > 1 && ovs > 0) {
+    set_error("RAS with overlap is single-GPU only; use block-Jacobi (kind 1) across slabs");
+    return RBF_EUNSUPPORTED;
+  }
+  if (n == 0) { P->nblocks = 0; P->bytes = 0; P->kind = 0; return RBF_OK; }   // empty slab
+
   // 1. non-empty cells
-  const int64_t nne = c->nonempty;
-  DevBuf flag, pos, ne_start, ne_key;
+  DevBuf flag, pos, ne_start, ne_key, nne_d;
   RBF_TRY(flag.alloc(4 * n, s));
   RBF_TRY(pos.alloc(4 * n, s));
+  RBF_TRY(nne_d.alloc(8, s));
+  flag_cells<<<grid_for(n, 256), 256, 0, s>>>(keys, n, flag.as<uint32_t>());
+  RBF_CHECK_LAUNCH();
+  RBF_TRY(exclusive_scan_u32(ctx, flag.as<uint32_t>(), pos.as<uint32_t>(), n, nne_d.as<uint32_t>()));
+  int64_t nne = c->nonempty;
+  if (n != c->n) {   // a slab: count its own non-empty cells
+    uint32_t h = 0;
+    RBF_CUDA_TRY(cudaMemcpyAsync(&h, nne_d.p, 4, cudaMemcpyDeviceToHost, s));
+    RBF_CUDA_TRY(cudaStreamSynchronize(s));
+    nne = h;
+  }
   RBF_TRY(ne_start.alloc(4 * nne, s));
   RBF_TRY(ne_key.alloc(4 * nne, s));
-  flag_cells<<<grid_for(n, 256), 256, 0, s>>>(c->keys.as<uint32_t>(), n, flag.as<uint32_t>());
-  RBF_CHECK_LAUNCH();
-  RBF_TRY(exclusive_scan_u32(ctx, flag.as<uint32_t>(), pos.as<uint32_t>(), n, nullptr));
-  compact_cells<<<grid_for(n, 256), 256, 0, s>>>(c->keys.as<uint32_t>(), n, flag.as<uint32_t>(),
+  compact_cells<<<grid_for(n, 256), 256, 0, s>>>(keys, n, flag.as<uint32_t>(),
                                                  pos.as<uint32_t>(), ne_start.as<int32_t>(), ne_key.as<uint32_t>());
   RBF_CHECK_LAUNCH();
   // 2. Morton order of the non-empty cells
@@ -781,7 +799,7 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
 #define RBF_GJ_LAUNCH(RM_, RC_)                                                                            \
   gj_inverse_f32_kernel<RM_, RC_><<<gblocks, kGjThreads, 0, s>>>(                                         \
       P->ext_ptr.as<int64_t>(), P->core_ptr.as<int64_t>(), P->ext_idx.as<int32_t>(), P->w_off.as<int64_t>(), \
-      c->sorted.as<float4>(), kp.amp, two_s2, c2, shift_abs, P->W.as<float>(), bl, cnt, info.as<int>())
+      sorted, kp.amp, two_s2, c2, shift_abs, P->W.as<float>(), bl, cnt, info.as<int>())
         if (bin == 0) RBF_GJ_LAUNCH(8, 4);
         else if (bin == 1) RBF_GJ_LAUNCH(12, 6);
         else RBF_GJ_LAUNCH(14, 7);
@@ -822,7 +840,7 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
     RBF_TRY(jobs_d.ensure(sizeof(LuJob) * jobs.size(), s));
     RBF_CUDA_TRY(cudaMemcpyAsync(jobs_d.p, jobs.data(), sizeof(LuJob) * jobs.size(), cudaMemcpyHostToDevice, s));
     dim3 ag(32, (unsigned)jobs.size());
-    assemble_kernel<<<ag, 256, 0, s>>>(jobs_d.as<LuJob>(), c->sorted.as<float4>(), P->ext_idx.as<int32_t>(),
+    assemble_kernel<<<ag, 256, 0, s>>>(jobs_d.as<LuJob>(), sorted, P->ext_idx.as<int32_t>(),
                                        ws.as<FT>(), kp.amp, two_s2, c2, shift_abs);
     RBF_CHECK_LAUNCH();
     RBF_TRY(batched_lu_restricted_inverse(ctx, jobs_d.as<LuJob>(), jobs, ws.as<FT>(),
@@ -922,6 +940,7 @@ rbf_status rbf_precond_apply(rbf_ctx* ctx, const rbf_precond* P, const float* r,
   RBF_CUDA_TRY(cudaSetDevice(ctx->device));
   const rbf_cells* c = P->cells;
   const int64_t n = P->n;
+  if (ctx->world > 1) { set_error("rbf_precond_apply is single-GPU only"); return RBF_EUNSUPPORTED; }
   RBF_TRY(ctx->vec_a.ensure(sizeof(float) * n, ctx->stream));
   RBF_TRY(ctx->vec_b.ensure(sizeof(float) * n, ctx->stream));
   RBF_TRY(gather_f32_to_sorted(ctx, r, c->perm.as<int32_t>(), ctx->vec_a.as<float>(), n));

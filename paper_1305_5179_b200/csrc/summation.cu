@@ -406,11 +406,12 @@ struct GridDesc {
 __device__ __forceinline__ float node_coord(const GridDesc& gd, int a, int i) {
   return (float)(gd.lo[a] + (double)i * gd.step[a]);
 }
+inline float node_coord_host(const GridDesc& gd, int a, int i) { return (float)(gd.lo[a] + (double)i * gd.step[a]); }
 
 template <int MODE, bool STATS, class OutT>
 __global__ void __launch_bounds__(kSumWarps * 32, 8)
 sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* __restrict__ src,
-               const int2* __restrict__ tiles, const float4* __restrict__ tbox, int64_t ntiles,
+               const int2* __restrict__ tiles, const float4* __restrict__ tbox, int64_t ntiles, int64_t tile_base,
                GridDesc gd, OutT* __restrict__ out, const int32_t* __restrict__ out_perm,
                int* __restrict__ work, unsigned long long* __restrict__ stats) {
   __shared__ __align__(16) float ring[kSumWarps][10][kBufPad];
@@ -426,6 +427,7 @@ sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
       tile = __shfl_sync(0xffffffffu, t0, 0);
     }
     if (tile >= ntiles) break;
+    tile += tile_base;   // this rank's tile range [tile_base, tile_base + ntiles) (slab partition)
     float3 blo, bhi;
     float xr[2], yr[2], zr[2];   // raw target coordinates
     bool tv[2];
@@ -590,7 +592,7 @@ struct Flush64 {
 __global__ void __launch_bounds__(kSumWarps * 32)
 sum_f64_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* __restrict__ src,
                const double* __restrict__ w, const int2* __restrict__ tiles,
-               const float4* __restrict__ tbox, int64_t ntiles, double* __restrict__ out,
+               const float4* __restrict__ tbox, int64_t ntiles, int64_t tile_base, double* __restrict__ out,
                const int32_t* __restrict__ out_perm, int* __restrict__ work) {
   __shared__ __align__(16) float ringf[kSumWarps][3][kBufPad];
   __shared__ __align__(16) double ringd[kSumWarps][kBufPad];
@@ -604,6 +606,7 @@ sum_f64_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
       tile = __shfl_sync(0xffffffffu, t0, 0);
     }
     if (tile >= ntiles) break;
+    tile += tile_base;
     const int2 tl = tiles[tile];
     const float4 a = tbox[2 * tile], b = tbox[2 * tile + 1];
     const float3 blo = make_float3(a.x, a.y, a.z), bhi = make_float3(b.x, b.y, b.z);
@@ -701,11 +704,14 @@ KernelParams kernel_params(const rbf_kernel* k) {
   return p;
 }
 
+// Public fp32 path (and the pair accounting): w_sorted covers all n centres
+// (sorted order); this rank's tiles write f_out[out_perm ? perm[j] : j].
 rbf_status matvec_sorted_f32(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
                              const float* w_sorted, float* f_out, const int32_t* out_perm,
                              unsigned long long* pair_stats) {
   cudaStream_t s = ctx->stream;
   const int64_t n = c->n;
+  const SlabView& V = c->view;
   RBF_TRY(ctx->src4.ensure(sizeof(float4) * n, s));
   RBF_TRY(ctx->counter.ensure(256, s));
   pack_src_f32<<<grid_for(n, 256), 256, 0, s>>>(c->sorted.as<float4>(), w_sorted, n, ctx->src4.as<float4>());
@@ -716,46 +722,70 @@ rbf_status matvec_sorted_f32(rbf_ctx* ctx, const rbf_cells* c, const KernelParam
   if (pair_stats) {
     sum_f32_kernel<0, true, float><<<sum_blocks(ctx, sum_f32_kernel<0, true, float>), kSumWarps * 32, 0, s>>>(
         G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), c->tiles.as<int2>(), c->tile_box.as<float4>(),
-        c->ntiles, gd, f_out, out_perm, ctx->counter.as<int>(), pair_stats);
+        V.t1 - V.t0, V.t0, gd, f_out, out_perm, ctx->counter.as<int>(), pair_stats);
   } else {
     ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
     sum_f32_kernel<0, false, float><<<sum_blocks(ctx, sum_f32_kernel<0, false, float>), kSumWarps * 32, 0, s>>>(
         G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), c->tiles.as<int2>(), c->tile_box.as<float4>(),
-        c->ntiles, gd, f_out, out_perm, ctx->counter.as<int>(), nullptr);
+        V.t1 - V.t0, V.t0, gd, f_out, out_perm, ctx->counter.as<int>(), nullptr);
   }
   RBF_CHECK_LAUNCH();
   return RBF_OK;
 }
 
-rbf_status matvec_sorted_f32_d(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp, const double* w_sorted,
-                               double* f_sorted) {
+// Solver path, fp32 tier: w_loc / f_loc are this rank's owned slice (sorted
+// order, fp64).  The source window [h0, h1) is assembled by the halo exchange
+// (world > 1); the kernel indexes sources and targets by global sorted
+// position, so the window and output pointers are shifted by h0 and o0.
+rbf_status matvec_sorted_f32_d(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp, const double* w_loc,
+                               double* f_loc) {
   cudaStream_t s = ctx->stream;
-  const int64_t n = c->n;
-  RBF_TRY(ctx->src4.ensure(sizeof(float4) * n, s));
+  const SlabView& V = c->view;
+  const int64_t nw = V.h1 - V.h0;
+  const double* w_win = w_loc;
+  if (ctx->world > 1 || c->emulated) {
+    RBF_TRY(ctx->win.ensure(sizeof(double) * std::max<int64_t>(nw, 1), s));
+    RBF_TRY(halo_exchange<double>(ctx, c, w_loc, ctx->win.as<double>()));
+    w_win = ctx->win.as<double>();
+  }
+  RBF_TRY(ctx->src4.ensure(sizeof(float4) * std::max<int64_t>(nw, 1), s));
   RBF_TRY(ctx->counter.ensure(256, s));
-  pack_src_f64w<<<grid_for(n, 256), 256, 0, s>>>(c->sorted.as<float4>(), w_sorted, n, ctx->src4.as<float4>());
-  RBF_CHECK_LAUNCH();
+  if (nw > 0) {
+    pack_src_f64w<<<grid_for(nw, 256), 256, 0, s>>>(c->sorted.as<float4>() + V.h0, w_win, nw, ctx->src4.as<float4>());
+    RBF_CHECK_LAUNCH();
+  }
   RBF_CUDA_TRY(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
   SumGeom G = make_geom(c, kp);
   GridDesc gd{};
   ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
   sum_f32_kernel<0, false, double><<<sum_blocks(ctx, sum_f32_kernel<0, false, double>), kSumWarps * 32, 0, s>>>(
-      G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), c->tiles.as<int2>(), c->tile_box.as<float4>(),
-      c->ntiles, gd, f_sorted, nullptr, ctx->counter.as<int>(), nullptr);
+      G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>() - V.h0, c->tiles.as<int2>(), c->tile_box.as<float4>(),
+      V.t1 - V.t0, V.t0, gd, f_loc - V.o0, nullptr, ctx->counter.as<int>(), nullptr);
   RBF_CHECK_LAUNCH();
   return RBF_OK;
 }
 
+// fp64 tier, same conventions as matvec_sorted_f32_d; out_perm (single GPU,
+// public path only) scatters to the caller's order.
 rbf_status matvec_sorted_f64(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
-                             const double* w_sorted, double* f_out, const int32_t* out_perm) {
+                             const double* w_loc, double* f_out, const int32_t* out_perm) {
   cudaStream_t s = ctx->stream;
+  const SlabView& V = c->view;
+  const int64_t nw = V.h1 - V.h0;
+  const double* w_win = w_loc;
+  if (ctx->world > 1 || c->emulated) {
+    RBF_TRY(ctx->win.ensure(sizeof(double) * std::max<int64_t>(nw, 1), s));
+    RBF_TRY(halo_exchange<double>(ctx, c, w_loc, ctx->win.as<double>()));
+    w_win = ctx->win.as<double>();
+  }
   RBF_TRY(ctx->counter.ensure(256, s));
   RBF_CUDA_TRY(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
   SumGeom G = make_geom(c, kp);
   ProfScope ps(ctx, RBF_PROF_MATVEC_F64);
   sum_f64_kernel<<<sum_blocks(ctx, sum_f64_kernel), kSumWarps * 32, 0, s>>>(
-      G, c->cell_start.as<int32_t>(), c->sorted.as<float4>(), w_sorted, c->tiles.as<int2>(),
-      c->tile_box.as<float4>(), c->ntiles, f_out, out_perm, ctx->counter.as<int>());
+      G, c->cell_start.as<int32_t>(), c->sorted.as<float4>(), w_win - V.h0, c->tiles.as<int2>(),
+      c->tile_box.as<float4>(), V.t1 - V.t0, V.t0, out_perm ? f_out : f_out - V.o0, out_perm,
+      ctx->counter.as<int>());
   RBF_CHECK_LAUNCH();
   return RBF_OK;
 }
@@ -782,17 +812,33 @@ rbf_status eval_grid_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams
     gd.n[a] = g->n[a];
     gd.nb[a] = (g->n[a] + 3) / 4;
   }
-  int64_t nblk = (int64_t)gd.nb[0] * gd.nb[1] * gd.nb[2];
+  const int64_t per_layer = (int64_t)gd.nb[0] * gd.nb[1];
+  int64_t b0 = 0, b1 = per_layer * gd.nb[2];
+  if (ctx->world > 1 || c->emulated) {
+    // node-block layers go to the rank owning the cell plane of their first node
+    int bz0 = gd.nb[2], bz1 = gd.nb[2];
+    for (int bz = 0; bz < gd.nb[2]; ++bz) {
+      const float z = node_coord_host(gd, 2, 4 * bz);
+      int pz = (int)std::floor((double)((z - c->lo[2]) * c->inv_h));
+      pz = std::min(std::max(pz, 0), c->dim[2] - 1);
+      const bool mine = pz >= c->view.p0 && pz < c->view.p1;
+      if (mine && bz0 == gd.nb[2]) bz0 = bz;
+      if (mine) bz1 = bz + 1;
+    }
+    if (bz0 == gd.nb[2]) bz1 = bz0;
+    b0 = per_layer * bz0;
+    b1 = per_layer * bz1;
+  }
   if (pair_stats) {
     sum_f32_kernel<1, true, float><<<sum_blocks(ctx, sum_f32_kernel<1, true, float>), kSumWarps * 32, 0, s>>>(
-        G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), nullptr, nullptr, nblk, gd, field, nullptr,
+        G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), nullptr, nullptr, b1 - b0, b0, gd, field, nullptr,
         ctx->counter.as<int>(), pair_stats);
     RBF_CHECK_LAUNCH();
     return RBF_OK;
   }
   ProfScope ps(ctx, RBF_PROF_GRID);
   sum_f32_kernel<1, false, float><<<sum_blocks(ctx, sum_f32_kernel<1, false, float>), kSumWarps * 32, 0, s>>>(
-      G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), nullptr, nullptr, nblk, gd, field, nullptr,
+      G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), nullptr, nullptr, b1 - b0, b0, gd, field, nullptr,
       ctx->counter.as<int>(), nullptr);
   RBF_CHECK_LAUNCH();
   return RBF_OK;

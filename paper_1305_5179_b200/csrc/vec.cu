@@ -37,6 +37,16 @@ rbf_status gather_f64_to_sorted_f32(rbf_ctx* ctx, const double* src, const int32
   RBF_CHECK_LAUNCH();
   return RBF_OK;
 }
+rbf_status gather_f32_to_sorted_f64(rbf_ctx* ctx, const float* src, const int32_t* perm, double* dst, int64_t n) {
+  gather_kernel<float, double><<<grid_for(n, 256), 256, 0, ctx->stream>>>(src, perm, dst, n);
+  RBF_CHECK_LAUNCH();
+  return RBF_OK;
+}
+rbf_status scatter_f64_from_sorted_f32(rbf_ctx* ctx, const double* src, const int32_t* perm, float* dst, int64_t n) {
+  scatter_kernel<double, float><<<grid_for(n, 256), 256, 0, ctx->stream>>>(src, perm, dst, n);
+  RBF_CHECK_LAUNCH();
+  return RBF_OK;
+}
 rbf_status scatter_f32_from_sorted(rbf_ctx* ctx, const float* src, const int32_t* perm, float* dst, int64_t n) {
   scatter_kernel<float, float><<<grid_for(n, 256), 256, 0, ctx->stream>>>(src, perm, dst, n);
   RBF_CHECK_LAUNCH();

@@ -82,11 +82,14 @@ EXPORTS = {
     "rbf_last_error": (C.c_char_p, []),
     "rbf_abi_version": (C.c_int, []),
     "rbf_launch_count": (C.c_int64, []),
+    "rbf_nccl_unique_id": (C.c_int, [_P]),
+    "rbf_slab_plan": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, _P, _P, _P, _P, _P]),
     "rbf_extend_points": (C.c_int, [_P, _P, _P, C.c_int64, C.c_double, C.c_double, _P, _P]),
     "rbf_build_cells": (C.c_int, [_P, _P, C.c_int64, C.POINTER(_Kernel), C.POINTER(_CellCfg),
                                   C.POINTER(_P)]),
     "rbf_cells_free": (None, [_P]),
     "rbf_cells_info": (C.c_int, [_P, C.POINTER(_CellsDesc)]),
+    "rbf_cells_slab": (C.c_int, [_P, _P]),
     "rbf_cells_view": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)]),
     "rbf_matvec": (C.c_int, [_P, _P, C.POINTER(_Kernel), C.c_int, _P, _P]),
     "rbf_matvec_pairs": (C.c_int, [_P, _P, C.POINTER(_Kernel), C.POINTER(C.c_int64),
@@ -180,15 +183,54 @@ class Kernel:
         return _Kernel(self.sigma, self.cutoff_sigmas, self.amplitude)
 
 
-class Context:
-    """rbf_create on `device`, issuing work on torch's current stream of that device."""
+def nccl_unique_id() -> bytes:
+    """rbf_nccl_unique_id: 128 bytes for rank 0 to broadcast (multi-GPU contexts)."""
+    buf = C.create_string_buffer(128)
+    _check(load_library().rbf_nccl_unique_id(buf))
+    return buf.raw
 
-    def __init__(self, device: int = 0, stream: torch.cuda.Stream | None = None):
+
+def slab_plan(plane_start, plane_weight, reach: int, world: int):
+    """rbf_slab_plan (host only): the slab partition the library uses for world > 1.
+    Returns dict(plane_lo, own_lo, own_hi, win_lo, win_hi) as numpy arrays."""
+    import numpy as np
+    ps = np.ascontiguousarray(plane_start, dtype=np.int64)
+    pw = np.ascontiguousarray(plane_weight, dtype=np.float64)
+    dimz = pw.size
+    if ps.size != dimz + 1:
+        raise ValueError("plane_start needs dimz + 1 entries")
+    out = dict(plane_lo=np.zeros(world + 1, np.int32), own_lo=np.zeros(world, np.int64),
+               own_hi=np.zeros(world, np.int64), win_lo=np.zeros(world, np.int64), win_hi=np.zeros(world, np.int64))
+    ptr = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    _check(load_library().rbf_slab_plan(ptr(ps), ptr(pw), dimz, reach, world, ptr(out["plane_lo"]),
+                                        ptr(out["own_lo"]), ptr(out["own_hi"]), ptr(out["win_lo"]),
+                                        ptr(out["win_hi"])))
+    return out
+
+
+class Context:
+    """rbf_create on `device`, issuing work on torch's current stream of that device.
+
+    distributed=True (and an initialised torch.distributed group with world > 1):
+    one context per rank/GPU sharing an NCCL communicator; rank 0's NCCL id is
+    broadcast with torch.distributed (plumbing only).  Calls then take and
+    return replicated (full) arrays while the library shards the work."""
+
+    def __init__(self, device: int = 0, stream: torch.cuda.Stream | None = None, distributed: bool = False):
         lib = load_library()
         self.device = device
         self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        rank, world, uid = 0, 1, None
+        if distributed:
+            import torch.distributed as dist
+            if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+                rank, world = dist.get_rank(), dist.get_world_size()
+                box = [nccl_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(box, src=0)
+                uid = C.create_string_buffer(box[0], 128)
+        self.rank, self.world = rank, world
         h = C.c_void_p()
-        _check(lib.rbf_create(C.byref(h), device, C.c_void_p(self.stream.cuda_stream), None, 0, 1))
+        _check(lib.rbf_create(C.byref(h), device, C.c_void_p(self.stream.cuda_stream), uid, rank, world))
         self._h = h
 
     PROF_STAGES = ("cells", "matvec_f32", "matvec_f64", "grid", "precond_setup", "precond_apply")
@@ -252,6 +294,14 @@ class Cells:
         _check(_lib.rbf_cells_info(self._h, C.byref(d)))
         return dict(n=d.n, dim=tuple(d.dim), lo=tuple(d.lo), inv_h=d.inv_h, cell_edge=d.cell_edge,
                     reach=d.reach, ncell=d.ncell, ntiles=d.ntiles, nonempty_cells=d.nonempty_cells)
+
+    def slab(self) -> dict:
+        """rbf_cells_slab: this rank's owned / window / tile / plane ranges."""
+        import numpy as np
+        v = np.zeros(8, dtype=np.int64)
+        _check(_lib.rbf_cells_slab(self._h, v.ctypes.data_as(C.c_void_p)))
+        return dict(own=(int(v[0]), int(v[1])), window=(int(v[2]), int(v[3])), tiles=(int(v[4]), int(v[5])),
+                    planes=(int(v[6]), int(v[7])))
 
     def view(self) -> dict:
         """Copies of the library's cell arrays (perm, sorted float4, keys, cell_start)."""
