@@ -114,6 +114,17 @@ def precond_name(cfg) -> str:
             f"{'fp32 on-chip' if cfg.local_fp32 else 'fp64'} local inverses)")
 
 
+def measured_traffic(cfg_name: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full
+    capture (profiles/), or None when there is none for this config."""
+    path = os.path.join(ROOT, "profiles", "r01", f"traffic_sum_f32_{cfg_name}.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def make_problem(cfg_name: str, seed: int):
     from synth import make_inputs
     t = time.time()
@@ -232,7 +243,7 @@ def run_ours(args, rank, world, local):
                 "frac_at_measured_clock": (achieved / (SMS * MUFU_PER_CLK_PER_SM * clk["sm_mhz"] * 1e6 / 1e12)
                                            if clk.get("sm_mhz") else None),
                 "avg_launch_ms": avg_mv_ms, "launches": n_mv, "useful_pairs_per_launch": useful_mv,
-                "visited_pairs_per_launch": visited_mv, "traffic": None}
+                "visited_pairs_per_launch": visited_mv, "traffic": measured_traffic(args.config)}
     stage_ms = {k: round(v[0] / args.steps, 3) for k, v in prof.items()}
 
     cpu = None

@@ -212,7 +212,9 @@ struct Ring32 {
   float* bs = nullptr;   // |s'|^2 (expansion path only)
 };
 
-// Dual-ring staging of the fp32 fast path (see traverse2).
+// Dual-ring staging of the fp32 fast path (see traverse2).  SPLIT = false: no
+// interior/boundary classification, every kept source goes to the unmasked ring.
+template <bool SPLIT>
 struct Stage32x2 {
   Ring32 rb, ri;
   const float4* __restrict__ src;
@@ -226,6 +228,7 @@ struct Stage32x2 {
     const float az = blo.z - p.z, bz = p.z - bhi.z;
     const float gx = fmaxf(0.f, fmaxf(ax, bx)), gy = fmaxf(0.f, fmaxf(ay, by)), gz = fmaxf(0.f, fmaxf(az, bz));
     if (!valid || gx * gx + gy * gy + gz * gz > cc2) return 0;
+    if (!SPLIT) return 2;
     // farthest point of the box
     const float fx = fmaxf(fabsf(ax), fabsf(bx)), fy = fmaxf(fabsf(ay), fabsf(by)), fz = fmaxf(fabsf(az), fabsf(bz));
     return (fx * fx + fy * fy + fz * fz <= ci2) ? 2 : 1;
@@ -494,7 +497,12 @@ sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
         th[t] = G.c2s - T2;
         tf[t] = ex2(-T2);
       }
-      Stage32x2 st{R, RI, src, blo, bhi, ctr, G.cc2, G.ci2, G.s, make_float4(0, 0, 0, 0)};
+      // matvec (MODE 0): every staged source goes through the unmasked ring --
+      // a pair beyond the cutoff but inside the culling radius adds a 2^-r <=
+      // 2^-(k c^2) = 2^-25.97 term (<= 1/4 ulp of the peak entry; DESIGN.md
+      // reading R18).  Grid (MODE 1) keeps the mask: nodes with no centre
+      // within the cutoff must be exactly 0 (reading R5).
+      Stage32x2<MODE != 0> st{R, RI, src, blo, bhi, ctr, G.cc2, G.ci2, G.s, make_float4(0, 0, 0, 0)};
       int nB = 0, nI = 0, cnt;
       if (two) {
         Flush32e<2, true> fb{R, acc, mx, my, mz, th};
