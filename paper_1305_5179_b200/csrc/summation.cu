@@ -580,7 +580,7 @@ struct Flush64 {
   Ring64 r;
   double* acc;                       // [2]
   const double* xt; const double* yt; const double* zt;
-  double c2, two_s2, amp;
+  double c2, nis;                    // cutoff^2 and -1/(2 sigma^2); the amplitude is applied at the end
   __device__ __forceinline__ void operator()(int cnt) {
     for (int j = 0; j < cnt; ++j) {
       const double sx = (double)r.bx[j], sy = (double)r.by[j], sz = (double)r.bz[j], wj = r.bw[j];
@@ -588,10 +588,10 @@ struct Flush64 {
       for (int t = 0; t < 2; ++t) {
         double dx = __dsub_rn(sx, xt[t]), dy = __dsub_rn(sy, yt[t]), dz = __dsub_rn(sz, zt[t]);
         double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-        if (d2 <= c2) {
-          double v = __dmul_rn(amp, exp(-d2 / two_s2));
-          acc[t] = __fma_rn(v, wj, acc[t]);
-        }
+        // predicated (no divergent branch); exp(-d2/(2 sigma^2)) as a product by
+        // the reciprocal: <= 1 ulp of the argument, ~1e-15 relative in the entry
+        const double e = exp(__dmul_rn(d2, nis));
+        acc[t] = __fma_rn(d2 <= c2 ? e : 0.0, wj, acc[t]);
       }
     }
   }
@@ -630,7 +630,7 @@ sum_f64_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
       xt[t] = p.x; yt[t] = p.y; zt[t] = p.z;
     }
     Stage64 st{R, src, w, blo, bhi, G.cc2, make_float4(0, 0, 0, 0), 0.0};
-    Flush64 fl{R, acc, xt, yt, zt, G.c2d, G.two_s2, G.ampd};
+    Flush64 fl{R, acc, xt, yt, zt, G.c2d, -1.0 / G.two_s2};
     int nbuf = 0;
     traverse(G, cell_start, blo, bhi, lane, st, fl, nbuf);
     __syncwarp();
@@ -640,7 +640,7 @@ sum_f64_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
     for (int t = 0; t < 2; ++t) {
       if (!tv[t]) continue;
       int64_t o = out_perm ? out_perm[tidx[t]] : tidx[t];
-      out[o] = acc[t];
+      out[o] = G.ampd * acc[t];
     }
   }
 }
