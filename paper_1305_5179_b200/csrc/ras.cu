@@ -555,6 +555,44 @@ __global__ void round_w_kernel(const int64_t* __restrict__ trip, int64_t ntrip, 
   }
 }
 
+// fp32 W: half-warp per core row (16 lanes stride the row, coalesced 64 B
+// segments), fp32 products and accumulation (W is an fp32 approximation of the
+// local inverse already), r_ext staged in shared memory as fp32.
+template <class VT>
+__global__ void __launch_bounds__(256)
+apply_f32w_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __restrict__ core_ptr,
+                  const int32_t* __restrict__ ext_idx, const int64_t* __restrict__ w_off, const float* __restrict__ W,
+                  const VT* __restrict__ r, VT* __restrict__ z, int64_t nblocks) {
+  extern __shared__ float srf[];
+  const int tid = threadIdx.x, l16 = tid & 15, half = (tid >> 4) & 1, wid = tid >> 5, nw = blockDim.x >> 5;
+  for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x) {
+    const int64_t e0 = ext_ptr[b];
+    const int m = (int)(ext_ptr[b + 1] - e0);
+    const int nc = (int)(core_ptr[b + 1] - core_ptr[b]);
+    for (int e = tid; e < m; e += blockDim.x) srf[e] = (float)r[ext_idx[e0 + e]];
+    __syncthreads();
+    const float* Wb = W + w_off[b];
+    // the warp stays converged: both halves run the same trip count (row pairs)
+    for (int c0 = 2 * wid; c0 < nc; c0 += 2 * nw) {
+      const int c = c0 + half;
+      const bool valid = c < nc;
+      const float* row = Wb + (int64_t)(valid ? c : c0) * m;
+      float a0 = 0.f, a1 = 0.f;
+      int e = l16;
+      for (; e + 16 < m; e += 32) {
+        a0 = fmaf(__ldg(row + e), srf[e], a0);
+        a1 = fmaf(__ldg(row + e + 16), srf[e + 16], a1);
+      }
+      if (e < m) a0 = fmaf(__ldg(row + e), srf[e], a0);
+      float acc = a0 + a1;
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (valid && l16 == 0) z[ext_idx[e0 + (m - nc) + c]] = (VT)acc;
+    }
+    __syncthreads();
+  }
+}
+
 template <class VT>
 __global__ void copy_kernel(const VT* __restrict__ a, VT* __restrict__ b, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -882,13 +920,14 @@ rbf_status precond_apply_sorted(rbf_ctx* ctx, const rbf_precond* P, const VT* r,
   const int blocks = (int)std::min<int64_t>(P->nblocks, (int64_t)ctx->sm_count * 16);
   const size_t smem = sizeof(double) * (size_t)P->max_m;
   if (P->w_fp32) {
-    if (smem > 48 * 1024)
-      RBF_CUDA_TRY(cudaFuncSetAttribute(apply_kernel<VT, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem));
+    const size_t smemf = sizeof(float) * (size_t)P->max_m;
+    if (smemf > 48 * 1024)
+      RBF_CUDA_TRY(cudaFuncSetAttribute(apply_f32w_kernel<VT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smemf));
     ProfScope ps(ctx, RBF_PROF_PRECOND_APPLY);
-    apply_kernel<VT, float><<<blocks, 256, smem, s>>>(P->ext_ptr.as<int64_t>(), P->core_ptr.as<int64_t>(),
-                                                      P->ext_idx.as<int32_t>(), P->w_off.as<int64_t>(),
-                                                      P->W.as<float>(), r, z, P->nblocks);
+    apply_f32w_kernel<VT><<<blocks, 256, smemf, s>>>(P->ext_ptr.as<int64_t>(), P->core_ptr.as<int64_t>(),
+                                                     P->ext_idx.as<int32_t>(), P->w_off.as<int64_t>(),
+                                                     P->W.as<float>(), r, z, P->nblocks);
     RBF_CHECK_LAUNCH();
     return RBF_OK;
   }
