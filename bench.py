@@ -114,6 +114,31 @@ def precond_name(cfg) -> str:
             f"{'fp32 on-chip' if cfg.local_fp32 else 'fp64'} local inverses)")
 
 
+def zero_set_quality(R, ctx, d, field, lo, hi, gn):
+    import torch
+    data = torch.as_tensor(d["x"], dtype=torch.float64, device=field.device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s = torch.cuda.current_stream()
+    e0.record(s)
+    pts = R.zero_set(ctx, field.reshape(-1), lo, hi, gn, data, 2 * d["sigma"])
+    e1.record(s)
+    torch.cuda.synchronize()
+    P = pts.cpu().numpy()
+    out = {"points": int(P.shape[0]), "ms": e0.elapsed_time(e1), "eps": 2 * d["sigma"]}
+    cfg = d["cfg"]
+    if cfg.kind == "blobby" and P.shape[0]:
+        from synth.surfaces import _blobby_params, blobby_field
+        K = cfg.kw.get("K", 16)
+        _, c, sk = _blobby_params(K, d.get("seed", 0), 0.25 if K <= 16 else 0.15)
+        sel = P[np.random.default_rng(0).choice(P.shape[0], min(P.shape[0], 200000), replace=False)]
+        g, grad = blobby_field(sel, c, sk)
+        dist = np.abs(g) / np.linalg.norm(grad, axis=1)
+        out.update(dist_to_true_surface={"mean": float(dist.mean()), "p99": float(np.quantile(dist, 0.99)),
+                                         "max": float(dist.max()), "sampled_points": int(sel.shape[0]),
+                                         "grid_step": float((hi[0] - lo[0]) / (gn[0] - 1))})
+    return out
+
+
 def measured_traffic(cfg_name: str):
     """DRAM bytes per launch of the dominant kernel from the committed ncu --set full
     capture (profiles/), or None when there is none for this config."""
@@ -232,6 +257,13 @@ def run_ours(args, rank, world, local):
                "h2d_bytes_per_step": int(xyz_h.numel() * 4 + b_h.numel() * 4),
                "d2h_bytes_per_step": int(w_h.numel() * 8 + f_h.numel() * 4)}
 
+    # Alg.1 step 3 output (outside the timed step): the eps-masked zero set of the
+    # last field (rbf_zero_set, eps = 2 sigma, reading R11) and its distance to
+    # the generator's exact surface g = 0 (first-order |g| / |grad g|)
+    zs = None
+    if rank == 0:
+        zs = zero_set_quality(R, ctx, d, field, lo, hi, gn)
+
     # roofline of the dominant kernel (fp32 summation), live CUDA-event timing
     t_mv, n_mv = prof["matvec_f32"]
     avg_mv_ms = t_mv / max(n_mv, 1)
@@ -271,7 +303,8 @@ def run_ours(args, rank, world, local):
                    "matvecs_f64_per_step": mv64 / args.steps, "stage_ms_per_step": stage_ms,
                    "iters_phase1": last["iters_phase1"], "iters_phase2": last["iters_phase2"],
                    "rel_residual_true": last["rel_residual_true"], "converged": last["converged"],
-                   "ras_blocks": last["nblocks"], "precond_bytes": last["precond_bytes"], "cells": info,
+                   "ras_blocks": last["nblocks"], "precond_bytes": last["precond_bytes"], "zero_set": zs,
+                   "cells": info,
                    "gen_s": round(d["gen_s"], 1)},
     }
     out["gpu_launches"] = launches

@@ -282,6 +282,21 @@ rbf_status rbf_gmres_solve(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kerne
 rbf_status rbf_eval_grid(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern,
                          const double* w, const rbf_grid* grid, float* field);
 
+/* ---- masked zero set of the interpolant (§2.1.3) ----------------
+ * The surface is the zero level set of P_f restricted to the eps-surrounding
+ * of the data, M* ~ M_ext^eps cap S_0 (reading R11).
+ * field: DEVICE fp32 values of P_f on `grid` (x fastest, as rbf_eval_grid
+ * writes them); data: DEVICE fp64 ndata x 3 (the surface points X, NOT the
+ * +/-delta offsets); eps > 0.  For each grid edge (a, b) along x, then y, then
+ * z, in order of the lower node's flat index: if F_a * F_b < 0 (fp64) and both
+ * nodes lie within eps of a data point (fp64 distances), the point
+ * p_a + t (p_b - p_a), t = F_a / (F_a - F_b), is written to points (DEVICE
+ * fp64, row-major x,y,z; at most cap rows).  *count (HOST) receives the total
+ * number of crossings (may exceed cap: call again with a larger buffer).
+ * Synchronises.  Errors: RBF_EINVAL (NULLs, eps <= 0, bad grid, non-finite data). */
+rbf_status rbf_zero_set(rbf_ctx* ctx, const float* field, const rbf_grid* grid, const double* data,
+                        int64_t ndata, double eps, double* points, int64_t cap, int64_t* count);
+
 /* ---- profiling (CUDA events on the context stream) -------------------------
  * When enabled, every launch of the listed device stages is bracketed by a
  * pair of CUDA events recorded on the context's stream.  rbf_profile_query

@@ -6,8 +6,8 @@ CPU oracle (oracle/, test infrastructure only) and has no CPU fallback.
 """
 from .rbf import (Context, Cells, Kernel, Precond, RbfError, SolveReport, eval_grid, eval_grid_pairs, extend_points,
                   gmres_solve, launch_count, load_library, matvec, matvec_pairs, nccl_unique_id, reconstruct_host,
-                  slab_plan)
+                  slab_plan, zero_set)
 
 __all__ = ["Context", "Cells", "Kernel", "Precond", "RbfError", "SolveReport", "eval_grid", "eval_grid_pairs",
            "extend_points", "gmres_solve", "launch_count", "load_library", "matvec", "matvec_pairs", "nccl_unique_id",
-           "reconstruct_host", "slab_plan"]
+           "reconstruct_host", "slab_plan", "zero_set"]

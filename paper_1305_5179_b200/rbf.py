@@ -104,6 +104,8 @@ EXPORTS = {
     "rbf_eval_grid": (C.c_int, [_P, _P, C.POINTER(_Kernel), _P, C.POINTER(_Grid), _P]),
     "rbf_eval_grid_pairs": (C.c_int, [_P, _P, C.POINTER(_Kernel), C.POINTER(_Grid), C.POINTER(C.c_int64),
                                       C.POINTER(C.c_int64)]),
+    "rbf_zero_set": (C.c_int, [_P, _P, C.POINTER(_Grid), _P, C.c_int64, C.c_double, _P, C.c_int64,
+                               C.POINTER(C.c_int64)]),
     "rbf_profile_enable": (C.c_int, [_P, C.c_int]),
     "rbf_profile_query": (C.c_int, [_P, _P, _P]),
     "rbf_reconstruct_host": (C.c_int, [_P, _P, _P, C.c_int64, C.POINTER(_Kernel), C.POINTER(_CellCfg),
@@ -370,6 +372,24 @@ def eval_grid_pairs(ctx: Context, cells: Cells, kernel: Kernel, lo, hi, n, visit
     u, v = C.c_int64(), C.c_int64()
     _check(_lib.rbf_eval_grid_pairs(ctx._h, cells._h, C.byref(kernel._c()), C.byref(g), C.byref(u), C.byref(v)))
     return (u.value, v.value) if visited else u.value
+
+
+def zero_set(ctx: Context, field: torch.Tensor, lo, hi, n, data: torch.Tensor, eps: float, cap: int | None = None):
+    """rbf_zero_set: points (K x 3, fp64, device) of the eps-masked zero set of the
+    grid field (§2.1.3); `data` = the surface points X (N x 3 fp64, device)."""
+    g, n3 = _grid_c(lo, hi, n)
+    _need(field, torch.float32, n3[0] * n3[1] * n3[2], "field")
+    _need(data, torch.float64, data.shape[0] * 3, "data")
+    cnt = C.c_int64()
+    cap = cap if cap is not None else max(1024, (n3[0] * n3[1] + n3[1] * n3[2] + n3[0] * n3[2]) * 2)
+    for _ in range(2):
+        pts = torch.empty((max(cap, 1), 3), dtype=torch.float64, device=field.device)
+        _check(_lib.rbf_zero_set(ctx._h, _ptr(field), C.byref(g), _ptr(data), data.shape[0], eps, _ptr(pts), cap,
+                                 C.byref(cnt)))
+        if cnt.value <= cap:
+            return pts[:cnt.value]
+        cap = cnt.value
+    return pts[:cnt.value]
 
 
 class Precond:

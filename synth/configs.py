@@ -84,6 +84,6 @@ def make_inputs(name: str, seed: int = 0, n: int | None = None, **over):
     else:
         x, nrm = blobby(cfg.n, seed=seed, **cfg.kw)
     lo, hi, gn = grid_box(cfg, x)
-    return dict(cfg=cfg, x=np.ascontiguousarray(x), normals=np.ascontiguousarray(nrm),
+    return dict(cfg=cfg, seed=seed, x=np.ascontiguousarray(x), normals=np.ascontiguousarray(nrm),
                 delta=cfg.delta, sigma=cfg.sigma, cutoff_sigmas=cfg.cutoff_sigmas,
                 grid_lo=lo, grid_hi=hi, grid_n=gn)

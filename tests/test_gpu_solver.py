@@ -316,3 +316,25 @@ def test_reconstruct_host_matches_device_path(R, ctx, c1_solution):
     Fd = host(R.eval_grid(ctx, s["cells"], s["kern"], dev(s["w"], torch.float64), d["grid_lo"], d["grid_hi"],
                           d["grid_n"]))
     np.testing.assert_array_equal(F.numpy(), Fd)
+
+
+def test_zero_set_matches_oracle_and_sphere(R, ctx, c1_solution):
+    """SURVEY §8(f) 1 / reading R11: rbf_zero_set on the GPU field equals the
+    oracle's zero_crossings of the same field point for point (same fp64
+    decisions, same order), and reconstructs the unit sphere (c1)."""
+    s = c1_solution
+    d = s["d"]
+    sigma = d["sigma"]
+    lo, hi, gn = d["grid_lo"], d["grid_hi"], d["grid_n"]
+    F = R.eval_grid(ctx, s["cells"], s["kern"], dev(s["w"], torch.float64), lo, hi, gn)
+    data = dev(d["x"], torch.float64)
+    pts = host(R.zero_set(ctx, F.reshape(-1), lo, hi, gn, data, 2 * sigma))
+    ref = OG.zero_crossings(host(F).ravel(), lo, hi, gn, d["x"], 2 * sigma)
+    assert pts.shape == ref.shape and len(pts) > 1000
+    np.testing.assert_array_equal(pts, ref)
+    assert np.abs(np.linalg.norm(pts, axis=1) - 1.0).max() <= 5e-3
+    # a too-small buffer reports the full count and fills what fits
+    few = host(R.zero_set(ctx, F.reshape(-1), lo, hi, gn, data, 2 * sigma, cap=10))
+    assert len(few) == len(ref)
+    # eps below the node-to-data distance everywhere: empty mask, no points
+    assert len(R.zero_set(ctx, F.reshape(-1), lo, hi, gn, data, 1e-9)) == 0
