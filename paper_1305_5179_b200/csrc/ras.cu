@@ -335,7 +335,7 @@ constexpr int kGjMax = 224;
 constexpr int kGjThreads = 512;
 
 template <int RM, int RC>
-__global__ void __launch_bounds__(kGjThreads, 1)
+__global__ void __launch_bounds__(kGjThreads, (RM * RC <= 32) ? 2 : 1)
 gj_inverse_f32_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __restrict__ core_ptr,
                       const int32_t* __restrict__ ext_idx, const int64_t* __restrict__ w_off,
                       const float4* __restrict__ sorted, double amp, double two_s2, double c2,
@@ -832,7 +832,8 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
       while (hi < small.size() && h_ext_ptr[small[hi] + 1] - h_ext_ptr[small[hi]] <= caps[bin]) ++hi;
       const int64_t cnt = (int64_t)(hi - lo);
       if (cnt > 0) {
-        const int gblocks = (int)std::min<int64_t>(cnt, (int64_t)ctx->sm_count);
+        // the 128-row variant fits 64 registers: two CTAs (blocks) per SM overlap their barrier latency
+        const int gblocks = (int)std::min<int64_t>(cnt, (int64_t)ctx->sm_count * (bin == 0 ? 2 : 1));
         const int64_t* bl = blist.as<int64_t>() + lo;
 #define RBF_GJ_LAUNCH(RM_, RC_)                                                                            \
   gj_inverse_f32_kernel<RM_, RC_><<<gblocks, kGjThreads, 0, s>>>(                                         \
