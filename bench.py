@@ -139,6 +139,22 @@ def zero_set_quality(R, ctx, d, field, lo, hi, gn):
     return out
 
 
+def density_report(R, ctx, d):
+    """Density measures of the surface points on the GPU (Eq.7-11, rbf_density):
+    q_X, h_max and the sigma heuristics next to the configured sigma."""
+    import torch
+    x = torch.as_tensor(d["x"], dtype=torch.float64, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s = torch.cuda.current_stream()
+    e0.record(s)
+    out = R.density(ctx, x)
+    e1.record(s)
+    torch.cuda.synchronize()
+    out = {k: float(v) for k, v in out.items()}
+    out.update(ms=e0.elapsed_time(e1), sigma_used=d["sigma"], points=int(x.shape[0]))
+    return out
+
+
 def measured_traffic(cfg_name: str):
     """DRAM bytes per launch of the dominant kernel from the committed ncu --set full
     capture (profiles/), or None when there is none for this config."""
@@ -260,9 +276,10 @@ def run_ours(args, rank, world, local):
     # Alg.1 step 3 output (outside the timed step): the eps-masked zero set of the
     # last field (rbf_zero_set, eps = 2 sigma, reading R11) and its distance to
     # the generator's exact surface g = 0 (first-order |g| / |grad g|)
-    zs = None
+    zs = dens = None
     if rank == 0:
         zs = zero_set_quality(R, ctx, d, field, lo, hi, gn)
+        dens = density_report(R, ctx, d)
 
     # roofline of the dominant kernel (fp32 summation), live CUDA-event timing
     t_mv, n_mv = prof["matvec_f32"]
@@ -304,6 +321,7 @@ def run_ours(args, rank, world, local):
                    "iters_phase1": last["iters_phase1"], "iters_phase2": last["iters_phase2"],
                    "rel_residual_true": last["rel_residual_true"], "converged": last["converged"],
                    "ras_blocks": last["nblocks"], "precond_bytes": last["precond_bytes"], "zero_set": zs,
+                   "density": dens,
                    "cells": info,
                    "gen_s": round(d["gen_s"], 1)},
     }

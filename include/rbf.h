@@ -297,6 +297,21 @@ rbf_status rbf_eval_grid(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel*
 rbf_status rbf_zero_set(rbf_ctx* ctx, const float* field, const rbf_grid* grid, const double* data,
                         int64_t ndata, double eps, double* points, int64_t cap, int64_t* count);
 
+/* ---- density measures of the data set (§4, Eq.7-11) --------------
+ * x: DEVICE fp64 n x 3 (for 2-D sets pass z = 0).  Distances in fp64,
+ * ((dx^2 + dy^2) + dz^2) then sqrt of the minimum (bit-identical to the oracle).
+ * rbf_nn_distance: dist[i] (DEVICE fp64) = min_j ||q_i - x_j|| for the m query
+ * points q (DEVICE fp64 m x 3), or, with q = NULL, min_{j != i} ||x_i - x_j||
+ * (n entries; duplicates give 0).  rbf_density: out3 (HOST) = {q_X (Eq.7,
+ * separation distance = half the smallest pairwise distance), h_max (P:614-619,
+ * largest nearest-neighbour distance), h_{X,Omega} (Eq.8, fill distance over
+ * the m sample points omega of Omega; NaN when omega = NULL)}.  Sigma
+ * heuristics: Eq.9 sigma ~ 2 q_X, Eq.10 sigma ~ sqrt(2) h, Eq.11 h ~ sqrt(2)
+ * h_max.  Synchronise.  Errors: RBF_EINVAL (n < 2 for self distances, NULLs,
+ * non-finite data). */
+rbf_status rbf_nn_distance(rbf_ctx* ctx, const double* x, int64_t n, const double* q, int64_t m, double* dist);
+rbf_status rbf_density(rbf_ctx* ctx, const double* x, int64_t n, const double* omega, int64_t m, double* out3);
+
 /* ---- profiling (CUDA events on the context stream) -------------------------
  * When enabled, every launch of the listed device stages is bracketed by a
  * pair of CUDA events recorded on the context's stream.  rbf_profile_query

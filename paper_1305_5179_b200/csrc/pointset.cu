@@ -1,5 +1,7 @@
-// the masked zero set of the interpolant on the grid.
+// Point-set geometry on the GPU: SURVEY.md §8(f) item 1 (the masked zero set
+// of the interpolant on the grid) and item 2 (density measures, Eq.7-11).
 //
+// ---- zero set ----
 // §2.1.3: the surface is the zero level set of P_f restricted to the
 // eps-surrounding of the data, M* ~ M_ext^eps cap S_0 ("undesired artifacts"
 // far from the data are cut away).  Reading R11: linear
@@ -237,5 +239,231 @@ extern "C" rbf_status rbf_zero_set(rbf_ctx* ctx, const float* field, const rbf_g
   }
   RBF_CUDA_TRY(cudaStreamSynchronize(s));
   *count = base;
+  return RBF_OK;
+}
+
+// ---- density measures (§4; Eq.7-11) ---------
+//   q_X        = 1/2 min_{i != j} ||x_i - x_j||            (Eq.7, separation distance)
+//   h_max      = max_j min_{i != j} ||x_i - x_j||
+//   h_{X,Omega}= max_{w in Omega} min_j ||w - x_j||         (Eq.8, fill distance over
+//                a caller-supplied discrete sample of Omega)
+// Nearest-neighbour distances by an expanding-ring search over a uniform cell
+// grid of the data (edge ~ (bbox volume / (n/2))^(1/3)): after the rings up to
+// Chebyshev distance R from the query's (unclamped) cell, every unvisited point
+// is at least (R - 1) h away, so the search stops once best <= (R - 1) h.
+// Distances in fp64 with the oracle's rounding ((dx^2 + dy^2) + dz^2, sqrt of the
+// minimum), so every distance equals oracle/density.py's bit for bit.
+namespace rbf {
+namespace {
+
+__global__ void bbox64_kernel(const double* __restrict__ X, int64_t n, double* __restrict__ part) {
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double v = X[3 * i + a];
+      if (!isfinite(v)) bad = true;
+      mn[a] = fmin(mn[a], v);
+      mx[a] = fmax(mx[a], v);
+    }
+  __shared__ double smn[3][256], smx[3][256];
+  __shared__ int sbad;
+  if (threadIdx.x == 0) sbad = 0;
+  __syncthreads();
+  if (bad) sbad = 1;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) { smn[a][threadIdx.x] = mn[a]; smx[a][threadIdx.x] = mx[a]; }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    const int a = threadIdx.x;
+    double lo = INFINITY, hi = -INFINITY;
+    for (int t = 0; t < (int)blockDim.x; ++t) { lo = fmin(lo, smn[a][t]); hi = fmax(hi, smx[a][t]); }
+    part[7 * blockIdx.x + a] = lo;
+    part[7 * blockIdx.x + 3 + a] = hi;
+  }
+  if (threadIdx.x == 0) part[7 * blockIdx.x + 6] = sbad ? 1.0 : 0.0;
+}
+
+// nn[i] = min over data points j (j != self index when exclude) of ||q_i - x_j||
+__global__ void nn_kernel(const double* __restrict__ Qp, int64_t m, bool exclude_self, DCells dc,
+                          const int32_t* __restrict__ start, const double* __restrict__ S,
+                          const int32_t* __restrict__ sorted_id, double h, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const double q[3] = {Qp[3 * i], Qp[3 * i + 1], Qp[3 * i + 2]};
+    int c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double t = floor((q[a] - dc.lo[a]) * dc.inv_h);
+      c[a] = (int)fmin(fmax(t, -1e9), 1e9);
+    }
+    // rings [r_lo, r_hi] intersect the grid (r_lo > 0 for queries outside it)
+    int r_lo = 0, r_hi = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      r_lo = max(r_lo, max(-c[a], c[a] - (dc.dim[a] - 1)));
+      r_hi = max(r_hi, max(c[a], dc.dim[a] - 1 - c[a]));
+    }
+    double best = INFINITY;
+    for (int r = r_lo; r <= r_hi; ++r) {
+      const int z0 = max(c[2] - r, 0), z1 = min(c[2] + r, dc.dim[2] - 1);
+      const int y0 = max(c[1] - r, 0), y1 = min(c[1] + r, dc.dim[1] - 1);
+      const int x0 = max(c[0] - r, 0), x1 = min(c[0] + r, dc.dim[0] - 1);
+      for (int cz = z0; cz <= z1; ++cz) {
+        for (int cy = y0; cy <= y1; ++cy) {
+          // cells of the shell max(|dx|, |dy|, |dz|) == r: a whole x row when
+          // (cy, cz) is on the shell, else only x = c0 -+ r
+          const bool face = (cz == c[2] - r || cz == c[2] + r || cy == c[1] - r || cy == c[1] + r);
+          for (int e = 0; e < (face ? x1 - x0 + 1 : 2); ++e) {
+            const int cx = face ? x0 + e : (e == 0 ? c[0] - r : c[0] + r);
+            if (cx < 0 || cx >= dc.dim[0] || (!face && r == 0)) continue;
+            const int64_t k = cx + (int64_t)dc.dim[0] * (cy + (int64_t)dc.dim[1] * cz);
+            for (int p = start[k]; p < start[k + 1]; ++p) {
+              if (exclude_self && sorted_id[p] == (int32_t)i) continue;
+              const double dx = __dsub_rn(q[0], S[3 * p]), dy = __dsub_rn(q[1], S[3 * p + 1]),
+                           dz = __dsub_rn(q[2], S[3 * p + 2]);
+              const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+              best = fmin(best, d2);
+            }
+          }
+        }
+      }
+      const double bound = (double)r * h;   // unvisited points are >= r h away after ring r
+      if (best <= bound * bound) break;
+    }
+    out[i] = __dsqrt_rn(best);
+  }
+}
+
+__global__ void minmax_kernel(const double* __restrict__ v, int64_t n, double* __restrict__ part) {
+  double lo = INFINITY, hi = -INFINITY;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    lo = fmin(lo, v[i]);
+    hi = fmax(hi, v[i]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  __shared__ double sl[32], sh[32];
+  if ((threadIdx.x & 31) == 0) { sl[threadIdx.x >> 5] = lo; sh[threadIdx.x >> 5] = hi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { lo = fmin(lo, sl[w]); hi = fmax(hi, sh[w]); }
+    lo = fmin(lo, sl[0]);
+    hi = fmax(hi, sh[0]);
+    part[2 * blockIdx.x] = lo;
+    part[2 * blockIdx.x + 1] = hi;
+  }
+}
+
+rbf_status host_minmax(rbf_ctx* ctx, const double* v, int64_t n, double* lo, double* hi) {
+  cudaStream_t s = ctx->stream;
+  const int nb = grid_for(n, 256, 1024);
+  DevBuf part;
+  RBF_TRY(part.alloc(16 * (size_t)nb, s));
+  minmax_kernel<<<nb, 256, 0, s>>>(v, n, part.as<double>());
+  RBF_CHECK_LAUNCH();
+  std::vector<double> hp(2 * (size_t)nb);
+  RBF_CUDA_TRY(cudaMemcpyAsync(hp.data(), part.p, 16 * (size_t)nb, cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  *lo = INFINITY;
+  *hi = -INFINITY;
+  for (int b = 0; b < nb; ++b) { *lo = std::min(*lo, hp[2 * b]); *hi = std::max(*hi, hp[2 * b + 1]); }
+  return RBF_OK;
+}
+
+}  // namespace
+
+// nearest-neighbour distances of Q (or of X itself, self excluded) to X
+rbf_status nn_distances(rbf_ctx* ctx, const double* X, int64_t n, const double* Q, int64_t m, double* out) {
+  cudaStream_t s = ctx->stream;
+  const int nbb = grid_for(n, 256, 1024);
+  DevBuf part;
+  RBF_TRY(part.alloc(sizeof(double) * 7 * nbb, s));
+  bbox64_kernel<<<nbb, 256, 0, s>>>(X, n, part.as<double>());
+  RBF_CHECK_LAUNCH();
+  std::vector<double> hp(7 * (size_t)nbb);
+  RBF_CUDA_TRY(cudaMemcpyAsync(hp.data(), part.p, sizeof(double) * 7 * nbb, cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int b = 0; b < nbb; ++b) {
+    if (hp[7 * b + 6] != 0.0) { set_error("non-finite data point"); return RBF_EINVAL; }
+    for (int a = 0; a < 3; ++a) { mn[a] = std::min(mn[a], hp[7 * b + a]); mx[a] = std::max(mx[a], hp[7 * b + 3 + a]); }
+  }
+  // cell edge: ~2 points per cell of the bounding box (degenerate extents floored)
+  double ext = 0.0;
+  for (int a = 0; a < 3; ++a) ext = std::max(ext, mx[a] - mn[a]);
+  if (!(ext > 0)) ext = 1.0;
+  double vol = 1.0;
+  for (int a = 0; a < 3; ++a) vol *= std::max(mx[a] - mn[a], ext * 1e-3);
+  double h = std::cbrt(vol / std::max<double>(1.0, 0.5 * (double)n));
+  DCells dc;
+  int64_t ncell = 1;
+  for (;;) {
+    double prod = 1.0;
+    for (int a = 0; a < 3; ++a) prod *= std::floor((mx[a] - (mn[a] - 0.5 * h)) / h) + 1.0;
+    if (prod <= (double)((int64_t)1 << 27)) break;
+    h *= 1.5;
+  }
+  for (int a = 0; a < 3; ++a) {
+    dc.lo[a] = mn[a] - 0.5 * h;
+    dc.dim[a] = (int)std::floor((mx[a] - dc.lo[a]) / h) + 1;
+    ncell *= dc.dim[a];
+  }
+  dc.inv_h = 1.0 / h;
+  DevBuf k1, v1, k2, v2, start, S;
+  RBF_TRY(k1.alloc(4 * n, s));
+  RBF_TRY(v1.alloc(4 * n, s));
+  RBF_TRY(k2.alloc(4 * n, s));
+  RBF_TRY(v2.alloc(4 * n, s));
+  data_keys_kernel<<<grid_for(n, 256), 256, 0, s>>>(X, n, dc, k1.as<uint32_t>(), v1.as<int32_t>());
+  RBF_CHECK_LAUNCH();
+  int bits = 1;
+  while (bits < 32 && ((int64_t)1 << bits) < ncell) ++bits;
+  RBF_TRY(radix_sort_pairs<uint32_t>(ctx, k1.as<uint32_t>(), v1.as<int32_t>(), k2.as<uint32_t>(), v2.as<int32_t>(), n,
+                                     bits));
+  RBF_TRY(start.alloc(4 * (ncell + 1), s));
+  data_start_kernel<<<grid_for(n + 1, 256), 256, 0, s>>>(k2.as<uint32_t>(), n, ncell, start.as<int32_t>());
+  RBF_CHECK_LAUNCH();
+  RBF_TRY(S.alloc(sizeof(double) * 3 * n, s));
+  data_gather_kernel<<<grid_for(n, 256), 256, 0, s>>>(X, v2.as<int32_t>(), n, S.as<double>());
+  RBF_CHECK_LAUNCH();
+  const bool self = (Q == nullptr);
+  nn_kernel<<<grid_for(self ? n : m, 128, 148 * 64), 128, 0, s>>>(self ? X : Q, self ? n : m, self, dc,
+                                                                  start.as<int32_t>(), S.as<double>(),
+                                                                  v2.as<int32_t>(), h, out);
+  RBF_CHECK_LAUNCH();
+  return RBF_OK;
+}
+
+}  // namespace rbf
+
+extern "C" rbf_status rbf_nn_distance(rbf_ctx* ctx, const double* x, int64_t n, const double* q, int64_t m,
+                                      double* dist) {
+  if (!ctx || !x || !dist || n < 1 || (q && m < 1)) { set_error("bad arguments"); return RBF_EINVAL; }
+  if (!q && n < 2) { set_error("self distances need n >= 2"); return RBF_EINVAL; }
+  RBF_CUDA_TRY(cudaSetDevice(ctx->device));
+  return nn_distances(ctx, x, n, q, m, dist);
+}
+
+extern "C" rbf_status rbf_density(rbf_ctx* ctx, const double* x, int64_t n, const double* omega, int64_t m,
+                                  double* out3) {
+  if (!ctx || !x || !out3 || n < 2 || (omega && m < 1)) { set_error("bad arguments"); return RBF_EINVAL; }
+  RBF_CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  DevBuf d;
+  RBF_TRY(d.alloc(sizeof(double) * (size_t)std::max<int64_t>(n, omega ? m : 0), s));
+  RBF_TRY(nn_distances(ctx, x, n, nullptr, 0, d.as<double>()));
+  double lo, hi;
+  RBF_TRY(host_minmax(ctx, d.as<double>(), n, &lo, &hi));
+  out3[0] = 0.5 * lo;   // q_X (Eq.7)
+  out3[1] = hi;         // h_max
+  out3[2] = NAN;
+  if (omega) {
+    RBF_TRY(nn_distances(ctx, x, n, omega, m, d.as<double>()));
+    RBF_TRY(host_minmax(ctx, d.as<double>(), m, &lo, &hi));
+    out3[2] = hi;       // h_{X,Omega} (Eq.8)
+  }
   return RBF_OK;
 }

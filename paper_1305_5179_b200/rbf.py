@@ -106,6 +106,8 @@ EXPORTS = {
                                       C.POINTER(C.c_int64)]),
     "rbf_zero_set": (C.c_int, [_P, _P, C.POINTER(_Grid), _P, C.c_int64, C.c_double, _P, C.c_int64,
                                C.POINTER(C.c_int64)]),
+    "rbf_nn_distance": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, _P]),
+    "rbf_density": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, _P]),
     "rbf_profile_enable": (C.c_int, [_P, C.c_int]),
     "rbf_profile_query": (C.c_int, [_P, _P, _P]),
     "rbf_reconstruct_host": (C.c_int, [_P, _P, _P, C.c_int64, C.POINTER(_Kernel), C.POINTER(_CellCfg),
@@ -390,6 +392,33 @@ def zero_set(ctx: Context, field: torch.Tensor, lo, hi, n, data: torch.Tensor, e
             return pts[:cnt.value]
         cap = cnt.value
     return pts[:cnt.value]
+
+
+def nn_distance(ctx: Context, x: torch.Tensor, q: torch.Tensor | None = None):
+    """rbf_nn_distance: nearest-data distances of q (or of x itself, self excluded)."""
+    _need(x, torch.float64, x.shape[0] * 3, "x")
+    m = x.shape[0] if q is None else q.shape[0]
+    if q is not None:
+        _need(q, torch.float64, m * 3, "q")
+    out = torch.empty(m, dtype=torch.float64, device=x.device)
+    _check(_lib.rbf_nn_distance(ctx._h, _ptr(x), x.shape[0], None if q is None else _ptr(q), m, _ptr(out)))
+    return out
+
+
+def density(ctx: Context, x: torch.Tensor, omega: torch.Tensor | None = None) -> dict:
+    """rbf_density: q_X (Eq.7), h_max, h_{X,Omega} (Eq.8) and the sigma heuristics (Eq.9-11)."""
+    import math
+    _need(x, torch.float64, x.shape[0] * 3, "x")
+    if omega is not None:
+        _need(omega, torch.float64, omega.shape[0] * 3, "omega")
+    out = (C.c_double * 3)()
+    _check(_lib.rbf_density(ctx._h, _ptr(x), x.shape[0], None if omega is None else _ptr(omega),
+                            0 if omega is None else omega.shape[0], out))
+    q, hm, h = out[0], out[1], out[2]
+    res = dict(q=q, h_max=hm, sigma_q=2.0 * q, sigma_hmax=hm * math.sqrt(2.0) * math.sqrt(2.0))
+    if omega is not None:
+        res.update(h=h, sigma_h=h * math.sqrt(2.0))
+    return res
 
 
 class Precond:
