@@ -370,7 +370,8 @@ def run_reference(args, rank, world, local):
     v = float(np.median(vals))
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "pairs/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(times)) * 1e3,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "higher_is_better": True, "scaling": "strong" if world > 1 and args.parallel == "slab" else "weak",
+           "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "config": {"workload": f"{args.config}: N={cfg.n} ({3 * cfg.n} centres) "
                                                       f"sampled-row brute-force matvec"},
            "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": os.cpu_count(), "kind": "oracle",
