@@ -135,6 +135,7 @@ typedef struct {
 typedef struct rbf_ctx rbf_ctx;
 typedef struct rbf_cells rbf_cells;
 typedef struct rbf_precond rbf_precond;
+typedef struct rbf_csr rbf_csr;
 
 /* Description of a built cell list (host struct, filled by rbf_cells_info). */
 typedef struct {
@@ -281,6 +282,22 @@ rbf_status rbf_gmres_solve(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kerne
  * (the other layers are 0 on each rank), so every rank returns the full field. */
 rbf_status rbf_eval_grid(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern,
                          const double* w, const rbf_grid* grid, float* field);
+
+/* ---- the ASSEMBLED operator, for comparison ---------
+ * The paper's GPU path assembles A (Alg.2 "truncation area") and
+ * multiplies it as a sparse matrix (PETSc AIJCUSP).  rbf_assemble
+ * builds that CSR on the device (library-owned; single GPU): rows = targets and
+ * columns = sources in the cell (sorted) order, entries for fp32 r^2 <= fp32(c^2)
+ * from the fp32 centres with value a * 2^(-k r^2) (the fp32 tier's arithmetic),
+ * fp32 values + int32 columns (8 B per entry) + int64 row pointers.  Needs
+ * 8 * nnz bytes of device memory (c4: 1.02e10 entries = 82 GB): RBF_ENOMEM if it
+ * does not fit.  Synchronises.  rbf_csr_spmv: f = A w with w, f DEVICE fp32 in
+ * the caller's order (same conventions as rbf_matvec(RBF_F32)).
+ * rbf_csr_info: nnz, device bytes, assembly seconds (HOST outputs, any NULL). */
+rbf_status rbf_assemble(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern, rbf_csr** out);
+void rbf_csr_free(rbf_csr* m);
+rbf_status rbf_csr_info(const rbf_csr* m, int64_t* nnz, int64_t* bytes, double* t_assemble);
+rbf_status rbf_csr_spmv(rbf_ctx* ctx, const rbf_csr* m, const float* w, float* f);
 
 /* ---- masked zero set of the interpolant (§2.1.3) ----------------
  * The surface is the zero level set of P_f restricted to the eps-surrounding

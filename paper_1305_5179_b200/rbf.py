@@ -106,6 +106,10 @@ EXPORTS = {
                                       C.POINTER(C.c_int64)]),
     "rbf_zero_set": (C.c_int, [_P, _P, C.POINTER(_Grid), _P, C.c_int64, C.c_double, _P, C.c_int64,
                                C.POINTER(C.c_int64)]),
+    "rbf_assemble": (C.c_int, [_P, _P, C.POINTER(_Kernel), C.POINTER(_P)]),
+    "rbf_csr_free": (None, [_P]),
+    "rbf_csr_info": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_double)]),
+    "rbf_csr_spmv": (C.c_int, [_P, _P, _P, _P]),
     "rbf_nn_distance": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, _P]),
     "rbf_density": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, _P]),
     "rbf_profile_enable": (C.c_int, [_P, C.c_int]),
@@ -419,6 +423,39 @@ def density(ctx: Context, x: torch.Tensor, omega: torch.Tensor | None = None) ->
     if omega is not None:
         res.update(h=h, sigma_h=h * math.sqrt(2.0))
     return res
+
+
+class AssembledOperator:
+    """rbf_assemble: the CSR form of A (the paper's assembled GPU path, Alg.2), for
+    comparison with the matrix-free summation."""
+
+    def __init__(self, ctx: Context, cells: Cells, kernel: Kernel):
+        self.ctx, self.cells = ctx, cells
+        h = C.c_void_p()
+        _check(_lib.rbf_assemble(ctx._h, cells._h, C.byref(kernel._c()), C.byref(h)))
+        self._h = h
+
+    def info(self) -> dict:
+        nnz, nbytes, t = C.c_int64(), C.c_int64(), C.c_double()
+        _check(_lib.rbf_csr_info(self._h, C.byref(nnz), C.byref(nbytes), C.byref(t)))
+        return dict(nnz=nnz.value, bytes=nbytes.value, t_assemble=t.value)
+
+    def spmv(self, w: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        _need(w, torch.float32, self.cells.n, "w")
+        f = torch.empty_like(w) if out is None else out
+        _check(_lib.rbf_csr_spmv(self.ctx._h, self._h, _ptr(w), _ptr(f)))
+        return f
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.rbf_csr_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Precond:
