@@ -30,35 +30,35 @@ namespace {
 constexpr int kVecThreads = 256;
 constexpr int kDotChunk = 8;
 
-// partial[j * nblk + blk] = sum over this block's slice of V_j . w, j in [0, k)
+// partial[j * nblk + blk] = sum over this block's slice of V_j . w, j in [0, k);
+// blockIdx.y selects the chunk of kDotChunk basis vectors (chunks run in parallel)
 __global__ void __launch_bounds__(kVecThreads)
 multi_dot_kernel(const double* __restrict__ V, int64_t ldv, int k, const double* __restrict__ w, int64_t n,
                  double* __restrict__ partial) {
   __shared__ double red[kVecThreads / 32][kDotChunk];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int j0 = 0; j0 < k; j0 += kDotChunk) {
-    double acc[kDotChunk];
+  const int j0 = blockIdx.y * kDotChunk;
+  const int nblk = gridDim.x;
+  double acc[kDotChunk];
 #pragma unroll
-    for (int q = 0; q < kDotChunk; ++q) acc[q] = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-      const double wi = w[i];
+  for (int q = 0; q < kDotChunk; ++q) acc[q] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)nblk * blockDim.x) {
+    const double wi = w[i];
 #pragma unroll
-      for (int q = 0; q < kDotChunk; ++q)
-        if (j0 + q < k) acc[q] = fma(V[(int64_t)(j0 + q) * ldv + i], wi, acc[q]);
-    }
+    for (int q = 0; q < kDotChunk; ++q)
+      if (j0 + q < k) acc[q] = fma(V[(int64_t)(j0 + q) * ldv + i], wi, acc[q]);
+  }
 #pragma unroll
-    for (int q = 0; q < kDotChunk; ++q) {
+  for (int q = 0; q < kDotChunk; ++q) {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
-      if (lane == 0) red[wid][q] = acc[q];
-    }
-    __syncthreads();
-    if (threadIdx.x < kDotChunk && j0 + (int)threadIdx.x < k) {
-      double s = 0.0;
-      for (int q = 0; q < kVecThreads / 32; ++q) s += red[q][threadIdx.x];
-      partial[(int64_t)(j0 + threadIdx.x) * gridDim.x + blockIdx.x] = s;
-    }
-    __syncthreads();
+    for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+    if (lane == 0) red[wid][q] = acc[q];
+  }
+  __syncthreads();
+  if (threadIdx.x < kDotChunk && j0 + (int)threadIdx.x < k) {
+    double s = 0.0;
+    for (int q = 0; q < kVecThreads / 32; ++q) s += red[q][threadIdx.x];
+    partial[(int64_t)(j0 + threadIdx.x) * nblk + blockIdx.x] = s;
   }
 }
 
@@ -134,7 +134,7 @@ struct Solver {
     RBF_TRY(w.alloc(sizeof(double) * n, s));
     RBF_TRY(f.alloc(sizeof(double) * n, s));
     RBF_TRY(b.alloc(sizeof(double) * n, s));
-    nblk = ctx->sm_count * 8;   // 64 warps per SM in flight for the HBM-bound multi-dot
+    nblk = ctx->sm_count * 4;   // x chunks of 8 basis vectors (grid.y): enough warps in flight
     RBF_TRY(partial.alloc(sizeof(double) * (size_t)nblk * (m + 2), s));
     RBF_TRY(dots.alloc(sizeof(double) * 4 * (m + 2), s));
     return RBF_OK;
@@ -150,7 +150,8 @@ struct Solver {
   // dots[0..k) = V_{0..k}^T w ; neg copy at dots[(m+2)...]
   rbf_status mdot(const double* Vb, int k, const double* vec, double* out, double* neg) {
     cudaStream_t s = ctx->stream;
-    multi_dot_kernel<<<nblk, kVecThreads, 0, s>>>(Vb, n, k, vec, n, partial.as<double>());
+    const dim3 grid((unsigned)nblk, (unsigned)((k + kDotChunk - 1) / kDotChunk));
+    multi_dot_kernel<<<grid, kVecThreads, 0, s>>>(Vb, n, k, vec, n, partial.as<double>());
     RBF_CHECK_LAUNCH();
     if (ctx->world == 1) {
       reduce_partials<<<k, 32, 0, s>>>(partial.as<double>(), k, nblk, out, neg != nullptr, neg);
