@@ -25,6 +25,7 @@
 //  * fp64 tier: same traversal; |x_i-x_j|^2 in fp64 with the oracle's
 //    rounding order ((dx^2 + dy^2) + dz^2), fp64 exp, fp64 weights.
 #include <cmath>
+#include <cstdlib>
 #include <algorithm>
 
 #include "internal.h"
@@ -155,7 +156,7 @@ __device__ __forceinline__ void traverse(const SumGeom& G, const int32_t* __rest
 template <class Load, class FlushB, class FlushI>
 __device__ __forceinline__ void traverse2(const SumGeom& G, const int32_t* __restrict__ cell_start,
                                           float3 blo, float3 bhi, int lane, Load&& load, FlushB&& flushB,
-                                          FlushI&& flushI, int& nB, int& nI) {
+                                          FlushI&& flushI, int& nB, int& nI, int skip_lo = 0, int skip_hi = 0) {
   const CellGrid& g = G.g;
   const float cc = G.cc, cc2 = G.cc2, h = g.h;
   const int z0 = cellof(blo.z - cc, g.lo[2], g.inv_h, g.dim[2]);
@@ -175,8 +176,11 @@ __device__ __forceinline__ void traverse2(const SumGeom& G, const int32_t* __res
       const int x0 = cellof(blo.x - rx, g.lo[0], g.inv_h, g.dim[0]);
       const int x1 = cellof(bhi.x + rx, g.lo[0], g.inv_h, g.dim[0]);
       const int64_t rowbase = ((int64_t)cz * g.dim[1] + cy) * g.dim[0];
-      const int sb = __ldg(cell_start + rowbase + x0);
+      int sb = __ldg(cell_start + rowbase + x0);
       const int se = __ldg(cell_start + rowbase + x1 + 1);
+      // symmetric matvec: sources in [skip_lo, skip_hi) are never loaded (a cell
+      // row lies in one z plane, so it never straddles skip_lo, a plane boundary)
+      if (sb >= skip_lo && sb < skip_hi) sb = min(se, skip_hi);
       for (int j0 = sb; j0 < se; j0 += 32) {
         const int j = j0 + lane;
         const int kind = load.classify(j, j < se);
@@ -210,24 +214,32 @@ __device__ __forceinline__ void traverse2(const SumGeom& G, const int32_t* __res
 struct Ring32 {
   float* bx; float* by; float* bz; float* bw;
   float* bs = nullptr;   // |s'|^2 (expansion path only)
+  int* bi = nullptr;     // sorted source index (symmetric ring only)
 };
 
 // Dual-ring staging of the fp32 fast path (see traverse2).  SPLIT = false: no
 // interior/boundary classification, every kept source goes to the unmasked ring.
-template <bool SPLIT>
+template <bool SPLIT, bool SYM = false>
 struct Stage32x2 {
   Ring32 rb, ri;
   const float4* __restrict__ src;
   float3 blo, bhi, ctr;
   float cc2, ci2, s;
   float4 p;
+  int jj = 0;
+  // SYM: sources in [skip_lo, skip_hi) are skipped (their tiles evaluate the
+  // pair), sources in [sym_lo, sym_hi) go to the symmetric ring rb
+  int skip_lo = 0, skip_hi = 0, sym_lo = 0, sym_hi = 0;
   __device__ __forceinline__ int classify(int j, bool valid) {
     p = valid ? __ldg(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    jj = j;
+    if (SYM && j >= skip_lo && j < skip_hi) return 0;
     const float ax = blo.x - p.x, bx = p.x - bhi.x;
     const float ay = blo.y - p.y, by = p.y - bhi.y;
     const float az = blo.z - p.z, bz = p.z - bhi.z;
     const float gx = fmaxf(0.f, fmaxf(ax, bx)), gy = fmaxf(0.f, fmaxf(ay, by)), gz = fmaxf(0.f, fmaxf(az, bz));
     if (!valid || gx * gx + gy * gy + gz * gz > cc2) return 0;
+    if (SYM) return (j >= sym_lo && j < sym_hi) ? 1 : 2;
     if (!SPLIT) return 2;
     // farthest point of the box
     const float fx = fmaxf(fabsf(ax), fabsf(bx)), fy = fmaxf(fabsf(ay), fabsf(by)), fz = fmaxf(fabsf(az), fabsf(bz));
@@ -244,12 +256,14 @@ struct Stage32x2 {
     r.bz[pos] = sz;
     r.bs[pos] = fmaf(sz, sz, fmaf(sy, sy, sx * sx));
     r.bw[pos] = p.w;
+    if (SYM && kind == 1) r.bi[pos] = jj;
   }
   __device__ __forceinline__ void shift_ring(Ring32& r, int rest, int lane) {
     if (lane < rest) {
       float a = r.bx[kFlush + lane], b = r.by[kFlush + lane], c = r.bz[kFlush + lane], d = r.bw[kFlush + lane];
       float e = r.bs[kFlush + lane];
       r.bx[lane] = a; r.by[lane] = b; r.bz[lane] = c; r.bw[lane] = d; r.bs[lane] = e;
+      if (SYM && r.bi) r.bi[lane] = r.bi[kFlush + lane];
     }
   }
 };
@@ -287,6 +301,67 @@ struct Flush32e {
         float2 eb = make_float2(ex2(-cut(rb.x, th)), ex2(-cut(rb.y, th)));
         acc[t] = fma2(ea, make_float2(W.x, W.y), acc[t]);
         acc[t] = fma2(eb, make_float2(W.z, W.w), acc[t]);
+      }
+    }
+  }
+};
+
+// Symmetric inner loop (A = A^T): every exponential of a staged source j
+// (sorted index beyond this tile, same rank) serves both f_i += a e_ij w_j
+// (this lane's targets, as Flush32e) and f_j += a e_ij w_i.  The source side
+// sums e'_ij (w_i 2^-|t'_i|^2) over the warp's targets per source -- a
+// transpose-reduction of 4 sources at a time (6 shuffles: two halving steps,
+// then three summing steps) -- and one lane per source adds it to f_j
+// (atomicAdd: the sum over tiles is order-dependent in the last bits).
+template <int T, class OutT>
+struct Flush32s {
+  Ring32 r;
+  float2* acc;                                         // [T] target side
+  const float* mx; const float* my; const float* mz;   // [T] -2 t'
+  const float* wt;                                     // [T] w_i 2^-|t'_i|^2 (0 for empty slots)
+  OutT* out;
+  const int32_t* out_perm;
+  float amp;
+  int lane;
+  __device__ __forceinline__ void operator()(int cnt) {
+    const bool h4 = lane & 16, h3 = lane & 8;
+    const int mys = (h4 ? 2 : 0) + (h3 ? 1 : 0);
+#pragma unroll 2
+    for (int j = 0; j < cnt; j += 4) {
+      const float4 X = *reinterpret_cast<const float4*>(r.bx + j);
+      const float4 Y = *reinterpret_cast<const float4*>(r.by + j);
+      const float4 Z = *reinterpret_cast<const float4*>(r.bz + j);
+      const float4 S = *reinterpret_cast<const float4*>(r.bs + j);
+      const float4 W = *reinterpret_cast<const float4*>(r.bw + j);
+      float2 pa = make_float2(0.f, 0.f), pb = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const float2 ax = make_float2(mx[t], mx[t]), ay = make_float2(my[t], my[t]), az = make_float2(mz[t], mz[t]);
+        float2 ra = fma2(make_float2(Z.x, Z.y), az, make_float2(S.x, S.y));
+        float2 rb = fma2(make_float2(Z.z, Z.w), az, make_float2(S.z, S.w));
+        ra = fma2(make_float2(Y.x, Y.y), ay, ra); rb = fma2(make_float2(Y.z, Y.w), ay, rb);
+        ra = fma2(make_float2(X.x, X.y), ax, ra); rb = fma2(make_float2(X.z, X.w), ax, rb);
+        const float2 ea = make_float2(ex2(-ra.x), ex2(-ra.y));
+        const float2 eb = make_float2(ex2(-rb.x), ex2(-rb.y));
+        acc[t] = fma2(ea, make_float2(W.x, W.y), acc[t]);
+        acc[t] = fma2(eb, make_float2(W.z, W.w), acc[t]);
+        const float2 wv = make_float2(wt[t], wt[t]);
+        pa = fma2(ea, wv, pa);
+        pb = fma2(eb, wv, pb);
+      }
+      // transpose-reduce (pa.x, pa.y, pb.x, pb.y) = sources j .. j+3 over the warp
+      float k0 = h4 ? pb.x : pa.x, k1 = h4 ? pb.y : pa.y;
+      const float s0 = h4 ? pa.x : pb.x, s1 = h4 ? pa.y : pb.y;
+      k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+      k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+      float k = h3 ? k1 : k0;
+      k += __shfl_xor_sync(0xffffffffu, h3 ? k0 : k1, 8);
+      k += __shfl_xor_sync(0xffffffffu, k, 4);
+      k += __shfl_xor_sync(0xffffffffu, k, 2);
+      k += __shfl_xor_sync(0xffffffffu, k, 1);
+      if ((lane & 7) == 0 && j + mys < cnt) {
+        const int src = r.bi[j + mys];
+        atomicAdd(out + (out_perm ? out_perm[src] : src), (OutT)(amp * k));
       }
     }
   }
@@ -399,6 +474,19 @@ __device__ __forceinline__ void pad_ring(Ring32 r, int nbuf, int lane, int& cnt,
   __syncwarp();
 }
 
+// Symmetric ring padding: zero-weight sources at |s'|^2 = 1e30 (2^-1e30 = 0)
+// whose index is a valid target of the tile (the source side adds exactly 0 there).
+__device__ __forceinline__ void pad_ring_sym(Ring32 r, int nbuf, int lane, int& cnt, int valid_idx) {
+  cnt = (nbuf + 3) & ~3;
+  if (lane < cnt - nbuf) {
+    const int q = nbuf + lane;
+    r.bw[q] = 0.f;
+    r.bx[q] = 0.f; r.by[q] = 0.f; r.bz[q] = 0.f; r.bs[q] = 1e30f;
+    r.bi[q] = valid_idx;
+  }
+  __syncwarp();
+}
+
 // Targets: mode 0 = tile of sorted centres, mode 1 = 4x4x4 block of grid nodes.
 struct GridDesc {
   double lo[3], step[3];
@@ -411,15 +499,18 @@ __device__ __forceinline__ float node_coord(const GridDesc& gd, int a, int i) {
 }
 inline float node_coord_host(const GridDesc& gd, int a, int i) { return (float)(gd.lo[a] + (double)i * gd.step[a]); }
 
-template <int MODE, bool STATS, class OutT>
+template <int MODE, bool STATS, class OutT, bool SYM = false>
 __global__ void __launch_bounds__(kSumWarps * 32, 8)
 sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* __restrict__ src,
                const int2* __restrict__ tiles, const float4* __restrict__ tbox, int64_t ntiles, int64_t tile_base,
                GridDesc gd, OutT* __restrict__ out, const int32_t* __restrict__ out_perm,
-               int* __restrict__ work, unsigned long long* __restrict__ stats) {
-  __shared__ __align__(16) float ring[kSumWarps][10][kBufPad];
+               int* __restrict__ work, unsigned long long* __restrict__ stats, int64_t own_lo = 0,
+               int64_t own_hi = 0) {
+  __shared__ __align__(16) float ring[kSumWarps][SYM ? 11 : 10][kBufPad];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  Ring32 R{ring[wib][0], ring[wib][1], ring[wib][2], ring[wib][3], ring[wib][8]};    // boundary sources
+  // boundary sources (grid) / symmetric sources (SYM matvec)
+  Ring32 R{ring[wib][0], ring[wib][1], ring[wib][2], ring[wib][3], ring[wib][8],
+           SYM ? reinterpret_cast<int*>(ring[wib][SYM ? 10 : 0]) : nullptr};
   Ring32 RI{ring[wib][4], ring[wib][5], ring[wib][6], ring[wib][7], ring[wib][9]};   // interior sources
   unsigned long long useful = 0, visited = 0;
   for (;;) {
@@ -502,6 +593,39 @@ sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
       // 2^-(k c^2) = 2^-25.97 term (<= 1/4 ulp of the peak entry; DESIGN.md
       // reading R18).  Grid (MODE 1) keeps the mask: nodes with no centre
       // within the cutoff must be exactly 0 (reading R5).
+      if constexpr (SYM) {
+        // sources of this rank before the tile: skipped (their tile holds the
+        // pair); after it: symmetric; the tile's own and other ranks' sources:
+        // one-sided (reading R19)
+        const int2 tl = tiles[tile];
+        Stage32x2<false, true> st{R, RI, src, blo, bhi, ctr, G.cc2, G.ci2, G.s, make_float4(0, 0, 0, 0)};
+        st.skip_lo = (int)own_lo;
+        st.skip_hi = tl.x;
+        st.sym_lo = tl.x + tl.y;
+        st.sym_hi = (int)own_hi;
+        float wt[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) wt[t] = tv[t] ? src[tidx[t]].w * tf[t] : 0.f;
+        int nB = 0, nI = 0, cnt;
+        if (two) {
+          Flush32s<2, OutT> fs{R, acc, mx, my, mz, wt, out, out_perm, G.amp, lane};
+          Flush32e<2, false> fi{RI, acc, mx, my, mz, th};
+          traverse2(G, cell_start, blo, bhi, lane, st, fs, fi, nB, nI, st.skip_lo, st.skip_hi);
+          pad_ring_sym(R, nB, lane, cnt, tl.x);
+          fs(cnt);
+          pad_ring(RI, nI, lane, cnt, true);
+          fi(cnt);
+        } else {
+          Flush32s<1, OutT> fs{R, acc, mx, my, mz, wt, out, out_perm, G.amp, lane};
+          Flush32e<1, false> fi{RI, acc, mx, my, mz, th};
+          traverse2(G, cell_start, blo, bhi, lane, st, fs, fi, nB, nI, st.skip_lo, st.skip_hi);
+          pad_ring_sym(R, nB, lane, cnt, tl.x);
+          fs(cnt);
+          pad_ring(RI, nI, lane, cnt, true);
+          fi(cnt);
+        }
+        __syncwarp();
+      } else {
       Stage32x2<MODE != 0> st{R, RI, src, blo, bhi, ctr, G.cc2, G.ci2, G.s, make_float4(0, 0, 0, 0)};
       int nB = 0, nI = 0, cnt;
       if (two) {
@@ -522,6 +646,7 @@ sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
         fi(cnt);
       }
       __syncwarp();
+      }
     }
     if (!STATS) {
 #pragma unroll
@@ -530,7 +655,8 @@ sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
         float v = G.amp * ((acc[t].x + acc[t].y) * tf[t]);
         int64_t o = tidx[t];
         if (MODE == 0 && out_perm) o = out_perm[o];
-        out[o] = (OutT)v;
+        if (SYM) atomicAdd(out + o, (OutT)v);
+        else out[o] = (OutT)v;
       }
     }
   }
@@ -690,6 +816,15 @@ SumGeom make_geom(const rbf_cells* c, const KernelParams& kp) {
   return G;
 }
 
+// Symmetric fp32 matvec of the solver (reading R19): opt-in with RBF_SUM_SYM=1
+// (read at every call).  Off by default: its atomics make the product
+// order-dependent in the last bits, and at c4 it gains only 6% (4.63 vs 4.94 ms:
+// the source-side reduction costs as many issue slots as the halved MUFU work saves).
+bool sym_enabled() {
+  const char* e = std::getenv("RBF_SUM_SYM");
+  return e && e[0] == '1';
+}
+
 // Persistent grid: as many CTAs as can be resident (the kernels pull tiles from a
 // work counter, so CTAs beyond one wave would only add tail imbalance).
 template <class K>
@@ -765,6 +900,18 @@ rbf_status matvec_sorted_f32_d(rbf_ctx* ctx, const rbf_cells* c, const KernelPar
   RBF_CUDA_TRY(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
   SumGeom G = make_geom(c, kp);
   GridDesc gd{};
+  if (sym_enabled()) {
+    // symmetric evaluation (reading R19): the output is accumulated
+    RBF_CUDA_TRY(cudaMemsetAsync(f_loc, 0, sizeof(double) * (size_t)c->n_loc(), s));
+    ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
+    sum_f32_kernel<0, false, double, true>
+        <<<sum_blocks(ctx, sum_f32_kernel<0, false, double, true>), kSumWarps * 32, 0, s>>>(
+            G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>() - V.h0, c->tiles.as<int2>(),
+            c->tile_box.as<float4>(), V.t1 - V.t0, V.t0, gd, f_loc - V.o0, nullptr, ctx->counter.as<int>(), nullptr,
+            V.o0, V.o1);
+    RBF_CHECK_LAUNCH();
+    return RBF_OK;
+  }
   ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
   sum_f32_kernel<0, false, double><<<sum_blocks(ctx, sum_f32_kernel<0, false, double>), kSumWarps * 32, 0, s>>>(
       G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>() - V.h0, c->tiles.as<int2>(), c->tile_box.as<float4>(),

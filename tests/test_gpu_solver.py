@@ -338,3 +338,26 @@ def test_zero_set_matches_oracle_and_sphere(R, ctx, c1_solution):
     assert len(few) == len(ref)
     # eps below the node-to-data distance everywhere: empty mask, no points
     assert len(R.zero_set(ctx, F.reshape(-1), lo, hi, gn, data, 1e-9)) == 0
+
+
+def test_symmetric_fp32_tier_opt_in(R, ctx):
+    """Reading R19 (opt-in RBF_SUM_SYM=1): the symmetric fp32 matvec of the solver
+    (each exponential serves f_i and f_j) gives the same fit as the one-sided one
+    to the fp32 tier's accuracy; both residuals certified by the oracle."""
+    import os
+    d, X, b = problem("c2", n=3000)
+    sigma = d["sigma"]
+    kern = R.Kernel(sigma)
+    cells = R.Cells(ctx, dev(X, torch.float32), kern)
+    out = {}
+    for sym in ("0", "1"):
+        os.environ["RBF_SUM_SYM"] = sym
+        try:
+            w, rep = R.gmres_solve(ctx, cells, kern, dev(b, torch.float32), restart=50, rtol=1e-6,
+                                   core_target=512, overlap_sigmas=1.3, max_iters=400)
+        finally:
+            del os.environ["RBF_SUM_SYM"]
+        res = np.linalg.norm(b - OK.matvec(X, host(w), sigma)) / np.linalg.norm(b)
+        out[sym] = (res, rep)
+    assert out["1"][0] <= 1.5e-6 and out["0"][0] <= 1.5e-6, out
+    assert abs(out["1"][1]["iters_phase1"] - out["0"][1]["iters_phase1"]) <= 5, out
