@@ -527,9 +527,38 @@ rbf_status build_cells(rbf_ctx* ctx, const float* xyz, int64_t n, const rbf_kern
         c->sorted.as<float4>(), c->tiles.as<int2>(), ntiles, c->tile_box.as<float4>());
     RBF_CHECK_LAUNCH();
   }
+  // wide plan of the symmetric fp32 matvec: chunks of <= 128 targets of a run of
+  // <= 4 cells (reading R19)
+  DevBuf rcw, row_w, totw;
+  RBF_TRY(rcw.alloc(sizeof(uint32_t) * rows, s));
+  RBF_TRY(row_w.alloc(sizeof(uint32_t) * rows, s));
+  RBF_TRY(totw.alloc(sizeof(uint32_t) * 2, s));
+  // (RBF_WIDE_CAP / RBF_WIDE_SPAN: tuning knobs, defaults 128 / 4)
+  const char* ecap = std::getenv("RBF_WIDE_CAP");
+  const char* espan = std::getenv("RBF_WIDE_SPAN");
+  const int cap_w = ecap ? std::min(128, std::max(32, std::atoi(ecap))) : 128;
+  const int span_w = espan ? std::max(1, std::atoi(espan)) : std::max(span, 4);
+  plan_count<<<grid_for(rows, 128), 128, 0, s>>>(c->cell_start.as<int32_t>(), g, cap_w, span_w, 0,
+                                                 rcw.as<uint32_t>());
+  RBF_CHECK_LAUNCH();
+  RBF_TRY(exclusive_scan_u32(ctx, rcw.as<uint32_t>(), row_w.as<uint32_t>(), rows, totw.as<uint32_t>()));
+  uint32_t ntiles_w = 0;
+  RBF_CUDA_TRY(cudaMemcpyAsync(&ntiles_w, totw.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  c->ntiles_w = ntiles_w;
+  RBF_TRY(c->tiles_w.alloc(sizeof(int2) * (size_t)std::max<uint32_t>(ntiles_w, 1), s));
+  RBF_TRY(c->tile_box_w.alloc(sizeof(float4) * 2 * (size_t)std::max<uint32_t>(ntiles_w, 1), s));
+  plan_emit<<<grid_for(rows, 128), 128, 0, s>>>(c->cell_start.as<int32_t>(), g, cap_w, span_w, 0,
+                                                row_w.as<uint32_t>(), c->tiles_w.as<int2>());
+  RBF_CHECK_LAUNCH();
+  if (ntiles_w > 0) {
+    tile_box_kernel<<<grid_for((int64_t)ntiles_w * 32, 256), 256, 0, s>>>(
+        c->sorted.as<float4>(), c->tiles_w.as<int2>(), ntiles_w, c->tile_box_w.as<float4>());
+    RBF_CHECK_LAUNCH();
+  }
   // this rank's share (dist.cu): everything on one GPU, a slab of z planes otherwise
   c->world = ctx->world;
-  c->view = SlabView{0, n, 0, n, 0, (int64_t)ntiles, 0, c->dim[2]};
+  c->view = SlabView{0, n, 0, n, 0, (int64_t)ntiles, 0, c->dim[2], 0, (int64_t)ntiles_w};
   // RBF_SLAB_EMULATE="r/W" (single GPU, tests only): give these cells rank r's
   // slab of a W-way partition so the slab kernels can be checked on one device
   int erank = 0, eworld = 1;
@@ -542,13 +571,14 @@ rbf_status build_cells(rbf_ctx* ctx, const float* xyz, int64_t n, const rbf_kern
     }
   }
   if (ctx->world > 1 || eworld > 1) {
-    std::vector<uint32_t> hro(rows);
+    std::vector<uint32_t> hro(rows), hrow(rows);
     RBF_CUDA_TRY(cudaMemcpyAsync(hro.data(), ro.p, sizeof(uint32_t) * rows, cudaMemcpyDeviceToHost, s));
+    RBF_CUDA_TRY(cudaMemcpyAsync(hrow.data(), row_w.p, sizeof(uint32_t) * rows, cudaMemcpyDeviceToHost, s));
     RBF_CUDA_TRY(cudaStreamSynchronize(s));
     if (ctx->world > 1) {
-      RBF_TRY(dist_plan_cells(ctx, c, hro, (int64_t)ntiles, ctx->rank, ctx->world));
+      RBF_TRY(dist_plan_cells(ctx, c, hro, (int64_t)ntiles, hrow, (int64_t)ntiles_w, ctx->rank, ctx->world));
     } else {
-      RBF_TRY(dist_plan_cells(ctx, c, hro, (int64_t)ntiles, erank, eworld));
+      RBF_TRY(dist_plan_cells(ctx, c, hro, (int64_t)ntiles, hrow, (int64_t)ntiles_w, erank, eworld));
       c->emulated = true;
     }
   }

@@ -164,7 +164,8 @@ void slab_plan(const int64_t* plane_start, const double* weight, int dimz, int r
 }
 
 rbf_status dist_plan_cells(rbf_ctx* ctx, rbf_cells* c, const std::vector<uint32_t>& row_tile_off,
-                           int64_t ntiles, int rank, int world) {
+                           int64_t ntiles, const std::vector<uint32_t>& row_tile_off_w, int64_t ntiles_w, int rank,
+                           int world) {
   cudaStream_t s = ctx->stream;
   const int dimz = c->dim[2];
   const int64_t plane_cells = (int64_t)c->dim[0] * c->dim[1];
@@ -203,6 +204,12 @@ rbf_status dist_plan_cells(rbf_ctx* ctx, rbf_cells* c, const std::vector<uint32_
   };
   V.t0 = row_tiles(V.p0);
   V.t1 = row_tiles(V.p1);
+  auto row_tiles_w = [&](int plane) -> int64_t {
+    const int64_t row = (int64_t)plane * dimy;
+    return row < (int64_t)row_tile_off_w.size() ? (int64_t)row_tile_off_w[row] : ntiles_w;
+  };
+  V.tw0 = row_tiles_w(V.p0);
+  V.tw1 = row_tiles_w(V.p1);
   return RBF_OK;
 }
 

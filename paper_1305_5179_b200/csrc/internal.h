@@ -130,6 +130,7 @@ struct SlabView {
   int64_t h0 = 0, h1 = 0;
   int64_t t0 = 0, t1 = 0;
   int p0 = 0, p1 = 0;
+  int64_t tw0 = 0, tw1 = 0;   // tiles of the wide plan
 };
 // Every rank's slab (identical on all ranks: computed from the replicated cells).
 struct SlabPlan {
@@ -159,6 +160,9 @@ struct rbf_cells {
   rbf::DevBuf cell_start;    // int32[ncell+1]
   rbf::DevBuf tiles;         // int2[ntiles] (start, count)
   rbf::DevBuf tile_box;      // float4[2*ntiles] (lo.xyz, ctr.x) (hi.xyz, unused)
+  // wide plan (<= 128 targets, 4 per lane) of the symmetric fp32 matvec (reading R19)
+  int64_t ntiles_w = 0;
+  rbf::DevBuf tiles_w, tile_box_w;
   cudaStream_t stream = nullptr;
   rbf::SlabView view;        // this rank's share (whole range on one GPU)
   rbf::SlabPlan plan;        // all ranks' slabs (world > 1)
@@ -208,7 +212,7 @@ rbf_status dist_init(rbf_ctx* ctx, const void* unique_id, int rank, int world);
 void dist_destroy(rbf_ctx* ctx);
 void slab_plan(const int64_t* plane_start, const double* weight, int dimz, int reach, int world, SlabPlan& P);
 rbf_status dist_plan_cells(rbf_ctx* ctx, rbf_cells* c, const std::vector<uint32_t>& row_tile_off, int64_t ntiles,
-                           int rank, int world);
+                           const std::vector<uint32_t>& row_tile_off_w, int64_t ntiles_w, int rank, int world);
 template <class T>
 rbf_status halo_exchange(rbf_ctx* ctx, const rbf_cells* c, const T* x_loc, T* win);
 rbf_status allreduce_sum(rbf_ctx* ctx, double* x, int64_t count);

@@ -669,6 +669,99 @@ sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
   }
 }
 
+#ifndef RBF_SYMW_MINB
+#define RBF_SYMW_MINB 7
+#endif
+// Symmetric fp32 matvec on the WIDE tile plan (reading R19): up to 128 targets
+// per warp (4 per lane), so the per-source transpose-reduction of the source
+// side is shared by 4 targets per lane.  Same conventions as sum_f32_kernel<0>
+// with SYM: out is accumulated (zeroed by the caller), sources of this rank
+// before the tile are never loaded, those after it are evaluated once for both
+// sides, the tile's own and other ranks' sources one-sidedly.
+template <int T, class OutT>
+__device__ __forceinline__ void symw_tile(const SumGeom& G, const int32_t* __restrict__ cell_start,
+                                          const float4* __restrict__ src, float3 blo, float3 bhi, float3 ctr,
+                                          const float* xr, const float* yr, const float* zr, const bool* tv,
+                                          const float* wtg, int2 tl, int64_t own_lo, int64_t own_hi, Ring32 R,
+                                          Ring32 RI, int lane, OutT* __restrict__ out, float* fout) {
+  float mx[T], my[T], mz[T], th[T], tf[T], wt[T];
+  float2 acc[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const float tx = (xr[t] - ctr.x) * G.s, ty = (yr[t] - ctr.y) * G.s, tz = (zr[t] - ctr.z) * G.s;
+    const float T2 = fmaf(tz, tz, fmaf(ty, ty, tx * tx));
+    mx[t] = -2.f * tx; my[t] = -2.f * ty; mz[t] = -2.f * tz;
+    th[t] = G.c2s - T2;
+    tf[t] = ex2(-T2);
+    wt[t] = tv[t] ? wtg[t] * tf[t] : 0.f;
+    acc[t] = make_float2(0.f, 0.f);
+  }
+  Stage32x2<false, true> st{R, RI, src, blo, bhi, ctr, G.cc2, G.ci2, G.s, make_float4(0, 0, 0, 0)};
+  st.skip_lo = (int)own_lo;
+  st.skip_hi = tl.x;
+  st.sym_lo = tl.x + tl.y;
+  st.sym_hi = (int)own_hi;
+  Flush32s<T, OutT> fs{R, acc, mx, my, mz, wt, out, nullptr, G.amp, lane};
+  Flush32e<T, false> fi{RI, acc, mx, my, mz, th};
+  int nB = 0, nI = 0, cnt;
+  traverse2(G, cell_start, blo, bhi, lane, st, fs, fi, nB, nI, st.skip_lo, st.skip_hi);
+  pad_ring_sym(R, nB, lane, cnt, tl.x);
+  fs(cnt);
+  pad_ring(RI, nI, lane, cnt, true);
+  fi(cnt);
+  __syncwarp();
+#pragma unroll
+  for (int t = 0; t < T; ++t) fout[t] = G.amp * ((acc[t].x + acc[t].y) * tf[t]);
+}
+
+template <class OutT>
+__global__ void __launch_bounds__(kSumWarps * 32, RBF_SYMW_MINB)
+sum_f32_symw_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* __restrict__ src,
+                    const int2* __restrict__ tiles, const float4* __restrict__ tbox, int64_t ntiles,
+                    int64_t tile_base, OutT* __restrict__ out, int* __restrict__ work, int64_t own_lo,
+                    int64_t own_hi) {
+  __shared__ __align__(16) float ring[kSumWarps][11][kBufPad];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  Ring32 R{ring[wib][0], ring[wib][1], ring[wib][2], ring[wib][3], ring[wib][8],
+           reinterpret_cast<int*>(ring[wib][10])};
+  Ring32 RI{ring[wib][4], ring[wib][5], ring[wib][6], ring[wib][7], ring[wib][9]};
+  for (;;) {
+    int64_t tile;
+    {
+      int t0 = 0;
+      if (lane == 0) t0 = atomicAdd(work, 1);
+      tile = __shfl_sync(0xffffffffu, t0, 0);
+    }
+    if (tile >= ntiles) break;
+    tile += tile_base;
+    const int2 tl = tiles[tile];
+    const float4 a = tbox[2 * tile], b = tbox[2 * tile + 1];
+    const float3 blo = make_float3(a.x, a.y, a.z), bhi = make_float3(b.x, b.y, b.z);
+    const float3 ctr = make_float3(0.5f * (blo.x + bhi.x), 0.5f * (blo.y + bhi.y), 0.5f * (blo.z + bhi.z));
+    float xr[4], yr[4], zr[4], wg[4], fo[4];
+    bool tv[4];
+    int64_t tidx[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int q = lane + 32 * t;
+      tv[t] = q < tl.y;
+      tidx[t] = tl.x + (tv[t] ? q : 0);
+      const float4 p = src[tidx[t]];
+      xr[t] = p.x; yr[t] = p.y; zr[t] = p.z; wg[t] = p.w;
+    }
+    const int T = (tl.y + 31) >> 5;
+    switch (T) {
+      case 1: symw_tile<1>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, own_lo, own_hi, R, RI, lane, out, fo); break;
+      case 2: symw_tile<2>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, own_lo, own_hi, R, RI, lane, out, fo); break;
+      case 3: symw_tile<3>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, own_lo, own_hi, R, RI, lane, out, fo); break;
+      default: symw_tile<4>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, own_lo, own_hi, R, RI, lane, out, fo); break;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (t < T && tv[t]) atomicAdd(out + tidx[t], (OutT)fo[t]);
+  }
+}
+
 // ------------------------------------------------------------- fp64 tier ---
 struct Ring64 {
   float* bx; float* by; float* bz; double* bw;
@@ -816,13 +909,13 @@ SumGeom make_geom(const rbf_cells* c, const KernelParams& kp) {
   return G;
 }
 
-// Symmetric fp32 matvec of the solver (reading R19): opt-in with RBF_SUM_SYM=1
-// (read at every call).  Off by default: its atomics make the product
-// order-dependent in the last bits, and at c4 it gains only 6% (4.63 vs 4.94 ms:
-// the source-side reduction costs as many issue slots as the halved MUFU work saves).
-bool sym_enabled() {
-  const char* e = std::getenv("RBF_SUM_SYM");
-  return e && e[0] == '1';
+// Solver fp32 tier variant: 0 = one-sided, 1 = symmetric on the 64-target plan,
+// 2 = symmetric on the wide plan (reading R19).  RBF_SUM_SYM overrides; the
+// default is 2 for slices of >= 2^18 centres (c4: 4.94 -> 3.61 ms) and 0 below
+// (small problems have too few tiles to hide the longer wide tiles: c2 0.16 vs 0.21 ms).
+int sym_mode(int64_t n_loc) {
+  if (const char* e = std::getenv("RBF_SUM_SYM")) return e[0] == '1' ? 1 : (e[0] == '2' ? 2 : 0);
+  return n_loc >= ((int64_t)1 << 18) ? 2 : 0;
 }
 
 // Persistent grid: as many CTAs as can be resident (the kernels pull tiles from a
@@ -900,8 +993,19 @@ rbf_status matvec_sorted_f32_d(rbf_ctx* ctx, const rbf_cells* c, const KernelPar
   RBF_CUDA_TRY(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
   SumGeom G = make_geom(c, kp);
   GridDesc gd{};
-  if (sym_enabled()) {
-    // symmetric evaluation (reading R19): the output is accumulated
+  const int sym = sym_mode(c->n_loc());
+  if (sym == 2) {
+    // symmetric evaluation on the wide plan (reading R19): the output is accumulated
+    RBF_CUDA_TRY(cudaMemsetAsync(f_loc, 0, sizeof(double) * (size_t)c->n_loc(), s));
+    ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
+    sum_f32_symw_kernel<double><<<sum_blocks(ctx, sum_f32_symw_kernel<double>), kSumWarps * 32, 0, s>>>(
+        G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>() - V.h0, c->tiles_w.as<int2>(),
+        c->tile_box_w.as<float4>(), V.tw1 - V.tw0, V.tw0, f_loc - V.o0, ctx->counter.as<int>(), V.o0, V.o1);
+    RBF_CHECK_LAUNCH();
+    return RBF_OK;
+  }
+  if (sym == 1) {
+    // symmetric evaluation on the 64-target plan (reading R19): the output is accumulated
     RBF_CUDA_TRY(cudaMemsetAsync(f_loc, 0, sizeof(double) * (size_t)c->n_loc(), s));
     ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
     sum_f32_kernel<0, false, double, true>
