@@ -286,9 +286,15 @@ def run_ours(args, rank, world, local):
     avg_mv_ms = t_mv / max(n_mv, 1)
     achieved = useful_mv / (avg_mv_ms * 1e-3) / 1e12
     peak_max = SMS * MUFU_PER_CLK_PER_SM * SM_MAX_MHZ * 1e6 / 1e12
-    roofline = {"bound": "alu", "kernel": "sum_f32_kernel (MUFU.EX2)", "achieved": achieved, "peak": peak_max,
+    sym = os.environ.get("RBF_SUM_SYM")
+    sym = int(sym) if sym in ("0", "1", "2") else (2 if 3 * cfg.n // max(world if slab else 1, 1) >= (1 << 18) else 0)
+    kname = {0: "sum_f32_kernel (one-sided)", 1: "sum_f32_kernel (symmetric, 64-target tiles)",
+             2: "sum_f32_symw_kernel (symmetric, 128-target tiles)"}[sym]
+    roofline = {"bound": "alu", "kernel": kname + ", MUFU.EX2", "achieved": achieved, "peak": peak_max,
                 "unit": "Tpairs/s", "frac": achieved / peak_max,
-                "peak_basis": "148 SMs x 16 MUFU.EX2/clk x 1965 MHz (max clock); 1 ex2 per useful pair",
+                "peak_basis": "148 SMs x 16 MUFU.EX2/clk x 1965 MHz (max clock; 16.00 ex2/clk/SM measured, "
+                              "profiles/r01/peaks_mufu_ffma2.json); roofline of the one-sided algorithm, 1 ex2 per "
+                              "useful pair (the symmetric kernel spends 1 ex2 per 2 pair contributions, reading R19)",
                 "frac_at_measured_clock": (achieved / (SMS * MUFU_PER_CLK_PER_SM * clk["sm_mhz"] * 1e6 / 1e12)
                                            if clk.get("sm_mhz") else None),
                 "avg_launch_ms": avg_mv_ms, "launches": n_mv, "useful_pairs_per_launch": useful_mv,
