@@ -143,9 +143,9 @@ struct Solver {
   double* Zj(int j) { return Z.as<double>() + (int64_t)j * n; }
 
   rbf_status op(bool fp64, const double* in, double* out) {
-    if (fp64) { ++mv64; return matvec_sorted_f64(ctx, c, kp, in, out, nullptr); }
+    if (fp64) { ++mv64; return matvec_sorted_f64(ctx, c, kp, in, out, nullptr, true); }
     ++mv32;
-    return matvec_sorted_f32_d(ctx, c, kp, in, out);
+    return matvec_sorted_f32_d(ctx, c, kp, in, out, true);
   }
   // dots[0..k) = V_{0..k}^T w ; neg copy at dots[(m+2)...]
   rbf_status mdot(const double* Vb, int k, const double* vec, double* out, double* neg) {

@@ -201,8 +201,10 @@ KernelParams kernel_params(const rbf_kernel* k);
 rbf_status matvec_sorted_f32(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
                              const float* w_sorted, float* f_sorted, const int32_t* out_perm,
                              unsigned long long* pair_stats);
+// solver = true: the GMRES operator (may use the symmetric variant, reading R19);
+// false: the public product (one-sided, deterministic)
 rbf_status matvec_sorted_f64(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
-                             const double* w_sorted, double* f_sorted, const int32_t* out_perm);
+                             const double* w_sorted, double* f_sorted, const int32_t* out_perm, bool solver = false);
 rbf_status eval_grid_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
                             const double* w_sorted, const rbf_grid* g, float* field,
                             unsigned long long* pair_stats = nullptr);

@@ -864,6 +864,135 @@ sum_f64_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
   }
 }
 
+// Symmetric fp64 tier of the solver (reading R19, fp64 variant): two rings
+// (one-sided: the tile's own and other ranks' sources; symmetric: this rank's
+// sources after the tile), sources before the tile never loaded.  Each
+// exponential of the symmetric ring serves f_i (lane accumulator) and f_j (warp
+// butterfly over the lane partials sum_t e_tj w_t, one atomicAdd per source).
+struct Ring64s {
+  float* bx; float* by; float* bz; double* bw; int* bi;
+};
+
+struct Stage64x2 {
+  Ring64s rb, ri;   // symmetric / one-sided
+  const float4* __restrict__ src;
+  const double* __restrict__ w;
+  float3 blo, bhi;
+  float cc2;
+  int skip_lo, skip_hi, sym_lo, sym_hi;
+  float4 p;
+  double wj;
+  int jj;
+  __device__ __forceinline__ int classify(int j, bool valid) {
+    p = valid ? __ldg(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    wj = valid ? __ldg(w + j) : 0.0;
+    jj = j;
+    if (j >= skip_lo && j < skip_hi) return 0;
+    const float gx = fmaxf(0.f, fmaxf(blo.x - p.x, p.x - bhi.x));
+    const float gy = fmaxf(0.f, fmaxf(blo.y - p.y, p.y - bhi.y));
+    const float gz = fmaxf(0.f, fmaxf(blo.z - p.z, p.z - bhi.z));
+    if (!valid || gx * gx + gy * gy + gz * gz > cc2) return 0;
+    return (j >= sym_lo && j < sym_hi) ? 1 : 2;
+  }
+  __device__ __forceinline__ void store2(int kind, int posb, int posi) {
+    if (kind == 0) return;
+    Ring64s& r = (kind == 1) ? rb : ri;
+    const int pos = (kind == 1) ? posb : posi;
+    r.bx[pos] = p.x; r.by[pos] = p.y; r.bz[pos] = p.z; r.bw[pos] = wj;
+    if (kind == 1) r.bi[pos] = jj;
+  }
+  __device__ __forceinline__ void shift_ring(Ring64s& r, int rest, int lane) {
+    if (lane < rest) {
+      float a = r.bx[kFlush + lane], b = r.by[kFlush + lane], c = r.bz[kFlush + lane];
+      double d = r.bw[kFlush + lane];
+      r.bx[lane] = a; r.by[lane] = b; r.bz[lane] = c; r.bw[lane] = d;
+      if (r.bi) r.bi[lane] = r.bi[kFlush + lane];
+    }
+  }
+};
+
+template <bool SYM>
+struct Flush64x {
+  Ring64s r;
+  double* acc;                       // [2]
+  const double* xt; const double* yt; const double* zt;
+  const double* wt;                  // [2] target weights (0 for empty slots), SYM only
+  double c2, nis, amp;
+  double* out;
+  int lane;
+  __device__ __forceinline__ void operator()(int cnt) {
+    for (int j = 0; j < cnt; ++j) {
+      const double sx = (double)r.bx[j], sy = (double)r.by[j], sz = (double)r.bz[j], wj = r.bw[j];
+      double pj = 0.0;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        double dx = __dsub_rn(sx, xt[t]), dy = __dsub_rn(sy, yt[t]), dz = __dsub_rn(sz, zt[t]);
+        double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+        const double e = d2 <= c2 ? exp(__dmul_rn(d2, nis)) : 0.0;
+        acc[t] = __fma_rn(e, wj, acc[t]);
+        if (SYM) pj = __fma_rn(e, wt[t], pj);
+      }
+      if (SYM) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) pj += __shfl_xor_sync(0xffffffffu, pj, o);
+        if (lane == 0) atomicAdd(out + r.bi[j], amp * pj);
+      }
+    }
+  }
+};
+
+__global__ void __launch_bounds__(kSumWarps * 32)
+sum_f64_sym_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* __restrict__ src,
+                   const double* __restrict__ w, const int2* __restrict__ tiles, const float4* __restrict__ tbox,
+                   int64_t ntiles, int64_t tile_base, double* __restrict__ out, int* __restrict__ work,
+                   int64_t own_lo, int64_t own_hi) {
+  __shared__ __align__(16) float ringf[kSumWarps][6][kBufPad];
+  __shared__ __align__(16) double ringd[kSumWarps][2][kBufPad];
+  __shared__ __align__(16) int ringi[kSumWarps][kBufPad];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  Ring64s RB{ringf[wib][0], ringf[wib][1], ringf[wib][2], ringd[wib][0], ringi[wib]};
+  Ring64s RI{ringf[wib][3], ringf[wib][4], ringf[wib][5], ringd[wib][1], nullptr};
+  for (;;) {
+    int64_t tile;
+    {
+      int t0 = 0;
+      if (lane == 0) t0 = atomicAdd(work, 1);
+      tile = __shfl_sync(0xffffffffu, t0, 0);
+    }
+    if (tile >= ntiles) break;
+    tile += tile_base;
+    const int2 tl = tiles[tile];
+    const float4 a = tbox[2 * tile], b = tbox[2 * tile + 1];
+    const float3 blo = make_float3(a.x, a.y, a.z), bhi = make_float3(b.x, b.y, b.z);
+    double xt[2], yt[2], zt[2], wt[2], acc[2] = {0.0, 0.0};
+    bool tv[2];
+    int64_t tidx[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      int q = lane + 32 * t;
+      tv[t] = q < tl.y;
+      tidx[t] = tl.x + (tv[t] ? q : 0);
+      float4 p = src[tidx[t]];
+      xt[t] = p.x; yt[t] = p.y; zt[t] = p.z;
+      wt[t] = tv[t] ? w[tidx[t]] : 0.0;
+    }
+    Stage64x2 st{RB, RI, src, w, blo, bhi, G.cc2, (int)own_lo, tl.x, tl.x + tl.y, (int)own_hi,
+                 make_float4(0, 0, 0, 0), 0.0, 0};
+    const double nis = -1.0 / G.two_s2;
+    Flush64x<true> fs{RB, acc, xt, yt, zt, wt, G.c2d, nis, G.ampd, out, lane};
+    Flush64x<false> fi{RI, acc, xt, yt, zt, wt, G.c2d, nis, G.ampd, out, lane};
+    int nB = 0, nI = 0;
+    traverse2(G, cell_start, blo, bhi, lane, st, fs, fi, nB, nI, st.skip_lo, st.skip_hi);
+    __syncwarp();
+    fs(nB);
+    fi(nI);
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+      if (tv[t]) atomicAdd(out + tidx[t], G.ampd * acc[t]);
+  }
+}
+
 // pack (x, y, z, w) records in sorted order for the fp32 tier
 __global__ void pack_src_f32(const float4* __restrict__ sorted, const float* __restrict__ w, int64_t n,
                              float4* __restrict__ src) {
@@ -974,7 +1103,7 @@ rbf_status matvec_sorted_f32(rbf_ctx* ctx, const rbf_cells* c, const KernelParam
 // (world > 1); the kernel indexes sources and targets by global sorted
 // position, so the window and output pointers are shifted by h0 and o0.
 rbf_status matvec_sorted_f32_d(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp, const double* w_loc,
-                               double* f_loc) {
+                               double* f_loc, bool solver) {
   cudaStream_t s = ctx->stream;
   const SlabView& V = c->view;
   const int64_t nw = V.h1 - V.h0;
@@ -993,7 +1122,7 @@ rbf_status matvec_sorted_f32_d(rbf_ctx* ctx, const rbf_cells* c, const KernelPar
   RBF_CUDA_TRY(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
   SumGeom G = make_geom(c, kp);
   GridDesc gd{};
-  const int sym = sym_mode(c->n_loc());
+  const int sym = solver ? sym_mode(c->n_loc()) : 0;   // the public product stays one-sided
   if (sym == 2) {
     // symmetric evaluation on the wide plan (reading R19): the output is accumulated
     RBF_CUDA_TRY(cudaMemsetAsync(f_loc, 0, sizeof(double) * (size_t)c->n_loc(), s));
@@ -1027,7 +1156,7 @@ rbf_status matvec_sorted_f32_d(rbf_ctx* ctx, const rbf_cells* c, const KernelPar
 // fp64 tier, same conventions as matvec_sorted_f32_d; out_perm (single GPU,
 // public path only) scatters to the caller's order.
 rbf_status matvec_sorted_f64(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
-                             const double* w_loc, double* f_out, const int32_t* out_perm) {
+                             const double* w_loc, double* f_out, const int32_t* out_perm, bool solver) {
   cudaStream_t s = ctx->stream;
   const SlabView& V = c->view;
   const int64_t nw = V.h1 - V.h0;
@@ -1040,6 +1169,16 @@ rbf_status matvec_sorted_f64(rbf_ctx* ctx, const rbf_cells* c, const KernelParam
   RBF_TRY(ctx->counter.ensure(256, s));
   RBF_CUDA_TRY(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
   SumGeom G = make_geom(c, kp);
+  if (solver && !out_perm && sym_mode(c->n_loc()) != 0) {
+    // solver path: symmetric fp64 tier (reading R19), accumulated output
+    RBF_CUDA_TRY(cudaMemsetAsync(f_out, 0, sizeof(double) * (size_t)c->n_loc(), s));
+    ProfScope ps(ctx, RBF_PROF_MATVEC_F64);
+    sum_f64_sym_kernel<<<sum_blocks(ctx, sum_f64_sym_kernel), kSumWarps * 32, 0, s>>>(
+        G, c->cell_start.as<int32_t>(), c->sorted.as<float4>(), w_win - V.h0, c->tiles.as<int2>(),
+        c->tile_box.as<float4>(), V.t1 - V.t0, V.t0, f_out - V.o0, ctx->counter.as<int>(), V.o0, V.o1);
+    RBF_CHECK_LAUNCH();
+    return RBF_OK;
+  }
   ProfScope ps(ctx, RBF_PROF_MATVEC_F64);
   sum_f64_kernel<<<sum_blocks(ctx, sum_f64_kernel), kSumWarps * 32, 0, s>>>(
       G, c->cell_start.as<int32_t>(), c->sorted.as<float4>(), w_win - V.h0, c->tiles.as<int2>(),
