@@ -3,6 +3,7 @@
 // library's kernels; there is no host compute fallback.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <new>
@@ -211,7 +212,11 @@ rbf_status rbf_matvec(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, 
   RBF_CUDA_TRY(cudaSetDevice(ctx->device));
   KernelParams kp = kernel_params(kern);
   const int64_t n = c->n;
-  if (ctx->world > 1 || c->emulated) {
+  // RBF_PUBLIC_SYM=1 (tests only): the public product runs the solver's operator
+  // (symmetric variants of reading R19) so it can be checked against the oracle
+  const char* ps = std::getenv("RBF_PUBLIC_SYM");
+  const bool solver_op = ps && ps[0] == '1';
+  if (ctx->world > 1 || c->emulated || solver_op) {
     // slab partition: replicated in, this rank's rows, gathered out
     if (prec != RBF_F32 && prec != RBF_F64) { set_error("bad precision"); return RBF_EINVAL; }
     RBF_TRY(ctx->vec_a.ensure(sizeof(double) * n, ctx->stream));
@@ -220,10 +225,10 @@ rbf_status rbf_matvec(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, 
     double* fs = ctx->vec_b.as<double>();
     if (prec == RBF_F32) {
       RBF_TRY(gather_f32_to_sorted_f64(ctx, static_cast<const float*>(w), c->perm.as<int32_t>(), ws, n));
-      RBF_TRY(matvec_sorted_f32_d(ctx, c, kp, ws + c->view.o0, fs + c->view.o0));
+      RBF_TRY(matvec_sorted_f32_d(ctx, c, kp, ws + c->view.o0, fs + c->view.o0, solver_op));
     } else {
       RBF_TRY(gather_f64_to_sorted(ctx, static_cast<const double*>(w), c->perm.as<int32_t>(), ws, n));
-      RBF_TRY(matvec_sorted_f64(ctx, c, kp, ws + c->view.o0, fs + c->view.o0, nullptr));
+      RBF_TRY(matvec_sorted_f64(ctx, c, kp, ws + c->view.o0, fs + c->view.o0, nullptr, solver_op));
     }
     RBF_TRY(allgather_sorted(ctx, c, fs));
     if (prec == RBF_F32) return scatter_f64_from_sorted_f32(ctx, fs, c->perm.as<int32_t>(), static_cast<float*>(f), n);

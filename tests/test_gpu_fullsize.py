@@ -77,6 +77,17 @@ def test_matvec_sampled_rows(R, ctx, big):
     assert (np.abs(f32[rows] - ref32) <= 5e-5 * g).all()
     assert np.linalg.norm(f32[rows] - ref32) / np.linalg.norm(ref32) <= 1e-4
     assert (np.abs(f64[rows] - ref64) <= 1e-12 * g).all()
+    # the solver's operators as benchmarked (symmetric variants at this size, reading R19)
+    os.environ["RBF_PUBLIC_SYM"] = "1"
+    try:
+        s32 = R.matvec(ctx, big["cells"], big["kern"], torch.as_tensor(w, dtype=torch.float32, device="cuda"))
+        s64 = R.matvec(ctx, big["cells"], big["kern"], torch.as_tensor(w, device="cuda"))
+    finally:
+        del os.environ["RBF_PUBLIC_SYM"]
+    s32, s64 = s32.cpu().numpy(), s64.cpu().numpy()
+    assert (np.abs(s32[rows] - ref32) <= 5e-5 * g).all()
+    assert np.linalg.norm(s32[rows] - ref32) / np.linalg.norm(ref32) <= 1e-4
+    assert (np.abs(s64[rows] - ref64) <= 1e-12 * g).all()
 
 
 def test_solve_as_benchmarked(R, ctx, big):
