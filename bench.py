@@ -197,7 +197,7 @@ def run_ours(args, rank, world, local):
     # the 1e-6 gate is unattainable at c4's sigma/spacing (DESIGN.md finding F1)
     solve_kw = dict(restart=cfg.restart, rtol=1e-6, phase1_rtol=1e-4, kind=cfg.precond_kind,
                     core_target=cfg.core_target, overlap_sigmas=cfg.overlap_sigmas, shift=cfg.shift,
-                    local_fp32=cfg.local_fp32, max_iters=args.fit_iters)
+                    local_fp32=cfg.local_fp32, cgs_passes=cfg.cgs_passes, max_iters=args.fit_iters)
 
     def step():
         centres, b = R.extend_points(ctx, x, nrm, d["delta"])

@@ -112,6 +112,7 @@ typedef struct {
   double phase1_rtol;    /* <= 0 => 1e-4 */
   int max_iters;         /* total inner iterations; <= 0 => 500 */
   int polish_fp64;       /* 1 => phase 2 in fp64 (needed for rtol < ~1e-5) */
+  int cgs_passes;        /* Gram-Schmidt passes per Arnoldi step: 1 (CGS) or 2 (CGS2); other => 2 */
 } rbf_gmres_cfg;
 
 typedef struct {

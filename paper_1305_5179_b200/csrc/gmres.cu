@@ -203,6 +203,7 @@ rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp
   const double p1tol = (gcfg && gcfg->phase1_rtol > 0) ? gcfg->phase1_rtol : 1e-4;
   const int maxit = (gcfg && gcfg->max_iters > 0) ? gcfg->max_iters : 500;
   const bool polish = gcfg ? gcfg->polish_fp64 != 0 : true;
+  const int passes = (gcfg && gcfg->cgs_passes == 1) ? 1 : 2;
   const int64_t n = S.n;
   const int m = S.m;
   RBF_TRY(S.alloc());
@@ -270,11 +271,15 @@ rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp
       RBF_TRY(precond_apply_sorted<double>(ctx, P, S.Vj(j), S.Zj(j)));
       RBF_TRY(S.op(fp64, S.Zj(j), S.w.as<double>()));
       double* wv = S.w.as<double>();
-      // CGS2
+      // classical Gram-Schmidt, one pass or two (CGS2, the default)
       RBF_TRY(S.mdot(S.V.as<double>(), j + 1, wv, dh, dneg));
       RBF_TRY(S.maxpy(wv, S.V.as<double>(), j + 1, dneg));
-      RBF_TRY(S.mdot(S.V.as<double>(), j + 1, wv, d2, dneg));
-      RBF_TRY(S.maxpy(wv, S.V.as<double>(), j + 1, dneg));
+      if (passes == 2) {
+        RBF_TRY(S.mdot(S.V.as<double>(), j + 1, wv, d2, dneg));
+        RBF_TRY(S.maxpy(wv, S.V.as<double>(), j + 1, dneg));
+      } else {
+        RBF_CUDA_TRY(cudaMemsetAsync(d2, 0, sizeof(double) * (j + 1), s));
+      }
       RBF_TRY(S.mdot(wv, 1, wv, dn, nullptr));
       scale_by_inv_norm<<<grid_for(n, 256), 256, 0, s>>>(wv, dn, S.Vj(j + 1), n);
       RBF_CHECK_LAUNCH();

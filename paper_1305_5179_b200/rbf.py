@@ -48,7 +48,7 @@ class _PrecondCfg(C.Structure):
 
 class _GmresCfg(C.Structure):
     _fields_ = [("restart", C.c_int), ("rtol", C.c_double), ("phase1_rtol", C.c_double),
-                ("max_iters", C.c_int), ("polish_fp64", C.c_int)]
+                ("max_iters", C.c_int), ("polish_fp64", C.c_int), ("cgs_passes", C.c_int)]
 
 
 class SolveReport(C.Structure):
@@ -508,13 +508,13 @@ class Precond:
 def gmres_solve(ctx: Context, cells: Cells, kernel: Kernel, b: torch.Tensor, precond: Precond | None = None,
                 kind: int = 2, core_target: int = 512, overlap_sigmas: float = 1.0, restart: int = 30,
                 rtol: float = 1e-6, phase1_rtol: float = 1e-4, max_iters: int = 500, polish_fp64: int = 1,
-                shift: float = 0.0, local_fp32: int = 0, out: torch.Tensor | None = None):
+                shift: float = 0.0, local_fp32: int = 0, cgs_passes: int = 2, out: torch.Tensor | None = None):
     """Solve A w = b (Eq.4) with RAS-preconditioned FGMRES; returns (w fp64, report dict)."""
     _need(b, torch.float32, cells.n, "b")
     w = torch.empty(cells.n, dtype=torch.float64, device=b.device) if out is None else out
     _need(w, torch.float64, cells.n, "w")
     pc = _PrecondCfg(kind, core_target, overlap_sigmas, 0, shift, local_fp32)
-    gc = _GmresCfg(restart, rtol, phase1_rtol, max_iters, polish_fp64)
+    gc = _GmresCfg(restart, rtol, phase1_rtol, max_iters, polish_fp64, cgs_passes)
     rep = SolveReport()
     _check(_lib.rbf_gmres_solve(ctx._h, cells._h, C.byref(kernel._c()), None if precond is None else precond._h,
                                 C.byref(pc), C.byref(gc), _ptr(b), _ptr(w), C.byref(rep)))
@@ -524,7 +524,7 @@ def gmres_solve(ctx: Context, cells: Cells, kernel: Kernel, b: torch.Tensor, pre
 def reconstruct_host(ctx: Context, xyz, b, kernel: Kernel, lo, hi, n, *, cell_edge: float = 0.0,
                      kind: int = 2, core_target: int = 512, overlap_sigmas: float = 1.0, restart: int = 30,
                      rtol: float = 1e-6, phase1_rtol: float = 1e-4, max_iters: int = 500,
-                     shift: float = 0.0, local_fp32: int = 0, w_out=None, field_out=None):
+                     shift: float = 0.0, local_fp32: int = 0, cgs_passes: int = 2, w_out=None, field_out=None):
     """Alg.1 steps 2-3 from HOST buffers (numpy or CPU tensors; pinned is fastest)."""
     import numpy as np
     xyz = torch.as_tensor(xyz, dtype=torch.float32).contiguous()
@@ -537,7 +537,7 @@ def reconstruct_host(ctx: Context, xyz, b, kernel: Kernel, lo, hi, n, *, cell_ed
     _check(_lib.rbf_reconstruct_host(ctx._h, _ptr(xyz), _ptr(b), nn, C.byref(kernel._c()),
                                      C.byref(_CellCfg(cell_edge, 64, 2, 0)),
                                      C.byref(_PrecondCfg(kind, core_target, overlap_sigmas, 0, shift, local_fp32)),
-                                     C.byref(_GmresCfg(restart, rtol, phase1_rtol, max_iters, 1)),
+                                     C.byref(_GmresCfg(restart, rtol, phase1_rtol, max_iters, 1, cgs_passes)),
                                      C.byref(g), _ptr(w), _ptr(field), C.byref(rep)))
     del np
     return w, field, rep.as_dict()

@@ -32,6 +32,7 @@ class Config:
     precond_kind: int = 2     # 0 none, 1 block-Jacobi, 2 RAS (include/rbf.h)
     shift: float = 0.0        # local diagonal shift in units of a (reading R17)
     local_fp32: int = 0       # fp32 on-chip local inverses (reading R17)
+    cgs_passes: int = 2       # Gram-Schmidt passes per Arnoldi step (1: CGS, 2: CGS2)
     kw: dict = field(default_factory=dict)
 
 
@@ -40,19 +41,21 @@ CONFIGS = {
     "c1": Config("c1", "sphere", 1000, 0.1, 0.01, 32, restart=30,
                  core_target=512, overlap_sigmas=3.0),
     # configs[1]: torus R=1 r=0.35, N=20k, noise 1e-3, delta 0.005, sigma 0.05, 128^3
-    "c2": Config("c2", "torus", 20000, 0.05, 0.005, 128, overlap_sigmas=1.3,
+    # (noisy data at sigma/spacing 1.9: ill-posed, finding F1; the least-bad
+    # preconditioner measured is RAS(128, 1 sigma) with a shift of 1.0 a: 0.18 in 100 its)
+    "c2": Config("c2", "torus", 20000, 0.05, 0.005, 128, core_target=128, overlap_sigmas=1.0, shift=1.0,
                  kw=dict(R=1.0, r=0.35, noise=1e-3)),
     # configs[2]: blobby K=16, N=200k, 10x density, sigma 0.02 (delta = 0.1 sigma, reading 4)
     # c3-c5 sit at sigma/spacing ~3-4 where exact local solves stall GMRES (DESIGN.md
     # finding F4): shifted block-Jacobi local solves, fp32 on chip (reading R17)
     "c3": Config("c3", "blobby", 200000, 0.02, 0.002, 256, core_target=64, overlap_sigmas=0.0,
-                 precond_kind=1, shift=0.003, local_fp32=1, kw=dict(K=16, density_mod=True)),
+                 precond_kind=1, shift=0.003, local_fp32=1, cgs_passes=1, kw=dict(K=16, density_mod=True)),
     # configs[3]: blobby K=64, N=1M, sigma 0.01, 256^3  (the metric config)
     "c4": Config("c4", "blobby", 1000000, 0.01, 0.001, 256, core_target=64, overlap_sigmas=0.0,
-                 precond_kind=1, shift=0.003, local_fp32=1, kw=dict(K=64)),
+                 precond_kind=1, shift=0.003, local_fp32=1, cgs_passes=1, kw=dict(K=64)),
     # configs[4]: blobby K=64 with 5 caps removed, N=10M, sigma 0.004, 512^3
     "c5": Config("c5", "blobby", 10000000, 0.004, 0.0004, 512, core_target=64, overlap_sigmas=0.0,
-                 precond_kind=1, shift=0.003, local_fp32=1, kw=dict(K=64, holes=5)),
+                 precond_kind=1, shift=0.003, local_fp32=1, cgs_passes=1, kw=dict(K=64, holes=5)),
 }
 
 

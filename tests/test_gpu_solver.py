@@ -362,3 +362,17 @@ def test_symmetric_fp32_tier_variants(R, ctx):
     for sym in ("0", "1", "2"):
         assert out[sym][0] <= 1.5e-6, out
         assert abs(out[sym][1]["iters_phase1"] - out["0"][1]["iters_phase1"]) <= 5, out
+
+
+def test_cgs1_and_cgs2_reach_the_gate(R, ctx):
+    """One classical Gram-Schmidt pass (the c3-c5 setting) and CGS2 (the default)
+    both reach the 1e-6 two-phase gate on the well-posed torus, certified by the oracle."""
+    d, X, b = problem("c2", n=3000)
+    sigma = d["sigma"]
+    kern = R.Kernel(sigma)
+    cells = R.Cells(ctx, dev(X, torch.float32), kern)
+    for passes in (1, 2):
+        w, rep = R.gmres_solve(ctx, cells, kern, dev(b, torch.float32), restart=50, rtol=1e-6, core_target=512,
+                               overlap_sigmas=1.3, max_iters=400, cgs_passes=passes)
+        res = np.linalg.norm(b - OK.matvec(X, host(w), sigma)) / np.linalg.norm(b)
+        assert rep["converged"] == 1 and res <= 1.5e-6, (passes, res, rep)
