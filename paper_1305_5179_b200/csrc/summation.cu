@@ -306,6 +306,11 @@ struct Flush32e {
   }
 };
 
+#ifndef RBF_SYMW_UNROLL
+#define RBF_SYMW_UNROLL 1
+#endif
+#define RBF_PRAGMA_STR(x) #x
+#define RBF_UNROLL(n) _Pragma(RBF_PRAGMA_STR(unroll n))
 // Symmetric inner loop (A = A^T): every exponential of a staged source j
 // (sorted index beyond this tile, same rank) serves both f_i += a e_ij w_j
 // (this lane's targets, as Flush32e) and f_j += a e_ij w_i.  The source side
@@ -326,7 +331,7 @@ struct Flush32s {
   __device__ __forceinline__ void operator()(int cnt) {
     const bool h4 = lane & 16, h3 = lane & 8;
     const int mys = (h4 ? 2 : 0) + (h3 ? 1 : 0);
-#pragma unroll 2
+    RBF_UNROLL(RBF_SYMW_UNROLL)
     for (int j = 0; j < cnt; j += 4) {
       const float4 X = *reinterpret_cast<const float4*>(r.bx + j);
       const float4 Y = *reinterpret_cast<const float4*>(r.by + j);
@@ -670,7 +675,7 @@ sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
 }
 
 #ifndef RBF_SYMW_MINB
-#define RBF_SYMW_MINB 7
+#define RBF_SYMW_MINB 8
 #endif
 // Symmetric fp32 matvec on the WIDE tile plan (reading R19): up to 128 targets
 // per warp (4 per lane), so the per-source transpose-reduction of the source
