@@ -24,7 +24,8 @@ def main():
     kern = R.Kernel(d["sigma"])
     c, b = R.extend_points(ctx, torch.as_tensor(d["x"], device="cuda"), torch.as_tensor(d["normals"], device="cuda"),
                            d["delta"])
-    cells = R.Cells(ctx, c, kern)
+    div = float(os.environ.get("CELL_DIV", "3.999"))
+    cells = R.Cells(ctx, c, kern, cell_edge=6 * d["sigma"] / div)
     kw = dict(restart=50, kind=cfg.precond_kind, core_target=cfg.core_target, overlap_sigmas=cfg.overlap_sigmas,
               shift=cfg.shift, local_fp32=cfg.local_fp32, max_iters=50)
     ref_w = None
