@@ -255,3 +255,40 @@ def test_grid_ragged_and_anisotropic(R, ctx):
     assert (np.abs(F - ref) <= 5e-5 * g + 1e-30).all()
     with pytest.raises(R.RbfError):
         R.eval_grid(ctx, cells, kern, dev(w, torch.float64), lo, hi, (1, 5, 5))
+
+
+@pytest.mark.parametrize("sym", ["1", "2"])
+def test_symmetric_operators_degenerate_clouds(R, ctx, sym):
+    """Reading R19 on degenerate inputs: one centre, two coincident centres, a
+    dense clump in one cell (tiles of 1..128 targets, sources equal to targets),
+    a line of points and a clump plus far outliers.  The solver's symmetric
+    fp32/fp64 operators (RBF_PUBLIC_SYM=1) equal the one-sided public products
+    to the tiers' accuracy, including exact zeros for isolated centres' neighbours."""
+    import os
+    rng = np.random.default_rng(21)
+    clouds = [
+        np.array([[0.1, 0.2, 0.3]]),
+        np.array([[0.0, 0.0, 0.0], [0.0, 0.0, 0.0]]),
+        rng.normal(scale=0.01, size=(300, 3)),
+        np.stack([np.linspace(0, 1, 777), np.zeros(777), np.zeros(777)], axis=1),
+        np.concatenate([rng.normal(scale=0.05, size=(500, 3)), [[5, 5, 5], [-5, 0, 0]]]),
+    ]
+    sigma = 0.05
+    kern = R.Kernel(sigma)
+    for X in clouds:
+        X = X.astype(np.float32)
+        cells = R.Cells(ctx, dev(X, torch.float32), kern)
+        w = rng.normal(size=len(X))
+        ref32 = host(R.matvec(ctx, cells, kern, dev(w, torch.float32)))
+        ref64 = host(R.matvec(ctx, cells, kern, dev(w, torch.float64)))
+        g = host(R.matvec(ctx, cells, kern, dev(np.abs(w), torch.float64)))
+        os.environ["RBF_SUM_SYM"] = sym
+        os.environ["RBF_PUBLIC_SYM"] = "1"
+        try:
+            s32 = host(R.matvec(ctx, cells, kern, dev(w, torch.float32)))
+            s64 = host(R.matvec(ctx, cells, kern, dev(w, torch.float64)))
+        finally:
+            del os.environ["RBF_SUM_SYM"]
+            del os.environ["RBF_PUBLIC_SYM"]
+        assert (np.abs(s32 - ref32) <= 5e-5 * g + 1e-30).all(), len(X)
+        assert (np.abs(s64 - ref64) <= 1e-12 * g + 1e-300).all(), len(X)
