@@ -910,6 +910,11 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
   return RBF_OK;
 }
 
+int apply_threads() {
+  const char* e = std::getenv("RBF_APPLY_THREADS");
+  return e ? std::atoi(e) : 128;
+}
+
 template <class VT>
 rbf_status precond_apply_sorted(rbf_ctx* ctx, const rbf_precond* P, const VT* r, VT* z) {
   cudaStream_t s = ctx->stream;
@@ -925,8 +930,12 @@ rbf_status precond_apply_sorted(rbf_ctx* ctx, const rbf_precond* P, const VT* r,
     if (smemf > 48 * 1024)
       RBF_CUDA_TRY(cudaFuncSetAttribute(apply_f32w_kernel<VT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smemf));
+    // one CTA (4 warps) per block: many small CTAs resident per SM hide the
+    // gather -> barrier -> row-latency chain of each block
+    const int threads = apply_threads();
+    const int ablocks = (int)std::min<int64_t>(P->nblocks, (int64_t)1 << 30);
     ProfScope ps(ctx, RBF_PROF_PRECOND_APPLY);
-    apply_f32w_kernel<VT><<<blocks, 256, smemf, s>>>(P->ext_ptr.as<int64_t>(), P->core_ptr.as<int64_t>(),
+    apply_f32w_kernel<VT><<<threads == 256 ? blocks : ablocks, threads, smemf, s>>>(P->ext_ptr.as<int64_t>(), P->core_ptr.as<int64_t>(),
                                                      P->ext_idx.as<int32_t>(), P->w_off.as<int64_t>(),
                                                      P->W.as<float>(), r, z, P->nblocks);
     RBF_CHECK_LAUNCH();
