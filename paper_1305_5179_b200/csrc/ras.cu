@@ -332,9 +332,14 @@ __global__ void assemble_kernel(const LuJob* __restrict__ jobs, const float4* __
 // Work per block: m^3 FMAs; HBM sees the W write (4 nc m bytes) and the centre
 // reads only.
 constexpr int kGjMax = 224;
+// shift (units of a) from which the on-chip inversion skips pivoting: B_i =
+// A_i + shift a I is then positive definite (A_i is a Gaussian matrix of
+// centres within one block, whose only deviation from positive semidefinite is
+// rounding, <= ~1e-6 a in fp32)
+constexpr double kNoPivShift = 1e-4;
 constexpr int kGjThreads = 512;
 
-template <int RM, int RC>
+template <int RM, int RC, bool PIV>
 __global__ void __launch_bounds__(kGjThreads, (RM * RC <= 32) ? 2 : 1)
 gj_inverse_f32_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __restrict__ core_ptr,
                       const int32_t* __restrict__ ext_idx, const int64_t* __restrict__ w_off,
@@ -396,7 +401,27 @@ gj_inverse_f32_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __rest
       cand_a[buf][wr] = bv;
       cand_i[buf][wr] = bi;
     };
-    publish(std::integral_constant<int, 0>{}, 0, 0);
+    // no-pivot variant (PIV = false, shift >= kNoPivShift: B_i is symmetric
+    // positive definite -- a Gaussian submatrix of a block narrower than the
+    // cutoff plus mu a I -- so elimination in order is stable): the owners publish
+    // row k+1 and column k+1 right after step k's update, ONE barrier per step.
+    auto pubcol = [&](auto cbt, int c, int buf) {
+      constexpr int CB = decltype(cbt)::value;
+      if (lane != (c & 31)) return;
+#pragma unroll
+      for (int a = 0; a < RM; ++a) colbuf[buf][wr + 16 * a] = B[a][CB];   // padding rows hold 0
+    };
+    auto pubrow = [&](auto at, int buf) {
+      constexpr int AR = decltype(at)::value;
+#pragma unroll
+      for (int b = 0; b < RC; ++b) rowbuf[buf][lane + 32 * b] = B[AR][b];
+    };
+    if constexpr (PIV) {
+      publish(std::integral_constant<int, 0>{}, 0, 0);
+    } else {
+      pubcol(std::integral_constant<int, 0>{}, 0, 0);
+      if (wr == 0) pubrow(std::integral_constant<int, 0>{}, 0);
+    }
     __syncthreads();
     // Step k = 32 KB + 16 H + q: column k is register column KB of lane
     // 16 H + q; row k is register row A = 2 KB + H of warp q.  Both indices
@@ -409,6 +434,44 @@ gj_inverse_f32_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __rest
         if (k >= m) return;
         const int cb = k & 1;
         const int kl = 16 * H + q;
+        if constexpr (!PIV) {
+          const float pv = rowbuf[cb][k];
+          if (pv == 0.0f) singular = 1;
+          const float d = __frcp_rn(pv);
+          float rkv[RC];
+#pragma unroll
+          for (int b = 0; b < RC; ++b) rkv[b] = rowbuf[cb][lane + 32 * b] * d;
+          float fa[RM];
+#pragma unroll
+          for (int a = 0; a < RM; ++a) {
+            fa[a] = colbuf[cb][wr + 16 * a];
+#pragma unroll
+            for (int b = 0; b < RC; ++b) B[a][b] = fmaf(-fa[a], rkv[b], B[a][b]);
+          }
+          if (lane == kl) {
+#pragma unroll
+            for (int a = 0; a < RM; ++a) B[a][KB] = -fa[a] * d;
+          }
+          if (wr == q) {
+#pragma unroll
+            for (int b = 0; b < RC; ++b) B[A][b] = rkv[b];
+            if (lane == kl) B[A][KB] = d;
+          }
+          if (k + 1 < m) {
+            if (q < 15) {
+              pubcol(std::integral_constant<int, KB>{}, k + 1, cb ^ 1);
+              if (wr == q + 1) pubrow(std::integral_constant<int, A>{}, cb ^ 1);
+            } else if constexpr (H == 0) {
+              pubcol(std::integral_constant<int, KB>{}, k + 1, cb ^ 1);
+              if (wr == 0) pubrow(std::integral_constant<int, A + 1>{}, cb ^ 1);
+            } else if constexpr (KB + 1 < RC) {
+              pubcol(std::integral_constant<int, KB + 1>{}, k + 1, cb ^ 1);
+              if (wr == 0) pubrow(std::integral_constant<int, A + 1>{}, cb ^ 1);
+            }
+          }
+          __syncthreads();
+          continue;
+        }
         // (1) every warp reduces the 16 per-warp candidates
         float ba = -1.0f, bv = 0.0f;
         int bi = 0x7fffffff;
@@ -489,7 +552,10 @@ gj_inverse_f32_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __rest
       ((block(std::integral_constant<int, KBs>{}, std::integral_constant<int, 0>{}),
         block(std::integral_constant<int, KBs>{}, std::integral_constant<int, 1>{})), ...);
     }(std::make_integer_sequence<int, RC>{});
-    if (tid == 0) {
+    if (!PIV) {
+      for (int j = tid; j < m; j += kGjThreads) piv[j] = j;   // no row swaps: identity
+    }
+    if (PIV && tid == 0) {
       for (int j = 0; j < m; ++j) pinv[j] = j;   // pi (built in place, then inverted below)
       for (int k = m - 1; k >= 0; --k) {
         const int q = pinv[k];
@@ -497,8 +563,8 @@ gj_inverse_f32_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __rest
         pinv[piv[k]] = q;
       }
       for (int e = 0; e < m; ++e) piv[pinv[e]] = e;   // piv := pi^-1
-      if (singular) atomicAdd(info, 1);
     }
+    if (tid == 0 && singular) atomicAdd(info, 1);
     __syncthreads();
     // W[c][e] = B[m-nc+c][pi[e]]  <=>  element (i, j) goes to column pi^-1[j]
     float* Wb = W + w_off[blk];
@@ -827,6 +893,8 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
     RBF_CUDA_TRY(cudaMemcpyAsync(blist.p, small.data(), 8 * small.size(), cudaMemcpyHostToDevice, s));
     size_t lo = 0;
     const int caps[3] = {128, 192, 224};
+    // shifted SPD blocks need no pivoting (one barrier per elimination step)
+    const bool nopiv = shift >= kNoPivShift && std::getenv("RBF_GJ_PIVOT") == nullptr;
     for (int bin = 0; bin < 3 && lo < small.size(); ++bin) {
       size_t hi = lo;
       while (hi < small.size() && h_ext_ptr[small[hi] + 1] - h_ext_ptr[small[hi]] <= caps[bin]) ++hi;
@@ -836,7 +904,7 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
         const int gblocks = (int)std::min<int64_t>(cnt, (int64_t)ctx->sm_count * (bin == 0 ? 2 : 1));
         const int64_t* bl = blist.as<int64_t>() + lo;
 #define RBF_GJ_LAUNCH(RM_, RC_)                                                                            \
-  gj_inverse_f32_kernel<RM_, RC_><<<gblocks, kGjThreads, 0, s>>>(                                         \
+  (nopiv ? gj_inverse_f32_kernel<RM_, RC_, false> : gj_inverse_f32_kernel<RM_, RC_, true>)<<<gblocks, kGjThreads, 0, s>>>( \
       P->ext_ptr.as<int64_t>(), P->core_ptr.as<int64_t>(), P->ext_idx.as<int32_t>(), P->w_off.as<int64_t>(), \
       sorted, kp.amp, two_s2, c2, shift_abs, P->W.as<float>(), bl, cnt, info.as<int>())
         if (bin == 0) RBF_GJ_LAUNCH(8, 4);

@@ -130,17 +130,24 @@ def _flat_cap(ratio=3.0, n_sphere=6000, zcut=0.55):
     return X, b, sigma
 
 
-@pytest.mark.parametrize("core", [128, 256])
-def test_gj_fp32_apply_parity(R, ctx, core):
+@pytest.mark.parametrize("core,pivot", [(128, False), (256, False), (128, True)])
+def test_gj_fp32_apply_parity(R, ctx, core, pivot):
     """Reading R17, on-chip fp32 Gauss-Jordan factors (local_fp32=1) against the
     oracle's fp64 LU of the same shifted blocks.  Bound: the fp32 inverse of B
     carries a relative error <= c kappa(B) m u32 (u32 = 2^-24); kappa(B) is
     computed here from the oracle's blocks, c = 4."""
+    import os
     X, _, sigma = _flat_cap()
     mu = 0.01
     kern = R.Kernel(sigma)
     cells = R.Cells(ctx, dev(X, torch.float32), kern)
-    P = R.Precond(ctx, cells, kern, kind=1, core_target=core, shift=mu, local_fp32=1)
+    # mu >= 1e-4 eliminates without pivoting (B_i SPD); RBF_GJ_PIVOT forces partial pivoting
+    if pivot:
+        os.environ["RBF_GJ_PIVOT"] = "1"
+    try:
+        P = R.Precond(ctx, cells, kern, kind=1, core_target=core, shift=mu, local_fp32=1)
+    finally:
+        os.environ.pop("RBF_GJ_PIVOT", None)
     cores, exts, nbytes = P.blocks()
     oc = OC.build(X, 6 * sigma, cell_edge=6 * sigma / 3.999)
     blocks = OS.ras_blocks(oc, sigma, core, 0.0)
