@@ -327,11 +327,17 @@ __global__ void assemble_kernel(const LuJob* __restrict__ jobs, const float4* __
 // (warp r, lane t) owns rows i = r + 16 a (a < RM) and columns j = t + 32 b
 // (b < RC), so m <= min(16 RM, 32 RC).  Per step only column k (for the pivot
 // search and the multipliers) and the two swapped rows go through shared
-// memory; the rank-1 update is RM*RC register FMAs per thread.  Three block
-// barriers per step; the multiplier buffer is double-buffered by step parity.
+// memory; the rank-1 update is RM*RC register FMAs per thread.  With partial
+// pivoting two block barriers and a warp reduction per step; without (PIV =
+// false, shifted SPD blocks) one barrier per step.  The multiplier buffer is
+// double-buffered by step parity.
 // Work per block: m^3 FMAs; HBM sees the W write (4 nc m bytes) and the centre
 // reads only.
 constexpr int kGjMax = 224;
+// offset of row i in a packed lower triangle
+__host__ __device__ __forceinline__ int64_t tri_off(int i) { return (int64_t)i * (i + 1) / 2; }
+// floats of a block's packed triangle, padded to 16 B (bulk-copy granularity)
+__host__ __device__ __forceinline__ int64_t tri_floats(int64_t m) { return (m * (m + 1) / 2 + 3) & ~(int64_t)3; }
 // shift (units of a) from which the on-chip inversion skips pivoting: B_i =
 // A_i + shift a I is then positive definite (A_i is a Gaussian matrix of
 // centres within one block, whose only deviation from positive semidefinite is
@@ -345,7 +351,7 @@ gj_inverse_f32_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __rest
                       const int32_t* __restrict__ ext_idx, const int64_t* __restrict__ w_off,
                       const float4* __restrict__ sorted, double amp, double two_s2, double c2,
                       double shift_abs, float* __restrict__ W, const int64_t* __restrict__ blist,
-                      int64_t nlist, int* __restrict__ info) {
+                      int64_t nlist, int* __restrict__ info, bool sym_out) {
   constexpr int MR = 16 * RM, MC = 32 * RC;
   constexpr int MM = MR < MC ? MR : MC;
   __shared__ float colbuf[2][MM];
@@ -566,7 +572,8 @@ gj_inverse_f32_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __rest
     }
     if (tid == 0 && singular) atomicAdd(info, 1);
     __syncthreads();
-    // W[c][e] = B[m-nc+c][pi[e]]  <=>  element (i, j) goes to column pi^-1[j]
+    // W[c][e] = B[m-nc+c][pi[e]]  <=>  element (i, j) goes to column pi^-1[j];
+    // sym_out (block-Jacobi, nc = m): only the lower triangle, packed by rows
     float* Wb = W + w_off[blk];
     const int r0 = m - nc;
 #pragma unroll
@@ -576,7 +583,11 @@ gj_inverse_f32_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __rest
 #pragma unroll
       for (int b = 0; b < RC; ++b) {
         const int j = lane + 32 * b;
-        if (j < m) Wb[(int64_t)(i - r0) * m + piv[j]] = B[a][b];
+        if (j < m) {
+          const int col = piv[j];
+          if (!sym_out) Wb[(int64_t)(i - r0) * m + col] = B[a][b];
+          else if (col <= i) Wb[tri_off(i) + col] = B[a][b];
+        }
       }
     }
     __syncthreads();
@@ -612,12 +623,133 @@ apply_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __restrict__ co
 }
 
 // fp64 restricted inverses of the blocks too large for the on-chip path,
-// rounded into the fp32 W (local_fp32): triples (src offset, dst offset, count)
+// rounded into the fp32 W (local_fp32): quadruples (src offset, dst offset,
+// count, m); m > 0: the source is a full m x m inverse of which the lower
+// triangle is stored packed (symmetric W, block-Jacobi)
 __global__ void round_w_kernel(const int64_t* __restrict__ trip, int64_t ntrip, const double* __restrict__ src,
                                float* __restrict__ dst) {
   for (int64_t t = blockIdx.x; t < ntrip; t += gridDim.x) {
-    const int64_t so = trip[3 * t], d0 = trip[3 * t + 1], cnt = trip[3 * t + 2];
-    for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) dst[d0 + i] = (float)src[so + i];
+    const int64_t so = trip[4 * t], d0 = trip[4 * t + 1], cnt = trip[4 * t + 2], m = trip[4 * t + 3];
+    if (m == 0) {
+      for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) dst[d0 + i] = (float)src[so + i];
+    } else {
+      for (int64_t i = 0; i < m; ++i)
+        for (int64_t j = threadIdx.x; j <= i; j += blockDim.x) dst[d0 + tri_off((int)i) + j] = (float)src[so + i * m + j];
+    }
+  }
+}
+
+// Symmetric W (block-Jacobi with fp32 W: W_i = B_i^-1, B_i symmetric), stored
+// as the packed lower triangle T (row i holds W[i][0..i] at i(i+1)/2, blocks
+// padded to 16 B): half the bytes of the full inverse.
+//
+// z_i = sum_{j<i} T[i][j] r_j + sum_{j>=i} T[j][i] r_j, thread i per row.  For a
+// warp (rows i0 .. i0+31) the j range splits into three warp-uniform parts:
+// j < i0 (every lane reads its own row at offset j: triangular numbers mod 32
+// are a permutation, so distinct banks; r_j .. r_j+3 one broadcast float4),
+// the warp's own 32 columns (a select between the two), and j >= i0 + 32
+// (lane i reads T[j][i]: consecutive addresses).
+template <class VT>
+__device__ __forceinline__ void apply_sym_rows(const float* __restrict__ T, const float* __restrict__ xs, int m,
+                                               int tid, int nthr, const int32_t* __restrict__ idx,
+                                               VT* __restrict__ z) {
+  const int lane = tid & 31;
+  for (int i0 = tid - lane; i0 < m; i0 += nthr) {
+    const int i = i0 + lane;
+    const int ic = i < m ? i : m - 1;            // idle lanes shadow the last row
+    const int ri = (int)tri_off(ic);
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    int j = 0;
+    for (; j < i0; j += 4) {                     // i0 is a multiple of 32
+      const float4 xv = *reinterpret_cast<const float4*>(xs + j);
+      a0 = fmaf(T[ri + j], xv.x, a0);
+      a1 = fmaf(T[ri + j + 1], xv.y, a1);
+      a2 = fmaf(T[ri + j + 2], xv.z, a2);
+      a3 = fmaf(T[ri + j + 3], xv.w, a3);
+    }
+    const int jc = min(i0 + 32, m);
+    int tj = (int)tri_off(i0);                   // j (j + 1) / 2
+    for (; j < jc; ++j) {
+      a0 = fmaf(T[j < ic ? ri + j : tj + ic], xs[j], a0);
+      tj += j + 1;
+    }
+    int o = tj + ic;
+    for (; j + 1 < m; j += 2) {
+      const float t0 = T[o];
+      const float t1 = T[o + j + 1];
+      o += 2 * j + 3;
+      a1 = fmaf(t0, xs[j], a1);
+      a2 = fmaf(t1, xs[j + 1], a2);
+    }
+    if (j < m) a3 = fmaf(T[o], xs[j], a3);
+    if (i < m) z[idx[i]] = (VT)((a0 + a1) + (a2 + a3));
+  }
+}
+
+// Persistent CTAs, blocks b = blockIdx.x + k gridDim.x: one thread streams the
+// NEXT block's triangle into the other shared-memory stage with a bulk copy
+// (TMA engine, mbarrier completion) while the CTA gathers r_ext of the current
+// block and multiplies -- HBM sees one continuous stream per CTA.  Triangles
+// above the stage size (rare big blocks) are read from global.
+template <class VT>
+__global__ void __launch_bounds__(128)
+apply_sym_kernel(const int64_t* __restrict__ ext_ptr, const int32_t* __restrict__ ext_idx,
+                 const int64_t* __restrict__ w_off, const float* __restrict__ W, const VT* __restrict__ r,
+                 VT* __restrict__ z, int64_t nblocks, int cap_floats, int max_m) {
+  extern __shared__ __align__(16) float sm[];
+  float* xs = sm;                                  // [max_m rounded to 4]
+  float* stage = sm + ((max_m + 3) & ~3);          // [2][cap_floats]
+  __shared__ __align__(8) uint64_t bar[2];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int k = 0; k < 2; ++k)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&bar[k])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t b, int st) {
+    if (b >= nblocks) return;
+    const int64_t w0 = w_off[b];
+    const int nfl = (int)(w_off[b + 1] - w0);
+    if (nfl > cap_floats) return;
+    const uint32_t ba = (uint32_t)__cvta_generic_to_shared(&bar[st]);
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(stage + (size_t)st * cap_floats);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ba), "r"(nfl * 4) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(W + w0), "r"(nfl * 4), "r"(ba)
+                 : "memory");
+  };
+  if (tid == 0) issue(blockIdx.x, 0);
+  uint32_t phase = 0;   // bit k: parity of stage k's next completion
+  int st = 0;
+  // (gridDim.x >= nblocks: one block per CTA, no prefetch, one stage)
+  for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, st ^= 1) {
+    // stage st^1 was last read before the barrier that closed the previous iteration
+    if (tid == 0) issue(b + gridDim.x, st ^ 1);
+    const int64_t e0 = ext_ptr[b];
+    const int m = (int)(ext_ptr[b + 1] - e0);
+    const int64_t w0 = w_off[b];
+    const bool staged = (w_off[b + 1] - w0) <= cap_floats;
+    for (int e = tid; e < m; e += blockDim.x) xs[e] = (float)r[ext_idx[e0 + e]];
+    for (int e = m + tid; e < ((m + 3) & ~3); e += blockDim.x) xs[e] = 0.f;
+    __syncthreads();
+    if (staged) {
+      const uint32_t ba = (uint32_t)__cvta_generic_to_shared(&bar[st]);
+      uint32_t done = 0;
+      while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(ba), "r"((phase >> st) & 1u)
+            : "memory");
+      }
+      phase ^= 1u << st;
+      apply_sym_rows(stage + (size_t)st * cap_floats, xs, m, tid, blockDim.x, ext_idx + e0, z);
+    } else {
+      apply_sym_rows(W + w0, xs, m, tid, blockDim.x, ext_idx + e0, z);
+    }
+    __syncthreads();
   }
 }
 
@@ -828,10 +960,16 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
   }
   std::vector<int64_t> h_ext_ptr(ncore + 1, 0), h_w_off(ncore + 1, 0);
   int64_t max_m = 0;
+  // block-Jacobi with fp32 W: W_i = B_i^-1 is symmetric -> packed lower triangles
+  // (RBF_APPLY_FULL=1 keeps the full inverses)
+  P->w_sym = want_fp32 && no_overlap && std::getenv("RBF_APPLY_FULL") == nullptr;
+  P->max_wblk = 0;
   for (int64_t b = 0; b < ncore; ++b) {
     h_ext_ptr[b + 1] = h_ext_ptr[b] + h_ecount[b];
     const int64_t m = h_ecount[b], nc = h_core_ptr[b + 1] - h_core_ptr[b];
-    h_w_off[b + 1] = h_w_off[b] + m * nc;
+    const int64_t wb = P->w_sym ? tri_floats(m) : m * nc;
+    h_w_off[b + 1] = h_w_off[b] + wb;
+    P->max_wblk = std::max(P->max_wblk, wb);
     max_m = std::max(max_m, m);
   }
   if (herr0 == 1) { set_error("RAS core larger than the ext-search capacity"); return RBF_EUNSUPPORTED; }
@@ -906,7 +1044,7 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
 #define RBF_GJ_LAUNCH(RM_, RC_)                                                                            \
   (nopiv ? gj_inverse_f32_kernel<RM_, RC_, false> : gj_inverse_f32_kernel<RM_, RC_, true>)<<<gblocks, kGjThreads, 0, s>>>( \
       P->ext_ptr.as<int64_t>(), P->core_ptr.as<int64_t>(), P->ext_idx.as<int32_t>(), P->w_off.as<int64_t>(), \
-      sorted, kp.amp, two_s2, c2, shift_abs, P->W.as<float>(), bl, cnt, info.as<int>())
+      sorted, kp.amp, two_s2, c2, shift_abs, P->W.as<float>(), bl, cnt, info.as<int>(), P->w_sym)
         if (bin == 0) RBF_GJ_LAUNCH(8, 4);
         else if (bin == 1) RBF_GJ_LAUNCH(12, 6);
         else RBF_GJ_LAUNCH(14, 7);
@@ -920,6 +1058,10 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
   const int64_t ws_limit = (int64_t)16 << 30;  // fp64 LU workspace bytes per chunk
   DevBuf w64;                                  // fp64 W of the big blocks when W is fp32
   std::vector<int64_t> trip;
+  if (P->w_fp32 && P->w_sym) {
+    big_w = 0;   // the fp64 staging holds full m x m inverses
+    for (int64_t b : big) big_w += (h_ext_ptr[b + 1] - h_ext_ptr[b]) * (h_ext_ptr[b + 1] - h_ext_ptr[b]);
+  }
   if (P->w_fp32 && !big.empty()) RBF_TRY(w64.alloc(sizeof(double) * (size_t)big_w, s));
   std::vector<LuJob> jobs;
   size_t bi = 0;
@@ -935,7 +1077,7 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
       if (!jobs.empty() && (used + need) * (int64_t)sizeof(FT) > ws_limit) break;
       int64_t wo = h_w_off[b];
       if (P->w_fp32) {
-        trip.insert(trip.end(), {tmp_off, h_w_off[b], (int64_t)m * nc});
+        trip.insert(trip.end(), {tmp_off, h_w_off[b], (int64_t)m * nc, P->w_sym ? (int64_t)m : 0});
         wo = tmp_off;
         tmp_off += (int64_t)m * nc;
       }
@@ -957,7 +1099,7 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
   }
   if (!trip.empty()) {
     DevBuf trip_d;
-    const int64_t nt = (int64_t)trip.size() / 3;
+    const int64_t nt = (int64_t)trip.size() / 4;
     RBF_TRY(trip_d.alloc(8 * trip.size(), s));
     RBF_CUDA_TRY(cudaMemcpyAsync(trip_d.p, trip.data(), 8 * trip.size(), cudaMemcpyHostToDevice, s));
     round_w_kernel<<<(unsigned)std::min<int64_t>(nt, 4096), 256, 0, s>>>(trip_d.as<int64_t>(), nt,
@@ -993,6 +1135,31 @@ rbf_status precond_apply_sorted(rbf_ctx* ctx, const rbf_precond* P, const VT* r,
   }
   const int blocks = (int)std::min<int64_t>(P->nblocks, (int64_t)ctx->sm_count * 16);
   const size_t smem = sizeof(double) * (size_t)P->max_m;
+  if (P->w_sym) {
+    // two staging buffers of up to cap floats per CTA (RBF_APPLY_CAP); larger
+    // triangles are read from global
+    static const int cap_env = std::getenv("RBF_APPLY_CAP") ? std::atoi(std::getenv("RBF_APPLY_CAP")) : 6144;
+    static const int thr_env = std::getenv("RBF_APPLY_SYM_THREADS") ? std::atoi(std::getenv("RBF_APPLY_SYM_THREADS")) : 128;
+    const int cap = (int)std::min<int64_t>(P->max_wblk, cap_env) & ~3;
+    // one CTA per block (default; many small CTAs per SM overlap the gather ->
+    // copy -> multiply latency chain of each block) or, RBF_APPLY_PERSIST=1,
+    // occupancy-sized persistent CTAs with a second stage prefetching the next block
+    static const bool persist = std::getenv("RBF_APPLY_PERSIST") != nullptr;
+    const size_t smems = sizeof(float) * ((size_t)((P->max_m + 3) & ~3) + (persist ? 2 : 1) * (size_t)cap);
+    if (smems > 48 * 1024)
+      RBF_CUDA_TRY(cudaFuncSetAttribute(apply_sym_kernel<VT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smems));
+    int per_sm = 0;
+    RBF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_sym_kernel<VT>, thr_env, smems));
+    const int64_t grid =
+        persist ? std::min<int64_t>(P->nblocks, (int64_t)ctx->sm_count * std::max(per_sm, 1)) : P->nblocks;
+    ProfScope ps(ctx, RBF_PROF_PRECOND_APPLY);
+    apply_sym_kernel<VT><<<(unsigned)grid, thr_env, smems, s>>>(P->ext_ptr.as<int64_t>(), P->ext_idx.as<int32_t>(),
+                                                               P->w_off.as<int64_t>(), P->W.as<float>(), r, z,
+                                                               P->nblocks, cap, P->max_m);
+    RBF_CHECK_LAUNCH();
+    return RBF_OK;
+  }
   if (P->w_fp32) {
     const size_t smemf = sizeof(float) * (size_t)P->max_m;
     if (smemf > 48 * 1024)

@@ -14,6 +14,8 @@ struct rbf_precond {
   double shift = 0.0;     // diagonal shift of the local matrices, units of the amplitude a
   bool w_fp32 = false;    // W stored in fp32 (local_fp32)
   int64_t gj_blocks = 0;  // blocks inverted on chip in fp32 (the rest by the fp64 batched LU)
+  bool w_sym = false;     // W_i stored as packed lower triangles (block-Jacobi, fp32 W: W_i = B_i^-1 symmetric)
+  int64_t max_wblk = 0;   // floats of the largest W_i
   double t_setup = 0.0;
   const rbf_cells* cells = nullptr;
   rbf::DevBuf core_ptr;   // int64[nblocks+1]
@@ -21,7 +23,8 @@ struct rbf_precond {
   rbf::DevBuf core_idx;   // int32[n]           sorted positions, block-major
   rbf::DevBuf ext_idx;    // int32[ext_ptr[nb]] sorted positions: [extra ascending] + [core]
   rbf::DevBuf w_off;      // int64[nblocks+1]   float offsets of W_i
-  rbf::DevBuf W;          // fp64 or fp32 (w_fp32): W_i (nc_i x m_i) row-major = (B_i^-1)[core, :],
+  rbf::DevBuf W;          // fp64 or fp32 (w_fp32): W_i (nc_i x m_i) row-major = (B_i^-1)[core, :]
+                          // (w_sym: row i of the lower triangle at i(i+1)/2, blocks padded to 4 floats),
                           // B_i = A_ext + shift*a*I
   std::vector<int64_t> h_core_ptr, h_ext_ptr;
 };

@@ -130,12 +130,15 @@ def _flat_cap(ratio=3.0, n_sphere=6000, zcut=0.55):
     return X, b, sigma
 
 
-@pytest.mark.parametrize("core,pivot", [(128, False), (256, False), (128, True)])
-def test_gj_fp32_apply_parity(R, ctx, core, pivot):
+@pytest.mark.parametrize("core,pivot,full", [(128, False, False), (256, False, False), (128, True, False),
+                                             (256, False, True)])
+def test_gj_fp32_apply_parity(R, ctx, core, pivot, full):
     """Reading R17, on-chip fp32 Gauss-Jordan factors (local_fp32=1) against the
     oracle's fp64 LU of the same shifted blocks.  Bound: the fp32 inverse of B
     carries a relative error <= c kappa(B) m u32 (u32 = 2^-24); kappa(B) is
-    computed here from the oracle's blocks, c = 4."""
+    computed here from the oracle's blocks, c = 4.  W_i = B_i^-1 is symmetric and
+    stored as packed lower triangles (read through the bulk-copy staging, or from
+    global for blocks above the staging size); RBF_APPLY_FULL keeps full rows."""
     import os
     X, _, sigma = _flat_cap()
     mu = 0.01
@@ -144,10 +147,13 @@ def test_gj_fp32_apply_parity(R, ctx, core, pivot):
     # mu >= 1e-4 eliminates without pivoting (B_i SPD); RBF_GJ_PIVOT forces partial pivoting
     if pivot:
         os.environ["RBF_GJ_PIVOT"] = "1"
+    if full:
+        os.environ["RBF_APPLY_FULL"] = "1"
     try:
         P = R.Precond(ctx, cells, kern, kind=1, core_target=core, shift=mu, local_fp32=1)
     finally:
         os.environ.pop("RBF_GJ_PIVOT", None)
+        os.environ.pop("RBF_APPLY_FULL", None)
     cores, exts, nbytes = P.blocks()
     oc = OC.build(X, 6 * sigma, cell_edge=6 * sigma / 3.999)
     blocks = OS.ras_blocks(oc, sigma, core, 0.0)
@@ -158,8 +164,17 @@ def test_gj_fp32_apply_parity(R, ctx, core, pivot):
         assert min(ms) <= 224 < max(ms), (min(ms), max(ms))
     assert len(cores) == len(blocks)
     assert all(np.array_equal(c, b_["core"]) for c, b_ in zip(cores, blocks))
-    # W is fp32: bytes = 4 * sum m^2 (+ index arrays)
-    assert nbytes < 8 * sum(len(e) ** 2 for e in exts)
+    # W is fp32: bytes = 4 * sum m^2, packed 4 * sum m (m + 1) / 2 (+ index arrays)
+    ms = [len(e) for e in exts]
+    wfull = 4 * sum(m * m for m in ms)
+    wtri = 4 * sum((m * (m + 1) // 2 + 3) // 4 * 4 for m in ms)
+    extra = 32 * (len(X) + len(ms) + 1)
+    if full:
+        assert wfull <= nbytes <= wfull + extra
+    else:
+        assert wtri <= nbytes <= wtri + extra
+        if core == 256:
+            assert max(m * (m + 1) // 2 for m in ms) > 10240     # some blocks read W from global
     a = OK.amplitude(sigma)
     kappa, mmax = 0.0, 0
     for blk in blocks:
