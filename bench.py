@@ -199,16 +199,20 @@ def run_ours(args, rank, world, local):
                     core_target=cfg.core_target, overlap_sigmas=cfg.overlap_sigmas, shift=cfg.shift,
                     local_fp32=cfg.local_fp32, cgs_passes=cfg.cgs_passes, max_iters=args.fit_iters)
 
+    # cell edge of the config (RBF_BENCH_CELL_DIV overrides, for sweeps)
+    cell_edge = kern.sigma * kern.cutoff_sigmas / float(os.environ.get("RBF_BENCH_CELL_DIV", cfg.cell_div))
+    solve_kw["cell_edge"] = cell_edge
+
     def step():
         centres, b = R.extend_points(ctx, x, nrm, d["delta"])
-        cells = R.Cells(ctx, centres, kern)
-        w, rep = R.gmres_solve(ctx, cells, kern, b, **solve_kw)
+        cells = R.Cells(ctx, centres, kern, cell_edge=cell_edge)
+        w, rep = R.gmres_solve(ctx, cells, kern, b, **{k: v for k, v in solve_kw.items() if k != "cell_edge"})
         field = R.eval_grid(ctx, cells, kern, w, lo, hi, gn)
         return cells, w, field, rep
 
     # pair accounting (outside the timed region): useful pairs per matvec and per grid pass
     centres, b = R.extend_points(ctx, x, nrm, d["delta"])
-    cells = R.Cells(ctx, centres, kern)
+    cells = R.Cells(ctx, centres, kern, cell_edge=cell_edge)
     useful_mv, visited_mv = R.matvec_pairs(ctx, cells, kern)
     useful_grid = R.eval_grid_pairs(ctx, cells, kern, lo, hi, gn)
     info = cells.info()

@@ -33,6 +33,7 @@ class Config:
     shift: float = 0.0        # local diagonal shift in units of a (reading R17)
     local_fp32: int = 0       # fp32 on-chip local inverses (reading R17)
     cgs_passes: int = 2       # Gram-Schmidt passes per Arnoldi step (1: CGS, 2: CGS2)
+    cell_div: float = 3.999   # cell edge = cutoff / cell_div (the library default)
     kw: dict = field(default_factory=dict)
 
 
