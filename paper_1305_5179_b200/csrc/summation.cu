@@ -768,6 +768,42 @@ sum_f32_symw_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const flo
 }
 
 // ------------------------------------------------------------- fp64 tier ---
+// exp(x) for the fp64 tier's arguments x = -d2 / (2 sigma^2), table-driven:
+// n = rint(64 x log2 e) (the 1.5 2^52 rounding trick), x = (n/64) ln2 + r with
+// |r| <= ln2/128 (two-part ln2/64: the high part has 32 significant bits, so
+// n (ln2/64)_hi is exact for |n| < 2^20), e^x = 2^(n>>6) * 2^((n&63)/64) * e^r,
+// 2^(j/64) from a 64-entry shared-memory table (exp2 at CTA start, <= 1 ulp),
+// e^r by its degree-5 Taylor polynomial (truncation < 4e-17 relative), 2^(n>>6)
+// added to the exponent field: 10 DP operations.  Valid (normal results) for x
+// in [-700, 0]; the kernels only keep x >= -k c^2 = -18 at 6 sigma (pairs beyond
+// the cutoff are computed and discarded by a select).  No range checks, no
+// branches; every coefficient is a constant-bank (uniform) operand.
+struct ExpConst {
+  double log2e64, magic, ln2_hi64, ln2_lo64;
+  double c[6];   // 1 / k!
+};
+__constant__ ExpConst kExp64 = {64 * 1.4426950408889634, 6755399441055744.0, 6.93147180369123816490e-01 / 64,
+                                1.90821492927058770002e-10 / 64,
+                                {1.0, 1.0, 1.0 / 2, 1.0 / 6, 1.0 / 24, 1.0 / 120}};
+constexpr int kExpTab = 64;
+
+__device__ __forceinline__ void exp_tier64_table(double* tab) {
+  for (int k = threadIdx.x; k < kExpTab; k += blockDim.x) tab[k] = exp2((double)k * (1.0 / kExpTab));
+}
+
+__device__ __forceinline__ double exp_tier64(double x, const double* __restrict__ tab) {
+  const double t = __fma_rn(x, kExp64.log2e64, kExp64.magic);
+  const double nd = __dsub_rn(t, kExp64.magic);
+  const int n = __double2loint(t);
+  double r = __fma_rn(-nd, kExp64.ln2_hi64, x);
+  r = __fma_rn(-nd, kExp64.ln2_lo64, r);
+  double p = kExp64.c[5];
+#pragma unroll
+  for (int k = 4; k >= 0; --k) p = __fma_rn(p, r, kExp64.c[k]);
+  p = __dmul_rn(p, tab[n & (kExpTab - 1)]);
+  return __hiloint2double(__double2hiint(p) + ((n >> 6) << 20), __double2loint(p));
+}
+
 struct Ring64 {
   float* bx; float* by; float* bz; double* bw;
 };
@@ -805,6 +841,7 @@ struct Flush64 {
   double* acc;                       // [2]
   const double* xt; const double* yt; const double* zt;
   double c2, nis;                    // cutoff^2 and -1/(2 sigma^2); the amplitude is applied at the end
+  const double* tab;                 // exp_tier64 table (shared memory)
   __device__ __forceinline__ void operator()(int cnt) {
     for (int j = 0; j < cnt; ++j) {
       const double sx = (double)r.bx[j], sy = (double)r.by[j], sz = (double)r.bz[j], wj = r.bw[j];
@@ -814,7 +851,8 @@ struct Flush64 {
         double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
         // predicated (no divergent branch); exp(-d2/(2 sigma^2)) as a product by
         // the reciprocal: <= 1 ulp of the argument, ~1e-15 relative in the entry
-        const double e = exp(__dmul_rn(d2, nis));
+        // (exp_tier64: a few ulp)
+        const double e = exp_tier64(__dmul_rn(d2, nis), tab);
         acc[t] = __fma_rn(d2 <= c2 ? e : 0.0, wj, acc[t]);
       }
     }
@@ -828,6 +866,9 @@ sum_f64_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
                const int32_t* __restrict__ out_perm, int* __restrict__ work) {
   __shared__ __align__(16) float ringf[kSumWarps][3][kBufPad];
   __shared__ __align__(16) double ringd[kSumWarps][kBufPad];
+  __shared__ double etab[kExpTab];
+  exp_tier64_table(etab);
+  __syncthreads();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   Ring64 R{ringf[wib][0], ringf[wib][1], ringf[wib][2], ringd[wib]};
   for (;;) {
@@ -854,7 +895,7 @@ sum_f64_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
       xt[t] = p.x; yt[t] = p.y; zt[t] = p.z;
     }
     Stage64 st{R, src, w, blo, bhi, G.cc2, make_float4(0, 0, 0, 0), 0.0};
-    Flush64 fl{R, acc, xt, yt, zt, G.c2d, -1.0 / G.two_s2};
+    Flush64 fl{R, acc, xt, yt, zt, G.c2d, -1.0 / G.two_s2, etab};
     int nbuf = 0;
     traverse(G, cell_start, blo, bhi, lane, st, fl, nbuf);
     __syncwarp();
@@ -925,6 +966,7 @@ struct Flush64x {
   double c2, nis, amp;
   double* out;
   int lane;
+  const double* tab;                 // exp_tier64 table (shared memory)
   __device__ __forceinline__ void operator()(int cnt) {
     for (int j = 0; j < cnt; ++j) {
       const double sx = (double)r.bx[j], sy = (double)r.by[j], sz = (double)r.bz[j], wj = r.bw[j];
@@ -933,7 +975,9 @@ struct Flush64x {
       for (int t = 0; t < 2; ++t) {
         double dx = __dsub_rn(sx, xt[t]), dy = __dsub_rn(sy, yt[t]), dz = __dsub_rn(sz, zt[t]);
         double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-        const double e = d2 <= c2 ? exp(__dmul_rn(d2, nis)) : 0.0;
+        // computed for every staged pair and selected (no divergent branch)
+        const double ex = exp_tier64(__dmul_rn(d2, nis), tab);
+        const double e = d2 <= c2 ? ex : 0.0;
         acc[t] = __fma_rn(e, wj, acc[t]);
         if (SYM) pj = __fma_rn(e, wt[t], pj);
       }
@@ -954,6 +998,9 @@ sum_f64_sym_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const floa
   __shared__ __align__(16) float ringf[kSumWarps][6][kBufPad];
   __shared__ __align__(16) double ringd[kSumWarps][2][kBufPad];
   __shared__ __align__(16) int ringi[kSumWarps][kBufPad];
+  __shared__ double etab[kExpTab];
+  exp_tier64_table(etab);
+  __syncthreads();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   Ring64s RB{ringf[wib][0], ringf[wib][1], ringf[wib][2], ringd[wib][0], ringi[wib]};
   Ring64s RI{ringf[wib][3], ringf[wib][4], ringf[wib][5], ringd[wib][1], nullptr};
@@ -984,8 +1031,8 @@ sum_f64_sym_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const floa
     Stage64x2 st{RB, RI, src, w, blo, bhi, G.cc2, (int)own_lo, tl.x, tl.x + tl.y, (int)own_hi,
                  make_float4(0, 0, 0, 0), 0.0, 0};
     const double nis = -1.0 / G.two_s2;
-    Flush64x<true> fs{RB, acc, xt, yt, zt, wt, G.c2d, nis, G.ampd, out, lane};
-    Flush64x<false> fi{RI, acc, xt, yt, zt, wt, G.c2d, nis, G.ampd, out, lane};
+    Flush64x<true> fs{RB, acc, xt, yt, zt, wt, G.c2d, nis, G.ampd, out, lane, etab};
+    Flush64x<false> fi{RI, acc, xt, yt, zt, wt, G.c2d, nis, G.ampd, out, lane, etab};
     int nB = 0, nI = 0;
     traverse2(G, cell_start, blo, bhi, lane, st, fs, fi, nB, nI, st.skip_lo, st.skip_hi);
     __syncwarp();
