@@ -75,10 +75,14 @@ class Clocks:
         self.p = None
 
     def start(self):
+        """Start the sampler and wait for its first (pre-timing, discarded) sample:
+        nvidia-smi's start-up (NVML init, driver queries) stays out of the timed
+        region, the samples read at stop() are all taken during it."""
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "200"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.p.stdout.readline()
         except OSError:
             self.p = None
 
