@@ -236,12 +236,23 @@ def run_ours(args, rank, world, local):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     reps = []
     launches0 = R.launch_count()
+    trace = os.environ.get("RBF_BENCH_TRACE") is not None
+    evs = []
     e0.record(s)
     for _ in range(args.steps):
         _, w, field, rep = step()
         reps.append(rep)
+        if trace:
+            evs.append((torch.cuda.Event(enable_timing=True), time.perf_counter()))
+            evs[-1][0].record(s)
     e1.record(s)
     torch.cuda.synchronize()
+    if trace:   # per-step device / host times (diagnostics, stderr)
+        prev_e, prev_h = e0, None
+        for ev, th in evs:
+            print(f"[bench trace] step {prev_e.elapsed_time(ev):.1f} ms (device)"
+                  + (f", {1e3 * (th - prev_h):.1f} ms (host)" if prev_h else ""), file=sys.stderr)
+            prev_e, prev_h = ev, th
     launches = R.launch_count() - launches0
     ms = e0.elapsed_time(e1)
     if world > 1:
