@@ -346,7 +346,7 @@ constexpr double kNoPivShift = 1e-4;
 constexpr int kGjThreads = 512;
 
 template <int RM, int RC, bool PIV>
-__global__ void __launch_bounds__(kGjThreads, (RM * RC <= 32) ? 2 : 1)
+__global__ void __launch_bounds__(kGjThreads, (RM * RC <= 8) ? 4 : (RM * RC <= 18) ? 3 : (RM * RC <= 32) ? 2 : 1)
 gj_inverse_f32_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __restrict__ core_ptr,
                       const int32_t* __restrict__ ext_idx, const int64_t* __restrict__ w_off,
                       const float4* __restrict__ sorted, double amp, double two_s2, double c2,
@@ -1023,33 +1023,44 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
   }
   DevBuf blist;
   if (!small.empty()) {
-    // bins by m: register tiles 128 (8x4), 192 (12x6), 224 (14x7)
+    // sorted by m for the size bins below
     std::stable_sort(small.begin(), small.end(), [&](int64_t x, int64_t y) {
       return (h_ext_ptr[x + 1] - h_ext_ptr[x]) < (h_ext_ptr[y + 1] - h_ext_ptr[y]);
     });
     RBF_TRY(blist.alloc(8 * small.size(), s));
     RBF_CUDA_TRY(cudaMemcpyAsync(blist.p, small.data(), 8 * small.size(), cudaMemcpyHostToDevice, s));
     size_t lo = 0;
-    const int caps[3] = {128, 192, 224};
+    // size bins: register tiles 64 (4x2), 96 (6x3), 128 (8x4), 192 (12x6), 224 (14x7);
+    // the smaller tiles hold fewer registers, so more CTAs (blocks) per SM
+    // overlap their per-step barrier latency
+    const int caps[5] = {64, 96, 128, 192, 224};
     // shifted SPD blocks need no pivoting (one barrier per elimination step)
     const bool nopiv = shift >= kNoPivShift && std::getenv("RBF_GJ_PIVOT") == nullptr;
-    for (int bin = 0; bin < 3 && lo < small.size(); ++bin) {
+    for (int bin = 0; bin < 5 && lo < small.size(); ++bin) {
       size_t hi = lo;
       while (hi < small.size() && h_ext_ptr[small[hi] + 1] - h_ext_ptr[small[hi]] <= caps[bin]) ++hi;
       const int64_t cnt = (int64_t)(hi - lo);
       if (cnt > 0) {
-        // the 128-row variant fits 64 registers: two CTAs (blocks) per SM overlap their barrier latency
-        const int gblocks = (int)std::min<int64_t>(cnt, (int64_t)ctx->sm_count * (bin == 0 ? 2 : 1));
         const int64_t* bl = blist.as<int64_t>() + lo;
-#define RBF_GJ_LAUNCH(RM_, RC_)                                                                            \
-  (nopiv ? gj_inverse_f32_kernel<RM_, RC_, false> : gj_inverse_f32_kernel<RM_, RC_, true>)<<<gblocks, kGjThreads, 0, s>>>( \
-      P->ext_ptr.as<int64_t>(), P->core_ptr.as<int64_t>(), P->ext_idx.as<int32_t>(), P->w_off.as<int64_t>(), \
-      sorted, kp.amp, two_s2, c2, shift_abs, P->W.as<float>(), bl, cnt, info.as<int>(), P->w_sym)
-        if (bin == 0) RBF_GJ_LAUNCH(8, 4);
-        else if (bin == 1) RBF_GJ_LAUNCH(12, 6);
+        auto launch = [&](auto kern) -> rbf_status {
+          int per_sm = 1;
+          RBF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGjThreads, 0));
+          const int gblocks = (int)std::min<int64_t>(cnt, (int64_t)ctx->sm_count * std::max(per_sm, 1));
+          kern<<<gblocks, kGjThreads, 0, s>>>(P->ext_ptr.as<int64_t>(), P->core_ptr.as<int64_t>(),
+                                              P->ext_idx.as<int32_t>(), P->w_off.as<int64_t>(), sorted, kp.amp,
+                                              two_s2, c2, shift_abs, P->W.as<float>(), bl, cnt, info.as<int>(),
+                                              P->w_sym);
+          RBF_CHECK_LAUNCH();
+          return RBF_OK;
+        };
+#define RBF_GJ_LAUNCH(RM_, RC_) \
+  RBF_TRY(nopiv ? launch(gj_inverse_f32_kernel<RM_, RC_, false>) : launch(gj_inverse_f32_kernel<RM_, RC_, true>))
+        if (bin == 0) RBF_GJ_LAUNCH(4, 2);
+        else if (bin == 1) RBF_GJ_LAUNCH(6, 3);
+        else if (bin == 2) RBF_GJ_LAUNCH(8, 4);
+        else if (bin == 3) RBF_GJ_LAUNCH(12, 6);
         else RBF_GJ_LAUNCH(14, 7);
 #undef RBF_GJ_LAUNCH
-        RBF_CHECK_LAUNCH();
       }
       lo = hi;
     }
