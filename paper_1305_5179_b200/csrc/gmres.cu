@@ -19,6 +19,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "internal.h"
@@ -32,8 +34,9 @@ constexpr int kDotChunk = 8;
 
 // partial[j * nblk + blk] = sum over this block's slice of V_j . w, j in [0, k);
 // blockIdx.y selects the chunk of kDotChunk basis vectors (chunks run in parallel)
+template <class VT>
 __global__ void __launch_bounds__(kVecThreads)
-multi_dot_kernel(const double* __restrict__ V, int64_t ldv, int k, const double* __restrict__ w, int64_t n,
+multi_dot_kernel(const VT* __restrict__ V, int64_t ldv, int k, const double* __restrict__ w, int64_t n,
                  double* __restrict__ partial) {
   __shared__ double red[kVecThreads / 32][kDotChunk];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -46,7 +49,7 @@ multi_dot_kernel(const double* __restrict__ V, int64_t ldv, int k, const double*
     const double wi = w[i];
 #pragma unroll
     for (int q = 0; q < kDotChunk; ++q)
-      if (j0 + q < k) acc[q] = fma(V[(int64_t)(j0 + q) * ldv + i], wi, acc[q]);
+      if (j0 + q < k) acc[q] = fma((double)V[(int64_t)(j0 + q) * ldv + i], wi, acc[q]);
   }
 #pragma unroll
   for (int q = 0; q < kDotChunk; ++q) {
@@ -78,28 +81,31 @@ __global__ void reduce_partials(const double* __restrict__ partial, int k, int n
 }
 
 // w[i] += sum_j coef[j] * V_j[i]
-__global__ void multi_axpy_kernel(double* __restrict__ w, const double* __restrict__ V, int64_t ldv, int k,
+template <class VT>
+__global__ void multi_axpy_kernel(double* __restrict__ w, const VT* __restrict__ V, int64_t ldv, int k,
                                   const double* __restrict__ coef, int64_t n) {
   __shared__ double sc[64];
   for (int q = threadIdx.x; q < k && q < 64; q += blockDim.x) sc[q] = coef[q];
   __syncthreads();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double acc = w[i];
-    for (int j = 0; j < k; ++j) acc = fma(sc[j], V[(int64_t)j * ldv + i], acc);
+    for (int j = 0; j < k; ++j) acc = fma(sc[j], (double)V[(int64_t)j * ldv + i], acc);
     w[i] = acc;
   }
 }
 
-__global__ void scale_kernel(const double* __restrict__ a, double s, double* __restrict__ b, int64_t n) {
+template <class OT>
+__global__ void scale_kernel(const double* __restrict__ a, double s, OT* __restrict__ b, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    b[i] = a[i] * s;
+    b[i] = (OT)(a[i] * s);
 }
 // b = a * (1 / *nrm)  (norm on the device)
+template <class OT>
 __global__ void scale_by_inv_norm(const double* __restrict__ a, const double* __restrict__ nrm2,
-                                  double* __restrict__ b, int64_t n) {
+                                  OT* __restrict__ b, int64_t n) {
   const double s = 1.0 / sqrt(*nrm2);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    b[i] = a[i] * s;
+    b[i] = (OT)(a[i] * s);
 }
 __global__ void residual_kernel(const double* __restrict__ b, const double* __restrict__ f, double* __restrict__ r,
                                 int64_t n) {
@@ -123,12 +129,27 @@ struct Solver {
   int m;
   int nblk;
   DevBuf V, Z, x, r, w, f, b, partial, dots;
+  // fp32 Krylov basis of the fp32 phase (V32, Z32; basis32): the phase works to
+  // a relative residual >= 1e-4 with an operator accurate to ~1e-6, so basis
+  // vectors rounded to fp32 (6e-8) cost nothing it can see; the fp64 phase keeps
+  // V, Z in fp64.  Halves the Krylov vector traffic of the fp32 phase.
+  DevBuf V32, Z32;
+  bool basis32 = true;
   int64_t mv32 = 0, mv64 = 0;
 
+  // the fp64 basis, allocated when a cycle first runs on it
+  rbf_status ensure64() {
+    cudaStream_t s = ctx->stream;
+    if (!V.p) RBF_TRY(V.alloc(sizeof(double) * n * (m + 1), s));
+    if (!Z.p) RBF_TRY(Z.alloc(sizeof(double) * n * m, s));
+    return RBF_OK;
+  }
   rbf_status alloc() {
     cudaStream_t s = ctx->stream;
-    RBF_TRY(V.alloc(sizeof(double) * n * (m + 1), s));
-    RBF_TRY(Z.alloc(sizeof(double) * n * m, s));
+    if (basis32) {
+      RBF_TRY(V32.alloc(sizeof(float) * n * (m + 1), s));
+      RBF_TRY(Z32.alloc(sizeof(float) * n * m, s));
+    }
     RBF_TRY(x.alloc(sizeof(double) * n, s));
     RBF_TRY(r.alloc(sizeof(double) * n, s));
     RBF_TRY(w.alloc(sizeof(double) * n, s));
@@ -139,19 +160,25 @@ struct Solver {
     RBF_TRY(dots.alloc(sizeof(double) * 4 * (m + 2), s));
     return RBF_OK;
   }
-  double* Vj(int j) { return V.as<double>() + (int64_t)j * n; }
-  double* Zj(int j) { return Z.as<double>() + (int64_t)j * n; }
+  template <class VT> VT* basis() { return std::is_same<VT, float>::value ? (VT*)V32.p : (VT*)V.p; }
+  template <class VT> VT* zbasis() { return std::is_same<VT, float>::value ? (VT*)Z32.p : (VT*)Z.p; }
 
   rbf_status op(bool fp64, const double* in, double* out) {
     if (fp64) { ++mv64; return matvec_sorted_f64(ctx, c, kp, in, out, nullptr, true); }
     ++mv32;
     return matvec_sorted_f32_d(ctx, c, kp, in, out, true);
   }
+  rbf_status op(bool fp64, const float* in, double* out) {   // fp32 basis: fp32 phase only
+    if (fp64) { set_error("internal: fp64 operator on an fp32 basis"); return RBF_EINVAL; }
+    ++mv32;
+    return matvec_sorted_f32_f(ctx, c, kp, in, out, true);
+  }
   // dots[0..k) = V_{0..k}^T w ; neg copy at dots[(m+2)...]
-  rbf_status mdot(const double* Vb, int k, const double* vec, double* out, double* neg) {
+  template <class VT>
+  rbf_status mdot(const VT* Vb, int k, const double* vec, double* out, double* neg) {
     cudaStream_t s = ctx->stream;
     const dim3 grid((unsigned)nblk, (unsigned)((k + kDotChunk - 1) / kDotChunk));
-    multi_dot_kernel<<<grid, kVecThreads, 0, s>>>(Vb, n, k, vec, n, partial.as<double>());
+    multi_dot_kernel<VT><<<grid, kVecThreads, 0, s>>>(Vb, n, k, vec, n, partial.as<double>());
     RBF_CHECK_LAUNCH();
     if (ctx->world == 1) {
       reduce_partials<<<k, 32, 0, s>>>(partial.as<double>(), k, nblk, out, neg != nullptr, neg);
@@ -168,8 +195,9 @@ struct Solver {
     }
     return RBF_OK;
   }
-  rbf_status maxpy(double* vec, const double* Vb, int k, const double* coef) {
-    multi_axpy_kernel<<<grid_for(n, kVecThreads), kVecThreads, 0, ctx->stream>>>(vec, Vb, n, k, coef, n);
+  template <class VT>
+  rbf_status maxpy(double* vec, const VT* Vb, int k, const double* coef) {
+    multi_axpy_kernel<VT><<<grid_for(n, kVecThreads), kVecThreads, 0, ctx->stream>>>(vec, Vb, n, k, coef, n);
     RBF_CHECK_LAUNCH();
     return RBF_OK;
   }
@@ -206,6 +234,8 @@ rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp
   const int passes = (gcfg && gcfg->cgs_passes == 1) ? 1 : 2;
   const int64_t n = S.n;
   const int m = S.m;
+  // RBF_GMRES_BASIS64=1: fp64 basis in both phases
+  S.basis32 = std::getenv("RBF_GMRES_BASIS64") == nullptr;
   RBF_TRY(S.alloc());
   f32_to_f64<<<grid_for(n, 256), 256, 0, s>>>(b_sorted32, S.b.as<double>(), n);
   RBF_CHECK_LAUNCH();
@@ -260,67 +290,82 @@ rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp
     last_beta = beta;
     cycle_beta = fp64 ? -1.0 : beta;
     const double target = fp64 ? rtol : std::max(p1tol, rtol);
-    // V0 = r / beta
-    scale_kernel<<<grid_for(n, 256), 256, 0, s>>>(S.r.as<double>(), 1.0 / beta, S.Vj(0), n);
-    RBF_CHECK_LAUNCH();
-    std::fill(g.begin(), g.end(), 0.0);
-    g[0] = beta;
+    // one restart cycle on a basis of type VT (float: fp32 phase with basis32)
     int k = 0;
     bool bd = false;
-    for (int j = 0; j < m; ++j) {
-      RBF_TRY(precond_apply_sorted<double>(ctx, P, S.Vj(j), S.Zj(j)));
-      RBF_TRY(S.op(fp64, S.Zj(j), S.w.as<double>()));
-      double* wv = S.w.as<double>();
-      // classical Gram-Schmidt, one pass or two (CGS2, the default)
-      RBF_TRY(S.mdot(S.V.as<double>(), j + 1, wv, dh, dneg));
-      RBF_TRY(S.maxpy(wv, S.V.as<double>(), j + 1, dneg));
-      if (passes == 2) {
-        RBF_TRY(S.mdot(S.V.as<double>(), j + 1, wv, d2, dneg));
-        RBF_TRY(S.maxpy(wv, S.V.as<double>(), j + 1, dneg));
-      } else {
-        RBF_CUDA_TRY(cudaMemsetAsync(d2, 0, sizeof(double) * (j + 1), s));
-      }
-      RBF_TRY(S.mdot(wv, 1, wv, dn, nullptr));
-      scale_by_inv_norm<<<grid_for(n, 256), 256, 0, s>>>(wv, dn, S.Vj(j + 1), n);
+    auto cycle = [&](auto tag) -> rbf_status {
+      using VT = decltype(tag);
+      VT* Vb = S.basis<VT>();
+      VT* Zb = S.zbasis<VT>();
+      auto Vj = [&](int j) { return Vb + (int64_t)j * n; };
+      auto Zj = [&](int j) { return Zb + (int64_t)j * n; };
+      // V0 = r / beta
+      scale_kernel<VT><<<grid_for(n, 256), 256, 0, s>>>(S.r.as<double>(), 1.0 / beta, Vj(0), n);
       RBF_CHECK_LAUNCH();
-      RBF_CUDA_TRY(cudaMemcpyAsync(hcol.data(), dh, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, s));
-      std::vector<double> h2(j + 1);
-      double hn2 = 0;
-      RBF_CUDA_TRY(cudaMemcpyAsync(h2.data(), d2, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, s));
-      RBF_CUDA_TRY(cudaMemcpyAsync(&hn2, dn, sizeof(double), cudaMemcpyDeviceToHost, s));
-      RBF_CUDA_TRY(cudaStreamSynchronize(s));
-      for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = hcol[i] + h2[i];
-      const double hn = std::sqrt(hn2);
-      H[(size_t)(j + 1) * m + j] = hn;
-      for (int i = 0; i < j; ++i) {
-        const double a = H[(size_t)i * m + j], bb = H[(size_t)(i + 1) * m + j];
-        H[(size_t)i * m + j] = cs[i] * a + sn[i] * bb;
-        H[(size_t)(i + 1) * m + j] = -sn[i] * a + cs[i] * bb;
+      std::fill(g.begin(), g.end(), 0.0);
+      g[0] = beta;
+      for (int j = 0; j < m; ++j) {
+        RBF_TRY(precond_apply_sorted<VT>(ctx, P, Vj(j), Zj(j)));
+        RBF_TRY(S.op(fp64, (const VT*)Zj(j), S.w.as<double>()));
+        double* wv = S.w.as<double>();
+        // classical Gram-Schmidt, one pass or two (CGS2, the default)
+        RBF_TRY(S.mdot<VT>(Vb, j + 1, wv, dh, dneg));
+        RBF_TRY(S.maxpy<VT>(wv, Vb, j + 1, dneg));
+        if (passes == 2) {
+          RBF_TRY(S.mdot<VT>(Vb, j + 1, wv, d2, dneg));
+          RBF_TRY(S.maxpy<VT>(wv, Vb, j + 1, dneg));
+        } else {
+          RBF_CUDA_TRY(cudaMemsetAsync(d2, 0, sizeof(double) * (j + 1), s));
+        }
+        RBF_TRY(S.mdot<double>(wv, 1, wv, dn, nullptr));
+        scale_by_inv_norm<VT><<<grid_for(n, 256), 256, 0, s>>>(wv, dn, Vj(j + 1), n);
+        RBF_CHECK_LAUNCH();
+        RBF_CUDA_TRY(cudaMemcpyAsync(hcol.data(), dh, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, s));
+        std::vector<double> h2(j + 1);
+        double hn2 = 0;
+        RBF_CUDA_TRY(cudaMemcpyAsync(h2.data(), d2, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, s));
+        RBF_CUDA_TRY(cudaMemcpyAsync(&hn2, dn, sizeof(double), cudaMemcpyDeviceToHost, s));
+        RBF_CUDA_TRY(cudaStreamSynchronize(s));
+        for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = hcol[i] + h2[i];
+        const double hn = std::sqrt(hn2);
+        H[(size_t)(j + 1) * m + j] = hn;
+        for (int i = 0; i < j; ++i) {
+          const double a = H[(size_t)i * m + j], bb = H[(size_t)(i + 1) * m + j];
+          H[(size_t)i * m + j] = cs[i] * a + sn[i] * bb;
+          H[(size_t)(i + 1) * m + j] = -sn[i] * a + cs[i] * bb;
+        }
+        const double a = H[(size_t)j * m + j], bb = H[(size_t)(j + 1) * m + j];
+        const double den = std::hypot(a, bb);
+        cs[j] = den > 0 ? a / den : 1.0;
+        sn[j] = den > 0 ? bb / den : 0.0;
+        H[(size_t)j * m + j] = den;
+        H[(size_t)(j + 1) * m + j] = 0.0;
+        g[j + 1] = -sn[j] * g[j];
+        g[j] = cs[j] * g[j];
+        ++it;
+        if (fp64) ++it2; else ++it1;
+        k = j + 1;
+        est = std::fabs(g[j + 1]) / bnorm;
+        if (!(hn > 1e-14 * beta) || !std::isfinite(hn)) { bd = true; break; }
+        if (est <= target || it >= maxit) break;
       }
-      const double a = H[(size_t)j * m + j], bb = H[(size_t)(j + 1) * m + j];
-      const double den = std::hypot(a, bb);
-      cs[j] = den > 0 ? a / den : 1.0;
-      sn[j] = den > 0 ? bb / den : 0.0;
-      H[(size_t)j * m + j] = den;
-      H[(size_t)(j + 1) * m + j] = 0.0;
-      g[j + 1] = -sn[j] * g[j];
-      g[j] = cs[j] * g[j];
-      ++it;
-      if (fp64) ++it2; else ++it1;
-      k = j + 1;
-      est = std::fabs(g[j + 1]) / bnorm;
-      if (!(hn > 1e-14 * beta) || !std::isfinite(hn)) { bd = true; break; }
-      if (est <= target || it >= maxit) break;
+      // y = H^-1 g, x += Z y
+      for (int i = k - 1; i >= 0; --i) {
+        double acc = g[i];
+        for (int q = i + 1; q < k; ++q) acc -= H[(size_t)i * m + q] * y[q];
+        const double dd = H[(size_t)i * m + i];
+        y[i] = dd != 0 ? acc / dd : 0.0;
+      }
+      RBF_CUDA_TRY(cudaMemcpyAsync(dneg, y.data(), sizeof(double) * k, cudaMemcpyHostToDevice, s));
+      RBF_TRY(S.maxpy<VT>(S.x.as<double>(), Zb, k, dneg));
+      return RBF_OK;
+    };
+    if (!fp64 && S.basis32) {
+      RBF_TRY(cycle(0.0f));
+    } else {
+      RBF_TRY(S.ensure64());
+      RBF_TRY(cycle(0.0));
     }
-    // y = H^-1 g, x += Z y
-    for (int i = k - 1; i >= 0; --i) {
-      double acc = g[i];
-      for (int q = i + 1; q < k; ++q) acc -= H[(size_t)i * m + q] * y[q];
-      const double dd = H[(size_t)i * m + i];
-      y[i] = dd != 0 ? acc / dd : 0.0;
-    }
-    RBF_CUDA_TRY(cudaMemcpyAsync(dneg, y.data(), sizeof(double) * k, cudaMemcpyHostToDevice, s));
-    RBF_TRY(S.maxpy(S.x.as<double>(), S.Z.as<double>(), k, dneg));
     ++R.restarts;
     if (bd) breakdown_any = true;
     RBF_TRY(S.residual(fp64, &beta));

@@ -27,6 +27,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <algorithm>
+#include <type_traits>
 
 #include "internal.h"
 #include "solver.h"
@@ -1154,21 +1155,27 @@ rbf_status matvec_sorted_f32(rbf_ctx* ctx, const rbf_cells* c, const KernelParam
 // order, fp64).  The source window [h0, h1) is assembled by the halo exchange
 // (world > 1); the kernel indexes sources and targets by global sorted
 // position, so the window and output pointers are shifted by h0 and o0.
-rbf_status matvec_sorted_f32_d(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp, const double* w_loc,
-                               double* f_loc, bool solver) {
+template <class WT>
+static rbf_status matvec_f32_solver(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp, const WT* w_loc,
+                                    double* f_loc, bool solver) {
   cudaStream_t s = ctx->stream;
   const SlabView& V = c->view;
   const int64_t nw = V.h1 - V.h0;
-  const double* w_win = w_loc;
+  const WT* w_win = w_loc;
   if (ctx->world > 1 || c->emulated) {
-    RBF_TRY(ctx->win.ensure(sizeof(double) * std::max<int64_t>(nw, 1), s));
-    RBF_TRY(halo_exchange<double>(ctx, c, w_loc, ctx->win.as<double>()));
-    w_win = ctx->win.as<double>();
+    RBF_TRY(ctx->win.ensure(sizeof(WT) * std::max<int64_t>(nw, 1), s));
+    RBF_TRY(halo_exchange<WT>(ctx, c, w_loc, ctx->win.as<WT>()));
+    w_win = ctx->win.as<WT>();
   }
   RBF_TRY(ctx->src4.ensure(sizeof(float4) * std::max<int64_t>(nw, 1), s));
   RBF_TRY(ctx->counter.ensure(256, s));
   if (nw > 0) {
-    pack_src_f64w<<<grid_for(nw, 256), 256, 0, s>>>(c->sorted.as<float4>() + V.h0, w_win, nw, ctx->src4.as<float4>());
+    if constexpr (std::is_same<WT, double>::value)
+      pack_src_f64w<<<grid_for(nw, 256), 256, 0, s>>>(c->sorted.as<float4>() + V.h0, w_win, nw,
+                                                      ctx->src4.as<float4>());
+    else
+      pack_src_f32<<<grid_for(nw, 256), 256, 0, s>>>(c->sorted.as<float4>() + V.h0, w_win, nw,
+                                                     ctx->src4.as<float4>());
     RBF_CHECK_LAUNCH();
   }
   RBF_CUDA_TRY(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
@@ -1203,6 +1210,15 @@ rbf_status matvec_sorted_f32_d(rbf_ctx* ctx, const rbf_cells* c, const KernelPar
       V.t1 - V.t0, V.t0, gd, f_loc - V.o0, nullptr, ctx->counter.as<int>(), nullptr);
   RBF_CHECK_LAUNCH();
   return RBF_OK;
+}
+
+rbf_status matvec_sorted_f32_d(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp, const double* w_loc,
+                               double* f_loc, bool solver) {
+  return matvec_f32_solver<double>(ctx, c, kp, w_loc, f_loc, solver);
+}
+rbf_status matvec_sorted_f32_f(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp, const float* w_loc,
+                               double* f_loc, bool solver) {
+  return matvec_f32_solver<float>(ctx, c, kp, w_loc, f_loc, solver);
 }
 
 // fp64 tier, same conventions as matvec_sorted_f32_d; out_perm (single GPU,
