@@ -398,3 +398,28 @@ def test_cgs1_and_cgs2_reach_the_gate(R, ctx):
                                overlap_sigmas=1.3, max_iters=400, cgs_passes=passes)
         res = np.linalg.norm(b - OK.matvec(X, host(w), sigma)) / np.linalg.norm(b)
         assert rep["converged"] == 1 and res <= 1.5e-6, (passes, res, rep)
+
+
+def test_fp32_phase_basis_matches_fp64_basis(R, ctx):
+    """The fp32 phase keeps its Krylov basis (V, Z) in fp32 (gmres.cu; the phase
+    stops at a relative residual >= 1e-4, far above the 6e-8 rounding of the
+    basis); RBF_GMRES_BASIS64=1 keeps it in fp64.  Both reach the 1e-6 gate,
+    certified by the oracle, with fp32-phase iteration counts within 2."""
+    import os
+    d, X, b = problem("c2", n=3000)
+    sigma = d["sigma"]
+    kern = R.Kernel(sigma)
+    cells = R.Cells(ctx, dev(X, torch.float32), kern)
+    reps = {}
+    for basis in ("32", "64"):
+        if basis == "64":
+            os.environ["RBF_GMRES_BASIS64"] = "1"
+        try:
+            w, rep = R.gmres_solve(ctx, cells, kern, dev(b, torch.float32), restart=50, rtol=1e-6,
+                                   core_target=512, overlap_sigmas=1.3, max_iters=400, cgs_passes=1)
+        finally:
+            os.environ.pop("RBF_GMRES_BASIS64", None)
+        res = np.linalg.norm(b - OK.matvec(X, host(w), sigma)) / np.linalg.norm(b)
+        assert rep["converged"] == 1 and res <= 1.5e-6, (basis, res, rep)
+        reps[basis] = rep
+    assert abs(reps["32"]["iters_phase1"] - reps["64"]["iters_phase1"]) <= 2, reps
