@@ -972,6 +972,16 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
     P->max_wblk = std::max(P->max_wblk, wb);
     max_m = std::max(max_m, m);
   }
+  if (P->w_sym && ncore > 0) {
+    // apply staging size: the 95th percentile of the triangles (a few larger
+    // blocks read W from global; a stage sized for the largest would cut the
+    // CTAs per SM for all), at least 6144 floats, at most 16384 (64 KB)
+    std::vector<int64_t> sz(ncore);
+    for (int64_t b = 0; b < ncore; ++b) sz[b] = h_w_off[b + 1] - h_w_off[b];
+    const size_t q = std::min<size_t>((size_t)ncore - 1, (size_t)(0.95 * (double)ncore));
+    std::nth_element(sz.begin(), sz.begin() + q, sz.end());
+    P->cap_w = (int)std::min<int64_t>(std::max<int64_t>(sz[q], 6144), 16384);
+  }
   if (herr0 == 1) { set_error("RAS core larger than the ext-search capacity"); return RBF_EUNSUPPORTED; }
   if (max_m > max_ext || herr0 == 2) {
     set_error("a RAS extended block holds " + std::to_string(max_m) + " centres (> max_ext " +
@@ -1149,9 +1159,9 @@ rbf_status precond_apply_sorted(rbf_ctx* ctx, const rbf_precond* P, const VT* r,
   if (P->w_sym) {
     // two staging buffers of up to cap floats per CTA (RBF_APPLY_CAP); larger
     // triangles are read from global
-    static const int cap_env = std::getenv("RBF_APPLY_CAP") ? std::atoi(std::getenv("RBF_APPLY_CAP")) : 6144;
+    static const int cap_env = std::getenv("RBF_APPLY_CAP") ? std::atoi(std::getenv("RBF_APPLY_CAP")) : 0;
     static const int thr_env = std::getenv("RBF_APPLY_SYM_THREADS") ? std::atoi(std::getenv("RBF_APPLY_SYM_THREADS")) : 128;
-    const int cap = (int)std::min<int64_t>(P->max_wblk, cap_env) & ~3;
+    const int cap = (int)std::min<int64_t>(P->max_wblk, cap_env > 0 ? cap_env : P->cap_w) & ~3;
     // one CTA per block (default; many small CTAs per SM overlap the gather ->
     // copy -> multiply latency chain of each block) or, RBF_APPLY_PERSIST=1,
     // occupancy-sized persistent CTAs with a second stage prefetching the next block

@@ -16,6 +16,7 @@ struct rbf_precond {
   int64_t gj_blocks = 0;  // blocks inverted on chip in fp32 (the rest by the fp64 batched LU)
   bool w_sym = false;     // W_i stored as packed lower triangles (block-Jacobi, fp32 W: W_i = B_i^-1 symmetric)
   int64_t max_wblk = 0;   // floats of the largest W_i
+  int cap_w = 6144;       // apply staging size (floats; w_sym)
   double t_setup = 0.0;
   const rbf_cells* cells = nullptr;
   rbf::DevBuf core_ptr;   // int64[nblocks+1]
