@@ -511,7 +511,7 @@ sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
                const int2* __restrict__ tiles, const float4* __restrict__ tbox, int64_t ntiles, int64_t tile_base,
                GridDesc gd, OutT* __restrict__ out, const int32_t* __restrict__ out_perm,
                int* __restrict__ work, unsigned long long* __restrict__ stats, int64_t own_lo = 0,
-               int64_t own_hi = 0) {
+               int64_t own_hi = 0, const int32_t* __restrict__ tlist = nullptr) {
   __shared__ __align__(16) float ring[kSumWarps][SYM ? 11 : 10][kBufPad];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   // boundary sources (grid) / symmetric sources (SYM matvec)
@@ -527,7 +527,9 @@ sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
       tile = __shfl_sync(0xffffffffu, t0, 0);
     }
     if (tile >= ntiles) break;
-    tile += tile_base;   // this rank's tile range [tile_base, tile_base + ntiles) (slab partition)
+    // this rank's tile range [tile_base, tile_base + ntiles) (slab partition),
+    // or (grid) the list of node blocks within reach of a centre
+    tile = tlist ? (int64_t)tlist[tile] : tile + tile_base;
     float3 blo, bhi;
     float xr[2], yr[2], zr[2];   // raw target coordinates
     bool tv[2];
@@ -1130,6 +1132,46 @@ int sym_mode(int64_t n_loc) {
 
 // Persistent grid: as many CTAs as can be resident (the kernels pull tiles from a
 // work counter, so CTAs beyond one wave would only add tail imbalance).
+// Node blocks (4x4x4 grid nodes) within the culling radius cc of a non-empty
+// cell, in block layers [bz0, bz1): the grid evaluation visits only those (the
+// others hold no centre within the cutoff of any node: exact zeros, written by a
+// memset).  Conservative by one node per side against the rounding of the
+// node coordinates.
+__global__ void mark_node_blocks(const int32_t* __restrict__ cell_start, CellGrid g, float cc, GridDesc gd,
+                                 int bz0, int bz1, uint32_t* __restrict__ flag) {
+  const int64_t ncell = (int64_t)g.dim[0] * g.dim[1] * g.dim[2];
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncell; c += (int64_t)gridDim.x * blockDim.x) {
+    if (cell_start[c + 1] == cell_start[c]) continue;
+    const int ci[3] = {(int)(c % g.dim[0]), (int)((c / g.dim[0]) % g.dim[1]), (int)(c / ((int64_t)g.dim[0] * g.dim[1]))};
+    int b0[3], b1[3];
+    bool empty = false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double lo = (double)g.lo[a] + (double)ci[a] * (double)g.h - (double)cc;
+      const double hi = (double)g.lo[a] + (double)(ci[a] + 1) * (double)g.h + (double)cc;
+      int i0 = (int)floor((lo - gd.lo[a]) / gd.step[a]) - 1, i1 = (int)ceil((hi - gd.lo[a]) / gd.step[a]) + 1;
+      i0 = max(i0, 0);
+      i1 = min(i1, gd.n[a] - 1);
+      if (i0 > i1) empty = true;
+      b0[a] = i0 >> 2;
+      b1[a] = i1 >> 2;
+    }
+    b0[2] = max(b0[2], bz0);
+    b1[2] = min(b1[2], bz1 - 1);
+    if (empty || b0[2] > b1[2]) continue;
+    for (int bz = b0[2]; bz <= b1[2]; ++bz)
+      for (int by = b0[1]; by <= b1[1]; ++by)
+        for (int bx = b0[0]; bx <= b1[0]; ++bx)
+          flag[((int64_t)bz * gd.nb[1] + by) * gd.nb[0] + bx] = 1u;
+  }
+}
+
+__global__ void compact_blocks(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos, int64_t n,
+                               int32_t* __restrict__ list) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n; b += (int64_t)gridDim.x * blockDim.x)
+    if (flag[b]) list[pos[b]] = (int32_t)b;
+}
+
 template <class K>
 int sum_blocks(rbf_ctx* ctx, K kernel) {
   int per_sm = 0;
@@ -1323,17 +1365,44 @@ rbf_status eval_grid_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams
     b0 = per_layer * bz0;
     b1 = per_layer * bz1;
   }
+  // node blocks within reach of a centre (the rest of this rank's layers are
+  // exact zeros): flags -> scan -> list (one host read of the count)
+  ProfScope ps(pair_stats ? nullptr : ctx, RBF_PROF_GRID);
+  const int64_t nbt = per_layer * gd.nb[2];
+  DevBuf flag, pos, list, cnt;
+  RBF_TRY(flag.alloc(4 * (size_t)std::max<int64_t>(nbt, 1), s));
+  RBF_TRY(pos.alloc(4 * (size_t)std::max<int64_t>(nbt, 1), s));
+  RBF_TRY(list.alloc(4 * (size_t)std::max<int64_t>(nbt, 1), s));
+  RBF_TRY(cnt.alloc(4, s));
+  RBF_CUDA_TRY(cudaMemsetAsync(flag.p, 0, 4 * (size_t)nbt, s));
+  const int64_t ncell = (int64_t)c->dim[0] * c->dim[1] * c->dim[2];
+  mark_node_blocks<<<grid_for(ncell, 256), 256, 0, s>>>(c->cell_start.as<int32_t>(), G.g, G.cc, gd,
+                                                         (int)(b0 / per_layer), (int)(b1 / per_layer),
+                                                         flag.as<uint32_t>());
+  RBF_CHECK_LAUNCH();
+  RBF_TRY(exclusive_scan_u32(ctx, flag.as<uint32_t>(), pos.as<uint32_t>(), nbt, cnt.as<uint32_t>()));
+  compact_blocks<<<grid_for(nbt, 256), 256, 0, s>>>(flag.as<uint32_t>(), pos.as<uint32_t>(), nbt,
+                                                     list.as<int32_t>());
+  RBF_CHECK_LAUNCH();
+  uint32_t nact = 0;
+  RBF_CUDA_TRY(cudaMemcpyAsync(&nact, cnt.p, 4, cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  // this rank's node layers [b0, b1) start as zeros; the active blocks overwrite theirs
+  const int64_t n0 = (int64_t)gd.n[0] * gd.n[1];
+  const int64_t k0 = std::min<int64_t>((b0 / per_layer) * 4, gd.n[2]), k1 = std::min<int64_t>((b1 / per_layer) * 4, gd.n[2]);
+  if (k1 > k0 && !pair_stats)
+    RBF_CUDA_TRY(cudaMemsetAsync(field + k0 * n0, 0, sizeof(float) * (size_t)((k1 - k0) * n0), s));
+  if (nact == 0) return RBF_OK;
   if (pair_stats) {
     sum_f32_kernel<1, true, float><<<sum_blocks(ctx, sum_f32_kernel<1, true, float>), kSumWarps * 32, 0, s>>>(
-        G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), nullptr, nullptr, b1 - b0, b0, gd, field, nullptr,
-        ctx->counter.as<int>(), pair_stats);
+        G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), nullptr, nullptr, nact, 0, gd, field, nullptr,
+        ctx->counter.as<int>(), pair_stats, 0, 0, list.as<int32_t>());
     RBF_CHECK_LAUNCH();
     return RBF_OK;
   }
-  ProfScope ps(ctx, RBF_PROF_GRID);
   sum_f32_kernel<1, false, float><<<sum_blocks(ctx, sum_f32_kernel<1, false, float>), kSumWarps * 32, 0, s>>>(
-      G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), nullptr, nullptr, b1 - b0, b0, gd, field, nullptr,
-      ctx->counter.as<int>(), nullptr);
+      G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), nullptr, nullptr, nact, 0, gd, field, nullptr,
+      ctx->counter.as<int>(), nullptr, 0, 0, list.as<int32_t>());
   RBF_CHECK_LAUNCH();
   return RBF_OK;
 }
