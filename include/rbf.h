@@ -90,9 +90,13 @@ typedef struct {
  * inverses bounded when sigma/spacing makes A_i numerically singular (the
  * preconditioner stays an approximation of A^-1 either way; GMRES iterates
  * with the unshifted A).  local_fp32 = 1 factors every block with m <= 224 on
- * chip in fp32 (Gauss-Jordan, partial pivoting) and stores W in fp32; it is
- * accurate only when shift*a dominates fp32 rounding of A_i (shift >= ~1e-4).
- * Larger blocks, and local_fp32 = 0, use the fp64 batched LU and fp64 W. */
+ * chip in fp32 (Gauss-Jordan; without pivoting when shift >= 1e-4, where the
+ * shifted block is symmetric positive definite, with partial pivoting below) and
+ * stores W in fp32 (block-Jacobi: only the lower triangle of the symmetric
+ * W_i = B_i^-1, half the bytes reported by rbf_precond_blocks); it is accurate
+ * only when shift*a dominates fp32 rounding of A_i (shift >= ~1e-4).  Larger
+ * blocks (their fp64 LU inverse rounded into the fp32 W), and local_fp32 = 0,
+ * use the fp64 batched LU; local_fp32 = 0 keeps fp64 W. */
 typedef struct {
   int kind;              /* 0 none, 1 block-Jacobi (overlap 0), 2 RAS */
   int core_target;       /* centres per core (whole cells); <= 0 => 512 */
