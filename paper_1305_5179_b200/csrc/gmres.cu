@@ -264,6 +264,17 @@ rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp
   int stagnant = 0;
   double beta = bnorm, last_beta = bnorm, est = 1.0;
   std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m), hcol(m + 2);
+  // pinned Hessenberg slots (one per Arnoldi step of a cycle) and two events
+  const size_t pstride = (size_t)2 * (m + 2) + 1;
+  RBF_TRY(ctx->pinned(sizeof(double) * pstride * (size_t)m));
+  double* hpin = static_cast<double*>(ctx->hpin);
+  cudaEvent_t ev[2];
+  RBF_CUDA_TRY(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  RBF_CUDA_TRY(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() { cudaEventDestroy(e[0]); cudaEventDestroy(e[1]); }
+  } ev_guard{ev};
   double t_switch = 0.0;
   // r = b (x = 0)
   RBF_CUDA_TRY(cudaMemcpyAsync(S.r.p, S.b.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
@@ -304,7 +315,9 @@ rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp
       RBF_CHECK_LAUNCH();
       std::fill(g.begin(), g.end(), 0.0);
       g[0] = beta;
-      for (int j = 0; j < m; ++j) {
+      // Arnoldi step j on the device; its Hessenberg column lands in pinned
+      // slot j (hcol, pass-2 h, |w|^2) and event ev[j & 1] marks it
+      auto enqueue = [&](int j) -> rbf_status {
         RBF_TRY(precond_apply_sorted<VT>(ctx, P, Vj(j), Zj(j)));
         RBF_TRY(S.op(fp64, (const VT*)Zj(j), S.w.as<double>()));
         double* wv = S.w.as<double>();
@@ -320,14 +333,24 @@ rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp
         RBF_TRY(S.mdot<double>(wv, 1, wv, dn, nullptr));
         scale_by_inv_norm<VT><<<grid_for(n, 256), 256, 0, s>>>(wv, dn, Vj(j + 1), n);
         RBF_CHECK_LAUNCH();
-        RBF_CUDA_TRY(cudaMemcpyAsync(hcol.data(), dh, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, s));
-        std::vector<double> h2(j + 1);
-        double hn2 = 0;
-        RBF_CUDA_TRY(cudaMemcpyAsync(h2.data(), d2, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, s));
-        RBF_CUDA_TRY(cudaMemcpyAsync(&hn2, dn, sizeof(double), cudaMemcpyDeviceToHost, s));
-        RBF_CUDA_TRY(cudaStreamSynchronize(s));
-        for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = hcol[i] + h2[i];
-        const double hn = std::sqrt(hn2);
+        double* slot = hpin + (size_t)j * pstride;
+        RBF_CUDA_TRY(cudaMemcpyAsync(slot, dh, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, s));
+        RBF_CUDA_TRY(cudaMemcpyAsync(slot + (m + 2), d2, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, s));
+        RBF_CUDA_TRY(cudaMemcpyAsync(slot + 2 * (m + 2), dn, sizeof(double), cudaMemcpyDeviceToHost, s));
+        RBF_CUDA_TRY(cudaEventRecord(ev[j & 1], s));
+        return RBF_OK;
+      };
+      // the next step is enqueued BEFORE the host reads this step's column
+      // (it depends only on device data), so the Givens update and the launch
+      // latency overlap the GPU; a step enqueued past a convergence or
+      // breakdown exit is discarded (it touches neither x nor r)
+      RBF_TRY(enqueue(0));
+      for (int j = 0; j < m; ++j) {
+        if (j + 1 < m && it + 1 < maxit) RBF_TRY(enqueue(j + 1));
+        RBF_CUDA_TRY(cudaEventSynchronize(ev[j & 1]));
+        const double* slot = hpin + (size_t)j * pstride;
+        for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = slot[i] + slot[(m + 2) + i];
+        const double hn = std::sqrt(slot[2 * (m + 2)]);
         H[(size_t)(j + 1) * m + j] = hn;
         for (int i = 0; i < j; ++i) {
           const double a = H[(size_t)i * m + j], bb = H[(size_t)(i + 1) * m + j];

@@ -108,11 +108,24 @@ struct rbf_ctx {
     for (auto& r : prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : ev_pool) cudaEventDestroy(e);
     if (aux_stream) cudaStreamDestroy(aux_stream);
+    if (hpin) cudaFreeHost(hpin);
   }
   rbf::DevBuf scratch;       // generic scratch (radix sort, scans)
   rbf::DevBuf counter;       // work counters (int32 x 64)
   rbf::DevBuf stats;         // pair counters (u64 x 4)
   rbf::DevBuf pinned_dummy;
+  // pinned host scratch (GMRES Hessenberg slots), grown on demand
+  void* hpin = nullptr;
+  size_t hpin_bytes = 0;
+  rbf_status pinned(size_t bytes) {
+    if (bytes <= hpin_bytes) return RBF_OK;
+    if (hpin) cudaFreeHost(hpin);
+    hpin = nullptr;
+    hpin_bytes = 0;
+    if (cudaMallocHost(&hpin, bytes) != cudaSuccess) { cudaGetLastError(); return RBF_ENOMEM; }
+    hpin_bytes = bytes;
+    return RBF_OK;
+  }
   // vector workspaces for matvec (sorted order)
   rbf::DevBuf vec_a, vec_b, src4;
   // multi-GPU (dist.cu): NCCL communicator (ncclComm_t), rank, world, halo window
