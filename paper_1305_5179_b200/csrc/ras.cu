@@ -1033,10 +1033,14 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
   }
   DevBuf blist;
   if (!small.empty()) {
-    // sorted by m for the size bins below
-    std::stable_sort(small.begin(), small.end(), [&](int64_t x, int64_t y) {
-      return (h_ext_ptr[x + 1] - h_ext_ptr[x]) < (h_ext_ptr[y + 1] - h_ext_ptr[y]);
-    });
+    // sorted by m (stable counting sort, m <= kGjMax) for the size bins below
+    {
+      std::vector<int64_t> cnt(kGjMax + 2, 0), out(small.size());
+      for (int64_t b : small) ++cnt[h_ext_ptr[b + 1] - h_ext_ptr[b] + 1];
+      for (int q = 1; q <= kGjMax + 1; ++q) cnt[q] += cnt[q - 1];
+      for (int64_t b : small) out[cnt[h_ext_ptr[b + 1] - h_ext_ptr[b]]++] = b;
+      small.swap(out);
+    }
     RBF_TRY(blist.alloc(8 * small.size(), s));
     RBF_CUDA_TRY(cudaMemcpyAsync(blist.p, small.data(), 8 * small.size(), cudaMemcpyHostToDevice, s));
     size_t lo = 0;
