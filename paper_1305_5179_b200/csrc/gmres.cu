@@ -260,7 +260,7 @@ rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp
   }
   bool fp64 = false;
   int it = 0, it1 = 0, it2 = 0;
-  bool converged = false, breakdown_any = false;
+  bool breakdown_any = false;
   int stagnant = 0;
   double beta = bnorm, last_beta = bnorm, est = 1.0;
   std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m), hcol(m + 2);
@@ -290,8 +290,8 @@ rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp
       t_switch = std::chrono::duration<double>(clk::now() - t_start).count();
       RBF_TRY(S.residual(true, &beta));
     }
-    if (fp64 && beta / bnorm <= rtol) { converged = true; break; }
-    if (!polish && beta / bnorm <= rtol) { converged = true; break; }
+    if (fp64 && beta / bnorm <= rtol) break;
+    if (!polish && beta / bnorm <= rtol) break;
     if (it >= maxit) break;
     if (beta >= last_beta * (1 - 1e-12) && it > 0) {
       if (++stagnant >= 3) break;
@@ -403,7 +403,6 @@ rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp
   R.rel_residual_true = tr / bnorm;
   R.rel_residual_est = est;
   R.converged = (R.rel_residual_true <= rtol) ? 1 : 0;
-  (void)converged;
   R.breakdown = breakdown_any ? 1 : 0;
   R.t_phase1 = fp64 ? t_switch : t_end;
   R.t_phase2 = fp64 ? t_end - t_switch : 0.0;

@@ -988,7 +988,7 @@ struct Flush64x {
     return pj;
   }
   __device__ __forceinline__ void operator()(int cnt) {
-    if (SYM) {
+    if constexpr (SYM) {
       // 4 sources at a time (cnt is a multiple of 4: the ring is padded with
       // far-away zero-weight sources), their source-side sums over the warp's
       // 64 targets by a transpose-reduction (12 32-bit shuffles per 4 sources
@@ -1008,9 +1008,9 @@ struct Flush64x {
         k += __shfl_xor_sync(0xffffffffu, k, 1);
         if ((lane & 7) == 0) atomicAdd(out + r.bi[j + mys], amp * k);
       }
-      return;
+    } else {
+      for (int j = 0; j < cnt; ++j) pair(j);
     }
-    for (int j = 0; j < cnt; ++j) pair(j);
   }
 };
 
