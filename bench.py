@@ -350,7 +350,7 @@ def run_ours(args, rank, world, local):
                    "global_centres": 3 * cfg.n if slab else 3 * cfg.n * world,
                    "parallelism": (f"slab x{world} (z cell planes, halo send/recv + allreduce over NCCL)" if slab
                                    else f"replicas x{world} (independent seeded instances)"),
-                   "l2": "working set >> 126 MB L2 (W 30+ GB, Krylov basis 2.4 GB); no explicit flush"},
+                   "l2": "working set >> 126 MB L2 (block inverses 0.5 GB, Krylov basis 1.2 GB, cells + vectors 0.2 GB); no explicit flush"},
         "e2e": e2e, "gpu_launches": None, "clocks": clk, "roofline": roofline, "cpu_baseline": cpu,
         "detail": {"useful_pairs_per_matvec": useful_mv, "visited_pairs_per_matvec": visited_mv,
                    "useful_pairs_grid": useful_grid, "matvecs_f32_per_step": mv32 / args.steps,
