@@ -36,9 +36,9 @@ namespace rbf {
 namespace {
 
 constexpr int kSumWarps = 4;            // warps per CTA
-constexpr int kFlush = 64;              // sources per inner-loop batch
+constexpr int kFlush = 96;              // sources per inner-loop batch
 constexpr int kBuf = kFlush + 32 + 4;   // staging ring capacity (SoA, floats)
-constexpr int kBufPad = 104;            // multiple of 4 >= kBuf
+constexpr int kBufPad = 136;            // multiple of 4 >= kBuf
 
 // --------------------------------------------------------------- packed ops
 __device__ __forceinline__ unsigned long long pk(float2 a) {
