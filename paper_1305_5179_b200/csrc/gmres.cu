@@ -30,7 +30,7 @@ namespace rbf {
 namespace {
 
 constexpr int kVecThreads = 256;
-constexpr int kDotChunk = 8;
+constexpr int kDotChunk = 4;
 
 // partial[j * nblk + blk] = sum over this block's slice of V_j . w, j in [0, k);
 // blockIdx.y selects the chunk of kDotChunk basis vectors (chunks run in parallel)
