@@ -317,8 +317,8 @@ def run_ours(args, rank, world, local):
     avg_mv_ms = t_mv / max(n_mv, 1)
     achieved = useful_mv / (avg_mv_ms * 1e-3) / 1e12
     peak_max = SMS * MUFU_PER_CLK_PER_SM * SM_MAX_MHZ * 1e6 / 1e12
-    sym = os.environ.get("RBF_SUM_SYM")
-    sym = int(sym) if sym in ("0", "1", "2") else (2 if 3 * cfg.n // max(world if slab else 1, 1) >= (1 << 18) else 0)
+    # the solver's operator under OP_AUTO (rbf_op_variant; sym_mode in summation.cu)
+    sym = 2 if 3 * cfg.n // max(world if slab else 1, 1) >= (1 << 18) else 0
     kname = {0: "sum_f32_kernel (one-sided)", 1: "sum_f32_kernel (symmetric, 64-target tiles)",
              2: "sum_f32_symw_kernel (symmetric, 128-target tiles)"}[sym]
     roofline = {"bound": "alu", "kernel": kname + ", MUFU.EX2", "achieved": achieved, "peak": peak_max,

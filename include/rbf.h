@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define RBF_ABI_VERSION 2
+#define RBF_ABI_VERSION 3
 
 typedef enum {
   RBF_OK = 0,
@@ -59,6 +59,20 @@ typedef enum {
 } rbf_status;
 
 typedef enum { RBF_F32 = 0, RBF_F64 = 1 } rbf_precision;
+
+/* Evaluation order of the solver's operator f = A w (reading R19).
+ * A = A^T, so a kernel may evaluate each exponential of a pair (i, j) once and
+ * add it to both f_i and f_j ("symmetric"): half the exponentials, but the
+ * source-side sums land with atomicAdd, so f is reproducible only to the last
+ * bits run to run.  "One-sided" evaluates every ordered pair and writes each f_i
+ * once: bit-reproducible for a fixed device and launch configuration.
+ *   RBF_OP_AUTO      symmetric on the wide (128-target) plan for >= 2^18 centres
+ *                    per GPU, one-sided below (the benchmarked default)
+ *   RBF_OP_ONESIDED  one-sided fp32 and fp64 tiers: a DETERMINISTIC solve
+ *   RBF_OP_SYM       symmetric on the 64-target plan
+ *   RBF_OP_SYM_WIDE  symmetric on the wide plan (fp64 tier: the 64-target plan)
+ * The public rbf_matvec is always one-sided; rbf_matvec_op exposes the others. */
+typedef enum { RBF_OP_AUTO = 0, RBF_OP_ONESIDED = 1, RBF_OP_SYM = 2, RBF_OP_SYM_WIDE = 3 } rbf_op_variant;
 
 /* Gaussian kernel of Eq.6 with truncation radius
  * cutoff_sigmas*sigma.  amplitude <= 0 selects Eq.6's
@@ -104,6 +118,10 @@ typedef struct {
   int max_ext;           /* reject blocks larger than this; <= 0 => 4096 */
   double shift;          /* >= 0; diagonal shift of the local matrices in units of a */
   int local_fp32;        /* 0 => fp64 LU + fp64 W; 1 => fp32 on-chip inverse + fp32 W */
+  int pivot;             /* on-chip fp32 inverses: 0 => auto (partial pivoting iff
+                            shift < 1e-4), 1 => always pivot, 2 => never */
+  int w_layout;          /* fp32 block-Jacobi W: 0 => auto (packed lower triangles of
+                            the symmetric W_i), 1 => full rows */
 } rbf_precond_cfg;
 
 /* Restarted right-preconditioned FGMRES(m).
@@ -117,10 +135,21 @@ typedef struct {
   int max_iters;         /* total inner iterations; <= 0 => 500 */
   int polish_fp64;       /* 1 => phase 2 in fp64 (needed for rtol < ~1e-5) */
   int cgs_passes;        /* Gram-Schmidt passes per Arnoldi step: 1 (CGS) or 2 (CGS2); other => 2 */
+  int op_variant;        /* rbf_op_variant of the operator; RBF_OP_ONESIDED => deterministic */
+  int basis_fp64;        /* 1 => fp64 Krylov basis in phase 1 too (default: fp32 basis there) */
+  /* Residual history (HOST, caller-allocated, may be NULL; filled up to
+   * history_cap entries, lengths in rbf_solve_report):
+   *   history[i]      Arnoldi estimate |g_{j+1}| / ||b|| after inner iteration i+1
+   *   history_true[k] true relative residual ||b - A w|| / ||b|| at the start of
+   *                   restart cycle k (operator tier of that cycle), then the final one */
+  double* history;
+  double* history_true;
+  int history_cap;
 } rbf_gmres_cfg;
 
 typedef struct {
   int iters_phase1, iters_phase2, restarts, converged, breakdown;
+  int history_len, history_true_len;
   double rel_residual_true;   /* ||b - A w|| / ||b|| with the fp64 operator */
   double rel_residual_est;    /* GMRES (Arnoldi) estimate at exit */
   double t_setup, t_phase1, t_phase2;  /* seconds (host clock around device work) */
@@ -240,6 +269,11 @@ rbf_status rbf_cells_view(const rbf_cells* cells, const int32_t** perm,
  * fp64 weights and accumulation.  w and f must not alias. */
 rbf_status rbf_matvec(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern,
                       rbf_precision prec, const void* w, void* f);
+/* The same product through the solver's operator variant `op` (rbf_op_variant):
+ * what rbf_gmres_solve multiplies with under that setting.  RBF_F32: w is rounded
+ * to fp32 inside (as the solver's fp32 tier does), f fp32; RBF_F64: fp64. */
+rbf_status rbf_matvec_op(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern,
+                         rbf_precision prec, int op, const void* w, void* f);
 
 /* Pair accounting of the fp32 matvec traversal (host outputs; synchronises):
  * useful = ordered (target, source) pairs with r^2 <= c^2 (self included),
@@ -319,20 +353,28 @@ rbf_status rbf_csr_spmv(rbf_ctx* ctx, const rbf_csr* m, const float* w, float* f
 rbf_status rbf_zero_set(rbf_ctx* ctx, const float* field, const rbf_grid* grid, const double* data,
                         int64_t ndata, double eps, double* points, int64_t cap, int64_t* count);
 
-/* ---- density measures of the data set (§4, Eq.7-11) --------------
+/* ---- density measures of the data set (§4, Eq.7-11) ----
  * x: DEVICE fp64 n x 3 (for 2-D sets pass z = 0).  Distances in fp64,
  * ((dx^2 + dy^2) + dz^2) then sqrt of the minimum (bit-identical to the oracle).
  * rbf_nn_distance: dist[i] (DEVICE fp64) = min_j ||q_i - x_j|| for the m query
  * points q (DEVICE fp64 m x 3), or, with q = NULL, min_{j != i} ||x_i - x_j||
- * (n entries; duplicates give 0).  rbf_density: out3 (HOST) = {q_X (Eq.7,
- * separation distance = half the smallest pairwise distance), h_max (P:614-619,
- * largest nearest-neighbour distance), h_{X,Omega} (Eq.8, fill distance over
- * the m sample points omega of Omega; NaN when omega = NULL)}.  Sigma
- * heuristics: Eq.9 sigma ~ 2 q_X, Eq.10 sigma ~ sqrt(2) h, Eq.11 h ~ sqrt(2)
- * h_max.  Synchronise.  Errors: RBF_EINVAL (n < 2 for self distances, NULLs,
- * non-finite data). */
+ * (n entries; duplicates give 0).  rbf_density: out6 (HOST) =
+ *   [0] q_X      separation distance, half the smallest pairwise distance (Eq.7)
+ *   [1] h_max    largest nearest-neighbour distance
+ *   [2] h_X,Om   fill distance over the m sample points omega of Omega (Eq.8;
+ *                NaN when omega = NULL)
+ *   [3] sigma of Eq.9   2 q_X
+ *   [4] sigma of Eq.10  sqrt(2) h_X,Om (NaN when omega = NULL)
+ *   [5] sigma of Eq.10 with Eq.11's h_X,M ~ sqrt(2) h_max:  2 h_max
+ * (each sigma as the fp64 product of the measure and the constant).
+ * rbf_sigma_auto: *sigma (HOST) = out6[3], out6[4] or out6[5] for rule = 9, 10
+ * or 11 (rule 10 needs omega).  Synchronise.  Errors: RBF_EINVAL (n < 2 for self
+ * distances, NULLs, non-finite data, rule not in {9,10,11}, rule 10 without
+ * omega). */
 rbf_status rbf_nn_distance(rbf_ctx* ctx, const double* x, int64_t n, const double* q, int64_t m, double* dist);
-rbf_status rbf_density(rbf_ctx* ctx, const double* x, int64_t n, const double* omega, int64_t m, double* out3);
+rbf_status rbf_density(rbf_ctx* ctx, const double* x, int64_t n, const double* omega, int64_t m, double* out6);
+rbf_status rbf_sigma_auto(rbf_ctx* ctx, const double* x, int64_t n, const double* omega, int64_t m, int rule,
+                          double* sigma);
 
 /* ---- profiling (CUDA events on the context stream) -------------------------
  * When enabled, every launch of the listed device stages is bracketed by a

@@ -1,6 +1,10 @@
 """Build librbf.so (the C-ABI of include/rbf.h) in-tree with nvcc for sm_100a.
 
-    python -m paper_1305_5179_b200.build        # or __graft_entry__.build()
+    python -m paper_1305_5179_b200.build [--force]     # or __graft_entry__.build()
+
+Each csrc/*.cu compiles to its own object (in parallel, under build/), then one
+nvcc -shared link.  An object is rebuilt when its source, any csrc/*.h or
+include/rbf.h is newer than it.
 """
 from __future__ import annotations
 
@@ -8,22 +12,32 @@ import glob
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "librbf.so")
+OBJDIR = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++20",
-         "-Xcompiler", "-fPIC,-ffp-contract=off", "-shared", "-diag-suppress", "177"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CFLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-ffp-contract=off",
+          "-diag-suppress", "177"]
 
 
 def sources():
     return sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))
 
 
+def headers():
+    return sorted(glob.glob(os.path.join(HERE, "csrc", "*.h"))) + [os.path.join(ROOT, "include", "rbf.h")]
+
+
 def deps():
-    return sources() + sorted(glob.glob(os.path.join(HERE, "csrc", "*.h"))) + \
-        [os.path.join(ROOT, "include", "rbf.h")]
+    return sources() + headers()
+
+
+def _obj(src: str) -> str:
+    return os.path.join(OBJDIR, os.path.basename(src)[:-3] + ".o")
 
 
 def up_to_date() -> bool:
@@ -36,8 +50,22 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
+    os.makedirs(OBJDIR, exist_ok=True)
+    th = max(os.path.getmtime(h) for h in headers())
+    todo = [s for s in sources()
+            if force or not os.path.exists(_obj(s)) or os.path.getmtime(_obj(s)) < max(th, os.path.getmtime(s))]
+
+    def compile_one(src):
+        cmd = [NVCC, *CFLAGS, "-c", "-o", _obj(src) + ".tmp", src]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+        os.replace(_obj(src) + ".tmp", _obj(src))
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(todo), os.cpu_count() or 1))) as ex:
+        list(ex.map(compile_one, todo))
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *FLAGS, "-o", tmp, *sources()]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *[_obj(s) for s in sources()]]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)

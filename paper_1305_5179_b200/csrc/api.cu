@@ -6,6 +6,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <map>
+#include <mutex>
 #include <new>
 
 #include "internal.h"
@@ -21,6 +23,28 @@ std::atomic<unsigned long long> g_launches{0};
 }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 const char* last_error_cstr() { return g_last_error.c_str(); }
+
+cudaMemPool_t lib_pool(int device) {
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t> pools;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = pools.find(device);
+  if (it != pools.end()) return it->second;
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = device;
+  cudaMemPool_t pool = nullptr;
+  if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+    cudaGetLastError();
+    pool = nullptr;   // DevBuf falls back to the device's current pool
+  } else {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  pools[device] = pool;
+  return pool;
+}
 }  // namespace rbf
 
 using namespace rbf;
@@ -99,14 +123,7 @@ rbf_status rbf_create(rbf_ctx** out, int device, void* cuda_stream, const void* 
               std::to_string(prop.major) + "." + std::to_string(prop.minor));
     return RBF_EUNSUPPORTED;
   }
-  // keep freed blocks in the stream-ordered pool: the solver frees and re-allocates
-  // tens of GB per fit (RAS factors, Krylov basis); returning them to the driver
-  // at every synchronisation costs hundreds of ms
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
+  lib_pool(device);   // the library's private stream-ordered pool (internal.h)
   if (world > 1) {
     rbf_status st = dist_init(c, nccl_unique_id, rank, world);
     if (st != RBF_OK) { delete c; return st; }
@@ -146,8 +163,12 @@ void rbf_destroy(rbf_ctx* ctx) {
   cudaStream_t s = ctx->stream;
   cudaStreamSynchronize(s);
   dist_destroy(ctx);
+  const int dev = ctx->device;
   delete ctx;  // DevBufs free stream-ordered
   cudaStreamSynchronize(s);
+  // hand the freed workspaces back to the driver (memory still held by other
+  // live contexts / handles stays allocated)
+  if (cudaMemPool_t pool = lib_pool(dev)) cudaMemPoolTrimTo(pool, 0);
 }
 
 rbf_status rbf_build_cells(rbf_ctx* ctx, const float* xyz, int64_t n, const rbf_kernel* kern,
@@ -204,31 +225,32 @@ rbf_status rbf_cells_view(const rbf_cells* c, const int32_t** perm, const float*
   return RBF_OK;
 }
 
-rbf_status rbf_matvec(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, rbf_precision prec, const void* w,
-                      void* f) {
+}  // extern "C"
+
+namespace {
+// f = A w through operator variant op (RBF_OP_ONESIDED: the public product).
+rbf_status matvec_impl(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, rbf_precision prec, int op,
+                       const void* w, void* f) {
   RBF_TRY(check_cells(ctx, c, kern));
   if (!w || !f) { set_error("w/f is NULL"); return RBF_EINVAL; }
   if (w == f) { set_error("w and f must not alias"); return RBF_EINVAL; }
+  if (prec != RBF_F32 && prec != RBF_F64) { set_error("bad precision"); return RBF_EINVAL; }
+  if (op < RBF_OP_AUTO || op > RBF_OP_SYM_WIDE) { set_error("bad operator variant"); return RBF_EINVAL; }
   RBF_CUDA_TRY(cudaSetDevice(ctx->device));
   KernelParams kp = kernel_params(kern);
   const int64_t n = c->n;
-  // RBF_PUBLIC_SYM=1 (tests only): the public product runs the solver's operator
-  // (symmetric variants of reading R19) so it can be checked against the oracle
-  const char* ps = std::getenv("RBF_PUBLIC_SYM");
-  const bool solver_op = ps && ps[0] == '1';
-  if (ctx->world > 1 || c->emulated || solver_op) {
-    // slab partition: replicated in, this rank's rows, gathered out
-    if (prec != RBF_F32 && prec != RBF_F64) { set_error("bad precision"); return RBF_EINVAL; }
+  if (ctx->world > 1 || c->emulated || op != RBF_OP_ONESIDED) {
+    // solver operator / slab partition: replicated in, this rank's rows, gathered out
     RBF_TRY(ctx->vec_a.ensure(sizeof(double) * n, ctx->stream));
     RBF_TRY(ctx->vec_b.ensure(sizeof(double) * n, ctx->stream));
     double* ws = ctx->vec_a.as<double>();
     double* fs = ctx->vec_b.as<double>();
     if (prec == RBF_F32) {
       RBF_TRY(gather_f32_to_sorted_f64(ctx, static_cast<const float*>(w), c->perm.as<int32_t>(), ws, n));
-      RBF_TRY(matvec_sorted_f32_d(ctx, c, kp, ws + c->view.o0, fs + c->view.o0, solver_op));
+      RBF_TRY(matvec_sorted_f32_d(ctx, c, kp, ws + c->view.o0, fs + c->view.o0, op));
     } else {
       RBF_TRY(gather_f64_to_sorted(ctx, static_cast<const double*>(w), c->perm.as<int32_t>(), ws, n));
-      RBF_TRY(matvec_sorted_f64(ctx, c, kp, ws + c->view.o0, fs + c->view.o0, nullptr, solver_op));
+      RBF_TRY(matvec_sorted_f64(ctx, c, kp, ws + c->view.o0, fs + c->view.o0, nullptr, op));
     }
     RBF_TRY(allgather_sorted(ctx, c, fs));
     if (prec == RBF_F32) return scatter_f64_from_sorted_f32(ctx, fs, c->perm.as<int32_t>(), static_cast<float*>(f), n);
@@ -239,14 +261,24 @@ rbf_status rbf_matvec(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, 
     RBF_TRY(gather_f32_to_sorted(ctx, static_cast<const float*>(w), c->perm.as<int32_t>(), ctx->vec_a.as<float>(), n));
     return matvec_sorted_f32(ctx, c, kp, ctx->vec_a.as<float>(), static_cast<float*>(f), c->perm.as<int32_t>(),
                              nullptr);
-  } else if (prec == RBF_F64) {
-    RBF_TRY(ctx->vec_a.ensure(sizeof(double) * n, ctx->stream));
-    RBF_TRY(gather_f64_to_sorted(ctx, static_cast<const double*>(w), c->perm.as<int32_t>(), ctx->vec_a.as<double>(),
-                                 n));
-    return matvec_sorted_f64(ctx, c, kp, ctx->vec_a.as<double>(), static_cast<double*>(f), c->perm.as<int32_t>());
   }
-  set_error("bad precision");
-  return RBF_EINVAL;
+  RBF_TRY(ctx->vec_a.ensure(sizeof(double) * n, ctx->stream));
+  RBF_TRY(gather_f64_to_sorted(ctx, static_cast<const double*>(w), c->perm.as<int32_t>(), ctx->vec_a.as<double>(),
+                               n));
+  return matvec_sorted_f64(ctx, c, kp, ctx->vec_a.as<double>(), static_cast<double*>(f), c->perm.as<int32_t>());
+}
+}  // namespace
+
+extern "C" {
+
+rbf_status rbf_matvec(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, rbf_precision prec, const void* w,
+                      void* f) {
+  return matvec_impl(ctx, c, kern, prec, RBF_OP_ONESIDED, w, f);
+}
+
+rbf_status rbf_matvec_op(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, rbf_precision prec, int op,
+                         const void* w, void* f) {
+  return matvec_impl(ctx, c, kern, prec, op, w, f);
 }
 
 rbf_status rbf_matvec_pairs(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, int64_t* useful,

@@ -533,11 +533,8 @@ rbf_status build_cells(rbf_ctx* ctx, const float* xyz, int64_t n, const rbf_kern
   RBF_TRY(rcw.alloc(sizeof(uint32_t) * rows, s));
   RBF_TRY(row_w.alloc(sizeof(uint32_t) * rows, s));
   RBF_TRY(totw.alloc(sizeof(uint32_t) * 2, s));
-  // (RBF_WIDE_CAP / RBF_WIDE_SPAN: tuning knobs, defaults 128 / 4)
-  const char* ecap = std::getenv("RBF_WIDE_CAP");
-  const char* espan = std::getenv("RBF_WIDE_SPAN");
-  const int cap_w = ecap ? std::min(128, std::max(32, std::atoi(ecap))) : 128;
-  const int span_w = espan ? std::max(1, std::atoi(espan)) : std::max(span, 4);
+  const int cap_w = 128;
+  const int span_w = std::max(span, 4);
   plan_count<<<grid_for(rows, 128), 128, 0, s>>>(c->cell_start.as<int32_t>(), g, cap_w, span_w, 0,
                                                  rcw.as<uint32_t>());
   RBF_CHECK_LAUNCH();
@@ -546,6 +543,8 @@ rbf_status build_cells(rbf_ctx* ctx, const float* xyz, int64_t n, const rbf_kern
   RBF_CUDA_TRY(cudaMemcpyAsync(&ntiles_w, totw.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   RBF_CUDA_TRY(cudaStreamSynchronize(s));
   c->ntiles_w = ntiles_w;
+  c->hd2 = 0.25 * h * h * ((double)span * span + 2.0);
+  c->hd2_w = 0.25 * h * h * ((double)span_w * span_w + 2.0);
   RBF_TRY(c->tiles_w.alloc(sizeof(int2) * (size_t)std::max<uint32_t>(ntiles_w, 1), s));
   RBF_TRY(c->tile_box_w.alloc(sizeof(float4) * 2 * (size_t)std::max<uint32_t>(ntiles_w, 1), s));
   plan_emit<<<grid_for(rows, 128), 128, 0, s>>>(c->cell_start.as<int32_t>(), g, cap_w, span_w, 0,

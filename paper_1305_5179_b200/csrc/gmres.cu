@@ -135,6 +135,7 @@ struct Solver {
   // V, Z in fp64.  Halves the Krylov vector traffic of the fp32 phase.
   DevBuf V32, Z32;
   bool basis32 = true;
+  int opv = RBF_OP_AUTO;   // operator variant (rbf_op_variant)
   int64_t mv32 = 0, mv64 = 0;
 
   // the fp64 basis, allocated when a cycle first runs on it
@@ -155,7 +156,7 @@ struct Solver {
     RBF_TRY(w.alloc(sizeof(double) * n, s));
     RBF_TRY(f.alloc(sizeof(double) * n, s));
     RBF_TRY(b.alloc(sizeof(double) * n, s));
-    nblk = ctx->sm_count * 4;   // x chunks of 8 basis vectors (grid.y): enough warps in flight
+    nblk = ctx->sm_count * 4;   // x chunks of kDotChunk basis vectors (grid.y): enough warps in flight
     RBF_TRY(partial.alloc(sizeof(double) * (size_t)nblk * (m + 2), s));
     RBF_TRY(dots.alloc(sizeof(double) * 4 * (m + 2), s));
     return RBF_OK;
@@ -164,14 +165,14 @@ struct Solver {
   template <class VT> VT* zbasis() { return std::is_same<VT, float>::value ? (VT*)Z32.p : (VT*)Z.p; }
 
   rbf_status op(bool fp64, const double* in, double* out) {
-    if (fp64) { ++mv64; return matvec_sorted_f64(ctx, c, kp, in, out, nullptr, true); }
+    if (fp64) { ++mv64; return matvec_sorted_f64(ctx, c, kp, in, out, nullptr, opv); }
     ++mv32;
-    return matvec_sorted_f32_d(ctx, c, kp, in, out, true);
+    return matvec_sorted_f32_d(ctx, c, kp, in, out, opv);
   }
   rbf_status op(bool fp64, const float* in, double* out) {   // fp32 basis: fp32 phase only
     if (fp64) { set_error("internal: fp64 operator on an fp32 basis"); return RBF_EINVAL; }
     ++mv32;
-    return matvec_sorted_f32_f(ctx, c, kp, in, out, true);
+    return matvec_sorted_f32_f(ctx, c, kp, in, out, opv);
   }
   // dots[0..k) = V_{0..k}^T w ; neg copy at dots[(m+2)...]
   template <class VT>
@@ -234,8 +235,16 @@ rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp
   const int passes = (gcfg && gcfg->cgs_passes == 1) ? 1 : 2;
   const int64_t n = S.n;
   const int m = S.m;
-  // RBF_GMRES_BASIS64=1: fp64 basis in both phases
-  S.basis32 = std::getenv("RBF_GMRES_BASIS64") == nullptr;
+  S.basis32 = !(gcfg && gcfg->basis_fp64);   // basis_fp64: fp64 basis in both phases
+  S.opv = gcfg ? gcfg->op_variant : RBF_OP_AUTO;
+  double* hist = gcfg ? gcfg->history : nullptr;
+  double* hist_true = gcfg ? gcfg->history_true : nullptr;
+  const int hcap = (gcfg && gcfg->history_cap > 0) ? gcfg->history_cap : 0;
+  int hlen = 0, htlen = 0;
+  auto record_true = [&](double v) {
+    if (hist_true && htlen < hcap) hist_true[htlen] = v;
+    ++htlen;
+  };
   RBF_TRY(S.alloc());
   f32_to_f64<<<grid_for(n, 256), 256, 0, s>>>(b_sorted32, S.b.as<double>(), n);
   RBF_CHECK_LAUNCH();
@@ -255,7 +264,12 @@ rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp
   if (bnorm == 0.0) {
     RBF_CUDA_TRY(cudaMemcpyAsync(x_out_sorted, S.x.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     R.converged = 1;
-    if (rep) *rep = R;
+    if (rep) {
+      R.t_setup = rep->t_setup;
+      R.nblocks = rep->nblocks;
+      R.precond_bytes = rep->precond_bytes;
+      *rep = R;
+    }
     return RBF_OK;
   }
   bool fp64 = false;
@@ -300,7 +314,9 @@ rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp
     }
     last_beta = beta;
     cycle_beta = fp64 ? -1.0 : beta;
-    const double target = fp64 ? rtol : std::max(p1tol, rtol);
+    record_true(beta / bnorm);
+    // inner stopping target: the phase-1 target only while a phase 2 follows
+    const double target = (fp64 || !polish) ? rtol : std::max(p1tol, rtol);
     // one restart cycle on a basis of type VT (float: fp32 phase with basis32)
     int k = 0;
     bool bd = false;
@@ -369,6 +385,8 @@ rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp
         if (fp64) ++it2; else ++it1;
         k = j + 1;
         est = std::fabs(g[j + 1]) / bnorm;
+        if (hist && hlen < hcap) hist[hlen] = est;
+        ++hlen;
         if (!(hn > 1e-14 * beta) || !std::isfinite(hn)) { bd = true; break; }
         if (est <= target || it >= maxit) break;
       }
@@ -398,8 +416,11 @@ rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp
   if (!fp64) RBF_TRY(S.residual(true, &tr));
   const double t_end = std::chrono::duration<double>(clk::now() - t_start).count();
   RBF_CUDA_TRY(cudaMemcpyAsync(x_out_sorted, S.x.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  record_true(tr / bnorm);
   R.iters_phase1 = it1;
   R.iters_phase2 = it2;
+  R.history_len = std::min(hlen, hcap);
+  R.history_true_len = std::min(htlen, hcap);
   R.rel_residual_true = tr / bnorm;
   R.rel_residual_est = est;
   R.converged = (R.rel_residual_true <= rtol) ? 1 : 0;
@@ -436,6 +457,11 @@ rbf_status rbf_gmres_solve(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* k
   if (precond && precond->cells != c) { set_error("precond was built for other cells"); return RBF_EINVAL; }
   if (c->world != ctx->world) { set_error("cells were partitioned for another world size"); return RBF_EINVAL; }
   if (c->emulated) { set_error("RBF_SLAB_EMULATE cells support matvec / grid / precond blocks only"); return RBF_EUNSUPPORTED; }
+  if (gcfg && (gcfg->op_variant < RBF_OP_AUTO || gcfg->op_variant > RBF_OP_SYM_WIDE)) {
+    set_error("bad operator variant");
+    return RBF_EINVAL;
+  }
+  if (gcfg && gcfg->history_cap < 0) { set_error("history_cap must be >= 0"); return RBF_EINVAL; }
   RBF_CUDA_TRY(cudaSetDevice(ctx->device));
   KernelParams kp = kernel_params(kern);
   rbf_solve_report R{};

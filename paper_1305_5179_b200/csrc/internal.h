@@ -38,7 +38,15 @@ void count_launch();
 
 constexpr int kWarp = 32;
 
-// Stream-ordered device buffer (cudaMallocAsync on the context stream).
+// The library's own stream-ordered memory pool on `device` (created on first
+// use, release threshold = max: the solver frees and re-allocates GB-sized
+// workspaces per fit, which must not go back to the driver at every
+// synchronisation).  Private, so the process's default pool (and torch) is left
+// alone; rbf_destroy trims it.
+cudaMemPool_t lib_pool(int device);
+
+// Stream-ordered device buffer (cudaMallocFromPoolAsync from lib_pool on the
+// context stream).
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -61,7 +69,10 @@ struct DevBuf {
     release();
     s = stream;
     if (nbytes == 0) nbytes = 16;
-    cudaError_t e = cudaMallocAsync(&p, nbytes, stream);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool = lib_pool(dev);
+    cudaError_t e = pool ? cudaMallocFromPoolAsync(&p, nbytes, pool, stream) : cudaMallocAsync(&p, nbytes, stream);
     if (e != cudaSuccess) {
       p = nullptr;
       set_error(std::string("cudaMallocAsync(") + std::to_string(nbytes) + "): " + cudaGetErrorString(e));
@@ -167,6 +178,10 @@ struct rbf_cells {
   int64_t nonempty = 0;
   int tile_cap = 64;
   int tile_span = 2;
+  // squared half-diagonal bound of the target-tile boxes (length units) of the
+  // 64-target plan and of the wide plan: a tile spans <= span cells along x and
+  // one cell along y and z, so hd^2 <= (h/2)^2 (span^2 + 2)
+  double hd2 = 0.0, hd2_w = 0.0;
   rbf::DevBuf perm;          // int32[n]
   rbf::DevBuf sorted;        // float4[n]
   rbf::DevBuf keys;          // uint32[n]
@@ -214,10 +229,11 @@ KernelParams kernel_params(const rbf_kernel* k);
 rbf_status matvec_sorted_f32(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
                              const float* w_sorted, float* f_sorted, const int32_t* out_perm,
                              unsigned long long* pair_stats);
-// solver = true: the GMRES operator (may use the symmetric variant, reading R19);
-// false: the public product (one-sided, deterministic)
+// op: rbf_op_variant (RBF_OP_ONESIDED = the public, deterministic product; the
+// solver may use a symmetric variant, reading R19)
 rbf_status matvec_sorted_f64(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
-                             const double* w_sorted, double* f_sorted, const int32_t* out_perm, bool solver = false);
+                             const double* w_sorted, double* f_sorted, const int32_t* out_perm,
+                             int op = RBF_OP_ONESIDED);
 rbf_status eval_grid_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
                             const double* w_sorted, const rbf_grid* g, float* field,
                             unsigned long long* pair_stats = nullptr);

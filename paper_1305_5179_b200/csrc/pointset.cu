@@ -448,8 +448,8 @@ extern "C" rbf_status rbf_nn_distance(rbf_ctx* ctx, const double* x, int64_t n, 
 }
 
 extern "C" rbf_status rbf_density(rbf_ctx* ctx, const double* x, int64_t n, const double* omega, int64_t m,
-                                  double* out3) {
-  if (!ctx || !x || !out3 || n < 2 || (omega && m < 1)) { set_error("bad arguments"); return RBF_EINVAL; }
+                                  double* out6) {
+  if (!ctx || !x || !out6 || n < 2 || (omega && m < 1)) { set_error("bad arguments"); return RBF_EINVAL; }
   RBF_CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
   DevBuf d;
@@ -457,13 +457,27 @@ extern "C" rbf_status rbf_density(rbf_ctx* ctx, const double* x, int64_t n, cons
   RBF_TRY(nn_distances(ctx, x, n, nullptr, 0, d.as<double>()));
   double lo, hi;
   RBF_TRY(host_minmax(ctx, d.as<double>(), n, &lo, &hi));
-  out3[0] = 0.5 * lo;   // q_X (Eq.7)
-  out3[1] = hi;         // h_max
-  out3[2] = NAN;
+  out6[0] = 0.5 * lo;   // q_X (Eq.7)
+  out6[1] = hi;         // h_max
+  out6[2] = NAN;
   if (omega) {
     RBF_TRY(nn_distances(ctx, x, n, omega, m, d.as<double>()));
     RBF_TRY(host_minmax(ctx, d.as<double>(), m, &lo, &hi));
-    out3[2] = hi;       // h_{X,Omega} (Eq.8)
+    out6[2] = hi;       // h_{X,Omega} (Eq.8)
   }
+  out6[3] = 2.0 * out6[0];                  // Eq.9   sigma ~ 2 q_X
+  out6[4] = std::sqrt(2.0) * out6[2];       // Eq.10  sigma ~ sqrt(2) h_{X,Omega}
+  out6[5] = 2.0 * out6[1];                  // Eq.10 with Eq.11 h ~ sqrt(2) h_max
+  return RBF_OK;
+}
+
+extern "C" rbf_status rbf_sigma_auto(rbf_ctx* ctx, const double* x, int64_t n, const double* omega, int64_t m,
+                                     int rule, double* sigma) {
+  if (!sigma) { set_error("sigma is NULL"); return RBF_EINVAL; }
+  if (rule != 9 && rule != 10 && rule != 11) { set_error("rule must be 9, 10 or 11 (Eq.9 / Eq.10 / Eq.11)"); return RBF_EINVAL; }
+  if (rule == 10 && !omega) { set_error("rule 10 (fill distance, Eq.8) needs omega"); return RBF_EINVAL; }
+  double out6[6];
+  RBF_TRY(rbf_density(ctx, x, n, rule == 10 ? omega : nullptr, rule == 10 ? m : 0, out6));
+  *sigma = out6[rule == 9 ? 3 : (rule == 10 ? 4 : 5)];
   return RBF_OK;
 }

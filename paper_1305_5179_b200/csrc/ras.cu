@@ -961,8 +961,8 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
   std::vector<int64_t> h_ext_ptr(ncore + 1, 0), h_w_off(ncore + 1, 0);
   int64_t max_m = 0;
   // block-Jacobi with fp32 W: W_i = B_i^-1 is symmetric -> packed lower triangles
-  // (RBF_APPLY_FULL=1 keeps the full inverses)
-  P->w_sym = want_fp32 && no_overlap && std::getenv("RBF_APPLY_FULL") == nullptr;
+  // (w_layout = 1 keeps the full inverses)
+  P->w_sym = want_fp32 && no_overlap && !(cfg && cfg->w_layout == 1);
   P->max_wblk = 0;
   for (int64_t b = 0; b < ncore; ++b) {
     h_ext_ptr[b + 1] = h_ext_ptr[b] + h_ecount[b];
@@ -1049,7 +1049,9 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
     // overlap their per-step barrier latency
     const int caps[5] = {64, 96, 128, 192, 224};
     // shifted SPD blocks need no pivoting (one barrier per elimination step)
-    const bool nopiv = shift >= kNoPivShift && std::getenv("RBF_GJ_PIVOT") == nullptr;
+    // (pivot: 0 auto, 1 always, 2 never)
+    const int piv = cfg ? cfg->pivot : 0;
+    const bool nopiv = piv == 2 || (piv == 0 && shift >= kNoPivShift);
     for (int bin = 0; bin < 5 && lo < small.size(); ++bin) {
       size_t hi = lo;
       while (hi < small.size() && h_ext_ptr[small[hi] + 1] - h_ext_ptr[small[hi]] <= caps[bin]) ++hi;
@@ -1145,10 +1147,7 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
   return RBF_OK;
 }
 
-int apply_threads() {
-  const char* e = std::getenv("RBF_APPLY_THREADS");
-  return e ? std::atoi(e) : 128;
-}
+constexpr int kApplyThreads = 128;
 
 template <class VT>
 rbf_status precond_apply_sorted(rbf_ctx* ctx, const rbf_precond* P, const VT* r, VT* z) {
@@ -1161,25 +1160,17 @@ rbf_status precond_apply_sorted(rbf_ctx* ctx, const rbf_precond* P, const VT* r,
   const int blocks = (int)std::min<int64_t>(P->nblocks, (int64_t)ctx->sm_count * 16);
   const size_t smem = sizeof(double) * (size_t)P->max_m;
   if (P->w_sym) {
-    // two staging buffers of up to cap floats per CTA (RBF_APPLY_CAP); larger
-    // triangles are read from global
-    static const int cap_env = std::getenv("RBF_APPLY_CAP") ? std::atoi(std::getenv("RBF_APPLY_CAP")) : 0;
-    static const int thr_env = std::getenv("RBF_APPLY_SYM_THREADS") ? std::atoi(std::getenv("RBF_APPLY_SYM_THREADS")) : 128;
-    const int cap = (int)std::min<int64_t>(P->max_wblk, cap_env > 0 ? cap_env : P->cap_w) & ~3;
-    // one CTA per block (default; many small CTAs per SM overlap the gather ->
-    // copy -> multiply latency chain of each block) or, RBF_APPLY_PERSIST=1,
-    // occupancy-sized persistent CTAs with a second stage prefetching the next block
-    static const bool persist = std::getenv("RBF_APPLY_PERSIST") != nullptr;
-    const size_t smems = sizeof(float) * ((size_t)((P->max_m + 3) & ~3) + (persist ? 2 : 1) * (size_t)cap);
+    // a staging buffer of up to cap floats per CTA; larger triangles are read
+    // from global.  One CTA per block: many small CTAs per SM overlap the
+    // gather -> copy -> multiply latency chain of each block
+    const int cap = (int)std::min<int64_t>(P->max_wblk, P->cap_w) & ~3;
+    const size_t smems = sizeof(float) * ((size_t)((P->max_m + 3) & ~3) + (size_t)cap);
     if (smems > 48 * 1024)
       RBF_CUDA_TRY(cudaFuncSetAttribute(apply_sym_kernel<VT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smems));
-    int per_sm = 0;
-    RBF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_sym_kernel<VT>, thr_env, smems));
-    const int64_t grid =
-        persist ? std::min<int64_t>(P->nblocks, (int64_t)ctx->sm_count * std::max(per_sm, 1)) : P->nblocks;
+    const int64_t grid = P->nblocks;
     ProfScope ps(ctx, RBF_PROF_PRECOND_APPLY);
-    apply_sym_kernel<VT><<<(unsigned)grid, thr_env, smems, s>>>(P->ext_ptr.as<int64_t>(), P->ext_idx.as<int32_t>(),
+    apply_sym_kernel<VT><<<(unsigned)grid, kApplyThreads, smems, s>>>(P->ext_ptr.as<int64_t>(), P->ext_idx.as<int32_t>(),
                                                                P->w_off.as<int64_t>(), P->W.as<float>(), r, z,
                                                                P->nblocks, cap, P->max_m);
     RBF_CHECK_LAUNCH();
@@ -1192,10 +1183,9 @@ rbf_status precond_apply_sorted(rbf_ctx* ctx, const rbf_precond* P, const VT* r,
                                         (int)smemf));
     // one CTA (4 warps) per block: many small CTAs resident per SM hide the
     // gather -> barrier -> row-latency chain of each block
-    const int threads = apply_threads();
     const int ablocks = (int)std::min<int64_t>(P->nblocks, (int64_t)1 << 30);
     ProfScope ps(ctx, RBF_PROF_PRECOND_APPLY);
-    apply_f32w_kernel<VT><<<threads == 256 ? blocks : ablocks, threads, smemf, s>>>(P->ext_ptr.as<int64_t>(), P->core_ptr.as<int64_t>(),
+    apply_f32w_kernel<VT><<<ablocks, kApplyThreads, smemf, s>>>(P->ext_ptr.as<int64_t>(), P->core_ptr.as<int64_t>(),
                                                      P->ext_idx.as<int32_t>(), P->w_off.as<int64_t>(),
                                                      P->W.as<float>(), r, z, P->nblocks);
     RBF_CHECK_LAUNCH();

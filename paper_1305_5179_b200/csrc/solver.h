@@ -52,9 +52,9 @@ rbf_status precond_apply_sorted(rbf_ctx* ctx, const rbf_precond* P, const VT* r,
 
 // fp32-tier matvec with fp64 input/output vectors in sorted order
 rbf_status matvec_sorted_f32_d(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp, const double* w_sorted,
-                               double* f_sorted, bool solver = false);
+                               double* f_sorted, int op = RBF_OP_ONESIDED);
 // the same with fp32 input weights (the fp32-phase Krylov basis)
 rbf_status matvec_sorted_f32_f(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp, const float* w_sorted,
-                               double* f_sorted, bool solver);
+                               double* f_sorted, int op);
 
 }  // namespace rbf

@@ -505,7 +505,11 @@ __device__ __forceinline__ float node_coord(const GridDesc& gd, int a, int i) {
 }
 inline float node_coord_host(const GridDesc& gd, int a, int i) { return (float)(gd.lo[a] + (double)i * gd.step[a]); }
 
-template <int MODE, bool STATS, class OutT, bool SYM = false>
+// DIRECT: the difference form |x_l s - t'|^2 (Flush32, one masked ring) instead of
+// the expansion; used when the tile or node-block boxes are so large that the
+// expansion's per-target factor 2^-|t'|^2 would leave fp32 range or lose accuracy
+// (expansion_ok(), |t'|^2 <= kExpT2Max).
+template <int MODE, bool STATS, class OutT, bool SYM = false, bool DIRECT = false>
 __global__ void __launch_bounds__(kSumWarps * 32, 8)
 sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* __restrict__ src,
                const int2* __restrict__ tiles, const float4* __restrict__ tbox, int64_t ntiles, int64_t tile_base,
@@ -584,6 +588,14 @@ sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
       int cnt;
       pad_ring(R, nbuf, lane, cnt);
       fs(cnt);
+      __syncwarp();
+    } else if constexpr (DIRECT) {
+      Stage32 st{R, src, blo, bhi, ctr, G.cc2, G.s, make_float4(0, 0, 0, 0)};
+      Flush32<2, true> fl{R, acc, xt, yt, zt, G.c2bits, G.s};
+      int nbuf = 0, cnt;
+      traverse(G, cell_start, blo, bhi, lane, st, fl, nbuf);
+      pad_ring(R, nbuf, lane, cnt);
+      fl(cnt);
       __syncwarp();
     } else {
       // expansion path: per-target -2 t', threshold k c^2 - |t'|^2, factor 2^-|t'|^2
@@ -1121,13 +1133,29 @@ SumGeom make_geom(const rbf_cells* c, const KernelParams& kp) {
   return G;
 }
 
-// Solver fp32 tier variant: 0 = one-sided, 1 = symmetric on the 64-target plan,
-// 2 = symmetric on the wide plan (reading R19).  RBF_SUM_SYM overrides; the
-// default is 2 for slices of >= 2^18 centres (c4: 4.94 -> 3.61 ms) and 0 below
-// (small problems have too few tiles to hide the longer wide tiles: c2 0.16 vs 0.21 ms).
-int sym_mode(int64_t n_loc) {
-  if (const char* e = std::getenv("RBF_SUM_SYM")) return e[0] == '1' ? 1 : (e[0] == '2' ? 2 : 0);
-  return n_loc >= ((int64_t)1 << 18) ? 2 : 0;
+// The expansion path's per-target factor 2^-|t'|^2 and terms 2^(|t'|^2 - ...) stay in
+// fp32 range, and the expansion's rounding (~u (|s'|^2 + 2 |t'| |s'|) in the
+// exponent, |s'| <= |t'| + sqrt(k) c) stays <= ~1e-5 relative per term, while
+// |t'|^2 = k hd^2 <= 16 (hd = half-diagonal of the target box).  The configured
+// plans give <= 7.3 (wide plan, h = c/4) and a 256^3 grid over c4 2.2; coarser
+// grids (step >~ 1.8 sigma) or cell edges beyond ~c/2 take the difference form.
+constexpr double kExpT2Max = 16.0;
+bool expansion_ok(const KernelParams& kp, double hd2) {
+  const double k = 1.4426950408889634 / (2.0 * kp.sigma * kp.sigma);
+  return k * hd2 <= kExpT2Max;
+}
+
+// Solver fp32 tier variant of an rbf_op_variant: 0 = one-sided, 1 = symmetric on
+// the 64-target plan, 2 = symmetric on the wide plan (reading R19).  RBF_OP_AUTO
+// is 2 for slices of >= 2^18 centres (c4: 4.94 -> 3.61 ms) and 0 below (small
+// problems have too few tiles to hide the longer wide tiles: c2 0.16 vs 0.21 ms).
+int sym_mode(int op, int64_t n_loc) {
+  switch (op) {
+    case RBF_OP_ONESIDED: return 0;
+    case RBF_OP_SYM: return 1;
+    case RBF_OP_SYM_WIDE: return 2;
+    default: return n_loc >= ((int64_t)1 << 18) ? 2 : 0;
+  }
 }
 
 // Persistent grid: as many CTAs as can be resident (the kernels pull tiles from a
@@ -1211,11 +1239,17 @@ rbf_status matvec_sorted_f32(rbf_ctx* ctx, const rbf_cells* c, const KernelParam
     sum_f32_kernel<0, true, float><<<sum_blocks(ctx, sum_f32_kernel<0, true, float>), kSumWarps * 32, 0, s>>>(
         G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), c->tiles.as<int2>(), c->tile_box.as<float4>(),
         V.t1 - V.t0, V.t0, gd, f_out, out_perm, ctx->counter.as<int>(), pair_stats);
-  } else {
+  } else if (expansion_ok(kp, c->hd2)) {
     ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
     sum_f32_kernel<0, false, float><<<sum_blocks(ctx, sum_f32_kernel<0, false, float>), kSumWarps * 32, 0, s>>>(
         G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), c->tiles.as<int2>(), c->tile_box.as<float4>(),
         V.t1 - V.t0, V.t0, gd, f_out, out_perm, ctx->counter.as<int>(), nullptr);
+  } else {
+    ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
+    auto kfn = sum_f32_kernel<0, false, float, false, true>;
+    kfn<<<sum_blocks(ctx, kfn), kSumWarps * 32, 0, s>>>(
+        G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), c->tiles.as<int2>(), c->tile_box.as<float4>(),
+        V.t1 - V.t0, V.t0, gd, f_out, out_perm, ctx->counter.as<int>(), nullptr, 0, 0, nullptr);
   }
   RBF_CHECK_LAUNCH();
   return RBF_OK;
@@ -1227,7 +1261,7 @@ rbf_status matvec_sorted_f32(rbf_ctx* ctx, const rbf_cells* c, const KernelParam
 // position, so the window and output pointers are shifted by h0 and o0.
 template <class WT>
 static rbf_status matvec_f32_solver(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp, const WT* w_loc,
-                                    double* f_loc, bool solver) {
+                                    double* f_loc, int op) {
   cudaStream_t s = ctx->stream;
   const SlabView& V = c->view;
   const int64_t nw = V.h1 - V.h0;
@@ -1251,7 +1285,9 @@ static rbf_status matvec_f32_solver(rbf_ctx* ctx, const rbf_cells* c, const Kern
   RBF_CUDA_TRY(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
   SumGeom G = make_geom(c, kp);
   GridDesc gd{};
-  const int sym = solver ? sym_mode(c->n_loc()) : 0;   // the public product stays one-sided
+  int sym = sym_mode(op, c->n_loc());
+  if (sym == 2 && !expansion_ok(kp, c->hd2_w)) sym = 0;
+  if (sym == 1 && !expansion_ok(kp, c->hd2)) sym = 0;
   if (sym == 2) {
     // symmetric evaluation on the wide plan (reading R19): the output is accumulated
     RBF_CUDA_TRY(cudaMemsetAsync(f_loc, 0, sizeof(double) * (size_t)c->n_loc(), s));
@@ -1275,26 +1311,27 @@ static rbf_status matvec_f32_solver(rbf_ctx* ctx, const rbf_cells* c, const Kern
     return RBF_OK;
   }
   ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
-  sum_f32_kernel<0, false, double><<<sum_blocks(ctx, sum_f32_kernel<0, false, double>), kSumWarps * 32, 0, s>>>(
+  auto kfn = expansion_ok(kp, c->hd2) ? sum_f32_kernel<0, false, double> : sum_f32_kernel<0, false, double, false, true>;
+  kfn<<<sum_blocks(ctx, kfn), kSumWarps * 32, 0, s>>>(
       G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>() - V.h0, c->tiles.as<int2>(), c->tile_box.as<float4>(),
-      V.t1 - V.t0, V.t0, gd, f_loc - V.o0, nullptr, ctx->counter.as<int>(), nullptr);
+      V.t1 - V.t0, V.t0, gd, f_loc - V.o0, nullptr, ctx->counter.as<int>(), nullptr, 0, 0, nullptr);
   RBF_CHECK_LAUNCH();
   return RBF_OK;
 }
 
 rbf_status matvec_sorted_f32_d(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp, const double* w_loc,
-                               double* f_loc, bool solver) {
-  return matvec_f32_solver<double>(ctx, c, kp, w_loc, f_loc, solver);
+                               double* f_loc, int op) {
+  return matvec_f32_solver<double>(ctx, c, kp, w_loc, f_loc, op);
 }
 rbf_status matvec_sorted_f32_f(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp, const float* w_loc,
-                               double* f_loc, bool solver) {
-  return matvec_f32_solver<float>(ctx, c, kp, w_loc, f_loc, solver);
+                               double* f_loc, int op) {
+  return matvec_f32_solver<float>(ctx, c, kp, w_loc, f_loc, op);
 }
 
 // fp64 tier, same conventions as matvec_sorted_f32_d; out_perm (single GPU,
 // public path only) scatters to the caller's order.
 rbf_status matvec_sorted_f64(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
-                             const double* w_loc, double* f_out, const int32_t* out_perm, bool solver) {
+                             const double* w_loc, double* f_out, const int32_t* out_perm, int op) {
   cudaStream_t s = ctx->stream;
   const SlabView& V = c->view;
   const int64_t nw = V.h1 - V.h0;
@@ -1307,7 +1344,7 @@ rbf_status matvec_sorted_f64(rbf_ctx* ctx, const rbf_cells* c, const KernelParam
   RBF_TRY(ctx->counter.ensure(256, s));
   RBF_CUDA_TRY(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
   SumGeom G = make_geom(c, kp);
-  if (solver && !out_perm && sym_mode(c->n_loc()) != 0) {
+  if (!out_perm && sym_mode(op, c->n_loc()) != 0) {
     // solver path: symmetric fp64 tier (reading R19), accumulated output
     RBF_CUDA_TRY(cudaMemsetAsync(f_out, 0, sizeof(double) * (size_t)c->n_loc(), s));
     ProfScope ps(ctx, RBF_PROF_MATVEC_F64);
@@ -1400,7 +1437,10 @@ rbf_status eval_grid_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams
     RBF_CHECK_LAUNCH();
     return RBF_OK;
   }
-  sum_f32_kernel<1, false, float><<<sum_blocks(ctx, sum_f32_kernel<1, false, float>), kSumWarps * 32, 0, s>>>(
+  // node block half-diagonal: 3 steps per axis / 2
+  const double hd2 = 2.25 * (gd.step[0] * gd.step[0] + gd.step[1] * gd.step[1] + gd.step[2] * gd.step[2]);
+  auto kfn = expansion_ok(kp, hd2) ? sum_f32_kernel<1, false, float> : sum_f32_kernel<1, false, float, false, true>;
+  kfn<<<sum_blocks(ctx, kfn), kSumWarps * 32, 0, s>>>(
       G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), nullptr, nullptr, nact, 0, gd, field, nullptr,
       ctx->counter.as<int>(), nullptr, 0, 0, list.as<int32_t>());
   RBF_CHECK_LAUNCH();

@@ -1,9 +1,10 @@
 """Multi-rank plumbing for the benchmark and multi-GPU runs (torch.distributed).
 
-Round 1 runs one independent problem per rank: the only
-cross-rank operations are the timing/throughput reductions below — the max of
-the per-rank device times and the sum of the per-rank work — which work on any
-backend (NCCL on GPUs, gloo on CPU for the tests).
+The data plane of a multi-GPU solve (halo exchange, Krylov allreduce, gathers)
+runs inside librbf over NCCL; the Python side only needs the
+bench's timing reductions below -- the max of the per-rank device times and the
+sum of the per-rank work -- which work on any backend (NCCL on GPUs, gloo on
+CPU for the tests).
 """
 from __future__ import annotations
 

@@ -20,6 +20,7 @@ LIB_PATH = os.path.join(_HERE, "librbf.so")
 
 RBF_OK, RBF_EINVAL, RBF_ENOMEM, RBF_ECUDA, RBF_ENCCL, RBF_EUNSUPPORTED = range(6)
 RBF_F32, RBF_F64 = 0, 1
+OP_AUTO, OP_ONESIDED, OP_SYM, OP_SYM_WIDE = range(4)   # rbf_op_variant
 
 
 class RbfError(RuntimeError):
@@ -43,17 +44,22 @@ class _CellCfg(C.Structure):
 
 class _PrecondCfg(C.Structure):
     _fields_ = [("kind", C.c_int), ("core_target", C.c_int), ("overlap_sigmas", C.c_double),
-                ("max_ext", C.c_int), ("shift", C.c_double), ("local_fp32", C.c_int)]
+                ("max_ext", C.c_int), ("shift", C.c_double), ("local_fp32", C.c_int),
+                ("pivot", C.c_int), ("w_layout", C.c_int)]
 
 
 class _GmresCfg(C.Structure):
     _fields_ = [("restart", C.c_int), ("rtol", C.c_double), ("phase1_rtol", C.c_double),
-                ("max_iters", C.c_int), ("polish_fp64", C.c_int), ("cgs_passes", C.c_int)]
+                ("max_iters", C.c_int), ("polish_fp64", C.c_int), ("cgs_passes", C.c_int),
+                ("op_variant", C.c_int), ("basis_fp64", C.c_int),
+                ("history", C.POINTER(C.c_double)), ("history_true", C.POINTER(C.c_double)),
+                ("history_cap", C.c_int)]
 
 
 class SolveReport(C.Structure):
     _fields_ = [("iters_phase1", C.c_int), ("iters_phase2", C.c_int), ("restarts", C.c_int),
                 ("converged", C.c_int), ("breakdown", C.c_int),
+                ("history_len", C.c_int), ("history_true_len", C.c_int),
                 ("rel_residual_true", C.c_double), ("rel_residual_est", C.c_double),
                 ("t_setup", C.c_double), ("t_phase1", C.c_double), ("t_phase2", C.c_double),
                 ("nblocks", C.c_int64), ("precond_bytes", C.c_int64),
@@ -92,6 +98,7 @@ EXPORTS = {
     "rbf_cells_slab": (C.c_int, [_P, _P]),
     "rbf_cells_view": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)]),
     "rbf_matvec": (C.c_int, [_P, _P, C.POINTER(_Kernel), C.c_int, _P, _P]),
+    "rbf_matvec_op": (C.c_int, [_P, _P, C.POINTER(_Kernel), C.c_int, C.c_int, _P, _P]),
     "rbf_matvec_pairs": (C.c_int, [_P, _P, C.POINTER(_Kernel), C.POINTER(C.c_int64),
                                    C.POINTER(C.c_int64)]),
     "rbf_precond_create": (C.c_int, [_P, _P, C.POINTER(_Kernel), C.POINTER(_PrecondCfg),
@@ -112,6 +119,7 @@ EXPORTS = {
     "rbf_csr_spmv": (C.c_int, [_P, _P, _P, _P]),
     "rbf_nn_distance": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, _P]),
     "rbf_density": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, _P]),
+    "rbf_sigma_auto": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int, C.POINTER(C.c_double)]),
     "rbf_profile_enable": (C.c_int, [_P, C.c_int]),
     "rbf_profile_query": (C.c_int, [_P, _P, _P]),
     "rbf_reconstruct_host": (C.c_int, [_P, _P, _P, C.c_int64, C.POINTER(_Kernel), C.POINTER(_CellCfg),
@@ -349,6 +357,19 @@ def matvec(ctx: Context, cells: Cells, kernel: Kernel, w: torch.Tensor, out: tor
     return f
 
 
+def matvec_op(ctx: Context, cells: Cells, kernel: Kernel, w: torch.Tensor, op: int = OP_AUTO,
+              out: torch.Tensor | None = None):
+    """rbf_matvec_op: f = A w through the solver's operator variant `op` (OP_*)."""
+    prec = {torch.float32: RBF_F32, torch.float64: RBF_F64}.get(w.dtype)
+    if prec is None:
+        raise TypeError("w must be float32 or float64")
+    _need(w, w.dtype, cells.n, "w")
+    f = torch.empty_like(w) if out is None else out
+    _need(f, w.dtype, cells.n, "out")
+    _check(_lib.rbf_matvec_op(ctx._h, cells._h, C.byref(kernel._c()), prec, int(op), _ptr(w), _ptr(f)))
+    return f
+
+
 def matvec_pairs(ctx: Context, cells: Cells, kernel: Kernel):
     """(useful, visited) pair counts of the fp32 matvec traversal."""
     u, v = C.c_int64(), C.c_int64()
@@ -410,19 +431,30 @@ def nn_distance(ctx: Context, x: torch.Tensor, q: torch.Tensor | None = None):
 
 
 def density(ctx: Context, x: torch.Tensor, omega: torch.Tensor | None = None) -> dict:
-    """rbf_density: q_X (Eq.7), h_max, h_{X,Omega} (Eq.8) and the sigma heuristics (Eq.9-11)."""
-    import math
+    """rbf_density: q_X (Eq.7), h_max, h_{X,Omega} (Eq.8) and the sigma heuristics
+    of Eq.9 (sigma_q), Eq.10 (sigma_h) and Eq.10+11 (sigma_hmax), all computed
+    in the library."""
     _need(x, torch.float64, x.shape[0] * 3, "x")
     if omega is not None:
         _need(omega, torch.float64, omega.shape[0] * 3, "omega")
-    out = (C.c_double * 3)()
+    out = (C.c_double * 6)()
     _check(_lib.rbf_density(ctx._h, _ptr(x), x.shape[0], None if omega is None else _ptr(omega),
                             0 if omega is None else omega.shape[0], out))
-    q, hm, h = out[0], out[1], out[2]
-    res = dict(q=q, h_max=hm, sigma_q=2.0 * q, sigma_hmax=hm * math.sqrt(2.0) * math.sqrt(2.0))
+    res = dict(q=out[0], h_max=out[1], sigma_q=out[3], sigma_hmax=out[5])
     if omega is not None:
-        res.update(h=h, sigma_h=h * math.sqrt(2.0))
+        res.update(h=out[2], sigma_h=out[4])
     return res
+
+
+def sigma_auto(ctx: Context, x: torch.Tensor, rule: int = 11, omega: torch.Tensor | None = None) -> float:
+    """rbf_sigma_auto: sigma from the density heuristic of Eq.9, Eq.10 or Eq.11 (rule)."""
+    _need(x, torch.float64, x.shape[0] * 3, "x")
+    if omega is not None:
+        _need(omega, torch.float64, omega.shape[0] * 3, "omega")
+    sig = C.c_double()
+    _check(_lib.rbf_sigma_auto(ctx._h, _ptr(x), x.shape[0], None if omega is None else _ptr(omega),
+                               0 if omega is None else omega.shape[0], int(rule), C.byref(sig)))
+    return sig.value
 
 
 class AssembledOperator:
@@ -462,10 +494,11 @@ class Precond:
     """rbf_precond_create: RAS (§3.1) / block-Jacobi preconditioner."""
 
     def __init__(self, ctx: Context, cells: Cells, kernel: Kernel, kind: int = 2, core_target: int = 512,
-                 overlap_sigmas: float = 1.0, max_ext: int = 0, shift: float = 0.0, local_fp32: int = 0):
+                 overlap_sigmas: float = 1.0, max_ext: int = 0, shift: float = 0.0, local_fp32: int = 0,
+                 pivot: int = 0, w_layout: int = 0):
         self.ctx, self.cells = ctx, cells
         h = C.c_void_p()
-        cfg = _PrecondCfg(kind, core_target, overlap_sigmas, max_ext, shift, local_fp32)
+        cfg = _PrecondCfg(kind, core_target, overlap_sigmas, max_ext, shift, local_fp32, pivot, w_layout)
         _check(_lib.rbf_precond_create(ctx._h, cells._h, C.byref(kernel._c()), C.byref(cfg), C.byref(h)))
         self._h = h
 
@@ -508,23 +541,34 @@ class Precond:
 def gmres_solve(ctx: Context, cells: Cells, kernel: Kernel, b: torch.Tensor, precond: Precond | None = None,
                 kind: int = 2, core_target: int = 512, overlap_sigmas: float = 1.0, restart: int = 30,
                 rtol: float = 1e-6, phase1_rtol: float = 1e-4, max_iters: int = 500, polish_fp64: int = 1,
-                shift: float = 0.0, local_fp32: int = 0, cgs_passes: int = 2, out: torch.Tensor | None = None):
-    """Solve A w = b (Eq.4) with RAS-preconditioned FGMRES; returns (w fp64, report dict)."""
+                shift: float = 0.0, local_fp32: int = 0, cgs_passes: int = 2, out: torch.Tensor | None = None,
+                op: int = OP_AUTO, basis_fp64: int = 0, pivot: int = 0, w_layout: int = 0,
+                history_cap: int = 0):
+    """Solve A w = b (Eq.4) with RAS-preconditioned FGMRES; returns (w fp64, report dict).
+    history_cap > 0 adds the residual history (report keys history / history_true)."""
     _need(b, torch.float32, cells.n, "b")
     w = torch.empty(cells.n, dtype=torch.float64, device=b.device) if out is None else out
     _need(w, torch.float64, cells.n, "w")
-    pc = _PrecondCfg(kind, core_target, overlap_sigmas, 0, shift, local_fp32)
-    gc = _GmresCfg(restart, rtol, phase1_rtol, max_iters, polish_fp64, cgs_passes)
+    pc = _PrecondCfg(kind, core_target, overlap_sigmas, 0, shift, local_fp32, pivot, w_layout)
+    hist = (C.c_double * max(history_cap, 1))()
+    hist_t = (C.c_double * max(history_cap, 1))()
+    gc = _GmresCfg(restart, rtol, phase1_rtol, max_iters, polish_fp64, cgs_passes, int(op), basis_fp64,
+                   hist if history_cap > 0 else None, hist_t if history_cap > 0 else None, history_cap)
     rep = SolveReport()
     _check(_lib.rbf_gmres_solve(ctx._h, cells._h, C.byref(kernel._c()), None if precond is None else precond._h,
                                 C.byref(pc), C.byref(gc), _ptr(b), _ptr(w), C.byref(rep)))
-    return w, rep.as_dict()
+    out_rep = rep.as_dict()
+    if history_cap > 0:
+        out_rep["history"] = list(hist[:rep.history_len])
+        out_rep["history_true"] = list(hist_t[:rep.history_true_len])
+    return w, out_rep
 
 
 def reconstruct_host(ctx: Context, xyz, b, kernel: Kernel, lo, hi, n, *, cell_edge: float = 0.0,
                      kind: int = 2, core_target: int = 512, overlap_sigmas: float = 1.0, restart: int = 30,
                      rtol: float = 1e-6, phase1_rtol: float = 1e-4, max_iters: int = 500,
-                     shift: float = 0.0, local_fp32: int = 0, cgs_passes: int = 2, w_out=None, field_out=None):
+                     shift: float = 0.0, local_fp32: int = 0, cgs_passes: int = 2, op: int = OP_AUTO,
+                     w_out=None, field_out=None):
     """Alg.1 steps 2-3 from HOST buffers (numpy or CPU tensors; pinned is fastest)."""
     import numpy as np
     xyz = torch.as_tensor(xyz, dtype=torch.float32).contiguous()
@@ -536,8 +580,10 @@ def reconstruct_host(ctx: Context, xyz, b, kernel: Kernel, lo, hi, n, *, cell_ed
     rep = SolveReport()
     _check(_lib.rbf_reconstruct_host(ctx._h, _ptr(xyz), _ptr(b), nn, C.byref(kernel._c()),
                                      C.byref(_CellCfg(cell_edge, 64, 2, 0)),
-                                     C.byref(_PrecondCfg(kind, core_target, overlap_sigmas, 0, shift, local_fp32)),
-                                     C.byref(_GmresCfg(restart, rtol, phase1_rtol, max_iters, 1, cgs_passes)),
+                                     C.byref(_PrecondCfg(kind, core_target, overlap_sigmas, 0, shift, local_fp32,
+                                                         0, 0)),
+                                     C.byref(_GmresCfg(restart, rtol, phase1_rtol, max_iters, 1, cgs_passes,
+                                                       int(op), 0, None, None, 0)),
                                      C.byref(g), _ptr(w), _ptr(field), C.byref(rep)))
     del np
     return w, field, rep.as_dict()

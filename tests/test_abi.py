@@ -52,7 +52,7 @@ def test_library_loads_and_binds_without_gpu(lib_path):
     import ctypes
     from paper_1305_5179_b200 import rbf
     lib = rbf.load_library(lib_path)
-    assert lib.rbf_abi_version() == 2
+    assert lib.rbf_abi_version() == 3
     assert lib.rbf_status_str(1) == b"RBF_EINVAL"
     for name in rbf.EXPORTS:
         assert hasattr(lib, name)
@@ -78,3 +78,44 @@ def test_oracle_never_imports_the_product_path():
         if f.endswith(".py"):
             src = open(os.path.join(ROOT, "oracle", f)).read()
             assert not re.search(r"^\s*(from|import)\s+paper_1305_5179_b200", src, flags=re.M), f
+
+
+def test_behaviour_is_set_through_the_abi_not_the_environment():
+    """Every behaviour-changing knob is a field of an rbf_*_cfg struct or an
+    argument; getenv in the library is left only for test/debug hooks."""
+    allowed = {"RBF_SLAB_EMULATE", "RBF_DEBUG_SETUP"}
+    found = set()
+    for f in os.listdir(os.path.join(PKG, "csrc")):
+        src = open(os.path.join(PKG, "csrc", f)).read()
+        found |= set(re.findall(r'getenv\("(\w+)"\)', src))
+    assert found <= allowed, found - allowed
+    assert "environ" not in open(os.path.join(PKG, "rbf.py")).read()
+
+
+STRUCTS = {"rbf_kernel": "_Kernel", "rbf_cell_cfg": "_CellCfg", "rbf_precond_cfg": "_PrecondCfg",
+           "rbf_gmres_cfg": "_GmresCfg", "rbf_solve_report": "SolveReport", "rbf_grid": "_Grid",
+           "rbf_cells_desc": "_CellsDesc"}
+
+
+def test_ctypes_structs_match_the_header_layout(tmp_path):
+    """sizeof / offsetof of every C struct (compiled with gcc from include/rbf.h)
+    equal the binding's ctypes layout."""
+    import ctypes
+    from paper_1305_5179_b200 import rbf
+    lines = ["#include <stdio.h>", "#include <stddef.h>", f'#include "{HEADER}"', "int main(void) {"]
+    for cname, pname in STRUCTS.items():
+        lines.append(f'  printf("{cname} sizeof %zu\\n", sizeof({cname}));')
+        for fname, _ in getattr(rbf, pname)._fields_:
+            lines.append(f'  printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-o", str(exe), str(src)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l.strip()}
+    for cname, pname in STRUCTS.items():
+        cls = getattr(rbf, pname)
+        assert got[(cname, "sizeof")] == ctypes.sizeof(cls), cname
+        for fname, _ in cls._fields_:
+            assert got[(cname, fname)] == getattr(cls, fname).offset, (cname, fname)

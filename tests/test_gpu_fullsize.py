@@ -2,14 +2,16 @@
 
 c4 (configs[3]: 1M surface points -> 3M centres, sigma 0.01, 256^3 grid) and c3
 (configs[2]: 200k points with a 10x density ramp -> 600k centres): the oracle
-cannot run the full products, so it computes SAMPLED outputs one by one (rows of
-the matvec, nodes of the grid) on all host cores; integer work (extension, cell
-lists) is compared in full, bit for bit.  Tolerances as in test_gpu_hotpath.py
-(DESIGN.md §9): fp32 tier per row <= 5e-5 g_i, fp64 tier per row <= 1e-12 g_i,
-grid per node <= 5e-5 g(xi) with exact zeros where no centre is in range.
+cannot run the full products, so it computes SAMPLED outputs one by one -- 10^4
+rows of the matvec and 10^4 nodes of the grid (+ 2000 non-zero nodes), each row
+the exact truncated sum of oracle.kernel.matvec_local (pinned against brute
+force in tests/test_oracle_kernel.py); integer work (extension, cell lists) is
+compared in full, bit for bit.  Weights: random N(0,1) AND the benchmarked
+solve's fitted weights (the harder case: ||w|| >> ||b||).
+Tolerances as in test_gpu_hotpath.py: fp32 tier per row <= 5e-5
+g_i, fp64 tier per row <= 1e-12 g_i, grid per node <= 5e-5 g(xi), exact zeros
+where no centre is in range, |F_gpu - F_ref|_inf <= 1e-3 max|b| (reading R3).
 """
-import os
-
 import numpy as np
 import pytest
 import torch
@@ -21,7 +23,7 @@ from oracle import kernel as OK
 from synth import make_inputs
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
-PROCS = os.cpu_count() or 1
+ROWS = 10_000
 
 
 @pytest.fixture(scope="module")
@@ -45,7 +47,14 @@ def big(request, R, ctx):
     X = OE.extend(d["x"], d["normals"], d["delta"])
     kern = R.Kernel(d["sigma"])
     cells = R.Cells(ctx, centres, kern)
-    return dict(name=request.param, d=d, X=X, centres=centres, b=b, kern=kern, cells=cells, sigma=d["sigma"])
+    # the benchmarked fit (bench.py: 50 iterations, shifted block-Jacobi)
+    cfg = d["cfg"]
+    w, rep = R.gmres_solve(ctx, cells, kern, b, restart=cfg.restart, rtol=1e-6, kind=cfg.precond_kind,
+                           core_target=cfg.core_target, overlap_sigmas=cfg.overlap_sigmas, shift=cfg.shift,
+                           local_fp32=cfg.local_fp32, cgs_passes=cfg.cgs_passes, max_iters=50)
+    torch.cuda.synchronize()
+    return dict(name=request.param, d=d, X=X, centres=centres, b=b, kern=kern, cells=cells, sigma=d["sigma"],
+                w_fit=w.cpu().numpy(), rep=rep)
 
 
 def _rows(n, k, seed):
@@ -62,69 +71,116 @@ def test_extension_and_cells_bit_exact(big):
     np.testing.assert_array_equal(v["cell_start"].cpu().numpy()[:-1], oc["cell_start"])
 
 
-def test_matvec_sampled_rows(R, ctx, big):
+@pytest.mark.parametrize("weights", ["random", "fitted"])
+def test_matvec_sampled_rows(R, ctx, big, weights):
+    """Public fp32/fp64 products and the solver's operator as benchmarked
+    (OP_AUTO: the symmetric wide-plan kernel at these sizes, reading R19) on 10^4
+    sampled rows.  rel-L2 <= 1e-4 is the north star's matvec gate; with fitted
+    weights f = A w ~ b is small against the terms (||w||/||b|| ~ 1e5), so the
+    per-row bound relative to g_i = a sum_j |A_ij w_j| is the binding one and
+    the rel-L2 of the fp32 tier is reported against g."""
     X, sigma = big["X"], big["sigma"]
     n = len(X)
-    w = np.random.default_rng(7).normal(size=n)
-    f32 = R.matvec(ctx, big["cells"], big["kern"], torch.as_tensor(w, dtype=torch.float32, device="cuda"))
-    f64 = R.matvec(ctx, big["cells"], big["kern"], torch.as_tensor(w, device="cuda"))
-    f32, f64 = f32.cpu().numpy(), f64.cpu().numpy()
-    rows = _rows(n, 192, 1)
+    w = np.random.default_rng(7).normal(size=n) if weights == "random" else big["w_fit"]
+    rows = _rows(n, ROWS, 1)
     w32 = w.astype(np.float32).astype(np.float64)
-    ref32 = OK.matvec_parallel(X, w32, sigma, rows=rows, procs=PROCS)
-    ref64 = OK.matvec_parallel(X, w, sigma, rows=rows, procs=PROCS)
-    g = OK.matvec_parallel(X, np.abs(w), sigma, rows=rows, procs=PROCS)
-    assert (np.abs(f32[rows] - ref32) <= 5e-5 * g).all()
-    assert np.linalg.norm(f32[rows] - ref32) / np.linalg.norm(ref32) <= 1e-4
-    assert (np.abs(f64[rows] - ref64) <= 1e-12 * g).all()
-    # the solver's operators as benchmarked (symmetric variants at this size, reading R19)
-    os.environ["RBF_PUBLIC_SYM"] = "1"
-    try:
-        s32 = R.matvec(ctx, big["cells"], big["kern"], torch.as_tensor(w, dtype=torch.float32, device="cuda"))
-        s64 = R.matvec(ctx, big["cells"], big["kern"], torch.as_tensor(w, device="cuda"))
-    finally:
-        del os.environ["RBF_PUBLIC_SYM"]
-    s32, s64 = s32.cpu().numpy(), s64.cpu().numpy()
-    assert (np.abs(s32[rows] - ref32) <= 5e-5 * g).all()
-    assert np.linalg.norm(s32[rows] - ref32) / np.linalg.norm(ref32) <= 1e-4
-    assert (np.abs(s64[rows] - ref64) <= 1e-12 * g).all()
+    ref32 = OK.matvec_local(X, w32, sigma, rows=rows)
+    ref64 = OK.matvec_local(X, w, sigma, rows=rows)
+    g = OK.matvec_local(X, np.abs(w), sigma, rows=rows)
+    for op in (None, R.OP_AUTO):
+        if op is None:
+            f32 = R.matvec(ctx, big["cells"], big["kern"], torch.as_tensor(w, dtype=torch.float32, device="cuda"))
+            f64 = R.matvec(ctx, big["cells"], big["kern"], torch.as_tensor(w, device="cuda"))
+        else:
+            f32 = R.matvec_op(ctx, big["cells"], big["kern"], torch.as_tensor(w, dtype=torch.float32, device="cuda"),
+                              op=op)
+            f64 = R.matvec_op(ctx, big["cells"], big["kern"], torch.as_tensor(w, device="cuda"), op=op)
+        f32, f64 = f32.cpu().numpy()[rows], f64.cpu().numpy()[rows]
+        assert (np.abs(f32 - ref32) <= 5e-5 * g).all(), (op, np.max(np.abs(f32 - ref32) / g))
+        assert (np.abs(f64 - ref64) <= 1e-12 * g).all(), (op, np.max(np.abs(f64 - ref64) / g))
+        if weights == "random":
+            assert np.linalg.norm(f32 - ref32) / np.linalg.norm(ref32) <= 1e-4
+        else:
+            assert np.linalg.norm(f32 - ref32) / np.linalg.norm(g) <= 1e-5
 
 
 def test_solve_as_benchmarked(R, ctx, big):
     """The bench's fit (50 iterations, shifted block-Jacobi): the reported true
     residual is ||b - A w|| / ||b|| of the fp64 tier, whose rows match the oracle."""
-    cfg = big["d"]["cfg"]
-    w, rep = R.gmres_solve(ctx, big["cells"], big["kern"], big["b"], restart=cfg.restart, rtol=1e-6,
-                           kind=cfg.precond_kind, core_target=cfg.core_target, overlap_sigmas=cfg.overlap_sigmas,
-                           shift=cfg.shift, local_fp32=cfg.local_fp32, max_iters=50)
+    rep = big["rep"]
     assert rep["iters_phase1"] + rep["iters_phase2"] <= 50
+    w = torch.as_tensor(big["w_fit"], device="cuda")
     Aw = R.matvec(ctx, big["cells"], big["kern"], w).cpu().numpy()
     b = big["b"].cpu().numpy().astype(np.float64)
     res = np.linalg.norm(b - Aw) / np.linalg.norm(b)
     assert res == pytest.approx(rep["rel_residual_true"], rel=1e-9)
     assert res < 1e-2                                       # the fit makes progress (finding F4)
-    wh = w.cpu().numpy()
-    rows = _rows(len(b), 96, 2)
-    ref = OK.matvec_parallel(big["X"], wh, big["sigma"], rows=rows, procs=PROCS)
-    g = OK.matvec_parallel(big["X"], np.abs(wh), big["sigma"], rows=rows, procs=PROCS)
+    rows = _rows(len(b), ROWS, 2)
+    ref = OK.matvec_local(big["X"], big["w_fit"], big["sigma"], rows=rows)
+    g = OK.matvec_local(big["X"], np.abs(big["w_fit"]), big["sigma"], rows=rows)
     assert (np.abs(Aw[rows] - ref) <= 1e-12 * g).all()
+    # the sampled residual agrees with the full one (sampling error only)
+    rs = np.linalg.norm(b[rows] - ref) / np.linalg.norm(b[rows])
+    assert rs == pytest.approx(res, rel=0.1)
 
 
-def test_grid_sampled_nodes(R, ctx, big):
-    d = big["d"]
-    lo, hi, gn = d["grid_lo"], d["grid_hi"], d["grid_n"]
-    w = np.random.default_rng(9).normal(size=len(big["X"]))
+def _grid_check(R, ctx, big, w, lo, hi, gn, seed):
     F = R.eval_grid(ctx, big["cells"], big["kern"], torch.as_tensor(w, device="cuda"), lo, hi, gn)
     F = F.cpu().numpy().ravel()
-    rng = np.random.default_rng(3)
+    rng = np.random.default_rng(seed)
     nz = np.nonzero(F)[0]
-    flat = np.sort(np.concatenate([rng.choice(F.size, 64, replace=False), rng.choice(nz, 192, replace=False)]))
+    flat = np.unique(np.concatenate([rng.choice(F.size, min(ROWS, F.size), replace=False),
+                                     rng.choice(nz, min(2000, nz.size), replace=False)]))
     P = OG.nodes(lo, hi, gn, flat=flat)
     w32 = w.astype(np.float32).astype(np.float64)        # the grid tier rounds w to fp32
-    ref = OK.matvec_parallel(big["X"], w32, big["sigma"], targets=P, procs=PROCS)
-    g = OK.matvec_parallel(big["X"], np.abs(w32), big["sigma"], targets=P, procs=PROCS)
-    assert (np.abs(F[flat] - ref) <= 5e-5 * g).all()
+    ref = OK.matvec_local(big["X"], w32, big["sigma"], targets=P)
+    g = OK.matvec_local(big["X"], np.abs(w32), big["sigma"], targets=P)
+    assert (np.abs(F[flat] - ref) <= 5e-5 * g).all(), np.max(np.abs(F[flat] - ref) / np.maximum(g, 1e-300))
     # exact zeros where no centre lies within c (1 + 1e-5) (reading R5: fp32 boundary flips)
-    g_wide = OK.matvec_parallel(big["X"], np.ones(len(big["X"])), big["sigma"], cutoff_sigmas=6 * (1 + 1e-5),
-                                targets=P, procs=PROCS)
+    g_wide = OK.matvec_local(big["X"], np.ones(len(big["X"])), big["sigma"], cutoff_sigmas=6 * (1 + 1e-5),
+                             targets=P)
     assert (F[flat][g_wide == 0] == 0).all()
+    return F, flat, ref
+
+
+def test_grid_sampled_nodes_random_weights(R, ctx, big):
+    d = big["d"]
+    w = np.random.default_rng(9).normal(size=len(big["X"]))
+    _grid_check(R, ctx, big, w, d["grid_lo"], d["grid_hi"], d["grid_n"], 3)
+
+
+def test_grid_from_fitted_weights(R, ctx, big):
+    """The bench's grid: F from the fitted weights at 10^4 + 2000 sampled nodes,
+    gate |F_gpu - F_ref|_inf <= 1e-3 max|b| (reading R3) and per node 5e-5 g."""
+    d = big["d"]
+    F, flat, ref = _grid_check(R, ctx, big, big["w_fit"], d["grid_lo"], d["grid_hi"], d["grid_n"], 4)
+    bmax = float(np.abs(big["b"].cpu().numpy()).max())
+    assert np.abs(F[flat] - ref).max() <= 1e-3 * bmax
+
+
+def test_grid_coarse_steps_take_the_difference_form(R, ctx, big):
+    """A 32^3 grid over c4/c3 has a step of ~5-7 sigma: the node-block half-
+    diagonal |t'|^2 (~150) would overflow the expansion form's 2^-|t'|^2 factor,
+    so the library evaluates these blocks by the difference form (summation.cu
+    expansion_ok).  Same gates as the fine grid, fitted and random weights."""
+    d = big["d"]
+    lo, hi = d["grid_lo"], d["grid_hi"]
+    for w, seed in ((big["w_fit"], 5), (np.random.default_rng(11).normal(size=len(big["X"])), 6)):
+        F, flat, ref = _grid_check(R, ctx, big, w, lo, hi, (32, 32, 32), seed)
+        assert np.isfinite(F).all()
+
+
+def test_matvec_large_cell_edge_difference_form(R, ctx, big):
+    """Cells with edge = cutoff (tile half-diagonal ~7 sigma: |t'|^2 ~ 39 > 16)
+    take the difference form in the public product and the solver's operator."""
+    X, sigma = big["X"], big["sigma"]
+    cells = R.Cells(ctx, big["centres"], big["kern"], cell_edge=6 * sigma)
+    w = np.random.default_rng(8).normal(size=len(X))
+    rows = _rows(len(X), 2000, 3)
+    ref = OK.matvec_local(X, w.astype(np.float32).astype(np.float64), sigma, rows=rows)
+    g = OK.matvec_local(X, np.abs(w), sigma, rows=rows)
+    wt = torch.as_tensor(w, dtype=torch.float32, device="cuda")
+    for f in (R.matvec(ctx, cells, big["kern"], wt), R.matvec_op(ctx, cells, big["kern"], wt, op=R.OP_AUTO)):
+        f = f.cpu().numpy()[rows]
+        assert np.isfinite(f).all()
+        assert (np.abs(f - ref) <= 5e-5 * g).all()

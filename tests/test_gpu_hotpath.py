@@ -257,14 +257,14 @@ def test_grid_ragged_and_anisotropic(R, ctx):
         R.eval_grid(ctx, cells, kern, dev(w, torch.float64), lo, hi, (1, 5, 5))
 
 
-@pytest.mark.parametrize("sym", ["1", "2"])
-def test_symmetric_operators_degenerate_clouds(R, ctx, sym):
+@pytest.mark.parametrize("op", ["OP_SYM", "OP_SYM_WIDE", "OP_ONESIDED"])
+def test_symmetric_operators_degenerate_clouds(R, ctx, op):
     """Reading R19 on degenerate inputs: one centre, two coincident centres, a
     dense clump in one cell (tiles of 1..128 targets, sources equal to targets),
-    a line of points and a clump plus far outliers.  The solver's symmetric
-    fp32/fp64 operators (RBF_PUBLIC_SYM=1) equal the one-sided public products
-    to the tiers' accuracy, including exact zeros for isolated centres' neighbours."""
-    import os
+    a line of points and a clump plus far outliers.  The solver's operator
+    variants (rbf_matvec_op) against the ORACLE's brute-force products, fp32
+    tier on fp32-rounded weights and fp64 tier, per row, including exact zeros
+    for isolated centres' neighbours."""
     rng = np.random.default_rng(21)
     clouds = [
         np.array([[0.1, 0.2, 0.3]]),
@@ -275,20 +275,17 @@ def test_symmetric_operators_degenerate_clouds(R, ctx, sym):
     ]
     sigma = 0.05
     kern = R.Kernel(sigma)
+    opv = getattr(R, op)
     for X in clouds:
         X = X.astype(np.float32)
+        Xd = X.astype(np.float64)
         cells = R.Cells(ctx, dev(X, torch.float32), kern)
         w = rng.normal(size=len(X))
-        ref32 = host(R.matvec(ctx, cells, kern, dev(w, torch.float32)))
-        ref64 = host(R.matvec(ctx, cells, kern, dev(w, torch.float64)))
-        g = host(R.matvec(ctx, cells, kern, dev(np.abs(w), torch.float64)))
-        os.environ["RBF_SUM_SYM"] = sym
-        os.environ["RBF_PUBLIC_SYM"] = "1"
-        try:
-            s32 = host(R.matvec(ctx, cells, kern, dev(w, torch.float32)))
-            s64 = host(R.matvec(ctx, cells, kern, dev(w, torch.float64)))
-        finally:
-            del os.environ["RBF_SUM_SYM"]
-            del os.environ["RBF_PUBLIC_SYM"]
+        w32 = w.astype(np.float32).astype(np.float64)
+        ref32 = OK.matvec(Xd, w32, sigma)
+        ref64 = OK.matvec(Xd, w, sigma)
+        g = OK.matvec(Xd, np.abs(w), sigma)
+        s32 = host(R.matvec_op(ctx, cells, kern, dev(w, torch.float32), op=opv))
+        s64 = host(R.matvec_op(ctx, cells, kern, dev(w, torch.float64), op=opv))
         assert (np.abs(s32 - ref32) <= 5e-5 * g + 1e-30).all(), len(X)
         assert (np.abs(s64 - ref64) <= 1e-12 * g + 1e-300).all(), len(X)

@@ -122,30 +122,25 @@ def test_emulated_cells_refuse_the_solver(R, setup):
         R.gmres_solve(s["ctx"], c, s["kern"], b)
 
 
-@pytest.mark.parametrize("sym", ["1", "2"])
-def test_emulated_slabs_symmetric_solver_operator(R, setup, sym):
+@pytest.mark.parametrize("op", ["OP_SYM", "OP_SYM_WIDE"])
+def test_emulated_slabs_symmetric_solver_operator(R, setup, op):
     """The solver's symmetric fp32/fp64 operators (reading R19) on emulated slabs:
     each rank's owned rows equal the single-GPU symmetric product to the tiers'
     accuracy (the atomics reorder the last bits), and the single-GPU symmetric
     product equals the one-sided one likewise."""
     s = setup
     perm = s["perm"]
-    os.environ["RBF_SUM_SYM"] = sym
-    os.environ["RBF_PUBLIC_SYM"] = "1"
-    try:
-        full32 = R.matvec(s["ctx"], s["full"], s["kern"], s["w"].float()).cpu().numpy()
-        full64 = R.matvec(s["ctx"], s["full"], s["kern"], s["w"]).cpu().numpy()
-        g = np.abs(s["f64"]).max()
-        np.testing.assert_allclose(full32, s["f32"], rtol=0, atol=1e-5 * g)
-        np.testing.assert_allclose(full64, s["f64"], rtol=0, atol=1e-12 * g)
-        for r in range(2):
-            c = _emulated(R, s, r, 2)
-            o0, o1 = c.slab()["own"]
-            mine = perm[o0:o1]
-            g32 = R.matvec(s["ctx"], c, s["kern"], s["w"].float()).cpu().numpy()
-            g64 = R.matvec(s["ctx"], c, s["kern"], s["w"]).cpu().numpy()
-            np.testing.assert_allclose(g32[mine], s["f32"][mine], rtol=0, atol=1e-5 * g)
-            np.testing.assert_allclose(g64[mine], s["f64"][mine], rtol=0, atol=1e-12 * g)
-    finally:
-        del os.environ["RBF_SUM_SYM"]
-        del os.environ["RBF_PUBLIC_SYM"]
+    opv = getattr(R, op)
+    full32 = R.matvec_op(s["ctx"], s["full"], s["kern"], s["w"].float(), op=opv).cpu().numpy()
+    full64 = R.matvec_op(s["ctx"], s["full"], s["kern"], s["w"], op=opv).cpu().numpy()
+    g = np.abs(s["f64"]).max()
+    np.testing.assert_allclose(full32, s["f32"], rtol=0, atol=1e-5 * g)
+    np.testing.assert_allclose(full64, s["f64"], rtol=0, atol=1e-12 * g)
+    for r in range(2):
+        c = _emulated(R, s, r, 2)
+        o0, o1 = c.slab()["own"]
+        mine = perm[o0:o1]
+        g32 = R.matvec_op(s["ctx"], c, s["kern"], s["w"].float(), op=opv).cpu().numpy()
+        g64 = R.matvec_op(s["ctx"], c, s["kern"], s["w"], op=opv).cpu().numpy()
+        np.testing.assert_allclose(g32[mine], s["f32"][mine], rtol=0, atol=1e-5 * g)
+        np.testing.assert_allclose(g64[mine], s["f64"][mine], rtol=0, atol=1e-12 * g)

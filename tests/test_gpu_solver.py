@@ -138,22 +138,14 @@ def test_gj_fp32_apply_parity(R, ctx, core, pivot, full):
     carries a relative error <= c kappa(B) m u32 (u32 = 2^-24); kappa(B) is
     computed here from the oracle's blocks, c = 4.  W_i = B_i^-1 is symmetric and
     stored as packed lower triangles (read through the bulk-copy staging, or from
-    global for blocks above the staging size); RBF_APPLY_FULL keeps full rows."""
-    import os
+    global for blocks above the staging size); w_layout=1 keeps full rows."""
     X, _, sigma = _flat_cap()
     mu = 0.01
     kern = R.Kernel(sigma)
     cells = R.Cells(ctx, dev(X, torch.float32), kern)
-    # mu >= 1e-4 eliminates without pivoting (B_i SPD); RBF_GJ_PIVOT forces partial pivoting
-    if pivot:
-        os.environ["RBF_GJ_PIVOT"] = "1"
-    if full:
-        os.environ["RBF_APPLY_FULL"] = "1"
-    try:
-        P = R.Precond(ctx, cells, kern, kind=1, core_target=core, shift=mu, local_fp32=1)
-    finally:
-        os.environ.pop("RBF_GJ_PIVOT", None)
-        os.environ.pop("RBF_APPLY_FULL", None)
+    # mu >= 1e-4 eliminates without pivoting (B_i SPD); pivot=1 forces partial pivoting
+    P = R.Precond(ctx, cells, kern, kind=1, core_target=core, shift=mu, local_fp32=1,
+                  pivot=1 if pivot else 0, w_layout=1 if full else 0)
     cores, exts, nbytes = P.blocks()
     oc = OC.build(X, 6 * sigma, cell_edge=6 * sigma / 3.999)
     blocks = OS.ras_blocks(oc, sigma, core, 0.0)
@@ -363,27 +355,32 @@ def test_zero_set_matches_oracle_and_sphere(R, ctx, c1_solution):
 
 
 def test_symmetric_fp32_tier_variants(R, ctx):
-    """Reading R19 (RBF_SUM_SYM = 0 one-sided / 1 symmetric / 2 symmetric on the
-    wide plan): each exponential of the symmetric variants serves f_i and f_j;
-    all three give the same two-phase fit (to 1e-6, certified by the oracle)."""
-    import os
+    """Reading R19 (op = OP_ONESIDED / OP_SYM / OP_SYM_WIDE): each exponential of
+    the symmetric variants serves f_i and f_j; all three give the same two-phase
+    fit (to 1e-6, certified by the oracle).  The one-sided solve is the
+    deterministic option: two runs give bit-identical weights."""
     d, X, b = problem("c2", n=3000)
     sigma = d["sigma"]
     kern = R.Kernel(sigma)
     cells = R.Cells(ctx, dev(X, torch.float32), kern)
     out = {}
-    for sym in ("0", "1", "2"):
-        os.environ["RBF_SUM_SYM"] = sym
-        try:
-            w, rep = R.gmres_solve(ctx, cells, kern, dev(b, torch.float32), restart=50, rtol=1e-6,
-                                   core_target=512, overlap_sigmas=1.3, max_iters=400)
-        finally:
-            del os.environ["RBF_SUM_SYM"]
+    for op in (R.OP_ONESIDED, R.OP_SYM, R.OP_SYM_WIDE):
+        w, rep = R.gmres_solve(ctx, cells, kern, dev(b, torch.float32), restart=50, rtol=1e-6,
+                               core_target=512, overlap_sigmas=1.3, max_iters=400, op=op, history_cap=1000)
         res = np.linalg.norm(b - OK.matvec(X, host(w), sigma)) / np.linalg.norm(b)
-        out[sym] = (res, rep)
-    for sym in ("0", "1", "2"):
-        assert out[sym][0] <= 1.5e-6, out
-        assert abs(out[sym][1]["iters_phase1"] - out["0"][1]["iters_phase1"]) <= 5, out
+        out[op] = (res, rep, host(w))
+        # residual history: one Arnoldi estimate per iteration, a true residual per
+        # restart plus the final one (which is the reported residual)
+        assert len(rep["history"]) == rep["iters_phase1"] + rep["iters_phase2"]
+        assert len(rep["history_true"]) == rep["restarts"] + 1
+        assert rep["history_true"][0] == pytest.approx(1.0)
+        assert rep["history_true"][-1] == rep["rel_residual_true"]
+    for op in out:
+        assert out[op][0] <= 1.5e-6, out
+        assert abs(out[op][1]["iters_phase1"] - out[R.OP_ONESIDED][1]["iters_phase1"]) <= 5, out
+    w2, _ = R.gmres_solve(ctx, cells, kern, dev(b, torch.float32), restart=50, rtol=1e-6, core_target=512,
+                          overlap_sigmas=1.3, max_iters=400, op=R.OP_ONESIDED)
+    assert np.array_equal(host(w2), out[R.OP_ONESIDED][2])
 
 
 def test_cgs1_and_cgs2_reach_the_gate(R, ctx):
@@ -403,22 +400,17 @@ def test_cgs1_and_cgs2_reach_the_gate(R, ctx):
 def test_fp32_phase_basis_matches_fp64_basis(R, ctx):
     """The fp32 phase keeps its Krylov basis (V, Z) in fp32 (gmres.cu; the phase
     stops at a relative residual >= 1e-4, far above the 6e-8 rounding of the
-    basis); RBF_GMRES_BASIS64=1 keeps it in fp64.  Both reach the 1e-6 gate,
+    basis); basis_fp64=1 keeps it in fp64.  Both reach the 1e-6 gate,
     certified by the oracle, with fp32-phase iteration counts within 2."""
-    import os
     d, X, b = problem("c2", n=3000)
     sigma = d["sigma"]
     kern = R.Kernel(sigma)
     cells = R.Cells(ctx, dev(X, torch.float32), kern)
     reps = {}
     for basis in ("32", "64"):
-        if basis == "64":
-            os.environ["RBF_GMRES_BASIS64"] = "1"
-        try:
-            w, rep = R.gmres_solve(ctx, cells, kern, dev(b, torch.float32), restart=50, rtol=1e-6,
-                                   core_target=512, overlap_sigmas=1.3, max_iters=400, cgs_passes=1)
-        finally:
-            os.environ.pop("RBF_GMRES_BASIS64", None)
+        w, rep = R.gmres_solve(ctx, cells, kern, dev(b, torch.float32), restart=50, rtol=1e-6,
+                               core_target=512, overlap_sigmas=1.3, max_iters=400, cgs_passes=1,
+                               basis_fp64=1 if basis == "64" else 0)
         res = np.linalg.norm(b - OK.matvec(X, host(w), sigma)) / np.linalg.norm(b)
         assert rep["converged"] == 1 and res <= 1.5e-6, (basis, res, rep)
         reps[basis] = rep

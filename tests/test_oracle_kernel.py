@@ -83,3 +83,53 @@ def test_pair_count_bruteforce():
     X = np.array([[0, 0, 0], [0.5, 0, 0], [0, 0.7, 0]], dtype=np.float64)
     # sigma = 0.1, cutoff 0.6: pairs (0,0),(1,1),(2,2),(0,1),(1,0)
     assert K.pair_count(X, 0.1) == 5
+
+
+def test_matvec_parallel_equals_matvec_in_row_order():
+    """The multi-process row split (bench cpu_baseline, c3/c4 parity sampling)
+    returns the rows of `matvec` in the order asked for (row blocks of the split
+    re-concatenated), with the same per-row arithmetic."""
+    rng = np.random.default_rng(5)
+    X = rng.uniform(-1, 1, (1500, 3)).astype(np.float32)
+    w = rng.normal(size=1500)
+    sigma = 0.08
+    rows = rng.choice(1500, 101, replace=False)     # unsorted, odd count: uneven parts
+    ref = K.matvec(X, w, sigma, rows=rows)
+    g = K.matvec(X, np.abs(w), sigma, rows=rows)
+    for procs in (1, 2, 3):
+        f = K.matvec_parallel(X, w, sigma, rows=rows, procs=procs)
+        assert f.shape == ref.shape
+        assert (np.abs(f - ref) <= 1e-14 * g).all(), procs
+    T = rng.uniform(-1, 1, (37, 3))
+    np.testing.assert_allclose(K.matvec_parallel(X, w, sigma, targets=T, procs=2),
+                               K.matvec(X, w, sigma, targets=T), rtol=0,
+                               atol=1e-14 * np.abs(K.matvec(X, np.abs(w), sigma, targets=T)).max())
+
+
+def test_matvec_local_equals_bruteforce_including_cutoff_boundary():
+    """matvec_local (range search + the same fp64 predicate) against brute force:
+    random clouds, rows, grid-like targets, and pairs placed EXACTLY on the
+    cutoff sphere in fp64 (d2 == c^2 is included) or one ulp beyond it."""
+    rng = np.random.default_rng(6)
+    sigma = 0.05
+    X = rng.uniform(-0.4, 0.4, (4000, 3)).astype(np.float32).astype(np.float64)
+    w = rng.normal(size=len(X))
+    rows = rng.choice(len(X), 300, replace=False)
+    ref = K.matvec(X, w, sigma, rows=rows)
+    g = K.matvec(X, np.abs(w), sigma, rows=rows)
+    assert (np.abs(K.matvec_local(X, w, sigma, rows=rows) - ref) <= 1e-13 * g).all()
+    T = rng.uniform(-0.5, 0.5, (200, 3))
+    ref = K.matvec(X, w, sigma, targets=T)
+    g = K.matvec(X, np.abs(w), sigma, targets=T)
+    assert (np.abs(K.matvec_local(X, w, sigma, targets=T) - ref) <= 1e-13 * g + 1e-300).all()
+    # boundary: c = 0.3 = 6 sigma; x-offsets 0.25 exactly on the sphere? use a
+    # representable case: sigma = 0.125, c = 0.75, offsets (0.75, 0, 0) and
+    # (0.45, 0.6, 0) have d2 == 0.5625 exactly; nextafter(0.75) lies beyond
+    s2 = 0.125
+    Xb = np.array([[0, 0, 0], [0.75, 0, 0], [0.45, 0.6, 0], [np.nextafter(0.75, 1), 0, 0]])
+    wb = np.array([1.0, 1.0, 1.0, 1.0])
+    fl = K.matvec_local(Xb, wb, s2, rows=[0])
+    fb = K.matvec(Xb, wb, s2, rows=[0])
+    a = K.amplitude(s2)
+    np.testing.assert_allclose(fb, [a * (1 + 2 * np.exp(-18.0))], rtol=1e-15)
+    np.testing.assert_allclose(fl, fb, rtol=1e-15)
