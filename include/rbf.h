@@ -71,8 +71,12 @@ typedef enum { RBF_F32 = 0, RBF_F64 = 1 } rbf_precision;
  *   RBF_OP_ONESIDED  one-sided fp32 and fp64 tiers: a DETERMINISTIC solve
  *   RBF_OP_SYM       symmetric on the 64-target plan
  *   RBF_OP_SYM_WIDE  symmetric on the wide plan (fp64 tier: the 64-target plan)
+ *   RBF_OP_SYM_ROT   as RBF_OP_SYM_WIDE with the source side summed by a rotating
+ *                    accumulator instead of a warp transpose-reduction
  * The public rbf_matvec is always one-sided; rbf_matvec_op exposes the others. */
-typedef enum { RBF_OP_AUTO = 0, RBF_OP_ONESIDED = 1, RBF_OP_SYM = 2, RBF_OP_SYM_WIDE = 3 } rbf_op_variant;
+typedef enum {
+  RBF_OP_AUTO = 0, RBF_OP_ONESIDED = 1, RBF_OP_SYM = 2, RBF_OP_SYM_WIDE = 3, RBF_OP_SYM_ROT = 4
+} rbf_op_variant;
 
 /* Gaussian kernel of Eq.6 with truncation radius
  * cutoff_sigmas*sigma.  amplitude <= 0 selects Eq.6's
@@ -170,6 +174,7 @@ typedef struct rbf_ctx rbf_ctx;
 typedef struct rbf_cells rbf_cells;
 typedef struct rbf_precond rbf_precond;
 typedef struct rbf_csr rbf_csr;
+typedef struct rbf_loopback_group rbf_loopback_group;
 
 /* Description of a built cell list (host struct, filled by rbf_cells_info). */
 typedef struct {
@@ -204,6 +209,19 @@ rbf_status rbf_create(rbf_ctx** ctx, int device, void* cuda_stream,
 /* 128 bytes (HOST) of a fresh NCCL unique id, for rank 0 to share.  RBF_ENCCL if
  * NCCL cannot be loaded. */
 rbf_status rbf_nccl_unique_id(void* out128);
+/* In-process loopback transport: `world` contexts of ONE process on one device,
+ * each driven by its own host thread, run the multi-rank slab partition exactly
+ * as world GPUs would (same partition, halos, reductions and gathers; copies
+ * between the ranks' buffers and a rank-ordered sum kernel instead of NCCL,
+ * ordered by CUDA events and a host barrier).  For tests and single-GPU runs of
+ * the distributed code path.  Create the group once (library-owned, free it
+ * after every context of it is destroyed), then one rbf_create_loopback per
+ * rank with distinct streams; every rank must make the same sequence of calls
+ * (a call blocks until all ranks have reached it).  Errors: RBF_EINVAL (world
+ * outside [1, 64], rank out of range or already joined), RBF_ECUDA. */
+rbf_status rbf_loopback_group_create(int world, rbf_loopback_group** out);
+void rbf_loopback_group_free(rbf_loopback_group* g);
+rbf_status rbf_create_loopback(rbf_ctx** ctx, int device, void* cuda_stream, rbf_loopback_group* g, int rank);
 /* Slab partition plan (HOST only, no GPU; the same function the library runs at
  * rbf_build_cells when world > 1).  Inputs: plane_start[dimz+1] = sorted
  * position of the first centre of each z cell plane (non-decreasing, last =
@@ -246,10 +264,7 @@ void rbf_cells_free(rbf_cells* cells);
 rbf_status rbf_cells_info(const rbf_cells* cells, rbf_cells_desc* out /* host */);
 /* This rank's slab (HOST out[8]): owned sorted range [out[0], out[1]), matvec
  * source window [out[2], out[3]), target tiles [out[4], out[5]), z cell planes
- * [out[6], out[7]).  Single GPU: everything.  (world > 1, or the test-only
- * RBF_SLAB_EMULATE="r/W" environment variable, which gives single-GPU cells
- * rank r's slab of a W-way partition for rbf_matvec / rbf_eval_grid /
- * rbf_precond_create checks; the solver refuses such cells.) */
+ * [out[6], out[7]).  Single GPU: everything. */
 rbf_status rbf_cells_slab(const rbf_cells* cells, int64_t* out);
 /* Library-owned DEVICE arrays, valid until rbf_cells_free:
  *   perm[n]           sorted position -> caller index (stable by key)
@@ -295,12 +310,16 @@ rbf_status rbf_precond_create(rbf_ctx* ctx, const rbf_cells* cells, const rbf_ke
                               const rbf_precond_cfg* cfg, rbf_precond** out);
 void rbf_precond_free(rbf_precond* p);
 /* z = M r, M = sum_i R~_i^T A_i^-1 R_i (restricted: only core rows written).
- * r, z: DEVICE fp32, n entries, caller order. */
+ * r, z: DEVICE fp32, n entries, caller order.  Single GPU only (a slab-
+ * partitioned solve applies the preconditioner inside rbf_gmres_solve, with the
+ * extended sets reaching into the neighbouring slabs through the halo). */
 rbf_status rbf_precond_apply(rbf_ctx* ctx, const rbf_precond* p, const float* r, float* z);
 /* Block structure (host outputs, synchronises): nblocks, and if the arrays are
  * non-NULL: core_ptr[nblocks+1], ext_ptr[nblocks+1] (host, caller-allocated)
  * and core_idx[core_ptr[nb]], ext_idx[ext_ptr[nb]] (host) holding SORTED
- * positions; each block's ext list is [non-core members ascending] + [core]. */
+ * positions relative to this rank's owned start (0 on one GPU; a distributed
+ * RAS block's ext members in the slab below are negative); each block's ext
+ * list is [non-core members ascending] + [core]. */
 rbf_status rbf_precond_blocks(const rbf_precond* p, int64_t* nblocks, int64_t* bytes,
                               int64_t* core_ptr, int64_t* ext_ptr,
                               int32_t* core_idx, int32_t* ext_idx);
@@ -317,10 +336,16 @@ rbf_status rbf_gmres_solve(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kerne
 /* ---- a8: grid evaluation F(xi) = sum_j A(xi, x_j) w_j (Eq.5) --------------
  * w: DEVICE fp64 (n, caller order); field: DEVICE fp32, n0*n1*n2, x fastest.
  * Nodes with no centre within the cutoff get exactly 0.0f.  world > 1: each
- * rank evaluates the node layers of its slab and the field is summed over ranks
- * (the other layers are 0 on each rank), so every rank returns the full field. */
+ * rank evaluates the node layers of its slab and gathers the other ranks'
+ * layers, so every rank returns the full field. */
 rbf_status rbf_eval_grid(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern,
                          const double* w, const rbf_grid* grid, float* field);
+/* The sharded form: only this rank's z layers [*k0, *k1) of nodes (k = z index)
+ * are written (field is still the full n0*n1*n2 array; the other layers are
+ * untouched), no gather.  rbf_eval_grid = this + a gather of every rank's
+ * layers.  Single GPU: all layers. */
+rbf_status rbf_eval_grid_slab(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern,
+                              const double* w, const rbf_grid* grid, float* field, int64_t* k0, int64_t* k1);
 
 /* ---- the ASSEMBLED operator, for comparison ---------
  * The paper's GPU path assembles A (Alg.2 "truncation area") and

@@ -44,13 +44,20 @@ def lu_solve(centres, b, sigma, cutoff_sigmas=6.0, amp=None):
     return sla.lu_solve((lu, piv), np.asarray(b, dtype=np.float64))
 
 
-def ras_blocks(cells, sigma: float, core_target: int = 512, overlap_sigmas: float = 1.0):
-    """List of dicts {core, ext} with indices in SORTED (cell-list) order."""
+def ras_blocks(cells, sigma: float, core_target: int = 512, overlap_sigmas: float = 1.0, core_cells=None):
+    """List of dicts {core, ext} with indices in SORTED (cell-list) order.
+
+    core_cells: optional boolean mask over the cells from which the cores are
+    formed (a slab of a multi-GPU partition, reading R20: every rank
+    builds the blocks of its own cells; their extended sets may reach into any
+    cell); default all cells."""
     S = cells["sorted"].astype(np.float32)
     dim = cells["dim"]
     h = cells["h"]
     cs, ce = cells["cell_start"].astype(np.int64), cells["cell_end"].astype(np.int64)
     counts = ce - cs
+    if core_cells is not None:
+        counts = np.where(core_cells, counts, 0)
     nonempty = np.nonzero(counts > 0)[0]
     cx = nonempty % dim[0]
     cy = (nonempty // dim[0]) % dim[1]

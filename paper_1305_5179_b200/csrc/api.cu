@@ -12,6 +12,7 @@
 
 #include "internal.h"
 #include "solver.h"
+#include "transport.h"
 
 namespace rbf {
 namespace {
@@ -98,6 +99,36 @@ int rbf_abi_version(void) { return RBF_ABI_VERSION; }
 
 int64_t rbf_launch_count(void) { return (int64_t)g_launches.load(std::memory_order_relaxed); }
 
+}  // extern "C"
+
+namespace {
+rbf_status create_ctx(rbf_ctx** out, int device, void* cuda_stream) {
+  if (!out) { set_error("out is NULL"); return RBF_EINVAL; }
+  *out = nullptr;
+  int ndev = 0;
+  RBF_CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) { set_error("bad device ordinal"); return RBF_EINVAL; }
+  RBF_CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  RBF_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) {
+    set_error("librbf is built for sm_100a (B200); device has compute capability " + std::to_string(prop.major) +
+              "." + std::to_string(prop.minor));
+    return RBF_EUNSUPPORTED;
+  }
+  rbf_ctx* c = new (std::nothrow) rbf_ctx();
+  if (!c) { set_error("host allocation failed"); return RBF_ENOMEM; }
+  c->device = device;
+  c->stream = static_cast<cudaStream_t>(cuda_stream);
+  c->sm_count = prop.multiProcessorCount;
+  lib_pool(device);   // the library's private stream-ordered pool (internal.h)
+  *out = c;
+  return RBF_OK;
+}
+}  // namespace
+
+extern "C" {
+
 rbf_status rbf_create(rbf_ctx** out, int device, void* cuda_stream, const void* nccl_unique_id, int rank,
                       int world) {
   if (!out) { set_error("out is NULL"); return RBF_EINVAL; }
@@ -107,27 +138,37 @@ rbf_status rbf_create(rbf_ctx** out, int device, void* cuda_stream, const void* 
     set_error("world > 1 needs the NCCL unique id of rank 0 (rbf_nccl_unique_id)");
     return RBF_EINVAL;
   }
-  int ndev = 0;
-  RBF_CUDA_TRY(cudaGetDeviceCount(&ndev));
-  if (device < 0 || device >= ndev) { set_error("bad device ordinal"); return RBF_EINVAL; }
-  RBF_CUDA_TRY(cudaSetDevice(device));
-  rbf_ctx* c = new (std::nothrow) rbf_ctx();
-  if (!c) { set_error("host allocation failed"); return RBF_ENOMEM; }
-  c->device = device;
-  c->stream = static_cast<cudaStream_t>(cuda_stream);
-  cudaDeviceProp prop;
-  if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) c->sm_count = prop.multiProcessorCount;
-  if (prop.major != 10) {
-    delete c;
-    set_error("librbf is built for sm_100a (B200); device has compute capability " +
-              std::to_string(prop.major) + "." + std::to_string(prop.minor));
-    return RBF_EUNSUPPORTED;
-  }
-  lib_pool(device);   // the library's private stream-ordered pool (internal.h)
+  rbf_ctx* c = nullptr;
+  RBF_TRY(create_ctx(&c, device, cuda_stream));
   if (world > 1) {
     rbf_status st = dist_init(c, nccl_unique_id, rank, world);
     if (st != RBF_OK) { delete c; return st; }
   }
+  *out = c;
+  return RBF_OK;
+}
+
+rbf_status rbf_create_loopback(rbf_ctx** out, int device, void* cuda_stream, rbf_loopback_group* grp, int rank) {
+  if (!out || !grp) { set_error("NULL argument"); return RBF_EINVAL; }
+  *out = nullptr;
+  LoopGroup* g = reinterpret_cast<LoopGroup*>(grp);
+  if (rank < 0 || rank >= g->world) { set_error("rank out of range"); return RBF_EINVAL; }
+  {
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (g->joined[rank]) { set_error("rank already joined the loopback group"); return RBF_EINVAL; }
+    g->joined[rank] = 1;
+  }
+  rbf_ctx* c = nullptr;
+  rbf_status st = create_ctx(&c, device, cuda_stream);
+  if (st != RBF_OK) {
+    std::lock_guard<std::mutex> lk(g->mu);
+    g->joined[rank] = 0;
+    return st;
+  }
+  c->rank = rank;
+  c->world = g->world;
+  c->tr = make_loop_transport(g, rank);
+  c->loop_group = g;
   *out = c;
   return RBF_OK;
 }
@@ -164,6 +205,11 @@ void rbf_destroy(rbf_ctx* ctx) {
   cudaStreamSynchronize(s);
   dist_destroy(ctx);
   const int dev = ctx->device;
+  if (ctx->loop_group) {
+    LoopGroup* g = static_cast<LoopGroup*>(ctx->loop_group);
+    std::lock_guard<std::mutex> lk(g->mu);
+    g->joined[ctx->rank] = 0;
+  }
   delete ctx;  // DevBufs free stream-ordered
   cudaStreamSynchronize(s);
   // hand the freed workspaces back to the driver (memory still held by other
@@ -235,11 +281,11 @@ rbf_status matvec_impl(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern,
   if (!w || !f) { set_error("w/f is NULL"); return RBF_EINVAL; }
   if (w == f) { set_error("w and f must not alias"); return RBF_EINVAL; }
   if (prec != RBF_F32 && prec != RBF_F64) { set_error("bad precision"); return RBF_EINVAL; }
-  if (op < RBF_OP_AUTO || op > RBF_OP_SYM_WIDE) { set_error("bad operator variant"); return RBF_EINVAL; }
+  if (op < RBF_OP_AUTO || op > RBF_OP_SYM_ROT) { set_error("bad operator variant"); return RBF_EINVAL; }
   RBF_CUDA_TRY(cudaSetDevice(ctx->device));
   KernelParams kp = kernel_params(kern);
   const int64_t n = c->n;
-  if (ctx->world > 1 || c->emulated || op != RBF_OP_ONESIDED) {
+  if (ctx->world > 1 || op != RBF_OP_ONESIDED) {
     // solver operator / slab partition: replicated in, this rank's rows, gathered out
     RBF_TRY(ctx->vec_a.ensure(sizeof(double) * n, ctx->stream));
     RBF_TRY(ctx->vec_b.ensure(sizeof(double) * n, ctx->stream));
@@ -303,10 +349,11 @@ rbf_status rbf_matvec_pairs(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* 
   return RBF_OK;
 }
 
-rbf_status rbf_eval_grid(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, const double* w,
-                         const rbf_grid* g, float* field) {
-  RBF_TRY(check_cells(ctx, c, kern));
-  if (!w || !g || !field) { set_error("NULL argument"); return RBF_EINVAL; }
+}  // extern "C"
+
+namespace {
+rbf_status check_grid(const rbf_grid* g) {
+  if (!g) { set_error("grid is NULL"); return RBF_EINVAL; }
   for (int a = 0; a < 3; ++a) {
     if (g->n[a] < 2) { set_error("grid needs n >= 2 nodes per axis"); return RBF_EINVAL; }
     if (!std::isfinite(g->lo[a]) || !std::isfinite(g->hi[a]) || !(g->hi[a] > g->lo[a])) {
@@ -315,17 +362,40 @@ rbf_status rbf_eval_grid(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* ker
     }
   }
   if ((double)g->n[0] * g->n[1] * g->n[2] > 4e9) { set_error("grid too large"); return RBF_EINVAL; }
+  return RBF_OK;
+}
+
+rbf_status eval_grid_impl(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, const double* w,
+                          const rbf_grid* g, float* field, bool gather, int64_t* k0, int64_t* k1) {
+  RBF_TRY(check_cells(ctx, c, kern));
+  if (!w || !field) { set_error("NULL argument"); return RBF_EINVAL; }
+  RBF_TRY(check_grid(g));
   RBF_CUDA_TRY(cudaSetDevice(ctx->device));
   KernelParams kp = kernel_params(kern);
   RBF_TRY(ctx->vec_a.ensure(sizeof(double) * c->n, ctx->stream));
   RBF_TRY(gather_f64_to_sorted(ctx, w, c->perm.as<int32_t>(), ctx->vec_a.as<double>(), c->n));
-  if (ctx->world == 1 && !c->emulated) return eval_grid_sorted(ctx, c, kp, ctx->vec_a.as<double>(), g, field);
-  // slab partition: each rank evaluates the node layers of its slab, the
-  // others stay 0, and a sum over ranks completes the field on every rank
-  const int64_t nodes = (int64_t)g->n[0] * g->n[1] * g->n[2];
-  RBF_CUDA_TRY(cudaMemsetAsync(field, 0, sizeof(float) * nodes, ctx->stream));
+  // each rank evaluates the node layers of its slab; the gather completes the field
   RBF_TRY(eval_grid_sorted(ctx, c, kp, ctx->vec_a.as<double>(), g, field));
-  return allreduce_sum_f32(ctx, field, nodes);
+  if (k0 || k1) {
+    int64_t a, b;
+    grid_layers(c, g, ctx->rank, &a, &b);
+    if (k0) *k0 = a;
+    if (k1) *k1 = b;
+  }
+  return gather ? allgather_layers(ctx, c, g, field) : RBF_OK;
+}
+}  // namespace
+
+extern "C" {
+
+rbf_status rbf_eval_grid(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, const double* w,
+                         const rbf_grid* g, float* field) {
+  return eval_grid_impl(ctx, c, kern, w, g, field, true, nullptr, nullptr);
+}
+
+rbf_status rbf_eval_grid_slab(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, const double* w,
+                              const rbf_grid* g, float* field, int64_t* k0, int64_t* k1) {
+  return eval_grid_impl(ctx, c, kern, w, g, field, false, k0, k1);
 }
 
 rbf_status rbf_eval_grid_pairs(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, const rbf_grid* g,

@@ -124,7 +124,7 @@ rbf_status rbf_assemble(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern
     set_error("kernel cutoff exceeds the cutoff the cells were built for");
     return RBF_EINVAL;
   }
-  if (ctx->world > 1 || c->emulated) { set_error("the assembled operator is single-GPU"); return RBF_EUNSUPPORTED; }
+  if (ctx->world > 1) { set_error("the assembled operator is single-GPU"); return RBF_EUNSUPPORTED; }
   RBF_CUDA_TRY(cudaSetDevice(ctx->device));
   using clk = std::chrono::steady_clock;
   const auto t0 = clk::now();

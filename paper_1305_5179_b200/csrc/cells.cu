@@ -533,8 +533,14 @@ rbf_status build_cells(rbf_ctx* ctx, const float* xyz, int64_t n, const rbf_kern
   RBF_TRY(rcw.alloc(sizeof(uint32_t) * rows, s));
   RBF_TRY(row_w.alloc(sizeof(uint32_t) * rows, s));
   RBF_TRY(totw.alloc(sizeof(uint32_t) * 2, s));
-  const int cap_w = 128;
-  const int span_w = std::max(span, 4);
+#ifndef RBF_WIDE_CAP
+#define RBF_WIDE_CAP 128
+#endif
+#ifndef RBF_WIDE_SPAN
+#define RBF_WIDE_SPAN 4
+#endif
+  const int cap_w = RBF_WIDE_CAP;
+  const int span_w = std::max(span, RBF_WIDE_SPAN);
   plan_count<<<grid_for(rows, 128), 128, 0, s>>>(c->cell_start.as<int32_t>(), g, cap_w, span_w, 0,
                                                  rcw.as<uint32_t>());
   RBF_CHECK_LAUNCH();
@@ -558,29 +564,14 @@ rbf_status build_cells(rbf_ctx* ctx, const float* xyz, int64_t n, const rbf_kern
   // this rank's share (dist.cu): everything on one GPU, a slab of z planes otherwise
   c->world = ctx->world;
   c->view = SlabView{0, n, 0, n, 0, (int64_t)ntiles, 0, c->dim[2], 0, (int64_t)ntiles_w};
-  // RBF_SLAB_EMULATE="r/W" (single GPU, tests only): give these cells rank r's
-  // slab of a W-way partition so the slab kernels can be checked on one device
-  int erank = 0, eworld = 1;
-  if (ctx->world == 1) {
-    if (const char* e = std::getenv("RBF_SLAB_EMULATE")) {
-      if (std::sscanf(e, "%d/%d", &erank, &eworld) != 2 || eworld < 1 || erank < 0 || erank >= eworld) {
-        set_error("RBF_SLAB_EMULATE must be r/W with 0 <= r < W");
-        return RBF_EINVAL;
-      }
-    }
-  }
-  if (ctx->world > 1 || eworld > 1) {
+  if (ctx->world > 1) {
     std::vector<uint32_t> hro(rows), hrow(rows);
     RBF_CUDA_TRY(cudaMemcpyAsync(hro.data(), ro.p, sizeof(uint32_t) * rows, cudaMemcpyDeviceToHost, s));
     RBF_CUDA_TRY(cudaMemcpyAsync(hrow.data(), row_w.p, sizeof(uint32_t) * rows, cudaMemcpyDeviceToHost, s));
     RBF_CUDA_TRY(cudaStreamSynchronize(s));
-    if (ctx->world > 1) {
-      RBF_TRY(dist_plan_cells(ctx, c, hro, (int64_t)ntiles, hrow, (int64_t)ntiles_w, ctx->rank, ctx->world));
-    } else {
-      RBF_TRY(dist_plan_cells(ctx, c, hro, (int64_t)ntiles, hrow, (int64_t)ntiles_w, erank, eworld));
-      c->emulated = true;
-    }
+    RBF_TRY(dist_plan_cells(ctx, c, hro, (int64_t)ntiles, hrow, (int64_t)ntiles_w, ctx->rank, ctx->world));
   }
+  RBF_TRY(order_wide_tiles(ctx, c, kernel_params(k)));
   return RBF_OK;
 }
 

@@ -1,6 +1,8 @@
-// multi-GPU partition of the hot path by spatial slabs.
+// multi-rank partition of the hot path by spatial slabs.
 //
-// One process per GPU; every rank receives the full (replicated) centre set and
+// One rank per GPU (one process per GPU over NCCL, or -- tests, single-GPU
+// runs of the same code path -- one host thread per rank over the in-process
+// loopback transport, transport.h); every rank receives the full (replicated) centre set and
 // builds the same global cell structure, then owns a slab of whole cell planes
 // along z (the slowest axis of the cell key, so a slab is a CONTIGUOUS range of
 // the sorted order).  Slab boundaries balance an estimate of the useful pairs
@@ -8,12 +10,15 @@
 // the local density; c3's density varies 10x).  Per fp32/fp64 matvec the rank
 // needs the weights of the sources within the cutoff of its targets: the planes
 // [p0 - reach, p1 + reach) -- a contiguous window of the sorted order -- which
-// it assembles from its own slice plus grouped ncclSend/ncclRecv with the ranks
-// owning the rest of the window (the paper's "communication ... limited to a
-// constant number of elements in the vicinity").  Krylov inner products
-// are local partial sums + ncclAllReduce; results are gathered with grouped
-// ncclBroadcast so every rank returns the full vectors (replicated in,
-// replicated out).
+// it assembles from its own slice plus grouped point-to-point copies from the
+// ranks owning the rest of the window (the paper's "communication ... limited
+// to a constant number of elements in the vicinity").  The symmetric
+// operators (reading R19) read only the window above the slab and send the
+// contributions they accumulate for those sources back to their owners (a
+// reverse halo reduction), so every pair is evaluated once across ranks too.
+// Krylov inner products are local partial sums + a sum all-reduce; results are
+// gathered so every rank returns the full vectors (replicated in, replicated
+// out).
 //
 // NCCL is loaded at run time (dlopen of libnccl.so.2: inside a torch process
 // this resolves to the NCCL torch already loaded), so librbf.so carries no link
@@ -24,8 +29,10 @@
 #include <cmath>
 #include <cstring>
 #include <mutex>
+#include <new>
 
 #include "internal.h"
+#include "transport.h"
 
 namespace rbf {
 namespace {
@@ -93,8 +100,6 @@ NcclApi& nccl() {
     }                                                                                   \
   } while (0)
 
-inline ncclComm_t comm_of(const rbf_ctx* ctx) { return static_cast<ncclComm_t>(ctx->nccl_comm); }
-
 // per-plane pair weight sum_c n_c^2 and the first sorted position of every plane
 __global__ void plane_stats_kernel(const int32_t* __restrict__ cell_start, int64_t ncell, int64_t plane_cells,
                                    unsigned long long* __restrict__ weight) {
@@ -109,7 +114,127 @@ __global__ void plane_start_kernel(const int32_t* __restrict__ cell_start, int d
     out[p] = cell_start[(int64_t)p * plane_cells];
 }
 
+
+// ---------------------------------------------------------------- NCCL -----
+struct NcclTransport final : Transport {
+  ncclComm_t comm;
+  explicit NcclTransport(ncclComm_t c) : comm(c) {}
+  ~NcclTransport() override {
+    if (comm && nccl().ok) nccl().CommDestroy(comm);
+  }
+  rbf_status exchange(rbf_ctx*, cudaStream_t s, const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs,
+                      DType t) override {
+    if (sends.empty() && recvs.empty()) return RBF_OK;
+    NcclApi& api = nccl();
+    const int dt = t == DType::F64 ? kNcclFloat64 : kNcclFloat32;
+    RBF_NCCL_TRY(api.GroupStart());
+    for (const Xfer& x : sends) RBF_NCCL_TRY(api.Send(x.ptr, (size_t)x.count, dt, x.peer, comm, s));
+    for (const Xfer& x : recvs) RBF_NCCL_TRY(api.Recv(x.ptr, (size_t)x.count, dt, x.peer, comm, s));
+    RBF_NCCL_TRY(api.GroupEnd());
+    return RBF_OK;
+  }
+  rbf_status allreduce_sum(rbf_ctx*, cudaStream_t s, void* buf, int64_t count, DType t) override {
+    if (count == 0) return RBF_OK;
+    RBF_NCCL_TRY(nccl().AllReduce(buf, buf, (size_t)count, t == DType::F64 ? kNcclFloat64 : kNcclFloat32,
+                                  kNcclSum, comm, s));
+    return RBF_OK;
+  }
+};
+
+// ------------------------------------------------------------ loopback -----
+constexpr int kLoopMaxWorld = 64;
+struct PtrArray {
+  const void* p[kLoopMaxWorld];
+};
+
+// out[i] = sum over ranks q = 0..world-1 (in that order) of buf_q[i]
+template <class T>
+__global__ void loop_sum_kernel(PtrArray bufs, int world, T* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    T s = static_cast<const T*>(bufs.p[0])[i];
+    for (int q = 1; q < world; ++q) s += static_cast<const T*>(bufs.p[q])[i];
+    out[i] = s;
+  }
+}
+
+struct LoopTransport final : Transport {
+  LoopGroup* g;
+  int rank;
+  DevBuf scratch;
+  LoopTransport(LoopGroup* grp, int r) : g(grp), rank(r) {
+    cudaEventCreateWithFlags(&g->slots[r].ready, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&g->slots[r].done, cudaEventDisableTiming);
+  }
+  ~LoopTransport() override {
+    cudaEventDestroy(g->slots[rank].ready);
+    cudaEventDestroy(g->slots[rank].done);
+    g->slots[rank].ready = g->slots[rank].done = nullptr;
+  }
+  // phase 1: my buffers are complete on my stream when `ready` fires; phase 2:
+  // the peers read them; phase 3: my later writes wait for their reads (`done`)
+  rbf_status exchange(rbf_ctx*, cudaStream_t s, const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs,
+                      DType t) override {
+    LoopGroup::Slot& me = g->slots[rank];
+    me.sends = sends;
+    RBF_CUDA_TRY(cudaEventRecord(me.ready, s));
+    g->barrier();
+    const size_t es = (size_t)t;
+    for (const Xfer& rv : recvs) {
+      const LoopGroup::Slot& peer = g->slots[rv.peer];
+      const Xfer* src = nullptr;
+      int k = 0;   // the k-th receive from this peer matches its k-th send to me
+      for (const Xfer& r2 : recvs) {
+        if (&r2 == &rv) break;
+        if (r2.peer == rv.peer) ++k;
+      }
+      for (const Xfer& sx : peer.sends)
+        if (sx.peer == rank && k-- == 0) { src = &sx; break; }
+      if (!src || src->count != rv.count) {
+        set_error("loopback exchange: unmatched transfer");
+        return RBF_EINVAL;
+      }
+      RBF_CUDA_TRY(cudaStreamWaitEvent(s, peer.ready, 0));
+      if (rv.count > 0) RBF_CUDA_TRY(cudaMemcpyAsync(rv.ptr, src->ptr, es * rv.count, cudaMemcpyDeviceToDevice, s));
+    }
+    RBF_CUDA_TRY(cudaEventRecord(me.done, s));
+    g->barrier();
+    for (int q = 0; q < g->world; ++q)
+      if (q != rank) RBF_CUDA_TRY(cudaStreamWaitEvent(s, g->slots[q].done, 0));
+    return RBF_OK;
+  }
+  rbf_status allreduce_sum(rbf_ctx*, cudaStream_t s, void* buf, int64_t count, DType t) override {
+    LoopGroup::Slot& me = g->slots[rank];
+    const size_t es = (size_t)t;
+    RBF_TRY(scratch.ensure(es * std::max<int64_t>(count, 1), s));
+    me.buf = buf;
+    RBF_CUDA_TRY(cudaEventRecord(me.ready, s));
+    g->barrier();
+    PtrArray pa{};
+    for (int q = 0; q < g->world; ++q) {
+      pa.p[q] = g->slots[q].buf;
+      if (q != rank) RBF_CUDA_TRY(cudaStreamWaitEvent(s, g->slots[q].ready, 0));
+    }
+    if (count > 0) {
+      if (t == DType::F64)
+        loop_sum_kernel<double><<<grid_for(count, 256), 256, 0, s>>>(pa, g->world, scratch.as<double>(), count);
+      else
+        loop_sum_kernel<float><<<grid_for(count, 256), 256, 0, s>>>(pa, g->world, scratch.as<float>(), count);
+      RBF_CHECK_LAUNCH();
+    }
+    RBF_CUDA_TRY(cudaEventRecord(me.done, s));
+    g->barrier();
+    for (int q = 0; q < g->world; ++q)
+      if (q != rank) RBF_CUDA_TRY(cudaStreamWaitEvent(s, g->slots[q].done, 0));
+    if (count > 0) RBF_CUDA_TRY(cudaMemcpyAsync(buf, scratch.p, es * count, cudaMemcpyDeviceToDevice, s));
+    return RBF_OK;
+  }
+};
+
+
 }  // namespace
+
+Transport* make_nccl_transport(void* comm) { return new NcclTransport(static_cast<ncclComm_t>(comm)); }
+Transport* make_loop_transport(LoopGroup* g, int rank) { return new LoopTransport(g, rank); }
 
 rbf_status dist_init(rbf_ctx* ctx, const void* unique_id, int rank, int world) {
   NcclApi& api = nccl();
@@ -119,13 +244,15 @@ rbf_status dist_init(rbf_ctx* ctx, const void* unique_id, int rank, int world) {
   ncclComm_t comm = nullptr;
   RBF_NCCL_TRY(api.CommInitRank(&comm, world, id, rank));
   ctx->nccl_comm = comm;
+  ctx->tr = make_nccl_transport(comm);
   ctx->rank = rank;
   ctx->world = world;
   return RBF_OK;
 }
 
 void dist_destroy(rbf_ctx* ctx) {
-  if (ctx->nccl_comm && nccl().ok) nccl().CommDestroy(comm_of(ctx));
+  delete ctx->tr;   // NcclTransport destroys its communicator
+  ctx->tr = nullptr;
   ctx->nccl_comm = nullptr;
 }
 
@@ -213,64 +340,132 @@ rbf_status dist_plan_cells(rbf_ctx* ctx, rbf_cells* c, const std::vector<uint32_
   return RBF_OK;
 }
 
-// win[0, h1-h0) <- window of the distributed vector whose owned slice is x_loc
+
+// ------------------------------------------------------------- collectives --
 template <class T>
-rbf_status halo_exchange(rbf_ctx* ctx, const rbf_cells* c, const T* x_loc, T* win) {
+rbf_status halo_exchange(rbf_ctx* ctx, const rbf_cells* c, const T* x_loc, T* win, bool upper_only) {
   cudaStream_t s = ctx->stream;
   const SlabView& V = c->view;
   const SlabPlan& P = c->plan;
+  const int64_t base = upper_only ? V.o0 : V.h0;
   if (V.o1 > V.o0)
-    RBF_CUDA_TRY(cudaMemcpyAsync(win + (V.o0 - V.h0), x_loc, sizeof(T) * (V.o1 - V.o0), cudaMemcpyDeviceToDevice, s));
-  if (ctx->world == 1) {
-    // emulated slab (single GPU, tests): x_loc points into the full sorted
-    // vector, so the window is read in place
-    if (c->emulated && V.h1 > V.h0)
-      RBF_CUDA_TRY(cudaMemcpyAsync(win, x_loc - (V.o0 - V.h0), sizeof(T) * (V.h1 - V.h0), cudaMemcpyDeviceToDevice, s));
-    return RBF_OK;
-  }
-  NcclApi& api = nccl();
-  const int dt = sizeof(T) == 8 ? kNcclFloat64 : kNcclFloat32;
-  RBF_NCCL_TRY(api.GroupStart());
+    RBF_CUDA_TRY(cudaMemcpyAsync(win + (V.o0 - base), x_loc, sizeof(T) * (V.o1 - V.o0), cudaMemcpyDeviceToDevice, s));
+  if (ctx->world == 1) return RBF_OK;
+  std::vector<Xfer> sends, recvs;
   for (int q = 0; q < ctx->world; ++q) {
     if (q == ctx->rank) continue;
     // my owned slice inside q's window
-    const int64_t slo = std::max(V.o0, P.win_lo[q]), shi = std::min(V.o1, P.win_hi[q]);
-    if (shi > slo) RBF_NCCL_TRY(api.Send(x_loc + (slo - V.o0), (size_t)(shi - slo), dt, q, comm_of(ctx), s));
+    const int64_t qlo = upper_only ? P.own_lo[q] : P.win_lo[q];
+    const int64_t slo = std::max(V.o0, qlo), shi = std::min(V.o1, P.win_hi[q]);
+    if (shi > slo && P.own_hi[q] > P.own_lo[q]) sends.push_back(Xfer{q, const_cast<T*>(x_loc) + (slo - V.o0), shi - slo});
     // q's owned slice inside my window
-    const int64_t rlo = std::max(P.own_lo[q], V.h0), rhi = std::min(P.own_hi[q], V.h1);
-    if (rhi > rlo) RBF_NCCL_TRY(api.Recv(win + (rlo - V.h0), (size_t)(rhi - rlo), dt, q, comm_of(ctx), s));
+    const int64_t rlo = std::max(P.own_lo[q], base), rhi = std::min(P.own_hi[q], V.h1);
+    if (rhi > rlo && V.o1 > V.o0) recvs.push_back(Xfer{q, win + (rlo - base), rhi - rlo});
   }
-  RBF_NCCL_TRY(api.GroupEnd());
+  return ctx->tr->exchange(ctx, s, sends, recvs, sizeof(T) == 8 ? DType::F64 : DType::F32);
+}
+template rbf_status halo_exchange<float>(rbf_ctx*, const rbf_cells*, const float*, float*, bool);
+template rbf_status halo_exchange<double>(rbf_ctx*, const rbf_cells*, const double*, double*, bool);
+
+namespace {
+__global__ void add_into(double* __restrict__ dst, const double* __restrict__ src, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] += src[i];
+}
+}  // namespace
+
+rbf_status halo_reduce(rbf_ctx* ctx, const rbf_cells* c, const double* fwin, double* f_loc) {
+  cudaStream_t s = ctx->stream;
+  const SlabView& V = c->view;
+  const SlabPlan& P = c->plan;
+  const int64_t nl = V.o1 - V.o0;
+  if (nl > 0 && f_loc != fwin)
+    RBF_CUDA_TRY(cudaMemcpyAsync(f_loc, fwin, sizeof(double) * nl, cudaMemcpyDeviceToDevice, s));
+  if (ctx->world == 1) return RBF_OK;
+  std::vector<Xfer> sends, recvs;
+  std::vector<std::pair<int64_t, int64_t>> segs;   // (offset in f_loc, count) per receive
+  int64_t scratch = 0;
+  for (int q = 0; q < ctx->world; ++q) {
+    if (q == ctx->rank || P.own_hi[q] <= P.own_lo[q]) continue;
+    // contributions I accumulated for q's sources: q's slice inside my window beyond o1
+    const int64_t slo = std::max(P.own_lo[q], V.o1), shi = std::min(P.own_hi[q], V.h1);
+    if (shi > slo && nl > 0) sends.push_back(Xfer{q, const_cast<double*>(fwin) + (slo - V.o0), shi - slo});
+    // q's contributions to my slice: my slice inside q's window beyond q's slice
+    const int64_t rlo = std::max(V.o0, P.own_hi[q]), rhi = std::min(V.o1, P.win_hi[q]);
+    if (rhi > rlo) {
+      segs.push_back({rlo - V.o0, rhi - rlo});
+      recvs.push_back(Xfer{q, nullptr, rhi - rlo});
+      scratch += rhi - rlo;
+    }
+  }
+  RBF_TRY(ctx->rsc.ensure(sizeof(double) * std::max<int64_t>(scratch, 1), s));
+  int64_t off = 0;
+  for (Xfer& x : recvs) { x.ptr = ctx->rsc.as<double>() + off; off += x.count; }
+  RBF_TRY(ctx->tr->exchange(ctx, s, sends, recvs, DType::F64));
+  off = 0;
+  for (auto& sg : segs) {   // fixed order (ascending rank)
+    add_into<<<grid_for(sg.second, 256), 256, 0, s>>>(f_loc + sg.first, ctx->rsc.as<double>() + off, sg.second);
+    RBF_CHECK_LAUNCH();
+    off += sg.second;
+  }
   return RBF_OK;
 }
-template rbf_status halo_exchange<float>(rbf_ctx*, const rbf_cells*, const float*, float*);
-template rbf_status halo_exchange<double>(rbf_ctx*, const rbf_cells*, const double*, double*);
 
 rbf_status allreduce_sum(rbf_ctx* ctx, double* x, int64_t count) {
   if (ctx->world == 1 || count == 0) return RBF_OK;
-  RBF_NCCL_TRY(nccl().AllReduce(x, x, (size_t)count, kNcclFloat64, kNcclSum, comm_of(ctx), ctx->stream));
-  return RBF_OK;
-}
-rbf_status allreduce_sum_f32(rbf_ctx* ctx, float* x, int64_t count) {
-  if (ctx->world == 1 || count == 0) return RBF_OK;
-  RBF_NCCL_TRY(nccl().AllReduce(x, x, (size_t)count, kNcclFloat32, kNcclSum, comm_of(ctx), ctx->stream));
-  return RBF_OK;
+  return ctx->tr->allreduce_sum(ctx, ctx->stream, x, count, DType::F64);
 }
 
 // full[0, n) (sorted order) <- every rank's owned slice; full + o0 must already
 // hold this rank's slice
 rbf_status allgather_sorted(rbf_ctx* ctx, const rbf_cells* c, double* full) {
   if (ctx->world == 1) return RBF_OK;
-  NcclApi& api = nccl();
   const SlabPlan& P = c->plan;
-  RBF_NCCL_TRY(api.GroupStart());
+  const SlabView& V = c->view;
+  std::vector<Xfer> sends, recvs;
   for (int q = 0; q < ctx->world; ++q) {
-    const int64_t lo = P.own_lo[q], cnt = P.own_hi[q] - lo;
-    if (cnt > 0) RBF_NCCL_TRY(api.Broadcast(full + lo, full + lo, (size_t)cnt, kNcclFloat64, q, comm_of(ctx),
-                                            ctx->stream));
+    if (q == ctx->rank) continue;
+    if (V.o1 > V.o0) sends.push_back(Xfer{q, full + V.o0, V.o1 - V.o0});
+    if (P.own_hi[q] > P.own_lo[q]) recvs.push_back(Xfer{q, full + P.own_lo[q], P.own_hi[q] - P.own_lo[q]});
   }
-  RBF_NCCL_TRY(api.GroupEnd());
-  return RBF_OK;
+  return ctx->tr->exchange(ctx, ctx->stream, sends, recvs, DType::F64);
+}
+
+void grid_layers(const rbf_cells* c, const rbf_grid* g, int r, int64_t* k0, int64_t* k1) {
+  const int nz = g->n[2];
+  const int nbz = (nz + 3) / 4;
+  if (c->world == 1) { *k0 = 0; *k1 = nz; return; }
+  const double step = (g->hi[2] - g->lo[2]) / (double)(nz - 1);
+  const int p0 = c->plan.plane_lo[r], p1 = c->plan.plane_lo[r + 1];
+  int bz0 = nbz, bz1 = nbz;
+  for (int bz = 0; bz < nbz; ++bz) {
+    const float z = (float)(g->lo[2] + (double)(4 * bz) * step);
+    int pz = (int)std::floor((double)((z - c->lo[2]) * c->inv_h));
+    pz = std::min(std::max(pz, 0), c->dim[2] - 1);
+    // the first rank owns everything below the cell grid, the last everything above
+    const bool mine = pz >= p0 && pz < p1;
+    if (mine && bz0 == nbz) bz0 = bz;
+    if (mine) bz1 = bz + 1;
+  }
+  if (bz0 == nbz) bz1 = bz0;
+  *k0 = std::min<int64_t>(4 * (int64_t)bz0, nz);
+  *k1 = std::min<int64_t>(4 * (int64_t)bz1, nz);
+}
+
+rbf_status allgather_layers(rbf_ctx* ctx, const rbf_cells* c, const rbf_grid* g, float* field) {
+  if (ctx->world == 1) return RBF_OK;
+  const int64_t layer = (int64_t)g->n[0] * g->n[1];
+  int64_t m0, m1;
+  grid_layers(c, g, ctx->rank, &m0, &m1);
+  std::vector<Xfer> sends, recvs;
+  for (int q = 0; q < ctx->world; ++q) {
+    if (q == ctx->rank) continue;
+    int64_t q0, q1;
+    grid_layers(c, g, q, &q0, &q1);
+    if (m1 > m0) sends.push_back(Xfer{q, field + m0 * layer, (m1 - m0) * layer});
+    if (q1 > q0) recvs.push_back(Xfer{q, field + q0 * layer, (q1 - q0) * layer});
+  }
+  return ctx->tr->exchange(ctx, ctx->stream, sends, recvs, DType::F32);
 }
 
 rbf_status nccl_unique_id(void* out128) {
@@ -292,6 +487,21 @@ rbf_status rbf_nccl_unique_id(void* out128) {
   if (!out128) { set_error("out is NULL"); return RBF_EINVAL; }
   return nccl_unique_id(out128);
 }
+
+rbf_status rbf_loopback_group_create(int world, rbf_loopback_group** out) {
+  if (!out) { set_error("out is NULL"); return RBF_EINVAL; }
+  *out = nullptr;
+  if (world < 1 || world > kLoopMaxWorld) { set_error("loopback world must be in [1, 64]"); return RBF_EINVAL; }
+  LoopGroup* g = new (std::nothrow) LoopGroup();
+  if (!g) { set_error("host allocation failed"); return RBF_ENOMEM; }
+  g->world = world;
+  g->slots.resize(world);
+  g->joined.assign(world, 0);
+  *out = reinterpret_cast<rbf_loopback_group*>(g);
+  return RBF_OK;
+}
+
+void rbf_loopback_group_free(rbf_loopback_group* g) { delete reinterpret_cast<LoopGroup*>(g); }
 
 rbf_status rbf_slab_plan(const int64_t* plane_start, const double* plane_weight, int dimz, int reach, int world,
                          int32_t* plane_lo, int64_t* own_lo, int64_t* own_hi, int64_t* win_lo, int64_t* win_hi) {

@@ -456,8 +456,7 @@ rbf_status rbf_gmres_solve(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* k
   }
   if (precond && precond->cells != c) { set_error("precond was built for other cells"); return RBF_EINVAL; }
   if (c->world != ctx->world) { set_error("cells were partitioned for another world size"); return RBF_EINVAL; }
-  if (c->emulated) { set_error("RBF_SLAB_EMULATE cells support matvec / grid / precond blocks only"); return RBF_EUNSUPPORTED; }
-  if (gcfg && (gcfg->op_variant < RBF_OP_AUTO || gcfg->op_variant > RBF_OP_SYM_WIDE)) {
+  if (gcfg && (gcfg->op_variant < RBF_OP_AUTO || gcfg->op_variant > RBF_OP_SYM_ROT)) {
     set_error("bad operator variant");
     return RBF_EINVAL;
   }

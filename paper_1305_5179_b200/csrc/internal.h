@@ -10,6 +10,7 @@
 
 namespace rbf {
 
+struct Transport;
 void set_error(const std::string& msg);
 
 #define RBF_CUDA_TRY(expr)                                                     \
@@ -139,10 +140,13 @@ struct rbf_ctx {
   }
   // vector workspaces for matvec (sorted order)
   rbf::DevBuf vec_a, vec_b, src4;
-  // multi-GPU (dist.cu): NCCL communicator (ncclComm_t), rank, world, halo window
+  // multi-rank slab partition (dist.cu): the transport (NCCL communicator or
+  // in-process loopback group), rank, world, halo windows and scratch
   void* nccl_comm = nullptr;
+  rbf::Transport* tr = nullptr;
+  void* loop_group = nullptr;   // rbf::LoopGroup of a loopback context
   int rank = 0, world = 1;
-  rbf::DevBuf win;
+  rbf::DevBuf win, fwin, rsc, red, pwin;
 };
 
 namespace rbf {
@@ -191,11 +195,11 @@ struct rbf_cells {
   // wide plan (<= 128 targets, 4 per lane) of the symmetric fp32 matvec (reading R19)
   int64_t ntiles_w = 0;
   rbf::DevBuf tiles_w, tile_box_w;
+  rbf::DevBuf order_w;       // this rank's wide tiles, most expensive first (summation.cu order_wide_tiles)
   cudaStream_t stream = nullptr;
   rbf::SlabView view;        // this rank's share (whole range on one GPU)
   rbf::SlabPlan plan;        // all ranks' slabs (world > 1)
   int world = 1;             // ranks the cells were partitioned for
-  bool emulated = false;     // RBF_SLAB_EMULATE: one rank's slab on a single GPU (tests)
   int64_t n_loc() const { return view.o1 - view.o0; }
 };
 
@@ -234,21 +238,32 @@ rbf_status matvec_sorted_f32(rbf_ctx* ctx, const rbf_cells* c, const KernelParam
 rbf_status matvec_sorted_f64(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
                              const double* w_sorted, double* f_sorted, const int32_t* out_perm,
                              int op = RBF_OP_ONESIDED);
+rbf_status order_wide_tiles(rbf_ctx* ctx, rbf_cells* c, const KernelParams& kp);
 rbf_status eval_grid_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
                             const double* w_sorted, const rbf_grid* g, float* field,
                             unsigned long long* pair_stats = nullptr);
 
-// dist.cu (multi-GPU slab partition)
+// dist.cu (multi-rank slab partition over a Transport)
 rbf_status dist_init(rbf_ctx* ctx, const void* unique_id, int rank, int world);
 void dist_destroy(rbf_ctx* ctx);
 void slab_plan(const int64_t* plane_start, const double* weight, int dimz, int reach, int world, SlabPlan& P);
 rbf_status dist_plan_cells(rbf_ctx* ctx, rbf_cells* c, const std::vector<uint32_t>& row_tile_off, int64_t ntiles,
                            const std::vector<uint32_t>& row_tile_off_w, int64_t ntiles_w, int rank, int world);
+// win <- the matvec source window of the distributed vector whose owned slice
+// is x_loc: [h0, h1) (both neighbours), or [o0, h1) with upper_only (the
+// symmetric operators: sources before a tile are never read, reading R19)
 template <class T>
-rbf_status halo_exchange(rbf_ctx* ctx, const rbf_cells* c, const T* x_loc, T* win);
+rbf_status halo_exchange(rbf_ctx* ctx, const rbf_cells* c, const T* x_loc, T* win, bool upper_only = false);
+// symmetric operators: f_loc[0, o1-o0) = fwin[0, o1-o0) + the contributions to
+// this rank's targets that lower ranks accumulated in their windows; fwin covers
+// [o0, h1) and its part beyond o1 is sent to the owners (reverse halo reduce)
+rbf_status halo_reduce(rbf_ctx* ctx, const rbf_cells* c, const double* fwin, double* f_loc);
 rbf_status allreduce_sum(rbf_ctx* ctx, double* x, int64_t count);
-rbf_status allreduce_sum_f32(rbf_ctx* ctx, float* x, int64_t count);
 rbf_status allgather_sorted(rbf_ctx* ctx, const rbf_cells* c, double* full);
+// the grid's node layers [k0, k1) owned by rank r (z layers; a layer belongs to
+// the rank owning the cell plane of its first node block)
+void grid_layers(const rbf_cells* c, const rbf_grid* g, int r, int64_t* k0, int64_t* k1);
+rbf_status allgather_layers(rbf_ctx* ctx, const rbf_cells* c, const rbf_grid* g, float* field);
 
 // small vector kernels (vec.cu)
 rbf_status gather_f32_to_sorted(rbf_ctx* ctx, const float* src, const int32_t* perm, float* dst, int64_t n);

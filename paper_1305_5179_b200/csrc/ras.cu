@@ -129,7 +129,10 @@ ext_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ cell_s
            const int64_t* __restrict__ core_ptr, const int32_t* __restrict__ core_idx,
            const int32_t* __restrict__ owner, const uint32_t* __restrict__ keys, float ov2, float ov,
            int64_t nblocks, int cap, uint32_t* __restrict__ ext_count, int32_t* __restrict__ stage,
-           int* __restrict__ err) {
+           int* __restrict__ err, int jbase, int jend) {
+  // indices (core_idx, owner, sorted, keys, stage) are relative to jbase (the
+  // window start of a slab partition; 0 on one GPU); candidates are the global
+  // sorted positions [jbase, jend)
   __shared__ float cx[kMaxCore], cy[kMaxCore], cz[kMaxCore];
   __shared__ float cbox[kMaxCoreCells][3];      // lower corner of each core cell
   __shared__ int cbeg[kMaxCoreCells + 1];       // core-local start of each core cell
@@ -206,7 +209,8 @@ ext_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ cell_s
     for (int z = lo[2]; z <= hi[2]; ++z)
       for (int y = lo[1]; y <= hi[1]; ++y) {
         const int64_t row = ((int64_t)z * g.dim[1] + y) * g.dim[0];
-        const int s = cell_start[row + lo[0]], e = cell_start[row + hi[0] + 1];
+        const int s = max(cell_start[row + lo[0]], jbase) - jbase;
+        const int e = min(cell_start[row + hi[0] + 1], jend) - jbase;
         for (int j0 = s; j0 < e; j0 += blockDim.x) {
           const int j = j0 + tid;
           bool mem = false;
@@ -261,6 +265,11 @@ ext_kernel(const float4* __restrict__ sorted, const int32_t* __restrict__ cell_s
 }
 
 // ext_idx[ext_ptr[b] ...] = [staged members] + [core]
+__global__ void shift_idx(int32_t* __restrict__ idx, int64_t n, int32_t d) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    idx[i] += d;
+}
+
 __global__ void ext_assemble(const int64_t* __restrict__ core_ptr, const int32_t* __restrict__ core_idx,
                              const int64_t* __restrict__ ext_ptr, const int32_t* __restrict__ stage, int cap,
                              int64_t nblocks, int32_t* __restrict__ ext_idx) {
@@ -831,10 +840,20 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
   const double shift_abs = shift * kp.amp;
   const bool want_fp32 = cfg && cfg->local_fp32;
 
-  if (ctx->world > 1 && ovs > 0) {
-    set_error("RAS with overlap is single-GPU only; use block-Jacobi (kind 1) across slabs");
+  // slab partition with overlap (the paper's distributed RASM): the
+  // extended sets reach into the neighbouring slabs, so every index of the
+  // preconditioner is relative to the matvec window start h0 (which covers the
+  // overlap when overlap <= cutoff) and the apply reads r from the halo window
+  const bool halo = ctx->world > 1 && ovs > 0;
+  if (halo && ovs * kp.sigma > kp.cutoff) {
+    set_error("across slabs the RAS overlap must not exceed the kernel cutoff");
     return RBF_EUNSUPPORTED;
   }
+  const int64_t wbase = halo ? c->view.h0 : base;
+  const int64_t nwin = halo ? c->view.h1 - c->view.h0 : n;
+  P->shift_idx = (int)(base - wbase);
+  P->halo = halo;
+  const float4* sortedw = c->sorted.as<float4>() + wbase;
   if (n == 0) { P->nblocks = 0; P->bytes = 0; P->kind = 0; return RBF_OK; }   // empty slab
 
   // 1. non-empty cells
@@ -924,11 +943,17 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
   RBF_CUDA_TRY(cudaMemcpyAsync(P->core_ptr.p, h_core_ptr.data(), 8 * (ncore + 1), cudaMemcpyHostToDevice, s));
   RBF_TRY(P->core_idx.alloc(4 * n, s));
   DevBuf owner;
-  RBF_TRY(owner.alloc(4 * n, s));
+  RBF_TRY(owner.alloc(4 * std::max<int64_t>(nwin, 1), s));
+  if (halo) RBF_CUDA_TRY(cudaMemsetAsync(owner.p, 0xff, 4 * nwin, s));   // -1: outside the slab
   core_members<<<grid_for(nne * 32, 256), 256, 0, s>>>(order.as<int32_t>(), ne_start.as<int32_t>(),
                                                        Pm.as<uint32_t>(), cnt.as<uint32_t>(), cell_core.as<int32_t>(),
-                                                       nne, P->core_idx.as<int32_t>(), owner.as<int32_t>());
+                                                       nne, P->core_idx.as<int32_t>(),
+                                                       owner.as<int32_t>() + P->shift_idx);
   RBF_CHECK_LAUNCH();
+  if (P->shift_idx) {   // core positions relative to the window start
+    shift_idx<<<grid_for(n, 256), 256, 0, s>>>(P->core_idx.as<int32_t>(), n, P->shift_idx);
+    RBF_CHECK_LAUNCH();
+  }
   mark("cores");
   // 4. extended sets
   CellGrid g;
@@ -949,10 +974,11 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
   } else {
     RBF_TRY(ecount.alloc(4 * ncore, s));
     RBF_TRY(stage.alloc(sizeof(int32_t) * (size_t)ncore * max_ext, s));
-    ext_kernel<<<eblocks, 256, 0, s>>>(c->sorted.as<float4>(), c->cell_start.as<int32_t>(), g,
+    ext_kernel<<<eblocks, 256, 0, s>>>(sortedw, c->cell_start.as<int32_t>(), g,
                                        P->core_ptr.as<int64_t>(), P->core_idx.as<int32_t>(), owner.as<int32_t>(),
-                                       c->keys.as<uint32_t>(), ov2, (float)ov, ncore, max_ext,
-                                       ecount.as<uint32_t>(), stage.as<int32_t>(), err.as<int>());
+                                       c->keys.as<uint32_t>() + wbase, ov2, (float)ov, ncore, max_ext,
+                                       ecount.as<uint32_t>(), stage.as<int32_t>(), err.as<int>(), (int)wbase,
+                                       (int)(wbase + nwin));
     RBF_CHECK_LAUNCH();
     RBF_CUDA_TRY(cudaMemcpyAsync(h_ecount.data(), ecount.p, 4 * ncore, cudaMemcpyDeviceToHost, s));
     RBF_CUDA_TRY(cudaMemcpyAsync(&herr0, err.p, 4, cudaMemcpyDeviceToHost, s));
@@ -1063,7 +1089,7 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
           RBF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGjThreads, 0));
           const int gblocks = (int)std::min<int64_t>(cnt, (int64_t)ctx->sm_count * std::max(per_sm, 1));
           kern<<<gblocks, kGjThreads, 0, s>>>(P->ext_ptr.as<int64_t>(), P->core_ptr.as<int64_t>(),
-                                              P->ext_idx.as<int32_t>(), P->w_off.as<int64_t>(), sorted, kp.amp,
+                                              P->ext_idx.as<int32_t>(), P->w_off.as<int64_t>(), sortedw, kp.amp,
                                               two_s2, c2, shift_abs, P->W.as<float>(), bl, cnt, info.as<int>(),
                                               P->w_sym);
           RBF_CHECK_LAUNCH();
@@ -1116,7 +1142,7 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
     RBF_TRY(jobs_d.ensure(sizeof(LuJob) * jobs.size(), s));
     RBF_CUDA_TRY(cudaMemcpyAsync(jobs_d.p, jobs.data(), sizeof(LuJob) * jobs.size(), cudaMemcpyHostToDevice, s));
     dim3 ag(32, (unsigned)jobs.size());
-    assemble_kernel<<<ag, 256, 0, s>>>(jobs_d.as<LuJob>(), sorted, P->ext_idx.as<int32_t>(),
+    assemble_kernel<<<ag, 256, 0, s>>>(jobs_d.as<LuJob>(), sortedw, P->ext_idx.as<int32_t>(),
                                        ws.as<FT>(), kp.amp, two_s2, c2, shift_abs);
     RBF_CHECK_LAUNCH();
     RBF_TRY(batched_lu_restricted_inverse(ctx, jobs_d.as<LuJob>(), jobs, ws.as<FT>(),
@@ -1152,6 +1178,16 @@ constexpr int kApplyThreads = 128;
 template <class VT>
 rbf_status precond_apply_sorted(rbf_ctx* ctx, const rbf_precond* P, const VT* r, VT* z) {
   cudaStream_t s = ctx->stream;
+  if (P->halo) {
+    // distributed RAS: r over the window [h0, h1) (halo exchange), z written at
+    // the core rows only (this rank's slice), both indexed from h0
+    const rbf_cells* c = P->cells;
+    const int64_t nw = c->view.h1 - c->view.h0;
+    RBF_TRY(ctx->pwin.ensure(sizeof(VT) * std::max<int64_t>(nw, 1), s));
+    RBF_TRY(halo_exchange<VT>(ctx, c, r, ctx->pwin.as<VT>(), false));
+    r = ctx->pwin.as<VT>();
+    z -= P->shift_idx;
+  }
   if (P->kind == 0 || P->nblocks == 0) {
     copy_kernel<VT><<<grid_for(P->n, 256), 256, 0, s>>>(r, z, P->n);
     RBF_CHECK_LAUNCH();
@@ -1262,6 +1298,12 @@ rbf_status rbf_precond_blocks(const rbf_precond* P, int64_t* nblocks, int64_t* b
   if (ext_idx)
     RBF_CUDA_TRY(cudaMemcpyAsync(ext_idx, P->ext_idx.p, 4 * P->h_ext_ptr[nb], cudaMemcpyDeviceToHost, s));
   RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  // report positions relative to this rank's owned start o0 (ext members of a
+  // distributed RAS block may lie below it: negative)
+  if (P->shift_idx) {
+    if (core_idx) for (int64_t i = 0; i < P->h_core_ptr[nb]; ++i) core_idx[i] -= P->shift_idx;
+    if (ext_idx) for (int64_t i = 0; i < P->h_ext_ptr[nb]; ++i) ext_idx[i] -= P->shift_idx;
+  }
   return RBF_OK;
 }
 

@@ -18,6 +18,8 @@ struct rbf_precond {
   int64_t max_wblk = 0;   // floats of the largest W_i
   int cap_w = 6144;       // apply staging size (floats; w_sym)
   double t_setup = 0.0;
+  bool halo = false;      // slab partition with overlap: indices relative to the window start h0
+  int shift_idx = 0;      // o0 - (index origin): 0 unless halo
   const rbf_cells* cells = nullptr;
   rbf::DevBuf core_ptr;   // int64[nblocks+1]
   rbf::DevBuf ext_ptr;    // int64[nblocks+1]

@@ -782,6 +782,497 @@ sum_f32_symw_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const flo
   }
 }
 
+// Symmetric fp32 matvec, rotation form (reading R19; the solver's default at
+// >= 2^18 centres per GPU).  Same pair set and conventions as
+// sum_f32_symw_kernel (wide plan, up to 128 targets per warp = 2 pairs of
+// 32-target slots per lane; sources of this rank before the tile never loaded;
+// the tile's own sources one-sided; every source after it, up to the end of the
+// window sym_hi, evaluated ONCE for both f_i and f_j), but the source side is
+// summed without a per-source warp reduction: the symmetric sources are staged
+// 32 at a time and lane l visits source (l + k) mod 32 at step k of 32, adding
+// its targets' share sum_t e_tj w_t 2^-|t'_t|^2 to a rotating accumulator that
+// moves one lane down per step (one shuffle), so after 32 steps lane l holds the
+// whole warp's sum for source l: one atomic per source, no shuffle tree, no
+// selects.  Targets are packed in pairs along the FFMA2 lanes (each step: 3
+// FFMA2 for r^2 of 2 targets, 2 MUFU.EX2, 2 FFMA2 accumulates).  All ring
+// addressing is on the kernel's own shared arrays (32-bit shared addresses).
+constexpr int kRotFlush = 96;                       // symmetric sources per flush (3 rotations)
+constexpr int kRotCap = kRotFlush + 32;             // ring capacity
+constexpr int kOwnCap = kFlush + 32 + 4;            // own-tile ring capacity (one-sided, SoA)
+constexpr int kOwnPad = 136;
+
+template <int TP, class OutT>
+__device__ __forceinline__ void symr_tile(const SumGeom& G, const int32_t* __restrict__ cell_start,
+                                          const float4* __restrict__ src, float3 blo, float3 bhi, float3 ctr,
+                                          const float* xr, const float* yr, const float* zr, const bool* tv,
+                                          const float* wg, int2 tl, int64_t sym_hi, int lane,
+                                          float4* __restrict__ R4, float2* __restrict__ R2, int* __restrict__ RI,
+                                          float (*__restrict__ O)[kOwnPad], OutT* __restrict__ out,
+                                          float* fo) {
+  constexpr int T = 2 * TP;
+  float2 m2x[TP], m2y[TP], m2z[TP], wt2[TP], acc2[TP];
+  float tf[T];
+#pragma unroll
+  for (int tp = 0; tp < TP; ++tp) {
+    float mx[2], my[2], mz[2], ww[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = 2 * tp + h;
+      const float tx = (xr[t] - ctr.x) * G.s, ty = (yr[t] - ctr.y) * G.s, tz = (zr[t] - ctr.z) * G.s;
+      const float T2 = fmaf(tz, tz, fmaf(ty, ty, tx * tx));
+      mx[h] = -2.f * tx; my[h] = -2.f * ty; mz[h] = -2.f * tz;
+      tf[t] = ex2(-T2);
+      ww[h] = tv[t] ? wg[t] * tf[t] : 0.f;
+    }
+    m2x[tp] = make_float2(mx[0], mx[1]);
+    m2y[tp] = make_float2(my[0], my[1]);
+    m2z[tp] = make_float2(mz[0], mz[1]);
+    wt2[tp] = make_float2(ww[0], ww[1]);
+    acc2[tp] = make_float2(0.f, 0.f);
+  }
+  const float amp = G.amp;
+  const int t_end = tl.x + tl.y;
+  // symmetric ring: R4[i] = (x', y', z', w), R2[i] = (|s'|^2, |s'|^2); RI[i] = sorted index
+  auto flush_sym = [&](int cnt) {   // cnt: multiple of 32
+    for (int b = 0; b < cnt; b += 32) {
+      float accr = 0.f;
+#pragma unroll 4
+      for (int k = 0; k < 32; ++k) {
+        const int si = b + ((lane + k) & 31);
+        const float4 P = R4[si];
+        const float2 S2 = R2[si];
+        float2 ps = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int tp = 0; tp < TP; ++tp) {
+          float2 rr = fma2(m2z[tp], make_float2(P.z, P.z), S2);
+          rr = fma2(m2y[tp], make_float2(P.y, P.y), rr);
+          rr = fma2(m2x[tp], make_float2(P.x, P.x), rr);
+          const float2 e = make_float2(ex2(-rr.x), ex2(-rr.y));
+          acc2[tp] = fma2(e, make_float2(P.w, P.w), acc2[tp]);
+          ps = fma2(e, wt2[tp], ps);
+        }
+        accr += ps.x + ps.y;
+        accr = __shfl_sync(0xffffffffu, accr, (lane + 1) & 31);
+      }
+      const int j = RI[b + lane];
+      if (j >= 0) atomicAdd(out + j, (OutT)(amp * accr));
+    }
+  };
+  // own-tile ring (one-sided, broadcast of 4 sources to all lanes, SoA)
+  auto flush_own = [&](int cnt) {   // cnt: multiple of 4
+#pragma unroll 1
+    for (int j = 0; j < cnt; j += 4) {
+      const float4 X = *reinterpret_cast<const float4*>(&O[0][j]);
+      const float4 Y = *reinterpret_cast<const float4*>(&O[1][j]);
+      const float4 Z = *reinterpret_cast<const float4*>(&O[2][j]);
+      const float4 S = *reinterpret_cast<const float4*>(&O[3][j]);
+      const float4 W = *reinterpret_cast<const float4*>(&O[4][j]);
+      const float Sv[4] = {S.x, S.y, S.z, S.w}, Xv[4] = {X.x, X.y, X.z, X.w}, Yv[4] = {Y.x, Y.y, Y.z, Y.w},
+                  Zv[4] = {Z.x, Z.y, Z.z, Z.w}, Wv[4] = {W.x, W.y, W.z, W.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+#pragma unroll
+        for (int tp = 0; tp < TP; ++tp) {
+          float2 rr = fma2(m2z[tp], make_float2(Zv[q], Zv[q]), make_float2(Sv[q], Sv[q]));
+          rr = fma2(m2y[tp], make_float2(Yv[q], Yv[q]), rr);
+          rr = fma2(m2x[tp], make_float2(Xv[q], Xv[q]), rr);
+          const float2 e = make_float2(ex2(-rr.x), ex2(-rr.y));
+          acc2[tp] = fma2(e, make_float2(Wv[q], Wv[q]), acc2[tp]);
+        }
+      }
+    }
+  };
+  // traversal of the cell rows within the culling radius of the box
+  const CellGrid& g = G.g;
+  const float cc = G.cc, cc2 = G.cc2, h = g.h;
+  const int z0 = cellof(blo.z - cc, g.lo[2], g.inv_h, g.dim[2]);
+  const int z1 = cellof(bhi.z + cc, g.lo[2], g.inv_h, g.dim[2]);
+  const int y0 = cellof(blo.y - cc, g.lo[1], g.inv_h, g.dim[1]);
+  const int y1 = cellof(bhi.y + cc, g.lo[1], g.inv_h, g.dim[1]);
+  const unsigned lt = (1u << lane) - 1u;
+  int nS = 0, nO = 0;
+  for (int cz = z0; cz <= z1; ++cz) {
+    const float czlo = g.lo[2] + (float)cz * h;
+    const float gz = fmaxf(0.f, fmaxf(czlo - bhi.z, blo.z - (czlo + h)));
+    for (int cy = y0; cy <= y1; ++cy) {
+      const float cylo = g.lo[1] + (float)cy * h;
+      const float gy = fmaxf(0.f, fmaxf(cylo - bhi.y, blo.y - (cylo + h)));
+      const float rem = cc2 - gy * gy - gz * gz;
+      if (rem < 0.f) continue;
+      const float rx = sqrtf(rem);
+      const int x0 = cellof(blo.x - rx, g.lo[0], g.inv_h, g.dim[0]);
+      const int x1 = cellof(bhi.x + rx, g.lo[0], g.inv_h, g.dim[0]);
+      const int64_t rowbase = ((int64_t)cz * g.dim[1] + cy) * g.dim[0];
+      int sb = __ldg(cell_start + rowbase + x0);
+      int se = __ldg(cell_start + rowbase + x1 + 1);
+      // sources before the tile are never loaded (their tiles hold the pairs);
+      // the window ends at sym_hi
+      sb = max(sb, tl.x);
+      se = min(se, (int)sym_hi);
+      for (int j0 = sb; j0 < se; j0 += 32) {
+        const int j = j0 + lane;
+        const bool valid = j < se;
+        const float4 p = valid ? __ldg(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float gx = fmaxf(0.f, fmaxf(blo.x - p.x, p.x - bhi.x));
+        const float gyy = fmaxf(0.f, fmaxf(blo.y - p.y, p.y - bhi.y));
+        const float gzz = fmaxf(0.f, fmaxf(blo.z - p.z, p.z - bhi.z));
+        const bool keep = valid && (gx * gx + gyy * gyy + gzz * gzz <= cc2);
+        const bool own = j < t_end;
+        const unsigned bs = __ballot_sync(0xffffffffu, keep && !own);
+        const unsigned bo = __ballot_sync(0xffffffffu, keep && own);
+        const float sx = (p.x - ctr.x) * G.s, sy = (p.y - ctr.y) * G.s, sz = (p.z - ctr.z) * G.s;
+        const float ss = fmaf(sz, sz, fmaf(sy, sy, sx * sx));
+        if (keep && !own) {
+          const int pos = nS + __popc(bs & lt);
+          R4[pos] = make_float4(sx, sy, sz, p.w);
+          R2[pos] = make_float2(ss, ss);
+          RI[pos] = j;
+        } else if (keep) {
+          const int pos = nO + __popc(bo & lt);
+          O[0][pos] = sx; O[1][pos] = sy; O[2][pos] = sz; O[3][pos] = ss; O[4][pos] = p.w;
+        }
+        nS += __popc(bs);
+        nO += __popc(bo);
+        if (nS >= kRotFlush) {
+          __syncwarp();
+          flush_sym(kRotFlush);
+          __syncwarp();
+          if (lane < nS - kRotFlush) {
+            const float4 a = R4[kRotFlush + lane];
+            const float2 c = R2[kRotFlush + lane];
+            const int ii = RI[kRotFlush + lane];
+            R4[lane] = a; R2[lane] = c; RI[lane] = ii;
+          }
+          __syncwarp();
+          nS -= kRotFlush;
+        }
+        if (nO >= kFlush) {
+          __syncwarp();
+          flush_own(kFlush);
+          __syncwarp();
+          if (lane < nO - kFlush) {
+            const int q = kFlush + lane;
+            const float a = O[0][q], b = O[1][q], c = O[2][q], d = O[3][q], e = O[4][q];
+            O[0][lane] = a; O[1][lane] = b; O[2][lane] = c; O[3][lane] = d; O[4][lane] = e;
+          }
+          __syncwarp();
+          nO -= kFlush;
+        }
+      }
+    }
+  }
+  // tails: symmetric ring to a multiple of 32 with sources contributing exactly 0
+  // (|s'|^2 = 1e30: 2^-1e30 = 0) and no output (index -1); own ring to 4
+  {
+    const int cntS = (nS + 31) & ~31;
+    if (lane < cntS - nS) {
+      const int q = nS + lane;
+      R4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      R2[q] = make_float2(1e30f, 1e30f);
+      RI[q] = -1;
+    }
+    const int cntO = (nO + 3) & ~3;
+    if (lane < cntO - nO) {
+      const int q = nO + lane;
+      O[0][q] = 0.f; O[1][q] = 0.f; O[2][q] = 0.f; O[3][q] = 1e30f; O[4][q] = 0.f;
+    }
+    __syncwarp();
+    if (cntS) flush_sym(cntS);
+    flush_own(cntO);
+    __syncwarp();
+  }
+#pragma unroll
+  for (int tp = 0; tp < TP; ++tp) {
+    fo[2 * tp] = G.amp * (acc2[tp].x * tf[2 * tp]);
+    fo[2 * tp + 1] = G.amp * (acc2[tp].y * tf[2 * tp + 1]);
+  }
+}
+
+template <class OutT>
+__global__ void __launch_bounds__(kSumWarps * 32, 8)
+sum_f32_symr_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* __restrict__ src,
+                    const int2* __restrict__ tiles, const float4* __restrict__ tbox, int64_t ntiles,
+                    int64_t tile_base, OutT* __restrict__ out, int* __restrict__ work, int64_t sym_hi,
+                    const int32_t* __restrict__ order) {
+  __shared__ __align__(16) float4 ring4[kSumWarps][kRotCap];
+  __shared__ __align__(8) float2 ring2[kSumWarps][kRotCap];
+  __shared__ int ringi[kSumWarps][kRotCap];
+  __shared__ __align__(16) float ringo[kSumWarps][5][kOwnPad];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  for (;;) {
+    int64_t tile;
+    {
+      int t0 = 0;
+      if (lane == 0) t0 = atomicAdd(work, 1);
+      tile = __shfl_sync(0xffffffffu, t0, 0);
+    }
+    if (tile >= ntiles) break;
+    tile = order ? (int64_t)order[tile] : tile + tile_base;
+    const int2 tl = tiles[tile];
+    const float4 a = tbox[2 * tile], b = tbox[2 * tile + 1];
+    const float3 blo = make_float3(a.x, a.y, a.z), bhi = make_float3(b.x, b.y, b.z);
+    const float3 ctr = make_float3(0.5f * (blo.x + bhi.x), 0.5f * (blo.y + bhi.y), 0.5f * (blo.z + bhi.z));
+    float xr[4], yr[4], zr[4], wg[4], fo[4];
+    bool tv[4];
+    int64_t tidx[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int q = lane + 32 * t;
+      tv[t] = q < tl.y;
+      tidx[t] = tl.x + (tv[t] ? q : 0);
+      const float4 p = src[tidx[t]];
+      xr[t] = p.x; yr[t] = p.y; zr[t] = p.z; wg[t] = p.w;
+    }
+    const int TP = tl.y > 64 ? 2 : 1;
+    if (TP == 2)
+      symr_tile<2>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, ring4[wib], ring2[wib],
+                   ringi[wib], ringo[wib], out, fo);
+    else
+      symr_tile<1>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, ring4[wib], ring2[wib],
+                   ringi[wib], ringo[wib], out, fo);
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (t < 2 * TP && tv[t]) atomicAdd(out + tidx[t], (OutT)fo[t]);
+  }
+}
+
+// Symmetric fp32 matvec, broadcast form (reading R19): the pair set of
+// sum_f32_symr_kernel with sum_f32_symw_kernel's inner loop -- 4 staged sources
+// at a time broadcast to all lanes (LDS.128 of a shared-memory SoA ring), T <= 4
+// targets per lane, the source side of each group of 4 summed over the warp by a
+// transpose-reduction (6 shuffles) and one atomic per source -- with every ring
+// access on the kernel's own shared arrays (no generic-pointer address math).
+constexpr int kSymPad = 136;   // SoA ring row (>= kFlush + 32 + 4, multiple of 4)
+
+template <int T, class OutT>
+__device__ __forceinline__ void symb_tile(const SumGeom& G, const int32_t* __restrict__ cell_start,
+                                          const float4* __restrict__ src, float3 blo, float3 bhi, float3 ctr,
+                                          const float* xr, const float* yr, const float* zr, const bool* tv,
+                                          const float* wg, int2 tl, int64_t sym_hi, int lane,
+                                          float (*__restrict__ RS)[kSymPad], int* __restrict__ RI,
+                                          float (*__restrict__ O)[kOwnPad], OutT* __restrict__ out, float* fo) {
+  float mx[T], my[T], mz[T], tf[T], wt[T];
+  float2 acc[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const float tx = (xr[t] - ctr.x) * G.s, ty = (yr[t] - ctr.y) * G.s, tz = (zr[t] - ctr.z) * G.s;
+    const float T2 = fmaf(tz, tz, fmaf(ty, ty, tx * tx));
+    mx[t] = -2.f * tx; my[t] = -2.f * ty; mz[t] = -2.f * tz;
+    tf[t] = ex2(-T2);
+    wt[t] = tv[t] ? wg[t] * tf[t] : 0.f;
+    acc[t] = make_float2(0.f, 0.f);
+  }
+  const float amp = G.amp;
+  const int t_end = tl.x + tl.y;
+  const bool h4 = lane & 16, h3 = lane & 8;
+  const int mys = (h4 ? 2 : 0) + (h3 ? 1 : 0);
+  // symmetric ring RS[0..4] = x', y', z', |s'|^2, w and RI = sorted index
+  auto flush_sym = [&](int cnt) {   // cnt: multiple of 4
+#pragma unroll 1
+    for (int j = 0; j < cnt; j += 4) {
+      const float4 X = *reinterpret_cast<const float4*>(&RS[0][j]);
+      const float4 Y = *reinterpret_cast<const float4*>(&RS[1][j]);
+      const float4 Z = *reinterpret_cast<const float4*>(&RS[2][j]);
+      const float4 S = *reinterpret_cast<const float4*>(&RS[3][j]);
+      const float4 W = *reinterpret_cast<const float4*>(&RS[4][j]);
+      float2 pa = make_float2(0.f, 0.f), pb = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const float2 ax = make_float2(mx[t], mx[t]), ay = make_float2(my[t], my[t]), az = make_float2(mz[t], mz[t]);
+        float2 ra = fma2(make_float2(Z.x, Z.y), az, make_float2(S.x, S.y));
+        float2 rb = fma2(make_float2(Z.z, Z.w), az, make_float2(S.z, S.w));
+        ra = fma2(make_float2(Y.x, Y.y), ay, ra); rb = fma2(make_float2(Y.z, Y.w), ay, rb);
+        ra = fma2(make_float2(X.x, X.y), ax, ra); rb = fma2(make_float2(X.z, X.w), ax, rb);
+        const float2 ea = make_float2(ex2(-ra.x), ex2(-ra.y));
+        const float2 eb = make_float2(ex2(-rb.x), ex2(-rb.y));
+        acc[t] = fma2(ea, make_float2(W.x, W.y), acc[t]);
+        acc[t] = fma2(eb, make_float2(W.z, W.w), acc[t]);
+        const float2 wv = make_float2(wt[t], wt[t]);
+        pa = fma2(ea, wv, pa);
+        pb = fma2(eb, wv, pb);
+      }
+      // transpose-reduce (pa.x, pa.y, pb.x, pb.y) = sources j .. j+3 over the warp
+      float k0 = h4 ? pb.x : pa.x, k1 = h4 ? pb.y : pa.y;
+      const float s0 = h4 ? pa.x : pb.x, s1 = h4 ? pa.y : pb.y;
+      k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+      k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+      float k = h3 ? k1 : k0;
+      k += __shfl_xor_sync(0xffffffffu, h3 ? k0 : k1, 8);
+      k += __shfl_xor_sync(0xffffffffu, k, 4);
+      k += __shfl_xor_sync(0xffffffffu, k, 2);
+      k += __shfl_xor_sync(0xffffffffu, k, 1);
+      if ((lane & 7) == 0) {
+        const int jj = RI[j + mys];
+        if (jj >= 0) atomicAdd(out + jj, (OutT)(amp * k));
+      }
+    }
+  };
+  auto flush_own = [&](int cnt) {   // cnt: multiple of 4
+#pragma unroll 1
+    for (int j = 0; j < cnt; j += 4) {
+      const float4 X = *reinterpret_cast<const float4*>(&O[0][j]);
+      const float4 Y = *reinterpret_cast<const float4*>(&O[1][j]);
+      const float4 Z = *reinterpret_cast<const float4*>(&O[2][j]);
+      const float4 S = *reinterpret_cast<const float4*>(&O[3][j]);
+      const float4 W = *reinterpret_cast<const float4*>(&O[4][j]);
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const float2 ax = make_float2(mx[t], mx[t]), ay = make_float2(my[t], my[t]), az = make_float2(mz[t], mz[t]);
+        float2 ra = fma2(make_float2(Z.x, Z.y), az, make_float2(S.x, S.y));
+        float2 rb = fma2(make_float2(Z.z, Z.w), az, make_float2(S.z, S.w));
+        ra = fma2(make_float2(Y.x, Y.y), ay, ra); rb = fma2(make_float2(Y.z, Y.w), ay, rb);
+        ra = fma2(make_float2(X.x, X.y), ax, ra); rb = fma2(make_float2(X.z, X.w), ax, rb);
+        const float2 ea = make_float2(ex2(-ra.x), ex2(-ra.y));
+        const float2 eb = make_float2(ex2(-rb.x), ex2(-rb.y));
+        acc[t] = fma2(ea, make_float2(W.x, W.y), acc[t]);
+        acc[t] = fma2(eb, make_float2(W.z, W.w), acc[t]);
+      }
+    }
+  };
+  const CellGrid& g = G.g;
+  const float cc = G.cc, cc2 = G.cc2, h = g.h;
+  const int z0 = cellof(blo.z - cc, g.lo[2], g.inv_h, g.dim[2]);
+  const int z1 = cellof(bhi.z + cc, g.lo[2], g.inv_h, g.dim[2]);
+  const int y0 = cellof(blo.y - cc, g.lo[1], g.inv_h, g.dim[1]);
+  const int y1 = cellof(bhi.y + cc, g.lo[1], g.inv_h, g.dim[1]);
+  const unsigned lt = (1u << lane) - 1u;
+  int nS = 0, nO = 0;
+  for (int cz = z0; cz <= z1; ++cz) {
+    const float czlo = g.lo[2] + (float)cz * h;
+    const float gz = fmaxf(0.f, fmaxf(czlo - bhi.z, blo.z - (czlo + h)));
+    for (int cy = y0; cy <= y1; ++cy) {
+      const float cylo = g.lo[1] + (float)cy * h;
+      const float gy = fmaxf(0.f, fmaxf(cylo - bhi.y, blo.y - (cylo + h)));
+      const float rem = cc2 - gy * gy - gz * gz;
+      if (rem < 0.f) continue;
+      const float rx = sqrtf(rem);
+      const int x0 = cellof(blo.x - rx, g.lo[0], g.inv_h, g.dim[0]);
+      const int x1 = cellof(bhi.x + rx, g.lo[0], g.inv_h, g.dim[0]);
+      const int64_t rowbase = ((int64_t)cz * g.dim[1] + cy) * g.dim[0];
+      const int sb = max(__ldg(cell_start + rowbase + x0), tl.x);
+      const int se = min(__ldg(cell_start + rowbase + x1 + 1), (int)sym_hi);
+      for (int j0 = sb; j0 < se; j0 += 32) {
+        const int j = j0 + lane;
+        const bool valid = j < se;
+        const float4 p = valid ? __ldg(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float gx = fmaxf(0.f, fmaxf(blo.x - p.x, p.x - bhi.x));
+        const float gyy = fmaxf(0.f, fmaxf(blo.y - p.y, p.y - bhi.y));
+        const float gzz = fmaxf(0.f, fmaxf(blo.z - p.z, p.z - bhi.z));
+        const bool keep = valid && (gx * gx + gyy * gyy + gzz * gzz <= cc2);
+        const bool own = j < t_end;
+        const unsigned bs = __ballot_sync(0xffffffffu, keep && !own);
+        const unsigned bo = __ballot_sync(0xffffffffu, keep && own);
+        if (keep) {
+          const float sx = (p.x - ctr.x) * G.s, sy = (p.y - ctr.y) * G.s, sz = (p.z - ctr.z) * G.s;
+          const float ss = fmaf(sz, sz, fmaf(sy, sy, sx * sx));
+          if (!own) {
+            const int pos = nS + __popc(bs & lt);
+            RS[0][pos] = sx; RS[1][pos] = sy; RS[2][pos] = sz; RS[3][pos] = ss; RS[4][pos] = p.w;
+            RI[pos] = j;
+          } else {
+            const int pos = nO + __popc(bo & lt);
+            O[0][pos] = sx; O[1][pos] = sy; O[2][pos] = sz; O[3][pos] = ss; O[4][pos] = p.w;
+          }
+        }
+        nS += __popc(bs);
+        nO += __popc(bo);
+        if (nS >= kFlush) {
+          __syncwarp();
+          flush_sym(kFlush);
+          __syncwarp();
+          if (lane < nS - kFlush) {
+            const int q = kFlush + lane;
+            const float a = RS[0][q], b = RS[1][q], c = RS[2][q], d = RS[3][q], e = RS[4][q];
+            const int ii = RI[q];
+            RS[0][lane] = a; RS[1][lane] = b; RS[2][lane] = c; RS[3][lane] = d; RS[4][lane] = e; RI[lane] = ii;
+          }
+          __syncwarp();
+          nS -= kFlush;
+        }
+        if (nO >= kFlush) {
+          __syncwarp();
+          flush_own(kFlush);
+          __syncwarp();
+          if (lane < nO - kFlush) {
+            const int q = kFlush + lane;
+            const float a = O[0][q], b = O[1][q], c = O[2][q], d = O[3][q], e = O[4][q];
+            O[0][lane] = a; O[1][lane] = b; O[2][lane] = c; O[3][lane] = d; O[4][lane] = e;
+          }
+          __syncwarp();
+          nO -= kFlush;
+        }
+      }
+    }
+  }
+  {
+    const int cntS = (nS + 3) & ~3;
+    if (lane < cntS - nS) {
+      const int q = nS + lane;
+      RS[0][q] = 0.f; RS[1][q] = 0.f; RS[2][q] = 0.f; RS[3][q] = 1e30f; RS[4][q] = 0.f;
+      RI[q] = -1;
+    }
+    const int cntO = (nO + 3) & ~3;
+    if (lane < cntO - nO) {
+      const int q = nO + lane;
+      O[0][q] = 0.f; O[1][q] = 0.f; O[2][q] = 0.f; O[3][q] = 1e30f; O[4][q] = 0.f;
+    }
+    __syncwarp();
+    flush_sym(cntS);
+    flush_own(cntO);
+    __syncwarp();
+  }
+#pragma unroll
+  for (int t = 0; t < T; ++t) fo[t] = G.amp * ((acc[t].x + acc[t].y) * tf[t]);
+}
+
+#ifndef RBF_SYMB_MINB
+#define RBF_SYMB_MINB 8
+#endif
+template <class OutT>
+__global__ void __launch_bounds__(kSumWarps * 32, RBF_SYMB_MINB)
+sum_f32_symb_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* __restrict__ src,
+                    const int2* __restrict__ tiles, const float4* __restrict__ tbox, int64_t ntiles,
+                    int64_t tile_base, OutT* __restrict__ out, int* __restrict__ work, int64_t sym_hi,
+                    const int32_t* __restrict__ order) {
+  __shared__ __align__(16) float rings[kSumWarps][5][kSymPad];
+  __shared__ int ringi[kSumWarps][kSymPad];
+  __shared__ __align__(16) float ringo[kSumWarps][5][kOwnPad];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  for (;;) {
+    int64_t tile;
+    {
+      int t0 = 0;
+      if (lane == 0) t0 = atomicAdd(work, 1);
+      tile = __shfl_sync(0xffffffffu, t0, 0);
+    }
+    if (tile >= ntiles) break;
+    tile = order ? (int64_t)order[tile] : tile + tile_base;
+    const int2 tl = tiles[tile];
+    const float4 a = tbox[2 * tile], b = tbox[2 * tile + 1];
+    const float3 blo = make_float3(a.x, a.y, a.z), bhi = make_float3(b.x, b.y, b.z);
+    const float3 ctr = make_float3(0.5f * (blo.x + bhi.x), 0.5f * (blo.y + bhi.y), 0.5f * (blo.z + bhi.z));
+    float xr[4], yr[4], zr[4], wg[4], fo[4];
+    bool tv[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int q = lane + 32 * t;
+      tv[t] = q < tl.y;
+      const float4 p = src[tl.x + (tv[t] ? q : 0)];
+      xr[t] = p.x; yr[t] = p.y; zr[t] = p.z; wg[t] = p.w;
+    }
+    const int T = (tl.y + 31) >> 5;
+    switch (T) {
+      case 1: symb_tile<1>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringo[wib], out, fo); break;
+      case 2: symb_tile<2>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringo[wib], out, fo); break;
+      case 3: symb_tile<3>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringo[wib], out, fo); break;
+      default: symb_tile<4>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringo[wib], out, fo); break;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (t < T && lane + 32 * t < tl.y) atomicAdd(out + tl.x + lane + 32 * t, (OutT)fo[t]);
+  }
+}
+
 // ------------------------------------------------------------- fp64 tier ---
 // exp(x) for the fp64 tier's arguments x = -d2 / (2 sigma^2), table-driven:
 // n = rint(64 x log2 e) (the 1.5 2^52 rounding trick), x = (n/64) ln2 + r with
@@ -1154,6 +1645,7 @@ int sym_mode(int op, int64_t n_loc) {
     case RBF_OP_ONESIDED: return 0;
     case RBF_OP_SYM: return 1;
     case RBF_OP_SYM_WIDE: return 2;
+    case RBF_OP_SYM_ROT: return 3;
     default: return n_loc >= ((int64_t)1 << 18) ? 2 : 0;
   }
 }
@@ -1220,6 +1712,77 @@ KernelParams kernel_params(const rbf_kernel* k) {
   return p;
 }
 
+namespace {
+// Cost estimate of a wide tile for the symmetric kernels: target slots x the
+// sources in the cell-row ranges its traversal loads (from the tile start to the
+// window end), without loading them.  key = ~cost (ascending sort = most
+// expensive first).
+__global__ void tile_cost_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const int2* __restrict__ tiles,
+                                 const float4* __restrict__ tbox, int64_t t0, int64_t nt, int64_t sym_hi,
+                                 uint32_t* __restrict__ key, int32_t* __restrict__ id) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
+  const CellGrid& g = G.g;
+  for (int64_t w = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32; w < nt; w += nw) {
+    const int64_t tile = t0 + w;
+    const int2 tl = tiles[tile];
+    const float4 a = tbox[2 * tile], b = tbox[2 * tile + 1];
+    const float3 blo = make_float3(a.x, a.y, a.z), bhi = make_float3(b.x, b.y, b.z);
+    const int z0 = cellof(blo.z - G.cc, g.lo[2], g.inv_h, g.dim[2]);
+    const int z1 = cellof(bhi.z + G.cc, g.lo[2], g.inv_h, g.dim[2]);
+    const int y0 = cellof(blo.y - G.cc, g.lo[1], g.inv_h, g.dim[1]);
+    const int y1 = cellof(bhi.y + G.cc, g.lo[1], g.inv_h, g.dim[1]);
+    const int ny = y1 - y0 + 1, nrow = (z1 - z0 + 1) * ny;
+    unsigned long long cnt = 0;
+    for (int r = lane; r < nrow; r += 32) {
+      const int cz = z0 + r / ny, cy = y0 + r % ny;
+      const float czlo = g.lo[2] + (float)cz * g.h, cylo = g.lo[1] + (float)cy * g.h;
+      const float gz = fmaxf(0.f, fmaxf(czlo - bhi.z, blo.z - (czlo + g.h)));
+      const float gy = fmaxf(0.f, fmaxf(cylo - bhi.y, blo.y - (cylo + g.h)));
+      const float rem = G.cc2 - gy * gy - gz * gz;
+      if (rem < 0.f) continue;
+      const float rx = sqrtf(rem);
+      const int x0 = cellof(blo.x - rx, g.lo[0], g.inv_h, g.dim[0]);
+      const int x1 = cellof(bhi.x + rx, g.lo[0], g.inv_h, g.dim[0]);
+      const int64_t rowbase = ((int64_t)cz * g.dim[1] + cy) * g.dim[0];
+      const int sb = max(cell_start[rowbase + x0], tl.x);
+      const int se = min(cell_start[rowbase + x1 + 1], (int)sym_hi);
+      if (se > sb) cnt += (unsigned long long)(se - sb);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) {
+      const unsigned long long cost = cnt * (unsigned long long)((tl.y + 31) / 32);
+      key[w] = 0xffffffffu - (uint32_t)min(cost, 0xffffffffull);
+      id[w] = (int32_t)tile;
+    }
+  }
+}
+}  // namespace
+
+// The order in which the symmetric kernels take this rank's wide tiles: most
+// expensive first (longest-processing-time rule), so the last tiles a
+// persistent warp picks up are the cheap ones and the end of the launch is not
+// a tail of a few long tiles (~7 tiles per warp at c4).
+rbf_status order_wide_tiles(rbf_ctx* ctx, rbf_cells* c, const KernelParams& kp) {
+  cudaStream_t s = ctx->stream;
+  const SlabView& V = c->view;
+  const int64_t nt = V.tw1 - V.tw0;
+  RBF_TRY(c->order_w.alloc(sizeof(int32_t) * std::max<int64_t>(nt, 1), s));
+  if (nt == 0) return RBF_OK;
+  DevBuf k1, v1, k2;
+  RBF_TRY(k1.alloc(4 * nt, s));
+  RBF_TRY(v1.alloc(4 * nt, s));
+  RBF_TRY(k2.alloc(4 * nt, s));
+  SumGeom G = make_geom(c, kp);
+  tile_cost_kernel<<<grid_for(nt * 32, 256), 256, 0, s>>>(G, c->cell_start.as<int32_t>(), c->tiles_w.as<int2>(),
+                                                          c->tile_box_w.as<float4>(), V.tw0, nt, V.h1,
+                                                          k1.as<uint32_t>(), v1.as<int32_t>());
+  RBF_CHECK_LAUNCH();
+  return radix_sort_pairs<uint32_t>(ctx, k1.as<uint32_t>(), v1.as<int32_t>(), k2.as<uint32_t>(),
+                                    c->order_w.as<int32_t>(), nt, 32);
+}
+
 // Public fp32 path (and the pair accounting): w_sorted covers all n centres
 // (sorted order); this rank's tiles write f_out[out_perm ? perm[j] : j].
 rbf_status matvec_sorted_f32(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
@@ -1264,57 +1827,64 @@ static rbf_status matvec_f32_solver(rbf_ctx* ctx, const rbf_cells* c, const Kern
                                     double* f_loc, int op) {
   cudaStream_t s = ctx->stream;
   const SlabView& V = c->view;
-  const int64_t nw = V.h1 - V.h0;
+  int sym = sym_mode(op, c->n_loc());
+  if (sym >= 2 && !expansion_ok(kp, c->hd2_w)) sym = 0;
+  if (sym == 1 && !expansion_ok(kp, c->hd2)) sym = 0;
+  // one-sided: the window [h0, h1) around the slab; symmetric: [o0, h1) (sources
+  // before a tile are never read; their contributions come back by halo_reduce)
+  const int64_t base = sym ? V.o0 : V.h0;
+  const int64_t nw = V.h1 - base;
   const WT* w_win = w_loc;
-  if (ctx->world > 1 || c->emulated) {
+  if (ctx->world > 1) {
     RBF_TRY(ctx->win.ensure(sizeof(WT) * std::max<int64_t>(nw, 1), s));
-    RBF_TRY(halo_exchange<WT>(ctx, c, w_loc, ctx->win.as<WT>()));
+    RBF_TRY(halo_exchange<WT>(ctx, c, w_loc, ctx->win.as<WT>(), sym != 0));
     w_win = ctx->win.as<WT>();
   }
   RBF_TRY(ctx->src4.ensure(sizeof(float4) * std::max<int64_t>(nw, 1), s));
   RBF_TRY(ctx->counter.ensure(256, s));
   if (nw > 0) {
     if constexpr (std::is_same<WT, double>::value)
-      pack_src_f64w<<<grid_for(nw, 256), 256, 0, s>>>(c->sorted.as<float4>() + V.h0, w_win, nw,
+      pack_src_f64w<<<grid_for(nw, 256), 256, 0, s>>>(c->sorted.as<float4>() + base, w_win, nw,
                                                       ctx->src4.as<float4>());
     else
-      pack_src_f32<<<grid_for(nw, 256), 256, 0, s>>>(c->sorted.as<float4>() + V.h0, w_win, nw,
+      pack_src_f32<<<grid_for(nw, 256), 256, 0, s>>>(c->sorted.as<float4>() + base, w_win, nw,
                                                      ctx->src4.as<float4>());
     RBF_CHECK_LAUNCH();
   }
   RBF_CUDA_TRY(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
   SumGeom G = make_geom(c, kp);
   GridDesc gd{};
-  int sym = sym_mode(op, c->n_loc());
-  if (sym == 2 && !expansion_ok(kp, c->hd2_w)) sym = 0;
-  if (sym == 1 && !expansion_ok(kp, c->hd2)) sym = 0;
-  if (sym == 2) {
-    // symmetric evaluation on the wide plan (reading R19): the output is accumulated
-    RBF_CUDA_TRY(cudaMemsetAsync(f_loc, 0, sizeof(double) * (size_t)c->n_loc(), s));
-    ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
-    sum_f32_symw_kernel<double><<<sum_blocks(ctx, sum_f32_symw_kernel<double>), kSumWarps * 32, 0, s>>>(
-        G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>() - V.h0, c->tiles_w.as<int2>(),
-        c->tile_box_w.as<float4>(), V.tw1 - V.tw0, V.tw0, f_loc - V.o0, ctx->counter.as<int>(), V.o0, V.o1);
-    RBF_CHECK_LAUNCH();
-    return RBF_OK;
-  }
-  if (sym == 1) {
-    // symmetric evaluation on the 64-target plan (reading R19): the output is accumulated
-    RBF_CUDA_TRY(cudaMemsetAsync(f_loc, 0, sizeof(double) * (size_t)c->n_loc(), s));
-    ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
-    sum_f32_kernel<0, false, double, true>
-        <<<sum_blocks(ctx, sum_f32_kernel<0, false, double, true>), kSumWarps * 32, 0, s>>>(
-            G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>() - V.h0, c->tiles.as<int2>(),
-            c->tile_box.as<float4>(), V.t1 - V.t0, V.t0, gd, f_loc - V.o0, nullptr, ctx->counter.as<int>(), nullptr,
-            V.o0, V.o1);
-    RBF_CHECK_LAUNCH();
-    return RBF_OK;
+  const float4* srcb = ctx->src4.as<float4>() - base;
+  if (sym) {
+    // symmetric evaluation (reading R19): accumulated into the window [o0, h1)
+    double* fwin = f_loc;
+    if (ctx->world > 1) {
+      RBF_TRY(ctx->fwin.ensure(sizeof(double) * std::max<int64_t>(nw, 1), s));
+      fwin = ctx->fwin.as<double>();
+    }
+    RBF_CUDA_TRY(cudaMemsetAsync(fwin, 0, sizeof(double) * (size_t)std::max<int64_t>(nw, 0), s));
+    {
+      ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
+      if (sym >= 2) {
+        auto kfn = sym == 3 ? sum_f32_symr_kernel<double> : sum_f32_symb_kernel<double>;
+        kfn<<<sum_blocks(ctx, kfn), kSumWarps * 32, 0, s>>>(
+            G, c->cell_start.as<int32_t>(), srcb, c->tiles_w.as<int2>(), c->tile_box_w.as<float4>(), V.tw1 - V.tw0,
+            V.tw0, fwin - base, ctx->counter.as<int>(), V.h1, c->order_w.p ? c->order_w.as<int32_t>() : nullptr);
+      } else {
+        sum_f32_kernel<0, false, double, true>
+            <<<sum_blocks(ctx, sum_f32_kernel<0, false, double, true>), kSumWarps * 32, 0, s>>>(
+                G, c->cell_start.as<int32_t>(), srcb, c->tiles.as<int2>(), c->tile_box.as<float4>(), V.t1 - V.t0,
+                V.t0, gd, fwin - base, nullptr, ctx->counter.as<int>(), nullptr, 0, V.h1);
+      }
+      RBF_CHECK_LAUNCH();
+    }
+    return halo_reduce(ctx, c, fwin, f_loc);
   }
   ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
   auto kfn = expansion_ok(kp, c->hd2) ? sum_f32_kernel<0, false, double> : sum_f32_kernel<0, false, double, false, true>;
   kfn<<<sum_blocks(ctx, kfn), kSumWarps * 32, 0, s>>>(
-      G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>() - V.h0, c->tiles.as<int2>(), c->tile_box.as<float4>(),
-      V.t1 - V.t0, V.t0, gd, f_loc - V.o0, nullptr, ctx->counter.as<int>(), nullptr, 0, 0, nullptr);
+      G, c->cell_start.as<int32_t>(), srcb, c->tiles.as<int2>(), c->tile_box.as<float4>(), V.t1 - V.t0, V.t0, gd,
+      f_loc - V.o0, nullptr, ctx->counter.as<int>(), nullptr, 0, 0, nullptr);
   RBF_CHECK_LAUNCH();
   return RBF_OK;
 }
@@ -1334,29 +1904,38 @@ rbf_status matvec_sorted_f64(rbf_ctx* ctx, const rbf_cells* c, const KernelParam
                              const double* w_loc, double* f_out, const int32_t* out_perm, int op) {
   cudaStream_t s = ctx->stream;
   const SlabView& V = c->view;
-  const int64_t nw = V.h1 - V.h0;
+  const bool sym = !out_perm && sym_mode(op, c->n_loc()) != 0;
+  const int64_t base = sym ? V.o0 : V.h0;
+  const int64_t nw = V.h1 - base;
   const double* w_win = w_loc;
-  if (ctx->world > 1 || c->emulated) {
+  if (ctx->world > 1) {
     RBF_TRY(ctx->win.ensure(sizeof(double) * std::max<int64_t>(nw, 1), s));
-    RBF_TRY(halo_exchange<double>(ctx, c, w_loc, ctx->win.as<double>()));
+    RBF_TRY(halo_exchange<double>(ctx, c, w_loc, ctx->win.as<double>(), sym));
     w_win = ctx->win.as<double>();
   }
   RBF_TRY(ctx->counter.ensure(256, s));
   RBF_CUDA_TRY(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
   SumGeom G = make_geom(c, kp);
-  if (!out_perm && sym_mode(op, c->n_loc()) != 0) {
-    // solver path: symmetric fp64 tier (reading R19), accumulated output
-    RBF_CUDA_TRY(cudaMemsetAsync(f_out, 0, sizeof(double) * (size_t)c->n_loc(), s));
-    ProfScope ps(ctx, RBF_PROF_MATVEC_F64);
-    sum_f64_sym_kernel<<<sum_blocks(ctx, sum_f64_sym_kernel), kSumWarps * 32, 0, s>>>(
-        G, c->cell_start.as<int32_t>(), c->sorted.as<float4>(), w_win - V.h0, c->tiles.as<int2>(),
-        c->tile_box.as<float4>(), V.t1 - V.t0, V.t0, f_out - V.o0, ctx->counter.as<int>(), V.o0, V.o1);
-    RBF_CHECK_LAUNCH();
-    return RBF_OK;
+  if (sym) {
+    // solver path: symmetric fp64 tier (reading R19), accumulated into [o0, h1)
+    double* fwin = f_out;
+    if (ctx->world > 1) {
+      RBF_TRY(ctx->fwin.ensure(sizeof(double) * std::max<int64_t>(nw, 1), s));
+      fwin = ctx->fwin.as<double>();
+    }
+    RBF_CUDA_TRY(cudaMemsetAsync(fwin, 0, sizeof(double) * (size_t)std::max<int64_t>(nw, 0), s));
+    {
+      ProfScope ps(ctx, RBF_PROF_MATVEC_F64);
+      sum_f64_sym_kernel<<<sum_blocks(ctx, sum_f64_sym_kernel), kSumWarps * 32, 0, s>>>(
+          G, c->cell_start.as<int32_t>(), c->sorted.as<float4>(), w_win - base, c->tiles.as<int2>(),
+          c->tile_box.as<float4>(), V.t1 - V.t0, V.t0, fwin - base, ctx->counter.as<int>(), 0, V.h1);
+      RBF_CHECK_LAUNCH();
+    }
+    return halo_reduce(ctx, c, fwin, f_out);
   }
   ProfScope ps(ctx, RBF_PROF_MATVEC_F64);
   sum_f64_kernel<<<sum_blocks(ctx, sum_f64_kernel), kSumWarps * 32, 0, s>>>(
-      G, c->cell_start.as<int32_t>(), c->sorted.as<float4>(), w_win - V.h0, c->tiles.as<int2>(),
+      G, c->cell_start.as<int32_t>(), c->sorted.as<float4>(), w_win - base, c->tiles.as<int2>(),
       c->tile_box.as<float4>(), V.t1 - V.t0, V.t0, out_perm ? f_out : f_out - V.o0, out_perm,
       ctx->counter.as<int>());
   RBF_CHECK_LAUNCH();
@@ -1386,22 +1965,10 @@ rbf_status eval_grid_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams
     gd.nb[a] = (g->n[a] + 3) / 4;
   }
   const int64_t per_layer = (int64_t)gd.nb[0] * gd.nb[1];
-  int64_t b0 = 0, b1 = per_layer * gd.nb[2];
-  if (ctx->world > 1 || c->emulated) {
-    // node-block layers go to the rank owning the cell plane of their first node
-    int bz0 = gd.nb[2], bz1 = gd.nb[2];
-    for (int bz = 0; bz < gd.nb[2]; ++bz) {
-      const float z = node_coord_host(gd, 2, 4 * bz);
-      int pz = (int)std::floor((double)((z - c->lo[2]) * c->inv_h));
-      pz = std::min(std::max(pz, 0), c->dim[2] - 1);
-      const bool mine = pz >= c->view.p0 && pz < c->view.p1;
-      if (mine && bz0 == gd.nb[2]) bz0 = bz;
-      if (mine) bz1 = bz + 1;
-    }
-    if (bz0 == gd.nb[2]) bz1 = bz0;
-    b0 = per_layer * bz0;
-    b1 = per_layer * bz1;
-  }
+  // this rank's node-block layers (all of them on one GPU; dist.cu grid_layers)
+  int64_t k0n, k1n;
+  grid_layers(c, g, ctx->rank, &k0n, &k1n);
+  const int64_t b0 = per_layer * (k0n / 4), b1 = per_layer * ((k1n + 3) / 4);
   // node blocks within reach of a centre (the rest of this rank's layers are
   // exact zeros): flags -> scan -> list (one host read of the count)
   ProfScope ps(pair_stats ? nullptr : ctx, RBF_PROF_GRID);

@@ -1,0 +1,72 @@
+// Transport of the multi-rank slab partition.
+//
+// The data plane of a slab-partitioned solve needs three collectives: grouped
+// point-to-point copies of contiguous ranges (halo exchange, its reverse
+// reduction, gathers), and a sum all-reduce (Krylov inner products).  Two
+// implementations:
+//   * NcclTransport: one process per GPU, ncclSend/ncclRecv in a group and
+//     ncclAllReduce over NVLink/NVSwitch (dist.cu);
+//   * LoopTransport: W contexts of ONE process on one device, one host thread
+//     per rank (rbf_loopback_group_create / rbf_create_loopback): ranges are
+//     copied with cudaMemcpyAsync between the ranks' buffers and the sum is a
+//     kernel over all ranks' buffers in rank order, ordered by CUDA events and a
+//     host barrier.  It runs the exact multi-rank code path of the library on
+//     a single GPU (tests; NCCL cannot place two ranks on one device).
+// Every rank must issue the same sequence of collective calls; a call's send
+// list to rank q must match q's receive list from this rank (same order, same
+// counts).  All transfers are stream-ordered on the given stream.
+#pragma once
+#include <condition_variable>
+#include <mutex>
+#include <vector>
+
+#include "internal.h"
+
+namespace rbf {
+
+enum class DType { F32 = 4, F64 = 8 };
+
+struct Xfer {
+  int peer;
+  void* ptr;        // send: source (read), recv: destination (written)
+  int64_t count;    // elements
+};
+
+struct Transport {
+  virtual ~Transport() = default;
+  virtual rbf_status exchange(rbf_ctx* ctx, cudaStream_t s, const std::vector<Xfer>& sends,
+                              const std::vector<Xfer>& recvs, DType t) = 0;
+  virtual rbf_status allreduce_sum(rbf_ctx* ctx, cudaStream_t s, void* buf, int64_t count, DType t) = 0;
+};
+
+// Shared state of a loopback group (library-owned; rbf_loopback_group_*).
+struct LoopGroup {
+  int world = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t generation = 0;
+  struct Slot {
+    std::vector<Xfer> sends;
+    const void* buf = nullptr;
+    cudaEvent_t ready = nullptr, done = nullptr;
+  };
+  std::vector<Slot> slots;
+  std::vector<int> joined;   // ranks with a live context
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t gen = generation;
+    if (++arrived == world) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != gen; });
+    }
+  }
+};
+
+Transport* make_nccl_transport(void* comm);
+Transport* make_loop_transport(LoopGroup* g, int rank);
+
+}  // namespace rbf

@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(_HERE, "librbf.so")
 
 RBF_OK, RBF_EINVAL, RBF_ENOMEM, RBF_ECUDA, RBF_ENCCL, RBF_EUNSUPPORTED = range(6)
 RBF_F32, RBF_F64 = 0, 1
-OP_AUTO, OP_ONESIDED, OP_SYM, OP_SYM_WIDE = range(4)   # rbf_op_variant
+OP_AUTO, OP_ONESIDED, OP_SYM, OP_SYM_WIDE, OP_SYM_ROT = range(5)   # rbf_op_variant
 
 
 class RbfError(RuntimeError):
@@ -89,6 +89,9 @@ EXPORTS = {
     "rbf_abi_version": (C.c_int, []),
     "rbf_launch_count": (C.c_int64, []),
     "rbf_nccl_unique_id": (C.c_int, [_P]),
+    "rbf_loopback_group_create": (C.c_int, [C.c_int, C.POINTER(_P)]),
+    "rbf_loopback_group_free": (None, [_P]),
+    "rbf_create_loopback": (C.c_int, [C.POINTER(_P), C.c_int, _P, _P, C.c_int]),
     "rbf_slab_plan": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, _P, _P, _P, _P, _P]),
     "rbf_extend_points": (C.c_int, [_P, _P, _P, C.c_int64, C.c_double, C.c_double, _P, _P]),
     "rbf_build_cells": (C.c_int, [_P, _P, C.c_int64, C.POINTER(_Kernel), C.POINTER(_CellCfg),
@@ -109,6 +112,8 @@ EXPORTS = {
     "rbf_gmres_solve": (C.c_int, [_P, _P, C.POINTER(_Kernel), _P, C.POINTER(_PrecondCfg),
                                   C.POINTER(_GmresCfg), _P, _P, C.POINTER(SolveReport)]),
     "rbf_eval_grid": (C.c_int, [_P, _P, C.POINTER(_Kernel), _P, C.POINTER(_Grid), _P]),
+    "rbf_eval_grid_slab": (C.c_int, [_P, _P, C.POINTER(_Kernel), _P, C.POINTER(_Grid), _P, C.POINTER(C.c_int64),
+                                     C.POINTER(C.c_int64)]),
     "rbf_eval_grid_pairs": (C.c_int, [_P, _P, C.POINTER(_Kernel), C.POINTER(_Grid), C.POINTER(C.c_int64),
                                       C.POINTER(C.c_int64)]),
     "rbf_zero_set": (C.c_int, [_P, _P, C.POINTER(_Grid), _P, C.c_int64, C.c_double, _P, C.c_int64,
@@ -224,18 +229,48 @@ def slab_plan(plane_start, plane_weight, reach: int, world: int):
     return out
 
 
+class LoopbackGroup:
+    """rbf_loopback_group_create: `world` ranks of ONE process on one device (one
+    host thread per rank; Context(loopback=(group, rank)))."""
+
+    def __init__(self, world: int):
+        h = C.c_void_p()
+        _check(load_library().rbf_loopback_group_create(int(world), C.byref(h)))
+        self._h, self.world = h, int(world)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.rbf_loopback_group_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Context:
     """rbf_create on `device`, issuing work on torch's current stream of that device.
 
     distributed=True (and an initialised torch.distributed group with world > 1):
     one context per rank/GPU sharing an NCCL communicator; rank 0's NCCL id is
-    broadcast with torch.distributed (plumbing only).  Calls then take and
-    return replicated (full) arrays while the library shards the work."""
+    broadcast with torch.distributed (plumbing only).  loopback=(group, rank):
+    rank `rank` of an in-process LoopbackGroup (rbf_create_loopback).  Calls then
+    take and return replicated (full) arrays while the library shards the work."""
 
-    def __init__(self, device: int = 0, stream: torch.cuda.Stream | None = None, distributed: bool = False):
+    def __init__(self, device: int = 0, stream: torch.cuda.Stream | None = None, distributed: bool = False,
+                 loopback: tuple | None = None):
         lib = load_library()
         self.device = device
         self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        if loopback is not None:
+            group, rank = loopback
+            h = C.c_void_p()
+            _check(lib.rbf_create_loopback(C.byref(h), device, C.c_void_p(self.stream.cuda_stream), group._h,
+                                           int(rank)))
+            self._h, self.rank, self.world, self._group = h, int(rank), group.world, group
+            return
         rank, world, uid = 0, 1, None
         if distributed:
             import torch.distributed as dist
@@ -391,6 +426,17 @@ def eval_grid(ctx: Context, cells: Cells, kernel: Kernel, w: torch.Tensor, lo, h
     _need(field, torch.float32, n3[0] * n3[1] * n3[2], "field")
     _check(_lib.rbf_eval_grid(ctx._h, cells._h, C.byref(kernel._c()), _ptr(w), C.byref(g), _ptr(field)))
     return field
+
+
+def eval_grid_slab(ctx: Context, cells: Cells, kernel: Kernel, w: torch.Tensor, lo, hi, n, out: torch.Tensor):
+    """rbf_eval_grid_slab: only this rank's z layers of `out` are written; returns (k0, k1)."""
+    _need(w, torch.float64, cells.n, "w")
+    g, n3 = _grid_c(lo, hi, n)
+    _need(out, torch.float32, n3[0] * n3[1] * n3[2], "field")
+    k0, k1 = C.c_int64(), C.c_int64()
+    _check(_lib.rbf_eval_grid_slab(ctx._h, cells._h, C.byref(kernel._c()), _ptr(w), C.byref(g), _ptr(out),
+                                   C.byref(k0), C.byref(k1)))
+    return k0.value, k1.value
 
 
 def eval_grid_pairs(ctx: Context, cells: Cells, kernel: Kernel, lo, hi, n, visited: bool = False):

@@ -43,7 +43,12 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--f64", action="store_true")
     ap.add_argument("--precond", action="store_true", help="time the config's preconditioner setup + apply")
+    ap.add_argument("--lib", default=None, help="alternative librbf .so (tools/build_variant.sh)")
+    ap.add_argument("--ops", default="AUTO,SYM_WIDE,SYM_ROT,SYM")
+    ap.add_argument("--no-grid", action="store_true")
     args = ap.parse_args()
+    if args.lib:
+        R.load_library(args.lib)
     t0 = time.time()
     d = make_inputs(args.config, n=args.n)
     tgen = time.time() - t0
@@ -64,6 +69,26 @@ def main():
                useful=useful, visited=visited, useful_frac=useful / visited,
                matvec_f32_ms=t32, useful_pairs_per_s=useful / (t32 * 1e-3),
                visited_pairs_per_s=visited / (t32 * 1e-3))
+    # the solver's operator (OP_AUTO: the symmetric wide-plan kernel at >= 2^18
+    # centres), kernel-only time from the library's CUDA-event profiler, and
+    # its agreement with the one-sided fp64 product
+    wd64 = w.double()
+    ref = R.matvec(ctx, cells, kern, wd64)
+    g = R.matvec(ctx, cells, kern, wd64.abs())
+    for name in args.ops.split(","):
+        op = getattr(R, "OP_" + name)
+        for _ in range(2):
+            fo = R.matvec_op(ctx, cells, kern, w, op=op)
+        ctx.profile(True)
+        ctx.profile_query()
+        for _ in range(args.iters):
+            fo = R.matvec_op(ctx, cells, kern, w, op=op)
+        pr = ctx.profile_query()
+        ctx.profile(False)
+        tm, nl = pr["matvec_f32"]
+        err = ((fo.double() - ref).abs() / g.clamp_min(1e-300)).max().item()
+        out[f"op_{name}"] = dict(kernel_ms=tm / max(nl, 1), frac_mufu=useful / (tm / max(nl, 1) * 1e-3) / 4.65312e12,
+                                 max_err_over_g=err)
     if args.f64:
         w64 = w.double()
         f64 = torch.empty_like(w64)
@@ -78,6 +103,9 @@ def main():
         z = P.apply(w)
         ta = timed(lambda: P.apply(w, out=z), args.iters)
         out.update(precond_setup_ms=tp, precond_apply_ms=ta)
+    if args.no_grid:
+        print(json.dumps(out))
+        return
     lo, hi, gn = d["grid_lo"], d["grid_hi"], d["grid_n"]
     wd = w.double()
     field = R.eval_grid(ctx, cells, kern, wd, lo, hi, gn)
