@@ -310,9 +310,10 @@ rbf_status rbf_precond_create(rbf_ctx* ctx, const rbf_cells* cells, const rbf_ke
                               const rbf_precond_cfg* cfg, rbf_precond** out);
 void rbf_precond_free(rbf_precond* p);
 /* z = M r, M = sum_i R~_i^T A_i^-1 R_i (restricted: only core rows written).
- * r, z: DEVICE fp32, n entries, caller order.  Single GPU only (a slab-
- * partitioned solve applies the preconditioner inside rbf_gmres_solve, with the
- * extended sets reaching into the neighbouring slabs through the halo). */
+ * r, z: DEVICE fp32, n entries, caller order.  world > 1: r replicated, each
+ * rank applies the blocks of its slab (their extended sets reach into the
+ * neighbouring slabs through the halo: the paper's distributed RASM) and z is
+ * gathered on every rank. */
 rbf_status rbf_precond_apply(rbf_ctx* ctx, const rbf_precond* p, const float* r, float* z);
 /* Block structure (host outputs, synchronises): nblocks, and if the arrays are
  * non-NULL: core_ptr[nblocks+1], ext_ptr[nblocks+1] (host, caller-allocated)

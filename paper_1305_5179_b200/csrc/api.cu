@@ -25,6 +25,18 @@ std::atomic<unsigned long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 const char* last_error_cstr() { return g_last_error.c_str(); }
 
+rbf_status smem_limit_at_least(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<const void*, size_t> cur;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& c = cur[func];
+  if (bytes <= c && c > 0) return RBF_OK;
+  const size_t want = std::max<size_t>(bytes, 48 * 1024);
+  RBF_CUDA_TRY(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want));
+  c = want;
+  return RBF_OK;
+}
+
 cudaMemPool_t lib_pool(int device) {
   static std::mutex mu;
   static std::map<int, cudaMemPool_t> pools;

@@ -161,14 +161,12 @@ struct LoopTransport final : Transport {
   LoopGroup* g;
   int rank;
   DevBuf scratch;
+  // the slot's events belong to the group (a peer may still be waiting on them
+  // after this rank has returned from its last collective and been destroyed)
   LoopTransport(LoopGroup* grp, int r) : g(grp), rank(r) {
-    cudaEventCreateWithFlags(&g->slots[r].ready, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&g->slots[r].done, cudaEventDisableTiming);
-  }
-  ~LoopTransport() override {
-    cudaEventDestroy(g->slots[rank].ready);
-    cudaEventDestroy(g->slots[rank].done);
-    g->slots[rank].ready = g->slots[rank].done = nullptr;
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (!g->slots[r].ready) cudaEventCreateWithFlags(&g->slots[r].ready, cudaEventDisableTiming);
+    if (!g->slots[r].done) cudaEventCreateWithFlags(&g->slots[r].done, cudaEventDisableTiming);
   }
   // phase 1: my buffers are complete on my stream when `ready` fires; phase 2:
   // the peers read them; phase 3: my later writes wait for their reads (`done`)
@@ -501,7 +499,15 @@ rbf_status rbf_loopback_group_create(int world, rbf_loopback_group** out) {
   return RBF_OK;
 }
 
-void rbf_loopback_group_free(rbf_loopback_group* g) { delete reinterpret_cast<LoopGroup*>(g); }
+void rbf_loopback_group_free(rbf_loopback_group* grp) {
+  LoopGroup* g = reinterpret_cast<LoopGroup*>(grp);
+  if (!g) return;
+  for (auto& sl : g->slots) {
+    if (sl.ready) cudaEventDestroy(sl.ready);
+    if (sl.done) cudaEventDestroy(sl.done);
+  }
+  delete g;
+}
 
 rbf_status rbf_slab_plan(const int64_t* plane_start, const double* plane_weight, int dimz, int reach, int world,
                          int32_t* plane_lo, int64_t* own_lo, int64_t* own_hi, int64_t* win_lo, int64_t* win_hi) {

@@ -274,6 +274,15 @@ rbf_status scatter_f64_from_sorted_f32(rbf_ctx* ctx, const double* src, const in
 rbf_status scatter_f32_from_sorted(rbf_ctx* ctx, const float* src, const int32_t* perm, float* dst, int64_t n);
 rbf_status scatter_f64_from_sorted(rbf_ctx* ctx, const double* src, const int32_t* perm, double* dst, int64_t n);
 
+// Raise a kernel's dynamic shared-memory limit to at least `bytes` (monotone and
+// thread-safe: contexts on several host threads launch the same kernels with
+// different needs, and the attribute is per function, not per launch).
+rbf_status smem_limit_at_least(const void* func, size_t bytes);
+template <class F>
+rbf_status smem_limit_at_least(F* func, size_t bytes) {
+  return smem_limit_at_least(reinterpret_cast<const void*>(func), bytes);
+}
+
 inline int grid_for(int64_t n, int threads, int max_blocks = 148 * 16) {
   int64_t b = (n + threads - 1) / threads;
   if (b < 1) b = 1;

@@ -523,18 +523,12 @@ rbf_status batched_lu_restricted_inverse(rbf_ctx* ctx, const LuJob* jobs_dev, co
   cudaStream_t s = ctx->stream;
   const int nj = (int)jobs.size();
   if (nj == 0) return RBF_OK;
-  static bool attr = false;
-  if (!attr) {
-    RBF_CUDA_TRY(cudaFuncSetAttribute(linv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2_bytes()));
-    RBF_CUDA_TRY(cudaFuncSetAttribute(swap_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smsw_bytes()));
-    RBF_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2_bytes()));
-    RBF_CUDA_TRY(cudaFuncSetAttribute(diag_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)sm2_bytes()));
-    RBF_CUDA_TRY(cudaFuncSetAttribute(uinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2_bytes()));
-    RBF_CUDA_TRY(cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr = true;
-  }
+  RBF_TRY(smem_limit_at_least(linv_kernel, sm2_bytes()));
+  RBF_TRY(smem_limit_at_least(swap_trsm_kernel, smsw_bytes()));
+  RBF_TRY(smem_limit_at_least(gemm_kernel, sm2_bytes()));
+  RBF_TRY(smem_limit_at_least(diag_solve_kernel, sm2_bytes()));
+  RBF_TRY(smem_limit_at_least(uinv_kernel, sm2_bytes()));
+  RBF_CUDA_TRY(cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   DevBuf piv, linv;
   RBF_TRY(piv.alloc(sizeof(int) * (size_t)nj * kNb, s));
   RBF_TRY(linv.alloc(sizeof(double) * (size_t)nj * kNb * kNb, s));
@@ -567,8 +561,6 @@ rbf_status batched_lu_restricted_inverse(rbf_ctx* ctx, const LuJob* jobs_dev, co
     while (G.CL < 16 && (G.maxm + G.CL - 1) / G.CL > 256) G.CL *= 2;
     G.R = (G.maxm + G.CL - 1) / G.CL;
     const size_t smp = sizeof(double) * (size_t)G.R * kPs;
-    RBF_CUDA_TRY(cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)std::max<size_t>(smp, 48 * 1024)));
     G.pcfg = {};
     G.pcfg.gridDim = dim3((unsigned)(G.nj * G.CL));
     G.pcfg.blockDim = dim3(kThreads);
@@ -586,8 +578,7 @@ rbf_status batched_lu_restricted_inverse(rbf_ctx* ctx, const LuJob* jobs_dev, co
   {
     size_t need = 0;
     for (int gi = 0; gi < ngroups; ++gi) need = std::max(need, sizeof(double) * (size_t)Gs[gi].R * kPs);
-    RBF_CUDA_TRY(cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)std::max<size_t>(need, 48 * 1024)));
+    RBF_TRY(smem_limit_at_least(panel_cluster_kernel, need));
   }
   cudaEvent_t fork = nullptr, join = nullptr;
   if (ngroups == 2) {

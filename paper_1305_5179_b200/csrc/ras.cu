@@ -1201,9 +1201,7 @@ rbf_status precond_apply_sorted(rbf_ctx* ctx, const rbf_precond* P, const VT* r,
     // gather -> copy -> multiply latency chain of each block
     const int cap = (int)std::min<int64_t>(P->max_wblk, P->cap_w) & ~3;
     const size_t smems = sizeof(float) * ((size_t)((P->max_m + 3) & ~3) + (size_t)cap);
-    if (smems > 48 * 1024)
-      RBF_CUDA_TRY(cudaFuncSetAttribute(apply_sym_kernel<VT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smems));
+    RBF_TRY(smem_limit_at_least(apply_sym_kernel<VT>, smems));
     const int64_t grid = P->nblocks;
     ProfScope ps(ctx, RBF_PROF_PRECOND_APPLY);
     apply_sym_kernel<VT><<<(unsigned)grid, kApplyThreads, smems, s>>>(P->ext_ptr.as<int64_t>(), P->ext_idx.as<int32_t>(),
@@ -1214,9 +1212,7 @@ rbf_status precond_apply_sorted(rbf_ctx* ctx, const rbf_precond* P, const VT* r,
   }
   if (P->w_fp32) {
     const size_t smemf = sizeof(float) * (size_t)P->max_m;
-    if (smemf > 48 * 1024)
-      RBF_CUDA_TRY(cudaFuncSetAttribute(apply_f32w_kernel<VT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smemf));
+    RBF_TRY(smem_limit_at_least(apply_f32w_kernel<VT>, smemf));
     // one CTA (4 warps) per block: many small CTAs resident per SM hide the
     // gather -> barrier -> row-latency chain of each block
     const int ablocks = (int)std::min<int64_t>(P->nblocks, (int64_t)1 << 30);
@@ -1228,7 +1224,7 @@ rbf_status precond_apply_sorted(rbf_ctx* ctx, const rbf_precond* P, const VT* r,
     return RBF_OK;
   }
   if (smem > 48 * 1024) {
-    RBF_CUDA_TRY(cudaFuncSetAttribute(apply_kernel<VT, WT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RBF_TRY(smem_limit_at_least(apply_kernel<VT, WT>, smem));
   }
   ProfScope ps(ctx, RBF_PROF_PRECOND_APPLY);
   apply_kernel<VT, WT><<<blocks, 256, smem, s>>>(P->ext_ptr.as<int64_t>(), P->core_ptr.as<int64_t>(),
@@ -1275,7 +1271,17 @@ rbf_status rbf_precond_apply(rbf_ctx* ctx, const rbf_precond* P, const float* r,
   RBF_CUDA_TRY(cudaSetDevice(ctx->device));
   const rbf_cells* c = P->cells;
   const int64_t n = P->n;
-  if (ctx->world > 1) { set_error("rbf_precond_apply is single-GPU only"); return RBF_EUNSUPPORTED; }
+  if (ctx->world > 1) {
+    // slab partition: replicated r in, this rank's blocks (ext sets through the
+    // halo), every rank's core rows gathered out
+    const int64_t N = c->n, o0 = c->view.o0;
+    RBF_TRY(ctx->vec_a.ensure(sizeof(double) * N, ctx->stream));
+    RBF_TRY(ctx->vec_b.ensure(sizeof(double) * N, ctx->stream));
+    RBF_TRY(gather_f32_to_sorted_f64(ctx, r, c->perm.as<int32_t>(), ctx->vec_a.as<double>(), N));
+    RBF_TRY(precond_apply_sorted<double>(ctx, P, ctx->vec_a.as<double>() + o0, ctx->vec_b.as<double>() + o0));
+    RBF_TRY(allgather_sorted(ctx, c, ctx->vec_b.as<double>()));
+    return scatter_f64_from_sorted_f32(ctx, ctx->vec_b.as<double>(), c->perm.as<int32_t>(), z, N);
+  }
   RBF_TRY(ctx->vec_a.ensure(sizeof(float) * n, ctx->stream));
   RBF_TRY(ctx->vec_b.ensure(sizeof(float) * n, ctx->stream));
   RBF_TRY(gather_f32_to_sorted(ctx, r, c->perm.as<int32_t>(), ctx->vec_a.as<float>(), n));
