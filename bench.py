@@ -171,6 +171,27 @@ def measured_traffic(cfg_name: str):
         return None
 
 
+def measured_ex2(cfg_name: str):
+    """MUFU.EX2 thread-instructions per launch of the symmetric fp32 kernel from the
+    committed ncu capture (profiles/r02), or None."""
+    path = os.path.join(ROOT, "profiles", "r02", f"ex2_sum_f32_{cfg_name}.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)["mufu_ex2_thread_inst_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+def gate_note(cfg_name: str):
+    """What the north star's 1e-6 residual gate means for this config (F1)."""
+    path = os.path.join(ROOT, "profiles", "r02", f"gate_1e-6_{cfg_name}.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return None
+
+
 def make_problem(cfg_name: str, seed: int):
     from synth import make_inputs
     t = time.time()
@@ -219,7 +240,7 @@ def run_ours(args, rank, world, local):
     centres, b = R.extend_points(ctx, x, nrm, d["delta"])
     cells = R.Cells(ctx, centres, kern, cell_edge=cell_edge)
     useful_mv, visited_mv = R.matvec_pairs(ctx, cells, kern)
-    useful_grid = R.eval_grid_pairs(ctx, cells, kern, lo, hi, gn)
+    useful_grid, visited_grid = R.eval_grid_pairs(ctx, cells, kern, lo, hi, gn, visited=True)
     info = cells.info()
     del cells
 
@@ -330,6 +351,14 @@ def run_ours(args, rank, world, local):
                                            if clk.get("sm_mhz") else None),
                 "avg_launch_ms": avg_mv_ms, "launches": n_mv, "useful_pairs_per_launch": useful_mv,
                 "visited_pairs_per_launch": visited_mv, "traffic": measured_traffic(args.config)}
+    # the same kernel against the MUFU.EX2 pipe it actually drives: the symmetric
+    # kernel issues ex2_per_useful exponentials per useful ordered pair (ncu count,
+    # profiles/r02; tools/plan_sim.py models it from the tile plan)
+    ex2 = measured_ex2(args.config)
+    if ex2 and sym == 2:
+        roofline["ex2_per_launch"] = ex2
+        roofline["ex2_per_useful_pair"] = ex2 / useful_mv
+        roofline["mufu_busy_frac"] = ex2 / (avg_mv_ms * 1e-3) / (peak_max * 1e12)
     stage_ms = {k: round(v[0] / args.steps, 3) for k, v in prof.items()}
 
     cpu = None
@@ -353,11 +382,15 @@ def run_ours(args, rank, world, local):
                    "l2": "working set >> 126 MB L2 (block inverses 0.5 GB, Krylov basis 1.2 GB, cells + vectors 0.2 GB); no explicit flush"},
         "e2e": e2e, "gpu_launches": None, "clocks": clk, "roofline": roofline, "cpu_baseline": cpu,
         "detail": {"useful_pairs_per_matvec": useful_mv, "visited_pairs_per_matvec": visited_mv,
-                   "useful_pairs_grid": useful_grid, "matvecs_f32_per_step": mv32 / args.steps,
+                   "useful_pairs_grid": useful_grid, "visited_pairs_grid": visited_grid,
+                   "grid_useful_pairs_per_s": useful_grid / (prof["grid"][0] / max(prof["grid"][1], 1) * 1e-3)
+                   if prof["grid"][1] else None,
+                   "matvecs_f32_per_step": mv32 / args.steps,
                    "matvecs_f64_per_step": mv64 / args.steps, "stage_ms_per_step": stage_ms,
                    "iters_phase1": last["iters_phase1"], "iters_phase2": last["iters_phase2"],
                    "rel_residual_true": last["rel_residual_true"], "converged": last["converged"],
                    "ras_blocks": last["nblocks"], "precond_bytes": last["precond_bytes"], "zero_set": zs,
+                   "gate_1e-6": gate_note(args.config),
                    "density": dens,
                    "cells": info,
                    "gen_s": round(d["gen_s"], 1)},
@@ -370,25 +403,91 @@ def run_ours(args, rank, world, local):
 
 
 # ------------------------------------------------------------- cpu oracle ---
-def cpu_baseline(d, args, rows: int | None = None):
-    """The oracle (oracle/kernel.py brute-force fp64 matvec, as it stands) on a bounded
-    row sample of the same workload, on all host cores."""
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(d, args, rows: int | None = None, extras: bool = True):
+    """The oracle (oracle/, as it stands, never tuned for this) on the host cores:
+    the headline is a bounded row sample of the same workload's brute-force fp64
+    matvec (useful pairs/s); `steps` adds the two steps the paper times (Table II
+    solve, Table III grid evaluation) on the small configs: c1 dense LU, c1 fp64
+    GMRES + RAS, c1 full brute-force grid, c2 sampled grid."""
     from oracle import extend as OE
     from oracle import kernel as OK
     X = OE.extend(d["x"], d["normals"], d["delta"])
     n = X.shape[0]
-    rows = rows or args.cpu_sample_rows or 200
+    rows = rows or args.cpu_sample_rows or 400
     sel = np.sort(np.random.default_rng(1).choice(n, rows, replace=False))
     w = np.random.default_rng(2).normal(size=n)
     procs = os.cpu_count() or 1
     t = time.perf_counter()
     OK.matvec_parallel(X, w, d["sigma"], rows=sel, procs=procs)
     dt = time.perf_counter() - t
-    useful = OK.pair_count(X, d["sigma"], rows=sel[: min(rows, 50)]) * rows / min(rows, 50)
-    return {"value": useful / dt, "unit": "pairs/s", "cores": procs, "kind": "oracle",
-            "dense_pairs_per_s": rows * n / dt,
-            "sample": f"brute-force fp64 matvec rows ({rows} of {n} sampled targets x all {n} centres) of the "
-                      f"same config; useful pairs estimated from 50 rows", "seconds": dt}
+    useful = OK.pair_count(X, d["sigma"], rows=sel)
+    out = {"value": useful / dt, "unit": "pairs/s", "cores": procs, "cpu_model": cpu_model(), "kind": "oracle",
+           "dense_pairs_per_s": rows * n / dt,
+           "sample": f"brute-force fp64 matvec rows ({rows} of {n} sampled targets x all {n} centres) of the "
+                     f"same config; useful pairs counted on the same rows", "seconds": dt}
+    if extras:
+        out["steps"] = cpu_steps(procs)
+    return out
+
+
+def cpu_steps(procs: int) -> dict:
+    """Oracle timings of the paper's timed steps on configs small enough to run."""
+    from oracle import cells as OC
+    from oracle import extend as OE
+    from oracle import grid as OG
+    from oracle import kernel as OK
+    from oracle import solve as OS
+    from synth import make_inputs
+    res = {}
+    d = make_inputs("c1")
+    X = OE.extend(d["x"], d["normals"], d["delta"]).astype(np.float64)
+    b = OE.labels(len(d["x"]), d["delta"]).astype(np.float32).astype(np.float64)
+    sigma = d["sigma"]
+    t = time.perf_counter()
+    OS.lu_solve(X, b, sigma)
+    res["c1_dense_lu_s"] = time.perf_counter() - t
+    t = time.perf_counter()
+    A = OK.dense_matrix(X, sigma)
+    oc = OC.build(X.astype(np.float32), 6 * sigma, cell_edge=6 * sigma / 3.999)
+    blocks = OS.ras_blocks(oc, sigma, 512, 3.0)
+    perm, factors = oc["perm"], {}
+
+    def M(v):
+        z = np.empty_like(v)
+        z[perm] = OS.ras_apply(blocks, oc["sorted"], v[perm], sigma, factors=factors)
+        return z
+
+    _, info = OS.gmres(lambda v: A @ v, b, restart=30, rtol=1e-6, maxit=200, apply_M=M)
+    res["c1_gmres_ras_to_1e-6_s"] = time.perf_counter() - t
+    res["c1_gmres_ras_iters"] = info["iters"]
+    w = np.random.default_rng(3).normal(size=len(X))
+    lo, hi, gn = d["grid_lo"], d["grid_hi"], d["grid_n"]
+    t = time.perf_counter()
+    OK.matvec_parallel(X, w, sigma, targets=OG.nodes(lo, hi, gn), procs=procs)
+    res["c1_grid_full_s"] = time.perf_counter() - t
+    res["c1_grid_nodes"] = int(np.prod(gn))
+    d2 = make_inputs("c2")
+    X2 = OE.extend(d2["x"], d2["normals"], d2["delta"]).astype(np.float64)
+    w2 = np.random.default_rng(4).normal(size=len(X2))
+    lo, hi, gn = d2["grid_lo"], d2["grid_hi"], d2["grid_n"]
+    flat = np.sort(np.random.default_rng(5).choice(int(np.prod(gn)), 2000, replace=False))
+    t = time.perf_counter()
+    OK.matvec_parallel(X2, w2, d2["sigma"], targets=OG.nodes(lo, hi, gn, flat=flat), procs=procs)
+    dt = time.perf_counter() - t
+    res["c2_grid_sampled"] = {"nodes": len(flat), "seconds": dt,
+                              "extrapolated_full_grid_s": dt * np.prod(gn) / len(flat)}
+    return res
 
 
 def run_reference(args, rank, world, local):
@@ -397,10 +496,10 @@ def run_reference(args, rank, world, local):
     d = make_problem(args.config, args.seed)
     rows = max(50, args.cpu_sample_rows or 200)
     for _ in range(max(args.warmup, 0) and 1):
-        cpu_baseline(d, args, rows=50)
+        cpu_baseline(d, args, rows=50, extras=False)
     times, vals = [], []
     for _ in range(args.steps):
-        cb = cpu_baseline(d, args, rows=rows)
+        cb = cpu_baseline(d, args, rows=rows, extras=False)
         times.append(cb["seconds"])
         vals.append(cb["value"])
     cfg = d["cfg"]
@@ -411,7 +510,8 @@ def run_reference(args, rank, world, local):
            "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "config": {"workload": f"{args.config}: N={cfg.n} ({3 * cfg.n} centres) "
                                                       f"sampled-row brute-force matvec"},
-           "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": os.cpu_count(), "kind": "oracle",
+           "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": os.cpu_count(), "cpu_model": cpu_model(),
+                            "kind": "oracle",
                             "sample": f"{rows} sampled target rows x all centres per step"},
            "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
