@@ -1050,7 +1050,8 @@ __device__ __forceinline__ void symb_tile(const SumGeom& G, const int32_t* __res
                                           const float* xr, const float* yr, const float* zr, const bool* tv,
                                           const float* wg, int2 tl, int64_t sym_hi, int lane,
                                           float (*__restrict__ RS)[kSymPad], int* __restrict__ RI,
-                                          float (*__restrict__ O)[kOwnPad], OutT* __restrict__ out, float* fo) {
+                                          float* __restrict__ KB, float (*__restrict__ O)[kOwnPad],
+                                          OutT* __restrict__ out, float* fo) {
   float mx[T], my[T], mz[T], tf[T], wt[T];
   float2 acc[T];
 #pragma unroll
@@ -1067,15 +1068,44 @@ __device__ __forceinline__ void symb_tile(const SumGeom& G, const int32_t* __res
   const bool h4 = lane & 16, h3 = lane & 8;
   const int mys = (h4 ? 2 : 0) + (h3 ? 1 : 0);
   // symmetric ring RS[0..4] = x', y', z', |s'|^2, w and RI = sorted index
+#ifndef RBF_SYMB_UNROLL
+#define RBF_SYMB_UNROLL 1
+#endif
+#ifndef RBF_SYMB_HALF
+#define RBF_SYMB_HALF 1   // 3.138 vs 3.153 ms at c4 (fewer live registers)
+#endif
   auto flush_sym = [&](int cnt) {   // cnt: multiple of 4
-#pragma unroll 1
+    RBF_UNROLL(RBF_SYMB_UNROLL)
     for (int j = 0; j < cnt; j += 4) {
+      float2 pa = make_float2(0.f, 0.f), pb = make_float2(0.f, 0.f);
+#if RBF_SYMB_HALF
+      // two source pairs one after the other: 10 live registers of staged
+      // sources instead of 20 (LDS.64 broadcasts)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const float2 X = *reinterpret_cast<const float2*>(&RS[0][j + 2 * hh]);
+        const float2 Y = *reinterpret_cast<const float2*>(&RS[1][j + 2 * hh]);
+        const float2 Z = *reinterpret_cast<const float2*>(&RS[2][j + 2 * hh]);
+        const float2 S = *reinterpret_cast<const float2*>(&RS[3][j + 2 * hh]);
+        const float2 W = *reinterpret_cast<const float2*>(&RS[4][j + 2 * hh]);
+        float2 p = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+          float2 ra = fma2(Z, make_float2(mz[t], mz[t]), S);
+          ra = fma2(Y, make_float2(my[t], my[t]), ra);
+          ra = fma2(X, make_float2(mx[t], mx[t]), ra);
+          const float2 ea = make_float2(ex2(-ra.x), ex2(-ra.y));
+          acc[t] = fma2(ea, W, acc[t]);
+          p = fma2(ea, make_float2(wt[t], wt[t]), p);
+        }
+        if (hh == 0) pa = p; else pb = p;
+      }
+#else
       const float4 X = *reinterpret_cast<const float4*>(&RS[0][j]);
       const float4 Y = *reinterpret_cast<const float4*>(&RS[1][j]);
       const float4 Z = *reinterpret_cast<const float4*>(&RS[2][j]);
       const float4 S = *reinterpret_cast<const float4*>(&RS[3][j]);
       const float4 W = *reinterpret_cast<const float4*>(&RS[4][j]);
-      float2 pa = make_float2(0.f, 0.f), pb = make_float2(0.f, 0.f);
 #pragma unroll
       for (int t = 0; t < T; ++t) {
         const float2 ax = make_float2(mx[t], mx[t]), ay = make_float2(my[t], my[t]), az = make_float2(mz[t], mz[t]);
@@ -1091,6 +1121,7 @@ __device__ __forceinline__ void symb_tile(const SumGeom& G, const int32_t* __res
         pa = fma2(ea, wv, pa);
         pb = fma2(eb, wv, pb);
       }
+#endif
       // transpose-reduce (pa.x, pa.y, pb.x, pb.y) = sources j .. j+3 over the warp
       float k0 = h4 ? pb.x : pa.x, k1 = h4 ? pb.y : pa.y;
       const float s0 = h4 ? pa.x : pb.x, s1 = h4 ? pa.y : pb.y;
@@ -1101,10 +1132,13 @@ __device__ __forceinline__ void symb_tile(const SumGeom& G, const int32_t* __res
       k += __shfl_xor_sync(0xffffffffu, k, 4);
       k += __shfl_xor_sync(0xffffffffu, k, 2);
       k += __shfl_xor_sync(0xffffffffu, k, 1);
-      if ((lane & 7) == 0) {
-        const int jj = RI[j + mys];
-        if (jj >= 0) atomicAdd(out + jj, (OutT)(amp * k));
-      }
+      if ((lane & 7) == 0) KB[j + mys] = k;
+    }
+    // the ring's source-side sums to f_j: one atomic per source, 32 lanes at a time
+    __syncwarp();
+    for (int q = lane; q < cnt; q += 32) {
+      const int jj = RI[q];
+      if (jj >= 0) atomicAdd(out + jj, (OutT)(amp * KB[q]));
     }
   };
   auto flush_own = [&](int cnt) {   // cnt: multiple of 4
@@ -1236,6 +1270,7 @@ sum_f32_symb_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const flo
                     const int32_t* __restrict__ order) {
   __shared__ __align__(16) float rings[kSumWarps][5][kSymPad];
   __shared__ int ringi[kSumWarps][kSymPad];
+  __shared__ float ringk[kSumWarps][kSymPad];
   __shared__ __align__(16) float ringo[kSumWarps][5][kOwnPad];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   for (;;) {
@@ -1262,10 +1297,10 @@ sum_f32_symb_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const flo
     }
     const int T = (tl.y + 31) >> 5;
     switch (T) {
-      case 1: symb_tile<1>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringo[wib], out, fo); break;
-      case 2: symb_tile<2>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringo[wib], out, fo); break;
-      case 3: symb_tile<3>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringo[wib], out, fo); break;
-      default: symb_tile<4>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringo[wib], out, fo); break;
+      case 1: symb_tile<1>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringk[wib], ringo[wib], out, fo); break;
+      case 2: symb_tile<2>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringk[wib], ringo[wib], out, fo); break;
+      case 3: symb_tile<3>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringk[wib], ringo[wib], out, fo); break;
+      default: symb_tile<4>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringk[wib], ringo[wib], out, fo); break;
     }
 #pragma unroll
     for (int t = 0; t < 4; ++t)

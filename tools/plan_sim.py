@@ -84,5 +84,50 @@ def main():
     print(f"  exponentials per useful ordered pair: {ex / useful:.3f}  (sample of {len(pick)} tiles)")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not (len(sys.argv) > 5 and sys.argv[5] == "groups"):
     main()
+
+
+def group_mask_model(name="c4", cap=128, span=4, nsample=1500):
+    """Exponentials if each staged source skipped the 32-target groups whose box it
+    cannot reach (per source, and OR-ed over the 4 consecutive sources the kernel
+    processes together)."""
+    d = make_inputs(name)
+    X = OE.extend(d["x"], d["normals"], d["delta"])
+    sigma = d["sigma"]
+    c = 6 * sigma
+    oc = OC.build(X, c, cell_edge=c / 3.999)
+    S = oc["sorted"].astype(np.float64)
+    T = plan(oc["cell_start"], oc["cell_end"], oc["dim"], cap, span)
+    from scipy.spatial import cKDTree
+    tree = cKDTree(S)
+    rng = np.random.default_rng(0)
+    cc = c * (1 + 1e-5)
+    base = per_src = or4 = 0
+    for i in rng.choice(len(T), min(nsample, len(T)), replace=False):
+        s0, n = T[i]
+        P = S[s0:s0 + n]
+        lo, hi = P.min(0), P.max(0)
+        cand = np.array(tree.query_ball_point(0.5 * (lo + hi), np.linalg.norm(0.5 * (hi - lo)) + cc), dtype=np.int64)
+        cand = np.sort(cand[cand >= s0 + n])
+        g = np.maximum(0, np.maximum(lo - S[cand], S[cand] - hi))
+        kept = cand[(g * g).sum(1) <= cc * cc]
+        ng = (n + 31) // 32
+        m = np.zeros((len(kept), ng), dtype=bool)
+        for t in range(ng):
+            Q = P[32 * t:32 * t + 32]
+            ql, qh = Q.min(0), Q.max(0)
+            gg = np.maximum(0, np.maximum(ql - S[kept], S[kept] - qh))
+            m[:, t] = (gg * gg).sum(1) <= cc * cc
+        base += len(kept) * ng
+        per_src += m.sum()
+        k4 = (len(kept) + 3) // 4 * 4
+        mm = np.zeros((k4, ng), dtype=bool)
+        mm[:len(kept)] = m
+        or4 += mm.reshape(-1, 4, ng).any(axis=1).sum() * 4
+    print(f"sym-ring source x group evaluations: box {base:.3e}, per-source group cull {per_src / base:.3f}, "
+          f"OR over 4 consecutive {or4 / base:.3f}")
+
+
+if __name__ == "__main__" and len(sys.argv) > 5 and sys.argv[5] == "groups":
+    group_mask_model(sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]))
