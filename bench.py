@@ -144,6 +144,36 @@ def zero_set_quality(R, ctx, d, field, lo, hi, gn):
     return out
 
 
+def isosurface_report(R, ctx, d, cells, kern, w, lo, hi, gn):
+    """Alg.1 steps 3-4 on the eps-surrounding (rbf_isosurface, eps = 2 sigma):
+    the grid evaluated on M_ext^eps only + the marching-tetrahedra mesh of its
+    zero set (reading R24), timed with CUDA events (one warm call, then 3)."""
+    import torch
+    data = torch.as_tensor(d["x"], dtype=torch.float64, device="cuda")
+    eps = 2 * d["sigma"]
+    fm = torch.empty(gn[0] * gn[1] * gn[2], dtype=torch.float32, device="cuda")
+    R.isosurface(ctx, cells, kern, w, lo, hi, gn, data, eps, field=fm)
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(3):
+        V, T = R.isosurface(ctx, cells, kern, w, lo, hi, gn, data, eps, field=fm)
+    e1.record(s)
+    torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(s)
+    for _ in range(3):
+        Fm = R.eval_grid_masked(ctx, cells, kern, w, lo, hi, gn, data, eps, out=fm)
+    e3.record(s)
+    torch.cuda.synchronize()
+    masked = int((~torch.isnan(fm)).sum().item())
+    return {"eps": eps, "ms": e0.elapsed_time(e1) / 3, "masked_eval_ms": e2.elapsed_time(e3) / 3,
+            "masked_nodes": masked, "grid_nodes": int(fm.numel()), "vertices": int(V.shape[0]),
+            "triangles": int(T.shape[0]),
+            "note": "rbf_isosurface = eps mask (fp64 distances) + grid on the masked node blocks + marching "
+                    "tetrahedra; outside the timed step (the step evaluates the full grid, Alg.1 step 3)"}
+
+
 def density_report(R, ctx, d):
     """Density measures of the surface points on the GPU (Eq.7-11, rbf_density):
     q_X, h_max and the sigma heuristics next to the configured sigma."""
@@ -269,7 +299,7 @@ def run_ours(args, rank, world, local):
     evs = []
     e0.record(s)
     for _ in range(args.steps):
-        _, w, field, rep = step()
+        cells_last, w, field, rep = step()
         reps.append(rep)
         if trace:
             evs.append((torch.cuda.Event(enable_timing=True), time.perf_counter()))
@@ -328,10 +358,11 @@ def run_ours(args, rank, world, local):
     # Alg.1 step 3 output (outside the timed step): the eps-masked zero set of the
     # last field (rbf_zero_set, eps = 2 sigma, reading R11) and its distance to
     # the generator's exact surface g = 0 (first-order |g| / |grad g|)
-    zs = dens = None
+    zs = dens = iso = None
     if rank == 0:
         zs = zero_set_quality(R, ctx, d, field, lo, hi, gn)
         dens = density_report(R, ctx, d)
+        iso = isosurface_report(R, ctx, d, cells_last, kern, w, lo, hi, gn)
 
     # roofline of the dominant kernel (fp32 summation), live CUDA-event timing
     t_mv, n_mv = prof["matvec_f32"]
@@ -389,7 +420,7 @@ def run_ours(args, rank, world, local):
                    "matvecs_f64_per_step": mv64 / args.steps, "stage_ms_per_step": stage_ms,
                    "iters_phase1": last["iters_phase1"], "iters_phase2": last["iters_phase2"],
                    "rel_residual_true": last["rel_residual_true"], "converged": last["converged"],
-                   "ras_blocks": last["nblocks"], "precond_bytes": last["precond_bytes"], "zero_set": zs,
+                   "ras_blocks": last["nblocks"], "precond_bytes": last["precond_bytes"], "zero_set": zs, "isosurface": iso,
                    "gate_1e-6": gate_note(args.config),
                    "density": dens,
                    "cells": info,

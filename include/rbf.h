@@ -379,6 +379,50 @@ rbf_status rbf_csr_spmv(rbf_ctx* ctx, const rbf_csr* m, const float* w, float* f
 rbf_status rbf_zero_set(rbf_ctx* ctx, const float* field, const rbf_grid* grid, const double* data,
                         int64_t ndata, double eps, double* points, int64_t cap, int64_t* count);
 
+/* ---- Alg.1 steps 3-4 on the eps-surrounding: masked grid + iso-surface mesh --
+ * §2.1.3: "evaluating the interpolant only in a small surrounding
+ * volume" M_ext^eps = {x : d(x, M) <= eps} of the surface, and Alg.1 step 4
+ * (MATLAB isosurface): the mesh of the zero iso-surface.
+ * data: DEVICE fp64 ndata x 3 (the surface points X); eps > 0; a node is in
+ * M_ext^eps iff some data point lies within eps (fp64 distances, the mask of
+ * rbf_zero_set).  grid, w, cells, kern as rbf_eval_grid.
+ *
+ * rbf_eval_grid_masked: field (DEVICE fp32, all nodes, x fastest) receives
+ *   P_f at the nodes of M_ext^eps -- bit-identical to rbf_eval_grid's value
+ *   there -- and NaN (all bits set) at every other node; only the 4x4x4 node
+ *   blocks holding a masked node are evaluated.  world > 1: every rank returns
+ *   the full field (slab layers gathered, as rbf_eval_grid).
+ * rbf_mesh_from_field: the mesh of the zero iso-surface of a given field on
+ *   M_ext^eps (nodes outside the mask are never read).  Reading R24
+ *   (oracle/mesh.py): marching tetrahedra on the Kuhn split of each
+ *   grid cube (6 tetrahedra per cube, for the axis permutations xyz xzy yxz
+ *   yzx zxy zyx); node "inside" iff F < 0; a vertex on every grid edge (v, v+d),
+ *   d in x, y, z, xy, xz, yz, xyz (this order), whose two nodes are in the mask
+ *   and on opposite sides, at p_v + t (p_{v+d} - p_v), t = F_v/(F_v - F_{v+d})
+ *   (fp64); vertices numbered in (v, d) order; a cube is polygonised iff its 8
+ *   nodes are in the mask; triangles in (cube, tetrahedron) order, oriented
+ *   with their normal (p1-p0) x (p2-p0) towards F > 0 (outward for the
+ *   ±delta labels of rbf_extend_points).  Inside the mask the mesh is closed
+ *   (every edge shared by two triangles); at the mask boundary it is open, and
+ *   vertices of boundary edges may be unreferenced.
+ * rbf_isosurface: rbf_eval_grid_masked followed by rbf_mesh_from_field, the
+ *   field never leaving the device (field may be NULL: library scratch).
+ * The mesh object is library-owned: rbf_mesh_view returns DEVICE pointers
+ *   (vertices fp64 nv x 3, triangles int32 nt x 3) valid until rbf_mesh_free,
+ *   which must precede rbf_destroy of the context that made it.
+ * Synchronise.  Errors: RBF_EINVAL (NULLs, eps <= 0, bad grid, non-finite
+ * data, more than 2^31 vertices), RBF_ENOMEM. */
+typedef struct rbf_mesh rbf_mesh;
+rbf_status rbf_eval_grid_masked(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern, const double* w,
+                                const rbf_grid* grid, const double* data, int64_t ndata, double eps, float* field);
+rbf_status rbf_mesh_from_field(rbf_ctx* ctx, const float* field, const rbf_grid* grid, const double* data,
+                               int64_t ndata, double eps, rbf_mesh** out);
+rbf_status rbf_isosurface(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern, const double* w,
+                          const rbf_grid* grid, const double* data, int64_t ndata, double eps, float* field,
+                          rbf_mesh** out);
+rbf_status rbf_mesh_view(const rbf_mesh* m, const double** vertices, int64_t* nv, const int32_t** tris, int64_t* nt);
+void rbf_mesh_free(rbf_mesh* m);
+
 /* ---- density measures of the data set (§4, Eq.7-11) ----
  * x: DEVICE fp64 n x 3 (for 2-D sets pass z = 0).  Distances in fp64,
  * ((dx^2 + dy^2) + dz^2) then sqrt of the minimum (bit-identical to the oracle).

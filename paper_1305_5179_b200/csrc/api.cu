@@ -398,6 +398,22 @@ rbf_status eval_grid_impl(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* ke
 }
 }  // namespace
 
+namespace rbf {
+// isosurface.cu: the grid evaluated on the eps-surrounding only (near != 0), NaN
+// elsewhere; the slab layers of every rank are gathered as in rbf_eval_grid
+rbf_status eval_grid_masked_impl(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, const double* w,
+                                 const rbf_grid* g, const uint8_t* near, float* field) {
+  RBF_TRY(check_cells(ctx, c, kern));
+  if (!w || !field || !near) { set_error("NULL argument"); return RBF_EINVAL; }
+  RBF_TRY(check_grid(g));
+  KernelParams kp = kernel_params(kern);
+  RBF_TRY(ctx->vec_a.ensure(sizeof(double) * c->n, ctx->stream));
+  RBF_TRY(gather_f64_to_sorted(ctx, w, c->perm.as<int32_t>(), ctx->vec_a.as<double>(), c->n));
+  RBF_TRY(eval_grid_sorted(ctx, c, kp, ctx->vec_a.as<double>(), g, field, nullptr, near));
+  return allgather_layers(ctx, c, g, field);
+}
+}  // namespace rbf
+
 extern "C" {
 
 rbf_status rbf_eval_grid(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, const double* w,

@@ -239,9 +239,12 @@ rbf_status matvec_sorted_f64(rbf_ctx* ctx, const rbf_cells* c, const KernelParam
                              const double* w_sorted, double* f_sorted, const int32_t* out_perm,
                              int op = RBF_OP_ONESIDED);
 rbf_status order_wide_tiles(rbf_ctx* ctx, rbf_cells* c, const KernelParams& kp);
+// near (optional, uint8 per node): evaluate only the node blocks holding a node
+// with near != 0 and write NaN (all bits set) at every node with near == 0
+// (the eps-surrounding M_ext^eps of §2.1.3)
 rbf_status eval_grid_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
                             const double* w_sorted, const rbf_grid* g, float* field,
-                            unsigned long long* pair_stats = nullptr);
+                            unsigned long long* pair_stats = nullptr, const uint8_t* near = nullptr);
 
 // dist.cu (multi-rank slab partition over a Transport)
 rbf_status dist_init(rbf_ctx* ctx, const void* unique_id, int rank, int world);
@@ -264,6 +267,11 @@ rbf_status allgather_sorted(rbf_ctx* ctx, const rbf_cells* c, double* full);
 // the rank owning the cell plane of its first node block)
 void grid_layers(const rbf_cells* c, const rbf_grid* g, int r, int64_t* k0, int64_t* k1);
 rbf_status allgather_layers(rbf_ctx* ctx, const rbf_cells* c, const rbf_grid* g, float* field);
+
+// pointset.cu: near[v] (uint8 per grid node, allocated here) = some data point
+// (DEVICE fp64 ndata x 3) within eps of node v, fp64 distances (rbf_zero_set's mask)
+rbf_status build_near_mask(rbf_ctx* ctx, const rbf_grid* grid, const double* data, int64_t ndata, double eps,
+                           DevBuf& near);
 
 // small vector kernels (vec.cu)
 rbf_status gather_f32_to_sorted(rbf_ctx* ctx, const float* src, const int32_t* perm, float* dst, int64_t n);

@@ -149,17 +149,12 @@ __global__ void edge_emit_kernel(const float* __restrict__ F, const uint8_t* __r
 
 using namespace rbf;
 
-extern "C" rbf_status rbf_zero_set(rbf_ctx* ctx, const float* field, const rbf_grid* grid, const double* data,
-                                   int64_t ndata, double eps, double* points, int64_t cap, int64_t* count) {
-  if (!ctx || !field || !grid || !count) { set_error("NULL argument"); return RBF_EINVAL; }
-  if (ndata < 0 || (ndata > 0 && !data) || cap < 0 || (cap > 0 && !points)) { set_error("bad data/points"); return RBF_EINVAL; }
-  if (!(eps > 0) || !std::isfinite(eps)) { set_error("eps must be finite and > 0"); return RBF_EINVAL; }
-  for (int a = 0; a < 3; ++a)
-    if (grid->n[a] < 2 || !(grid->hi[a] > grid->lo[a])) { set_error("bad grid"); return RBF_EINVAL; }
-  RBF_CUDA_TRY(cudaSetDevice(ctx->device));
+namespace rbf {
+// near[v] (uint8, one per grid node) = some data point within eps of node v
+// (fp64 distances; steps 1-2 above).  ndata == 0: all zeros.
+rbf_status build_near_mask(rbf_ctx* ctx, const rbf_grid* grid, const double* data, int64_t ndata, double eps,
+                           DevBuf& near) {
   cudaStream_t s = ctx->stream;
-  *count = 0;
-  if (ndata == 0) return RBF_OK;   // no data: the eps-surrounding is empty
   ZGrid g;
   for (int a = 0; a < 3; ++a) {
     g.lo[a] = grid->lo[a];
@@ -167,6 +162,11 @@ extern "C" rbf_status rbf_zero_set(rbf_ctx* ctx, const float* field, const rbf_g
     g.n[a] = grid->n[a];
   }
   const int64_t nn = (int64_t)g.n[0] * g.n[1] * g.n[2];
+  RBF_TRY(near.alloc(nn, s));
+  if (ndata == 0) {
+    RBF_CUDA_TRY(cudaMemsetAsync(near.p, 0, nn, s));
+    return RBF_OK;
+  }
   // 1. data cells of edge h >= eps over the data bounding box (host bbox via a copy)
   std::vector<double> hx(3 * (size_t)ndata);
   RBF_CUDA_TRY(cudaMemcpyAsync(hx.data(), data, sizeof(double) * 3 * ndata, cudaMemcpyDeviceToHost, s));
@@ -194,7 +194,7 @@ extern "C" rbf_status rbf_zero_set(rbf_ctx* ctx, const float* field, const rbf_g
     ncell *= dc.dim[a];
   }
   dc.inv_h = 1.0 / h;
-  DevBuf k1, v1, k2, v2, start, S, near, flag, pos, tot;
+  DevBuf k1, v1, k2, v2, start, S;
   RBF_TRY(k1.alloc(4 * ndata, s));
   RBF_TRY(v1.alloc(4 * ndata, s));
   RBF_TRY(k2.alloc(4 * ndata, s));
@@ -212,10 +212,33 @@ extern "C" rbf_status rbf_zero_set(rbf_ctx* ctx, const float* field, const rbf_g
   data_gather_kernel<<<grid_for(ndata, 256), 256, 0, s>>>(data, v2.as<int32_t>(), ndata, S.as<double>());
   RBF_CHECK_LAUNCH();
   // 2. the eps mask
-  RBF_TRY(near.alloc(nn, s));
   near_kernel<<<grid_for(nn, 256, 148 * 32), 256, 0, s>>>(g, dc, start.as<int32_t>(), S.as<double>(), eps,
                                                           near.as<uint8_t>());
   RBF_CHECK_LAUNCH();
+  return RBF_OK;
+}
+}  // namespace rbf
+
+extern "C" rbf_status rbf_zero_set(rbf_ctx* ctx, const float* field, const rbf_grid* grid, const double* data,
+                                   int64_t ndata, double eps, double* points, int64_t cap, int64_t* count) {
+  if (!ctx || !field || !grid || !count) { set_error("NULL argument"); return RBF_EINVAL; }
+  if (ndata < 0 || (ndata > 0 && !data) || cap < 0 || (cap > 0 && !points)) { set_error("bad data/points"); return RBF_EINVAL; }
+  if (!(eps > 0) || !std::isfinite(eps)) { set_error("eps must be finite and > 0"); return RBF_EINVAL; }
+  for (int a = 0; a < 3; ++a)
+    if (grid->n[a] < 2 || !(grid->hi[a] > grid->lo[a])) { set_error("bad grid"); return RBF_EINVAL; }
+  RBF_CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  *count = 0;
+  if (ndata == 0) return RBF_OK;   // no data: the eps-surrounding is empty
+  ZGrid g;
+  for (int a = 0; a < 3; ++a) {
+    g.lo[a] = grid->lo[a];
+    g.step[a] = (grid->hi[a] - grid->lo[a]) / (double)(grid->n[a] - 1);
+    g.n[a] = grid->n[a];
+  }
+  const int64_t nn = (int64_t)g.n[0] * g.n[1] * g.n[2];
+  DevBuf near, flag, pos, tot;
+  RBF_TRY(build_near_mask(ctx, grid, data, ndata, eps, near));
   // 3. crossings per axis, in the oracle's (axis, lower node) order
   RBF_TRY(flag.alloc(4 * nn, s));
   RBF_TRY(pos.alloc(4 * nn, s));

@@ -515,7 +515,8 @@ sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
                const int2* __restrict__ tiles, const float4* __restrict__ tbox, int64_t ntiles, int64_t tile_base,
                GridDesc gd, OutT* __restrict__ out, const int32_t* __restrict__ out_perm,
                int* __restrict__ work, unsigned long long* __restrict__ stats, int64_t own_lo = 0,
-               int64_t own_hi = 0, const int32_t* __restrict__ tlist = nullptr) {
+               int64_t own_hi = 0, const int32_t* __restrict__ tlist = nullptr,
+               const uint8_t* __restrict__ nmask = nullptr) {
   __shared__ __align__(16) float ring[kSumWarps][SYM ? 11 : 10][kBufPad];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   // boundary sources (grid) / symmetric sources (SYM matvec)
@@ -675,6 +676,8 @@ sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
         float v = G.amp * ((acc[t].x + acc[t].y) * tf[t]);
         int64_t o = tidx[t];
         if (MODE == 0 && out_perm) o = out_perm[o];
+        // masked grid (M_ext^eps): nodes outside the eps-surrounding are NaN
+        if (MODE == 1 && nmask && !nmask[o]) v = __int_as_float(-1);
         if (SYM) atomicAdd(out + o, (OutT)v);
         else out[o] = (OutT)v;
       }
@@ -1721,6 +1724,19 @@ __global__ void mark_node_blocks(const int32_t* __restrict__ cell_start, CellGri
   }
 }
 
+// node blocks of layers [bz0, bz1) holding a node of the eps-surrounding
+__global__ void mark_near_blocks(const uint8_t* __restrict__ near, GridDesc gd, int bz0, int bz1,
+                                 uint32_t* __restrict__ flag) {
+  const int64_t nn = (int64_t)gd.n[0] * gd.n[1] * gd.n[2];
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nn; v += (int64_t)gridDim.x * blockDim.x) {
+    if (!near[v]) continue;
+    const int i = (int)(v % gd.n[0]), j = (int)((v / gd.n[0]) % gd.n[1]), k = (int)(v / ((int64_t)gd.n[0] * gd.n[1]));
+    const int bz = k >> 2;
+    if (bz < bz0 || bz >= bz1) continue;
+    flag[((int64_t)bz * gd.nb[1] + (j >> 2)) * gd.nb[0] + (i >> 2)] = 1u;
+  }
+}
+
 __global__ void compact_blocks(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos, int64_t n,
                                int32_t* __restrict__ list) {
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n; b += (int64_t)gridDim.x * blockDim.x)
@@ -1847,7 +1863,7 @@ rbf_status matvec_sorted_f32(rbf_ctx* ctx, const rbf_cells* c, const KernelParam
     auto kfn = sum_f32_kernel<0, false, float, false, true>;
     kfn<<<sum_blocks(ctx, kfn), kSumWarps * 32, 0, s>>>(
         G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), c->tiles.as<int2>(), c->tile_box.as<float4>(),
-        V.t1 - V.t0, V.t0, gd, f_out, out_perm, ctx->counter.as<int>(), nullptr, 0, 0, nullptr);
+        V.t1 - V.t0, V.t0, gd, f_out, out_perm, ctx->counter.as<int>(), nullptr, 0, 0, nullptr, nullptr);
   }
   RBF_CHECK_LAUNCH();
   return RBF_OK;
@@ -1919,7 +1935,7 @@ static rbf_status matvec_f32_solver(rbf_ctx* ctx, const rbf_cells* c, const Kern
   auto kfn = expansion_ok(kp, c->hd2) ? sum_f32_kernel<0, false, double> : sum_f32_kernel<0, false, double, false, true>;
   kfn<<<sum_blocks(ctx, kfn), kSumWarps * 32, 0, s>>>(
       G, c->cell_start.as<int32_t>(), srcb, c->tiles.as<int2>(), c->tile_box.as<float4>(), V.t1 - V.t0, V.t0, gd,
-      f_loc - V.o0, nullptr, ctx->counter.as<int>(), nullptr, 0, 0, nullptr);
+      f_loc - V.o0, nullptr, ctx->counter.as<int>(), nullptr, 0, 0, nullptr, nullptr);
   RBF_CHECK_LAUNCH();
   return RBF_OK;
 }
@@ -1979,7 +1995,7 @@ rbf_status matvec_sorted_f64(rbf_ctx* ctx, const rbf_cells* c, const KernelParam
 
 rbf_status eval_grid_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
                             const double* w_sorted, const rbf_grid* g, float* field,
-                            unsigned long long* pair_stats) {
+                            unsigned long long* pair_stats, const uint8_t* near) {
   cudaStream_t s = ctx->stream;
   const int64_t n = c->n;
   RBF_TRY(ctx->src4.ensure(sizeof(float4) * n, s));
@@ -2015,9 +2031,16 @@ rbf_status eval_grid_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams
   RBF_TRY(cnt.alloc(4, s));
   RBF_CUDA_TRY(cudaMemsetAsync(flag.p, 0, 4 * (size_t)nbt, s));
   const int64_t ncell = (int64_t)c->dim[0] * c->dim[1] * c->dim[2];
-  mark_node_blocks<<<grid_for(ncell, 256), 256, 0, s>>>(c->cell_start.as<int32_t>(), G.g, G.cc, gd,
-                                                         (int)(b0 / per_layer), (int)(b1 / per_layer),
-                                                         flag.as<uint32_t>());
+  if (near) {
+    // eps-surrounding: the node blocks holding a node within eps of the data
+    const int64_t nn = (int64_t)gd.n[0] * gd.n[1] * gd.n[2];
+    mark_near_blocks<<<grid_for(nn, 256), 256, 0, s>>>(near, gd, (int)(b0 / per_layer), (int)(b1 / per_layer),
+                                                       flag.as<uint32_t>());
+  } else {
+    mark_node_blocks<<<grid_for(ncell, 256), 256, 0, s>>>(c->cell_start.as<int32_t>(), G.g, G.cc, gd,
+                                                           (int)(b0 / per_layer), (int)(b1 / per_layer),
+                                                           flag.as<uint32_t>());
+  }
   RBF_CHECK_LAUNCH();
   RBF_TRY(exclusive_scan_u32(ctx, flag.as<uint32_t>(), pos.as<uint32_t>(), nbt, cnt.as<uint32_t>()));
   compact_blocks<<<grid_for(nbt, 256), 256, 0, s>>>(flag.as<uint32_t>(), pos.as<uint32_t>(), nbt,
@@ -2029,8 +2052,8 @@ rbf_status eval_grid_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams
   // this rank's node layers [b0, b1) start as zeros; the active blocks overwrite theirs
   const int64_t n0 = (int64_t)gd.n[0] * gd.n[1];
   const int64_t k0 = std::min<int64_t>((b0 / per_layer) * 4, gd.n[2]), k1 = std::min<int64_t>((b1 / per_layer) * 4, gd.n[2]);
-  if (k1 > k0 && !pair_stats)
-    RBF_CUDA_TRY(cudaMemsetAsync(field + k0 * n0, 0, sizeof(float) * (size_t)((k1 - k0) * n0), s));
+  if (k1 > k0 && !pair_stats)   // zeros, or NaN (all bits set) outside the eps-surrounding
+    RBF_CUDA_TRY(cudaMemsetAsync(field + k0 * n0, near ? 0xff : 0, sizeof(float) * (size_t)((k1 - k0) * n0), s));
   if (nact == 0) return RBF_OK;
   if (pair_stats) {
     sum_f32_kernel<1, true, float><<<sum_blocks(ctx, sum_f32_kernel<1, true, float>), kSumWarps * 32, 0, s>>>(
@@ -2044,7 +2067,7 @@ rbf_status eval_grid_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams
   auto kfn = expansion_ok(kp, hd2) ? sum_f32_kernel<1, false, float> : sum_f32_kernel<1, false, float, false, true>;
   kfn<<<sum_blocks(ctx, kfn), kSumWarps * 32, 0, s>>>(
       G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), nullptr, nullptr, nact, 0, gd, field, nullptr,
-      ctx->counter.as<int>(), nullptr, 0, 0, list.as<int32_t>());
+      ctx->counter.as<int>(), nullptr, 0, 0, list.as<int32_t>(), near);
   RBF_CHECK_LAUNCH();
   return RBF_OK;
 }

@@ -118,6 +118,13 @@ EXPORTS = {
                                       C.POINTER(C.c_int64)]),
     "rbf_zero_set": (C.c_int, [_P, _P, C.POINTER(_Grid), _P, C.c_int64, C.c_double, _P, C.c_int64,
                                C.POINTER(C.c_int64)]),
+    "rbf_eval_grid_masked": (C.c_int, [_P, _P, C.POINTER(_Kernel), _P, C.POINTER(_Grid), _P, C.c_int64,
+                                       C.c_double, _P]),
+    "rbf_mesh_from_field": (C.c_int, [_P, _P, C.POINTER(_Grid), _P, C.c_int64, C.c_double, C.POINTER(_P)]),
+    "rbf_isosurface": (C.c_int, [_P, _P, C.POINTER(_Kernel), _P, C.POINTER(_Grid), _P, C.c_int64, C.c_double, _P,
+                                 C.POINTER(_P)]),
+    "rbf_mesh_view": (C.c_int, [_P, C.POINTER(_P), C.POINTER(C.c_int64), C.POINTER(_P), C.POINTER(C.c_int64)]),
+    "rbf_mesh_free": (None, [_P]),
     "rbf_assemble": (C.c_int, [_P, _P, C.POINTER(_Kernel), C.POINTER(_P)]),
     "rbf_csr_free": (None, [_P]),
     "rbf_csr_info": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_double)]),
@@ -463,6 +470,59 @@ def zero_set(ctx: Context, field: torch.Tensor, lo, hi, n, data: torch.Tensor, e
             return pts[:cnt.value]
         cap = cnt.value
     return pts[:cnt.value]
+
+
+def eval_grid_masked(ctx: Context, cells: Cells, kernel: Kernel, w: torch.Tensor, lo, hi, n, data: torch.Tensor,
+                     eps: float, out: torch.Tensor | None = None):
+    """rbf_eval_grid_masked: P_f on the nodes within eps of the data (M_ext^eps,
+    §2.1.3), NaN elsewhere; returns (nz, ny, nx) fp32."""
+    _need(w, torch.float64, cells.n, "w")
+    _need(data, torch.float64, data.shape[0] * 3, "data")
+    g, n3 = _grid_c(lo, hi, n)
+    field = torch.empty((n3[2], n3[1], n3[0]), dtype=torch.float32, device=w.device) if out is None else out
+    _need(field, torch.float32, n3[0] * n3[1] * n3[2], "field")
+    _check(_lib.rbf_eval_grid_masked(ctx._h, cells._h, C.byref(kernel._c()), _ptr(w), C.byref(g), _ptr(data),
+                                     data.shape[0], eps, _ptr(field)))
+    return field
+
+
+def _take_mesh(h, device):
+    """Copies a library mesh into torch tensors and frees it: (vertices (nv,3) fp64, triangles (nt,3) int32)."""
+    try:
+        vp, tp = C.c_void_p(), C.c_void_p()
+        nv, nt = C.c_int64(), C.c_int64()
+        _check(_lib.rbf_mesh_view(h, C.byref(vp), C.byref(nv), C.byref(tp), C.byref(nt)))
+        V = _wrap_copy(vp.value if nv.value else None, (nv.value, 3), "<f8", torch.float64, device)
+        T = _wrap_copy(tp.value if nt.value else None, (nt.value, 3), "<i4", torch.int32, device)
+        return V, T
+    finally:
+        _lib.rbf_mesh_free(h)
+
+
+def mesh_from_field(ctx: Context, field: torch.Tensor, lo, hi, n, data: torch.Tensor, eps: float):
+    """rbf_mesh_from_field: triangle mesh (reading R24) of the zero iso-surface of a
+    grid field on M_ext^eps; returns (vertices, triangles) on the device."""
+    g, n3 = _grid_c(lo, hi, n)
+    _need(field, torch.float32, n3[0] * n3[1] * n3[2], "field")
+    _need(data, torch.float64, data.shape[0] * 3, "data")
+    h = C.c_void_p()
+    _check(_lib.rbf_mesh_from_field(ctx._h, _ptr(field), C.byref(g), _ptr(data), data.shape[0], eps, C.byref(h)))
+    return _take_mesh(h, field.device)
+
+
+def isosurface(ctx: Context, cells: Cells, kernel: Kernel, w: torch.Tensor, lo, hi, n, data: torch.Tensor,
+               eps: float, field: torch.Tensor | None = None):
+    """rbf_isosurface (Alg.1 steps 3-4 on M_ext^eps): masked grid evaluation + mesh.
+    Returns (vertices, triangles); `field`, if given, receives the masked field."""
+    _need(w, torch.float64, cells.n, "w")
+    _need(data, torch.float64, data.shape[0] * 3, "data")
+    g, n3 = _grid_c(lo, hi, n)
+    if field is not None:
+        _need(field, torch.float32, n3[0] * n3[1] * n3[2], "field")
+    h = C.c_void_p()
+    _check(_lib.rbf_isosurface(ctx._h, cells._h, C.byref(kernel._c()), _ptr(w), C.byref(g), _ptr(data),
+                               data.shape[0], eps, _ptr(field), C.byref(h)))
+    return _take_mesh(h, w.device)
 
 
 def nn_distance(ctx: Context, x: torch.Tensor, q: torch.Tensor | None = None):

@@ -189,3 +189,51 @@ def test_matvec_large_cell_edge_difference_form(R, ctx, big):
         f = f.cpu().numpy()[rows]
         assert np.isfinite(f).all()
         assert (np.abs(f - ref) <= 5e-5 * g).all()
+
+
+def test_masked_grid_and_mesh_crop(R, ctx, big):
+    """rbf_isosurface at the bench's grid (§8(f) 1): the masked field equals the
+    full field bit for bit on M_ext^eps (eps = 2 sigma) and is NaN elsewhere (the
+    mask checked against the oracle's fp64 distances on sampled nodes); the mesh
+    of a 24^3-node crop equals the oracle's marching tetrahedra on the same
+    values (vertex positions to 1e-12: the crop's node coordinates are re-derived
+    from its own box; triangles exactly, through the vertex match)."""
+    from scipy.spatial import cKDTree
+    from oracle import mesh as OM
+    d = big["d"]
+    lo, hi, gn = d["grid_lo"], d["grid_hi"], d["grid_n"]
+    eps = 2 * big["sigma"]
+    w = torch.as_tensor(big["w_fit"], device="cuda")
+    data = torch.as_tensor(d["x"], device="cuda")
+    full = R.eval_grid(ctx, big["cells"], big["kern"], w, lo, hi, gn).cpu().numpy().ravel()
+    Fm = torch.empty(full.size, dtype=torch.float32, device="cuda")
+    V, T = R.isosurface(ctx, big["cells"], big["kern"], w, lo, hi, gn, data, eps, field=Fm)
+    Fm = Fm.cpu().numpy()
+    near = ~np.isnan(Fm)
+    assert np.array_equal(Fm[near].view(np.uint32), full[near].view(np.uint32))
+    rng = np.random.default_rng(12)
+    fl = np.concatenate([rng.choice(np.nonzero(near)[0], 150, replace=False),
+                         rng.choice(np.nonzero(~near & (full != 0))[0], 150, replace=False)])
+    dist = OG._min_dist(OG.nodes(lo, hi, gn, flat=fl), d["x"], chunk=4)
+    np.testing.assert_array_equal(dist <= eps, near[fl])
+    V, T = V.cpu().numpy(), T.cpu().numpy()
+    assert len(T) > 100_000
+    # crop around the first surface point
+    nx, ny, nz = gn
+    step = [(hi[a] - lo[a]) / (gn[a] - 1) for a in range(3)]
+    c0 = [int(np.clip(round((d["x"][0][a] - lo[a]) / step[a]) - 12, 0, gn[a] - 24)) for a in range(3)]
+    Fg = Fm.reshape(nz, ny, nx)
+    crop = Fg[c0[2]:c0[2] + 24, c0[1]:c0[1] + 24, c0[0]:c0[0] + 24].ravel()
+    clo = [lo[a] + c0[a] * step[a] for a in range(3)]
+    chi = [lo[a] + (c0[a] + 23) * step[a] for a in range(3)]
+    Vo, To = OM.marching_tets(np.nan_to_num(crop, nan=1.0), clo, chi, (24, 24, 24), ~np.isnan(crop))
+    assert len(To) > 50
+    dist_v, idx = cKDTree(V).query(Vo)
+    assert dist_v.max() <= 1e-12
+    mapped = {tuple(np.roll(t, -int(np.argmin(t)))) for t in idx[To]}
+    gpu = {tuple(np.roll(t, -int(np.argmin(t)))) for t in T}
+    assert mapped <= gpu
+    # and nothing more: GPU triangles whose centroid lies strictly inside the crop
+    cen = V[T].mean(axis=1)
+    inside = np.all((cen > np.array(clo)) & (cen < np.array(chi)), axis=1)
+    assert inside.sum() == len(To)
