@@ -94,6 +94,35 @@ __global__ void multi_axpy_kernel(double* __restrict__ w, const VT* __restrict__
   }
 }
 
+// multi_axpy fused with the next norm: w[i] += sum_j coef[j] V_j[i], and
+// partial[blockIdx.x] = this block's sum of the new w[i]^2 (grid-stride over a
+// fixed grid, fixed reduction order: deterministic), saving a pass over w
+template <class VT>
+__global__ void __launch_bounds__(kVecThreads)
+multi_axpy_nrm_kernel(double* __restrict__ w, const VT* __restrict__ V, int64_t ldv, int k,
+                      const double* __restrict__ coef, int64_t n, double* __restrict__ partial) {
+  __shared__ double sc[64];
+  __shared__ double red[kVecThreads / 32];
+  for (int q = threadIdx.x; q < k && q < 64; q += blockDim.x) sc[q] = coef[q];
+  __syncthreads();
+  double ss = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = w[i];
+    for (int j = 0; j < k; ++j) acc = fma(sc[j], (double)V[(int64_t)j * ldv + i], acc);
+    w[i] = acc;
+    ss = fma(acc, acc, ss);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < kVecThreads / 32; ++q) t += red[q];
+    partial[blockIdx.x] = t;
+  }
+}
+
 template <class OT>
 __global__ void scale_kernel(const double* __restrict__ a, double s, OT* __restrict__ b, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -200,6 +229,17 @@ struct Solver {
   rbf_status maxpy(double* vec, const VT* Vb, int k, const double* coef) {
     multi_axpy_kernel<VT><<<grid_for(n, kVecThreads), kVecThreads, 0, ctx->stream>>>(vec, Vb, n, k, coef, n);
     RBF_CHECK_LAUNCH();
+    return RBF_OK;
+  }
+  // maxpy, and *nrm2_out = ||vec||^2 of the result (one pass)
+  template <class VT>
+  rbf_status maxpy_nrm(double* vec, const VT* Vb, int k, const double* coef, double* nrm2_out) {
+    cudaStream_t s = ctx->stream;
+    multi_axpy_nrm_kernel<VT><<<nblk, kVecThreads, 0, s>>>(vec, Vb, n, k, coef, n, partial.as<double>());
+    RBF_CHECK_LAUNCH();
+    reduce_partials<<<1, 32, 0, s>>>(partial.as<double>(), 1, nblk, nrm2_out, 0, nullptr);
+    RBF_CHECK_LAUNCH();
+    if (ctx->world > 1) RBF_TRY(allreduce_sum(ctx, nrm2_out, 1));
     return RBF_OK;
   }
   // r = b - A x ; returns ||r|| (synchronises)
@@ -338,15 +378,16 @@ rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp
         RBF_TRY(S.op(fp64, (const VT*)Zj(j), S.w.as<double>()));
         double* wv = S.w.as<double>();
         // classical Gram-Schmidt, one pass or two (CGS2, the default)
+        // (the last axpy pass also forms |w|^2 for the normalisation)
         RBF_TRY(S.mdot<VT>(Vb, j + 1, wv, dh, dneg));
-        RBF_TRY(S.maxpy<VT>(wv, Vb, j + 1, dneg));
         if (passes == 2) {
-          RBF_TRY(S.mdot<VT>(Vb, j + 1, wv, d2, dneg));
           RBF_TRY(S.maxpy<VT>(wv, Vb, j + 1, dneg));
+          RBF_TRY(S.mdot<VT>(Vb, j + 1, wv, d2, dneg));
+          RBF_TRY(S.maxpy_nrm<VT>(wv, Vb, j + 1, dneg, dn));
         } else {
+          RBF_TRY(S.maxpy_nrm<VT>(wv, Vb, j + 1, dneg, dn));
           RBF_CUDA_TRY(cudaMemsetAsync(d2, 0, sizeof(double) * (j + 1), s));
         }
-        RBF_TRY(S.mdot<double>(wv, 1, wv, dn, nullptr));
         scale_by_inv_norm<VT><<<grid_for(n, 256), 256, 0, s>>>(wv, dn, Vj(j + 1), n);
         RBF_CHECK_LAUNCH();
         double* slot = hpin + (size_t)j * pstride;

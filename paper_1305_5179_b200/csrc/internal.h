@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "../../include/rbf.h"
+#include "checks.h"
 
 namespace rbf {
 

@@ -42,6 +42,12 @@ constexpr int kLd = kNb + 4;   // padded smem row (doubles)
 // pivot row and the displaced row are exchanged through DSMEM -> local rank-1
 // update of the owned rows (fused with the next column's candidate search).
 // HBM sees one read and one write of the panel per elimination step.
+// block barrier, preceded in the CHECKED build by a jitter (checks.h)
+#define RBF_SYNC()     \
+  do {                 \
+    RBF_JITTER();      \
+    __syncthreads();   \
+  } while (0)
 constexpr int kPs = kNb + 1;   // smem row stride (doubles) of the cluster panel
 
 __global__ void __launch_bounds__(kThreads)
@@ -70,7 +76,7 @@ panel_cluster_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, in
     const int lr = q / kb, c = q % kb;
     Pn[lr * kPs + c] = A[(int64_t)(k0 + rb + lr) * ld + k0 + c];
   }
-  __syncthreads();
+  RBF_SYNC();
   int singular = 0;
   double best = -1.0;
   int bi = 0x7fffffff;
@@ -87,7 +93,7 @@ panel_cluster_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, in
       if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
     }
     if (lane == 0) { sv[wid] = best; si[wid] = bi; }
-    __syncthreads();
+    RBF_SYNC();
     if (tid == 0) {
       double b2 = sv[0];
       int i2 = si[0];
@@ -96,7 +102,7 @@ panel_cluster_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, in
       cand_v = b2;
       cand_i = i2;
     }
-    cl.sync();
+    RBF_JITTER(); cl.sync();
     // global pivot: reduce the CL candidates (DSMEM), identically in every CTA
     if (wid == 0) {
       double v = -1.0;
@@ -113,20 +119,20 @@ panel_cluster_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, in
       }
       if (lane == 0) s_p = i;
     }
-    __syncthreads();
+    RBF_SYNC();
     const int p = s_p;
     const int own_p = p / R, own_j = jj / R;
     if (tid < kb) {
       srow[tid] = cl.map_shared_rank(Pn, own_p)[(p - own_p * R) * kPs + tid];
       if (rank == own_p && p != jj) tmp[tid] = cl.map_shared_rank(Pn, own_j)[(jj - own_j * R) * kPs + tid];
     }
-    cl.sync();                               // all reads of the old rows are done
+    RBF_JITTER(); cl.sync();                               // all reads of the old rows are done
     if (tid < kb) {
       if (rank == own_j) Pn[(jj - rb) * kPs + tid] = srow[tid];
       if (rank == own_p && p != jj) Pn[(p - rb) * kPs + tid] = tmp[tid];
     }
     if (rank == 0 && tid == 0) piv[(int64_t)job * kNb + jj] = k0 + p;
-    __syncthreads();
+    RBF_SYNC();
     double pv = srow[jj];
     if (pv == 0.0) { singular = 1; pv = 1e-300; }
     const double inv = 1.0 / pv;
@@ -143,14 +149,14 @@ panel_cluster_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, in
         for (int c = jj + 2; c < kb; ++c) row[c] = fma(-l, srow[c], row[c]);
       }
     }
-    __syncthreads();
+    RBF_SYNC();
   }
   for (int q = tid; q < nl * kb; q += kThreads) {
     const int lr = q / kb, c = q % kb;
     A[(int64_t)(k0 + rb + lr) * ld + k0 + c] = Pn[lr * kPs + c];
   }
   if (singular && tid == 0) atomicAdd(info, 1);
-  cl.sync();                                 // keep DSMEM alive until all peers are done
+  RBF_JITTER(); cl.sync();                                 // keep DSMEM alive until all peers are done
 }
 
 // inv(L11) of every block after its panel (one CTA per block)
@@ -169,7 +175,7 @@ linv_kernel(const LuJob* __restrict__ jobs, const double* __restrict__ ws, int k
     const int r = q / kNb, c = q % kNb;
     sL[r * kLd + c] = (r < kb && c < kb) ? A[(int64_t)(k0 + r) * ld + k0 + c] : 0.0;
   }
-  __syncthreads();
+  RBF_SYNC();
   if (tid < kNb) {
     const int t = tid;
     for (int r = 0; r < kNb; ++r) {
@@ -184,7 +190,7 @@ linv_kernel(const LuJob* __restrict__ jobs, const double* __restrict__ ws, int k
       sI[r * kLd + t] = x;
     }
   }
-  __syncthreads();
+  RBF_SYNC();
   double* Li = linv + (int64_t)blockIdx.x * kNb * kNb;
   for (int q = tid; q < kNb * kNb; q += kThreads) Li[q] = sI[(q / kNb) * kLd + q % kNb];
 }
@@ -221,7 +227,7 @@ swap_trsm_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, int k0
   }
   const double* Li = linv + (int64_t)blockIdx.x * kNb * kNb;
   for (int q = tid; q < kNb * kNb; q += kThreads) sI[(q / kNb) * kLd + q % kNb] = Li[q];
-  __syncthreads();
+  RBF_SYNC();
   const int n = s_n;
   const int tx = tid & 15, ty = tid >> 4;
   for (int c0 = k0 + kb + kNb * blockIdx.y; c0 < ld; c0 += kNb * gridDim.y) {
@@ -231,17 +237,17 @@ swap_trsm_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, int k0
       const int i = q / kNb, c = q % kNb;
       if (c < cw) sT[i * kNb + c] = A[(int64_t)s_src[i] * ld + c0 + c];
     }
-    __syncthreads();
+    RBF_SYNC();
     for (int q = tid; q < n * kNb; q += kThreads) {
       const int i = q / kNb, c = q % kNb;
       if (c < cw && s_src[i] != s_rows[i]) A[(int64_t)s_rows[i] * ld + c0 + c] = sT[i * kNb + c];
     }
-    __syncthreads();
+    RBF_SYNC();
     for (int q = tid; q < kNb * kNb; q += kThreads) {
       const int r = q / kNb, c = q % kNb;
       sT[r * kLd + c] = (r < kb && c < cw) ? A[(int64_t)(k0 + r) * ld + c0 + c] : 0.0;
     }
-    __syncthreads();
+    RBF_SYNC();
     // U12 = inv(L11) * A12 : thread owns rows 4ty.., cols 4tx..
     double acc[4][4] = {};
     for (int t = 0; t < kb; ++t) {
@@ -263,7 +269,7 @@ swap_trsm_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, int k0
         if (c < cw) A[(int64_t)(k0 + r) * ld + c0 + c] = acc[q][p];
       }
     }
-    __syncthreads();
+    RBF_SYNC();
   }
 }
 
@@ -317,7 +323,7 @@ gemm_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, int k0, int
       const int c = tc + j;
       sB[t * kLd + j] = (c < cb1 && t < kb) ? A[(int64_t)(k0 + t) * ld + c] : 0.0;
     }
-    __syncthreads();
+    RBF_SYNC();
 #pragma unroll 4
     for (int kk = 0; kk < kNb / 4; ++kk) {
       double af[2], bf[4];
@@ -346,7 +352,7 @@ gemm_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, int k0, int
           if (c < cb1) row[c] = acc[mt][nt][i];
         }
     }
-    __syncthreads();
+    RBF_SYNC();
   }
 }
 
@@ -367,7 +373,7 @@ uinv_kernel(const LuJob* __restrict__ jobs, const double* __restrict__ ws, int k
     const int r = q / kNb, c = q % kNb;
     sU[r * kLd + c] = (r < kb && c < kb) ? A[(int64_t)(k0 + r) * ld + k0 + c] : (r == c ? 1.0 : 0.0);
   }
-  __syncthreads();
+  RBF_SYNC();
   if (tid < kNb) {
     // column t of inv(U): back substitution of U x = e_t
     const int t = tid;
@@ -384,7 +390,7 @@ uinv_kernel(const LuJob* __restrict__ jobs, const double* __restrict__ ws, int k
       sI[r * kLd + t] = x;
     }
   }
-  __syncthreads();
+  RBF_SYNC();
   double* Ui = uinv + (int64_t)blockIdx.x * kNb * kNb;
   for (int q = tid; q < kNb * kNb; q += kThreads) Ui[q] = sI[(q / kNb) * kLd + q % kNb];
 }
@@ -411,7 +417,7 @@ diag_solve_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, int k
       const int r = q / kNb, c = q % kNb;
       sY[r * kLd + c] = (r < kb && c < cw) ? A[(int64_t)(k0 + r) * ld + c0 + c] : 0.0;
     }
-    __syncthreads();
+    RBF_SYNC();
     double acc[4][4] = {};
     for (int t = 0; t < kb; ++t) {
       double a[4], b[4];
@@ -432,7 +438,7 @@ diag_solve_kernel(const LuJob* __restrict__ jobs, double* __restrict__ ws, int k
         if (c < cw) A[(int64_t)(k0 + r) * ld + c0 + c] = acc[q][p];
       }
     }
-    __syncthreads();
+    RBF_SYNC();
   }
 }
 
@@ -453,12 +459,12 @@ __global__ void transpose_w_kernel(const LuJob* __restrict__ jobs, const double*
       const int e = e0 + r, c = c0 + tx;
       t[r][tx] = (e < m && c < nc) ? A[(int64_t)e * ld + m + c] : 0.0;
     }
-    __syncthreads();
+    RBF_SYNC();
     for (int r = ty; r < 32; r += 8) {
       const int c = c0 + r, e = e0 + tx;
       if (c < nc && e < m) Wb[(int64_t)c * m + e] = (WT)t[tx][r];
     }
-    __syncthreads();
+    RBF_SYNC();
   }
 }
 

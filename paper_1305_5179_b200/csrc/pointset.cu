@@ -37,6 +37,11 @@ struct DCells {
   int dim[3];
 };
 
+}  // namespace
+// bounding box of n fp64 points on the device (RBF_EINVAL on a non-finite one)
+rbf_status data_bbox(rbf_ctx* ctx, const double* X, int64_t n, double mn[3], double mx[3]);
+namespace {
+
 // no contraction: the oracle forms lo + (i * step) with two roundings
 __device__ __forceinline__ double zcoord(const ZGrid& g, int a, int i) {
   return __dadd_rn(g.lo[a], __dmul_rn((double)i, g.step[a]));
@@ -78,12 +83,57 @@ __global__ void data_gather_kernel(const double* __restrict__ X, const int32_t* 
   }
 }
 
-// near[node] = exists data point p with sqrt(|node - p|^2) <= eps (fp64)
+// 4x4x4 node blocks within eps of some data point: one thread per non-empty data
+// cell marks the blocks whose box (fp64 node coordinates) lies within
+// eps (1 + 1e-9) of the cell's tight bounding box -- a superset of the blocks
+// holding a near node; near_kernel searches only those
+__global__ void near_blocks_kernel(ZGrid g, DCells dc, const int32_t* __restrict__ start,
+                                   const double* __restrict__ S, double eps, uint32_t* __restrict__ bflag) {
+  const int64_t ncell = (int64_t)dc.dim[0] * dc.dim[1] * dc.dim[2];
+  const int nb[3] = {(g.n[0] + 3) / 4, (g.n[1] + 3) / 4, (g.n[2] + 3) / 4};
+  const double e = eps * (1.0 + 1e-9);
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncell; c += (int64_t)gridDim.x * blockDim.x) {
+    const int s0 = start[c], s1 = start[c + 1];
+    if (s1 == s0) continue;
+    double lo3[3] = {INFINITY, INFINITY, INFINITY}, hi3[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int q = s0; q < s1; ++q)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) { lo3[a] = fmin(lo3[a], S[3 * q + a]); hi3[a] = fmax(hi3[a], S[3 * q + a]); }
+    int b0[3], b1[3];
+    bool none = false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      int i0 = (int)floor((lo3[a] - e - g.lo[a]) / g.step[a]) - 1, i1 = (int)ceil((hi3[a] + e - g.lo[a]) / g.step[a]) + 1;
+      i0 = max(i0, 0);
+      i1 = min(i1, g.n[a] - 1);
+      if (i0 > i1) none = true;
+      b0[a] = i0 >> 2;
+      b1[a] = i1 >> 2;
+    }
+    if (none) continue;
+    for (int bz = b0[2]; bz <= b1[2]; ++bz) {
+      const double gz = fmax(0.0, fmax(zcoord(g, 2, 4 * bz) - hi3[2], lo3[2] - zcoord(g, 2, min(4 * bz + 3, g.n[2] - 1))));
+      for (int by = b0[1]; by <= b1[1]; ++by) {
+        const double gy = fmax(0.0, fmax(zcoord(g, 1, 4 * by) - hi3[1], lo3[1] - zcoord(g, 1, min(4 * by + 3, g.n[1] - 1))));
+        if (gy * gy + gz * gz > e * e) continue;
+        for (int bx = b0[0]; bx <= b1[0]; ++bx) {
+          const double gx = fmax(0.0, fmax(zcoord(g, 0, 4 * bx) - hi3[0], lo3[0] - zcoord(g, 0, min(4 * bx + 3, g.n[0] - 1))));
+          if (gx * gx + gy * gy + gz * gz <= e * e) bflag[((int64_t)bz * nb[1] + by) * nb[0] + bx] = 1u;
+        }
+      }
+    }
+  }
+}
+
+// near[node] = exists data point p with sqrt(|node - p|^2) <= eps (fp64); nodes
+// of unmarked blocks (bflag) have no data point within eps: 0 without a search
 __global__ void near_kernel(ZGrid g, DCells dc, const int32_t* __restrict__ start, const double* __restrict__ S,
-                            double eps, uint8_t* __restrict__ near) {
+                            double eps, const uint32_t* __restrict__ bflag, uint8_t* __restrict__ near) {
   const int64_t nn = (int64_t)g.n[0] * g.n[1] * g.n[2];
+  const int nb0 = (g.n[0] + 3) / 4, nb1 = (g.n[1] + 3) / 4;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nn; v += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(v % g.n[0]), j = (int)((v / g.n[0]) % g.n[1]), k = (int)(v / ((int64_t)g.n[0] * g.n[1]));
+    if (!bflag[((int64_t)(k >> 2) * nb1 + (j >> 2)) * nb0 + (i >> 2)]) { near[v] = 0; continue; }
     const double p[3] = {zcoord(g, 0, i), zcoord(g, 1, j), zcoord(g, 2, k)};
     int c[3];
 #pragma unroll
@@ -167,18 +217,9 @@ rbf_status build_near_mask(rbf_ctx* ctx, const rbf_grid* grid, const double* dat
     RBF_CUDA_TRY(cudaMemsetAsync(near.p, 0, nn, s));
     return RBF_OK;
   }
-  // 1. data cells of edge h >= eps over the data bounding box (host bbox via a copy)
-  std::vector<double> hx(3 * (size_t)ndata);
-  RBF_CUDA_TRY(cudaMemcpyAsync(hx.data(), data, sizeof(double) * 3 * ndata, cudaMemcpyDeviceToHost, s));
-  RBF_CUDA_TRY(cudaStreamSynchronize(s));
-  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
-  for (int64_t i = 0; i < ndata; ++i)
-    for (int a = 0; a < 3; ++a) {
-      const double v = hx[3 * i + a];
-      if (!std::isfinite(v)) { set_error("non-finite data point"); return RBF_EINVAL; }
-      mn[a] = std::min(mn[a], v);
-      mx[a] = std::max(mx[a], v);
-    }
+  // 1. data cells of edge h >= eps over the data bounding box
+  double mn[3], mx[3];
+  RBF_TRY(data_bbox(ctx, data, ndata, mn, mx));
   double h = eps * (1.0 + 1e-6);
   DCells dc;
   int64_t ncell = 1;
@@ -211,9 +252,16 @@ rbf_status build_near_mask(rbf_ctx* ctx, const rbf_grid* grid, const double* dat
   RBF_TRY(S.alloc(sizeof(double) * 3 * ndata, s));
   data_gather_kernel<<<grid_for(ndata, 256), 256, 0, s>>>(data, v2.as<int32_t>(), ndata, S.as<double>());
   RBF_CHECK_LAUNCH();
-  // 2. the eps mask
+  // 2. the eps mask: candidate node blocks, then the per-node search inside them
+  const int64_t nbt = (int64_t)((g.n[0] + 3) / 4) * ((g.n[1] + 3) / 4) * ((g.n[2] + 3) / 4);
+  DevBuf bflag;
+  RBF_TRY(bflag.alloc(4 * nbt, s));
+  RBF_CUDA_TRY(cudaMemsetAsync(bflag.p, 0, 4 * nbt, s));
+  near_blocks_kernel<<<grid_for(ncell, 256), 256, 0, s>>>(g, dc, start.as<int32_t>(), S.as<double>(), eps,
+                                                          bflag.as<uint32_t>());
+  RBF_CHECK_LAUNCH();
   near_kernel<<<grid_for(nn, 256, 148 * 32), 256, 0, s>>>(g, dc, start.as<int32_t>(), S.as<double>(), eps,
-                                                          near.as<uint8_t>());
+                                                          bflag.as<uint32_t>(), near.as<uint8_t>());
   RBF_CHECK_LAUNCH();
   return RBF_OK;
 }
@@ -504,3 +552,23 @@ extern "C" rbf_status rbf_sigma_auto(rbf_ctx* ctx, const double* x, int64_t n, c
   *sigma = out6[rule == 9 ? 3 : (rule == 10 ? 4 : 5)];
   return RBF_OK;
 }
+
+namespace rbf {
+rbf_status data_bbox(rbf_ctx* ctx, const double* X, int64_t n, double mn[3], double mx[3]) {
+  cudaStream_t s = ctx->stream;
+  const int nbb = grid_for(n, 256, 148 * 4);
+  DevBuf part;
+  RBF_TRY(part.alloc(sizeof(double) * 7 * nbb, s));
+  bbox64_kernel<<<nbb, 256, 0, s>>>(X, n, part.as<double>());
+  RBF_CHECK_LAUNCH();
+  std::vector<double> hp(7 * (size_t)nbb);
+  RBF_CUDA_TRY(cudaMemcpyAsync(hp.data(), part.p, sizeof(double) * 7 * nbb, cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  for (int a = 0; a < 3; ++a) { mn[a] = INFINITY; mx[a] = -INFINITY; }
+  for (int b = 0; b < nbb; ++b) {
+    if (hp[7 * b + 6] != 0.0) { set_error("non-finite data point"); return RBF_EINVAL; }
+    for (int a = 0; a < 3; ++a) { mn[a] = std::min(mn[a], hp[7 * b + a]); mx[a] = std::max(mx[a], hp[7 * b + 3 + a]); }
+  }
+  return RBF_OK;
+}
+}  // namespace rbf

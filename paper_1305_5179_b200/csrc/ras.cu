@@ -375,6 +375,7 @@ gj_inverse_f32_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __rest
     const int64_t e0 = ext_ptr[blk];
     const int m = (int)(ext_ptr[blk + 1] - e0);
     const int nc = (int)(core_ptr[blk + 1] - core_ptr[blk]);
+    RBF_DCHECK(m <= MM);
     for (int i = tid; i < m; i += kGjThreads) pos[i] = sorted[ext_idx[e0 + i]];
     __syncthreads();
     float B[RM][RC];
@@ -450,6 +451,7 @@ gj_inverse_f32_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __rest
         const int cb = k & 1;
         const int kl = 16 * H + q;
         if constexpr (!PIV) {
+          RBF_JITTER();
           const float pv = rowbuf[cb][k];
           if (pv == 0.0f) singular = 1;
           const float d = __frcp_rn(pv);
@@ -488,6 +490,7 @@ gj_inverse_f32_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __rest
           continue;
         }
         // (1) every warp reduces the 16 per-warp candidates
+        RBF_JITTER();
         float ba = -1.0f, bv = 0.0f;
         int bi = 0x7fffffff;
         if (lane < 16) { ba = cand_a[cb][lane]; bv = cand_v[cb][lane]; bi = cand_i[cb][lane]; }
@@ -596,6 +599,163 @@ gj_inverse_f32_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __rest
           const int col = piv[j];
           if (!sym_out) Wb[(int64_t)(i - r0) * m + col] = B[a][b];
           else if (col <= i) Wb[tri_off(i) + col] = B[a][b];
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long d, pa, pb, pc;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(pa) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1,%2};" : "=l"(pb) : "f"(b.x), "f"(b.y));
+  asm("mov.b64 %0, {%1,%2};" : "=l"(pc) : "f"(c.x), "f"(c.y));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pa), "l"(pb), "l"(pc));
+  float2 r;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(d));
+  return r;
+}
+
+// Gauss-Jordan inversion of SPD blocks (shift >= kNoPivShift: no pivoting),
+// NW warps per block.  Row i of the MR x MR register tile belongs to warp
+// i % NW (register row i / NW), column j to lane j % 32 (register column
+// j / 32); rows are stored as float2 pairs (rows 2a', 2a'+1 of a warp) so the
+// rank-1 update is packed FFMA2.  Step k = NW a + q (a unrolled: compile-time
+// register indices; q = the owner warp, run time): every thread reads the
+// published column k (its warp's rows, contiguous, LDS.128) and row k, and
+// applies B[i][j] -= B[i][k] r_j with r_j = B[k][j] / p and r_k = 1 + 1/p --
+// the last makes the column-k update produce -B[i][k] / p, the Gauss-Jordan
+// column, without a fix-up pass; the owner warp then overwrites row k with r
+// (and 1/p on the diagonal).  One barrier per step: the owners of column k+1
+// and row k+1 publish them into the other buffer right after their update.
+template <int NW, int MR>
+__global__ void __launch_bounds__(32 * NW, 512 / (32 * NW))
+gj_spd_f32_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __restrict__ core_ptr,
+                  const int32_t* __restrict__ ext_idx, const int64_t* __restrict__ w_off,
+                  const float4* __restrict__ sorted, double amp, double two_s2, double c2, double shift_abs,
+                  float* __restrict__ W, const int64_t* __restrict__ blist, int64_t nlist, int* __restrict__ info,
+                  bool sym_out) {
+  constexpr int RW = MR / NW, RC = MR / 32, RP = RW / 2;
+  static_assert(MR % 32 == 0 && RW % 4 == 0 && 32 % NW == 0, "tile shape");
+  __shared__ __align__(16) float colbuf[2][MR];   // warp-major: [w * RW + a] = row NW a + w
+  __shared__ __align__(16) float rowbuf[2][MR];
+  __shared__ float4 pos[MR];
+  const int tid = threadIdx.x, lane = tid & 31, wr = tid >> 5;
+  for (int64_t t = blockIdx.x; t < nlist; t += gridDim.x) {
+    const int64_t blk = blist[t];
+    const int64_t e0 = ext_ptr[blk];
+    const int m = (int)(ext_ptr[blk + 1] - e0);
+    const int nc = (int)(core_ptr[blk + 1] - core_ptr[blk]);
+    RBF_DCHECK(m <= MR);
+    for (int i = tid; i < m; i += 32 * NW) pos[i] = sorted[ext_idx[e0 + i]];
+    __syncthreads();
+    float2 B[RP][RC];
+#pragma unroll
+    for (int a = 0; a < RW; ++a) {
+      const int i = NW * a + wr;
+#pragma unroll
+      for (int b = 0; b < RC; ++b) {
+        const int j = lane + 32 * b;
+        double v = 0.0;
+        if (i < m && j < m) {
+          const float4 pi4 = pos[i], pj4 = pos[j];
+          const double dx = (double)pi4.x - (double)pj4.x, dy = (double)pi4.y - (double)pj4.y,
+                       dz = (double)pi4.z - (double)pj4.z;
+          const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+          v = d2 <= c2 ? amp * exp(-d2 / two_s2) : 0.0;
+          if (i == j) v += shift_abs;
+        }
+        if (a & 1) B[a >> 1][b].y = (float)v;
+        else B[a >> 1][b].x = (float)v;
+      }
+    }
+    auto get = [&](int a, int b) -> float { return (a & 1) ? B[a >> 1][b].y : B[a >> 1][b].x; };
+    // publish column c (register column CB, owner lane c & 31) and row c (warp wq, register row AR)
+    auto pub = [&](auto cbt, auto art, int c, int wq, int buf) {
+      constexpr int CB = decltype(cbt)::value, AR = decltype(art)::value;
+      if (lane == (c & 31)) {
+#pragma unroll
+        for (int a4 = 0; a4 < RW / 4; ++a4) {
+          float4 v;
+          v.x = get(4 * a4, CB); v.y = get(4 * a4 + 1, CB); v.z = get(4 * a4 + 2, CB); v.w = get(4 * a4 + 3, CB);
+          *reinterpret_cast<float4*>(&colbuf[buf][wr * RW + 4 * a4]) = v;
+        }
+      }
+      if (wr == wq) {
+#pragma unroll
+        for (int b = 0; b < RC; ++b) rowbuf[buf][lane + 32 * b] = get(AR, b);
+      }
+    };
+    int singular = 0;
+    pub(std::integral_constant<int, 0>{}, std::integral_constant<int, 0>{}, 0, 0, 0);
+    __syncthreads();
+    [&]<int... As>(std::integer_sequence<int, As...>) {
+      bool done = false;
+      auto step_a = [&](auto at) {
+        constexpr int A = decltype(at)::value;
+        constexpr int KB = (NW * A) / 32;
+        if (done) return;
+        for (int q = 0; q < NW; ++q) {
+          const int k = NW * A + q;
+          if (k >= m) { done = true; return; }
+          const int cb = k & 1;
+          const int kl = k & 31;
+          RBF_JITTER();
+          const float pv = rowbuf[cb][k];
+          if (pv == 0.0f) singular = 1;
+          const float d = __frcp_rn(pv);
+          float nr[RC];
+#pragma unroll
+          for (int b = 0; b < RC; ++b) nr[b] = -(rowbuf[cb][lane + 32 * b] * d);
+          if (lane == kl) nr[KB] = -(1.0f + d);
+          float2 fa[RP];
+#pragma unroll
+          for (int a4 = 0; a4 < RW / 4; ++a4) {
+            const float4 v = *reinterpret_cast<const float4*>(&colbuf[cb][wr * RW + 4 * a4]);
+            fa[2 * a4] = make_float2(v.x, v.y);
+            fa[2 * a4 + 1] = make_float2(v.z, v.w);
+          }
+#pragma unroll
+          for (int ap = 0; ap < RP; ++ap)
+#pragma unroll
+            for (int b = 0; b < RC; ++b) B[ap][b] = fma2(fa[ap], make_float2(nr[b], nr[b]), B[ap][b]);
+          if (wr == q) {
+#pragma unroll
+            for (int b = 0; b < RC; ++b) {
+              const float v = (b == KB && lane == kl) ? d : -nr[b];
+              if (A & 1) B[A >> 1][b].y = v;
+              else B[A >> 1][b].x = v;
+            }
+          }
+          if (k + 1 < m) {
+            if (q + 1 < NW) {
+              pub(std::integral_constant<int, KB>{}, std::integral_constant<int, A>{}, k + 1, q + 1, cb ^ 1);
+            } else if constexpr (A + 1 < RW) {
+              pub(std::integral_constant<int, (NW * (A + 1)) / 32>{}, std::integral_constant<int, A + 1>{}, k + 1, 0,
+                  cb ^ 1);
+            }
+          }
+          __syncthreads();
+        }
+      };
+      (step_a(std::integral_constant<int, As>{}), ...);
+    }(std::make_integer_sequence<int, RW>{});
+    if (tid == 0 && singular) atomicAdd(info, 1);
+    // W = B^-1 (no row swaps): core rows i >= m - nc; sym_out (block-Jacobi, nc = m):
+    // only the lower triangle, packed by rows
+    float* Wb = W + w_off[blk];
+    const int r0 = m - nc;
+#pragma unroll
+    for (int a = 0; a < RW; ++a) {
+      const int i = NW * a + wr;
+      if (i < r0 || i >= m) continue;
+#pragma unroll
+      for (int b = 0; b < RC; ++b) {
+        const int j = lane + 32 * b;
+        if (j < m) {
+          if (!sym_out) Wb[(int64_t)(i - r0) * m + j] = get(a, b);
+          else if (j <= i) Wb[tri_off(i) + j] = get(a, b);
         }
       }
     }
@@ -742,7 +902,9 @@ apply_sym_kernel(const int64_t* __restrict__ ext_ptr, const int32_t* __restrict_
     const bool staged = (w_off[b + 1] - w0) <= cap_floats;
     for (int e = tid; e < m; e += blockDim.x) xs[e] = (float)r[ext_idx[e0 + e]];
     for (int e = m + tid; e < ((m + 3) & ~3); e += blockDim.x) xs[e] = 0.f;
+    RBF_JITTER();
     __syncthreads();
+    RBF_JITTER();
     if (staged) {
       const uint32_t ba = (uint32_t)__cvta_generic_to_shared(&bar[st]);
       uint32_t done = 0;
@@ -1095,13 +1257,31 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
           RBF_CHECK_LAUNCH();
           return RBF_OK;
         };
-#define RBF_GJ_LAUNCH(RM_, RC_) \
-  RBF_TRY(nopiv ? launch(gj_inverse_f32_kernel<RM_, RC_, false>) : launch(gj_inverse_f32_kernel<RM_, RC_, true>))
-        if (bin == 0) RBF_GJ_LAUNCH(4, 2);
-        else if (bin == 1) RBF_GJ_LAUNCH(6, 3);
-        else if (bin == 2) RBF_GJ_LAUNCH(8, 4);
-        else if (bin == 3) RBF_GJ_LAUNCH(12, 6);
-        else RBF_GJ_LAUNCH(14, 7);
+        // SPD (no pivoting): few-warp register tiles, more blocks per SM
+        auto launch_spd = [&](auto kern, int threads) -> rbf_status {
+          int per_sm = 1;
+          RBF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0));
+          const int gblocks = (int)std::min<int64_t>(cnt, (int64_t)ctx->sm_count * std::max(per_sm, 1));
+          kern<<<gblocks, threads, 0, s>>>(P->ext_ptr.as<int64_t>(), P->core_ptr.as<int64_t>(),
+                                           P->ext_idx.as<int32_t>(), P->w_off.as<int64_t>(), sortedw, kp.amp, two_s2,
+                                           c2, shift_abs, P->W.as<float>(), bl, cnt, info.as<int>(), P->w_sym);
+          RBF_CHECK_LAUNCH();
+          return RBF_OK;
+        };
+#define RBF_GJ_LAUNCH(RM_, RC_) RBF_TRY(launch(gj_inverse_f32_kernel<RM_, RC_, true>))
+        if (nopiv) {
+          if (bin == 0) RBF_TRY(launch_spd(gj_spd_f32_kernel<4, 64>, 128));
+          else if (bin == 1) RBF_TRY(launch_spd(gj_spd_f32_kernel<4, 96>, 128));
+          else if (bin == 2) RBF_TRY(launch_spd(gj_spd_f32_kernel<8, 128>, 256));
+          else if (bin == 3) RBF_TRY(launch_spd(gj_spd_f32_kernel<16, 192>, 512));
+          else RBF_TRY(launch(gj_inverse_f32_kernel<14, 7, false>));
+        } else {
+          if (bin == 0) RBF_GJ_LAUNCH(4, 2);
+          else if (bin == 1) RBF_GJ_LAUNCH(6, 3);
+          else if (bin == 2) RBF_GJ_LAUNCH(8, 4);
+          else if (bin == 3) RBF_GJ_LAUNCH(12, 6);
+          else RBF_GJ_LAUNCH(14, 7);
+        }
 #undef RBF_GJ_LAUNCH
       }
       lo = hi;

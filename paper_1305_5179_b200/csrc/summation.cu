@@ -134,6 +134,8 @@ __device__ __forceinline__ void traverse(const SumGeom& G, const int32_t* __rest
         bool keep = load(j, j < se);  // loads + culls into registers
         unsigned bal = __ballot_sync(0xffffffffu, keep);
         int pos = nbuf + __popc(bal & lt);
+        RBF_JITTER();
+        RBF_DCHECK(!keep || pos < kBufPad);
         load.store(keep, pos);
         nbuf += __popc(bal);
         if (nbuf >= kFlush) {
@@ -187,6 +189,8 @@ __device__ __forceinline__ void traverse2(const SumGeom& G, const int32_t* __res
         const int kind = load.classify(j, j < se);
         const unsigned bi = __ballot_sync(0xffffffffu, kind == 2);
         const unsigned bb = __ballot_sync(0xffffffffu, kind == 1);
+        RBF_JITTER();
+        RBF_DCHECK(nB + __popc(bb & lt) < kBufPad && nI + __popc(bi & lt) < kBufPad);
         load.store2(kind, nB + __popc(bb & lt), nI + __popc(bi & lt));
         nB += __popc(bb);
         nI += __popc(bi);
@@ -1078,6 +1082,8 @@ __device__ __forceinline__ void symb_tile(const SumGeom& G, const int32_t* __res
 #define RBF_SYMB_HALF 1   // 3.138 vs 3.153 ms at c4 (fewer live registers)
 #endif
   auto flush_sym = [&](int cnt) {   // cnt: multiple of 4
+    RBF_JITTER();
+    RBF_DCHECK(cnt <= kSymPad && (cnt & 3) == 0);
     RBF_UNROLL(RBF_SYMB_UNROLL)
     for (int j = 0; j < cnt; j += 4) {
       float2 pa = make_float2(0.f, 0.f), pb = make_float2(0.f, 0.f);
@@ -1139,6 +1145,7 @@ __device__ __forceinline__ void symb_tile(const SumGeom& G, const int32_t* __res
     }
     // the ring's source-side sums to f_j: one atomic per source, 32 lanes at a time
     __syncwarp();
+    RBF_JITTER();
     for (int q = lane; q < cnt; q += 32) {
       const int jj = RI[q];
       if (jj >= 0) atomicAdd(out + jj, (OutT)(amp * KB[q]));
@@ -1199,15 +1206,18 @@ __device__ __forceinline__ void symb_tile(const SumGeom& G, const int32_t* __res
         const bool own = j < t_end;
         const unsigned bs = __ballot_sync(0xffffffffu, keep && !own);
         const unsigned bo = __ballot_sync(0xffffffffu, keep && own);
+        RBF_JITTER();
         if (keep) {
           const float sx = (p.x - ctr.x) * G.s, sy = (p.y - ctr.y) * G.s, sz = (p.z - ctr.z) * G.s;
           const float ss = fmaf(sz, sz, fmaf(sy, sy, sx * sx));
           if (!own) {
             const int pos = nS + __popc(bs & lt);
+            RBF_DCHECK(pos < kSymPad);
             RS[0][pos] = sx; RS[1][pos] = sy; RS[2][pos] = sz; RS[3][pos] = ss; RS[4][pos] = p.w;
             RI[pos] = j;
           } else {
             const int pos = nO + __popc(bo & lt);
+            RBF_DCHECK(pos < kOwnPad);
             O[0][pos] = sx; O[1][pos] = sy; O[2][pos] = sz; O[3][pos] = ss; O[4][pos] = p.w;
           }
         }
@@ -1688,25 +1698,33 @@ int sym_mode(int op, int64_t n_loc) {
   }
 }
 
-// Persistent grid: as many CTAs as can be resident (the kernels pull tiles from a
-// work counter, so CTAs beyond one wave would only add tail imbalance).
-// Node blocks (4x4x4 grid nodes) within the culling radius cc of a non-empty
-// cell, in block layers [bz0, bz1): the grid evaluation visits only those (the
-// others hold no centre within the cutoff of any node: exact zeros, written by a
-// memset).  Conservative by one node per side against the rounding of the
-// node coordinates.
-__global__ void mark_node_blocks(const int32_t* __restrict__ cell_start, CellGrid g, float cc, GridDesc gd,
-                                 int bz0, int bz1, uint32_t* __restrict__ flag) {
+// Node blocks (4x4x4 grid nodes) in block layers [bz0, bz1) that hold a node
+// within the culling radius cc of some centre: the grid evaluation visits only
+// those (every other node has no centre within the cutoff: an exact zero,
+// written by a memset).  One thread per non-empty cell: the tight bounding box
+// of the cell's centres, the candidate blocks within cc of it per axis, and for
+// each candidate the box-to-box distance (fp64) against cc (1 + 1e-6) -- the
+// block box is the kernel's own (fp32 node coordinates), so a block whose nodes
+// the kernel could give a non-zero value is never skipped.
+__global__ void mark_node_blocks(const int32_t* __restrict__ cell_start, const float4* __restrict__ sorted,
+                                 CellGrid g, float cc, GridDesc gd, int bz0, int bz1, uint32_t* __restrict__ flag) {
   const int64_t ncell = (int64_t)g.dim[0] * g.dim[1] * g.dim[2];
+  const double ccd = (double)cc * (1.0 + 1e-6);
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncell; c += (int64_t)gridDim.x * blockDim.x) {
-    if (cell_start[c + 1] == cell_start[c]) continue;
-    const int ci[3] = {(int)(c % g.dim[0]), (int)((c / g.dim[0]) % g.dim[1]), (int)(c / ((int64_t)g.dim[0] * g.dim[1]))};
+    const int s0 = cell_start[c], s1 = cell_start[c + 1];
+    if (s1 == s0) continue;
+    float lo3[3] = {INFINITY, INFINITY, INFINITY}, hi3[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int q = s0; q < s1; ++q) {
+      const float4 p = sorted[q];
+      lo3[0] = fminf(lo3[0], p.x); hi3[0] = fmaxf(hi3[0], p.x);
+      lo3[1] = fminf(lo3[1], p.y); hi3[1] = fmaxf(hi3[1], p.y);
+      lo3[2] = fminf(lo3[2], p.z); hi3[2] = fmaxf(hi3[2], p.z);
+    }
     int b0[3], b1[3];
     bool empty = false;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      const double lo = (double)g.lo[a] + (double)ci[a] * (double)g.h - (double)cc;
-      const double hi = (double)g.lo[a] + (double)(ci[a] + 1) * (double)g.h + (double)cc;
+      const double lo = (double)lo3[a] - ccd, hi = (double)hi3[a] + ccd;
       int i0 = (int)floor((lo - gd.lo[a]) / gd.step[a]) - 1, i1 = (int)ceil((hi - gd.lo[a]) / gd.step[a]) + 1;
       i0 = max(i0, 0);
       i1 = min(i1, gd.n[a] - 1);
@@ -1717,10 +1735,20 @@ __global__ void mark_node_blocks(const int32_t* __restrict__ cell_start, CellGri
     b0[2] = max(b0[2], bz0);
     b1[2] = min(b1[2], bz1 - 1);
     if (empty || b0[2] > b1[2]) continue;
-    for (int bz = b0[2]; bz <= b1[2]; ++bz)
-      for (int by = b0[1]; by <= b1[1]; ++by)
-        for (int bx = b0[0]; bx <= b1[0]; ++bx)
-          flag[((int64_t)bz * gd.nb[1] + by) * gd.nb[0] + bx] = 1u;
+    for (int bz = b0[2]; bz <= b1[2]; ++bz) {
+      const double gz = fmax(0.0, fmax((double)node_coord(gd, 2, 4 * bz) - hi3[2],
+                                       (double)lo3[2] - (double)node_coord(gd, 2, min(4 * bz + 3, gd.n[2] - 1))));
+      for (int by = b0[1]; by <= b1[1]; ++by) {
+        const double gy = fmax(0.0, fmax((double)node_coord(gd, 1, 4 * by) - hi3[1],
+                                         (double)lo3[1] - (double)node_coord(gd, 1, min(4 * by + 3, gd.n[1] - 1))));
+        if (gy * gy + gz * gz > ccd * ccd) continue;
+        for (int bx = b0[0]; bx <= b1[0]; ++bx) {
+          const double gx = fmax(0.0, fmax((double)node_coord(gd, 0, 4 * bx) - hi3[0],
+                                           (double)lo3[0] - (double)node_coord(gd, 0, min(4 * bx + 3, gd.n[0] - 1))));
+          if (gx * gx + gy * gy + gz * gz <= ccd * ccd) flag[((int64_t)bz * gd.nb[1] + by) * gd.nb[0] + bx] = 1u;
+        }
+      }
+    }
   }
 }
 
@@ -1743,6 +1771,8 @@ __global__ void compact_blocks(const uint32_t* __restrict__ flag, const uint32_t
     if (flag[b]) list[pos[b]] = (int32_t)b;
 }
 
+// Persistent grid: as many CTAs as can be resident (the kernels pull tiles from a
+// work counter, so CTAs beyond one wave would only add tail imbalance).
 template <class K>
 int sum_blocks(rbf_ctx* ctx, K kernel) {
   int per_sm = 0;
@@ -2037,7 +2067,8 @@ rbf_status eval_grid_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams
     mark_near_blocks<<<grid_for(nn, 256), 256, 0, s>>>(near, gd, (int)(b0 / per_layer), (int)(b1 / per_layer),
                                                        flag.as<uint32_t>());
   } else {
-    mark_node_blocks<<<grid_for(ncell, 256), 256, 0, s>>>(c->cell_start.as<int32_t>(), G.g, G.cc, gd,
+    mark_node_blocks<<<grid_for(ncell, 256), 256, 0, s>>>(c->cell_start.as<int32_t>(), c->sorted.as<float4>(), G.g,
+                                                           G.cc, gd,
                                                            (int)(b0 / per_layer), (int)(b1 / per_layer),
                                                            flag.as<uint32_t>());
   }

@@ -88,7 +88,7 @@ def test_mesh_from_field_matches_oracle(R, ctx):
     """Analytic fields (torus, tilted plane, a random field for every tet case),
     mask from a few data points with a partial cover."""
     rng = np.random.default_rng(5)
-    lo, hi, gn = (-1.5, -1.4, -0.7), (1.5, 1.3, 0.8), (29, 23, 17)
+    lo, hi, gn = (-1.5, -1.45, -0.7), (1.5, 1.45, 0.8), (29, 25, 17)
     P = OG.nodes(lo, hi, gn)
     fields = {
         "torus": np.hypot(np.hypot(P[:, 0], P[:, 1]) - 1.0, P[:, 2]) - 0.35,

@@ -130,7 +130,7 @@ def _flat_cap(ratio=3.0, n_sphere=6000, zcut=0.55):
     return X, b, sigma
 
 
-@pytest.mark.parametrize("core,pivot,full", [(128, False, False), (256, False, False), (128, True, False),
+@pytest.mark.parametrize("core,pivot,full", [(48, False, False), (128, False, False), (256, False, False), (128, True, False),
                                              (256, False, True)])
 def test_gj_fp32_apply_parity(R, ctx, core, pivot, full):
     """Reading R17, on-chip fp32 Gauss-Jordan factors (local_fp32=1) against the
