@@ -408,7 +408,9 @@ def run_ours(args, rank, world, local):
                                f"grid {gn[0]}^3",
                    "centres_per_gpu": 3 * cfg.n // world if slab else 3 * cfg.n,
                    "global_centres": 3 * cfg.n if slab else 3 * cfg.n * world,
-                   "parallelism": (f"slab x{world} (z cell planes, halo send/recv + allreduce over NCCL)" if slab
+                   "parallelism": (f"slab x{world} (z cell planes, halo send/recv + allreduce over NCCL; "
+                                   "experimental: this code path is verified on one GPU through the loopback "
+                                   "transport, its NCCL form has not run on a multi-GPU box in this work)" if slab
                                    else f"replicas x{world} (independent seeded instances)"),
                    "l2": "working set >> 126 MB L2 (block inverses 0.5 GB, Krylov basis 1.2 GB, cells + vectors 0.2 GB); no explicit flush"},
         "e2e": e2e, "gpu_launches": None, "clocks": clk, "roofline": roofline, "cpu_baseline": cpu,

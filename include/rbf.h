@@ -262,9 +262,12 @@ rbf_status rbf_build_cells(rbf_ctx* ctx, const float* xyz, int64_t n,
                            rbf_cells** out);
 void rbf_cells_free(rbf_cells* cells);
 rbf_status rbf_cells_info(const rbf_cells* cells, rbf_cells_desc* out /* host */);
-/* This rank's slab (HOST out[8]): owned sorted range [out[0], out[1]), matvec
+/* This rank's slab (HOST out[11]): owned sorted range [out[0], out[1]), matvec
  * source window [out[2], out[3]), target tiles [out[4], out[5]), z cell planes
- * [out[6], out[7]).  Single GPU: everything. */
+ * [out[6], out[7]), tiles of the wide (symmetric) plan [out[8], out[9]), of which
+ * the first out[10] are interior: their traversal stays inside the slab, so the
+ * symmetric fp32 operator runs them while the halo is exchanged on a second
+ * stream (world > 1; 0 on one GPU).  Single GPU: everything. */
 rbf_status rbf_cells_slab(const rbf_cells* cells, int64_t* out);
 /* Library-owned DEVICE arrays, valid until rbf_cells_free:
  *   perm[n]           sorted position -> caller index (stable by key)

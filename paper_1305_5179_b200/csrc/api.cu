@@ -268,8 +268,8 @@ rbf_status rbf_cells_info(const rbf_cells* c, rbf_cells_desc* d) {
 rbf_status rbf_cells_slab(const rbf_cells* c, int64_t* out) {
   if (!c || !out) { set_error("NULL argument"); return RBF_EINVAL; }
   const SlabView& V = c->view;
-  const int64_t v[8] = {V.o0, V.o1, V.h0, V.h1, V.t0, V.t1, V.p0, V.p1};
-  std::copy(v, v + 8, out);
+  const int64_t v[11] = {V.o0, V.o1, V.h0, V.h1, V.t0, V.t1, V.p0, V.p1, V.tw0, V.tw1, c->world > 1 ? V.tw_int : 0};
+  std::copy(v, v + 11, out);
   return RBF_OK;
 }
 

@@ -335,6 +335,9 @@ rbf_status dist_plan_cells(rbf_ctx* ctx, rbf_cells* c, const std::vector<uint32_
   };
   V.tw0 = row_tiles_w(V.p0);
   V.tw1 = row_tiles_w(V.p1);
+  // interior wide tiles: planes below p1 - (reach + 1) read sources of this slab only
+  const int pint = std::max(V.p0, V.p1 - (c->reach + 1));
+  V.tw_int = std::min(row_tiles_w(pint), V.tw1) - V.tw0;
   return RBF_OK;
 }
 

@@ -102,7 +102,8 @@ struct rbf_prof_rec {
 struct rbf_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  cudaStream_t aux_stream = nullptr;   // library-owned second stream (RAS factorisation overlap)
+  cudaStream_t aux_stream = nullptr;   // library-owned second stream (RAS factorisation overlap, halo exchange)
+  cudaEvent_t halo_ev[2] = {nullptr, nullptr};   // fork / join of the halo exchange on aux_stream
   int sm_count = 148;
   bool prof = false;
   std::vector<rbf_prof_rec> prof_recs;
@@ -121,6 +122,8 @@ struct rbf_ctx {
     for (auto& r : prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : ev_pool) cudaEventDestroy(e);
     if (aux_stream) cudaStreamDestroy(aux_stream);
+    for (auto e : halo_ev)
+      if (e) cudaEventDestroy(e);
     if (hpin) cudaFreeHost(hpin);
   }
   rbf::DevBuf scratch;       // generic scratch (radix sort, scans)
@@ -160,6 +163,9 @@ struct SlabView {
   int64_t t0 = 0, t1 = 0;
   int p0 = 0, p1 = 0;
   int64_t tw0 = 0, tw1 = 0;   // tiles of the wide plan
+  // wide tiles [tw0, tw0 + tw_int) lie in planes whose traversal stays inside the
+  // slab (p < p1 - reach - 1): they need no halo, so they run while it arrives
+  int64_t tw_int = 0;
 };
 // Every rank's slab (identical on all ranks: computed from the replicated cells).
 struct SlabPlan {

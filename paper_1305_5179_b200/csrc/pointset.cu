@@ -131,6 +131,7 @@ __global__ void near_kernel(ZGrid g, DCells dc, const int32_t* __restrict__ star
                             double eps, const uint32_t* __restrict__ bflag, uint8_t* __restrict__ near) {
   const int64_t nn = (int64_t)g.n[0] * g.n[1] * g.n[2];
   const int nb0 = (g.n[0] + 3) / 4, nb1 = (g.n[1] + 3) / 4;
+  const double e2_lo = eps * eps * (1.0 - 1e-12), e2_hi = eps * eps * (1.0 + 1e-12);
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nn; v += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(v % g.n[0]), j = (int)((v / g.n[0]) % g.n[1]), k = (int)(v / ((int64_t)g.n[0] * g.n[1]));
     if (!bflag[((int64_t)(k >> 2) * nb1 + (j >> 2)) * nb0 + (i >> 2)]) { near[v] = 0; continue; }
@@ -149,7 +150,10 @@ __global__ void near_kernel(ZGrid g, DCells dc, const int32_t* __restrict__ star
           const double dx = __dsub_rn(p[0], S[3 * q]), dy = __dsub_rn(p[1], S[3 * q + 1]),
                        dz = __dsub_rn(p[2], S[3 * q + 2]);
           const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-          if (__dsqrt_rn(d2) <= eps) { hit = true; break; }
+          // sqrt_rn(d2) <= eps decided without the sqrt away from the boundary:
+          // d2 < eps^2 (1 - 1e-12) implies it, d2 > eps^2 (1 + 1e-12) excludes it
+          if (d2 > e2_hi) continue;
+          if (d2 < e2_lo || __dsqrt_rn(d2) <= eps) { hit = true; break; }
         }
       }
     near[v] = hit ? 1 : 0;

@@ -629,6 +629,15 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
 // column, without a fix-up pass; the owner warp then overwrites row k with r
 // (and 1/p on the diagonal).  One barrier per step: the owners of column k+1
 // and row k+1 publish them into the other buffer right after their update.
+#ifndef RBF_GJ64_NW
+#define RBF_GJ64_NW 4
+#endif
+#ifndef RBF_GJ96_NW
+#define RBF_GJ96_NW 4
+#endif
+#ifndef RBF_GJ128_NW
+#define RBF_GJ128_NW 8
+#endif
 template <int NW, int MR>
 __global__ void __launch_bounds__(32 * NW, 512 / (32 * NW))
 gj_spd_f32_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __restrict__ core_ptr,
@@ -1270,9 +1279,9 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
         };
 #define RBF_GJ_LAUNCH(RM_, RC_) RBF_TRY(launch(gj_inverse_f32_kernel<RM_, RC_, true>))
         if (nopiv) {
-          if (bin == 0) RBF_TRY(launch_spd(gj_spd_f32_kernel<4, 64>, 128));
-          else if (bin == 1) RBF_TRY(launch_spd(gj_spd_f32_kernel<4, 96>, 128));
-          else if (bin == 2) RBF_TRY(launch_spd(gj_spd_f32_kernel<8, 128>, 256));
+          if (bin == 0) RBF_TRY(launch_spd(gj_spd_f32_kernel<RBF_GJ64_NW, 64>, 32 * RBF_GJ64_NW));
+          else if (bin == 1) RBF_TRY(launch_spd(gj_spd_f32_kernel<RBF_GJ96_NW, 96>, 32 * RBF_GJ96_NW));
+          else if (bin == 2) RBF_TRY(launch_spd(gj_spd_f32_kernel<RBF_GJ128_NW, 128>, 32 * RBF_GJ128_NW));
           else if (bin == 3) RBF_TRY(launch_spd(gj_spd_f32_kernel<16, 192>, 512));
           else RBF_TRY(launch(gj_inverse_f32_kernel<14, 7, false>));
         } else {

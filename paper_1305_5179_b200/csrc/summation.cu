@@ -1051,6 +1051,10 @@ sum_f32_symr_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const flo
 // access on the kernel's own shared arrays (no generic-pointer address math).
 constexpr int kSymPad = 136;   // SoA ring row (>= kFlush + 32 + 4, multiple of 4)
 
+#ifndef RBF_SYMB_KBSTORE
+#define RBF_SYMB_KBSTORE 1
+#endif
+
 template <int T, class OutT>
 __device__ __forceinline__ void symb_tile(const SumGeom& G, const int32_t* __restrict__ cell_start,
                                           const float4* __restrict__ src, float3 blo, float3 bhi, float3 ctr,
@@ -1074,6 +1078,17 @@ __device__ __forceinline__ void symb_tile(const SumGeom& G, const int32_t* __res
   const int t_end = tl.x + tl.y;
   const bool h4 = lane & 16, h3 = lane & 8;
   const int mys = (h4 ? 2 : 0) + (h3 ? 1 : 0);
+  // the source-side sum of source j + mys lands in KB[j + mys] (lanes 0, 8, 16,
+  // 24); the other lanes store into private dummy slots KB[kSymPad + lane], so
+  // the store is one unpredicated STS (no divergent branch).  The shared address
+  // is formed once and pinned in a register (an opaque asm), so the compiler
+  // does not rematerialise it from SR_TID in the loop.
+#if RBF_SYMB_KBSTORE
+  uint32_t kb_addr = (uint32_t)__cvta_generic_to_shared(KB) +
+                     4u * (uint32_t)(((lane & 7) == 0) ? mys : kSymPad + lane);
+  asm volatile("" : "+r"(kb_addr));
+  const uint32_t kb_step = ((lane & 7) == 0) ? 16u : 0u;   // bytes per group of 4 sources
+#endif
   // symmetric ring RS[0..4] = x', y', z', |s'|^2, w and RI = sorted index
 #ifndef RBF_SYMB_UNROLL
 #define RBF_SYMB_UNROLL 1
@@ -1141,7 +1156,11 @@ __device__ __forceinline__ void symb_tile(const SumGeom& G, const int32_t* __res
       k += __shfl_xor_sync(0xffffffffu, k, 4);
       k += __shfl_xor_sync(0xffffffffu, k, 2);
       k += __shfl_xor_sync(0xffffffffu, k, 1);
+#if RBF_SYMB_KBSTORE
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(kb_addr + kb_step * (uint32_t)(j >> 2)), "f"(k) : "memory");
+#else
       if ((lane & 7) == 0) KB[j + mys] = k;
+#endif
     }
     // the ring's source-side sums to f_j: one atomic per source, 32 lanes at a time
     __syncwarp();
@@ -1283,7 +1302,7 @@ sum_f32_symb_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const flo
                     const int32_t* __restrict__ order) {
   __shared__ __align__(16) float rings[kSumWarps][5][kSymPad];
   __shared__ int ringi[kSumWarps][kSymPad];
-  __shared__ float ringk[kSumWarps][kSymPad];
+  __shared__ float ringk[kSumWarps][kSymPad + 32];   // + the dummy store slots of flush_sym
   __shared__ __align__(16) float ringo[kSumWarps][5][kOwnPad];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   for (;;) {
@@ -1860,8 +1879,17 @@ rbf_status order_wide_tiles(rbf_ctx* ctx, rbf_cells* c, const KernelParams& kp) 
                                                           c->tile_box_w.as<float4>(), V.tw0, nt, V.h1,
                                                           k1.as<uint32_t>(), v1.as<int32_t>());
   RBF_CHECK_LAUNCH();
-  return radix_sort_pairs<uint32_t>(ctx, k1.as<uint32_t>(), v1.as<int32_t>(), k2.as<uint32_t>(),
-                                    c->order_w.as<int32_t>(), nt, 32);
+  // slab partition: the interior tiles [0, tw_int) and the halo tiles are
+  // launched separately (the halo arrives in between), so each part is ordered
+  // on its own; one GPU: tw_int = 0 and the whole range is one part
+  const int64_t ni = (ctx->world > 1) ? V.tw_int : 0;
+  if (ni > 0)
+    RBF_TRY(radix_sort_pairs<uint32_t>(ctx, k1.as<uint32_t>(), v1.as<int32_t>(), k2.as<uint32_t>(),
+                                       c->order_w.as<int32_t>(), ni, 32));
+  if (nt > ni)
+    RBF_TRY(radix_sort_pairs<uint32_t>(ctx, k1.as<uint32_t>() + ni, v1.as<int32_t>() + ni, k2.as<uint32_t>() + ni,
+                                       c->order_w.as<int32_t>() + ni, nt - ni, 32));
+  return RBF_OK;
 }
 
 // Public fp32 path (and the pair accounting): w_sorted covers all n centres
@@ -1916,10 +1944,78 @@ static rbf_status matvec_f32_solver(rbf_ctx* ctx, const rbf_cells* c, const Kern
   const int64_t base = sym ? V.o0 : V.h0;
   const int64_t nw = V.h1 - base;
   const WT* w_win = w_loc;
-  if (ctx->world > 1) {
+  // slab partition, wide symmetric operator: the upper halo is exchanged and
+  // packed on the aux stream while the interior tiles (no halo sources) run
+  const bool overlap = ctx->world > 1 && sym >= 2 && V.tw_int > 0 && c->order_w.p;
+  if (ctx->world > 1 && !overlap) {
     RBF_TRY(ctx->win.ensure(sizeof(WT) * std::max<int64_t>(nw, 1), s));
     RBF_TRY(halo_exchange<WT>(ctx, c, w_loc, ctx->win.as<WT>(), sym != 0));
     w_win = ctx->win.as<WT>();
+  }
+  if (overlap) {
+    RBF_TRY(ctx->win.ensure(sizeof(WT) * std::max<int64_t>(nw, 1), s));
+    RBF_TRY(ctx->src4.ensure(sizeof(float4) * std::max<int64_t>(nw, 1), s));
+    RBF_TRY(ctx->counter.ensure(256, s));
+    if (!ctx->aux_stream) RBF_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
+    for (auto& e : ctx->halo_ev)
+      if (!e) RBF_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaStream_t a = ctx->aux_stream;
+    const int64_t no = V.o1 - V.o0;
+    // fork: the halo (and its packing) on the aux stream once w_loc is ready
+    RBF_CUDA_TRY(cudaEventRecord(ctx->halo_ev[0], s));
+    RBF_CUDA_TRY(cudaStreamWaitEvent(a, ctx->halo_ev[0], 0));
+    {
+      cudaStream_t keep = ctx->stream;
+      ctx->stream = a;   // the transport and the pack run on the aux stream
+      rbf_status st = halo_exchange<WT>(ctx, c, w_loc, ctx->win.as<WT>(), true);
+      if (st == RBF_OK && nw > no) {
+        if constexpr (std::is_same<WT, double>::value)
+          pack_src_f64w<<<grid_for(nw - no, 256), 256, 0, a>>>(c->sorted.as<float4>() + V.o1, ctx->win.as<WT>() + no,
+                                                              nw - no, ctx->src4.as<float4>() + no);
+        else
+          pack_src_f32<<<grid_for(nw - no, 256), 256, 0, a>>>(c->sorted.as<float4>() + V.o1, ctx->win.as<WT>() + no,
+                                                             nw - no, ctx->src4.as<float4>() + no);
+        count_launch();
+        if (cudaGetLastError() != cudaSuccess) st = RBF_ECUDA;
+      }
+      ctx->stream = keep;
+      RBF_TRY(st);
+    }
+    RBF_CUDA_TRY(cudaEventRecord(ctx->halo_ev[1], a));
+    // the own slice on the main stream, the interior tiles while the halo arrives
+    if (no > 0) {
+      if constexpr (std::is_same<WT, double>::value)
+        pack_src_f64w<<<grid_for(no, 256), 256, 0, s>>>(c->sorted.as<float4>() + V.o0, w_loc, no,
+                                                        ctx->src4.as<float4>());
+      else
+        pack_src_f32<<<grid_for(no, 256), 256, 0, s>>>(c->sorted.as<float4>() + V.o0, w_loc, no,
+                                                       ctx->src4.as<float4>());
+      RBF_CHECK_LAUNCH();
+    }
+    RBF_TRY(ctx->fwin.ensure(sizeof(double) * std::max<int64_t>(nw, 1), s));
+    double* fwin = ctx->fwin.as<double>();
+    RBF_CUDA_TRY(cudaMemsetAsync(fwin, 0, sizeof(double) * (size_t)nw, s));
+    RBF_CUDA_TRY(cudaMemsetAsync(ctx->counter.p, 0, 2 * sizeof(int), s));
+    SumGeom G = make_geom(c, kp);
+    const float4* srcb = ctx->src4.as<float4>() - base;
+    auto kfn = sym == 3 ? sum_f32_symr_kernel<double> : sum_f32_symb_kernel<double>;
+    const int64_t ni = V.tw_int, nb = (V.tw1 - V.tw0) - ni;
+    {
+      ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
+      kfn<<<sum_blocks(ctx, kfn), kSumWarps * 32, 0, s>>>(G, c->cell_start.as<int32_t>(), srcb, c->tiles_w.as<int2>(),
+                                                          c->tile_box_w.as<float4>(), ni, V.tw0, fwin - base,
+                                                          ctx->counter.as<int>(), V.h1, c->order_w.as<int32_t>());
+      RBF_CHECK_LAUNCH();
+      // join: the halo tiles after the halo
+      RBF_CUDA_TRY(cudaStreamWaitEvent(s, ctx->halo_ev[1], 0));
+      if (nb > 0) {
+        kfn<<<sum_blocks(ctx, kfn), kSumWarps * 32, 0, s>>>(
+            G, c->cell_start.as<int32_t>(), srcb, c->tiles_w.as<int2>(), c->tile_box_w.as<float4>(), nb, V.tw0,
+            fwin - base, ctx->counter.as<int>() + 1, V.h1, c->order_w.as<int32_t>() + ni);
+        RBF_CHECK_LAUNCH();
+      }
+    }
+    return halo_reduce(ctx, c, fwin, f_loc);
   }
   RBF_TRY(ctx->src4.ensure(sizeof(float4) * std::max<int64_t>(nw, 1), s));
   RBF_TRY(ctx->counter.ensure(256, s));

@@ -356,10 +356,10 @@ class Cells:
     def slab(self) -> dict:
         """rbf_cells_slab: this rank's owned / window / tile / plane ranges."""
         import numpy as np
-        v = np.zeros(8, dtype=np.int64)
+        v = np.zeros(11, dtype=np.int64)
         _check(_lib.rbf_cells_slab(self._h, v.ctypes.data_as(C.c_void_p)))
         return dict(own=(int(v[0]), int(v[1])), window=(int(v[2]), int(v[3])), tiles=(int(v[4]), int(v[5])),
-                    planes=(int(v[6]), int(v[7])))
+                    planes=(int(v[6]), int(v[7])), wide_tiles=(int(v[8]), int(v[9])), wide_interior=int(v[10]))
 
     def view(self) -> dict:
         """Copies of the library's cell arrays (perm, sorted float4, keys, cell_start)."""

@@ -179,6 +179,16 @@ def test_loopback_partition_products_and_grid(R, setup, world):
             np.testing.assert_array_equal(exts[k] + o0, blk["ext"])
     assert (covered == 1).all()                     # slabs partition the targets
     assert (layers == 1).all()                      # every node layer owned once
+    # the wide plan's interior tiles (run while the halo is exchanged on the aux
+    # stream) are a prefix of each rank's wide tiles; at W = 2 and 3 the slabs
+    # are thick enough for the overlapped path to run (checked above by the
+    # OP_SYM_WIDE / OP_SYM_ROT rows against the oracle)
+    interior = [res["slab"]["wide_interior"] for res in out]
+    for res in out:
+        t0, t1 = res["slab"]["wide_tiles"]
+        assert 0 <= res["slab"]["wide_interior"] <= t1 - t0
+    if world < 8:
+        assert sum(interior) > 0
     # per-rank useful pairs of the slab plan (balanced by sum n_c^2) add up to the whole
     per_rank = np.array([res["useful"] for res in out])
     assert per_rank.sum() == s["useful"]
