@@ -12,12 +12,12 @@
 // distances ((dx^2 + dy^2) + dz^2), sqrt(d2) <= eps, F_a * F_b < 0 on the fp32
 // field promoted to fp64, t = F_a / (F_a - F_b)), so the output equals
 // oracle/grid.py::zero_crossings on the same field point for point:
-//   1. the data points are binned into cells of edge >= eps (radix sort + starts);
-//   2. near[node] = some data point within eps (27 neighbour cells, early exit);
-//   3. per axis x, y, z: flag the edges, exclusive scan, write the crossing
+//   1. near[node] = some data point within eps, scattered from the points (one
+//      thread per point tests the nodes of its eps box exactly);
+//   2. per axis x, y, z: flag the edges, exclusive scan, write the crossing
 //      points in (axis, lower-node flat index) order -- the oracle's order.
-// Work: one pass over the nodes for the mask (bounded by the data points in
-// the 27 cells of near-surface nodes), three HBM passes over the field.
+// Work: ~(2 eps / step + 3)^3 exact distance tests per data point for the mask
+// (c4: 1M points, ~1.2e8 tests), three HBM passes over the field.
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -83,80 +83,40 @@ __global__ void data_gather_kernel(const double* __restrict__ X, const int32_t* 
   }
 }
 
-// 4x4x4 node blocks within eps of some data point: one thread per non-empty data
-// cell marks the blocks whose box (fp64 node coordinates) lies within
-// eps (1 + 1e-9) of the cell's tight bounding box -- a superset of the blocks
-// holding a near node; near_kernel searches only those
-__global__ void near_blocks_kernel(ZGrid g, DCells dc, const int32_t* __restrict__ start,
-                                   const double* __restrict__ S, double eps, uint32_t* __restrict__ bflag) {
-  const int64_t ncell = (int64_t)dc.dim[0] * dc.dim[1] * dc.dim[2];
-  const int nb[3] = {(g.n[0] + 3) / 4, (g.n[1] + 3) / 4, (g.n[2] + 3) / 4};
-  const double e = eps * (1.0 + 1e-9);
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncell; c += (int64_t)gridDim.x * blockDim.x) {
-    const int s0 = start[c], s1 = start[c + 1];
-    if (s1 == s0) continue;
-    double lo3[3] = {INFINITY, INFINITY, INFINITY}, hi3[3] = {-INFINITY, -INFINITY, -INFINITY};
-    for (int q = s0; q < s1; ++q)
-#pragma unroll
-      for (int a = 0; a < 3; ++a) { lo3[a] = fmin(lo3[a], S[3 * q + a]); hi3[a] = fmax(hi3[a], S[3 * q + a]); }
-    int b0[3], b1[3];
+// near[node] = 1 for every grid node within eps of data point i, scattered from
+// the points: one thread per point tests the nodes of the box [x_i - eps,
+// x_i + eps] (widened by one node per side against the rounding of the index
+// range) with the oracle's arithmetic, sqrt_rn(((dx^2 + dy^2) + dz^2)) <= eps
+// on the fp64 node coordinates lo + i * step.  Every (node, point) pair within
+// eps is tested exactly once, so near[] is the oracle's mask bit for bit (the
+// stores are idempotent: racing threads write the same 1).
+__global__ void near_scatter_kernel(ZGrid g, const double* __restrict__ X, int64_t n, double eps,
+                                    uint8_t* __restrict__ near) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double x[3] = {X[3 * i], X[3 * i + 1], X[3 * i + 2]};
+    int lo[3], hi[3];
     bool none = false;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      int i0 = (int)floor((lo3[a] - e - g.lo[a]) / g.step[a]) - 1, i1 = (int)ceil((hi3[a] + e - g.lo[a]) / g.step[a]) + 1;
-      i0 = max(i0, 0);
-      i1 = min(i1, g.n[a] - 1);
-      if (i0 > i1) none = true;
-      b0[a] = i0 >> 2;
-      b1[a] = i1 >> 2;
+      lo[a] = max((int)floor((x[a] - eps - g.lo[a]) / g.step[a]) - 1, 0);
+      hi[a] = min((int)ceil((x[a] + eps - g.lo[a]) / g.step[a]) + 1, g.n[a] - 1);
+      if (lo[a] > hi[a]) none = true;
     }
     if (none) continue;
-    for (int bz = b0[2]; bz <= b1[2]; ++bz) {
-      const double gz = fmax(0.0, fmax(zcoord(g, 2, 4 * bz) - hi3[2], lo3[2] - zcoord(g, 2, min(4 * bz + 3, g.n[2] - 1))));
-      for (int by = b0[1]; by <= b1[1]; ++by) {
-        const double gy = fmax(0.0, fmax(zcoord(g, 1, 4 * by) - hi3[1], lo3[1] - zcoord(g, 1, min(4 * by + 3, g.n[1] - 1))));
-        if (gy * gy + gz * gz > e * e) continue;
-        for (int bx = b0[0]; bx <= b1[0]; ++bx) {
-          const double gx = fmax(0.0, fmax(zcoord(g, 0, 4 * bx) - hi3[0], lo3[0] - zcoord(g, 0, min(4 * bx + 3, g.n[0] - 1))));
-          if (gx * gx + gy * gy + gz * gz <= e * e) bflag[((int64_t)bz * nb[1] + by) * nb[0] + bx] = 1u;
+    for (int k = lo[2]; k <= hi[2]; ++k) {
+      const double dz = __dsub_rn(zcoord(g, 2, k), x[2]);
+      const double dz2 = __dmul_rn(dz, dz);
+      for (int jj = lo[1]; jj <= hi[1]; ++jj) {
+        const double dy = __dsub_rn(zcoord(g, 1, jj), x[1]);
+        const double dy2 = __dmul_rn(dy, dy);
+        const int64_t row = ((int64_t)k * g.n[1] + jj) * g.n[0];
+        for (int ii = lo[0]; ii <= hi[0]; ++ii) {
+          const double dx = __dsub_rn(zcoord(g, 0, ii), x[0]);
+          const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), dy2), dz2);
+          if (__dsqrt_rn(d2) <= eps) near[row + ii] = 1;
         }
       }
     }
-  }
-}
-
-// near[node] = exists data point p with sqrt(|node - p|^2) <= eps (fp64); nodes
-// of unmarked blocks (bflag) have no data point within eps: 0 without a search
-__global__ void near_kernel(ZGrid g, DCells dc, const int32_t* __restrict__ start, const double* __restrict__ S,
-                            double eps, const uint32_t* __restrict__ bflag, uint8_t* __restrict__ near) {
-  const int64_t nn = (int64_t)g.n[0] * g.n[1] * g.n[2];
-  const int nb0 = (g.n[0] + 3) / 4, nb1 = (g.n[1] + 3) / 4;
-  const double e2_lo = eps * eps * (1.0 - 1e-12), e2_hi = eps * eps * (1.0 + 1e-12);
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nn; v += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(v % g.n[0]), j = (int)((v / g.n[0]) % g.n[1]), k = (int)(v / ((int64_t)g.n[0] * g.n[1]));
-    if (!bflag[((int64_t)(k >> 2) * nb1 + (j >> 2)) * nb0 + (i >> 2)]) { near[v] = 0; continue; }
-    const double p[3] = {zcoord(g, 0, i), zcoord(g, 1, j), zcoord(g, 2, k)};
-    int c[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) c[a] = dcell(p[a], dc.lo[a], dc.inv_h, dc.dim[a]);
-    bool hit = false;
-    for (int cz = max(c[2] - 1, 0); cz <= min(c[2] + 1, dc.dim[2] - 1) && !hit; ++cz)
-      for (int cy = max(c[1] - 1, 0); cy <= min(c[1] + 1, dc.dim[1] - 1) && !hit; ++cy) {
-        const int x0 = max(c[0] - 1, 0), x1 = min(c[0] + 1, dc.dim[0] - 1);
-        if (x0 > x1) continue;
-        const int64_t row = ((int64_t)cz * dc.dim[1] + cy) * dc.dim[0];
-        const int s0 = start[row + x0], s1 = start[row + x1 + 1];
-        for (int q = s0; q < s1; ++q) {
-          const double dx = __dsub_rn(p[0], S[3 * q]), dy = __dsub_rn(p[1], S[3 * q + 1]),
-                       dz = __dsub_rn(p[2], S[3 * q + 2]);
-          const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-          // sqrt_rn(d2) <= eps decided without the sqrt away from the boundary:
-          // d2 < eps^2 (1 - 1e-12) implies it, d2 > eps^2 (1 + 1e-12) excludes it
-          if (d2 > e2_hi) continue;
-          if (d2 < e2_lo || __dsqrt_rn(d2) <= eps) { hit = true; break; }
-        }
-      }
-    near[v] = hit ? 1 : 0;
   }
 }
 
@@ -217,55 +177,11 @@ rbf_status build_near_mask(rbf_ctx* ctx, const rbf_grid* grid, const double* dat
   }
   const int64_t nn = (int64_t)g.n[0] * g.n[1] * g.n[2];
   RBF_TRY(near.alloc(nn, s));
-  if (ndata == 0) {
-    RBF_CUDA_TRY(cudaMemsetAsync(near.p, 0, nn, s));
-    return RBF_OK;
-  }
-  // 1. data cells of edge h >= eps over the data bounding box
+  RBF_CUDA_TRY(cudaMemsetAsync(near.p, 0, nn, s));
+  if (ndata == 0) return RBF_OK;
   double mn[3], mx[3];
-  RBF_TRY(data_bbox(ctx, data, ndata, mn, mx));
-  double h = eps * (1.0 + 1e-6);
-  DCells dc;
-  int64_t ncell = 1;
-  for (;;) {   // coarsen the cells (edge stays >= eps) if the box would need too many
-    double prod = 1.0;
-    for (int a = 0; a < 3; ++a) prod *= std::floor((mx[a] - (mn[a] - 0.5 * h)) / h) + 1.0;
-    if (prod <= (double)((int64_t)1 << 28)) break;
-    h *= 2.0;
-  }
-  for (int a = 0; a < 3; ++a) {
-    dc.lo[a] = mn[a] - 0.5 * h;
-    dc.dim[a] = (int)std::floor((mx[a] - dc.lo[a]) / h) + 1;
-    ncell *= dc.dim[a];
-  }
-  dc.inv_h = 1.0 / h;
-  DevBuf k1, v1, k2, v2, start, S;
-  RBF_TRY(k1.alloc(4 * ndata, s));
-  RBF_TRY(v1.alloc(4 * ndata, s));
-  RBF_TRY(k2.alloc(4 * ndata, s));
-  RBF_TRY(v2.alloc(4 * ndata, s));
-  data_keys_kernel<<<grid_for(ndata, 256), 256, 0, s>>>(data, ndata, dc, k1.as<uint32_t>(), v1.as<int32_t>());
-  RBF_CHECK_LAUNCH();
-  int bits = 1;
-  while (bits < 32 && ((int64_t)1 << bits) < ncell) ++bits;
-  RBF_TRY(radix_sort_pairs<uint32_t>(ctx, k1.as<uint32_t>(), v1.as<int32_t>(), k2.as<uint32_t>(), v2.as<int32_t>(),
-                                     ndata, bits));
-  RBF_TRY(start.alloc(4 * (ncell + 1), s));
-  data_start_kernel<<<grid_for(ndata + 1, 256), 256, 0, s>>>(k2.as<uint32_t>(), ndata, ncell, start.as<int32_t>());
-  RBF_CHECK_LAUNCH();
-  RBF_TRY(S.alloc(sizeof(double) * 3 * ndata, s));
-  data_gather_kernel<<<grid_for(ndata, 256), 256, 0, s>>>(data, v2.as<int32_t>(), ndata, S.as<double>());
-  RBF_CHECK_LAUNCH();
-  // 2. the eps mask: candidate node blocks, then the per-node search inside them
-  const int64_t nbt = (int64_t)((g.n[0] + 3) / 4) * ((g.n[1] + 3) / 4) * ((g.n[2] + 3) / 4);
-  DevBuf bflag;
-  RBF_TRY(bflag.alloc(4 * nbt, s));
-  RBF_CUDA_TRY(cudaMemsetAsync(bflag.p, 0, 4 * nbt, s));
-  near_blocks_kernel<<<grid_for(ncell, 256), 256, 0, s>>>(g, dc, start.as<int32_t>(), S.as<double>(), eps,
-                                                          bflag.as<uint32_t>());
-  RBF_CHECK_LAUNCH();
-  near_kernel<<<grid_for(nn, 256, 148 * 32), 256, 0, s>>>(g, dc, start.as<int32_t>(), S.as<double>(), eps,
-                                                          bflag.as<uint32_t>(), near.as<uint8_t>());
+  RBF_TRY(data_bbox(ctx, data, ndata, mn, mx));   // rejects non-finite points
+  near_scatter_kernel<<<grid_for(ndata, 256, 148 * 32), 256, 0, s>>>(g, data, ndata, eps, near.as<uint8_t>());
   RBF_CHECK_LAUNCH();
   return RBF_OK;
 }
