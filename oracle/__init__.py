@@ -19,6 +19,9 @@ Modules and the passage each follows:
   grid     evaluation on a regular grid (Eq. 5, l.264-271; §2.1.3 l.200-221),
            masked zero-crossings (M_ext^eps cap S_0, l.211-221)
   density  separation / fill distance and h_max (Eq. 7, 8, 11; l.490-625)
+  mesh     the triangle mesh of the masked zero iso-surface (Alg. 1 step 4,
+           l.317-328, restricted to M_ext^eps, l.200-221): marching tetrahedra
+           on the Kuhn split of the grid cubes (reading R24)
 
 Parity pins: tests/test_oracle_*.py (run with -m "not gpu").  Functions
 without an independent pin say "parity unpinned" in their docstring.
