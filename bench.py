@@ -193,12 +193,14 @@ def density_report(R, ctx, d):
 def measured_traffic(cfg_name: str):
     """DRAM bytes per launch of the dominant kernel from the committed ncu --set full
     capture (profiles/), or None when there is none for this config."""
-    path = os.path.join(ROOT, "profiles", "r01", f"traffic_sum_f32_{cfg_name}.json")
-    try:
-        with open(path) as fh:
-            return json.load(fh)["dram_bytes_per_launch"]
-    except (OSError, KeyError, ValueError):
-        return None
+    for rnd in ("r02", "r01"):
+        path = os.path.join(ROOT, "profiles", rnd, f"traffic_sum_f32_{cfg_name}.json")
+        try:
+            with open(path) as fh:
+                return json.load(fh)["dram_bytes_per_launch"]
+        except (OSError, KeyError, ValueError):
+            continue
+    return None
 
 
 def measured_ex2(cfg_name: str):
