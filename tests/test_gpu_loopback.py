@@ -307,3 +307,33 @@ def test_loopback_reconstruct_host(R):
     cells1 = R.Cells(ctx1, torch.as_tensor(X, device="cuda"), kern)
     F1 = R.eval_grid(ctx1, cells1, kern, torch.as_tensor(w, device="cuda"), lo, hi, gn).cpu().numpy()
     np.testing.assert_array_equal(out[0][1], F1)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_loopback_isosurface(R, setup, world):
+    """rbf_isosurface over slab ranks: each rank evaluates the masked node blocks
+    of its own layers, the layers are gathered (NaN outside M_ext^eps travels as
+    data), and every rank's mesh equals the single-GPU mesh bit for bit."""
+    s = setup
+    lo, hi, gn = s["grid"]
+    data = np.ascontiguousarray(s["d"]["x"], dtype=np.float64)
+    eps = 2 * s["sigma"]
+    ctx = R.Context(0)
+    c1 = R.Cells(ctx, torch.as_tensor(s["X"], device="cuda"), s["kern"])
+    wt = torch.as_tensor(s["w"], device="cuda")
+    F1 = torch.empty(gn[0] * gn[1] * gn[2], dtype=torch.float32, device="cuda")
+    V1, T1 = R.isosurface(ctx, c1, s["kern"], wt, lo, hi, gn, torch.as_tensor(data, device="cuda"), eps, field=F1)
+    V1, T1, F1 = V1.cpu().numpy(), T1.cpu().numpy(), F1.cpu().numpy()
+    assert len(T1) > 100
+
+    def rank(ctx, r):
+        c = R.Cells(ctx, torch.as_tensor(s["X"], device="cuda"), s["kern"])
+        F = torch.empty(gn[0] * gn[1] * gn[2], dtype=torch.float32, device="cuda")
+        V, T = R.isosurface(ctx, c, s["kern"], torch.as_tensor(s["w"], device="cuda"), lo, hi, gn,
+                            torch.as_tensor(data, device="cuda"), eps, field=F)
+        return V.cpu().numpy(), T.cpu().numpy(), F.cpu().numpy()
+
+    for V, T, F in run_ranks(R, world, rank):
+        assert np.array_equal(F.view(np.uint32), F1.view(np.uint32))
+        np.testing.assert_array_equal(V, V1)
+        np.testing.assert_array_equal(T, T1)
