@@ -261,6 +261,22 @@ def run_ours(args, rank, world, local):
     cell_edge = kern.sigma * kern.cutoff_sigmas / float(os.environ.get("RBF_BENCH_CELL_DIV", cfg.cell_div))
     solve_kw["cell_edge"] = cell_edge
 
+    if slab:
+        # the slab path over NCCL has only run on one GPU through the loopback
+        # transport: before timing it, every rank checks the
+        # distributed one-sided product against its own single-GPU product of the
+        # same replicated input (bit-identical by construction) and fails loudly
+        centres, _ = R.extend_points(ctx, x, nrm, d["delta"])
+        wchk = torch.as_tensor(np.random.default_rng(5).normal(size=centres.shape[0]), device=dev)
+        fd = R.matvec(ctx, R.Cells(ctx, centres, kern, cell_edge=cell_edge), kern, wchk)
+        solo = R.Context(local)
+        fs = R.matvec(solo, R.Cells(solo, centres, kern, cell_edge=cell_edge), kern, wchk)
+        torch.cuda.synchronize()
+        if not torch.equal(fd, fs):
+            raise RuntimeError(f"rank {rank}: distributed product differs from the single-GPU product "
+                               f"(max |diff| {float((fd - fs).abs().max()):.3e}); slab path not trusted")
+        del solo, fd, fs, centres
+
     def step():
         centres, b = R.extend_points(ctx, x, nrm, d["delta"])
         cells = R.Cells(ctx, centres, kern, cell_edge=cell_edge)
