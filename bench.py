@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-rows", type=int, default=0)
     ap.add_argument("--fit-iters", type=int, default=50)
+    ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
+                    help="N>1 slab mode: the library's data plane over CUDA-IPC peer memory (default; the transport "
+                         "the multi-process GPU tests run) or over NCCL send/recv + allreduce")
     ap.add_argument("--parallel", default="slab", choices=["slab", "replicas"],
                     help="N>1: one problem split by slabs over the ranks (strong scaling, SURVEY §8(e)) "
                          "or one independent seeded problem per rank (weak scaling)")
@@ -61,6 +64,10 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook (tests/test_gpu_bench_slab.py): every rank on cuda:0 over a gloo
+    # group, to run the N>1 plumbing on a one-GPU box -- never a measurement
+    if os.environ.get("RBF_BENCH_SHARED_GPU") == "1":
+        local = 0
     return rank, world, local
 
 
@@ -240,13 +247,18 @@ def run_ours(args, rank, world, local):
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    shared = os.environ.get("RBF_BENCH_SHARED_GPU") == "1"
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    red_dev = None if shared else dev   # device of the max/sum reductions of the timings
     slab = world > 1 and args.parallel == "slab"
     d = make_problem(args.config, args.seed if slab else args.seed + rank)
     cfg = d["cfg"]
-    ctx = R.Context(local, distributed=slab)
+    ctx = R.Context(local, distributed=slab, transport=args.transport)
     kern = R.Kernel(d["sigma"], d["cutoff_sigmas"])
     x = torch.as_tensor(d["x"], device=dev)
     nrm = torch.as_tensor(d["normals"], device=dev)
@@ -341,7 +353,7 @@ def run_ours(args, rank, world, local):
     mv32 = sum(r["matvecs_f32"] for r in reps)
     mv64 = sum(r["matvecs_f64"] for r in reps)
     pairs_rank = useful_mv * (mv32 + mv64) + useful_grid * args.steps
-    ms_max, pairs_all, value = throughput(ms, pairs_rank, dev)
+    ms_max, pairs_all, value = throughput(ms, pairs_rank, red_dev)
 
     # e2e through the C-ABI with HOST buffers (rank-local problem)
     e2e = None
@@ -368,7 +380,7 @@ def run_ours(args, rank, world, local):
         te = (time.perf_counter() - t0) * 1e3
         gc.enable()
         pe = useful_mv * mv_e2e + useful_grid * args.steps
-        te, pe, ve = throughput(te, pe, dev)
+        te, pe, ve = throughput(te, pe, red_dev)
         e2e = {"value": ve, "unit": "pairs/s", "ms_per_step": te / args.steps,
                "h2d_bytes_per_step": int(xyz_h.numel() * 4 + b_h.numel() * 4),
                "d2h_bytes_per_step": int(w_h.numel() * 8 + f_h.numel() * 4)}
@@ -380,7 +392,8 @@ def run_ours(args, rank, world, local):
     if rank == 0:
         zs = zero_set_quality(R, ctx, d, field, lo, hi, gn)
         dens = density_report(R, ctx, d)
-        iso = isosurface_report(R, ctx, d, cells_last, kern, w, lo, hi, gn)
+    # collective in slab mode (the masked grid gathers the ranks' layers): every rank calls it
+    iso = isosurface_report(R, ctx, d, cells_last, kern, w, lo, hi, gn)
 
     # roofline of the dominant kernel (fp32 summation), live CUDA-event timing
     t_mv, n_mv = prof["matvec_f32"]
@@ -426,9 +439,10 @@ def run_ours(args, rank, world, local):
                                f"grid {gn[0]}^3",
                    "centres_per_gpu": 3 * cfg.n // world if slab else 3 * cfg.n,
                    "global_centres": 3 * cfg.n if slab else 3 * cfg.n * world,
-                   "parallelism": (f"slab x{world} (z cell planes, halo send/recv + allreduce over NCCL; "
-                                   "experimental: this code path is verified on one GPU through the loopback "
-                                   "transport, its NCCL form has not run on a multi-GPU box in this work)" if slab
+                   "parallelism": (f"slab x{world} (z cell planes; halo exchange, reverse halo reduction and "
+                                   f"Krylov all-reduces over the {args.transport} transport; the multi-rank path "
+                                   "is verified on one GPU -- threads over the loopback transport and separate "
+                                   "processes over the IPC transport -- not yet on a multi-GPU box)" if slab
                                    else f"replicas x{world} (independent seeded instances)"),
                    "l2": "working set >> 126 MB L2 (block inverses 0.5 GB, Krylov basis 1.2 GB, cells + vectors 0.2 GB); no explicit flush"},
         "e2e": e2e, "gpu_launches": None, "clocks": clk, "roofline": roofline, "cpu_baseline": cpu,
@@ -449,6 +463,8 @@ def run_ours(args, rank, world, local):
     out["gpu_launches"] = launches
     if rank == 0:
         print(json.dumps(out), flush=True)
+    del cells_last, w, field
+    ctx.close()
     if world > 1:
         torch.distributed.destroy_process_group()
 

@@ -222,6 +222,19 @@ rbf_status rbf_nccl_unique_id(void* out128);
 rbf_status rbf_loopback_group_create(int world, rbf_loopback_group** out);
 void rbf_loopback_group_free(rbf_loopback_group* g);
 rbf_status rbf_create_loopback(rbf_ctx** ctx, int device, void* cuda_stream, rbf_loopback_group* g, int rank);
+/* Peer-memory transport (one process per GPU on ONE node, NCCL not used): the
+ * ranks' exchange arenas are mapped into each other by CUDA IPC (NVLink /
+ * NVSwitch peer access; several processes may also share one device, for
+ * tests), transfers are cudaMemcpyAsync between device pointers (copy engines),
+ * the all-reduce is a rank-ordered sum kernel over every rank's arena, and
+ * ordering is by interprocess CUDA events plus a host barrier in POSIX shared
+ * memory (no kernel waits on another rank).  key16: 16 HOST bytes, identical on
+ * every rank and fresh per group (rank 0 draws them and shares them, e.g. over
+ * torch.distributed); it names the shared-memory segment.  Every rank must make
+ * the same sequence of calls; a rank that does not arrive makes the others fail
+ * with RBF_ECUDA after 600 s.  Errors: RBF_EINVAL (rank/world, segment setup),
+ * RBF_ECUDA (IPC or event calls, barrier timeout). */
+rbf_status rbf_create_ipc(rbf_ctx** ctx, int device, void* cuda_stream, const void* key16, int rank, int world);
 /* Slab partition plan (HOST only, no GPU; the same function the library runs at
  * rbf_build_cells when world > 1).  Inputs: plane_start[dimz+1] = sorted
  * position of the first centre of each z cell plane (non-decreasing, last =

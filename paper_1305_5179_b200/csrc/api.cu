@@ -185,6 +185,22 @@ rbf_status rbf_create_loopback(rbf_ctx** out, int device, void* cuda_stream, rbf
   return RBF_OK;
 }
 
+rbf_status rbf_create_ipc(rbf_ctx** out, int device, void* cuda_stream, const void* key16, int rank, int world) {
+  if (!out || !key16) { set_error("NULL argument"); return RBF_EINVAL; }
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world) { set_error("need 0 <= rank < world"); return RBF_EINVAL; }
+  rbf_ctx* c = nullptr;
+  RBF_TRY(create_ctx(&c, device, cuda_stream));
+  Transport* t = nullptr;
+  rbf_status st = make_ipc_transport(device, key16, rank, world, &t);
+  if (st != RBF_OK) { delete c; return st; }
+  c->rank = rank;
+  c->world = world;
+  c->tr = t;
+  *out = c;
+  return RBF_OK;
+}
+
 rbf_status rbf_profile_enable(rbf_ctx* ctx, int on) {
   if (!ctx) { set_error("ctx is NULL"); return RBF_EINVAL; }
   ctx->prof = on != 0;

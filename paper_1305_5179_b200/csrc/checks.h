@@ -28,10 +28,6 @@
     __nanosleep((_h >> 24) & 0xFFu);                                                               \
   } while (0)
 #else
-#define RBF_DCHECK(cond) \
-  do {                   \
-  } while (0)
-#define RBF_JITTER() \
-  do {               \
-  } while (0)
+#define RBF_DCHECK(cond) ((void)0)
+#define RBF_JITTER() ((void)0)
 #endif

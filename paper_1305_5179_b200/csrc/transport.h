@@ -3,7 +3,7 @@
 // The data plane of a slab-partitioned solve needs three collectives: grouped
 // point-to-point copies of contiguous ranges (halo exchange, its reverse
 // reduction, gathers), and a sum all-reduce (Krylov inner products).  Two
-// implementations:
+// implementations (plus the CUDA-IPC peer-memory transport of ipc.cu):
 //   * NcclTransport: one process per GPU, ncclSend/ncclRecv in a group and
 //     ncclAllReduce over NVLink/NVSwitch (dist.cu);
 //   * LoopTransport: W contexts of ONE process on one device, one host thread
@@ -67,6 +67,8 @@ struct LoopGroup {
 };
 
 Transport* make_nccl_transport(void* comm);
+// ipc.cu: CUDA-IPC peer-memory transport (one process per GPU, one node)
+rbf_status make_ipc_transport(int device, const void* key16, int rank, int world, Transport** out);
 Transport* make_loop_transport(LoopGroup* g, int rank);
 
 }  // namespace rbf

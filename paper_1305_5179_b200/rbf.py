@@ -92,6 +92,7 @@ EXPORTS = {
     "rbf_loopback_group_create": (C.c_int, [C.c_int, C.POINTER(_P)]),
     "rbf_loopback_group_free": (None, [_P]),
     "rbf_create_loopback": (C.c_int, [C.POINTER(_P), C.c_int, _P, _P, C.c_int]),
+    "rbf_create_ipc": (C.c_int, [C.POINTER(_P), C.c_int, _P, _P, C.c_int, C.c_int]),
     "rbf_slab_plan": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, _P, _P, _P, _P, _P]),
     "rbf_extend_points": (C.c_int, [_P, _P, _P, C.c_int64, C.c_double, C.c_double, _P, _P]),
     "rbf_build_cells": (C.c_int, [_P, _P, C.c_int64, C.POINTER(_Kernel), C.POINTER(_CellCfg),
@@ -263,11 +264,14 @@ class Context:
     distributed=True (and an initialised torch.distributed group with world > 1):
     one context per rank/GPU sharing an NCCL communicator; rank 0's NCCL id is
     broadcast with torch.distributed (plumbing only).  loopback=(group, rank):
-    rank `rank` of an in-process LoopbackGroup (rbf_create_loopback).  Calls then
-    take and return replicated (full) arrays while the library shards the work."""
+    rank `rank` of an in-process LoopbackGroup (rbf_create_loopback).
+    transport="ipc" with distributed=True: the CUDA-IPC peer-memory transport
+    (rbf_create_ipc, one node) instead of NCCL; rank 0's 16-byte group key is
+    broadcast with torch.distributed (any backend).  Calls then take and return
+    replicated (full) arrays while the library shards the work."""
 
     def __init__(self, device: int = 0, stream: torch.cuda.Stream | None = None, distributed: bool = False,
-                 loopback: tuple | None = None):
+                 loopback: tuple | None = None, transport: str = "nccl"):
         lib = load_library()
         self.device = device
         self.stream = stream if stream is not None else torch.cuda.current_stream(device)
@@ -278,11 +282,22 @@ class Context:
                                            int(rank)))
             self._h, self.rank, self.world, self._group = h, int(rank), group.world, group
             return
+        if transport not in ("nccl", "ipc"):
+            raise ValueError("transport must be 'nccl' or 'ipc'")
         rank, world, uid = 0, 1, None
         if distributed:
             import torch.distributed as dist
             if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
                 rank, world = dist.get_rank(), dist.get_world_size()
+                if transport == "ipc":
+                    box = [os.urandom(16) if rank == 0 else None]
+                    dist.broadcast_object_list(box, src=0)
+                    self.rank, self.world = rank, world
+                    h = C.c_void_p()
+                    _check(lib.rbf_create_ipc(C.byref(h), device, C.c_void_p(self.stream.cuda_stream),
+                                              C.create_string_buffer(box[0], 16), rank, world))
+                    self._h = h
+                    return
                 box = [nccl_unique_id() if rank == 0 else None]
                 dist.broadcast_object_list(box, src=0)
                 uid = C.create_string_buffer(box[0], 128)
