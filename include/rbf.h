@@ -235,6 +235,16 @@ rbf_status rbf_create_loopback(rbf_ctx** ctx, int device, void* cuda_stream, rbf
  * with RBF_ECUDA after 600 s.  Errors: RBF_EINVAL (rank/world, segment setup),
  * RBF_ECUDA (IPC or event calls, barrier timeout). */
 rbf_status rbf_create_ipc(rbf_ctx** ctx, int device, void* cuda_stream, const void* key16, int rank, int world);
+/* Peer-memory form of the solver's symmetric fp32 operator (on by default; used
+ * when the context's transport can address the other ranks' device memory --
+ * loopback and CUDA IPC, not NCCL): ONE summation kernel per rank reads the upper
+ * ranks' packed sources and atomically adds the source-side sums into their
+ * accumulators directly (NVLink / NVSwitch peer memory) instead of a halo
+ * exchange before the kernel and a reverse halo reduction after it; the ranks
+ * are ordered by events and a host barrier before and after the kernels.  on = 0
+ * keeps the copy-based halo (the NCCL path's form) on any transport.  Results
+ * are the same up to the atomics' summation order. */
+rbf_status rbf_ctx_peer_memory(rbf_ctx* ctx, int on);
 /* Slab partition plan (HOST only, no GPU; the same function the library runs at
  * rbf_build_cells when world > 1).  Inputs: plane_start[dimz+1] = sorted
  * position of the first centre of each z cell plane (non-decreasing, last =

@@ -201,6 +201,12 @@ rbf_status rbf_create_ipc(rbf_ctx** out, int device, void* cuda_stream, const vo
   return RBF_OK;
 }
 
+rbf_status rbf_ctx_peer_memory(rbf_ctx* ctx, int on) {
+  if (!ctx) { set_error("ctx is NULL"); return RBF_EINVAL; }
+  ctx->peer_mem = on != 0;
+  return RBF_OK;
+}
+
 rbf_status rbf_profile_enable(rbf_ctx* ctx, int on) {
   if (!ctx) { set_error("ctx is NULL"); return RBF_EINVAL; }
   ctx->prof = on != 0;

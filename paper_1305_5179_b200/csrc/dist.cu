@@ -161,6 +161,31 @@ struct LoopTransport final : Transport {
   LoopGroup* g;
   int rank;
   DevBuf scratch;
+  DevBuf pbuf;   // peer-memory mode buffer
+  bool peer_capable() const override { return true; }
+  rbf_status peer_begin(rbf_ctx*, cudaStream_t s, uint64_t need, const std::function<rbf_status(void*)>& stage,
+                        std::vector<void*>* peers) override {
+    LoopGroup::Slot& me = g->slots[rank];
+    // every rank's buffer stays alive (and is not regrown) until peer_end
+    RBF_TRY(pbuf.ensure(std::max<uint64_t>(need, 16), s));
+    RBF_TRY(stage(pbuf.p));
+    me.peer_buf = pbuf.p;
+    RBF_CUDA_TRY(cudaEventRecord(me.ready, s));
+    g->barrier();
+    peers->assign(g->world, nullptr);
+    for (int q = 0; q < g->world; ++q) {
+      (*peers)[q] = g->slots[q].peer_buf;
+      if (q != rank) RBF_CUDA_TRY(cudaStreamWaitEvent(s, g->slots[q].ready, 0));
+    }
+    return RBF_OK;
+  }
+  rbf_status peer_end(rbf_ctx*, cudaStream_t s) override {
+    RBF_CUDA_TRY(cudaEventRecord(g->slots[rank].done, s));
+    g->barrier();
+    for (int q = 0; q < g->world; ++q)
+      if (q != rank) RBF_CUDA_TRY(cudaStreamWaitEvent(s, g->slots[q].done, 0));
+    return RBF_OK;
+  }
   // the slot's events belong to the group (a peer may still be waiting on them
   // after this rank has returned from its last collective and been destroyed)
   LoopTransport(LoopGroup* grp, int r) : g(grp), rank(r) {

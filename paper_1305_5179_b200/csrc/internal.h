@@ -150,6 +150,7 @@ struct rbf_ctx {
   rbf::Transport* tr = nullptr;
   void* loop_group = nullptr;   // rbf::LoopGroup of a loopback context
   int rank = 0, world = 1;
+  bool peer_mem = true;   // use the transport's peer-memory mode when it has one (rbf_ctx_peer_memory)
   rbf::DevBuf win, fwin, rsc, red, pwin;
 };
 

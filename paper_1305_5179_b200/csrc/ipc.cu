@@ -305,6 +305,18 @@ struct IpcTransport final : Transport {
     return finish(s);
   }
 
+  bool peer_capable() const override { return true; }
+  rbf_status peer_begin(rbf_ctx*, cudaStream_t s, uint64_t need, const std::function<rbf_status(void*)>& stage,
+                        std::vector<void*>* peers) override {
+    shm->slots[rank].nsend = 0;
+    RBF_TRY(publish(s, need, [&]() { return stage(arena); }));
+    peers->assign(peer_arena.begin(), peer_arena.end());
+    for (int q = 0; q < world; ++q)
+      if (q != rank) RBF_CUDA_TRY(cudaStreamWaitEvent(s, peer_ready[q], 0));
+    return RBF_OK;
+  }
+  rbf_status peer_end(rbf_ctx*, cudaStream_t s) override { return finish(s); }
+
   rbf_status allreduce_sum(rbf_ctx*, cudaStream_t s, void* buf, int64_t count, DType t) override {
     const size_t es = (size_t)t;
     shm->slots[rank].nsend = 0;

@@ -31,6 +31,7 @@
 
 #include "internal.h"
 #include "solver.h"
+#include "transport.h"
 
 namespace rbf {
 namespace {
@@ -1003,12 +1004,31 @@ __device__ __forceinline__ void symr_tile(const SumGeom& G, const int32_t* __res
   }
 }
 
+// Peer-memory form of the slab partition: the ranks whose slices
+// cover this rank's source window [o0, h1), this rank first; slice k holds the
+// sorted positions [lo[k], lo[k+1]) and lives in rank k's buffer -- its packed
+// sources src[k][j - lo[k]] and its fp64 sums f[k][j - lo[k]], which the kernel
+// reads and atomically updates directly (NVLink / NVSwitch peer memory), in
+// place of the halo exchange and the reverse halo reduction.
+constexpr int kPeerMax = 8;
+struct PeerTab {
+  int n;
+  int64_t lo[kPeerMax + 1];
+  const float4* src[kPeerMax];   // already shifted: src[k] + j addresses position j
+  double* f[kPeerMax];           // already shifted
+};
+__device__ __forceinline__ int peer_of(const PeerTab& P, int64_t j) {
+  int k = 0;
+  while (k + 1 < P.n && j >= P.lo[k + 1]) ++k;
+  return k;
+}
+
 template <class OutT>
 __global__ void __launch_bounds__(kSumWarps * 32, 8)
 sum_f32_symr_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* __restrict__ src,
                     const int2* __restrict__ tiles, const float4* __restrict__ tbox, int64_t ntiles,
                     int64_t tile_base, OutT* __restrict__ out, int* __restrict__ work, int64_t sym_hi,
-                    const int32_t* __restrict__ order) {
+                    const int32_t* __restrict__ order, PeerTab = PeerTab{}) {   // (no peer-memory form)
   __shared__ __align__(16) float4 ring4[kSumWarps][kRotCap];
   __shared__ __align__(8) float2 ring2[kSumWarps][kRotCap];
   __shared__ int ringi[kSumWarps][kRotCap];
@@ -1063,14 +1083,14 @@ constexpr int kSymPad = 136;   // SoA ring row (>= kFlush + 32 + 4, multiple of 
 #define RBF_SYMB_KBSTORE 1
 #endif
 
-template <int T, class OutT>
+template <int T, class OutT, bool PEER = false>
 __device__ __forceinline__ void symb_tile(const SumGeom& G, const int32_t* __restrict__ cell_start,
                                           const float4* __restrict__ src, float3 blo, float3 bhi, float3 ctr,
                                           const float* xr, const float* yr, const float* zr, const bool* tv,
                                           const float* wg, int2 tl, int64_t sym_hi, int lane,
                                           float (*__restrict__ RS)[kSymPad], int* __restrict__ RI,
                                           float* __restrict__ KB, float (*__restrict__ O)[kOwnPad],
-                                          OutT* __restrict__ out, float* fo) {
+                                          OutT* __restrict__ out, float* fo, const PeerTab* PT = nullptr) {
   float mx[T], my[T], mz[T], tf[T], wt[T];
   float2 acc[T];
 #pragma unroll
@@ -1175,7 +1195,11 @@ __device__ __forceinline__ void symb_tile(const SumGeom& G, const int32_t* __res
     RBF_JITTER();
     for (int q = lane; q < cnt; q += 32) {
       const int jj = RI[q];
-      if (jj >= 0) atomicAdd(out + jj, (OutT)(amp * KB[q]));
+      if constexpr (PEER) {
+        if (jj >= 0) atomicAdd(PT->f[peer_of(*PT, jj)] + jj, (double)(amp * KB[q]));
+      } else {
+        if (jj >= 0) atomicAdd(out + jj, (OutT)(amp * KB[q]));
+      }
     }
   };
   auto flush_own = [&](int cnt) {   // cnt: multiple of 4
@@ -1222,10 +1246,15 @@ __device__ __forceinline__ void symb_tile(const SumGeom& G, const int32_t* __res
       const int64_t rowbase = ((int64_t)cz * g.dim[1] + cy) * g.dim[0];
       const int sb = max(__ldg(cell_start + rowbase + x0), tl.x);
       const int se = min(__ldg(cell_start + rowbase + x1 + 1), (int)sym_hi);
+      // a cell row lies in one z plane, so in one rank's slice
+      const float4* __restrict__ srow = src;
+      if constexpr (PEER) {
+        if (sb < se) srow = PT->src[peer_of(*PT, sb)];
+      }
       for (int j0 = sb; j0 < se; j0 += 32) {
         const int j = j0 + lane;
         const bool valid = j < se;
-        const float4 p = valid ? __ldg(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 p = valid ? __ldg(srow + j) : make_float4(0.f, 0.f, 0.f, 0.f);
         const float gx = fmaxf(0.f, fmaxf(blo.x - p.x, p.x - bhi.x));
         const float gyy = fmaxf(0.f, fmaxf(blo.y - p.y, p.y - bhi.y));
         const float gzz = fmaxf(0.f, fmaxf(blo.z - p.z, p.z - bhi.z));
@@ -1302,12 +1331,12 @@ __device__ __forceinline__ void symb_tile(const SumGeom& G, const int32_t* __res
 #ifndef RBF_SYMB_MINB
 #define RBF_SYMB_MINB 8
 #endif
-template <class OutT>
+template <class OutT, bool PEER = false>
 __global__ void __launch_bounds__(kSumWarps * 32, RBF_SYMB_MINB)
 sum_f32_symb_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* __restrict__ src,
                     const int2* __restrict__ tiles, const float4* __restrict__ tbox, int64_t ntiles,
                     int64_t tile_base, OutT* __restrict__ out, int* __restrict__ work, int64_t sym_hi,
-                    const int32_t* __restrict__ order) {
+                    const int32_t* __restrict__ order, PeerTab PT = PeerTab{}) {
   __shared__ __align__(16) float rings[kSumWarps][5][kSymPad];
   __shared__ int ringi[kSumWarps][kSymPad];
   __shared__ float ringk[kSumWarps][kSymPad + 32];   // + the dummy store slots of flush_sym
@@ -1337,10 +1366,10 @@ sum_f32_symb_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const flo
     }
     const int T = (tl.y + 31) >> 5;
     switch (T) {
-      case 1: symb_tile<1>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringk[wib], ringo[wib], out, fo); break;
-      case 2: symb_tile<2>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringk[wib], ringo[wib], out, fo); break;
-      case 3: symb_tile<3>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringk[wib], ringo[wib], out, fo); break;
-      default: symb_tile<4>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringk[wib], ringo[wib], out, fo); break;
+      case 1: symb_tile<1, OutT, PEER>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringk[wib], ringo[wib], out, fo, &PT); break;
+      case 2: symb_tile<2, OutT, PEER>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringk[wib], ringo[wib], out, fo, &PT); break;
+      case 3: symb_tile<3, OutT, PEER>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringk[wib], ringo[wib], out, fo, &PT); break;
+      default: symb_tile<4, OutT, PEER>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringk[wib], ringo[wib], out, fo, &PT); break;
     }
 #pragma unroll
     for (int t = 0; t < 4; ++t)
@@ -1953,6 +1982,63 @@ static rbf_status matvec_f32_solver(rbf_ctx* ctx, const rbf_cells* c, const Kern
   const int64_t base = sym ? V.o0 : V.h0;
   const int64_t nw = V.h1 - base;
   const WT* w_win = w_loc;
+  // slab partition over a peer-memory transport (loopback, CUDA IPC), wide
+  // symmetric operator: ONE kernel reads the upper ranks' packed sources and
+  // adds the source-side sums into their accumulators in place, through peer
+  // memory -- no halo exchange, no reverse halo reduction
+  if (ctx->world > 1 && sym == 2 && ctx->peer_mem && ctx->tr->peer_capable() && c->order_w.p) {
+    const SlabPlan& P = c->plan;
+    PeerTab PT{};
+    PT.n = 0;
+    for (int q = ctx->rank; q < P.world && P.own_lo[q] < V.h1; ++q) {
+      if (PT.n == kPeerMax) { PT.n = -1; break; }
+      PT.lo[PT.n++] = P.own_lo[q];
+    }
+    if (PT.n > 0) {
+      PT.lo[PT.n] = V.h1;
+      // rank q's buffer: its packed sources, then (256-B aligned) its fp64 sums
+      auto f_off = [&](int q) { return ((uint64_t)(P.own_hi[q] - P.own_lo[q]) * sizeof(float4) + 255) & ~(uint64_t)255; };
+      const int64_t no = V.o1 - V.o0;
+      const uint64_t need = f_off(ctx->rank) + (uint64_t)no * sizeof(double);
+      std::vector<void*> bufs;
+      auto stage = [&](void* mine) -> rbf_status {
+        if (no > 0) {
+          if constexpr (std::is_same<WT, double>::value)
+            pack_src_f64w<<<grid_for(no, 256), 256, 0, s>>>(c->sorted.as<float4>() + V.o0, w_loc, no,
+                                                            static_cast<float4*>(mine));
+          else
+            pack_src_f32<<<grid_for(no, 256), 256, 0, s>>>(c->sorted.as<float4>() + V.o0, w_loc, no,
+                                                           static_cast<float4*>(mine));
+          RBF_CHECK_LAUNCH();
+          RBF_CUDA_TRY(cudaMemsetAsync(static_cast<char*>(mine) + f_off(ctx->rank), 0, sizeof(double) * no, s));
+        }
+        return RBF_OK;
+      };
+      RBF_TRY(ctx->tr->peer_begin(ctx, s, need, stage, &bufs));
+      for (int k = 0; k < PT.n; ++k) {
+        const int q = ctx->rank + k;
+        PT.src[k] = static_cast<const float4*>(bufs[q]) - P.own_lo[q];
+        PT.f[k] = reinterpret_cast<double*>(static_cast<char*>(bufs[q]) + f_off(q)) - P.own_lo[q];
+      }
+      RBF_TRY(ctx->counter.ensure(256, s));
+      RBF_CUDA_TRY(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), s));
+      SumGeom G = make_geom(c, kp);
+      {
+        ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
+        auto kfn = sum_f32_symb_kernel<double, true>;
+        kfn<<<sum_blocks(ctx, kfn), kSumWarps * 32, 0, s>>>(G, c->cell_start.as<int32_t>(), PT.src[0],
+                                                            c->tiles_w.as<int2>(), c->tile_box_w.as<float4>(),
+                                                            V.tw1 - V.tw0, V.tw0, PT.f[0], ctx->counter.as<int>(),
+                                                            V.h1, c->order_w.as<int32_t>(), PT);
+        RBF_CHECK_LAUNCH();
+      }
+      RBF_TRY(ctx->tr->peer_end(ctx, s));   // every rank's kernel has added into my sums
+      if (no > 0)
+        RBF_CUDA_TRY(cudaMemcpyAsync(f_loc, static_cast<char*>(bufs[ctx->rank]) + f_off(ctx->rank),
+                                     sizeof(double) * no, cudaMemcpyDeviceToDevice, s));
+      return RBF_OK;
+    }
+  }
   // slab partition, wide symmetric operator: the upper halo is exchanged and
   // packed on the aux stream while the interior tiles (no halo sources) run
   const bool overlap = ctx->world > 1 && sym >= 2 && V.tw_int > 0 && c->order_w.p;
@@ -2013,14 +2099,15 @@ static rbf_status matvec_f32_solver(rbf_ctx* ctx, const rbf_cells* c, const Kern
       ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
       kfn<<<sum_blocks(ctx, kfn), kSumWarps * 32, 0, s>>>(G, c->cell_start.as<int32_t>(), srcb, c->tiles_w.as<int2>(),
                                                           c->tile_box_w.as<float4>(), ni, V.tw0, fwin - base,
-                                                          ctx->counter.as<int>(), V.h1, c->order_w.as<int32_t>());
+                                                          ctx->counter.as<int>(), V.h1, c->order_w.as<int32_t>(),
+                                                          PeerTab{});
       RBF_CHECK_LAUNCH();
       // join: the halo tiles after the halo
       RBF_CUDA_TRY(cudaStreamWaitEvent(s, ctx->halo_ev[1], 0));
       if (nb > 0) {
         kfn<<<sum_blocks(ctx, kfn), kSumWarps * 32, 0, s>>>(
             G, c->cell_start.as<int32_t>(), srcb, c->tiles_w.as<int2>(), c->tile_box_w.as<float4>(), nb, V.tw0,
-            fwin - base, ctx->counter.as<int>() + 1, V.h1, c->order_w.as<int32_t>() + ni);
+            fwin - base, ctx->counter.as<int>() + 1, V.h1, c->order_w.as<int32_t>() + ni, PeerTab{});
         RBF_CHECK_LAUNCH();
       }
     }
@@ -2055,7 +2142,8 @@ static rbf_status matvec_f32_solver(rbf_ctx* ctx, const rbf_cells* c, const Kern
         auto kfn = sym == 3 ? sum_f32_symr_kernel<double> : sum_f32_symb_kernel<double>;
         kfn<<<sum_blocks(ctx, kfn), kSumWarps * 32, 0, s>>>(
             G, c->cell_start.as<int32_t>(), srcb, c->tiles_w.as<int2>(), c->tile_box_w.as<float4>(), V.tw1 - V.tw0,
-            V.tw0, fwin - base, ctx->counter.as<int>(), V.h1, c->order_w.p ? c->order_w.as<int32_t>() : nullptr);
+            V.tw0, fwin - base, ctx->counter.as<int>(), V.h1, c->order_w.p ? c->order_w.as<int32_t>() : nullptr,
+            PeerTab{});
       } else {
         sum_f32_kernel<0, false, double, true>
             <<<sum_blocks(ctx, sum_f32_kernel<0, false, double, true>), kSumWarps * 32, 0, s>>>(

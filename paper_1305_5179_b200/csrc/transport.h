@@ -17,6 +17,7 @@
 // counts).  All transfers are stream-ordered on the given stream.
 #pragma once
 #include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <vector>
 
@@ -37,6 +38,20 @@ struct Transport {
   virtual rbf_status exchange(rbf_ctx* ctx, cudaStream_t s, const std::vector<Xfer>& sends,
                               const std::vector<Xfer>& recvs, DType t) = 0;
   virtual rbf_status allreduce_sum(rbf_ctx* ctx, cudaStream_t s, void* buf, int64_t count, DType t) = 0;
+  // Peer-memory mode (transports whose ranks can address each other's device
+  // memory: loopback and CUDA IPC).  peer_begin: every rank's device buffer of
+  // `need` bytes (one per rank, symmetric role; grown collectively), `stage`
+  // fills mine on stream s, then -- ordered by events and a host barrier -- the
+  // peers' buffers are ready and addressable here: peers[q] points at rank q's
+  // buffer (mine at [rank]).  Until peer_end the caller's kernels may read and
+  // atomically update any rank's buffer; peer_end orders every rank after all
+  // ranks' kernels (no buffer is reused before its readers and writers are done).
+  virtual bool peer_capable() const { return false; }
+  virtual rbf_status peer_begin(rbf_ctx*, cudaStream_t, uint64_t, const std::function<rbf_status(void*)>&,
+                                std::vector<void*>*) {
+    return RBF_EUNSUPPORTED;
+  }
+  virtual rbf_status peer_end(rbf_ctx*, cudaStream_t) { return RBF_EUNSUPPORTED; }
 };
 
 // Shared state of a loopback group (library-owned; rbf_loopback_group_*).
@@ -49,6 +64,7 @@ struct LoopGroup {
   struct Slot {
     std::vector<Xfer> sends;
     const void* buf = nullptr;
+    void* peer_buf = nullptr;   // peer-memory mode: this rank's buffer
     cudaEvent_t ready = nullptr, done = nullptr;
   };
   std::vector<Slot> slots;

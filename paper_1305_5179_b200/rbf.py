@@ -93,6 +93,7 @@ EXPORTS = {
     "rbf_loopback_group_free": (None, [_P]),
     "rbf_create_loopback": (C.c_int, [C.POINTER(_P), C.c_int, _P, _P, C.c_int]),
     "rbf_create_ipc": (C.c_int, [C.POINTER(_P), C.c_int, _P, _P, C.c_int, C.c_int]),
+    "rbf_ctx_peer_memory": (C.c_int, [_P, C.c_int]),
     "rbf_slab_plan": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, _P, _P, _P, _P, _P]),
     "rbf_extend_points": (C.c_int, [_P, _P, _P, C.c_int64, C.c_double, C.c_double, _P, _P]),
     "rbf_build_cells": (C.c_int, [_P, _P, C.c_int64, C.POINTER(_Kernel), C.POINTER(_CellCfg),
@@ -307,6 +308,11 @@ class Context:
         self._h = h
 
     PROF_STAGES = ("cells", "matvec_f32", "matvec_f64", "grid", "precond_setup", "precond_apply")
+
+    def peer_memory(self, on: bool = True):
+        """rbf_ctx_peer_memory: the peer-memory (fused halo) form of the symmetric
+        operator on transports that support it (default on)."""
+        _check(_lib.rbf_ctx_peer_memory(self._h, 1 if on else 0))
 
     def profile(self, on: bool = True):
         """rbf_profile_enable: bracket the library's stage launches with CUDA events."""

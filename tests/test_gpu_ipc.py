@@ -57,7 +57,8 @@ def test_ipc_transport_multiprocess(tmp_path, world):
             assert np.array_equal(r[f"{k}_d"].view(np.uint8), r[f"{k}_s"].view(np.uint8)), k
         for k, tol in (("symw32", 1e-5), ("symw64", 1e-12)):
             scale = np.abs(r[f"{k}_s"]).max()
-            assert np.abs(r[f"{k}_d"] - r[f"{k}_s"]).max() <= tol * scale, k
+            assert np.abs(r[f"{k}_d"] - r[f"{k}_s"]).max() <= tol * scale, k        # peer-memory form
+            assert np.abs(r[f"{k}_copy"] - r[f"{k}_s"]).max() <= tol * scale, k     # copy-based halo form
         np.testing.assert_array_equal(r["w_solve"], res[0]["w_solve"])
     d = make_inputs("c1", n=8000, sigma=0.035, delta=0.0035)
     X = OE.extend(d["x"], d["normals"], d["delta"]).astype(np.float32).astype(np.float64)

@@ -121,6 +121,13 @@ def test_loopback_partition_products_and_grid(R, setup, world):
         for op in ("OP_SYM", "OP_SYM_WIDE", "OP_SYM_ROT", "OP_ONESIDED"):
             res[op] = (R.matvec_op(ctx, c, s["kern"], wt.float(), op=getattr(R, op)).cpu().numpy(),
                        R.matvec_op(ctx, c, s["kern"], wt, op=getattr(R, op)).cpu().numpy())
+        # the wide operator's two distributed forms: peer memory (default on this
+        # transport: one kernel reads and updates the other ranks' buffers) and
+        # the copy-based halo exchange + reverse reduction (NCCL's form)
+        ctx.peer_memory(False)
+        res["OP_SYM_WIDE_copy"] = (R.matvec_op(ctx, c, s["kern"], wt.float(), op=R.OP_SYM_WIDE).cpu().numpy(),
+                                   R.matvec_op(ctx, c, s["kern"], wt, op=R.OP_SYM_WIDE).cpu().numpy())
+        ctx.peer_memory(True)
         res["F"] = R.eval_grid(ctx, c, s["kern"], wt, lo, hi, gn).cpu().numpy()
         part = torch.full((gn[2], gn[1], gn[0]), -1.0, device="cuda")
         res["layers"] = R.eval_grid_slab(ctx, c, s["kern"], wt, lo, hi, gn, part)
@@ -154,7 +161,7 @@ def test_loopback_partition_products_and_grid(R, setup, world):
         assert (res["part"][:k0] == -1).all() and (res["part"][k1:] == -1).all()
         layers[k0:k1] += 1
         # solver operators across slabs against the oracle (tier tolerances)
-        for op in ("OP_SYM", "OP_SYM_WIDE", "OP_SYM_ROT", "OP_ONESIDED"):
+        for op in ("OP_SYM", "OP_SYM_WIDE", "OP_SYM_ROT", "OP_ONESIDED", "OP_SYM_WIDE_copy"):
             a32, a64 = res[op]
             assert (np.abs(a32 - s["ref32"]) <= 5e-5 * s["g"]).all(), (op, r)
             assert (np.abs(a64 - s["ref64"]) <= 1e-12 * s["g"]).all(), (op, r)
@@ -263,8 +270,9 @@ def test_loopback_distributed_solve(R, world):
     w1, rep1 = R.gmres_solve(ctx1, cells1, kern, torch.as_tensor(b, device="cuda"), **kw)
     res1 = np.linalg.norm(b - OK.matvec(X.astype(np.float64), w1.cpu().numpy(), sigma)) / np.linalg.norm(b)
     assert res1 <= 1.5e-6, (res1, rep1)
-    for op in (R.OP_AUTO, R.OP_SYM_WIDE, R.OP_ONESIDED):
+    for op, peer in ((R.OP_AUTO, True), (R.OP_SYM_WIDE, True), (R.OP_SYM_WIDE, False), (R.OP_ONESIDED, True)):
         def rank(ctx, r):
+            ctx.peer_memory(peer)
             c = R.Cells(ctx, torch.as_tensor(X, device="cuda"), kern)
             w, rep = R.gmres_solve(ctx, c, kern, torch.as_tensor(b, device="cuda"), op=op, **kw)
             return w.cpu().numpy(), rep

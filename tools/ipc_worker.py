@@ -34,6 +34,10 @@ kern = R.Kernel(d["sigma"])
 w = torch.as_tensor(np.random.default_rng(3).normal(size=X.shape[0]), device="cuda")
 cd, cs = R.Cells(ctx, X, kern), R.Cells(solo, X, kern)
 res["slab"] = np.array(cd.slab()["own"])
+ctx.peer_memory(False)   # the copy-based halo form of the wide operator, then the peer-memory form (default)
+res["symw32_copy"] = R.matvec_op(ctx, cd, kern, w.float(), op=R.OP_SYM_WIDE).cpu().numpy()
+res["symw64_copy"] = R.matvec_op(ctx, cd, kern, w, op=R.OP_SYM_WIDE).cpu().numpy()
+ctx.peer_memory(True)
 for name, ctx_, c in (("d", ctx, cd), ("s", solo, cs)):
     res[f"mv32_{name}"] = R.matvec(ctx_, c, kern, w.float()).cpu().numpy()
     res[f"mv64_{name}"] = R.matvec(ctx_, c, kern, w).cpu().numpy()
