@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-rows", type=int, default=0)
     ap.add_argument("--fit-iters", type=int, default=50)
+    ap.add_argument("--weak", action="store_true",
+                    help="c5 weak scaling (configs[4]): 1.25M points per GPU, sigma scaled to keep sigma/spacing")
     ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
                     help="N>1 slab mode: the library's data plane over CUDA-IPC peer memory (default; the transport "
                          "the multi-process GPU tests run) or over NCCL send/recv + allreduce")
@@ -231,10 +233,22 @@ def gate_note(cfg_name: str):
         return None
 
 
-def make_problem(cfg_name: str, seed: int):
+def make_problem(cfg_name: str, seed: int, weak_world: int = 0):
+    """weak_world = G > 0 (c5 only, BASELINE configs[4] "weak scaling from 1.25M
+    points per GPU at 8 B200"; SURVEY §8(c) reading 15): N = 1.25M G points,
+    sigma = 0.004 sqrt(8/G) (constant sigma/spacing: constant work per GPU),
+    grid n = round(512 (G/8)^(1/3)), delta = 0.1 sigma."""
     from synth import make_inputs
     t = time.time()
-    d = make_inputs(cfg_name, seed=seed)
+    if weak_world:
+        if cfg_name != "c5":
+            raise SystemExit("--weak applies to c5 (BASELINE configs[4])")
+        g = weak_world
+        sig = 0.004 * (8.0 / g) ** 0.5
+        d = make_inputs(cfg_name, seed=seed, n=1250000 * g, sigma=sig, delta=0.1 * sig,
+                        grid_n=int(round(512 * (g / 8.0) ** (1.0 / 3.0))))
+    else:
+        d = make_inputs(cfg_name, seed=seed)
     d["gen_s"] = time.time() - t
     return d
 
@@ -256,7 +270,7 @@ def run_ours(args, rank, world, local):
             dist.init_process_group("nccl", device_id=dev)
     red_dev = None if shared else dev   # device of the max/sum reductions of the timings
     slab = world > 1 and args.parallel == "slab"
-    d = make_problem(args.config, args.seed if slab else args.seed + rank)
+    d = make_problem(args.config, args.seed if slab else args.seed + rank, world if args.weak else 0)
     cfg = d["cfg"]
     ctx = R.Context(local, distributed=slab, transport=args.transport)
     kern = R.Kernel(d["sigma"], d["cutoff_sigmas"])
@@ -430,7 +444,7 @@ def run_ours(args, rank, world, local):
     out = {
         "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "fit_eval_s": ms_max / args.steps / 1e3,
-        "higher_is_better": True, "scaling": "strong" if slab else "weak", "vs_baseline": None, "dtype": "f32+f64",
+        "higher_is_better": True, "scaling": "strong" if slab and not args.weak else "weak", "vs_baseline": None, "dtype": "f32+f64",
         "data": "synthetic (seeded blobby surface, SURVEY §8(c) reading 14)",
         "config": {"workload": f"{args.config}: {cfg.kind} K={cfg.kw.get('K')} N={cfg.n} surface points "
                                f"({3 * cfg.n} centres), sigma={cfg.sigma}, cutoff 6 sigma, GMRES({cfg.restart}) "
@@ -573,7 +587,7 @@ def run_reference(args, rank, world, local):
     v = float(np.median(vals))
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "pairs/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(times)) * 1e3,
-           "higher_is_better": True, "scaling": "strong" if world > 1 and args.parallel == "slab" else "weak",
+           "higher_is_better": True, "scaling": "strong" if world > 1 and args.parallel == "slab" and not args.weak else "weak",
            "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "config": {"workload": f"{args.config}: N={cfg.n} ({3 * cfg.n} centres) "
                                                       f"sampled-row brute-force matvec"},
