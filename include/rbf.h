@@ -280,6 +280,16 @@ rbf_status rbf_extend_points(rbf_ctx* ctx, const double* x, const double* nrm, i
  * during the call.  n >= 1.  Non-finite coordinates => RBF_EINVAL.
  * Synchronises once (reads back the bounding box to size the grid of cells).
  * *out receives a library-owned handle (free with rbf_cells_free). */
+/* Sharded input: rank r passes its shard of the caller-order
+ * centres, xyz_local (DEVICE fp32 n_local x 3) = global ids [id0, id0 + n_local);
+ * the shards of all ranks must tile [0, n_total) (any assignment of ranges to
+ * ranks, ranks with n_local = 0 allowed).  The library gathers the shards
+ * (transport exchange) and builds the same cells as rbf_build_cells on the full
+ * array -- every rank holds the replicated geometry, the work stays sharded
+ * (reading R22).  Single GPU: id0 = 0, n_local = n.  Errors as
+ * rbf_build_cells, plus RBF_EINVAL when the shards do not tile [0, n_total). */
+rbf_status rbf_build_cells_shard(rbf_ctx* ctx, const float* xyz_local, int64_t n_local, int64_t id0,
+                                 const rbf_kernel* kern, const rbf_cell_cfg* cfg, rbf_cells** out);
 rbf_status rbf_build_cells(rbf_ctx* ctx, const float* xyz, int64_t n,
                            const rbf_kernel* kern, const rbf_cell_cfg* cfg,
                            rbf_cells** out);
@@ -359,6 +369,16 @@ rbf_status rbf_gmres_solve(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kerne
                            const rbf_precond* precond, const rbf_precond_cfg* pcfg,
                            const rbf_gmres_cfg* gcfg, const float* b, double* w,
                            rbf_solve_report* rep);
+
+/* Sharded form of rbf_gmres_solve: b_local (DEVICE fp32) is this rank's shard
+ * [id0, id0 + n_local) of the caller-order right-hand side, w_local (DEVICE
+ * fp64) receives the same shard of the weights; the shards tile [0, n) as in
+ * rbf_build_cells_shard (n = the cells' centre count, else RBF_EINVAL).
+ * Synchronises; report as rbf_gmres_solve. */
+rbf_status rbf_gmres_solve_shard(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern,
+                                 const rbf_precond* precond, const rbf_precond_cfg* pcfg, const rbf_gmres_cfg* gcfg,
+                                 const float* b_local, int64_t n_local, int64_t id0, double* w_local,
+                                 rbf_solve_report* rep);
 
 /* ---- a8: grid evaluation F(xi) = sum_j A(xi, x_j) w_j (Eq.5) --------------
  * w: DEVICE fp64 (n, caller order); field: DEVICE fp32, n0*n1*n2, x fastest.

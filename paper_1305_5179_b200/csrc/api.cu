@@ -251,6 +251,22 @@ void rbf_destroy(rbf_ctx* ctx) {
   if (cudaMemPool_t pool = lib_pool(dev)) cudaMemPoolTrimTo(pool, 0);
 }
 
+rbf_status rbf_build_cells_shard(rbf_ctx* ctx, const float* xyz_local, int64_t n_local, int64_t id0,
+                                 const rbf_kernel* kern, const rbf_cell_cfg* cfg, rbf_cells** out) {
+  if (!ctx || !out) { set_error("ctx/out is NULL"); return RBF_EINVAL; }
+  *out = nullptr;
+  if (n_local < 0 || id0 < 0 || (n_local > 0 && !xyz_local)) { set_error("bad shard"); return RBF_EINVAL; }
+  RBF_CUDA_TRY(cudaSetDevice(ctx->device));
+  std::vector<int64_t> id0s, ns;
+  int64_t total = 0;
+  RBF_TRY(shard_layout(ctx, id0, n_local, id0s, ns, &total));
+  if (total < 1 || total > (int64_t)INT32_MAX / 2) { set_error("n out of range"); return RBF_EINVAL; }
+  DevBuf full;
+  RBF_TRY(full.alloc(sizeof(float) * 3 * total, ctx->stream));
+  RBF_TRY(allgather_shards(ctx, xyz_local, id0s, ns, 3, full.p, DType::F32));
+  return rbf_build_cells(ctx, full.as<float>(), total, kern, cfg, out);
+}
+
 rbf_status rbf_build_cells(rbf_ctx* ctx, const float* xyz, int64_t n, const rbf_kernel* kern,
                            const rbf_cell_cfg* cfg, rbf_cells** out) {
   if (!ctx || !out) { set_error("ctx/out is NULL"); return RBF_EINVAL; }

@@ -437,6 +437,58 @@ rbf_status halo_reduce(rbf_ctx* ctx, const rbf_cells* c, const double* fwin, dou
   return RBF_OK;
 }
 
+// Every rank's shard (id0, n) of a caller-order array; checks that the shards
+// tile [0, total) (any order of ranks, no overlap, no gap).
+rbf_status shard_layout(rbf_ctx* ctx, int64_t id0, int64_t n_local, std::vector<int64_t>& id0s,
+                        std::vector<int64_t>& ns, int64_t* total) {
+  const int W = ctx->world;
+  id0s.assign(W, 0);
+  ns.assign(W, 0);
+  if (W == 1) {
+    id0s[0] = id0;
+    ns[0] = n_local;
+  } else {
+    DevBuf d;
+    RBF_TRY(d.alloc(sizeof(double) * 2 * W, ctx->stream));
+    std::vector<double> h(2 * W, 0.0);
+    h[2 * ctx->rank] = (double)id0;
+    h[2 * ctx->rank + 1] = (double)n_local;
+    RBF_CUDA_TRY(cudaMemcpyAsync(d.p, h.data(), sizeof(double) * 2 * W, cudaMemcpyHostToDevice, ctx->stream));
+    RBF_TRY(allreduce_sum(ctx, d.as<double>(), 2 * W));
+    RBF_CUDA_TRY(cudaMemcpyAsync(h.data(), d.p, sizeof(double) * 2 * W, cudaMemcpyDeviceToHost, ctx->stream));
+    RBF_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    for (int q = 0; q < W; ++q) { id0s[q] = (int64_t)h[2 * q]; ns[q] = (int64_t)h[2 * q + 1]; }
+  }
+  std::vector<int> ord(W);
+  for (int q = 0; q < W; ++q) ord[q] = q;
+  std::sort(ord.begin(), ord.end(), [&](int a, int b) { return id0s[a] < id0s[b]; });
+  int64_t at = 0;
+  for (int q : ord) {
+    if (ns[q] < 0 || id0s[q] != at) { set_error("shards must tile [0, n_total) (id0 of each rank = sum of the lower shards)"); return RBF_EINVAL; }
+    at += ns[q];
+  }
+  *total = at;
+  return RBF_OK;
+}
+
+// full[id0_q * per ..] <- rank q's shard of `per` elements per item, for every q
+rbf_status allgather_shards(rbf_ctx* ctx, const void* local, const std::vector<int64_t>& id0s,
+                            const std::vector<int64_t>& ns, int per, void* full, DType t) {
+  const size_t es = (size_t)t;
+  const int r = ctx->rank;
+  if (ns[r] > 0)
+    RBF_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(full) + es * per * id0s[r], local, es * per * ns[r],
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
+  if (ctx->world == 1) return RBF_OK;
+  std::vector<Xfer> sends, recvs;
+  for (int q = 0; q < ctx->world; ++q) {
+    if (q == r) continue;
+    if (ns[r] > 0) sends.push_back(Xfer{q, const_cast<void*>(local), ns[r] * per});
+    if (ns[q] > 0) recvs.push_back(Xfer{q, static_cast<char*>(full) + es * per * id0s[q], ns[q] * per});
+  }
+  return ctx->tr->exchange(ctx, ctx->stream, sends, recvs, t);
+}
+
 rbf_status allreduce_sum(rbf_ctx* ctx, double* x, int64_t count) {
   if (ctx->world == 1 || count == 0) return RBF_OK;
   return ctx->tr->allreduce_sum(ctx, ctx->stream, x, count, DType::F64);

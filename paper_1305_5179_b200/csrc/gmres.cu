@@ -25,6 +25,7 @@
 
 #include "internal.h"
 #include "solver.h"
+#include "transport.h"
 
 namespace rbf {
 namespace {
@@ -540,6 +541,29 @@ rbf_status rbf_gmres_solve(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* k
   delete own;
   if (rep) *rep = R;
   return st;
+}
+
+rbf_status rbf_gmres_solve_shard(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern,
+                                 const rbf_precond* precond, const rbf_precond_cfg* pcfg, const rbf_gmres_cfg* gcfg,
+                                 const float* b_local, int64_t n_local, int64_t id0, double* w_local,
+                                 rbf_solve_report* rep) {
+  if (!ctx || !c) { set_error("NULL argument"); return RBF_EINVAL; }
+  if (n_local < 0 || id0 < 0 || (n_local > 0 && (!b_local || !w_local))) { set_error("bad shard"); return RBF_EINVAL; }
+  RBF_CUDA_TRY(cudaSetDevice(ctx->device));
+  std::vector<int64_t> id0s, ns;
+  int64_t total = 0;
+  RBF_TRY(shard_layout(ctx, id0, n_local, id0s, ns, &total));
+  if (total != c->n) { set_error("the shards of b do not cover the cells' centres"); return RBF_EINVAL; }
+  DevBuf bf, wf;
+  RBF_TRY(bf.alloc(sizeof(float) * total, ctx->stream));
+  RBF_TRY(wf.alloc(sizeof(double) * total, ctx->stream));
+  RBF_TRY(allgather_shards(ctx, b_local, id0s, ns, 1, bf.p, DType::F32));
+  RBF_TRY(rbf_gmres_solve(ctx, c, kern, precond, pcfg, gcfg, bf.as<float>(), wf.as<double>(), rep));
+  if (n_local > 0)
+    RBF_CUDA_TRY(cudaMemcpyAsync(w_local, wf.as<double>() + id0, sizeof(double) * n_local, cudaMemcpyDeviceToDevice,
+                                 ctx->stream));
+  RBF_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return RBF_OK;
 }
 
 rbf_status rbf_reconstruct_host(rbf_ctx* ctx, const float* xyz, const float* b, int64_t n, const rbf_kernel* kern,

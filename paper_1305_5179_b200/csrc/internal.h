@@ -271,6 +271,10 @@ rbf_status halo_exchange(rbf_ctx* ctx, const rbf_cells* c, const T* x_loc, T* wi
 rbf_status halo_reduce(rbf_ctx* ctx, const rbf_cells* c, const double* fwin, double* f_loc);
 rbf_status allreduce_sum(rbf_ctx* ctx, double* x, int64_t count);
 rbf_status allgather_sorted(rbf_ctx* ctx, const rbf_cells* c, double* full);
+// sharded caller-order inputs (rank r holds items [id0_r, id0_r + n_r)): every
+// rank's (id0, n), checked to tile [0, total); and the replicated array from the shards
+rbf_status shard_layout(rbf_ctx* ctx, int64_t id0, int64_t n_local, std::vector<int64_t>& id0s,
+                        std::vector<int64_t>& ns, int64_t* total);
 // the grid's node layers [k0, k1) owned by rank r (z layers; a layer belongs to
 // the rank owning the cell plane of its first node block)
 void grid_layers(const rbf_cells* c, const rbf_grid* g, int r, int64_t* k0, int64_t* k1);

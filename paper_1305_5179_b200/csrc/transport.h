@@ -83,6 +83,8 @@ struct LoopGroup {
 };
 
 Transport* make_nccl_transport(void* comm);
+rbf_status allgather_shards(rbf_ctx* ctx, const void* local, const std::vector<int64_t>& id0s,
+                            const std::vector<int64_t>& ns, int per, void* full, DType t);
 // ipc.cu: CUDA-IPC peer-memory transport (one process per GPU, one node)
 rbf_status make_ipc_transport(int device, const void* key16, int rank, int world, Transport** out);
 Transport* make_loop_transport(LoopGroup* g, int rank);

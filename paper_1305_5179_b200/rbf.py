@@ -96,6 +96,10 @@ EXPORTS = {
     "rbf_ctx_peer_memory": (C.c_int, [_P, C.c_int]),
     "rbf_slab_plan": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, _P, _P, _P, _P, _P]),
     "rbf_extend_points": (C.c_int, [_P, _P, _P, C.c_int64, C.c_double, C.c_double, _P, _P]),
+    "rbf_build_cells_shard": (C.c_int, [_P, _P, C.c_int64, C.c_int64, C.POINTER(_Kernel), C.POINTER(_CellCfg),
+                                        C.POINTER(_P)]),
+    "rbf_gmres_solve_shard": (C.c_int, [_P, _P, C.POINTER(_Kernel), _P, C.POINTER(_PrecondCfg),
+                                        C.POINTER(_GmresCfg), _P, C.c_int64, C.c_int64, _P, C.POINTER(SolveReport)]),
     "rbf_build_cells": (C.c_int, [_P, _P, C.c_int64, C.POINTER(_Kernel), C.POINTER(_CellCfg),
                                   C.POINTER(_P)]),
     "rbf_cells_free": (None, [_P]),
@@ -356,16 +360,24 @@ class Cells:
     """rbf_build_cells: cell list + tile plan over the centres (Alg.2 'truncation area')."""
 
     def __init__(self, ctx: Context, xyz: torch.Tensor, kernel: Kernel, cell_edge: float = 0.0,
-                 tile_cap: int = 64, tile_span: int = 2, tile_mode: int = 0):
+                 tile_cap: int = 64, tile_span: int = 2, tile_mode: int = 0, id0: int | None = None):
+        """id0 given: xyz is this rank's shard, global ids [id0, id0 + len(xyz))
+        (rbf_build_cells_shard); otherwise the full (replicated) centre set."""
         _need(xyz, torch.float32, name="xyz")
         if xyz.dim() != 2 or xyz.shape[1] != 3:
             raise ValueError("xyz must be (n, 3)")
         self.ctx, self.kernel = ctx, kernel
-        self.n = xyz.shape[0]
         h = C.c_void_p()
         cfg = _CellCfg(cell_edge, tile_cap, tile_span, tile_mode)
-        _check(_lib.rbf_build_cells(ctx._h, _ptr(xyz), self.n, C.byref(kernel._c()), C.byref(cfg),
-                                    C.byref(h)))
+        if id0 is None:
+            self.n = xyz.shape[0]
+            _check(_lib.rbf_build_cells(ctx._h, _ptr(xyz), self.n, C.byref(kernel._c()), C.byref(cfg),
+                                        C.byref(h)))
+        else:
+            _check(_lib.rbf_build_cells_shard(ctx._h, _ptr(xyz), xyz.shape[0], int(id0), C.byref(kernel._c()),
+                                              C.byref(cfg), C.byref(h)))
+            self._h = h
+            self.n = self.info()["n"]
         self._h = h
 
     def info(self) -> dict:
@@ -689,6 +701,22 @@ def gmres_solve(ctx: Context, cells: Cells, kernel: Kernel, b: torch.Tensor, pre
         out_rep["history"] = list(hist[:rep.history_len])
         out_rep["history_true"] = list(hist_t[:rep.history_true_len])
     return w, out_rep
+
+
+def gmres_solve_shard(ctx: Context, cells: Cells, kernel: Kernel, b_local: torch.Tensor, id0: int,
+                      kind: int = 2, core_target: int = 512, overlap_sigmas: float = 1.0, restart: int = 30,
+                      rtol: float = 1e-6, phase1_rtol: float = 1e-4, max_iters: int = 500, polish_fp64: int = 1,
+                      shift: float = 0.0, local_fp32: int = 0, cgs_passes: int = 2, op: int = OP_AUTO):
+    """rbf_gmres_solve_shard: b_local = this rank's shard [id0, id0 + len) of b;
+    returns (this rank's shard of w, report dict)."""
+    _need(b_local, torch.float32, name="b_local")
+    w = torch.empty(b_local.shape[0], dtype=torch.float64, device=b_local.device)
+    pc = _PrecondCfg(kind, core_target, overlap_sigmas, 0, shift, local_fp32, 0, 0)
+    gc = _GmresCfg(restart, rtol, phase1_rtol, max_iters, polish_fp64, cgs_passes, int(op), 0, None, None, 0)
+    rep = SolveReport()
+    _check(_lib.rbf_gmres_solve_shard(ctx._h, cells._h, C.byref(kernel._c()), None, C.byref(pc), C.byref(gc),
+                                      _ptr(b_local), b_local.shape[0], int(id0), _ptr(w), C.byref(rep)))
+    return w, rep.as_dict()
 
 
 def reconstruct_host(ctx: Context, xyz, b, kernel: Kernel, lo, hi, n, *, cell_edge: float = 0.0,

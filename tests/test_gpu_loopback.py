@@ -345,3 +345,41 @@ def test_loopback_isosurface(R, setup, world):
         assert np.array_equal(F.view(np.uint32), F1.view(np.uint32))
         np.testing.assert_array_equal(V, V1)
         np.testing.assert_array_equal(T, T1)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_loopback_sharded_inputs(R, world):
+    """SURVEY §8(b)'s sharded interface: rank r passes only its shard of the
+    caller-order centres and right-hand side (global ids [id0, id0 + n_r); the
+    ranges are assigned to ranks in a shuffled order to exercise the tiling
+    check) and receives its shard of the weights -- equal bit for bit to the
+    replicated call's cells and weights."""
+    d = make_inputs("c1")
+    X = OE.extend(d["x"], d["normals"], d["delta"]).astype(np.float32)
+    b = OE.labels(len(d["x"]), d["delta"]).astype(np.float32)
+    kern = R.Kernel(d["sigma"])
+    kw = dict(restart=30, rtol=1e-6, kind=2, core_target=512, overlap_sigmas=3.0, max_iters=400)
+    n = len(X)
+    cuts = np.linspace(0, n, world + 1).astype(int)
+    order = np.random.default_rng(world).permutation(world)       # rank r holds range order[r]
+
+    def rank(ctx, r):
+        k = order[r]
+        lo, hi = int(cuts[k]), int(cuts[k + 1])
+        c = R.Cells(ctx, torch.as_tensor(X[lo:hi], device="cuda"), kern, id0=lo)
+        full = R.Cells(ctx, torch.as_tensor(X, device="cuda"), kern)
+        vs, vf = c.view(), full.view()
+        same = all(torch.equal(vs[key], vf[key]) for key in ("perm", "keys", "cell_start"))
+        ws, rep = R.gmres_solve_shard(ctx, c, kern, torch.as_tensor(b[lo:hi], device="cuda"), lo, **kw)
+        wf, _ = R.gmres_solve(ctx, full, kern, torch.as_tensor(b, device="cuda"), **kw)
+        return same, ws.cpu().numpy(), wf.cpu().numpy()[lo:hi], c.n
+
+    for same, ws, wf, nc in run_ranks(R, world, rank):
+        assert same and nc == n
+        np.testing.assert_array_equal(ws, wf)
+    # shards that do not tile [0, n) are rejected on every rank
+    def bad(ctx, r):
+        with pytest.raises(R.RbfError):
+            R.Cells(ctx, torch.as_tensor(X[:10], device="cuda"), kern, id0=5 * r + 1)
+        return True
+    assert all(run_ranks(R, world, bad))
