@@ -1,7 +1,7 @@
 #!/bin/bash
 # build_variant.sh NAME "NVCC -D flags" [files]: librbf with the given csrc files (default
 # summation.cu) recompiled under the flags, at paper_1305_5179_b200/variants/librbf_NAME.so
-# (tuning experiments; tools/bench_kernels.py --lib, tools/sess_var.sh)
+# (tuning experiments; tools/bench_kernels.py --lib, tools/sessions/sess_var.sh)
 set -e
 cd "$(dirname "$0")/.."
 python -m paper_1305_5179_b200.build >/dev/null
