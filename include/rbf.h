@@ -149,6 +149,11 @@ typedef struct {
   double* history;
   double* history_true;
   int history_cap;
+  /* Initial guess (DEVICE fp64, caller order, n entries; NULL => zero): resumes a
+   * solve from a checkpointed w (e.g. a restart boundary); the first
+   * residual is the true b - A x0 of the fp32 tier (fp64 once phase 2 starts).
+   * Not read by rbf_gmres_solve_shard (which starts from zero). */
+  const double* x0;
 } rbf_gmres_cfg;
 
 typedef struct {

@@ -269,6 +269,7 @@ rbf_status rbf_build_cells_shard(rbf_ctx* ctx, const float* xyz_local, int64_t n
 
 rbf_status rbf_build_cells(rbf_ctx* ctx, const float* xyz, int64_t n, const rbf_kernel* kern,
                            const rbf_cell_cfg* cfg, rbf_cells** out) {
+  RBF_NVTX("rbf_build_cells");
   if (!ctx || !out) { set_error("ctx/out is NULL"); return RBF_EINVAL; }
   *out = nullptr;
   RBF_TRY(check_kernel(kern));
@@ -369,6 +370,7 @@ extern "C" {
 
 rbf_status rbf_matvec(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, rbf_precision prec, const void* w,
                       void* f) {
+  RBF_NVTX("rbf_matvec");
   return matvec_impl(ctx, c, kern, prec, RBF_OP_ONESIDED, w, f);
 }
 
@@ -456,6 +458,7 @@ extern "C" {
 
 rbf_status rbf_eval_grid(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, const double* w,
                          const rbf_grid* g, float* field) {
+  RBF_NVTX("rbf_eval_grid");
   return eval_grid_impl(ctx, c, kern, w, g, field, true, nullptr, nullptr);
 }
 

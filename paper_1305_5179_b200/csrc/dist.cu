@@ -134,6 +134,7 @@ struct NcclTransport final : Transport {
     return RBF_OK;
   }
   rbf_status allreduce_sum(rbf_ctx*, cudaStream_t s, void* buf, int64_t count, DType t) override {
+  RBF_NVTX("allreduce_sum");
     if (count == 0) return RBF_OK;
     RBF_NCCL_TRY(nccl().AllReduce(buf, buf, (size_t)count, t == DType::F64 ? kNcclFloat64 : kNcclFloat32,
                                   kNcclSum, comm, s));
@@ -370,6 +371,7 @@ rbf_status dist_plan_cells(rbf_ctx* ctx, rbf_cells* c, const std::vector<uint32_
 // ------------------------------------------------------------- collectives --
 template <class T>
 rbf_status halo_exchange(rbf_ctx* ctx, const rbf_cells* c, const T* x_loc, T* win, bool upper_only) {
+  RBF_NVTX("halo_exchange");
   cudaStream_t s = ctx->stream;
   const SlabView& V = c->view;
   const SlabPlan& P = c->plan;
@@ -401,6 +403,7 @@ __global__ void add_into(double* __restrict__ dst, const double* __restrict__ sr
 }  // namespace
 
 rbf_status halo_reduce(rbf_ctx* ctx, const rbf_cells* c, const double* fwin, double* f_loc) {
+  RBF_NVTX("halo_reduce");
   cudaStream_t s = ctx->stream;
   const SlabView& V = c->view;
   const SlabPlan& P = c->plan;

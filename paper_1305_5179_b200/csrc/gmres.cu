@@ -263,7 +263,7 @@ struct Solver {
 
 rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp, const rbf_precond* P,
                         const rbf_gmres_cfg* gcfg, const float* b_sorted32, double* x_out_sorted,
-                        rbf_solve_report* rep) {
+                        rbf_solve_report* rep, const double* x0_sorted) {
   using clk = std::chrono::steady_clock;
   cudaStream_t s = ctx->stream;
   Solver S{ctx, c, P, kp, c->n_loc(), 30, 0};   // this rank's owned slice (all of it on one GPU)
@@ -331,8 +331,15 @@ rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp
     ~EvGuard() { cudaEventDestroy(e[0]); cudaEventDestroy(e[1]); }
   } ev_guard{ev};
   double t_switch = 0.0;
-  // r = b (x = 0)
-  RBF_CUDA_TRY(cudaMemcpyAsync(S.r.p, S.b.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  if (x0_sorted) {
+    // warm start: x = x0, r = b - A x0 (fp32 tier; phase 2 recomputes it in fp64)
+    RBF_CUDA_TRY(cudaMemcpyAsync(S.x.p, x0_sorted, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    RBF_TRY(S.residual(false, &beta));
+    last_beta = beta;
+  } else {
+    // r = b (x = 0)
+    RBF_CUDA_TRY(cudaMemcpyAsync(S.r.p, S.b.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  }
   double cycle_beta = -1.0;   // true residual at the start of the previous cycle
   for (;;) {
     // phase switch: phase-1 target reached, or the fp32 tier stopped making
@@ -359,6 +366,7 @@ rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp
     // inner stopping target: the phase-1 target only while a phase 2 follows
     const double target = (fp64 || !polish) ? rtol : std::max(p1tol, rtol);
     // one restart cycle on a basis of type VT (float: fp32 phase with basis32)
+    RBF_NVTX(fp64 ? "gmres cycle (fp64 tier)" : "gmres cycle (fp32 tier)");
     int k = 0;
     bool bd = false;
     auto cycle = [&](auto tag) -> rbf_status {
@@ -490,6 +498,7 @@ extern "C" {
 rbf_status rbf_gmres_solve(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* kern, const rbf_precond* precond,
                            const rbf_precond_cfg* pcfg, const rbf_gmres_cfg* gcfg, const float* b, double* w,
                            rbf_solve_report* rep) {
+  RBF_NVTX("rbf_gmres_solve");
   if (!ctx || !c || !kern || !b || !w) { set_error("NULL argument"); return RBF_EINVAL; }
   if (!(kern->sigma > 0) || !(kern->cutoff_sigmas > 0)) { set_error("bad kernel"); return RBF_EINVAL; }
   if (kern->cutoff_sigmas * kern->sigma > c->cutoff * (1 + 1e-12)) {
@@ -531,7 +540,15 @@ rbf_status rbf_gmres_solve(rbf_ctx* ctx, const rbf_cells* c, const rbf_kernel* k
   if (st == RBF_OK) st = gather_f32_to_sorted(ctx, b, c->perm.as<int32_t>(), bs.as<float>(), n);
   // the solve runs on this rank's slice [o0, o1) of the sorted order; the full
   // solution is gathered from all ranks (replicated out)
-  if (st == RBF_OK) st = gmres_sorted(ctx, c, kp, P, gcfg, bs.as<float>() + o0, xs.as<double>() + o0, &R);
+  DevBuf x0s;
+  const double* x0p = nullptr;
+  if (st == RBF_OK && gcfg && gcfg->x0) {
+    st = x0s.alloc(sizeof(double) * n, ctx->stream);
+    if (st == RBF_OK) st = gather_f64_to_sorted(ctx, gcfg->x0, c->perm.as<int32_t>(), x0s.as<double>(), n);
+    x0p = x0s.as<double>() + o0;
+  }
+  if (st == RBF_OK)
+    st = gmres_sorted(ctx, c, kp, P, gcfg, bs.as<float>() + o0, xs.as<double>() + o0, &R, x0p);
   if (st == RBF_OK) st = allgather_sorted(ctx, c, xs.as<double>());
   if (st == RBF_OK) st = scatter_f64_from_sorted(ctx, xs.as<double>(), c->perm.as<int32_t>(), w, n);
   if (st == RBF_OK) {
@@ -569,6 +586,7 @@ rbf_status rbf_gmres_solve_shard(rbf_ctx* ctx, const rbf_cells* c, const rbf_ker
 rbf_status rbf_reconstruct_host(rbf_ctx* ctx, const float* xyz, const float* b, int64_t n, const rbf_kernel* kern,
                                 const rbf_cell_cfg* ccfg, const rbf_precond_cfg* pcfg, const rbf_gmres_cfg* gcfg,
                                 const rbf_grid* grid, double* w_out, float* field_out, rbf_solve_report* rep) {
+  RBF_NVTX("rbf_reconstruct_host");
   if (!ctx || !xyz || !b || !kern || !grid || !w_out || !field_out) { set_error("NULL argument"); return RBF_EINVAL; }
   if (n < 1) { set_error("n must be >= 1"); return RBF_EINVAL; }
   for (int a = 0; a < 3; ++a)

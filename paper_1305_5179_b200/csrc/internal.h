@@ -9,6 +9,8 @@
 #include "../../include/rbf.h"
 #include "checks.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace rbf {
 
 struct Transport;
@@ -314,6 +316,18 @@ inline int grid_for(int64_t n, int threads, int max_blocks = 148 * 16) {
 
 namespace rbf {
 const char* last_error_cstr();
+
+// NVTX range over a library phase (timelines in Nsight Systems; a few ns when no
+// tool is attached).  RBF_NVTX("rbf_gmres_solve") at the top of a scope.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define RBF_NVTX_CAT2(a, b) a##b
+#define RBF_NVTX_CAT(a, b) RBF_NVTX_CAT2(a, b)
+#define RBF_NVTX(name) ::rbf::NvtxRange RBF_NVTX_CAT(rbf_nvtx_, __LINE__)(name)
 
 // Brackets the launches issued in its scope with CUDA events when profiling is on.
 struct ProfScope {

@@ -322,6 +322,7 @@ extern "C" {
 
 rbf_status rbf_eval_grid_masked(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern, const double* w,
                                 const rbf_grid* grid, const double* data, int64_t ndata, double eps, float* field) {
+  RBF_NVTX("rbf_eval_grid_masked");
   RBF_TRY(check_mesh_args(ctx, grid, data, ndata, eps));
   RBF_CUDA_TRY(cudaSetDevice(ctx->device));
   DevBuf near;
@@ -347,6 +348,7 @@ rbf_status rbf_mesh_from_field(rbf_ctx* ctx, const float* field, const rbf_grid*
 rbf_status rbf_isosurface(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern, const double* w,
                           const rbf_grid* grid, const double* data, int64_t ndata, double eps, float* field,
                           rbf_mesh** out) {
+  RBF_NVTX("rbf_isosurface");
   if (!out) { set_error("NULL argument"); return RBF_EINVAL; }
   *out = nullptr;
   RBF_TRY(check_mesh_args(ctx, grid, data, ndata, eps));

@@ -189,6 +189,7 @@ rbf_status build_near_mask(rbf_ctx* ctx, const rbf_grid* grid, const double* dat
 
 extern "C" rbf_status rbf_zero_set(rbf_ctx* ctx, const float* field, const rbf_grid* grid, const double* data,
                                    int64_t ndata, double eps, double* points, int64_t cap, int64_t* count) {
+  RBF_NVTX("rbf_zero_set");
   if (!ctx || !field || !grid || !count) { set_error("NULL argument"); return RBF_EINVAL; }
   if (ndata < 0 || (ndata > 0 && !data) || cap < 0 || (cap > 0 && !points)) { set_error("bad data/points"); return RBF_EINVAL; }
   if (!(eps > 0) || !std::isfinite(eps)) { set_error("eps must be finite and > 0"); return RBF_EINVAL; }

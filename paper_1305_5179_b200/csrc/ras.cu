@@ -1436,6 +1436,7 @@ extern "C" {
 
 rbf_status rbf_precond_create(rbf_ctx* ctx, const rbf_cells* cells, const rbf_kernel* kern,
                               const rbf_precond_cfg* cfg, rbf_precond** out) {
+  RBF_NVTX("rbf_precond_create");
   if (!ctx || !cells || !kern || !out) { set_error("NULL argument"); return RBF_EINVAL; }
   *out = nullptr;
   if (!(kern->sigma > 0)) { set_error("sigma must be > 0"); return RBF_EINVAL; }
@@ -1458,6 +1459,7 @@ rbf_status rbf_precond_create(rbf_ctx* ctx, const rbf_cells* cells, const rbf_ke
 void rbf_precond_free(rbf_precond* p) { delete p; }
 
 rbf_status rbf_precond_apply(rbf_ctx* ctx, const rbf_precond* P, const float* r, float* z) {
+  RBF_NVTX("rbf_precond_apply");
   if (!ctx || !P || !r || !z) { set_error("NULL argument"); return RBF_EINVAL; }
   if (r == z) { set_error("r and z must not alias"); return RBF_EINVAL; }
   RBF_CUDA_TRY(cudaSetDevice(ctx->device));

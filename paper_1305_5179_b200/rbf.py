@@ -53,7 +53,7 @@ class _GmresCfg(C.Structure):
                 ("max_iters", C.c_int), ("polish_fp64", C.c_int), ("cgs_passes", C.c_int),
                 ("op_variant", C.c_int), ("basis_fp64", C.c_int),
                 ("history", C.POINTER(C.c_double)), ("history_true", C.POINTER(C.c_double)),
-                ("history_cap", C.c_int)]
+                ("history_cap", C.c_int), ("x0", C.c_void_p)]
 
 
 class SolveReport(C.Structure):
@@ -682,17 +682,21 @@ def gmres_solve(ctx: Context, cells: Cells, kernel: Kernel, b: torch.Tensor, pre
                 rtol: float = 1e-6, phase1_rtol: float = 1e-4, max_iters: int = 500, polish_fp64: int = 1,
                 shift: float = 0.0, local_fp32: int = 0, cgs_passes: int = 2, out: torch.Tensor | None = None,
                 op: int = OP_AUTO, basis_fp64: int = 0, pivot: int = 0, w_layout: int = 0,
-                history_cap: int = 0):
+                history_cap: int = 0, x0: torch.Tensor | None = None):
     """Solve A w = b (Eq.4) with RAS-preconditioned FGMRES; returns (w fp64, report dict).
-    history_cap > 0 adds the residual history (report keys history / history_true)."""
+    history_cap > 0 adds the residual history (report keys history / history_true);
+    x0 (fp64, caller order) warm-starts the solve (resume from a checkpoint)."""
     _need(b, torch.float32, cells.n, "b")
+    if x0 is not None:
+        _need(x0, torch.float64, cells.n, "x0")
     w = torch.empty(cells.n, dtype=torch.float64, device=b.device) if out is None else out
     _need(w, torch.float64, cells.n, "w")
     pc = _PrecondCfg(kind, core_target, overlap_sigmas, 0, shift, local_fp32, pivot, w_layout)
     hist = (C.c_double * max(history_cap, 1))()
     hist_t = (C.c_double * max(history_cap, 1))()
     gc = _GmresCfg(restart, rtol, phase1_rtol, max_iters, polish_fp64, cgs_passes, int(op), basis_fp64,
-                   hist if history_cap > 0 else None, hist_t if history_cap > 0 else None, history_cap)
+                   hist if history_cap > 0 else None, hist_t if history_cap > 0 else None, history_cap,
+                   None if x0 is None else x0.data_ptr())
     rep = SolveReport()
     _check(_lib.rbf_gmres_solve(ctx._h, cells._h, C.byref(kernel._c()), None if precond is None else precond._h,
                                 C.byref(pc), C.byref(gc), _ptr(b), _ptr(w), C.byref(rep)))

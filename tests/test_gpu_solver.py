@@ -415,3 +415,23 @@ def test_fp32_phase_basis_matches_fp64_basis(R, ctx):
         assert rep["converged"] == 1 and res <= 1.5e-6, (basis, res, rep)
         reps[basis] = rep
     assert abs(reps["32"]["iters_phase1"] - reps["64"]["iters_phase1"]) <= 2, reps
+
+
+def test_warm_start_resumes_a_solve(R, ctx):
+    """rbf_gmres_cfg.x0 (checkpoint / resume): a solve stopped early and
+    resumed from its weights reaches the 1e-8 gate (certified by the ORACLE's fp64
+    matvec); resuming from converged weights takes no iteration."""
+    d, X, b = problem("c1")
+    sigma = d["sigma"]
+    kern = R.Kernel(sigma)
+    cells = R.Cells(ctx, dev(X, torch.float32), kern)
+    bd = dev(b, torch.float32)
+    kw = dict(restart=30, kind=2, core_target=512, overlap_sigmas=3.0)
+    w1, rep1 = R.gmres_solve(ctx, cells, kern, bd, rtol=1e-8, max_iters=8, **kw)        # stopped early
+    assert rep1["converged"] == 0
+    w2, rep2 = R.gmres_solve(ctx, cells, kern, bd, rtol=1e-8, max_iters=400, x0=w1, **kw)
+    res = np.linalg.norm(b - OK.matvec(X, host(w2), sigma)) / np.linalg.norm(b)
+    assert rep2["converged"] == 1 and res <= 1.5e-8, (res, rep2)
+    w3, rep3 = R.gmres_solve(ctx, cells, kern, bd, rtol=1e-8, max_iters=400, x0=w2, **kw)
+    assert rep3["iters_phase1"] + rep3["iters_phase2"] == 0 and rep3["converged"] == 1
+    np.testing.assert_array_equal(host(w3), host(w2))
