@@ -417,7 +417,7 @@ def run_ours(args, rank, world, local):
     # the solver's operator under OP_AUTO (rbf_op_variant; sym_mode in summation.cu)
     sym = 2 if 3 * cfg.n // max(world if slab else 1, 1) >= (1 << 18) else 0
     kname = {0: "sum_f32_kernel (one-sided)", 1: "sum_f32_kernel (symmetric, 64-target tiles)",
-             2: "sum_f32_symw_kernel (symmetric, 128-target tiles)"}[sym]
+             2: "sum_f32_symb_kernel (symmetric, 128-target tiles)"}[sym]
     roofline = {"bound": "alu", "kernel": kname + ", MUFU.EX2", "achieved": achieved, "peak": peak_max,
                 "unit": "Tpairs/s", "frac": achieved / peak_max,
                 "peak_basis": "148 SMs x 16 MUFU.EX2/clk x 1965 MHz (max clock; 16.00 ex2/clk/SM measured, "

@@ -1,7 +1,7 @@
 """Small driver for ncu: cell build, a few solver iterations (operator variant
 argv[2], default OP_AUTO) and one grid evaluation of a config (argv[1], c4).
 
-    ncu --set full -k regex:sum_f32_symw -s 1 -c 1 -o out python tools/prof_step.py c4
+    ncu --set full -k regex:sum_f32_symb -s 1 -c 1 -o out python tools/prof_step.py c4
 """
 import os
 import sys
