@@ -250,6 +250,19 @@ rbf_status rbf_create_ipc(rbf_ctx** ctx, int device, void* cuda_stream, const vo
  * keeps the copy-based halo (the NCCL path's form) on any transport.  Results
  * are the same up to the atomics' summation order. */
 rbf_status rbf_ctx_peer_memory(rbf_ctx* ctx, int on);
+/* Neighbour-list form of the solver's symmetric fp32 operator (RBF_OP_SYM_WIDE,
+ * and RBF_OP_AUTO where it selects it; on by default).  The first product with
+ * a cell structure lists, for every target tile of the wide plan, the sorted
+ * positions of the sources after the tile that survive the tile's box cull
+ * (the same cell rows, cull and order as the traversal; Alg.2 "truncation
+ * area") and keeps the list with the cells (DEVICE memory owned by
+ * the library, 4 bytes per listed source: 0.33 GB at 3M centres, sigma = 0.01);
+ * later products read the list instead of re-walking and re-culling the cell
+ * rows.  on = 0 runs the traversal every time.  The list is rebuilt when the
+ * kernel's cutoff or the source window changes, and skipped (traversal form)
+ * when it would exceed 2^31 entries or does not fit in memory.  Results equal
+ * the traversal form's up to the atomics' summation order. */
+rbf_status rbf_ctx_neighbour_lists(rbf_ctx* ctx, int on);
 /* Slab partition plan (HOST only, no GPU; the same function the library runs at
  * rbf_build_cells when world > 1).  Inputs: plane_start[dimz+1] = sorted
  * position of the first centre of each z cell plane (non-decreasing, last =

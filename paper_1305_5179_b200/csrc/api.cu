@@ -207,6 +207,12 @@ rbf_status rbf_ctx_peer_memory(rbf_ctx* ctx, int on) {
   return RBF_OK;
 }
 
+rbf_status rbf_ctx_neighbour_lists(rbf_ctx* ctx, int on) {
+  if (!ctx) { set_error("ctx is NULL"); return RBF_EINVAL; }
+  ctx->nl_on = on != 0;
+  return RBF_OK;
+}
+
 rbf_status rbf_profile_enable(rbf_ctx* ctx, int on) {
   if (!ctx) { set_error("ctx is NULL"); return RBF_EINVAL; }
   ctx->prof = on != 0;

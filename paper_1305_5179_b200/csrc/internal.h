@@ -152,6 +152,7 @@ struct rbf_ctx {
   rbf::Transport* tr = nullptr;
   void* loop_group = nullptr;   // rbf::LoopGroup of a loopback context
   int rank = 0, world = 1;
+  bool nl_on = true;      // neighbour-list form of the symmetric fp32 operator (rbf_ctx_neighbour_lists)
   bool peer_mem = true;   // use the transport's peer-memory mode when it has one (rbf_ctx_peer_memory)
   rbf::DevBuf win, fwin, rsc, red, pwin;
 };
@@ -206,6 +207,13 @@ struct rbf_cells {
   int64_t ntiles_w = 0;
   rbf::DevBuf tiles_w, tile_box_w;
   rbf::DevBuf order_w;       // this rank's wide tiles, most expensive first (summation.cu order_wide_tiles)
+  // neighbour lists of the wide tiles (summation.cu ensure_nl; built on first use
+  // by the symmetric fp32 operator): nl_off[nt + 1] (uint32), nl_idx[entries]
+  // (int32 sorted source positions); keyed by the culling radius and the window
+  mutable rbf::DevBuf nl_idx, nl_off;
+  mutable int nl_state = 0;          // 0 not built, 1 valid, -1 unavailable for this key
+  mutable float nl_cc = 0.f;
+  mutable int64_t nl_hi = -1, nl_t0 = -1, nl_nt = -1, nl_entries = 0;
   cudaStream_t stream = nullptr;
   rbf::SlabView view;        // this rank's share (whole range on one GPU)
   rbf::SlabPlan plan;        // all ranks' slabs (world > 1)
@@ -249,6 +257,7 @@ rbf_status matvec_sorted_f64(rbf_ctx* ctx, const rbf_cells* c, const KernelParam
                              const double* w_sorted, double* f_sorted, const int32_t* out_perm,
                              int op = RBF_OP_ONESIDED);
 rbf_status order_wide_tiles(rbf_ctx* ctx, rbf_cells* c, const KernelParams& kp);
+rbf_status ensure_nl(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp, bool* ok);
 // near (optional, uint8 per node): evaluate only the node blocks holding a node
 // with near != 0 and write NaN (all bits set) at every node with near == 0
 // (the eps-surrounding M_ext^eps of §2.1.3)

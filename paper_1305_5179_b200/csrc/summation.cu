@@ -1028,7 +1028,8 @@ __global__ void __launch_bounds__(kSumWarps * 32, 8)
 sum_f32_symr_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* __restrict__ src,
                     const int2* __restrict__ tiles, const float4* __restrict__ tbox, int64_t ntiles,
                     int64_t tile_base, OutT* __restrict__ out, int* __restrict__ work, int64_t sym_hi,
-                    const int32_t* __restrict__ order, PeerTab = PeerTab{}) {   // (no peer-memory form)
+                    const int32_t* __restrict__ order, PeerTab = PeerTab{},   // (no peer-memory form,
+                    const int32_t* = nullptr, const uint32_t* = nullptr) {         //  no neighbour lists)
   __shared__ __align__(16) float4 ring4[kSumWarps][kRotCap];
   __shared__ __align__(8) float2 ring2[kSumWarps][kRotCap];
   __shared__ int ringi[kSumWarps][kRotCap];
@@ -1083,14 +1084,26 @@ constexpr int kSymPad = 136;   // SoA ring row (>= kFlush + 32 + 4, multiple of 
 #define RBF_SYMB_KBSTORE 1
 #endif
 
-template <int T, class OutT, bool PEER = false>
+// Staging batch of the neighbour-list form (NL): the ring is filled with exactly
+// kNlBatch listed sources (no cull, no overflow), then flushed.
+constexpr int kNlBatch = 128;
+static_assert(kNlBatch <= kSymPad && kNlBatch <= kOwnPad, "NL batch exceeds the rings");
+
+// NL = false: the tile streams the cell rows within the cutoff of its box and
+// culls (the traversal); NL = true: the tile's culled sources after it were
+// listed once per cell structure (nl_build_kernel, the same traversal and cull,
+// same order) and are read from nl_idx[nl_b, nl_e) -- no row setup, no cull, no
+// ballot compaction in the 51 matvecs of a solve.
+template <int T, class OutT, bool PEER = false, bool NL = false>
 __device__ __forceinline__ void symb_tile(const SumGeom& G, const int32_t* __restrict__ cell_start,
                                           const float4* __restrict__ src, float3 blo, float3 bhi, float3 ctr,
                                           const float* xr, const float* yr, const float* zr, const bool* tv,
                                           const float* wg, int2 tl, int64_t sym_hi, int lane,
                                           float (*__restrict__ RS)[kSymPad], int* __restrict__ RI,
                                           float* __restrict__ KB, float (*__restrict__ O)[kOwnPad],
-                                          OutT* __restrict__ out, float* fo, const PeerTab* PT = nullptr) {
+                                          OutT* __restrict__ out, float* fo, const PeerTab* PT = nullptr,
+                                          const int32_t* __restrict__ nl_idx = nullptr, uint32_t nl_b = 0,
+                                          uint32_t nl_e = 0) {
   float mx[T], my[T], mz[T], tf[T], wt[T];
   float2 acc[T];
 #pragma unroll
@@ -1224,6 +1237,62 @@ __device__ __forceinline__ void symb_tile(const SumGeom& G, const int32_t* __res
       }
     }
   };
+  if constexpr (NL) {
+    // the tile's own sources (one-sided), at most 128
+    for (int b = tl.x; b < t_end; b += kNlBatch) {
+      const int cnt = min(kNlBatch, t_end - b), c4 = (cnt + 3) & ~3;
+#pragma unroll
+      for (int q = 0; q < kNlBatch / 32; ++q) {
+        const int i = q * 32 + lane;
+        if (i < c4) {
+          const float4 p = i < cnt ? __ldg(src + b + i) : make_float4(ctr.x, ctr.y, ctr.z, 0.f);
+          const float sx = (p.x - ctr.x) * G.s, sy = (p.y - ctr.y) * G.s, sz = (p.z - ctr.z) * G.s;
+          O[0][i] = sx; O[1][i] = sy; O[2][i] = sz;
+          O[3][i] = i < cnt ? fmaf(sz, sz, fmaf(sy, sy, sx * sx)) : 1e30f;
+          O[4][i] = p.w;
+        }
+      }
+      __syncwarp();
+      flush_own(c4);
+      __syncwarp();
+    }
+    // the listed sources after the tile (symmetric), kNlBatch per flush
+    for (uint32_t b = nl_b; b < nl_e; b += kNlBatch) {
+      const int cnt = (int)min((uint32_t)kNlBatch, nl_e - b), c4 = (cnt + 3) & ~3;
+      int id[kNlBatch / 32];
+#pragma unroll
+      for (int q = 0; q < kNlBatch / 32; ++q) {
+        const int i = q * 32 + lane;
+        id[q] = i < cnt ? __ldg(nl_idx + b + i) : -1;
+      }
+      float4 p[kNlBatch / 32];
+#pragma unroll
+      for (int q = 0; q < kNlBatch / 32; ++q) {
+        const float4* __restrict__ srow = src;
+        if constexpr (PEER) {
+          if (id[q] >= 0) srow = PT->src[peer_of(*PT, id[q])];
+        }
+        p[q] = id[q] >= 0 ? __ldg(srow + id[q]) : make_float4(ctr.x, ctr.y, ctr.z, 0.f);
+      }
+#pragma unroll
+      for (int q = 0; q < kNlBatch / 32; ++q) {
+        const int i = q * 32 + lane;
+        if (i < c4) {
+          const float sx = (p[q].x - ctr.x) * G.s, sy = (p[q].y - ctr.y) * G.s, sz = (p[q].z - ctr.z) * G.s;
+          RS[0][i] = sx; RS[1][i] = sy; RS[2][i] = sz;
+          RS[3][i] = id[q] >= 0 ? fmaf(sz, sz, fmaf(sy, sy, sx * sx)) : 1e30f;
+          RS[4][i] = p[q].w;
+          RI[i] = id[q];
+        }
+      }
+      __syncwarp();
+      flush_sym(c4);
+      __syncwarp();
+    }
+#pragma unroll
+    for (int t = 0; t < T; ++t) fo[t] = G.amp * ((acc[t].x + acc[t].y) * tf[t]);
+    return;
+  }
   const CellGrid& g = G.g;
   const float cc = G.cc, cc2 = G.cc2, h = g.h;
   const int z0 = cellof(blo.z - cc, g.lo[2], g.inv_h, g.dim[2]);
@@ -1331,12 +1400,15 @@ __device__ __forceinline__ void symb_tile(const SumGeom& G, const int32_t* __res
 #ifndef RBF_SYMB_MINB
 #define RBF_SYMB_MINB 8
 #endif
-template <class OutT, bool PEER = false>
+// NL: nl_off[tile] .. nl_off[tile + 1] (absolute tile ids; the pointer is shifted
+// by the first tile of the list) delimit the tile's listed sources in nl_idx.
+template <class OutT, bool PEER = false, bool NL = false>
 __global__ void __launch_bounds__(kSumWarps * 32, RBF_SYMB_MINB)
 sum_f32_symb_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* __restrict__ src,
                     const int2* __restrict__ tiles, const float4* __restrict__ tbox, int64_t ntiles,
                     int64_t tile_base, OutT* __restrict__ out, int* __restrict__ work, int64_t sym_hi,
-                    const int32_t* __restrict__ order, PeerTab PT = PeerTab{}) {
+                    const int32_t* __restrict__ order, PeerTab PT = PeerTab{},
+                    const int32_t* __restrict__ nl_idx = nullptr, const uint32_t* __restrict__ nl_off = nullptr) {
   __shared__ __align__(16) float rings[kSumWarps][5][kSymPad];
   __shared__ int ringi[kSumWarps][kSymPad];
   __shared__ float ringk[kSumWarps][kSymPad + 32];   // + the dummy store slots of flush_sym
@@ -1365,11 +1437,13 @@ sum_f32_symb_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const flo
       xr[t] = p.x; yr[t] = p.y; zr[t] = p.z; wg[t] = p.w;
     }
     const int T = (tl.y + 31) >> 5;
+    uint32_t nb = 0, ne = 0;
+    if constexpr (NL) { nb = nl_off[tile]; ne = nl_off[tile + 1]; }
     switch (T) {
-      case 1: symb_tile<1, OutT, PEER>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringk[wib], ringo[wib], out, fo, &PT); break;
-      case 2: symb_tile<2, OutT, PEER>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringk[wib], ringo[wib], out, fo, &PT); break;
-      case 3: symb_tile<3, OutT, PEER>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringk[wib], ringo[wib], out, fo, &PT); break;
-      default: symb_tile<4, OutT, PEER>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringk[wib], ringo[wib], out, fo, &PT); break;
+      case 1: symb_tile<1, OutT, PEER, NL>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringk[wib], ringo[wib], out, fo, &PT, nl_idx, nb, ne); break;
+      case 2: symb_tile<2, OutT, PEER, NL>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringk[wib], ringo[wib], out, fo, &PT, nl_idx, nb, ne); break;
+      case 3: symb_tile<3, OutT, PEER, NL>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringk[wib], ringo[wib], out, fo, &PT, nl_idx, nb, ne); break;
+      default: symb_tile<4, OutT, PEER, NL>(G, cell_start, src, blo, bhi, ctr, xr, yr, zr, tv, wg, tl, sym_hi, lane, rings[wib], ringi[wib], ringk[wib], ringo[wib], out, fo, &PT, nl_idx, nb, ne); break;
     }
 #pragma unroll
     for (int t = 0; t < 4; ++t)
@@ -1620,6 +1694,177 @@ struct Flush64x {
     }
   }
 };
+
+// Expansion form of the symmetric fp64 tier: sources staged (once per tile, one
+// lane per source) in the tile-local frame scaled by q = 1/sqrt(2 sigma^2),
+// s' = (x - ctr) q, with |s'|^2; a pair is then rr = |s'|^2 - 2 t'.s' (3 DFMA)
+// and e = exp(-rr) exp(-|t'|^2), the per-target factor applied once at the end
+// (cutoff: rr <= c^2 q^2 - |t'|^2 per target).  Against the difference form
+// (3 F2F + 3 DADD + 3 DMUL + 2 DADD + 1 DMUL per pair) this removes ~6 of the
+// ~22 DP operations per pair.  Rounding: |s'|, |t'| <= ~5 at the cutoff, so the
+// expansion costs ~1e-14 absolute in the exponent (the fp64
+// tier's gate is 1e-12 g_i per row).
+struct Ring64e {
+  double* sx; double* sy; double* sz; double* ss; double* w; int* bi;
+};
+
+struct Stage64e {
+  Ring64e rb, ri;   // symmetric / one-sided
+  const float4* __restrict__ src;
+  const double* __restrict__ w;
+  float3 blo, bhi;
+  double cx, cy, cz, q;
+  float cc2;
+  int skip_lo, skip_hi, sym_lo, sym_hi;
+  float4 p;
+  double wj;
+  int jj;
+  __device__ __forceinline__ int classify(int j, bool valid) {
+    p = valid ? __ldg(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    wj = valid ? __ldg(w + j) : 0.0;
+    jj = j;
+    if (j >= skip_lo && j < skip_hi) return 0;
+    const float gx = fmaxf(0.f, fmaxf(blo.x - p.x, p.x - bhi.x));
+    const float gy = fmaxf(0.f, fmaxf(blo.y - p.y, p.y - bhi.y));
+    const float gz = fmaxf(0.f, fmaxf(blo.z - p.z, p.z - bhi.z));
+    if (!valid || gx * gx + gy * gy + gz * gz > cc2) return 0;
+    return (j >= sym_lo && j < sym_hi) ? 1 : 2;
+  }
+  __device__ __forceinline__ void store2(int kind, int posb, int posi) {
+    if (kind == 0) return;
+    Ring64e& r = (kind == 1) ? rb : ri;
+    const int pos = (kind == 1) ? posb : posi;
+    const double sx = ((double)p.x - cx) * q, sy = ((double)p.y - cy) * q, sz = ((double)p.z - cz) * q;
+    r.sx[pos] = sx; r.sy[pos] = sy; r.sz[pos] = sz;
+    r.ss[pos] = __fma_rn(sz, sz, __fma_rn(sy, sy, sx * sx));
+    r.w[pos] = wj;
+    if (kind == 1) r.bi[pos] = jj;
+  }
+  __device__ __forceinline__ void shift_ring(Ring64e& r, int rest, int lane) {
+    if (lane < rest) {
+      const int q0 = kFlush + lane;
+      const double a = r.sx[q0], b = r.sy[q0], c = r.sz[q0], d = r.ss[q0], e = r.w[q0];
+      r.sx[lane] = a; r.sy[lane] = b; r.sz[lane] = c; r.ss[lane] = d; r.w[lane] = e;
+      if (r.bi) r.bi[lane] = r.bi[q0];
+    }
+  }
+};
+
+template <bool SYM>
+struct Flush64e {
+  Ring64e r;
+  double* acc;                                            // [2]
+  const double* mx; const double* my; const double* mz;   // [2] -2 t'
+  const double* thr;                                      // [2] c^2 q^2 - |t'|^2
+  const double* wt;                                       // [2] w_t exp(-|t'|^2) (0 for empty slots), SYM only
+  double amp;
+  double* out;
+  int lane;
+  const double* tab;
+  __device__ __forceinline__ double pair(int j) {
+    const double sx = r.sx[j], sy = r.sy[j], sz = r.sz[j], ss = r.ss[j], wj = r.w[j];
+    double pj = 0.0;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const double rr = __fma_rn(mz[t], sz, __fma_rn(my[t], sy, __fma_rn(mx[t], sx, ss)));
+      const double ex = exp_tier64(-rr, tab);
+      const double e = rr <= thr[t] ? ex : 0.0;
+      acc[t] = __fma_rn(e, wj, acc[t]);
+      if (SYM) pj = __fma_rn(e, wt[t], pj);
+    }
+    return pj;
+  }
+  __device__ __forceinline__ void operator()(int cnt) {
+    if constexpr (SYM) {
+      const bool h4 = lane & 16, h3 = lane & 8;
+      const int mys = (h4 ? 2 : 0) + (h3 ? 1 : 0);
+      for (int j = 0; j < cnt; j += 4) {
+        const double p0 = pair(j), p1 = pair(j + 1), p2 = pair(j + 2), p3 = pair(j + 3);
+        double k0 = h4 ? p2 : p0, k1 = h4 ? p3 : p1;
+        const double s0 = h4 ? p0 : p2, s1 = h4 ? p1 : p3;
+        k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+        k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+        double k = h3 ? k1 : k0;
+        k += __shfl_xor_sync(0xffffffffu, h3 ? k0 : k1, 8);
+        k += __shfl_xor_sync(0xffffffffu, k, 4);
+        k += __shfl_xor_sync(0xffffffffu, k, 2);
+        k += __shfl_xor_sync(0xffffffffu, k, 1);
+        if ((lane & 7) == 0) atomicAdd(out + r.bi[j + mys], amp * k);
+      }
+    } else {
+      for (int j = 0; j < cnt; ++j) pair(j);
+    }
+  }
+};
+
+__global__ void __launch_bounds__(kSumWarps * 32)
+sum_f64_syme_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* __restrict__ src,
+                    const double* __restrict__ w, const int2* __restrict__ tiles, const float4* __restrict__ tbox,
+                    int64_t ntiles, int64_t tile_base, double* __restrict__ out, int* __restrict__ work,
+                    int64_t own_lo, int64_t own_hi) {
+  __shared__ __align__(16) double ringd[kSumWarps][10][kBufPad];
+  __shared__ __align__(16) int ringi[kSumWarps][kBufPad];
+  __shared__ double etab[kExpTab];
+  exp_tier64_table(etab);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  Ring64e RB{ringd[wib][0], ringd[wib][1], ringd[wib][2], ringd[wib][3], ringd[wib][4], ringi[wib]};
+  Ring64e RI{ringd[wib][5], ringd[wib][6], ringd[wib][7], ringd[wib][8], ringd[wib][9], nullptr};
+  const double q = 1.0 / sqrt(G.two_s2);
+  const double c2q = G.c2d / G.two_s2;
+  for (;;) {
+    int64_t tile;
+    {
+      int t0 = 0;
+      if (lane == 0) t0 = atomicAdd(work, 1);
+      tile = __shfl_sync(0xffffffffu, t0, 0);
+    }
+    if (tile >= ntiles) break;
+    tile += tile_base;
+    const int2 tl = tiles[tile];
+    const float4 a = tbox[2 * tile], b = tbox[2 * tile + 1];
+    const float3 blo = make_float3(a.x, a.y, a.z), bhi = make_float3(b.x, b.y, b.z);
+    // tile centre (any fixed point: the expansion is exact algebra around it)
+    const double cx = 0.5 * ((double)blo.x + (double)bhi.x), cy = 0.5 * ((double)blo.y + (double)bhi.y),
+                 cz = 0.5 * ((double)blo.z + (double)bhi.z);
+    double mx[2], my[2], mz[2], thr[2], tf[2], wt[2], acc[2] = {0.0, 0.0};
+    bool tv[2];
+    int64_t tidx[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      int qq = lane + 32 * t;
+      tv[t] = qq < tl.y;
+      tidx[t] = tl.x + (tv[t] ? qq : 0);
+      const float4 p = src[tidx[t]];
+      const double tx = ((double)p.x - cx) * q, ty = ((double)p.y - cy) * q, tz = ((double)p.z - cz) * q;
+      const double tt = __fma_rn(tz, tz, __fma_rn(ty, ty, tx * tx));
+      mx[t] = -2.0 * tx; my[t] = -2.0 * ty; mz[t] = -2.0 * tz;
+      thr[t] = c2q - tt;
+      tf[t] = exp_tier64(-tt, etab);
+      wt[t] = tv[t] ? w[tidx[t]] * tf[t] : 0.0;
+    }
+    Stage64e st{RB, RI, src, w, blo, bhi, cx, cy, cz, q, G.cc2, (int)own_lo, tl.x, tl.x + tl.y, (int)own_hi,
+                make_float4(0, 0, 0, 0), 0.0, 0};
+    Flush64e<true> fs{RB, acc, mx, my, mz, thr, wt, G.ampd, out, lane, etab};
+    Flush64e<false> fi{RI, acc, mx, my, mz, thr, wt, G.ampd, out, lane, etab};
+    int nB = 0, nI = 0;
+    traverse2(G, cell_start, blo, bhi, lane, st, fs, fi, nB, nI, st.skip_lo, st.skip_hi);
+    // pad the symmetric ring to a multiple of 4 with zero-weight sources beyond
+    // every cutoff (rr = 1e300 > thr: they contribute to neither side)
+    const int cntB = (nB + 3) & ~3;
+    if (lane < cntB - nB) {
+      const int qq = nB + lane;
+      RB.sx[qq] = 0.0; RB.sy[qq] = 0.0; RB.sz[qq] = 0.0; RB.ss[qq] = 1e300; RB.w[qq] = 0.0; RB.bi[qq] = tl.x;
+    }
+    __syncwarp();
+    fs(cntB);
+    fi(nI);
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+      if (tv[t]) atomicAdd(out + tidx[t], G.ampd * (acc[t] * tf[t]));
+  }
+}
 
 __global__ void __launch_bounds__(kSumWarps * 32)
 sum_f64_sym_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* __restrict__ src,
@@ -1930,6 +2175,125 @@ rbf_status order_wide_tiles(rbf_ctx* ctx, rbf_cells* c, const KernelParams& kp) 
   return RBF_OK;
 }
 
+namespace {
+// Neighbour lists of the wide symmetric plan (NL form of sum_f32_symb_kernel):
+// for every tile, the sorted indices of the sources after it (j >= tile end,
+// j < sym_hi) that its traversal keeps -- the same cell rows, the same box cull
+// and the same order as symb_tile's symmetric ring.  EMIT = false counts (and
+// adds the total), EMIT = true writes them at off[w].  One warp per tile.
+template <bool EMIT>
+__global__ void nl_build_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* __restrict__ pos,
+                                const int2* __restrict__ tiles, const float4* __restrict__ tbox, int64_t t0,
+                                int64_t nt, int64_t sym_hi, uint32_t* __restrict__ cnt,
+                                const uint32_t* __restrict__ off, int32_t* __restrict__ idx,
+                                unsigned long long* __restrict__ total) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
+  const CellGrid& g = G.g;
+  const float cc = G.cc, cc2 = G.cc2, h = g.h;
+  for (int64_t w = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32; w < nt; w += nw) {
+    const int64_t tile = t0 + w;
+    const int2 tl = tiles[tile];
+    const float4 a = tbox[2 * tile], b = tbox[2 * tile + 1];
+    const float3 blo = make_float3(a.x, a.y, a.z), bhi = make_float3(b.x, b.y, b.z);
+    const int t_end = tl.x + tl.y;
+    const int z0 = cellof(blo.z - cc, g.lo[2], g.inv_h, g.dim[2]);
+    const int z1 = cellof(bhi.z + cc, g.lo[2], g.inv_h, g.dim[2]);
+    const int y0 = cellof(blo.y - cc, g.lo[1], g.inv_h, g.dim[1]);
+    const int y1 = cellof(bhi.y + cc, g.lo[1], g.inv_h, g.dim[1]);
+    uint32_t n = 0;
+    int32_t* __restrict__ dst = EMIT ? idx + off[w] : nullptr;
+    for (int cz = z0; cz <= z1; ++cz) {
+      const float czlo = g.lo[2] + (float)cz * h;
+      const float gz = fmaxf(0.f, fmaxf(czlo - bhi.z, blo.z - (czlo + h)));
+      for (int cy = y0; cy <= y1; ++cy) {
+        const float cylo = g.lo[1] + (float)cy * h;
+        const float gy = fmaxf(0.f, fmaxf(cylo - bhi.y, blo.y - (cylo + h)));
+        const float rem = cc2 - gy * gy - gz * gz;
+        if (rem < 0.f) continue;
+        const float rx = sqrtf(rem);
+        const int x0 = cellof(blo.x - rx, g.lo[0], g.inv_h, g.dim[0]);
+        const int x1 = cellof(bhi.x + rx, g.lo[0], g.inv_h, g.dim[0]);
+        const int64_t rowbase = ((int64_t)cz * g.dim[1] + cy) * g.dim[0];
+        const int sb = max(__ldg(cell_start + rowbase + x0), t_end);
+        const int se = min(__ldg(cell_start + rowbase + x1 + 1), (int)sym_hi);
+        for (int j0 = sb; j0 < se; j0 += 32) {
+          const int j = j0 + lane;
+          const bool valid = j < se;
+          const float4 p = valid ? __ldg(pos + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float gx = fmaxf(0.f, fmaxf(blo.x - p.x, p.x - bhi.x));
+          const float gyy = fmaxf(0.f, fmaxf(blo.y - p.y, p.y - bhi.y));
+          const float gzz = fmaxf(0.f, fmaxf(blo.z - p.z, p.z - bhi.z));
+          const bool keep = valid && (gx * gx + gyy * gyy + gzz * gzz <= cc2);
+          const unsigned bal = __ballot_sync(0xffffffffu, keep);
+          if (EMIT && keep) dst[n + __popc(bal & lt)] = j;
+          n += __popc(bal);
+        }
+      }
+    }
+    if (!EMIT && lane == 0) {
+      cnt[w] = n;
+      atomicAdd(total, (unsigned long long)n);
+    }
+  }
+}
+}  // namespace
+
+// The neighbour lists of this rank's wide tiles for the kernel geometry kp
+// (built on first use, kept with the cells while the culling radius and the
+// source window stay the same).  *ok = false when they are switched off
+// (rbf_ctx_neighbour_lists), exceed 2^31 entries, or do not fit in memory: the
+// caller then runs the traversal form.
+rbf_status ensure_nl(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp, bool* ok) {
+  *ok = false;
+  if (!ctx->nl_on) return RBF_OK;
+  const SlabView& V = c->view;
+  const int64_t nt = V.tw1 - V.tw0;
+  SumGeom G = make_geom(c, kp);
+  if (c->nl_state != 0 && c->nl_cc == G.cc && c->nl_hi == V.h1 && c->nl_t0 == V.tw0 && c->nl_nt == nt) {
+    *ok = c->nl_state > 0;
+    return RBF_OK;
+  }
+  cudaStream_t s = ctx->stream;
+  c->nl_state = -1;
+  c->nl_cc = G.cc; c->nl_hi = V.h1; c->nl_t0 = V.tw0; c->nl_nt = nt;
+  c->nl_idx.release();
+  c->nl_off.release();
+  if (nt <= 0) return RBF_OK;
+  ProfScope ps(ctx, RBF_PROF_CELLS);   // part of the cell structure's cost
+  DevBuf cnt, tot;
+  RBF_TRY(cnt.alloc(sizeof(uint32_t) * (nt + 1), s));
+  RBF_TRY(tot.alloc(sizeof(unsigned long long), s));
+  RBF_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, sizeof(uint32_t) * (nt + 1), s));
+  RBF_CUDA_TRY(cudaMemsetAsync(tot.p, 0, sizeof(unsigned long long), s));
+  const int blocks = (int)std::min<int64_t>((nt + 7) / 8, 148 * 16);
+  nl_build_kernel<false><<<blocks, 256, 0, s>>>(G, c->cell_start.as<int32_t>(), c->sorted.as<float4>(),
+                                                 c->tiles_w.as<int2>(), c->tile_box_w.as<float4>(), V.tw0, nt, V.h1,
+                                                 cnt.as<uint32_t>(), nullptr, nullptr, tot.as<unsigned long long>());
+  RBF_CHECK_LAUNCH();
+  unsigned long long total = 0;
+  RBF_CUDA_TRY(cudaMemcpyAsync(&total, tot.p, sizeof(total), cudaMemcpyDeviceToHost, s));
+  RBF_CUDA_TRY(cudaStreamSynchronize(s));
+  if (total >= (1ull << 31)) return RBF_OK;
+  if (c->nl_off.alloc(sizeof(uint32_t) * (nt + 1), s) != RBF_OK ||
+      c->nl_idx.alloc(sizeof(int32_t) * std::max<unsigned long long>(total, 1), s) != RBF_OK) {
+    cudaGetLastError();
+    c->nl_idx.release();
+    c->nl_off.release();
+    return RBF_OK;   // no room: the traversal form
+  }
+  RBF_TRY(exclusive_scan_u32(ctx, cnt.as<uint32_t>(), c->nl_off.as<uint32_t>(), nt + 1, nullptr));
+  nl_build_kernel<true><<<blocks, 256, 0, s>>>(G, c->cell_start.as<int32_t>(), c->sorted.as<float4>(),
+                                                c->tiles_w.as<int2>(), c->tile_box_w.as<float4>(), V.tw0, nt, V.h1,
+                                                nullptr, c->nl_off.as<uint32_t>(), c->nl_idx.as<int32_t>(), nullptr);
+  RBF_CHECK_LAUNCH();
+  c->nl_state = 1;
+  c->nl_entries = (int64_t)total;
+  *ok = true;
+  return RBF_OK;
+}
+
 // Public fp32 path (and the pair accounting): w_sorted covers all n centres
 // (sorted order); this rank's tiles write f_out[out_perm ? perm[j] : j].
 rbf_status matvec_sorted_f32(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp,
@@ -1982,6 +2346,11 @@ static rbf_status matvec_f32_solver(rbf_ctx* ctx, const rbf_cells* c, const Kern
   const int64_t base = sym ? V.o0 : V.h0;
   const int64_t nw = V.h1 - base;
   const WT* w_win = w_loc;
+  // neighbour-list form of the wide symmetric kernel (built on the first product)
+  bool nl = false;
+  if (sym == 2) RBF_TRY(ensure_nl(ctx, c, kp, &nl));
+  const int32_t* nl_idx = nl ? c->nl_idx.as<int32_t>() : nullptr;
+  const uint32_t* nl_off = nl ? c->nl_off.as<uint32_t>() - V.tw0 : nullptr;
   // slab partition over a peer-memory transport (loopback, CUDA IPC), wide
   // symmetric operator: ONE kernel reads the upper ranks' packed sources and
   // adds the source-side sums into their accumulators in place, through peer
@@ -2025,11 +2394,11 @@ static rbf_status matvec_f32_solver(rbf_ctx* ctx, const rbf_cells* c, const Kern
       SumGeom G = make_geom(c, kp);
       {
         ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
-        auto kfn = sum_f32_symb_kernel<double, true>;
+        auto kfn = nl ? sum_f32_symb_kernel<double, true, true> : sum_f32_symb_kernel<double, true>;
         kfn<<<sum_blocks(ctx, kfn), kSumWarps * 32, 0, s>>>(G, c->cell_start.as<int32_t>(), PT.src[0],
                                                             c->tiles_w.as<int2>(), c->tile_box_w.as<float4>(),
                                                             V.tw1 - V.tw0, V.tw0, PT.f[0], ctx->counter.as<int>(),
-                                                            V.h1, c->order_w.as<int32_t>(), PT);
+                                                            V.h1, c->order_w.as<int32_t>(), PT, nl_idx, nl_off);
         RBF_CHECK_LAUNCH();
       }
       RBF_TRY(ctx->tr->peer_end(ctx, s));   // every rank's kernel has added into my sums
@@ -2093,21 +2462,23 @@ static rbf_status matvec_f32_solver(rbf_ctx* ctx, const rbf_cells* c, const Kern
     RBF_CUDA_TRY(cudaMemsetAsync(ctx->counter.p, 0, 2 * sizeof(int), s));
     SumGeom G = make_geom(c, kp);
     const float4* srcb = ctx->src4.as<float4>() - base;
-    auto kfn = sym == 3 ? sum_f32_symr_kernel<double> : sum_f32_symb_kernel<double>;
+    auto kfn = sym == 3 ? sum_f32_symr_kernel<double>
+                        : (nl ? sum_f32_symb_kernel<double, false, true> : sum_f32_symb_kernel<double>);
     const int64_t ni = V.tw_int, nb = (V.tw1 - V.tw0) - ni;
     {
       ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
       kfn<<<sum_blocks(ctx, kfn), kSumWarps * 32, 0, s>>>(G, c->cell_start.as<int32_t>(), srcb, c->tiles_w.as<int2>(),
                                                           c->tile_box_w.as<float4>(), ni, V.tw0, fwin - base,
                                                           ctx->counter.as<int>(), V.h1, c->order_w.as<int32_t>(),
-                                                          PeerTab{});
+                                                          PeerTab{}, nl_idx, nl_off);
       RBF_CHECK_LAUNCH();
       // join: the halo tiles after the halo
       RBF_CUDA_TRY(cudaStreamWaitEvent(s, ctx->halo_ev[1], 0));
       if (nb > 0) {
         kfn<<<sum_blocks(ctx, kfn), kSumWarps * 32, 0, s>>>(
             G, c->cell_start.as<int32_t>(), srcb, c->tiles_w.as<int2>(), c->tile_box_w.as<float4>(), nb, V.tw0,
-            fwin - base, ctx->counter.as<int>() + 1, V.h1, c->order_w.as<int32_t>() + ni, PeerTab{});
+            fwin - base, ctx->counter.as<int>() + 1, V.h1, c->order_w.as<int32_t>() + ni, PeerTab{}, nl_idx,
+            nl_off);
         RBF_CHECK_LAUNCH();
       }
     }
@@ -2139,11 +2510,12 @@ static rbf_status matvec_f32_solver(rbf_ctx* ctx, const rbf_cells* c, const Kern
     {
       ProfScope ps(ctx, RBF_PROF_MATVEC_F32);
       if (sym >= 2) {
-        auto kfn = sym == 3 ? sum_f32_symr_kernel<double> : sum_f32_symb_kernel<double>;
+        auto kfn = sym == 3 ? sum_f32_symr_kernel<double>
+                            : (nl ? sum_f32_symb_kernel<double, false, true> : sum_f32_symb_kernel<double>);
         kfn<<<sum_blocks(ctx, kfn), kSumWarps * 32, 0, s>>>(
             G, c->cell_start.as<int32_t>(), srcb, c->tiles_w.as<int2>(), c->tile_box_w.as<float4>(), V.tw1 - V.tw0,
             V.tw0, fwin - base, ctx->counter.as<int>(), V.h1, c->order_w.p ? c->order_w.as<int32_t>() : nullptr,
-            PeerTab{});
+            PeerTab{}, nl_idx, nl_off);
       } else {
         sum_f32_kernel<0, false, double, true>
             <<<sum_blocks(ctx, sum_f32_kernel<0, false, double, true>), kSumWarps * 32, 0, s>>>(
@@ -2200,7 +2572,10 @@ rbf_status matvec_sorted_f64(rbf_ctx* ctx, const rbf_cells* c, const KernelParam
     RBF_CUDA_TRY(cudaMemsetAsync(fwin, 0, sizeof(double) * (size_t)std::max<int64_t>(nw, 0), s));
     {
       ProfScope ps(ctx, RBF_PROF_MATVEC_F64);
-      sum_f64_sym_kernel<<<sum_blocks(ctx, sum_f64_sym_kernel), kSumWarps * 32, 0, s>>>(
+      // expansion form unless the tile boxes are too large for exp(+|t'|^2) (never
+      // with the default cells: |t'|^2 <= hd2 / (2 sigma^2))
+      auto kfn = (c->hd2 / (2.0 * kp.sigma * kp.sigma) <= 300.0) ? sum_f64_syme_kernel : sum_f64_sym_kernel;
+      kfn<<<sum_blocks(ctx, kfn), kSumWarps * 32, 0, s>>>(
           G, c->cell_start.as<int32_t>(), c->sorted.as<float4>(), w_win - base, c->tiles.as<int2>(),
           c->tile_box.as<float4>(), V.t1 - V.t0, V.t0, fwin - base, ctx->counter.as<int>(), 0, V.h1);
       RBF_CHECK_LAUNCH();

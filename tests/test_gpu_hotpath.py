@@ -285,7 +285,13 @@ def test_symmetric_operators_degenerate_clouds(R, ctx, op):
         ref32 = OK.matvec(Xd, w32, sigma)
         ref64 = OK.matvec(Xd, w, sigma)
         g = OK.matvec(Xd, np.abs(w), sigma)
-        s32 = host(R.matvec_op(ctx, cells, kern, dev(w, torch.float32), op=opv))
-        s64 = host(R.matvec_op(ctx, cells, kern, dev(w, torch.float64), op=opv))
-        assert (np.abs(s32 - ref32) <= 5e-5 * g + 1e-30).all(), len(X)
-        assert (np.abs(s64 - ref64) <= 1e-12 * g + 1e-300).all(), len(X)
+        # OP_SYM_WIDE: the neighbour-list form (default) and the traversal form
+        for nl in ((True, False) if op == "OP_SYM_WIDE" else (True,)):
+            ctx.neighbour_lists(nl)
+            try:
+                s32 = host(R.matvec_op(ctx, cells, kern, dev(w, torch.float32), op=opv))
+                s64 = host(R.matvec_op(ctx, cells, kern, dev(w, torch.float64), op=opv))
+            finally:
+                ctx.neighbour_lists(True)
+            assert (np.abs(s32 - ref32) <= 5e-5 * g + 1e-30).all(), (len(X), nl)
+            assert (np.abs(s64 - ref64) <= 1e-12 * g + 1e-300).all(), (len(X), nl)
