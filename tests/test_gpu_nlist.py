@@ -69,9 +69,12 @@ def test_nl_equals_traversal_and_oracle(R, ctx, torus):
     for f in (f_nl, f_nl2, f_tr):
         assert (np.abs(f[rows] - ref) <= 5e-5 * g).all()
         assert np.linalg.norm(f[rows] - ref) <= 1e-4 * np.linalg.norm(ref)
-    # the two forms evaluate the same pairs: they differ by the fp32 summation
-    # order only (a few ulp of the row's absolute sum g)
-    assert (np.abs(f_nl[rows] - f_tr[rows]) <= 2e-6 * g).all()
+    # the two forms evaluate the same pairs except those the list drops because
+    # they lie beyond the cutoff of every target of a 32-target group (each such
+    # term <= 2^-26 of its weight's peak entry, reading R18), and sum in another
+    # order: a few ulp of the row's absolute sum g
+    assert (np.abs(f_nl[rows] - f_tr[rows]) <= 5e-6 * g).all()
+    # the cached list gives the same pairs; only the atomics' order differs
     assert (np.abs(f_nl[rows] - f_nl2[rows]) <= 2e-6 * g).all()
 
 
