@@ -263,6 +263,18 @@ rbf_status rbf_ctx_peer_memory(rbf_ctx* ctx, int on);
  * when it would exceed 2^31 entries or does not fit in memory.  Results equal
  * the traversal form's up to the atomics' summation order. */
 rbf_status rbf_ctx_neighbour_lists(rbf_ctx* ctx, int on);
+/* Separable form of the grid evaluation (default on).  The evaluation points of
+ * Eq.5 are a regular grid, so for a 4 x 4 x 4 block of
+ * nodes the Gaussian of a (node, centre) pair factors along the axes,
+ * exp(-|xi - x_j|^2 / (2 sigma^2)) = ex[i] ey[j] ez[k]: 12 exponentials per
+ * (block, centre) instead of 64; the cutoff predicate r^2 <= (6 sigma)^2 is
+ * still evaluated per pair (reading R5: exact zeros beyond the cutoff).  on = 0
+ * evaluates one exponential per pair (the matvec kernels' form).  Both forms
+ * satisfy the same per-node tolerance against the fp64 definition; they differ
+ * from each other by rounding (three ex2.approx factors instead of one).
+ * Applies to rbf_eval_grid, rbf_eval_grid_masked, rbf_eval_grid_slab,
+ * rbf_isosurface and rbf_reconstruct_host. */
+rbf_status rbf_ctx_grid_separable(rbf_ctx* ctx, int on);
 /* Slab partition plan (HOST only, no GPU; the same function the library runs at
  * rbf_build_cells when world > 1).  Inputs: plane_start[dimz+1] = sorted
  * position of the first centre of each z cell plane (non-decreasing, last =

@@ -213,6 +213,12 @@ rbf_status rbf_ctx_neighbour_lists(rbf_ctx* ctx, int on) {
   return RBF_OK;
 }
 
+rbf_status rbf_ctx_grid_separable(rbf_ctx* ctx, int on) {
+  if (!ctx) { set_error("ctx is NULL"); return RBF_EINVAL; }
+  ctx->grid_per_pair = on == 0;
+  return RBF_OK;
+}
+
 rbf_status rbf_profile_enable(rbf_ctx* ctx, int on) {
   if (!ctx) { set_error("ctx is NULL"); return RBF_EINVAL; }
   ctx->prof = on != 0;

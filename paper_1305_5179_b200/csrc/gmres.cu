@@ -124,6 +124,136 @@ multi_axpy_nrm_kernel(double* __restrict__ w, const VT* __restrict__ V, int64_t 
   }
 }
 
+// ---- 4-wide forms (n % 4 == 0: every basis vector V + j n is 16-byte aligned).
+// Same sums in a different (still fixed) order: a thread owns 4 consecutive
+// elements per sweep, the basis is read as 16-byte (fp32) or 2 x 16-byte (fp64)
+// loads with a whole chunk of vectors in flight per thread, w as two double2.
+// The scalar kernels above read 4 bytes per load and re-read w (fp64) once per
+// chunk of 4 vectors; here a chunk is kDotChunkV vectors.
+constexpr int kDotChunkV = 8;
+
+// the raw 4-element load is kept in registers and converted where it is used
+template <class VT> struct Vec4;
+template <> struct Vec4<float> {
+  float4 a;
+  __device__ __forceinline__ void load(const float* p) { a = __ldcs(reinterpret_cast<const float4*>(p)); }
+  __device__ __forceinline__ double x0() const { return a.x; }
+  __device__ __forceinline__ double x1() const { return a.y; }
+  __device__ __forceinline__ double x2() const { return a.z; }
+  __device__ __forceinline__ double x3() const { return a.w; }
+};
+template <> struct Vec4<double> {
+  double2 a, b;
+  __device__ __forceinline__ void load(const double* p) {
+    a = __ldcs(reinterpret_cast<const double2*>(p));
+    b = __ldcs(reinterpret_cast<const double2*>(p) + 1);
+  }
+  __device__ __forceinline__ double x0() const { return a.x; }
+  __device__ __forceinline__ double x1() const { return a.y; }
+  __device__ __forceinline__ double x2() const { return b.x; }
+  __device__ __forceinline__ double x3() const { return b.y; }
+};
+
+template <class VT>
+__global__ void __launch_bounds__(kVecThreads, sizeof(VT) == 4 ? 3 : 1)
+multi_dot4_kernel(const VT* __restrict__ V, int64_t ldv, int k, const double* __restrict__ w, int64_t n,
+                  double* __restrict__ partial) {
+  __shared__ double red[kVecThreads / 32][kDotChunkV];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int j0 = blockIdx.y * kDotChunkV;
+  const int nq = min(kDotChunkV, k - j0);
+  const int nblk = gridDim.x;
+  const VT* __restrict__ Vc = V + (int64_t)j0 * ldv;
+  double acc[kDotChunkV];
+#pragma unroll
+  for (int q = 0; q < kDotChunkV; ++q) acc[q] = 0.0;
+  const int64_t n4 = n >> 2;
+  for (int64_t i4 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i4 < n4; i4 += (int64_t)nblk * blockDim.x) {
+    const int64_t i = i4 << 2;
+    const double2 wa = *reinterpret_cast<const double2*>(w + i), wb = *reinterpret_cast<const double2*>(w + i + 2);
+    Vec4<VT> v[kDotChunkV];
+#pragma unroll
+    for (int q = 0; q < kDotChunkV; ++q)
+      if (q < nq) v[q].load(Vc + (int64_t)q * ldv + i);
+#pragma unroll
+    for (int q = 0; q < kDotChunkV; ++q)
+      if (q < nq) {
+        double a = acc[q];
+        a = fma(v[q].x0(), wa.x, a); a = fma(v[q].x1(), wa.y, a);
+        a = fma(v[q].x2(), wb.x, a); a = fma(v[q].x3(), wb.y, a);
+        acc[q] = a;
+      }
+  }
+#pragma unroll
+  for (int q = 0; q < kDotChunkV; ++q) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+    if (lane == 0) red[wid][q] = acc[q];
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < nq) {
+    double s = 0.0;
+    for (int q = 0; q < kVecThreads / 32; ++q) s += red[q][threadIdx.x];
+    partial[(int64_t)(j0 + threadIdx.x) * nblk + blockIdx.x] = s;
+  }
+}
+
+// w[i] += sum_j coef[j] V_j[i] (4 elements per thread and sweep, 8 basis vectors
+// in flight), and, with NRM, partial[blockIdx.x] = this block's sum of the new
+// w[i]^2 (fixed grid, fixed order: deterministic)
+template <class VT, bool NRM>
+__global__ void __launch_bounds__(kVecThreads)
+multi_axpy4_kernel(double* __restrict__ w, const VT* __restrict__ V, int64_t ldv, int k,
+                   const double* __restrict__ coef, int64_t n, double* __restrict__ partial) {
+  __shared__ double sc[64];
+  __shared__ double red[kVecThreads / 32];
+  for (int q = threadIdx.x; q < k && q < 64; q += blockDim.x) sc[q] = coef[q];
+  __syncthreads();
+  double ss = 0.0;
+  const int64_t n4 = n >> 2;
+  for (int64_t i4 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i4 < n4;
+       i4 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i4 << 2;
+    double2 wa = *reinterpret_cast<const double2*>(w + i), wb = *reinterpret_cast<const double2*>(w + i + 2);
+    int j = 0;
+    for (; j + 8 <= k; j += 8) {
+      Vec4<VT> v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q].load(V + (int64_t)(j + q) * ldv + i);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double c = sc[j + q];
+        wa.x = fma(c, v[q].x0(), wa.x); wa.y = fma(c, v[q].x1(), wa.y);
+        wb.x = fma(c, v[q].x2(), wb.x); wb.y = fma(c, v[q].x3(), wb.y);
+      }
+    }
+    for (; j < k; ++j) {
+      Vec4<VT> v;
+      v.load(V + (int64_t)j * ldv + i);
+      const double c = sc[j];
+      wa.x = fma(c, v.x0(), wa.x); wa.y = fma(c, v.x1(), wa.y);
+      wb.x = fma(c, v.x2(), wb.x); wb.y = fma(c, v.x3(), wb.y);
+    }
+    *reinterpret_cast<double2*>(w + i) = wa;
+    *reinterpret_cast<double2*>(w + i + 2) = wb;
+    if (NRM) {
+      ss = fma(wa.x, wa.x, ss); ss = fma(wa.y, wa.y, ss);
+      ss = fma(wb.x, wb.x, ss); ss = fma(wb.y, wb.y, ss);
+    }
+  }
+  if (NRM) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int q = 0; q < kVecThreads / 32; ++q) t += red[q];
+      partial[blockIdx.x] = t;
+    }
+  }
+}
+
 template <class OT>
 __global__ void scale_kernel(const double* __restrict__ a, double s, OT* __restrict__ b, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -165,6 +295,7 @@ struct Solver {
   // V, Z in fp64.  Halves the Krylov vector traffic of the fp32 phase.
   DevBuf V32, Z32;
   bool basis32 = true;
+  bool vec4 = false;       // n % 4 == 0: the 4-wide Krylov kernels (aligned 16-byte loads)
   int opv = RBF_OP_AUTO;   // operator variant (rbf_op_variant)
   int64_t mv32 = 0, mv64 = 0;
 
@@ -186,6 +317,7 @@ struct Solver {
     RBF_TRY(w.alloc(sizeof(double) * n, s));
     RBF_TRY(f.alloc(sizeof(double) * n, s));
     RBF_TRY(b.alloc(sizeof(double) * n, s));
+    vec4 = (n % 4) == 0 && n >= 4;
     nblk = ctx->sm_count * 4;   // x chunks of kDotChunk basis vectors (grid.y): enough warps in flight
     RBF_TRY(partial.alloc(sizeof(double) * (size_t)nblk * (m + 2), s));
     RBF_TRY(dots.alloc(sizeof(double) * 4 * (m + 2), s));
@@ -208,8 +340,13 @@ struct Solver {
   template <class VT>
   rbf_status mdot(const VT* Vb, int k, const double* vec, double* out, double* neg) {
     cudaStream_t s = ctx->stream;
-    const dim3 grid((unsigned)nblk, (unsigned)((k + kDotChunk - 1) / kDotChunk));
-    multi_dot_kernel<VT><<<grid, kVecThreads, 0, s>>>(Vb, n, k, vec, n, partial.as<double>());
+    if (vec4) {
+      const dim3 grid((unsigned)nblk, (unsigned)((k + kDotChunkV - 1) / kDotChunkV));
+      multi_dot4_kernel<VT><<<grid, kVecThreads, 0, s>>>(Vb, n, k, vec, n, partial.as<double>());
+    } else {
+      const dim3 grid((unsigned)nblk, (unsigned)((k + kDotChunk - 1) / kDotChunk));
+      multi_dot_kernel<VT><<<grid, kVecThreads, 0, s>>>(Vb, n, k, vec, n, partial.as<double>());
+    }
     RBF_CHECK_LAUNCH();
     if (ctx->world == 1) {
       reduce_partials<<<k, 32, 0, s>>>(partial.as<double>(), k, nblk, out, neg != nullptr, neg);
@@ -228,7 +365,10 @@ struct Solver {
   }
   template <class VT>
   rbf_status maxpy(double* vec, const VT* Vb, int k, const double* coef) {
-    multi_axpy_kernel<VT><<<grid_for(n, kVecThreads), kVecThreads, 0, ctx->stream>>>(vec, Vb, n, k, coef, n);
+    if (vec4)
+      multi_axpy4_kernel<VT, false><<<nblk, kVecThreads, 0, ctx->stream>>>(vec, Vb, n, k, coef, n, nullptr);
+    else
+      multi_axpy_kernel<VT><<<grid_for(n, kVecThreads), kVecThreads, 0, ctx->stream>>>(vec, Vb, n, k, coef, n);
     RBF_CHECK_LAUNCH();
     return RBF_OK;
   }
@@ -236,7 +376,10 @@ struct Solver {
   template <class VT>
   rbf_status maxpy_nrm(double* vec, const VT* Vb, int k, const double* coef, double* nrm2_out) {
     cudaStream_t s = ctx->stream;
-    multi_axpy_nrm_kernel<VT><<<nblk, kVecThreads, 0, s>>>(vec, Vb, n, k, coef, n, partial.as<double>());
+    if (vec4)
+      multi_axpy4_kernel<VT, true><<<nblk, kVecThreads, 0, s>>>(vec, Vb, n, k, coef, n, partial.as<double>());
+    else
+      multi_axpy_nrm_kernel<VT><<<nblk, kVecThreads, 0, s>>>(vec, Vb, n, k, coef, n, partial.as<double>());
     RBF_CHECK_LAUNCH();
     reduce_partials<<<1, 32, 0, s>>>(partial.as<double>(), 1, nblk, nrm2_out, 0, nullptr);
     RBF_CHECK_LAUNCH();
@@ -341,6 +484,7 @@ rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp
     RBF_CUDA_TRY(cudaMemcpyAsync(S.r.p, S.b.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   }
   double cycle_beta = -1.0;   // true residual at the start of the previous cycle
+  bool final_fp64 = false;    // beta already is the fp64 true residual of the final x
   for (;;) {
     // phase switch: phase-1 target reached, or the fp32 tier stopped making
     // progress (a cycle that did not halve the true residual, or > 3m
@@ -459,11 +603,19 @@ rbf_status gmres_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& kp
     }
     ++R.restarts;
     if (bd) breakdown_any = true;
+    if (it >= maxit && !fp64) {
+      // out of iterations in the fp32 phase: the loop would only recompute the
+      // fp32 residual to break on it >= maxit and then certify with the fp64
+      // operator -- go to the certification directly (same x, same report)
+      RBF_TRY(S.residual(true, &beta));
+      final_fp64 = true;
+      break;
+    }
     RBF_TRY(S.residual(fp64, &beta));
   }
   // final true residual with the fp64 operator
   double tr = beta;
-  if (!fp64) RBF_TRY(S.residual(true, &tr));
+  if (!fp64 && !final_fp64) RBF_TRY(S.residual(true, &tr));
   const double t_end = std::chrono::duration<double>(clk::now() - t_start).count();
   RBF_CUDA_TRY(cudaMemcpyAsync(x_out_sorted, S.x.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   record_true(tr / bnorm);

@@ -153,6 +153,7 @@ struct rbf_ctx {
   void* loop_group = nullptr;   // rbf::LoopGroup of a loopback context
   int rank = 0, world = 1;
   bool nl_on = true;      // neighbour-list form of the symmetric fp32 operator (rbf_ctx_neighbour_lists)
+  bool grid_per_pair = false;   // one exponential per (node, centre) pair instead of the separable form (rbf_ctx_grid_separable)
   bool peer_mem = true;   // use the transport's peer-memory mode when it has one (rbf_ctx_peer_memory)
   rbf::DevBuf win, fwin, rsc, red, pwin;
 };

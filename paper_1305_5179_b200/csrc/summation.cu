@@ -705,6 +705,262 @@ sum_f32_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* 
   }
 }
 
+// ---------------------------------------------- grid, separable form (a8) ---
+// The nodes of a block lie on a lattice, so the Gaussian of a (node, centre)
+// pair factors along the axes: 2^-|xi - s|^2 = ex[i] ey[j] ez[k] with only
+// 4 + 4 + 4 exponentials per centre for the 64 nodes of a 4 x 4 x 4 block instead
+// of 64 (Eq.5: the evaluation points of the paper are a regular grid,
+// P:203-204).  Roles are swapped against the matvec kernels: a LANE owns one
+// staged centre at a time and the 64 node sums live in its registers; one
+// transposed warp reduction per block (62 shuffles) folds the 32 lanes' partial
+// sums so that lane l ends with nodes l and l + 32 (the layout the store uses).
+// Per centre and lane: 12 MUFU.EX2, 12 differences + 12 squares, 4 + 16 products,
+// then per node one FFMA (interior centres: packed, 32 FFMA2) or FSETP + FFMA
+// under the exact cutoff predicate dx^2 + dy^2 + dz^2 <= k c^2 (reading R5;
+// boundary centres, same dual-ring classification as the traversal's) -- 1.4 /
+// 3.3 instructions per pair against 3.6 / 5.6 for the per-pair exponential form,
+// and 0.19 MUFU per pair instead of 1.  The difference form has no per-target
+// factor, so it needs no bound on the block size (sum_f32_kernel<1>'s expansion
+// does: expansion_ok).
+struct SepNodes {
+  float tx[4], ty[4], tz[4];   // scaled node offsets from the block centre
+};
+
+template <bool MASK>
+struct FlushSep {
+  Ring32 r;
+  float2* acc;          // [32]: nodes (i, j, k = 2 h), (i, j, 2 h + 1) at [i + 4 j + 16 h]
+  const SepNodes* nd;
+  float c2s;
+  int lane;
+  __device__ __forceinline__ void operator()(int cnt) {   // cnt: multiple of 32
+#pragma unroll 1
+    for (int j0 = 0; j0 < cnt; j0 += 32) {
+      const float sx = r.bx[j0 + lane], sy = r.by[j0 + lane], sz = r.bz[j0 + lane], w = r.bw[j0 + lane];
+      float qx[4], qy[4], qz[4], ex[4], ey[4], ez[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float dx = sx - nd->tx[i], dy = sy - nd->ty[i], dz = sz - nd->tz[i];
+        qx[i] = dx * dx; qy[i] = dy * dy; qz[i] = dz * dz;
+        ex[i] = ex2(-qx[i]) * w; ey[i] = ex2(-qy[i]); ez[i] = ex2(-qz[i]);
+      }
+      if constexpr (MASK) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float wxy = ex[i] * ey[j];
+            const float lim = (c2s - qx[i]) - qy[j];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              float2& a = acc[i + 4 * j + 16 * h];
+              if (qz[2 * h] <= lim) a.x = fmaf(wxy, ez[2 * h], a.x);
+              if (qz[2 * h + 1] <= lim) a.y = fmaf(wxy, ez[2 * h + 1], a.y);
+            }
+          }
+      } else {
+        const float2 ez01 = make_float2(ez[0], ez[1]), ez23 = make_float2(ez[2], ez[3]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 eyj = make_float2(ey[j], ey[j]);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 wxy = mul2(make_float2(ex[i], ex[i]), eyj);
+            acc[i + 4 * j] = fma2(wxy, ez01, acc[i + 4 * j]);
+            acc[i + 4 * j + 16] = fma2(wxy, ez23, acc[i + 4 * j + 16]);
+          }
+        }
+      }
+    }
+  }
+};
+
+// pads a ring to a multiple of 32 with zero-weight centres far away (every
+// factor 2^-1e36 = 0, every cutoff test false)
+__device__ __forceinline__ void pad_ring32(Ring32 r, int nbuf, int lane, int& cnt) {
+  cnt = (nbuf + 31) & ~31;
+  if (lane < cnt - nbuf) {
+    const int q = nbuf + lane;
+    r.bx[q] = 1e18f; r.by[q] = 1e18f; r.bz[q] = 1e18f; r.bw[q] = 0.f;
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kSumWarps * 32, 4)
+grid_sep_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const float4* __restrict__ src, int64_t ntiles,
+                GridDesc gd, float* __restrict__ out, int* __restrict__ work, const int32_t* __restrict__ tlist,
+                const uint8_t* __restrict__ nmask) {
+  static_assert(kFlush % 32 == 0, "the separable flush takes 32 centres at a time");
+  __shared__ __align__(16) float ring[kSumWarps][8][kBufPad];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  Ring32 R{ring[wib][0], ring[wib][1], ring[wib][2], ring[wib][3], nullptr, nullptr};    // boundary centres
+  Ring32 RI{ring[wib][4], ring[wib][5], ring[wib][6], ring[wib][7], nullptr, nullptr};   // interior centres
+  const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4, b2 = lane & 2, b1 = lane & 1;
+  for (;;) {
+    int64_t tile;
+    {
+      int t0 = 0;
+      if (lane == 0) t0 = atomicAdd(work, 1);
+      tile = __shfl_sync(0xffffffffu, t0, 0);
+    }
+    if (tile >= ntiles) break;
+    tile = tlist ? (int64_t)tlist[tile] : tile;
+    const int bx = (int)(tile % gd.nb[0]);
+    const int by = (int)((tile / gd.nb[0]) % gd.nb[1]);
+    const int bz = (int)(tile / ((int64_t)gd.nb[0] * gd.nb[1]));
+    const int i0 = 4 * bx, j0 = 4 * by, k0 = 4 * bz;
+    const int i1 = min(i0 + 3, gd.n[0] - 1), j1 = min(j0 + 3, gd.n[1] - 1), k1 = min(k0 + 3, gd.n[2] - 1);
+    const float3 blo = make_float3(node_coord(gd, 0, i0), node_coord(gd, 1, j0), node_coord(gd, 2, k0));
+    const float3 bhi = make_float3(node_coord(gd, 0, i1), node_coord(gd, 1, j1), node_coord(gd, 2, k1));
+    const float3 ctr = make_float3(0.5f * (blo.x + bhi.x), 0.5f * (blo.y + bhi.y), 0.5f * (blo.z + bhi.z));
+    SepNodes nd;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      // nodes past the grid edge shadow the last one (never stored)
+      nd.tx[q] = (node_coord(gd, 0, min(i0 + q, i1)) - ctr.x) * G.s;
+      nd.ty[q] = (node_coord(gd, 1, min(j0 + q, j1)) - ctr.y) * G.s;
+      nd.tz[q] = (node_coord(gd, 2, min(k0 + q, k1)) - ctr.z) * G.s;
+    }
+    float2 acc[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) acc[q] = make_float2(0.f, 0.f);
+    {
+      FlushSep<true> fb{R, acc, &nd, G.c2s, lane};
+      FlushSep<false> fi{RI, acc, &nd, G.c2s, lane};
+      int nB = 0, nI = 0, cnt;
+      // the traversal of traverse2 / Stage32x2<true> (same cell rows, same cull,
+      // same interior / boundary classes, same ring order) written on the
+      // kernel's own shared arrays: with 64 pairs per staged centre and lane the
+      // staging is half of this kernel's instructions, and the generic rings'
+      // pointer selects were a third of that
+      const CellGrid& g = G.g;
+      const float cc = G.cc, cc2 = G.cc2, ci2 = G.ci2, h = g.h, sc = G.s;
+      const int z0 = cellof(blo.z - cc, g.lo[2], g.inv_h, g.dim[2]);
+      const int z1 = cellof(bhi.z + cc, g.lo[2], g.inv_h, g.dim[2]);
+      const int y0 = cellof(blo.y - cc, g.lo[1], g.inv_h, g.dim[1]);
+      const int y1 = cellof(bhi.y + cc, g.lo[1], g.inv_h, g.dim[1]);
+      const unsigned lt = (1u << lane) - 1u;
+      float* const rbase = &ring[wib][0][0];
+      for (int cz = z0; cz <= z1; ++cz) {
+        const float czlo = g.lo[2] + (float)cz * h;
+        const float gz = fmaxf(0.f, fmaxf(czlo - bhi.z, blo.z - (czlo + h)));
+        for (int cy = y0; cy <= y1; ++cy) {
+          const float cylo = g.lo[1] + (float)cy * h;
+          const float gy = fmaxf(0.f, fmaxf(cylo - bhi.y, blo.y - (cylo + h)));
+          const float rem = cc2 - gy * gy - gz * gz;
+          if (rem < 0.f) continue;
+          const float rx = sqrtf(rem);
+          const int x0 = cellof(blo.x - rx, g.lo[0], g.inv_h, g.dim[0]);
+          const int x1 = cellof(bhi.x + rx, g.lo[0], g.inv_h, g.dim[0]);
+          const int64_t rowbase = ((int64_t)cz * g.dim[1] + cy) * g.dim[0];
+          const int sb = __ldg(cell_start + rowbase + x0);
+          const int se = __ldg(cell_start + rowbase + x1 + 1);
+          for (int jb = sb; jb < se; jb += 32) {
+            const int j = jb + lane;
+            const bool valid = j < se;
+            const float4 p = valid ? __ldg(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float ax = blo.x - p.x, bx2 = p.x - bhi.x;
+            const float ay = blo.y - p.y, by2 = p.y - bhi.y;
+            const float az = blo.z - p.z, bz2 = p.z - bhi.z;
+            const float ox = fmaxf(0.f, fmaxf(ax, bx2)), oy = fmaxf(0.f, fmaxf(ay, by2)), oz = fmaxf(0.f, fmaxf(az, bz2));
+            const bool keep = valid && (ox * ox + oy * oy + oz * oz <= cc2);
+            // farthest point of the block's box: every node within c (1 - 1e-4)
+            const float fx = fmaxf(fabsf(ax), fabsf(bx2)), fy = fmaxf(fabsf(ay), fabsf(by2)), fz = fmaxf(fabsf(az), fabsf(bz2));
+            const bool inner = fx * fx + fy * fy + fz * fz <= ci2;
+            const unsigned bi = __ballot_sync(0xffffffffu, keep && inner);
+            const unsigned bb = __ballot_sync(0xffffffffu, keep && !inner);
+            RBF_JITTER();
+            if (keep) {
+              const int pos = inner ? 4 * kBufPad + nI + __popc(bi & lt) : nB + __popc(bb & lt);
+              RBF_DCHECK((inner ? nI + __popc(bi & lt) : nB + __popc(bb & lt)) < kBufPad);
+              float* q = rbase + pos;
+              q[0] = (p.x - ctr.x) * sc;
+              q[kBufPad] = (p.y - ctr.y) * sc;
+              q[2 * kBufPad] = (p.z - ctr.z) * sc;
+              q[3 * kBufPad] = p.w;
+            }
+            nB += __popc(bb);
+            nI += __popc(bi);
+            if (nB >= kFlush) {
+              __syncwarp();
+              fb(kFlush);
+              __syncwarp();
+              if (lane < nB - kFlush) {
+                float* q = rbase + lane;
+                const float a = q[kFlush], b = q[kBufPad + kFlush], c = q[2 * kBufPad + kFlush], d = q[3 * kBufPad + kFlush];
+                q[0] = a; q[kBufPad] = b; q[2 * kBufPad] = c; q[3 * kBufPad] = d;
+              }
+              __syncwarp();
+              nB -= kFlush;
+            }
+            if (nI >= kFlush) {
+              __syncwarp();
+              fi(kFlush);
+              __syncwarp();
+              if (lane < nI - kFlush) {
+                float* q = rbase + 4 * kBufPad + lane;
+                const float a = q[kFlush], b = q[kBufPad + kFlush], c = q[2 * kBufPad + kFlush], d = q[3 * kBufPad + kFlush];
+                q[0] = a; q[kBufPad] = b; q[2 * kBufPad] = c; q[3 * kBufPad] = d;
+              }
+              __syncwarp();
+              nI -= kFlush;
+            }
+          }
+        }
+      }
+      pad_ring32(R, nB, lane, cnt);
+      fb(cnt);
+      pad_ring32(RI, nI, lane, cnt);
+      fi(cnt);
+      __syncwarp();
+    }
+    // transposed reduction over the warp: v[n], n = i + 4 j + 16 k (k = 2 h + c is
+    // component c of acc[i + 4 j + 16 h]), 64 -> 2 values per lane; lane l ends
+    // with the sums of nodes l (k = l >> 4) and l + 32 (k = (l >> 4) + 2)
+    float v5[32];   // index n without bit 4: m = (n & 15) | ((n >> 5) << 4)
+#pragma unroll
+    for (int m = 0; m < 32; ++m) {
+      const int ij = m & 15, kh = m >> 4;   // k = {0, 1} + 2 kh
+      const float lo = acc[ij + 16 * kh].x, hi = acc[ij + 16 * kh].y;   // bit 4 of n = k & 1
+      v5[m] = (b16 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b16 ? lo : hi, 16);
+    }
+    float v4[16];   // without bit 3: q = (m & 7) | ((m >> 4) << 3)
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int lo_i = (q & 7) | ((q >> 3) << 4), hi_i = lo_i | 8;
+      v4[q] = (b8 ? v5[hi_i] : v5[lo_i]) + __shfl_xor_sync(0xffffffffu, b8 ? v5[lo_i] : v5[hi_i], 8);
+    }
+    float v3[8];    // without bit 2
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int lo_i = (q & 3) | ((q >> 2) << 3), hi_i = lo_i | 4;
+      v3[q] = (b4 ? v4[hi_i] : v4[lo_i]) + __shfl_xor_sync(0xffffffffu, b4 ? v4[lo_i] : v4[hi_i], 4);
+    }
+    float v2[4];    // without bit 1
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int lo_i = (q & 1) | ((q >> 1) << 2), hi_i = lo_i | 2;
+      v2[q] = (b2 ? v3[hi_i] : v3[lo_i]) + __shfl_xor_sync(0xffffffffu, b2 ? v3[lo_i] : v3[hi_i], 2);
+    }
+    float v1[2];    // without bit 0: index = bit 5 of n
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int lo_i = q << 1, hi_i = lo_i | 1;
+      v1[q] = (b1 ? v2[hi_i] : v2[lo_i]) + __shfl_xor_sync(0xffffffffu, b1 ? v2[lo_i] : v2[hi_i], 1);
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int i = i0 + (lane & 3), j = j0 + ((lane >> 2) & 3), k = k0 + (lane >> 4) + 2 * t;
+      if (i > i1 || j > j1 || k > k1) continue;
+      const int64_t o = (int64_t)i + (int64_t)gd.n[0] * ((int64_t)j + (int64_t)gd.n[1] * k);
+      float v = G.amp * v1[t];
+      // masked grid (M_ext^eps): nodes outside the eps-surrounding are NaN
+      if (nmask && !nmask[o]) v = __int_as_float(-1);
+      out[o] = v;
+    }
+  }
+}
+
 #ifndef RBF_SYMW_MINB
 #define RBF_SYMW_MINB 8
 #endif
@@ -1488,6 +1744,40 @@ __device__ __forceinline__ double exp_tier64(double x, const double* __restrict_
   return __hiloint2double(__double2hiint(p) + ((n >> 6) << 20), __double2loint(p));
 }
 
+// 2^(-y / 1024) for the expansion-form fp64 kernel, whose frame is scaled so that
+// a pair's exponent arrives as y = 1024 |.|^2 log2(e) / (2 sigma^2) directly (no
+// multiplication by log2 e, no two-part ln 2 reduction): n = rint(-y) by the
+// 1.5 2^52 trick, g = y + n (exact: the two are within 1/2 of each other),
+// 2^(-y/1024) = 2^(n >> 10) * 2^((n & 1023)/1024) * e^(-g ln2/1024), |g| <= 1/2:
+// the last factor by its degree-3 Taylor polynomial (|arg| <= 3.4e-4,
+// truncation 5.5e-16 relative), the middle one from a 1024-entry shared-memory
+// table (exp2 at CTA start, <= 1 ulp): 2 DADD + 3 DFMA + 1 DMUL + the magic
+// DADD = 7 DP operations instead of exp_tier64's 10.  Valid for -1e6 < y (the
+// result is normal for |y| < 1e6); padded sources (y = 1e300) give a finite or
+// non-finite garbage value that the caller's cutoff select discards.
+constexpr int kExp2Tab = 1024;
+struct Exp2Const {
+  double magic, c1, c2, c3;   // (ln2/1024)^k / k!
+};
+__constant__ Exp2Const kExp2 = {6755399441055744.0, 6.769015435155716e-04, 2.290978498068816e-07,
+                                5.169222938345892e-11};
+
+__device__ __forceinline__ void exp2m_table(double* tab) {
+  for (int k = threadIdx.x; k < kExp2Tab; k += blockDim.x) tab[k] = exp2((double)k * (1.0 / kExp2Tab));
+}
+
+__device__ __forceinline__ double exp2m_1024(double y, const double* __restrict__ tab) {
+  const double t = __dsub_rn(kExp2.magic, y);
+  const double nd = __dsub_rn(t, kExp2.magic);
+  const int n = __double2loint(t);
+  const double g = __dadd_rn(y, nd);
+  double p = __fma_rn(-kExp2.c3, g, kExp2.c2);
+  p = __fma_rn(p, g, -kExp2.c1);
+  p = __fma_rn(p, g, 1.0);
+  p = __dmul_rn(p, tab[n & (kExp2Tab - 1)]);
+  return __hiloint2double(__double2hiint(p) + ((n >> 10) << 20), __double2loint(p));
+}
+
 struct Ring64 {
   float* bx; float* by; float* bz; double* bw;
 };
@@ -1767,7 +2057,7 @@ struct Flush64e {
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
       const double rr = __fma_rn(mz[t], sz, __fma_rn(my[t], sy, __fma_rn(mx[t], sx, ss)));
-      const double ex = exp_tier64(-rr, tab);
+      const double ex = exp2m_1024(rr, tab);
       const double e = rr <= thr[t] ? ex : 0.0;
       acc[t] = __fma_rn(e, wj, acc[t]);
       if (SYM) pj = __fma_rn(e, wt[t], pj);
@@ -1804,14 +2094,17 @@ sum_f64_syme_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const flo
                     int64_t own_lo, int64_t own_hi) {
   __shared__ __align__(16) double ringd[kSumWarps][10][kBufPad];
   __shared__ __align__(16) int ringi[kSumWarps][kBufPad];
-  __shared__ double etab[kExpTab];
-  exp_tier64_table(etab);
+  // the exp2 table lives in dynamic shared memory (the rings fill the 48 KB static limit)
+  extern __shared__ __align__(16) double etab[];
+  exp2m_table(etab);
   __syncthreads();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   Ring64e RB{ringd[wib][0], ringd[wib][1], ringd[wib][2], ringd[wib][3], ringd[wib][4], ringi[wib]};
   Ring64e RI{ringd[wib][5], ringd[wib][6], ringd[wib][7], ringd[wib][8], ringd[wib][9], nullptr};
-  const double q = 1.0 / sqrt(G.two_s2);
-  const double c2q = G.c2d / G.two_s2;
+  // frame scale: |.|^2 q^2 = 1024 log2(e) |.|^2 / (2 sigma^2) (exp2m_1024's argument)
+  const double q2 = 1024.0 * 1.4426950408889634 / G.two_s2;
+  const double q = sqrt(q2);
+  const double c2q = G.c2d * q2;
   for (;;) {
     int64_t tile;
     {
@@ -1840,7 +2133,7 @@ sum_f64_syme_kernel(SumGeom G, const int32_t* __restrict__ cell_start, const flo
       const double tt = __fma_rn(tz, tz, __fma_rn(ty, ty, tx * tx));
       mx[t] = -2.0 * tx; my[t] = -2.0 * ty; mz[t] = -2.0 * tz;
       thr[t] = c2q - tt;
-      tf[t] = exp_tier64(-tt, etab);
+      tf[t] = exp2m_1024(tt, etab);
       wt[t] = tv[t] ? w[tidx[t]] * tf[t] : 0.0;
     }
     Stage64e st{RB, RI, src, w, blo, bhi, cx, cy, cz, q, G.cc2, (int)own_lo, tl.x, tl.x + tl.y, (int)own_hi,
@@ -2076,9 +2369,10 @@ __global__ void compact_blocks(const uint32_t* __restrict__ flag, const uint32_t
 // Persistent grid: as many CTAs as can be resident (the kernels pull tiles from a
 // work counter, so CTAs beyond one wave would only add tail imbalance).
 template <class K>
-int sum_blocks(rbf_ctx* ctx, K kernel) {
+int sum_blocks(rbf_ctx* ctx, K kernel, size_t dyn_smem = 0) {
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kSumWarps * 32, 0) != cudaSuccess || per_sm < 1) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kSumWarps * 32, dyn_smem) != cudaSuccess ||
+      per_sm < 1) {
     cudaGetLastError();
     per_sm = 4;
   }
@@ -2574,8 +2868,11 @@ rbf_status matvec_sorted_f64(rbf_ctx* ctx, const rbf_cells* c, const KernelParam
       ProfScope ps(ctx, RBF_PROF_MATVEC_F64);
       // expansion form unless the tile boxes are too large for exp(+|t'|^2) (never
       // with the default cells: |t'|^2 <= hd2 / (2 sigma^2))
-      auto kfn = (c->hd2 / (2.0 * kp.sigma * kp.sigma) <= 300.0) ? sum_f64_syme_kernel : sum_f64_sym_kernel;
-      kfn<<<sum_blocks(ctx, kfn), kSumWarps * 32, 0, s>>>(
+      const bool expf = c->hd2 / (2.0 * kp.sigma * kp.sigma) <= 300.0;
+      auto kfn = expf ? sum_f64_syme_kernel : sum_f64_sym_kernel;
+      const size_t dyn = expf ? sizeof(double) * kExp2Tab : 0;   // exp2m_1024's table
+      if (dyn) RBF_TRY(smem_limit_at_least(kfn, dyn));
+      kfn<<<sum_blocks(ctx, kfn, dyn), kSumWarps * 32, dyn, s>>>(
           G, c->cell_start.as<int32_t>(), c->sorted.as<float4>(), w_win - base, c->tiles.as<int2>(),
           c->tile_box.as<float4>(), V.t1 - V.t0, V.t0, fwin - base, ctx->counter.as<int>(), 0, V.h1);
       RBF_CHECK_LAUNCH();
@@ -2666,6 +2963,14 @@ rbf_status eval_grid_sorted(rbf_ctx* ctx, const rbf_cells* c, const KernelParams
   // node block half-diagonal: 3 steps along x, y and bz - 1 along z, halved
   const double hz = 0.5 * (kGridBz - 1);
   const double hd2 = 2.25 * (gd.step[0] * gd.step[0] + gd.step[1] * gd.step[1]) + hz * hz * gd.step[2] * gd.step[2];
+  if (kGridBz == 4 && !ctx->grid_per_pair) {
+    // separable form: 12 exponentials per centre and 4 x 4 x 4 node block
+    grid_sep_kernel<<<sum_blocks(ctx, grid_sep_kernel), kSumWarps * 32, 0, s>>>(
+        G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), nact, gd, field, ctx->counter.as<int>(),
+        list.as<int32_t>(), near);
+    RBF_CHECK_LAUNCH();
+    return RBF_OK;
+  }
   auto kfn = expansion_ok(kp, hd2) ? sum_f32_kernel<1, false, float> : sum_f32_kernel<1, false, float, false, true>;
   kfn<<<sum_blocks(ctx, kfn), kSumWarps * 32, 0, s>>>(
       G, c->cell_start.as<int32_t>(), ctx->src4.as<float4>(), nullptr, nullptr, nact, 0, gd, field, nullptr,

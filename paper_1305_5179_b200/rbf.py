@@ -95,6 +95,7 @@ EXPORTS = {
     "rbf_create_ipc": (C.c_int, [C.POINTER(_P), C.c_int, _P, _P, C.c_int, C.c_int]),
     "rbf_ctx_peer_memory": (C.c_int, [_P, C.c_int]),
     "rbf_ctx_neighbour_lists": (C.c_int, [_P, C.c_int]),
+    "rbf_ctx_grid_separable": (C.c_int, [_P, C.c_int]),
     "rbf_slab_plan": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, _P, _P, _P, _P, _P]),
     "rbf_extend_points": (C.c_int, [_P, _P, _P, C.c_int64, C.c_double, C.c_double, _P, _P]),
     "rbf_build_cells_shard": (C.c_int, [_P, _P, C.c_int64, C.c_int64, C.POINTER(_Kernel), C.POINTER(_CellCfg),
@@ -323,6 +324,11 @@ class Context:
         """rbf_ctx_neighbour_lists: the neighbour-list form of the symmetric fp32
         operator (tile source lists built once per cell structure; default on)."""
         _check(_lib.rbf_ctx_neighbour_lists(self._h, 1 if on else 0))
+
+    def grid_separable(self, on: bool = True):
+        """rbf_ctx_grid_separable: the separable (12 exponentials per centre and
+        node block) form of the grid evaluation (default on)."""
+        _check(_lib.rbf_ctx_grid_separable(self._h, 1 if on else 0))
 
     def profile(self, on: bool = True):
         """rbf_profile_enable: bracket the library's stage launches with CUDA events."""

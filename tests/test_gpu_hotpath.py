@@ -203,7 +203,17 @@ def test_matvec_degenerate(R, ctx):
 
 
 # ------------------------------------------------------------------ a8 -------
-def test_grid_parity_c1(R, ctx):
+@pytest.fixture(params=["separable", "per_pair"])
+def grid_form(request, ctx):
+    """Both forms of the grid evaluation (rbf_ctx_grid_separable: 12 exponentials
+    per centre and 4x4x4 node block, the default, or one per pair) against the
+    same oracle and the same tolerances."""
+    ctx.grid_separable(request.param == "separable")
+    yield request.param
+    ctx.grid_separable(True)
+
+
+def test_grid_parity_c1(R, ctx, grid_form):
     d = make_inputs("c1")
     X = OE.extend(d["x"], d["normals"], d["delta"])
     b = OE.labels(len(d["x"]), d["delta"])
@@ -224,7 +234,7 @@ def test_grid_parity_c1(R, ctx):
     assert far.sum() > 1000
 
 
-def test_grid_parity_sampled_c2(R, ctx):
+def test_grid_parity_sampled_c2(R, ctx, grid_form):
     d = make_inputs("c2")
     X = OE.extend(d["x"], d["normals"], d["delta"])
     sigma = d["sigma"]
@@ -241,7 +251,7 @@ def test_grid_parity_sampled_c2(R, ctx):
     assert ((F[flat] == 0) == (g == 0)).mean() > 0.999
 
 
-def test_grid_ragged_and_anisotropic(R, ctx):
+def test_grid_ragged_and_anisotropic(R, ctx, grid_form):
     rng = np.random.default_rng(2)
     X = rng.uniform(-0.5, 0.5, (2000, 3)).astype(np.float32)
     sigma = 0.05
@@ -255,6 +265,40 @@ def test_grid_ragged_and_anisotropic(R, ctx):
     assert (np.abs(F - ref) <= 5e-5 * g + 1e-30).all()
     with pytest.raises(R.RbfError):
         R.eval_grid(ctx, cells, kern, dev(w, torch.float64), lo, hi, (1, 5, 5))
+
+
+def test_grid_forms_agree_and_coarse_grid(R, ctx):
+    """The separable and the per-pair form agree to rounding on the same inputs
+    (same zeros: the cutoff predicate is per pair in both), and a grid whose
+    step exceeds the cutoff (node blocks far larger than 6 sigma: the expansion
+    form's per-target factor would leave fp32 range there) stays finite and
+    within the oracle's tolerance."""
+    rng = np.random.default_rng(12)
+    X = rng.uniform(-0.5, 0.5, (6000, 3)).astype(np.float32)
+    sigma = 0.02
+    w = rng.normal(size=6000)
+    kern = R.Kernel(sigma)
+    cells = R.Cells(ctx, dev(X, torch.float32), kern)
+    wd = dev(w, torch.float64)
+    for lo, hi, n in [((-0.55,) * 3, (0.55,) * 3, (41, 38, 45)), ((-0.6,) * 3, (0.6,) * 3, (9, 8, 7))]:
+        try:
+            ctx.grid_separable(True)
+            Fs = host(R.eval_grid(ctx, cells, kern, wd, lo, hi, n)).ravel()
+            ctx.grid_separable(False)
+            Fp = host(R.eval_grid(ctx, cells, kern, wd, lo, hi, n)).ravel()
+        finally:
+            ctx.grid_separable(True)
+        ref = OG.evaluate(X, w, sigma, lo, hi, n)
+        g = OG.evaluate(X, np.abs(w), sigma, lo, hi, n)
+        assert np.isfinite(Fs).all() and np.isfinite(Fp).all()
+        assert (np.abs(Fs - ref) <= 5e-5 * g + 1e-30).all()
+        assert (np.abs(Fp - ref) <= 5e-5 * g + 1e-30).all()
+        assert (np.abs(Fs - Fp) <= 1e-5 * g + 1e-30).all()
+        # a node is zero in one form iff in the other, up to pairs within 1e-5 c of the cutoff
+        dmin = OG._min_dist(OG.nodes(lo, hi, n), X.astype(np.float64))
+        clear = np.abs(dmin - 6 * sigma) > 1e-5 * 6 * sigma
+        assert ((Fs == 0) == (Fp == 0))[clear].all()
+        assert ((Fs == 0) == (dmin > 6 * sigma))[clear].all()
 
 
 @pytest.mark.parametrize("op", ["OP_SYM", "OP_SYM_WIDE", "OP_ONESIDED"])

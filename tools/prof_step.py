@@ -1,5 +1,5 @@
 """Small driver for ncu: cell build, a few solver iterations (operator variant
-argv[2], default OP_AUTO) and one grid evaluation of a config (argv[1], c4).
+argv[2], default OP_AUTO; argv[3] iterations, default 3) and one grid evaluation of a config (argv[1], c4).
 
     ncu --set full -k regex:sum_f32_symb -s 1 -c 1 -o out python tools/prof_step.py c4
 """
@@ -14,6 +14,7 @@ from synth import make_inputs  # noqa: E402
 
 d = make_inputs(sys.argv[1] if len(sys.argv) > 1 else "c4")
 op = int(sys.argv[2]) if len(sys.argv) > 2 else R.OP_AUTO
+iters = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 cfg = d["cfg"]
 ctx = R.Context(0)
 kern = R.Kernel(d["sigma"])
@@ -21,7 +22,7 @@ c, b = R.extend_points(ctx, torch.as_tensor(d["x"], device="cuda"), torch.as_ten
                        d["delta"])
 cells = R.Cells(ctx, c, kern)
 w, _ = R.gmres_solve(ctx, cells, kern, b, restart=50, kind=cfg.precond_kind, core_target=cfg.core_target,
-                     overlap_sigmas=cfg.overlap_sigmas, shift=cfg.shift, local_fp32=cfg.local_fp32, max_iters=3,
+                     overlap_sigmas=cfg.overlap_sigmas, shift=cfg.shift, local_fp32=cfg.local_fp32, max_iters=iters,
                      op=op)
 R.eval_grid(ctx, cells, kern, w, d["grid_lo"], d["grid_hi"], d["grid_n"])
 torch.cuda.synchronize()
