@@ -106,6 +106,7 @@ struct rbf_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t aux_stream = nullptr;   // library-owned second stream (RAS factorisation overlap, halo exchange)
   cudaEvent_t halo_ev[2] = {nullptr, nullptr};   // fork / join of the halo exchange on aux_stream
+  cudaEvent_t apply_ev[2] = {nullptr, nullptr};  // fork / join of the block-Jacobi apply's launch bins on aux_stream
   int sm_count = 148;
   bool prof = false;
   std::vector<rbf_prof_rec> prof_recs;
@@ -125,6 +126,8 @@ struct rbf_ctx {
     for (auto e : ev_pool) cudaEventDestroy(e);
     if (aux_stream) cudaStreamDestroy(aux_stream);
     for (auto e : halo_ev)
+      if (e) cudaEventDestroy(e);
+    for (auto e : apply_ev)
       if (e) cudaEventDestroy(e);
     if (hpin) cudaFreeHost(hpin);
   }

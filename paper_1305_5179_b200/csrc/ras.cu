@@ -864,19 +864,37 @@ __device__ __forceinline__ void apply_sym_rows(const float* __restrict__ T, cons
   }
 }
 
-// Persistent CTAs, blocks b = blockIdx.x + k gridDim.x: one thread streams the
-// NEXT block's triangle into the other shared-memory stage with a bulk copy
-// (TMA engine, mbarrier completion) while the CTA gathers r_ext of the current
-// block and multiplies -- HBM sees one continuous stream per CTA.  Triangles
-// above the stage size (rare big blocks) are read from global.
+// One CTA per block of the launch's bin (records rec[0 .. nblocks), see
+// rbf_precond::ameta; more blocks than CTAs: b = blockIdx.x + k gridDim.x with the
+// next triangle prefetched into the other stage).  One thread streams the block's
+// triangle into shared memory with a bulk copy (TMA engine, mbarrier completion)
+// while the CTA gathers r_ext.  Triangles above the stage size (rare big blocks)
+// are read from global.  A block's record is ONE 32-byte read (it was four
+// dependent-chain heads: ext_ptr[b], ext_ptr[b+1], w_off[b], w_off[b+1]).
+struct ApplyRec {
+  int64_t e0, w0;    // first entry of the block in ext_idx; float offset of its triangle
+  int32_t m, nfl;    // rows; floats of the packed triangle (multiple of 4)
+  int32_t blk, pad;
+};
+static_assert(sizeof(ApplyRec) == 32, "ApplyRec is read as two 16-byte words");
+
+__device__ __forceinline__ ApplyRec load_rec(const ApplyRec* __restrict__ rec, int64_t k) {
+  const int4 a = __ldg(reinterpret_cast<const int4*>(rec + k));
+  const int4 b = __ldg(reinterpret_cast<const int4*>(rec + k) + 1);
+  ApplyRec R;
+  R.e0 = ((int64_t)(uint32_t)a.x) | ((int64_t)a.y << 32);
+  R.w0 = ((int64_t)(uint32_t)a.z) | ((int64_t)a.w << 32);
+  R.m = b.x; R.nfl = b.y; R.blk = b.z; R.pad = 0;
+  return R;
+}
+
 template <class VT>
 __global__ void __launch_bounds__(128)
-apply_sym_kernel(const int64_t* __restrict__ ext_ptr, const int32_t* __restrict__ ext_idx,
-                 const int64_t* __restrict__ w_off, const float* __restrict__ W, const VT* __restrict__ r,
-                 VT* __restrict__ z, int64_t nblocks, int cap_floats, int max_m) {
+apply_sym_kernel(const ApplyRec* __restrict__ rec, const int32_t* __restrict__ ext_idx, const float* __restrict__ W,
+                 const VT* __restrict__ r, VT* __restrict__ z, int64_t nblocks, int cap_floats, int max_m) {
   extern __shared__ __align__(16) float sm[];
   float* xs = sm;                                  // [max_m rounded to 4]
-  float* stage = sm + ((max_m + 3) & ~3);          // [2][cap_floats]
+  float* stage = sm + ((max_m + 3) & ~3);          // [1 or 2][cap_floats]
   __shared__ __align__(8) uint64_t bar[2];
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -887,15 +905,14 @@ apply_sym_kernel(const int64_t* __restrict__ ext_ptr, const int32_t* __restrict_
   __syncthreads();
   auto issue = [&](int64_t b, int st) {
     if (b >= nblocks) return;
-    const int64_t w0 = w_off[b];
-    const int nfl = (int)(w_off[b + 1] - w0);
-    if (nfl > cap_floats) return;
+    const ApplyRec R = load_rec(rec, b);
+    if (R.nfl > cap_floats) return;
     const uint32_t ba = (uint32_t)__cvta_generic_to_shared(&bar[st]);
     const uint32_t dst = (uint32_t)__cvta_generic_to_shared(stage + (size_t)st * cap_floats);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ba), "r"(nfl * 4) : "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ba), "r"(R.nfl * 4) : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                 "l"(W + w0), "r"(nfl * 4), "r"(ba)
+                 "l"(W + R.w0), "r"(R.nfl * 4), "r"(ba)
                  : "memory");
   };
   if (tid == 0) issue(blockIdx.x, 0);
@@ -905,10 +922,10 @@ apply_sym_kernel(const int64_t* __restrict__ ext_ptr, const int32_t* __restrict_
   for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, st ^= 1) {
     // stage st^1 was last read before the barrier that closed the previous iteration
     if (tid == 0) issue(b + gridDim.x, st ^ 1);
-    const int64_t e0 = ext_ptr[b];
-    const int m = (int)(ext_ptr[b + 1] - e0);
-    const int64_t w0 = w_off[b];
-    const bool staged = (w_off[b + 1] - w0) <= cap_floats;
+    const ApplyRec R = load_rec(rec, b);
+    const int64_t e0 = R.e0;
+    const int m = R.m;
+    const bool staged = R.nfl <= cap_floats;
     for (int e = tid; e < m; e += blockDim.x) xs[e] = (float)r[ext_idx[e0 + e]];
     for (int e = m + tid; e < ((m + 3) & ~3); e += blockDim.x) xs[e] = 0.f;
     RBF_JITTER();
@@ -927,7 +944,7 @@ apply_sym_kernel(const int64_t* __restrict__ ext_ptr, const int32_t* __restrict_
       phase ^= 1u << st;
       apply_sym_rows(stage + (size_t)st * cap_floats, xs, m, tid, blockDim.x, ext_idx + e0, z);
     } else {
-      apply_sym_rows(W + w0, xs, m, tid, blockDim.x, ext_idx + e0, z);
+      apply_sym_rows(W + R.w0, xs, m, tid, blockDim.x, ext_idx + e0, z);
     }
     __syncthreads();
   }
@@ -1178,6 +1195,40 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
     const size_t q = std::min<size_t>((size_t)ncore - 1, (size_t)(0.95 * (double)ncore));
     std::nth_element(sz.begin(), sz.begin() + q, sz.end());
     P->cap_w = (int)std::min<int64_t>(std::max<int64_t>(sz[q], 6144), 16384);
+    // launch bins of the apply, each with the stage its triangles need (so the
+    // small ones get more CTAs per SM and the big ones are staged too instead of
+    // being read from global row by row): <= 3584 floats (m <= 84: a 14 KB
+    // stage, 14 CTAs per SM; skipped if fewer than a quarter of the blocks),
+    // <= cap_w (the 95th percentile: 8 CTAs per SM), the rest (stage of the
+    // largest triangle, at most 96 KB)
+    P->cap_small = 3584;
+    P->cap_big = (int)std::min<int64_t>(P->max_wblk, 24576) & ~3;
+    std::vector<ApplyRec> recs((size_t)ncore);
+    size_t nA = 0, nB = 0;
+    for (int64_t b = 0; b < ncore; ++b) {
+      const int64_t nfl = h_w_off[b + 1] - h_w_off[b];
+      nA += nfl <= P->cap_small;
+      nB += nfl > P->cap_small && nfl <= P->cap_w;
+    }
+    if (nA * 4 < (size_t)ncore) { nB += nA; nA = 0; }
+    P->n_small = (int64_t)nA;
+    P->n_mid = (int64_t)nB;
+    size_t ia = 0, ib = nA, ic = nA + nB;
+    int msm = 0, mmid = 0;
+    for (int64_t b = 0; b < ncore; ++b) {
+      const int64_t nfl = h_w_off[b + 1] - h_w_off[b];
+      const int bin = (nA > 0 && nfl <= P->cap_small) ? 0 : (nfl <= P->cap_w ? 1 : 2);
+      ApplyRec& R = recs[bin == 0 ? ia++ : (bin == 1 ? ib++ : ic++)];
+      R.e0 = h_ext_ptr[b]; R.w0 = h_w_off[b]; R.m = (int32_t)h_ecount[b]; R.nfl = (int32_t)nfl;
+      R.blk = (int32_t)b; R.pad = 0;
+      if (bin == 0) msm = std::max(msm, R.m);
+      if (bin == 1) mmid = std::max(mmid, R.m);
+    }
+    P->m_small = msm;
+    P->m_mid = mmid;
+    RBF_TRY(P->ameta.alloc(sizeof(ApplyRec) * (size_t)ncore, s));
+    RBF_CUDA_TRY(cudaMemcpyAsync(P->ameta.p, recs.data(), sizeof(ApplyRec) * (size_t)ncore, cudaMemcpyHostToDevice, s));
+    RBF_CUDA_TRY(cudaStreamSynchronize(s));   // recs is a local
   }
   if (herr0 == 1) { set_error("RAS core larger than the ext-search capacity"); return RBF_EUNSUPPORTED; }
   if (max_m > max_ext || herr0 == 2) {
@@ -1392,14 +1443,38 @@ rbf_status precond_apply_sorted(rbf_ctx* ctx, const rbf_precond* P, const VT* r,
     // (2 or 4 blocks per CTA with the next triangle prefetched into a second
     // stage measured slower: 0.34 / 0.33 vs 0.236 ms at c4 -- the apply is bound
     // by each block's gather -> copy -> rows latency, not by CTA launches)
-    const size_t smems = sizeof(float) * ((size_t)((P->max_m + 3) & ~3) + (size_t)cap);
-    RBF_TRY(smem_limit_at_least(apply_sym_kernel<VT>, smems));
-    const int64_t grid = P->nblocks;
     ProfScope ps(ctx, RBF_PROF_PRECOND_APPLY);
-    apply_sym_kernel<VT><<<(unsigned)grid, kApplyThreads, smems, s>>>(P->ext_ptr.as<int64_t>(), P->ext_idx.as<int32_t>(),
-                                                               P->w_off.as<int64_t>(), P->W.as<float>(), r, z,
-                                                               P->nblocks, cap, P->max_m);
-    RBF_CHECK_LAUNCH();
+    const ApplyRec* rec = P->ameta.as<ApplyRec>();
+    auto launch = [&](int64_t first, int64_t count, int cap_f, int mx, cudaStream_t st) -> rbf_status {
+      if (count <= 0) return RBF_OK;
+      const size_t smems = sizeof(float) * ((size_t)((mx + 3) & ~3) + (size_t)cap_f);
+      RBF_TRY(smem_limit_at_least(apply_sym_kernel<VT>, smems));
+      apply_sym_kernel<VT><<<(unsigned)count, kApplyThreads, smems, st>>>(rec + first, P->ext_idx.as<int32_t>(),
+                                                                          P->W.as<float>(), r, z, count, cap_f, mx);
+      RBF_CHECK_LAUNCH();
+      return RBF_OK;
+    };
+    // three bins, each with its own stage size; the middle and big bins run on
+    // the context's second stream next to the small one (one launch after the
+    // other would add each launch's tail)
+    const int64_t nA = P->n_small, nB = P->n_mid, nC = P->nblocks - nA - nB;
+    const bool fork = nA > 0 && nB + nC > 0 && P->nblocks >= 4 * (int64_t)ctx->sm_count;
+    cudaStream_t s2 = s;
+    if (fork) {
+      if (!ctx->aux_stream) RBF_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
+      for (auto& e : ctx->apply_ev)
+        if (!e) RBF_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      s2 = ctx->aux_stream;
+      RBF_CUDA_TRY(cudaEventRecord(ctx->apply_ev[0], s));
+      RBF_CUDA_TRY(cudaStreamWaitEvent(s2, ctx->apply_ev[0], 0));
+    }
+    RBF_TRY(launch(nA + nB, nC, P->cap_big, P->max_m, s2));
+    RBF_TRY(launch(nA, nB, cap, P->m_mid, s2));
+    RBF_TRY(launch(0, nA, std::min(cap, P->cap_small), P->m_small, s));
+    if (fork) {
+      RBF_CUDA_TRY(cudaEventRecord(ctx->apply_ev[1], s2));
+      RBF_CUDA_TRY(cudaStreamWaitEvent(s, ctx->apply_ev[1], 0));
+    }
     return RBF_OK;
   }
   if (P->w_fp32) {

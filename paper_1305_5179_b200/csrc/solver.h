@@ -17,6 +17,14 @@ struct rbf_precond {
   bool w_sym = false;     // W_i stored as packed lower triangles (block-Jacobi, fp32 W: W_i = B_i^-1 symmetric)
   int64_t max_wblk = 0;   // floats of the largest W_i
   int cap_w = 6144;       // apply staging size (floats; w_sym)
+  // w_sym apply: per-block records {e0, w0, m, nfl} (32 bytes) in launch order,
+  // the blocks whose triangle fits cap_small floats first (their launch takes a
+  // smaller stage, so more CTAs per SM are resident), then the others
+  rbf::DevBuf ameta;
+  int64_t n_small = 0, n_mid = 0;   // then the blocks up to cap_w floats, then the rest (stage of cap_big floats)
+  int cap_small = 0;      // floats
+  int cap_big = 0;
+  int m_small = 0, m_mid = 0;   // largest block of the small / middle bin
   double t_setup = 0.0;
   bool halo = false;      // slab partition with overlap: indices relative to the window start h0
   int shift_idx = 0;      // o0 - (index origin): 0 unless halo

@@ -1342,7 +1342,10 @@ constexpr int kSymPad = 136;   // SoA ring row (>= kFlush + 32 + 4, multiple of 
 
 // Staging batch of the neighbour-list form (NL): the ring is filled with exactly
 // kNlBatch listed sources (no cull, no overflow), then flushed.
-constexpr int kNlBatch = 128;
+#ifndef RBF_NL_BATCH
+#define RBF_NL_BATCH 128
+#endif
+constexpr int kNlBatch = RBF_NL_BATCH;   // (96 and 64 measured with tools/sessions/sess_var.sh)
 static_assert(kNlBatch <= kSymPad && kNlBatch <= kOwnPad, "NL batch exceeds the rings");
 
 // NL = false: the tile streams the cell rows within the cutoff of its box and
