@@ -458,7 +458,9 @@ def run_ours(args, rank, world, local):
                                    "is verified on one GPU -- threads over the loopback transport and separate "
                                    "processes over the IPC transport -- not yet on a multi-GPU box)" if slab
                                    else f"replicas x{world} (independent seeded instances)"),
-                   "l2": "working set >> 126 MB L2 (block inverses 0.5 GB, Krylov basis 1.2 GB, cells + vectors 0.2 GB); no explicit flush"},
+                   "l2": (f"working set >> 126 MB L2 (block inverses {last['precond_bytes'] / 1e9:.2f} GB, fp32 Krylov "
+                          f"basis {4 * 3 * cfg.n * (2 * cfg.restart + 1) / 1e9:.2f} GB, cells + vectors + neighbour lists "
+                          f"{(0.07 + 0.11) * 3 * cfg.n / 1e6:.2f} GB); no explicit flush")},
         "e2e": e2e, "gpu_launches": None, "clocks": clk, "roofline": roofline, "cpu_baseline": cpu,
         "detail": {"useful_pairs_per_matvec": useful_mv, "visited_pairs_per_matvec": visited_mv,
                    "useful_pairs_grid": useful_grid, "visited_pairs_grid": visited_grid,

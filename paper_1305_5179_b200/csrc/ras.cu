@@ -659,6 +659,13 @@ gj_spd_f32_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __restrict
     RBF_DCHECK(m <= MR);
     for (int i = tid; i < m; i += 32 * NW) pos[i] = sorted[ext_idx[e0 + i]];
     __syncthreads();
+    // B = A_ext + shift a I in fp32: distance and cutoff predicate in fp64 (the
+    // oracle's), the Gaussian by the fp32 tier's ex2.approx of the fp32-rounded
+    // exponent (entry accurate to ~1e-6 relative, as the fp32 operator itself;
+    // B is inverted in fp32 and kappa(B) <= ~1/shift, reading R17).  The fp64
+    // libdevice exp of the m^2 entries was a third of this kernel's instructions.
+    const double nk = -1.4426950408889634 / two_s2;
+    const float ampf = (float)amp, shf = (float)shift_abs;
     float2 B[RP][RC];
 #pragma unroll
     for (int a = 0; a < RW; ++a) {
@@ -666,17 +673,19 @@ gj_spd_f32_kernel(const int64_t* __restrict__ ext_ptr, const int64_t* __restrict
 #pragma unroll
       for (int b = 0; b < RC; ++b) {
         const int j = lane + 32 * b;
-        double v = 0.0;
+        float v = 0.f;
         if (i < m && j < m) {
           const float4 pi4 = pos[i], pj4 = pos[j];
           const double dx = (double)pi4.x - (double)pj4.x, dy = (double)pi4.y - (double)pj4.y,
                        dz = (double)pi4.z - (double)pj4.z;
           const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-          v = d2 <= c2 ? amp * exp(-d2 / two_s2) : 0.0;
-          if (i == j) v += shift_abs;
+          float e;
+          asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"((float)(d2 * nk)));
+          v = d2 <= c2 ? ampf * e : 0.f;
+          if (i == j) v += shf;
         }
-        if (a & 1) B[a >> 1][b].y = (float)v;
-        else B[a >> 1][b].x = (float)v;
+        if (a & 1) B[a >> 1][b].y = v;
+        else B[a >> 1][b].x = v;
       }
     }
     auto get = [&](int a, int b) -> float { return (a & 1) ? B[a >> 1][b].y : B[a >> 1][b].x; };
@@ -1198,37 +1207,50 @@ rbf_status precond_build(rbf_ctx* ctx, const rbf_cells* c, const KernelParams& k
     // launch bins of the apply, each with the stage its triangles need (so the
     // small ones get more CTAs per SM and the big ones are staged too instead of
     // being read from global row by row): <= 3584 floats (m <= 84: a 14 KB
-    // stage, 14 CTAs per SM; skipped if fewer than a quarter of the blocks),
-    // <= cap_w (the 95th percentile: 8 CTAs per SM), the rest (stage of the
-    // largest triangle, at most 96 KB)
-    P->cap_small = 3584;
-    P->cap_big = (int)std::min<int64_t>(P->max_wblk, 24576) & ~3;
-    std::vector<ApplyRec> recs((size_t)ncore);
-    size_t nA = 0, nB = 0;
-    for (int64_t b = 0; b < ncore; ++b) {
-      const int64_t nfl = h_w_off[b + 1] - h_w_off[b];
-      nA += nfl <= P->cap_small;
-      nB += nfl > P->cap_small && nfl <= P->cap_w;
+    // stage, 14 CTAs per SM), <= cap_w (the 95th percentile: 8 CTAs per SM),
+    // <= 10240 floats (m <= 142: 5 CTAs per SM), the rest (stage of the largest
+    // triangle, at most 96 KB; larger ones are read from global).  A bin with
+    // fewer than 1/64 of the blocks joins the next larger one.
+    const int64_t capmax = std::min<int64_t>(P->max_wblk, 24576) & ~(int64_t)3;
+    int64_t thr[4] = {3584, P->cap_w, 10240, capmax};
+    for (int k = 0; k < 3; ++k) thr[k] = std::min(thr[k], capmax);
+    auto bin_of = [&](int64_t nfl, const int64_t* t, int nb) {
+      for (int k = 0; k < nb - 1; ++k)
+        if (nfl <= t[k]) return k;
+      return nb - 1;
+    };
+    int nb = 4;
+    for (;;) {
+      int64_t cnt[4] = {0, 0, 0, 0};
+      for (int64_t b = 0; b < ncore; ++b) ++cnt[bin_of(h_w_off[b + 1] - h_w_off[b], thr, nb)];
+      int drop = -1;
+      for (int k = 0; k < nb - 1 && drop < 0; ++k)
+        if (cnt[k] * 64 < ncore || thr[k] >= thr[k + 1]) drop = k;
+      if (drop < 0 || nb == 1) {
+        P->nbins = nb;
+        P->bin_first[0] = 0;
+        for (int k = 0; k < nb; ++k) {
+          P->bin_first[k + 1] = P->bin_first[k] + cnt[k];
+          P->bin_cap[k] = (int)thr[k];
+          P->bin_m[k] = 0;
+        }
+        break;
+      }
+      for (int k = drop; k < nb - 1; ++k) thr[k] = thr[k + 1];
+      --nb;
     }
-    if (nA * 4 < (size_t)ncore) { nB += nA; nA = 0; }
-    P->n_small = (int64_t)nA;
-    P->n_mid = (int64_t)nB;
-    size_t ia = 0, ib = nA, ic = nA + nB;
-    int msm = 0, mmid = 0;
+    std::vector<ApplyRec> recs((size_t)ncore);
+    int64_t fill[4] = {P->bin_first[0], P->bin_first[1], P->bin_first[2], P->bin_first[3]};
     for (int64_t b = 0; b < ncore; ++b) {
       const int64_t nfl = h_w_off[b + 1] - h_w_off[b];
-      const int bin = (nA > 0 && nfl <= P->cap_small) ? 0 : (nfl <= P->cap_w ? 1 : 2);
-      ApplyRec& R = recs[bin == 0 ? ia++ : (bin == 1 ? ib++ : ic++)];
+      const int k = bin_of(nfl, thr, P->nbins);
+      ApplyRec& R = recs[(size_t)fill[k]++];
       R.e0 = h_ext_ptr[b]; R.w0 = h_w_off[b]; R.m = (int32_t)h_ecount[b]; R.nfl = (int32_t)nfl;
       R.blk = (int32_t)b; R.pad = 0;
-      if (bin == 0) msm = std::max(msm, R.m);
-      if (bin == 1) mmid = std::max(mmid, R.m);
+      P->bin_m[k] = std::max(P->bin_m[k], (int)R.m);
     }
-    P->m_small = msm;
-    P->m_mid = mmid;
     RBF_TRY(P->ameta.alloc(sizeof(ApplyRec) * (size_t)ncore, s));
     RBF_CUDA_TRY(cudaMemcpyAsync(P->ameta.p, recs.data(), sizeof(ApplyRec) * (size_t)ncore, cudaMemcpyHostToDevice, s));
-    RBF_CUDA_TRY(cudaStreamSynchronize(s));   // recs is a local
   }
   if (herr0 == 1) { set_error("RAS core larger than the ext-search capacity"); return RBF_EUNSUPPORTED; }
   if (max_m > max_ext || herr0 == 2) {
@@ -1436,13 +1458,10 @@ rbf_status precond_apply_sorted(rbf_ctx* ctx, const rbf_precond* P, const VT* r,
   const int blocks = (int)std::min<int64_t>(P->nblocks, (int64_t)ctx->sm_count * 16);
   const size_t smem = sizeof(double) * (size_t)P->max_m;
   if (P->w_sym) {
-    // a staging buffer of up to cap floats per CTA; larger triangles are read
-    // from global.  One CTA per block: many small CTAs per SM overlap the
-    // gather -> copy -> multiply latency chain of each block
-    const int cap = (int)std::min<int64_t>(P->max_wblk, P->cap_w) & ~3;
-    // (2 or 4 blocks per CTA with the next triangle prefetched into a second
-    // stage measured slower: 0.34 / 0.33 vs 0.236 ms at c4 -- the apply is bound
-    // by each block's gather -> copy -> rows latency, not by CTA launches)
+    // one CTA per block: many small CTAs per SM overlap the gather -> copy ->
+    // multiply latency chain of each block (2 or 4 blocks per CTA with the next
+    // triangle prefetched into a second stage measured slower: 0.34 / 0.33 vs
+    // 0.236 ms at c4; a fully pipelined persistent form 0.262 ms: DESIGN.md §5)
     ProfScope ps(ctx, RBF_PROF_PRECOND_APPLY);
     const ApplyRec* rec = P->ameta.as<ApplyRec>();
     auto launch = [&](int64_t first, int64_t count, int cap_f, int mx, cudaStream_t st) -> rbf_status {
@@ -1454,11 +1473,10 @@ rbf_status precond_apply_sorted(rbf_ctx* ctx, const rbf_precond* P, const VT* r,
       RBF_CHECK_LAUNCH();
       return RBF_OK;
     };
-    // three bins, each with its own stage size; the middle and big bins run on
-    // the context's second stream next to the small one (one launch after the
-    // other would add each launch's tail)
-    const int64_t nA = P->n_small, nB = P->n_mid, nC = P->nblocks - nA - nB;
-    const bool fork = nA > 0 && nB + nC > 0 && P->nblocks >= 4 * (int64_t)ctx->sm_count;
+    // the bins, each with its own stage size; the smallest bin runs on the main
+    // stream and the others on the context's second stream next to it, largest
+    // first (one launch after the other would add each launch's tail)
+    const bool fork = P->nbins > 1 && P->nblocks >= 4 * (int64_t)ctx->sm_count;
     cudaStream_t s2 = s;
     if (fork) {
       if (!ctx->aux_stream) RBF_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
@@ -1468,9 +1486,9 @@ rbf_status precond_apply_sorted(rbf_ctx* ctx, const rbf_precond* P, const VT* r,
       RBF_CUDA_TRY(cudaEventRecord(ctx->apply_ev[0], s));
       RBF_CUDA_TRY(cudaStreamWaitEvent(s2, ctx->apply_ev[0], 0));
     }
-    RBF_TRY(launch(nA + nB, nC, P->cap_big, P->max_m, s2));
-    RBF_TRY(launch(nA, nB, cap, P->m_mid, s2));
-    RBF_TRY(launch(0, nA, std::min(cap, P->cap_small), P->m_small, s));
+    for (int k = P->nbins - 1; k >= 1; --k)
+      RBF_TRY(launch(P->bin_first[k], P->bin_first[k + 1] - P->bin_first[k], P->bin_cap[k], P->bin_m[k], s2));
+    RBF_TRY(launch(0, P->bin_first[1], P->bin_cap[0], P->bin_m[0], s));
     if (fork) {
       RBF_CUDA_TRY(cudaEventRecord(ctx->apply_ev[1], s2));
       RBF_CUDA_TRY(cudaStreamWaitEvent(s, ctx->apply_ev[1], 0));

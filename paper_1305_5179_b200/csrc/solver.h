@@ -17,14 +17,15 @@ struct rbf_precond {
   bool w_sym = false;     // W_i stored as packed lower triangles (block-Jacobi, fp32 W: W_i = B_i^-1 symmetric)
   int64_t max_wblk = 0;   // floats of the largest W_i
   int cap_w = 6144;       // apply staging size (floats; w_sym)
-  // w_sym apply: per-block records {e0, w0, m, nfl} (32 bytes) in launch order,
-  // the blocks whose triangle fits cap_small floats first (their launch takes a
-  // smaller stage, so more CTAs per SM are resident), then the others
+  // w_sym apply: per-block records {e0, w0, m, nfl} (32 bytes) in launch order:
+  // up to 4 launch bins by triangle size, each launched with the stage its
+  // triangles need (small triangles: more CTAs per SM; big ones: staged instead
+  // of read from global)
   rbf::DevBuf ameta;
-  int64_t n_small = 0, n_mid = 0;   // then the blocks up to cap_w floats, then the rest (stage of cap_big floats)
-  int cap_small = 0;      // floats
-  int cap_big = 0;
-  int m_small = 0, m_mid = 0;   // largest block of the small / middle bin
+  int nbins = 0;
+  int64_t bin_first[5] = {0, 0, 0, 0, 0};   // records [bin_first[k], bin_first[k + 1])
+  int bin_cap[4] = {0, 0, 0, 0};             // stage size, floats
+  int bin_m[4] = {0, 0, 0, 0};               // largest block of the bin
   double t_setup = 0.0;
   bool halo = false;      // slab partition with overlap: indices relative to the window start h0
   int shift_idx = 0;      // o0 - (index origin): 0 unless halo
