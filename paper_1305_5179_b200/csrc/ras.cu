@@ -898,7 +898,7 @@ __device__ __forceinline__ ApplyRec load_rec(const ApplyRec* __restrict__ rec, i
 }
 
 template <class VT>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
 apply_sym_kernel(const ApplyRec* __restrict__ rec, const int32_t* __restrict__ ext_idx, const float* __restrict__ W,
                  const VT* __restrict__ r, VT* __restrict__ z, int64_t nblocks, int cap_floats, int max_m) {
   extern __shared__ __align__(16) float sm[];
@@ -1468,7 +1468,10 @@ rbf_status precond_apply_sorted(rbf_ctx* ctx, const rbf_precond* P, const VT* r,
       if (count <= 0) return RBF_OK;
       const size_t smems = sizeof(float) * ((size_t)((mx + 3) & ~3) + (size_t)cap_f);
       RBF_TRY(smem_limit_at_least(apply_sym_kernel<VT>, smems));
-      apply_sym_kernel<VT><<<(unsigned)count, kApplyThreads, smems, st>>>(rec + first, P->ext_idx.as<int32_t>(),
+      // a thread per row of the bin's largest block (whole warps, 64 .. 256): no idle
+      // warp in the small bins, one pass over the rows in the big ones
+      const int threads = std::min(256, std::max(64, (mx + 31) & ~31));
+      apply_sym_kernel<VT><<<(unsigned)count, threads, smems, st>>>(rec + first, P->ext_idx.as<int32_t>(),
                                                                           P->W.as<float>(), r, z, count, cap_f, mx);
       RBF_CHECK_LAUNCH();
       return RBF_OK;
