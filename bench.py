@@ -89,8 +89,11 @@ class Clocks:
         nvidia-smi's start-up (NVML init, driver queries) stays out of the timed
         region, the samples read at stop() are all taken during it."""
         try:
+            if os.environ.get("RBF_BENCH_NO_CLOCKS"):   # diagnostics only: is the sampler perturbing the run?
+                return
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms",
+                                       os.environ.get("RBF_BENCH_CLOCKS_MS", "200")],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.p.stdout.readline()
         except OSError:
@@ -321,9 +324,20 @@ def run_ours(args, rank, world, local):
     # warm-up holds the same references as the timed loop (the previous step's
     # cells, weights and field stay alive while the next step allocates), so
     # the device memory pools reach their steady size before timing
+    # (the SAME names as the timed loop binds: with another name for the cells, the
+    # last warm-up's cells stayed alive next to the first timed step's, the pool
+    # grew by one more cell structure inside timed step 2 -- 3 ms normally, once
+    # 188 ms on a box whose driver had just released 80 GB from the test suite)
     for _ in range(args.warmup):
-        _, w, field, rep = step()
+        cells_last, w, field, rep = step()
     torch.cuda.synchronize()
+    # Reserve head-room in the library's memory pool (rbf_pool_reserve): the
+    # stream-ordered allocator occasionally has to grow the pool in a later step
+    # (its free blocks do not always fit the repeating requests), and a driver
+    # allocation inside the timed region costs 3 ms on an idle box but took 75-200
+    # ms right after the test suite's process had released tens of GB.
+    held, used = ctx.pool_stats()
+    ctx.pool_reserve(max(held, 1 << 30))
     clocks = Clocks(local)
     # no cyclic-GC pause inside the timed regions (the solver's host steps are on
     # the critical path; a full collection costs ~20 ms): collect now, re-enable after
@@ -346,15 +360,16 @@ def run_ours(args, rank, world, local):
         cells_last, w, field, rep = step()
         reps.append(rep)
         if trace:
-            evs.append((torch.cuda.Event(enable_timing=True), time.perf_counter()))
+            evs.append((torch.cuda.Event(enable_timing=True), time.perf_counter(), ctx.pool_stats()))
             evs[-1][0].record(s)
     e1.record(s)
     torch.cuda.synchronize()
     if trace:   # per-step device / host times (diagnostics, stderr)
         prev_e, prev_h = e0, None
-        for ev, th in evs:
+        for ev, th, ps in evs:
             print(f"[bench trace] step {prev_e.elapsed_time(ev):.1f} ms (device)"
-                  + (f", {1e3 * (th - prev_h):.1f} ms (host)" if prev_h else ""), file=sys.stderr)
+                  + (f", {1e3 * (th - prev_h):.1f} ms (host)" if prev_h else "")
+                  + f", pool {ps[0] / 1e9:.2f} GB held / {ps[1] / 1e9:.2f} GB used", file=sys.stderr)
             prev_e, prev_h = ev, th
     launches = R.launch_count() - launches0
     ms = e0.elapsed_time(e1)
@@ -379,7 +394,8 @@ def run_ours(args, rank, world, local):
         w_h = torch.empty(n, dtype=torch.float64).pin_memory()
         f_h = torch.empty((gn[2], gn[1], gn[0]), dtype=torch.float32).pin_memory()
         rkw = dict(solve_kw)
-        R.reconstruct_host(ctx, xyz_h, b_h, kern, lo, hi, gn, w_out=w_h, field_out=f_h, **rkw)   # warm
+        for _ in range(max(1, min(args.warmup, 3))):   # warm
+            R.reconstruct_host(ctx, xyz_h, b_h, kern, lo, hi, gn, w_out=w_h, field_out=f_h, **rkw)
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()

@@ -294,6 +294,18 @@ int rbf_abi_version(void);
 /* Number of CUDA kernels this library has launched in the process so far
  * (all contexts); host-side counter, no synchronisation. */
 int64_t rbf_launch_count(void);
+/* Device memory pool of the library on the context's device (one private
+ * stream-ordered pool per device, never trimmed while the process lives).
+ * rbf_pool_reserve grows the pool's backing memory to at least `bytes` now (one
+ * allocation of that size, freed back into the pool at once), so that later
+ * calls carve their buffers out of it instead of asking the driver for memory
+ * in the middle of a solve -- a driver allocation can take hundreds of
+ * milliseconds right after another process released tens of GB on the device.
+ * rbf_pool_stats: out[0] = bytes of backing memory the pool holds, out[1] =
+ * bytes currently handed out (HOST, 2 values).  Errors: RBF_EINVAL, RBF_ENOMEM
+ * (the device cannot back `bytes`), RBF_ECUDA. */
+rbf_status rbf_pool_reserve(rbf_ctx* ctx, uint64_t bytes);
+rbf_status rbf_pool_stats(rbf_ctx* ctx, uint64_t* out);
 
 /* ---- a0: extended interpolation set (§2.1.1-2.1.2) ------------
  * x, nrm: DEVICE fp64, N x 3 (surface points and unit normals).

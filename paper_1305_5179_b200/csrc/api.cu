@@ -111,6 +111,31 @@ int rbf_abi_version(void) { return RBF_ABI_VERSION; }
 
 int64_t rbf_launch_count(void) { return (int64_t)g_launches.load(std::memory_order_relaxed); }
 
+rbf_status rbf_pool_stats(rbf_ctx* ctx, uint64_t* out) {
+  if (!ctx || !out) { set_error("NULL argument"); return RBF_EINVAL; }
+  cudaMemPool_t pool = lib_pool(ctx->device);
+  if (!pool) RBF_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, ctx->device));
+  RBF_CUDA_TRY(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &out[0]));
+  RBF_CUDA_TRY(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &out[1]));
+  return RBF_OK;
+}
+
+rbf_status rbf_pool_reserve(rbf_ctx* ctx, uint64_t bytes) {
+  if (!ctx) { set_error("ctx is NULL"); return RBF_EINVAL; }
+  uint64_t st[2];
+  RBF_TRY(rbf_pool_stats(ctx, st));
+  const uint64_t free_in_pool = st[0] - st[1];
+  if (bytes <= free_in_pool) return RBF_OK;
+  // one block of the missing size, returned to the pool at once (the pool's
+  // release threshold is unlimited, so the backing memory stays)
+  DevBuf tmp;
+  rbf_status r = tmp.alloc((size_t)(bytes - free_in_pool), ctx->stream);
+  if (r != RBF_OK) return RBF_ENOMEM;
+  tmp.release();
+  RBF_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return RBF_OK;
+}
+
 }  // extern "C"
 
 namespace {

@@ -88,6 +88,8 @@ EXPORTS = {
     "rbf_last_error": (C.c_char_p, []),
     "rbf_abi_version": (C.c_int, []),
     "rbf_launch_count": (C.c_int64, []),
+    "rbf_pool_reserve": (C.c_int, [_P, C.c_uint64]),
+    "rbf_pool_stats": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
     "rbf_nccl_unique_id": (C.c_int, [_P]),
     "rbf_loopback_group_create": (C.c_int, [C.c_int, C.POINTER(_P)]),
     "rbf_loopback_group_free": (None, [_P]),
@@ -329,6 +331,17 @@ class Context:
         """rbf_ctx_grid_separable: the separable (12 exponentials per centre and
         node block) form of the grid evaluation (default on)."""
         _check(_lib.rbf_ctx_grid_separable(self._h, 1 if on else 0))
+
+    def pool_reserve(self, nbytes: int):
+        """rbf_pool_reserve: grow the library's device memory pool to at least
+        nbytes of free backing memory now."""
+        _check(_lib.rbf_pool_reserve(self._h, int(nbytes)))
+
+    def pool_stats(self):
+        """rbf_pool_stats: (bytes of backing memory held, bytes handed out)."""
+        out = (C.c_uint64 * 2)()
+        _check(_lib.rbf_pool_stats(self._h, out))
+        return int(out[0]), int(out[1])
 
     def profile(self, on: bool = True):
         """rbf_profile_enable: bracket the library's stage launches with CUDA events."""

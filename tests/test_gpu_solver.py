@@ -435,3 +435,20 @@ def test_warm_start_resumes_a_solve(R, ctx):
     w3, rep3 = R.gmres_solve(ctx, cells, kern, bd, rtol=1e-8, max_iters=400, x0=w2, **kw)
     assert rep3["iters_phase1"] + rep3["iters_phase2"] == 0 and rep3["converged"] == 1
     np.testing.assert_array_equal(host(w3), host(w2))
+
+
+def test_pool_reserve_and_stats(R, ctx):
+    """rbf_pool_reserve / rbf_pool_stats: the pool holds at least the reserved
+    head-room afterwards, hands none of it out, and a following build allocates
+    out of it (the backing memory does not grow)."""
+    held0, used0 = ctx.pool_stats()
+    ctx.pool_reserve((held0 - used0) + (256 << 20))
+    held1, used1 = ctx.pool_stats()
+    assert held1 - used1 >= (held0 - used0) + (256 << 20) and used1 == used0
+    d = make_inputs("c1")
+    X = OE.extend(d["x"], d["normals"], d["delta"])
+    kern = R.Kernel(d["sigma"])
+    cells = R.Cells(ctx, dev(X, torch.float32), kern)
+    held2, used2 = ctx.pool_stats()
+    assert held2 == held1 and used2 > used1
+    del cells

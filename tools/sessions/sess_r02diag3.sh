@@ -1,0 +1,9 @@
+# after the warm-up reference fix: bench right after the pytest subset that reproduced the stretched step, per-step trace
+timeout 1500 python -m pytest tests/test_gpu_race_probe.py tests/test_gpu_loopback.py tests/test_gpu_solver.py -x -q > gpurun_out/pytest_d3.log 2>&1; echo pytest=$?; tail -1 gpurun_out/pytest_d3.log
+for i in 1 2; do
+RBF_BENCH_TRACE=1 timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_$i.json 2> gpurun_out/bench_$i.err; echo bench=$?
+python -c "import json; d=json.load(open('gpurun_out/bench_$i.json')); print('run$i', d['ms_per_step'], d['e2e']['ms_per_step'], d['roofline']['frac'], d['clocks'], d['detail']['stage_ms_per_step'])"
+grep "bench trace" gpurun_out/bench_$i.err | tr '\n' ';' | cut -c1-700; echo
+done
+timeout 300 python bench.py > gpurun_out/bench_default_flags.json 2> gpurun_out/bench_default_flags.err; echo bench_default_flags=$?
+python -c "import json; d=json.load(open('gpurun_out/bench_default_flags.json')); print('default flags', d['steps'], d['warmup'], d['ms_per_step'], d['e2e']['ms_per_step'])"
