@@ -328,16 +328,22 @@ def run_ours(args, rank, world, local):
     # last warm-up's cells stayed alive next to the first timed step's, the pool
     # grew by one more cell structure inside timed step 2 -- 3 ms normally, once
     # 188 ms on a box whose driver had just released 80 GB from the test suite)
-    for _ in range(args.warmup):
+    # Head-room in the library's memory pool (rbf_pool_reserve), taken after the
+    # first warm-up step (which shows the footprint) so that the remaining
+    # warm-up steps are the first users of the new memory: the stream-ordered
+    # allocator occasionally has to grow the pool in a later step (its free
+    # blocks do not always fit the repeating requests), and a driver allocation
+    # inside the timed region costs 3 ms on an idle box but took 75-200 ms right
+    # after the test suite's process had released tens of GB; the first step that
+    # touches freshly reserved memory is 12-90 ms slower, so it must not be a
+    # timed one either.
+    for k in range(max(args.warmup, 2)):
         cells_last, w, field, rep = step()
+        if k == 0:
+            torch.cuda.synchronize()
+            held, used = ctx.pool_stats()
+            ctx.pool_reserve(max(held, 1 << 30))
     torch.cuda.synchronize()
-    # Reserve head-room in the library's memory pool (rbf_pool_reserve): the
-    # stream-ordered allocator occasionally has to grow the pool in a later step
-    # (its free blocks do not always fit the repeating requests), and a driver
-    # allocation inside the timed region costs 3 ms on an idle box but took 75-200
-    # ms right after the test suite's process had released tens of GB.
-    held, used = ctx.pool_stats()
-    ctx.pool_reserve(max(held, 1 << 30))
     clocks = Clocks(local)
     # no cyclic-GC pause inside the timed regions (the solver's host steps are on
     # the critical path; a full collection costs ~20 ms): collect now, re-enable after

@@ -296,8 +296,9 @@ int rbf_abi_version(void);
 int64_t rbf_launch_count(void);
 /* Device memory pool of the library on the context's device (one private
  * stream-ordered pool per device, never trimmed while the process lives).
- * rbf_pool_reserve grows the pool's backing memory to at least `bytes` now (one
- * allocation of that size, freed back into the pool at once), so that later
+ * rbf_pool_reserve makes sure the pool holds a free block of at least `bytes`
+ * now (one allocation of that size, freed back into the pool at once: the pool
+ * grows by what its free blocks cannot serve contiguously), so that later
  * calls carve their buffers out of it instead of asking the driver for memory
  * in the middle of a solve -- a driver allocation can take hundreds of
  * milliseconds right after another process released tens of GB on the device.
@@ -538,7 +539,10 @@ rbf_status rbf_sigma_auto(rbf_ctx* ctx, const double* x, int64_t n, const double
  * When enabled, every launch of the listed device stages is bracketed by a
  * pair of CUDA events recorded on the context's stream.  rbf_profile_query
  * synchronises, sums the elapsed times per stage into the HOST arrays
- * ms[RBF_PROF_COUNT] and launches[RBF_PROF_COUNT], and clears the records. */
+ * ms[RBF_PROF_COUNT] and launches[RBF_PROF_COUNT], and clears the records.
+ * Enabling creates a stock of 16384 events at once (returned by each query), so
+ * that no event is created -- and the driver never extends its event storage --
+ * in the middle of a timed region. */
 typedef enum {
   RBF_PROF_CELLS = 0,          /* a1/a2: cell build + tile plan (whole call) */
   RBF_PROF_MATVEC_F32 = 1,     /* a3: fp32 summation kernel */

@@ -122,14 +122,12 @@ rbf_status rbf_pool_stats(rbf_ctx* ctx, uint64_t* out) {
 
 rbf_status rbf_pool_reserve(rbf_ctx* ctx, uint64_t bytes) {
   if (!ctx) { set_error("ctx is NULL"); return RBF_EINVAL; }
-  uint64_t st[2];
-  RBF_TRY(rbf_pool_stats(ctx, st));
-  const uint64_t free_in_pool = st[0] - st[1];
-  if (bytes <= free_in_pool) return RBF_OK;
-  // one block of the missing size, returned to the pool at once (the pool's
-  // release threshold is unlimited, so the backing memory stays)
+  if (bytes == 0) return RBF_OK;
+  // one block of `bytes`, returned to the pool at once: the pool grows by what
+  // its free blocks cannot serve contiguously, and keeps it (its release
+  // threshold is unlimited)
   DevBuf tmp;
-  rbf_status r = tmp.alloc((size_t)(bytes - free_in_pool), ctx->stream);
+  rbf_status r = tmp.alloc((size_t)bytes, ctx->stream);
   if (r != RBF_OK) return RBF_ENOMEM;
   tmp.release();
   RBF_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
@@ -247,6 +245,21 @@ rbf_status rbf_ctx_grid_separable(rbf_ctx* ctx, int on) {
 rbf_status rbf_profile_enable(rbf_ctx* ctx, int on) {
   if (!ctx) { set_error("ctx is NULL"); return RBF_EINVAL; }
   ctx->prof = on != 0;
+  if (ctx->prof) {
+    // The stage timers take two CUDA events per bracket (a few hundred per
+    // reconstruction) and return them at rbf_profile_query.  Create a stock of
+    // them NOW: created on demand, the ~2000th event of a process made the
+    // driver extend its event storage in the middle of a timed step -- 10 ms on
+    // an idle box, 100-300 ms right after another process had released tens of
+    // GB (the stall landed in whichever stage asked for the event).
+    constexpr size_t kStock = 16384;
+    ctx->ev_pool.reserve(kStock);
+    while (ctx->ev_pool.size() < kStock) {
+      cudaEvent_t e = nullptr;
+      RBF_CUDA_TRY(cudaEventCreate(&e));
+      ctx->ev_pool.push_back(e);
+    }
+  }
   return RBF_OK;
 }
 

@@ -333,8 +333,8 @@ class Context:
         _check(_lib.rbf_ctx_grid_separable(self._h, 1 if on else 0))
 
     def pool_reserve(self, nbytes: int):
-        """rbf_pool_reserve: grow the library's device memory pool to at least
-        nbytes of free backing memory now."""
+        """rbf_pool_reserve: make sure the library's device memory pool holds a
+        free block of at least nbytes now."""
         _check(_lib.rbf_pool_reserve(self._h, int(nbytes)))
 
     def pool_stats(self):
